@@ -1,0 +1,147 @@
+/* conetrx_cuda.h — C ABI of the B200-native CoNet-Rx inference engine (libconetrx_cuda.so).
+ *
+ * Drop-in boundary.  The reference exposes the hot path as a header-only C++ template,
+ *     Tensor<T> Network<T>::forward(const Tensor<T>& x, NormMode mode, ForwardCache<T>* cache = nullptr,
+ *                                   const std::map<int,T>* overrides = nullptr)
+ * (/root/reference/proj/core/include/conetrx/network.hpp:162-163), dispatching the closed LayerOp
+ * vocabulary (network.hpp:17) node by node (network.hpp:380-420).  There is no plugin registry, so the
+ * replacement takes the network's own description — its GraphNode list (network.hpp:19-26, nodes()
+ * :335), NamedParam list (network.hpp:28-33, params() :140) and BN-ready flags (bn_ready() :337) —
+ * compiles it once into a device plan, and runs forward on B200.  include/conetrx/gpu_plan.hpp is the
+ * C++ wrapper that builds these arrays from a live conetrx::Network<float> and rethrows errors as the
+ * reference's exception types; INTEGRATION.md shows the binding.
+ *
+ * Plain pointers and sizes only; no CUDA, torch or C++ types.  `stream` arguments are cudaStream_t
+ * passed as void* (NULL = the plan's own stream).
+ */
+#ifndef CONETRX_CUDA_H
+#define CONETRX_CUDA_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The reference reports errors as exceptions; the C++ wrapper maps them back:
+ *   CNRX_ERR_INVALID_ARGUMENT  <- std::invalid_argument from require() (tensor.hpp:13-15), e.g. the
+ *                                 channel-count check in forward (network.hpp:164-166)
+ *   CNRX_ERR_NOT_READY         <- std::runtime_error for eval-mode BN without statistics (norms.hpp:66-69)
+ *   CNRX_ERR_UNSUPPORTED       graph / mode this engine does not run (e.g. NormMode::train, which
+ *                              mutates running statistics; no CPU fallback exists by design)
+ *   CNRX_ERR_CUDA              a CUDA runtime error (message names the call)                          */
+#define CNRX_OK 0
+#define CNRX_ERR_INVALID_ARGUMENT 1
+#define CNRX_ERR_NOT_READY 2
+#define CNRX_ERR_UNSUPPORTED 3
+#define CNRX_ERR_CUDA 4
+
+/* LayerOp values (network.hpp:17) */
+#define CNRX_OP_INPUT 0
+#define CNRX_OP_CONV 1
+#define CNRX_OP_DWCONV 2
+#define CNRX_OP_RELU 3
+#define CNRX_OP_BN 4
+#define CNRX_OP_LN 5
+#define CNRX_OP_ADD 6
+#define CNRX_OP_MUL 7
+#define CNRX_OP_CONCAT 8
+
+/* NormMode (norms.hpp:12) */
+#define CNRX_MODE_TRAIN 0
+#define CNRX_MODE_EVAL 1
+
+/* Arithmetic of the compiled plan. FP32: CUDA-core fp32 kernels, LLRs within 1e-4 relative of the
+ * reference.  BF16: bf16 weights/activations with fp32 accumulation on tcgen05 tensor cores. */
+#define CNRX_FP32 0
+#define CNRX_BF16 1
+
+/* GraphNode (network.hpp:19-26) + dilation_f (extension for BASELINE config 3; 1 = reference). */
+typedef struct {
+  int32_t op, in0, in1, w, b, gamma, beta, rmean, rvar, bn_flag, out_channels, dilation_f;
+} cnrx_node;
+
+/* NamedParam (network.hpp:28-33): row-major fp32 data, dims[0..rank) (conv weights [kh,kw,Cin,Cout]). */
+typedef struct {
+  const char* name;
+  int32_t rank;
+  int32_t learnable;
+  int64_t dims[4];
+  const float* data;
+} cnrx_param;
+
+typedef struct cnrx_plan cnrx_plan;
+
+/* Compile a network into a device plan on `device`.  Validates the graph the way the reference's
+ * builders and forward() do; copies (and for BF16 folds/converts) all weights once — the caller's
+ * arrays are not referenced afterwards.  Every batch norm must be ready (bn_ready[flag] != 0), as
+ * eval-mode forward requires (norms.hpp:66-69). */
+int cnrx_plan_create(const cnrx_node* nodes, int32_t n_nodes, int32_t input_node, int32_t output_node,
+                     const cnrx_param* params, int32_t n_params, const uint8_t* bn_ready, int32_t n_bn,
+                     int32_t precision, int32_t device, cnrx_plan** out);
+void cnrx_plan_destroy(cnrx_plan* plan);
+
+/* Thread-local message for the last non-zero status on this thread. */
+const char* cnrx_last_error(void);
+
+/* Network<float>::forward(x, mode) (network.hpp:162): x is [B,T,F,C] fp32 channels-last host memory
+ * (tensor.hpp:17-19), out receives [B,T,F,output_channels] fp32.  Synchronous.  mode must be
+ * CNRX_MODE_EVAL. */
+int cnrx_forward(cnrx_plan* plan, const float* x, int64_t B, int64_t T, int64_t F, int64_t C, int32_t mode,
+                 float* out);
+/* Same with device pointers, enqueued on `stream` (asynchronous). */
+int cnrx_forward_device(cnrx_plan* plan, const float* x_dev, int64_t B, int64_t T, int64_t F, int64_t C,
+                        int32_t mode, float* out_dev, void* stream);
+
+/* Receiver path (featurize -> subnetworks -> fusion -> head).  The pilot grid is fixed per plan
+ * (pilots.cpp:13-31 "identical across samples"): pilots [T,F] complex (re,im) fp32, mask [T,F]. */
+int cnrx_set_pilots(cnrx_plan* plan, int64_t T, int64_t F, const float* pilots, const uint8_t* mask);
+/* y: [B,T,F,N] complex (re,im) fp32 received grid -> llr [B,T,F,bits] fp32; the plan's input must have
+ * 6N channels (per antenna: Re y, Im y, Re x_p, Im x_p, Re h_ls, Im h_ls).  Host memory, synchronous. */
+int cnrx_receive(cnrx_plan* plan, const float* y, int64_t B, int64_t T, int64_t F, int64_t N, float* llr);
+int cnrx_receive_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t T, int64_t F, int64_t N,
+                        float* llr_dev, void* stream);
+/* Featurize alone (device): feat [B,T,F,6N] fp32 in the reference layout. */
+int cnrx_featurize_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t T, int64_t F, int64_t N,
+                          float* feat_dev, void* stream);
+
+/* Slot-sharded receive across several plans (one per GPU, built from the same network): slots are
+ * split into contiguous ranges, each GPU runs its range from host memory on its own thread, LLRs land
+ * in the caller's buffer.  No collective on the data path. */
+int cnrx_receive_sharded(cnrx_plan* const* plans, int32_t n_plans, const float* y, int64_t B, int64_t T,
+                         int64_t F, int64_t N, float* llr);
+
+/* Introspection for benchmarks and tests. */
+typedef struct {
+  int32_t precision;
+  int32_t device;
+  int32_t n_launches;        /* kernels per forward at the last shape (0 before the first forward) */
+  int32_t n_tc_convs;        /* convs lowered to tcgen05 implicit GEMM */
+  int32_t input_channels;
+  int32_t output_channels;
+  int64_t macs_per_re;       /* algorithmic MACs per resource element (all taps) */
+  int64_t rows_per_slot;     /* padded activation rows per slot in the BF16 plane layout */
+  int64_t workspace_bytes;
+} cnrx_plan_info;
+int cnrx_get_plan_info(const cnrx_plan* plan, cnrx_plan_info* info);
+
+/* Capture the forward of the current shape into a CUDA graph and replay it on subsequent calls
+ * with identical (B,T,F) and pointers (enable=1), or disable (0). */
+int cnrx_set_graph_capture(cnrx_plan* plan, int32_t enable);
+
+/* Per-launch device timing: with profiling enabled every forward records a CUDA event after each
+ * kernel on the launching stream; cnrx_read_profile synchronises, accumulates the per-position
+ * durations (ms) and call counts since the last read into ms[]/counts[] (up to max_n entries) and
+ * returns the number of positions in *n_out.  Position i is the kernel cnrx_launch_name(i). */
+int cnrx_set_profiling(cnrx_plan* plan, int32_t enable);
+int cnrx_read_profile(cnrx_plan* plan, int32_t max_n, float* ms, int32_t* counts, int32_t* n_out);
+
+/* Name of the kernel launched at position i of the last forward (for profiling / tests), and its
+ * algorithmic FLOPs per resource element (2 x MACs over all taps; 0 for non-GEMM kernels, -1 past
+ * the end). */
+const char* cnrx_launch_name(const cnrx_plan* plan, int32_t i);
+int64_t cnrx_launch_flops(const cnrx_plan* plan, int32_t i);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CONETRX_CUDA_H */

@@ -1,0 +1,1390 @@
+// api.cpp — the C ABI (include/conetrx_cuda.h): plan creation, the plan compiler and the executor.
+//
+// A plan is compiled once from the reference network's own description (GraphNode list + named
+// params + BN-ready flags, network.hpp:19-33,335-337) and then runs Network<float>::forward
+// (network.hpp:162-180) on the GPU:
+//
+//   CNRX_FP32  node-level executor in the reference layout [B,T,F,C]: every LayerOp has an fp32 CUDA
+//              kernel (generic_f32.cu); a conv absorbs the single-consumer BN / ReLU / add|mul chain
+//              after it.  Any graph the reference builders produce runs on this path.
+//   CNRX_BF16  lowering onto tcgen05 implicit-GEMM convolutions over bf16 activation planes
+//              (conv_tc.cu): BN after a conv is folded into its weights, ReLU / residual add / the next
+//              block's pre-activation go into the conv epilogue, same-level convs of different
+//              subnetworks share one grouped launch, and the fusion tail + 1x1 head is a single
+//              pointwise-program kernel (pointwise.cu).  Graph shapes the lowering cannot express are
+//              rejected with CNRX_ERR_UNSUPPORTED — there is no CPU fallback anywhere.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/conetrx_cuda.h"
+#include "common.h"
+#include "conv_tc.h"
+#include "kernels.h"
+
+using namespace cnrx;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return CNRX_OK;
+  } catch (const Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::exception& e) {
+    return fail(CNRX_ERR_INVALID_ARGUMENT, e.what());
+  }
+}
+
+struct HostParam {
+  std::string name;
+  std::vector<int64_t> dims;
+  std::vector<float> data;
+  bool learnable = true;
+  int64_t numel() const {
+    int64_t n = 1;
+    for (auto d : dims) n *= d;
+    return n;
+  }
+};
+
+constexpr double kBnEps = 1e-5;  // network.hpp:429
+constexpr double kLnEps = 1e-5;  // network.hpp:431
+
+// Eval BN as a per-channel affine, computed exactly like norms.hpp:81-88 (istd in double, then float).
+void bn_affine(const HostParam& g, const HostParam& s, const HostParam& rm, const HostParam& rv,
+               std::vector<float>& scale, std::vector<float>& shift) {
+  const size_t c = g.data.size();
+  scale.resize(c);
+  shift.resize(c);
+  for (size_t i = 0; i < c; ++i) {
+    const float istd = static_cast<float>(1.0 / std::sqrt(static_cast<double>(rv.data[i]) + kBnEps));
+    scale[i] = g.data[i] * istd;
+    shift[i] = s.data[i] - rm.data[i] * scale[i];
+  }
+}
+
+int round_cin(int c) {
+  if (c <= 16) return 16;
+  if (c <= 32) return 32;
+  if (c <= 64) return 64;
+  if (c <= 96) return 96;
+  return (c + 63) / 64 * 64;
+}
+int round_cout(int c) { return (c + 31) / 32 * 32; }
+
+// ------------------------------------------------------------------------------------------------
+// FP32 program
+// ------------------------------------------------------------------------------------------------
+enum F32Kind { F_CONV, F_DWCONV, F_AFFINE, F_RELU, F_BINARY, F_LN, F_CONCAT };
+struct F32Step {
+  F32Kind kind;
+  int out_val;              // value id written
+  int in0 = -1, in1 = -1;   // value ids read
+  int node = -1;            // primary node
+  ConvF32 conv{};           // static parts (weights, epilogue tables)
+  int op = 0;               // binary op
+  int relu = 0;
+  const float* s = nullptr;
+  const float* t = nullptr;
+  const float* g = nullptr;
+  const float* b = nullptr;
+  int C = 0, C2 = 0, kh = 0, kw = 0;
+  const float* w = nullptr;
+  const float* bias = nullptr;
+};
+
+// ------------------------------------------------------------------------------------------------
+// BF16 program
+// ------------------------------------------------------------------------------------------------
+struct PlaneInfo {
+  int C = 0;           // padded channels
+  bool nonneg = false; // every valid value >= 0 (output of a ReLU)
+  int level = 0;       // level of its producer
+  int last_use = 0;    // last level reading it
+  int buffer = -1;     // workspace buffer index
+};
+struct TcOp {
+  int node = -1;
+  int cin = 0, cout = 0, ks = 1, dil = 1;
+  int cin_real = 0, cout_real = 0;
+  int in_plane = -1, res_plane = -1, out_plane = -1, out2_plane = -1;
+  int relu = 0;
+  void* wimg = nullptr;
+  float* bias = nullptr;
+  float* s2 = nullptr;
+  float* t2 = nullptr;
+  int level = 0;
+};
+struct PwStep {
+  PwProgram prog{};
+  int plane_ids[kPwMaxPlanes];
+  int n_planes = 0;
+  int out_plane = -1;  // -1: head
+  int level = 0;
+};
+
+struct Workspace {
+  int B = -1, T = -1, F = -1;
+  PlaneGeom geo{};
+  std::vector<void*> buffers;
+  std::vector<size_t> sizes;
+  void* in_buf = nullptr;   // device copy of host input
+  size_t in_bytes = 0;
+  void* out_buf = nullptr;  // device output for host APIs
+  size_t out_bytes = 0;
+  void* feat_buf = nullptr; // fp32 features when an FP32 plan runs the receive path
+  size_t feat_bytes = 0;
+  std::vector<TcLaunch> launches;   // prepared tensor maps per TC group (bf16)
+};
+
+}  // namespace
+
+struct cnrx_plan {
+  int precision = CNRX_FP32;
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::vector<cnrx_node> nodes;
+  int in_node = -1, out_node = -1;
+  std::vector<HostParam> params;
+  std::vector<uint8_t> bn_ready;
+  std::vector<std::vector<int>> consumers;
+  int in_ch = 0, out_ch = 0;
+  int64_t macs = 0;
+  std::vector<void*> dev_allocs;
+
+  // fp32
+  std::vector<F32Step> f32;
+  std::vector<int> f32_val_channels;  // channels of each value
+  std::vector<int> f32_val_buffer;    // buffer index per value (-1 = external input/output)
+  int f32_in_val = -1, f32_out_val = -1;
+  int f32_nbuf = 0;
+  std::vector<int> f32_buf_channels;
+
+  // bf16
+  std::vector<PlaneInfo> planes;
+  std::vector<TcOp> tc;
+  std::vector<PwStep> pw;
+  std::vector<std::vector<std::vector<int>>> tc_groups_by_level;  // [level] -> groups -> op ids
+  std::vector<std::vector<int>> pw_by_level;
+  int n_levels = 0;
+  int npad = 1;
+  std::vector<int> buf_channels;  // plane buffers
+
+  // pilots
+  bool has_pilots = false;
+  int pT = 0, pF = 0;
+  PilotTablesDev pt{};
+
+  Workspace ws;
+  std::vector<std::string> launch_names;
+  std::mutex mu;
+
+  // per-launch profiling (events around every launch of a forward)
+  bool profile = false;
+  std::vector<std::vector<cudaEvent_t>> prof_events;  // one vector per profiled forward
+  std::vector<cudaEvent_t> event_pool;
+  std::vector<double> prof_ms;
+  std::vector<int32_t> prof_count;
+  cudaEvent_t take_event() {
+    cudaEvent_t e;
+    if (!event_pool.empty()) {
+      e = event_pool.back();
+      event_pool.pop_back();
+    } else {
+      CNRX_CUDA(cudaEventCreate(&e));
+    }
+    return e;
+  }
+  std::vector<int64_t> launch_flops;  // algorithmic FLOP per resource element of each launch
+  void note(const char* name, cudaStream_t s, int64_t flops_per_re = 0) {
+    launch_names.emplace_back(name);
+    launch_flops.push_back(flops_per_re);
+    if (profile && !prof_events.empty()) {
+      cudaEvent_t e = take_event();
+      CNRX_CUDA(cudaEventRecord(e, s));
+      prof_events.back().push_back(e);
+    }
+  }
+
+  // graph capture
+  bool capture = false;
+  cudaGraphExec_t gexec = nullptr;
+  std::string gkey;
+
+  float* upload(const std::vector<float>& v) {
+    float* d = nullptr;
+    CNRX_CUDA(cudaMalloc(&d, std::max<size_t>(1, v.size()) * sizeof(float)));
+    dev_allocs.push_back(d);
+    if (!v.empty()) CNRX_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice));
+    return d;
+  }
+  void* upload_bytes(const void* p, size_t n) {
+    void* d = nullptr;
+    CNRX_CUDA(cudaMalloc(&d, std::max<size_t>(16, n)));
+    dev_allocs.push_back(d);
+    CNRX_CUDA(cudaMemcpy(d, p, n, cudaMemcpyHostToDevice));
+    return d;
+  }
+  const HostParam& P(int i) const { return params[static_cast<size_t>(i)]; }
+  const cnrx_node& N(int i) const { return nodes[static_cast<size_t>(i)]; }
+  int single_consumer(int i) const {
+    const auto& c = consumers[static_cast<size_t>(i)];
+    return c.size() == 1 ? c[0] : -1;
+  }
+};
+
+namespace {
+
+// ------------------------------------------------------------------------------------------------
+// Validation (mirrors the checks the reference's builders and forward perform)
+// ------------------------------------------------------------------------------------------------
+void validate_graph(cnrx_plan& p) {
+  const int n = static_cast<int>(p.nodes.size());
+  require(p.in_node >= 0 && p.in_node < n && p.out_node >= 0 && p.out_node < n, "network has no input/output");
+  require(p.N(p.in_node).op == CNRX_OP_INPUT, "input node is not an input op");
+  p.consumers.assign(static_cast<size_t>(n), {});
+  auto param_ok = [&](int idx) { return idx >= 0 && idx < static_cast<int>(p.params.size()); };
+  for (int i = 0; i < n; ++i) {
+    const cnrx_node& nd = p.N(i);
+    if (nd.op == CNRX_OP_INPUT) {
+      require(i == p.in_node, "network already has an input node");
+      continue;
+    }
+    require(nd.in0 >= 0 && nd.in0 < i, "bad input node index");
+    const int cin = p.N(nd.in0).out_channels;
+    if (nd.in1 >= 0) require(nd.in1 < i, "bad input node index");
+    p.consumers[static_cast<size_t>(nd.in0)].push_back(i);
+    if (nd.in1 >= 0) p.consumers[static_cast<size_t>(nd.in1)].push_back(i);
+    switch (nd.op) {
+      case CNRX_OP_CONV: {
+        require(param_ok(nd.w), "conv without weights");
+        const auto& w = p.P(nd.w);
+        require(w.dims.size() == 4, "conv weights must be [kh,kw,Cin,Cout]");
+        require(w.dims[0] % 2 == 1 && w.dims[1] % 2 == 1, "conv kernel dims must be odd");
+        require(w.dims[2] == cin, "conv input has " + std::to_string(cin) + " channels but weights expect " +
+                                      std::to_string(w.dims[2]));
+        require(w.dims[3] == nd.out_channels, "conv output channel mismatch");
+        if (nd.b >= 0) require(param_ok(nd.b) && p.P(nd.b).numel() == w.dims[3], "conv bias must be [Cout]");
+        require(nd.dilation_f >= 1, "dilation must be >= 1");
+        p.macs += w.dims[0] * w.dims[1] * w.dims[2] * w.dims[3];
+        break;
+      }
+      case CNRX_OP_DWCONV: {
+        require(param_ok(nd.w), "dwconv without weights");
+        const auto& w = p.P(nd.w);
+        require(w.dims.size() == 4 && w.dims[3] == 1 && w.dims[2] == cin, "depthwise weights must be [kh,kw,C,1]");
+        p.macs += w.dims[0] * w.dims[1] * w.dims[2];
+        break;
+      }
+      case CNRX_OP_BN:
+        require(param_ok(nd.gamma) && param_ok(nd.beta) && param_ok(nd.rmean) && param_ok(nd.rvar),
+                "batch norm parameters missing");
+        require(p.P(nd.gamma).numel() == cin, "batch norm gain must be [C]");
+        require(nd.bn_flag >= 0 && nd.bn_flag < static_cast<int>(p.bn_ready.size()), "bad bn flag");
+        if (!p.bn_ready[static_cast<size_t>(nd.bn_flag)])
+          throw Error(CNRX_ERR_NOT_READY,
+                      "batch norm evaluated in eval mode before any train-mode update; train first or seed the "
+                      "running statistics");
+        break;
+      case CNRX_OP_LN:
+        require(param_ok(nd.gamma) && param_ok(nd.beta) && p.P(nd.gamma).numel() == cin, "layer norm gain must be [C]");
+        break;
+      case CNRX_OP_ADD:
+      case CNRX_OP_MUL:
+        require(nd.in1 >= 0, "binary op needs two inputs");
+        require(p.N(nd.in1).out_channels == cin, "elementwise fusion requires equal channel counts");
+        break;
+      case CNRX_OP_CONCAT:
+        require(nd.in1 >= 0, "concat needs two inputs");
+        break;
+      case CNRX_OP_RELU:
+        break;
+      default:
+        throw Error(CNRX_ERR_INVALID_ARGUMENT, "unknown op " + std::to_string(nd.op));
+    }
+  }
+  p.in_ch = p.N(p.in_node).out_channels;
+  p.out_ch = p.N(p.out_node).out_channels;
+  for (auto& nd : p.nodes) p.npad = std::max(p.npad, nd.op == CNRX_OP_CONV ? nd.dilation_f : 1);
+}
+
+// ------------------------------------------------------------------------------------------------
+// FP32 compile
+// ------------------------------------------------------------------------------------------------
+void compile_f32(cnrx_plan& p) {
+  const int n = static_cast<int>(p.nodes.size());
+  std::vector<int> val_of(static_cast<size_t>(n), -1);
+  std::vector<char> absorbed(static_cast<size_t>(n), 0);
+  auto new_val = [&](int C) {
+    p.f32_val_channels.push_back(C);
+    return static_cast<int>(p.f32_val_channels.size()) - 1;
+  };
+  p.f32_in_val = new_val(p.in_ch);
+  val_of[static_cast<size_t>(p.in_node)] = p.f32_in_val;
+  for (int i = 0; i < n; ++i) {
+    if (i == p.in_node || absorbed[static_cast<size_t>(i)]) continue;
+    const cnrx_node& nd = p.N(i);
+    F32Step st{};
+    st.node = i;
+    st.in0 = val_of[static_cast<size_t>(nd.in0)];
+    int end = i;
+    switch (nd.op) {
+      case CNRX_OP_CONV: {
+        st.kind = F_CONV;
+        const auto& w = p.P(nd.w);
+        st.conv.w = p.upload(w.data);
+        st.conv.bias = nd.b >= 0 ? p.upload(p.P(nd.b).data) : nullptr;
+        st.conv.kh = static_cast<int>(w.dims[0]);
+        st.conv.kw = static_cast<int>(w.dims[1]);
+        st.conv.cin = static_cast<int>(w.dims[2]);
+        st.conv.cout = static_cast<int>(w.dims[3]);
+        st.conv.dil_f = nd.dilation_f;
+        int c = p.single_consumer(end);
+        if (c >= 0 && p.N(c).op == CNRX_OP_BN && end != p.out_node) {
+          std::vector<float> s, t;
+          const auto& bn = p.N(c);
+          bn_affine(p.P(bn.gamma), p.P(bn.beta), p.P(bn.rmean), p.P(bn.rvar), s, t);
+          st.conv.aff_s = p.upload(s);
+          st.conv.aff_t = p.upload(t);
+          absorbed[static_cast<size_t>(c)] = 1;
+          end = c;
+          c = p.single_consumer(end);
+        }
+        if (c >= 0 && p.N(c).op == CNRX_OP_RELU && end != p.out_node) {
+          st.conv.relu = 1;
+          absorbed[static_cast<size_t>(c)] = 1;
+          end = c;
+          c = p.single_consumer(end);
+        }
+        if (c >= 0 && (p.N(c).op == CNRX_OP_ADD || p.N(c).op == CNRX_OP_MUL) && end != p.out_node) {
+          const int other = p.N(c).in0 == end ? p.N(c).in1 : p.N(c).in0;
+          if (other != end && other < i && val_of[static_cast<size_t>(other)] >= 0) {
+            st.conv.other_op = p.N(c).op;
+            st.in1 = val_of[static_cast<size_t>(other)];
+            absorbed[static_cast<size_t>(c)] = 1;
+            end = c;
+          }
+        }
+        break;
+      }
+      case CNRX_OP_DWCONV: {
+        st.kind = F_DWCONV;
+        const auto& w = p.P(nd.w);
+        st.w = p.upload(w.data);
+        st.bias = nd.b >= 0 ? p.upload(p.P(nd.b).data) : nullptr;
+        st.kh = static_cast<int>(w.dims[0]);
+        st.kw = static_cast<int>(w.dims[1]);
+        break;
+      }
+      case CNRX_OP_BN: {
+        st.kind = F_AFFINE;
+        std::vector<float> s, t;
+        bn_affine(p.P(nd.gamma), p.P(nd.beta), p.P(nd.rmean), p.P(nd.rvar), s, t);
+        st.s = p.upload(s);
+        st.t = p.upload(t);
+        const int c = p.single_consumer(i);
+        if (c >= 0 && p.N(c).op == CNRX_OP_RELU && i != p.out_node) {
+          st.relu = 1;
+          absorbed[static_cast<size_t>(c)] = 1;
+          end = c;
+        }
+        break;
+      }
+      case CNRX_OP_RELU:
+        st.kind = F_RELU;
+        break;
+      case CNRX_OP_ADD:
+      case CNRX_OP_MUL:
+        st.kind = F_BINARY;
+        st.op = nd.op;
+        st.in1 = val_of[static_cast<size_t>(nd.in1)];
+        break;
+      case CNRX_OP_LN:
+        st.kind = F_LN;
+        st.g = p.upload(p.P(nd.gamma).data);
+        st.b = p.upload(p.P(nd.beta).data);
+        break;
+      case CNRX_OP_CONCAT:
+        st.kind = F_CONCAT;
+        st.in1 = val_of[static_cast<size_t>(nd.in1)];
+        st.C2 = p.N(nd.in1).out_channels;
+        break;
+      default:
+        throw Error(CNRX_ERR_UNSUPPORTED, "op not supported");
+    }
+    st.C = p.N(nd.in0).out_channels;
+    st.out_val = new_val(p.N(end).out_channels);
+    val_of[static_cast<size_t>(end)] = st.out_val;
+    p.f32.push_back(st);
+  }
+  p.f32_out_val = val_of[static_cast<size_t>(p.out_node)];
+  require(p.f32_out_val >= 0, "output node is not computed");
+  // buffer assignment by liveness (values live from their producing step to their last reader)
+  const int nv = static_cast<int>(p.f32_val_channels.size());
+  std::vector<int> last(static_cast<size_t>(nv), -1);
+  for (int s = 0; s < static_cast<int>(p.f32.size()); ++s) {
+    const auto& st = p.f32[static_cast<size_t>(s)];
+    if (st.in0 >= 0) last[static_cast<size_t>(st.in0)] = s;
+    if (st.in1 >= 0) last[static_cast<size_t>(st.in1)] = s;
+  }
+  p.f32_val_buffer.assign(static_cast<size_t>(nv), -1);
+  std::vector<int> free_at;  // per buffer: step after which it is free
+  for (int s = 0; s < static_cast<int>(p.f32.size()); ++s) {
+    auto& st = p.f32[static_cast<size_t>(s)];
+    if (st.out_val == p.f32_out_val) continue;  // external
+    const int C = p.f32_val_channels[static_cast<size_t>(st.out_val)];
+    int chosen = -1;
+    for (int b = 0; b < p.f32_nbuf; ++b)
+      if (p.f32_buf_channels[static_cast<size_t>(b)] == C && free_at[static_cast<size_t>(b)] < s) {
+        chosen = b;
+        break;
+      }
+    if (chosen < 0) {
+      chosen = p.f32_nbuf++;
+      p.f32_buf_channels.push_back(C);
+      free_at.push_back(0);
+    }
+    p.f32_val_buffer[static_cast<size_t>(st.out_val)] = chosen;
+    free_at[static_cast<size_t>(chosen)] = std::max(s, last[static_cast<size_t>(st.out_val)]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// BF16 compile
+// ------------------------------------------------------------------------------------------------
+struct Bf16Compiler {
+  cnrx_plan& p;
+  std::vector<int> node_plane;    // node -> plane holding its value
+  std::vector<int> plane_producer_tc;  // plane -> tc op index that writes it as primary/out2 (-1 none)
+
+  explicit Bf16Compiler(cnrx_plan& pl) : p(pl) {}
+
+  int new_plane(int C, int level, bool nonneg) {
+    PlaneInfo pi;
+    pi.C = C;
+    pi.level = level;
+    pi.nonneg = nonneg;
+    p.planes.push_back(pi);
+    plane_producer_tc.push_back(-1);
+    return static_cast<int>(p.planes.size()) - 1;
+  }
+  void use(int plane, int level) {
+    auto& pi = p.planes[static_cast<size_t>(plane)];
+    pi.last_use = std::max(pi.last_use, level);
+  }
+
+  // Linear pointwise chain ending at node u whose leaves are planes.  Appends instructions and
+  // returns true on success.
+  bool build_chain(int u, PwStep& st, std::vector<std::vector<float>>& aff_tables, int& level) {
+    if (node_plane[static_cast<size_t>(u)] >= 0) {
+      const int pl = node_plane[static_cast<size_t>(u)];
+      if (st.n_planes >= kPwMaxPlanes) return false;
+      st.plane_ids[st.n_planes] = pl;
+      st.prog.ins[st.prog.n_ins++] = {PW_LOAD, st.n_planes++};
+      level = std::max(level, p.planes[static_cast<size_t>(pl)].level);
+      return true;
+    }
+    const cnrx_node& nd = p.N(u);
+    if (st.prog.n_ins >= kPwMaxIns - 1) return false;
+    switch (nd.op) {
+      case CNRX_OP_RELU:
+        if (!build_chain(nd.in0, st, aff_tables, level)) return false;
+        st.prog.ins[st.prog.n_ins++] = {PW_RELU, 0};
+        return true;
+      case CNRX_OP_BN: {
+        if (!build_chain(nd.in0, st, aff_tables, level)) return false;
+        std::vector<float> s, t;
+        bn_affine(p.P(nd.gamma), p.P(nd.beta), p.P(nd.rmean), p.P(nd.rvar), s, t);
+        const int k = static_cast<int>(aff_tables.size()) / 2;
+        if (k >= kPwMaxAff) return false;
+        aff_tables.push_back(s);
+        aff_tables.push_back(t);
+        st.prog.ins[st.prog.n_ins++] = {PW_AFF, k};
+        return true;
+      }
+      case CNRX_OP_ADD:
+      case CNRX_OP_MUL: {
+        // one operand must be a plane leaf
+        int leaf = -1, rest = -1;
+        if (node_plane[static_cast<size_t>(nd.in1)] >= 0) {
+          leaf = nd.in1;
+          rest = nd.in0;
+        } else if (node_plane[static_cast<size_t>(nd.in0)] >= 0) {
+          leaf = nd.in0;
+          rest = nd.in1;
+        } else {
+          return false;
+        }
+        if (!build_chain(rest, st, aff_tables, level)) return false;
+        const int pl = node_plane[static_cast<size_t>(leaf)];
+        if (st.n_planes >= kPwMaxPlanes) return false;
+        st.plane_ids[st.n_planes] = pl;
+        st.prog.ins[st.prog.n_ins++] = {nd.op == CNRX_OP_MUL ? PW_MUL : PW_ADD, st.n_planes++};
+        level = std::max(level, p.planes[static_cast<size_t>(pl)].level);
+        return true;
+      }
+      default:
+        return false;
+    }
+  }
+
+  void finish_pw(PwStep& st, std::vector<std::vector<float>>& aff_tables, int C) {
+    st.prog.C = C;
+    for (size_t k = 0; k < aff_tables.size() / 2; ++k) {
+      auto s = aff_tables[2 * k], t = aff_tables[2 * k + 1];
+      s.resize(static_cast<size_t>(C), 0.f);
+      t.resize(static_cast<size_t>(C), 0.f);
+      st.prog.aff_s[k] = p.upload(s);
+      st.prog.aff_t[k] = p.upload(t);
+    }
+    for (int k = 0; k < st.n_planes; ++k) use(st.plane_ids[k], st.level);
+  }
+
+  // Materialise node u as a plane (for a conv input or a residual operand).
+  int plane_for(int u) {
+    int pl = node_plane[static_cast<size_t>(u)];
+    if (pl >= 0) return pl;
+    const cnrx_node& nd = p.N(u);
+    // relu(v) / relu(bn(v)) where v's plane comes from a TC epilogue: second epilogue output.
+    if (nd.op == CNRX_OP_RELU) {
+      int v = nd.in0;
+      const cnrx_node* bn = nullptr;
+      if (node_plane[static_cast<size_t>(v)] < 0 && p.N(v).op == CNRX_OP_BN &&
+          node_plane[static_cast<size_t>(p.N(v).in0)] >= 0) {
+        bn = &p.N(v);
+        v = p.N(v).in0;
+      }
+      const int vp = node_plane[static_cast<size_t>(v)];
+      if (vp >= 0) {
+        if (!bn && p.planes[static_cast<size_t>(vp)].nonneg) {  // relu(relu(x)) = relu(x)
+          node_plane[static_cast<size_t>(u)] = vp;
+          return vp;
+        }
+        const int prod = plane_producer_tc[static_cast<size_t>(vp)];
+        if (prod >= 0 && p.tc[static_cast<size_t>(prod)].out_plane == vp && p.tc[static_cast<size_t>(prod)].out2_plane < 0) {
+          TcOp& op = p.tc[static_cast<size_t>(prod)];
+          const int np = new_plane(p.planes[static_cast<size_t>(vp)].C, op.level, true);
+          op.out2_plane = np;
+          if (bn) {
+            std::vector<float> s, t;
+            bn_affine(p.P(bn->gamma), p.P(bn->beta), p.P(bn->rmean), p.P(bn->rvar), s, t);
+            s.resize(static_cast<size_t>(op.cout), 0.f);
+            t.resize(static_cast<size_t>(op.cout), 0.f);
+            op.s2 = p.upload(s);
+            op.t2 = p.upload(t);
+          }
+          plane_producer_tc[static_cast<size_t>(np)] = prod;
+          node_plane[static_cast<size_t>(u)] = np;
+          return np;
+        }
+      }
+    }
+    // general linear pointwise chain -> pointwise program kernel
+    PwStep st;
+    std::vector<std::vector<float>> aff;
+    int level = 0;
+    if (!build_chain(u, st, aff, level))
+      throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: node " + std::to_string(u) + " (" +
+                                            std::to_string(nd.op) + ") is not a linear pointwise chain over planes");
+    const int C = round_cin(nd.out_channels);
+    st.level = level + 1;
+    st.out_plane = new_plane(C, st.level, false);
+    finish_pw(st, aff, C);
+    p.pw.push_back(st);
+    node_plane[static_cast<size_t>(u)] = st.out_plane;
+    return st.out_plane;
+  }
+
+  void compile() {
+    const int n = static_cast<int>(p.nodes.size());
+    node_plane.assign(static_cast<size_t>(n), -1);
+    std::vector<char> absorbed(static_cast<size_t>(n), 0);
+    const int cin0 = round_cin(p.in_ch);
+    node_plane[static_cast<size_t>(p.in_node)] = new_plane(cin0, 0, false);
+    for (int i = 0; i < n; ++i) {
+      const cnrx_node& nd = p.N(i);
+      if (nd.op != CNRX_OP_CONV || absorbed[static_cast<size_t>(i)] || i == p.out_node) continue;
+      const auto& w = p.P(nd.w);
+      TcOp op;
+      op.node = i;
+      op.ks = static_cast<int>(w.dims[0]);
+      require(w.dims[0] == w.dims[1], "bf16 plan supports square kernels only");
+      if (op.ks != 1 && op.ks != 3)
+        throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan supports 1x1 and 3x3 convolutions");
+      op.dil = nd.dilation_f;
+      op.in_plane = plane_for(nd.in0);
+      op.cin = p.planes[static_cast<size_t>(op.in_plane)].C;
+      op.cout = round_cout(nd.out_channels);
+      op.cin_real = static_cast<int>(w.dims[2]);
+      op.cout_real = static_cast<int>(w.dims[3]);
+      if (!conv_tc_supported(op.cin, op.cout, op.ks))
+        throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: no tcgen05 conv for cin=" + std::to_string(op.cin) +
+                                              " cout=" + std::to_string(op.cout) + " k=" + std::to_string(op.ks));
+      // epilogue absorption: [BN] [ReLU] [add residual]
+      std::vector<float> scale, shift;
+      std::vector<float> bias(static_cast<size_t>(op.cout), 0.f);
+      if (nd.b >= 0)
+        for (int c = 0; c < nd.out_channels; ++c) bias[static_cast<size_t>(c)] = p.P(nd.b).data[static_cast<size_t>(c)];
+      int end = i;
+      int c = p.single_consumer(end);
+      if (c >= 0 && p.N(c).op == CNRX_OP_BN && c != p.out_node) {
+        const auto& bn = p.N(c);
+        bn_affine(p.P(bn.gamma), p.P(bn.beta), p.P(bn.rmean), p.P(bn.rvar), scale, shift);
+        for (int k = 0; k < nd.out_channels; ++k)
+          bias[static_cast<size_t>(k)] = bias[static_cast<size_t>(k)] * scale[static_cast<size_t>(k)] + shift[static_cast<size_t>(k)];
+        absorbed[static_cast<size_t>(c)] = 1;
+        end = c;
+        c = p.single_consumer(end);
+      }
+      if (c >= 0 && p.N(c).op == CNRX_OP_RELU) {
+        op.relu = 1;
+        absorbed[static_cast<size_t>(c)] = 1;
+        end = c;
+        c = p.single_consumer(end);
+      }
+      if (!op.relu && c >= 0 && p.N(c).op == CNRX_OP_ADD) {
+        const int other = p.N(c).in0 == end ? p.N(c).in1 : p.N(c).in0;
+        if (other != end && other < i) {
+          op.res_plane = plane_for(other);
+          if (p.planes[static_cast<size_t>(op.res_plane)].C == op.cout) {
+            absorbed[static_cast<size_t>(c)] = 1;
+            end = c;
+          } else {
+            op.res_plane = -1;
+          }
+        }
+      }
+      int level = p.planes[static_cast<size_t>(op.in_plane)].level;
+      if (op.res_plane >= 0) level = std::max(level, p.planes[static_cast<size_t>(op.res_plane)].level);
+      op.level = level + 1;
+      use(op.in_plane, op.level);
+      if (op.res_plane >= 0) use(op.res_plane, op.level);
+      // weights (BN scale folded per output channel) and bias
+      std::vector<uint8_t> img(conv_tc_wimg_bytes(op.cin, op.cout, op.ks));
+      conv_tc_pack_weights(w.data.data(), op.ks, static_cast<int>(w.dims[2]), static_cast<int>(w.dims[3]),
+                           scale.empty() ? nullptr : scale.data(), op.cin, op.cout, img.data());
+      op.wimg = p.upload_bytes(img.data(), img.size());
+      op.bias = p.upload(bias);
+      op.out_plane = new_plane(op.cout, op.level, op.relu != 0);
+      p.tc.push_back(op);
+      plane_producer_tc[static_cast<size_t>(op.out_plane)] = static_cast<int>(p.tc.size()) - 1;
+      node_plane[static_cast<size_t>(end)] = op.out_plane;
+    }
+    // output: 1x1 conv head over a linear pointwise chain
+    const cnrx_node& on = p.N(p.out_node);
+    if (on.op != CNRX_OP_CONV) throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: output node must be a conv");
+    const auto& hw = p.P(on.w);
+    if (hw.dims[0] != 1 || hw.dims[1] != 1 || on.out_channels > kPwMaxBits)
+      throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: output conv must be 1x1 with <= 16 outputs");
+    PwStep st;
+    std::vector<std::vector<float>> aff;
+    int level = 0;
+    if (!build_chain(on.in0, st, aff, level))
+      throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: head input is not a linear pointwise chain over planes");
+    st.level = level + 1;
+    st.out_plane = -1;
+    const int C = round_cin(static_cast<int>(hw.dims[2]));
+    for (int k = 0; k < st.n_planes; ++k)
+      require(p.planes[static_cast<size_t>(st.plane_ids[k])].C == C, "bf16 plan: head operand channel mismatch");
+    std::vector<float> wpad(static_cast<size_t>(C) * on.out_channels, 0.f);
+    for (int ci = 0; ci < hw.dims[2]; ++ci)
+      for (int co = 0; co < on.out_channels; ++co)
+        wpad[static_cast<size_t>(ci) * on.out_channels + co] = hw.data[static_cast<size_t>(ci) * on.out_channels + co];
+    std::vector<float> hb(static_cast<size_t>(on.out_channels), 0.f);
+    if (on.b >= 0) hb = p.P(on.b).data;
+    st.prog.head_bits = on.out_channels;
+    st.prog.head_w = p.upload(wpad);
+    st.prog.head_b = p.upload(hb);
+    finish_pw(st, aff, C);
+    p.pw.push_back(st);
+    // level schedule
+    int maxl = 0;
+    for (auto& op : p.tc) maxl = std::max(maxl, op.level);
+    for (auto& s2 : p.pw) maxl = std::max(maxl, s2.level);
+    p.n_levels = maxl + 1;
+    p.tc_groups_by_level.assign(static_cast<size_t>(p.n_levels), {});
+    p.pw_by_level.assign(static_cast<size_t>(p.n_levels), {});
+    for (int k = 0; k < static_cast<int>(p.tc.size()); ++k) {
+      const TcOp& op = p.tc[static_cast<size_t>(k)];
+      auto& groups = p.tc_groups_by_level[static_cast<size_t>(op.level)];
+      bool placed = false;
+      for (auto& g : groups) {
+        const TcOp& o0 = p.tc[static_cast<size_t>(g[0])];
+        if (static_cast<int>(g.size()) < kTcMaxGroups && o0.cin == op.cin && o0.cout == op.cout && o0.ks == op.ks) {
+          g.push_back(k);
+          placed = true;
+          break;
+        }
+      }
+      if (!placed) groups.push_back({k});
+    }
+    for (int k = 0; k < static_cast<int>(p.pw.size()); ++k)
+      p.pw_by_level[static_cast<size_t>(p.pw[static_cast<size_t>(k)].level)].push_back(k);
+    // out2 planes share their producer's level; every plane is live from its level to last use
+    for (auto& op : p.tc) {
+      if (op.out2_plane >= 0) p.planes[static_cast<size_t>(op.out2_plane)].level = op.level;
+    }
+    // buffer assignment by liveness over levels (a buffer is reusable once every reader's level passed)
+    std::vector<int> order(p.planes.size());
+    for (size_t k = 0; k < order.size(); ++k) order[k] = static_cast<int>(k);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return p.planes[static_cast<size_t>(a)].level < p.planes[static_cast<size_t>(b)].level;
+    });
+    std::vector<int> buf_free_after;
+    for (int pl : order) {
+      auto& pi = p.planes[static_cast<size_t>(pl)];
+      if (pi.last_use < pi.level) pi.last_use = pi.level;
+      int chosen = -1;
+      for (size_t b = 0; b < p.buf_channels.size(); ++b)
+        if (p.buf_channels[b] == pi.C && buf_free_after[b] < pi.level) {
+          chosen = static_cast<int>(b);
+          break;
+        }
+      if (chosen < 0) {
+        chosen = static_cast<int>(p.buf_channels.size());
+        p.buf_channels.push_back(pi.C);
+        buf_free_after.push_back(-1);
+      }
+      pi.buffer = chosen;
+      buf_free_after[static_cast<size_t>(chosen)] = pi.last_use;
+    }
+  }
+};
+
+// ------------------------------------------------------------------------------------------------
+// Execution
+// ------------------------------------------------------------------------------------------------
+void ensure_workspace(cnrx_plan& p, int B, int T, int F) {
+  Workspace& ws = p.ws;
+  if (ws.B == B && ws.T == T && ws.F == F) return;
+  for (void* b : ws.buffers) cudaFree(b);
+  ws.buffers.clear();
+  ws.sizes.clear();
+  ws.launches.clear();
+  if (p.gexec) {
+    cudaGraphExecDestroy(p.gexec);
+    p.gexec = nullptr;
+    p.gkey.clear();
+  }
+  ws.B = B;
+  ws.T = T;
+  ws.F = F;
+  if (p.precision == CNRX_FP32) {
+    const int64_t rows = static_cast<int64_t>(B) * T * F;
+    for (int c : p.f32_buf_channels) {
+      void* d = nullptr;
+      CNRX_CUDA(cudaMalloc(&d, static_cast<size_t>(rows) * c * sizeof(float)));
+      ws.buffers.push_back(d);
+    }
+    return;
+  }
+  ws.geo = make_geom(B, T, F, p.npad);
+  for (int c : p.buf_channels) {
+    void* d = nullptr;
+    const size_t bytes = static_cast<size_t>(ws.geo.Nalloc) * c * 2;
+    CNRX_CUDA(cudaMalloc(&d, bytes));
+    CNRX_CUDA(cudaMemset(d, 0, bytes));
+    ws.buffers.push_back(d);
+  }
+  // tensor maps / launch descriptors per TC group
+  for (int lv = 0; lv < p.n_levels; ++lv)
+    for (auto& grp : p.tc_groups_by_level[static_cast<size_t>(lv)]) {
+      TcLaunch L;
+      std::memset(&L, 0, sizeof(L));
+      L.geo = ws.geo;
+      L.ngroups = static_cast<int>(grp.size());
+      int win_alloc = 0;
+      for (size_t gi = 0; gi < grp.size(); ++gi) {
+        const TcOp& op = p.tc[static_cast<size_t>(grp[gi])];
+        TcGroup& g = L.g[gi];
+        auto plane_ptr = [&](int pl) -> __nv_bfloat16* {
+          return pl < 0 ? nullptr
+                        : static_cast<__nv_bfloat16*>(ws.buffers[static_cast<size_t>(p.planes[static_cast<size_t>(pl)].buffer)]);
+        };
+        g.halo = op.ks == 1 ? 0 : ws.geo.T1 * op.dil + 1;
+        g.dil = op.dil;
+        const int rows = 128 + 2 * g.halo;
+        win_alloc = std::max(win_alloc, (rows + 31) / 32 * 32);
+        conv_tc_make_maps(plane_ptr(op.in_plane), ws.geo.Nalloc, op.cin, 32, g.map);
+        g.wimg = static_cast<const uint8_t*>(op.wimg);
+        g.bias = op.bias;
+        g.res = plane_ptr(op.res_plane);
+        g.out = plane_ptr(op.out_plane);
+        g.out2 = plane_ptr(op.out2_plane);
+        g.s2 = op.s2;
+        g.t2 = op.t2;
+        g.relu = op.relu;
+      }
+      L.win_alloc = win_alloc;
+      const TcOp& op0 = p.tc[static_cast<size_t>(grp[0])];
+      int stages = 4;
+      while (stages > 1 && conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc) > 227 * 1024) --stages;
+      if (conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc) > 227 * 1024)
+        throw Error(CNRX_ERR_UNSUPPORTED, "tcgen05 conv working set exceeds shared memory");
+      L.stages = stages;
+      ws.launches.push_back(L);
+    }
+}
+
+void run_f32(cnrx_plan& p, const float* x, float* out, cudaStream_t s) {
+  Workspace& ws = p.ws;
+  auto val_ptr = [&](int v) -> float* {
+    if (v == p.f32_in_val) return const_cast<float*>(x);
+    if (v == p.f32_out_val) return out;
+    return static_cast<float*>(ws.buffers[static_cast<size_t>(p.f32_val_buffer[static_cast<size_t>(v)])]);
+  };
+  const int B = ws.B, T = ws.T, F = ws.F;
+  const int64_t rows = static_cast<int64_t>(B) * T * F;
+  for (const auto& st : p.f32) {
+    float* y = val_ptr(st.out_val);
+    const float* a = val_ptr(st.in0);
+    switch (st.kind) {
+      case F_CONV: {
+        ConvF32 c = st.conv;
+        c.x = a;
+        c.y = y;
+        c.B = B;
+        c.T = T;
+        c.F = F;
+        c.other = st.in1 >= 0 ? val_ptr(st.in1) : nullptr;
+        p.note(launch_conv_f32(c, s), s, 2ll * c.kh * c.kw * c.cin * c.cout);
+        break;
+      }
+      case F_DWCONV:
+        p.note(launch_dwconv_f32(a, st.w, st.bias, y, B, T, F, st.C, st.kh, st.kw, s), s, 2ll * st.kh * st.kw * st.C);
+        break;
+      case F_AFFINE:
+        p.note(launch_affine_f32(a, st.s, st.t, st.relu, y, rows, st.C, s), s);
+        break;
+      case F_RELU:
+        p.note(launch_relu_f32(a, y, rows * st.C, s), s);
+        break;
+      case F_BINARY:
+        p.note(launch_binary_f32(st.op, a, val_ptr(st.in1), y, rows * st.C, s), s);
+        break;
+      case F_LN:
+        p.note(launch_layernorm_f32(a, st.g, st.b, y, rows, st.C, kLnEps, s), s);
+        break;
+      case F_CONCAT:
+        p.note(launch_concat_f32(a, st.C, val_ptr(st.in1), st.C2, y, rows, s), s);
+        break;
+    }
+  }
+}
+
+// input_kind: 0 = features [B,T,F,C] fp32, 1 = received grid y [B,T,F,N] complex
+void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, cudaStream_t s) {
+  Workspace& ws = p.ws;
+  auto plane_ptr = [&](int pl) {
+    return static_cast<__nv_bfloat16*>(ws.buffers[static_cast<size_t>(p.planes[static_cast<size_t>(pl)].buffer)]);
+  };
+  __nv_bfloat16* in_plane = plane_ptr(0);
+  if (input_kind == 0)
+    p.note(launch_pack_plane(in, ws.geo, p.in_ch, in_plane, p.planes[0].C, s), s);
+  else
+    p.note(launch_featurize_plane(in, ws.geo, N, p.pt, in_plane, p.planes[0].C, s), s);
+  size_t li = 0;
+  for (int lv = 0; lv < p.n_levels; ++lv) {
+    for (size_t gi = 0; gi < p.tc_groups_by_level[static_cast<size_t>(lv)].size(); ++gi) {
+      const auto& grp = p.tc_groups_by_level[static_cast<size_t>(lv)][gi];
+      const TcOp& op0 = p.tc[static_cast<size_t>(grp[0])];
+      int64_t fl = 0;
+      for (int k : grp) {
+        const TcOp& o = p.tc[static_cast<size_t>(k)];
+        fl += 2ll * o.ks * o.ks * o.cin_real * o.cout_real;
+      }
+      p.note(conv_tc_launch(op0.cin, op0.cout, op0.ks, ws.launches[li++], p.num_sms, s), s, fl);
+    }
+    for (int k : p.pw_by_level[static_cast<size_t>(lv)]) {
+      PwStep& st = p.pw[static_cast<size_t>(k)];
+      PwProgram prog = st.prog;
+      for (int j = 0; j < st.n_planes; ++j) prog.planes[j] = plane_ptr(st.plane_ids[j]);
+      if (st.out_plane >= 0)
+        prog.out_plane = plane_ptr(st.out_plane);
+      else
+        prog.llr = out;
+      p.note(launch_pw_program(prog, ws.geo, s), s);
+    }
+  }
+}
+
+void check_shape(cnrx_plan& p, int64_t B, int64_t T, int64_t F, int64_t C) {
+  require(B > 0 && T > 0 && F > 0 && C > 0, "tensor dimensions must be positive");
+  require(C == p.in_ch, "network expects " + std::to_string(p.in_ch) + " input channels, got [" + std::to_string(B) +
+                            "," + std::to_string(T) + "," + std::to_string(F) + "," + std::to_string(C) + "]");
+  require(B < (1ll << 31) && T < 4096 && F < (1 << 20), "tensor dimensions too large");
+}
+
+void* ensure_dev(void*& buf, size_t& cap, size_t bytes) {
+  if (cap < bytes) {
+    if (buf) cudaFree(buf);
+    CNRX_CUDA(cudaMalloc(&buf, bytes));
+    cap = bytes;
+  }
+  return buf;
+}
+
+void run_forward(cnrx_plan& p, const float* x_dev, int64_t B, int64_t T, int64_t F, float* out_dev, int input_kind,
+                 int N, cudaStream_t s) {
+  ensure_workspace(p, static_cast<int>(B), static_cast<int>(T), static_cast<int>(F));
+  auto enqueue = [&]() {
+    p.launch_names.clear();
+    p.launch_flops.clear();
+    if (p.profile && !p.capture) {
+      p.prof_events.emplace_back();
+      cudaEvent_t e = p.take_event();
+      CNRX_CUDA(cudaEventRecord(e, s));
+      p.prof_events.back().push_back(e);
+    }
+    if (p.precision == CNRX_FP32) {
+      if (input_kind == 1) {
+        // featurize into an fp32 reference-layout buffer, then run the node program on it
+        const size_t bytes = static_cast<size_t>(B * T * F * p.in_ch) * sizeof(float);
+        float* feat = static_cast<float*>(ensure_dev(p.ws.feat_buf, p.ws.feat_bytes, bytes));
+        PlaneGeom g = make_geom(static_cast<int>(B), static_cast<int>(T), static_cast<int>(F), 1);
+        p.note(launch_featurize_ref(x_dev, g, N, p.pt, feat, s), s);
+        run_f32(p, feat, out_dev, s);
+      } else {
+        run_f32(p, x_dev, out_dev, s);
+      }
+    } else {
+      run_bf16(p, x_dev, input_kind, N, out_dev, s);
+    }
+  };
+  if (!p.capture) {
+    enqueue();
+    return;
+  }
+  char key[256];
+  snprintf(key, sizeof key, "%p/%p/%lld/%lld/%lld/%d/%p", static_cast<const void*>(x_dev), static_cast<void*>(out_dev),
+           static_cast<long long>(B), static_cast<long long>(T), static_cast<long long>(F), input_kind,
+           static_cast<void*>(s));
+  if (!p.gexec || p.gkey != key) {
+    if (p.gexec) {
+      cudaGraphExecDestroy(p.gexec);
+      p.gexec = nullptr;
+    }
+    cudaGraph_t graph;
+    CNRX_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue();
+    } catch (...) {
+      cudaStreamEndCapture(s, &graph);
+      throw;
+    }
+    CNRX_CUDA(cudaStreamEndCapture(s, &graph));
+    CNRX_CUDA(cudaGraphInstantiate(&p.gexec, graph, 0));
+    cudaGraphDestroy(graph);
+    p.gkey = key;
+  }
+  CNRX_CUDA(cudaGraphLaunch(p.gexec, s));
+}
+
+
+void build_pilot_tables(cnrx_plan& p, int64_t T, int64_t F, const float* pilots, const uint8_t* mask) {
+  std::vector<int> syms;
+  for (int64_t t = 0; t < T; ++t) {
+    bool any = false;
+    for (int64_t f = 0; f < F; ++f) any |= mask[t * F + f] != 0;
+    if (any) syms.push_back(static_cast<int>(t));
+  }
+  require(!syms.empty(), "pilot pattern has no pilots");
+  if (static_cast<int>(syms.size()) > kMaxPilotSyms) throw Error(CNRX_ERR_UNSUPPORTED, "more than 8 pilot symbols");
+  const int ns = static_cast<int>(syms.size());
+  std::vector<int32_t> flo(static_cast<size_t>(ns * F)), fhi(static_cast<size_t>(ns * F));
+  std::vector<float> wf(static_cast<size_t>(ns * F));
+  std::vector<float> x(static_cast<size_t>(2 * T * F), 0.f), inv(static_cast<size_t>(2 * T * F), 0.f);
+  for (int64_t i = 0; i < T * F; ++i)
+    if (mask[i]) {
+      const double xr = pilots[2 * i], xi = pilots[2 * i + 1];
+      const double den = xr * xr + xi * xi;
+      require(den > 0, "zero pilot symbol");
+      x[static_cast<size_t>(2 * i)] = static_cast<float>(xr);
+      x[static_cast<size_t>(2 * i + 1)] = static_cast<float>(xi);
+      inv[static_cast<size_t>(2 * i)] = static_cast<float>(xr / den);
+      inv[static_cast<size_t>(2 * i + 1)] = static_cast<float>(-xi / den);
+    }
+  for (int j = 0; j < ns; ++j) {
+    std::vector<int> pf;
+    for (int64_t f = 0; f < F; ++f)
+      if (mask[syms[static_cast<size_t>(j)] * F + f]) pf.push_back(static_cast<int>(f));
+    for (int64_t f = 0; f < F; ++f) {
+      int k0, k1;
+      double w;
+      if (f <= pf.front()) {
+        k0 = k1 = 0;
+        w = 0;
+      } else if (f >= pf.back()) {
+        k0 = k1 = static_cast<int>(pf.size()) - 1;
+        w = 0;
+      } else {
+        k0 = 0;
+        while (pf[static_cast<size_t>(k0 + 1)] < f) ++k0;
+        k1 = k0 + 1;
+        w = static_cast<double>(f - pf[static_cast<size_t>(k0)]) / (pf[static_cast<size_t>(k1)] - pf[static_cast<size_t>(k0)]);
+      }
+      flo[static_cast<size_t>(j * F + f)] = pf[static_cast<size_t>(k0)];
+      fhi[static_cast<size_t>(j * F + f)] = pf[static_cast<size_t>(k1)];
+      wf[static_cast<size_t>(j * F + f)] = static_cast<float>(w);
+    }
+  }
+  std::vector<int32_t> jlo(static_cast<size_t>(T)), jhi(static_cast<size_t>(T));
+  std::vector<float> wt(static_cast<size_t>(T));
+  for (int64_t t = 0; t < T; ++t) {
+    int j0, j1;
+    double w;
+    if (t <= syms.front()) {
+      j0 = j1 = 0;
+      w = 0;
+    } else if (t >= syms.back()) {
+      j0 = j1 = ns - 1;
+      w = 0;
+    } else {
+      j0 = 0;
+      while (syms[static_cast<size_t>(j0 + 1)] < t) ++j0;
+      j1 = j0 + 1;
+      w = static_cast<double>(t - syms[static_cast<size_t>(j0)]) / (syms[static_cast<size_t>(j1)] - syms[static_cast<size_t>(j0)]);
+    }
+    jlo[static_cast<size_t>(t)] = j0;
+    jhi[static_cast<size_t>(t)] = j1;
+    wt[static_cast<size_t>(t)] = static_cast<float>(w);
+  }
+  PilotTablesDev pt{};
+  pt.n_sym = ns;
+  for (int j = 0; j < ns; ++j) pt.sym[j] = syms[static_cast<size_t>(j)];
+  pt.flo = static_cast<const int32_t*>(p.upload_bytes(flo.data(), flo.size() * 4));
+  pt.fhi = static_cast<const int32_t*>(p.upload_bytes(fhi.data(), fhi.size() * 4));
+  pt.wf = p.upload(wf);
+  pt.jlo = static_cast<const int32_t*>(p.upload_bytes(jlo.data(), jlo.size() * 4));
+  pt.jhi = static_cast<const int32_t*>(p.upload_bytes(jhi.data(), jhi.size() * 4));
+  pt.wt = p.upload(wt);
+  pt.x = p.upload(x);
+  pt.inv_x = p.upload(inv);
+  p.pt = pt;
+  p.pT = static_cast<int>(T);
+  p.pF = static_cast<int>(F);
+  p.has_pilots = true;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CNRX_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+// ================================================================================================
+// C ABI
+// ================================================================================================
+extern "C" {
+
+const char* cnrx_last_error(void) { return g_last_error.c_str(); }
+
+int cnrx_plan_create(const cnrx_node* nodes, int32_t n_nodes, int32_t input_node, int32_t output_node,
+                     const cnrx_param* params, int32_t n_params, const uint8_t* bn_ready, int32_t n_bn,
+                     int32_t precision, int32_t device, cnrx_plan** out) {
+  if (!out) return fail(CNRX_ERR_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  auto plan = std::make_unique<cnrx_plan>();
+  const int rc = guarded([&] {
+    require(nodes && n_nodes > 0, "empty network");
+    require(precision == CNRX_FP32 || precision == CNRX_BF16, "unknown precision");
+    int ndev = 0;
+    CNRX_CUDA(cudaGetDeviceCount(&ndev));
+    require(device >= 0 && device < ndev, "no such CUDA device " + std::to_string(device));
+    DeviceGuard dg(device);
+    cudaDeviceProp prop;
+    CNRX_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (precision == CNRX_BF16 && prop.major != 10)
+      throw Error(CNRX_ERR_UNSUPPORTED, "bf16 tcgen05 plan needs an sm_100 (Blackwell) device");
+    plan->precision = precision;
+    plan->device = device;
+    plan->num_sms = prop.multiProcessorCount;
+    plan->nodes.assign(nodes, nodes + n_nodes);
+    plan->in_node = input_node;
+    plan->out_node = output_node;
+    plan->params.resize(static_cast<size_t>(n_params));
+    for (int i = 0; i < n_params; ++i) {
+      HostParam& hp = plan->params[static_cast<size_t>(i)];
+      hp.name = params[i].name ? params[i].name : "";
+      require(params[i].rank >= 1 && params[i].rank <= 4, "parameter rank must be 1..4");
+      hp.dims.assign(params[i].dims, params[i].dims + params[i].rank);
+      hp.learnable = params[i].learnable != 0;
+      const int64_t nel = hp.numel();
+      require(nel > 0 && params[i].data, "parameter " + hp.name + " has no data");
+      hp.data.assign(params[i].data, params[i].data + nel);
+    }
+    plan->bn_ready.assign(bn_ready, bn_ready + n_bn);
+    validate_graph(*plan);
+    CNRX_CUDA(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+    if (precision == CNRX_FP32)
+      compile_f32(*plan);
+    else
+      Bf16Compiler(*plan).compile();
+  });
+  if (rc != CNRX_OK) {
+    cnrx_plan_destroy(plan.release());
+    return rc;
+  }
+  *out = plan.release();
+  return CNRX_OK;
+}
+
+void cnrx_plan_destroy(cnrx_plan* plan) {
+  if (!plan) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(plan->device);
+  if (plan->stream) cudaStreamSynchronize(plan->stream);
+  if (plan->gexec) cudaGraphExecDestroy(plan->gexec);
+  for (void* b : plan->ws.buffers) cudaFree(b);
+  if (plan->ws.in_buf) cudaFree(plan->ws.in_buf);
+  if (plan->ws.out_buf) cudaFree(plan->ws.out_buf);
+  if (plan->ws.feat_buf) cudaFree(plan->ws.feat_buf);
+  for (void* d : plan->dev_allocs) cudaFree(d);
+  for (auto& evs : plan->prof_events)
+    for (auto e : evs) cudaEventDestroy(e);
+  for (auto e : plan->event_pool) cudaEventDestroy(e);
+  if (plan->stream) cudaStreamDestroy(plan->stream);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete plan;
+}
+
+int cnrx_forward_device(cnrx_plan* plan, const float* x_dev, int64_t B, int64_t T, int64_t F, int64_t C,
+                        int32_t mode, float* out_dev, void* stream) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    if (mode != CNRX_MODE_EVAL)
+      throw Error(CNRX_ERR_UNSUPPORTED, "only NormMode::eval is supported (train mutates running statistics)");
+    check_shape(*plan, B, T, F, C);
+    require(x_dev && out_dev, "null tensor pointer");
+    DeviceGuard dg(plan->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->stream;
+    run_forward(*plan, x_dev, B, T, F, out_dev, 0, 0, s);
+  });
+}
+
+int cnrx_forward(cnrx_plan* plan, const float* x, int64_t B, int64_t T, int64_t F, int64_t C, int32_t mode,
+                 float* out) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    if (mode != CNRX_MODE_EVAL)
+      throw Error(CNRX_ERR_UNSUPPORTED, "only NormMode::eval is supported (train mutates running statistics)");
+    check_shape(*plan, B, T, F, C);
+    require(x && out, "null tensor pointer");
+    DeviceGuard dg(plan->device);
+    const size_t in_bytes = static_cast<size_t>(B * T * F * C) * sizeof(float);
+    const size_t out_bytes = static_cast<size_t>(B * T * F * plan->out_ch) * sizeof(float);
+    float* din = static_cast<float*>(ensure_dev(plan->ws.in_buf, plan->ws.in_bytes, in_bytes));
+    float* dout = static_cast<float*>(ensure_dev(plan->ws.out_buf, plan->ws.out_bytes, out_bytes));
+    CNRX_CUDA(cudaMemcpyAsync(din, x, in_bytes, cudaMemcpyHostToDevice, plan->stream));
+    run_forward(*plan, din, B, T, F, dout, 0, 0, plan->stream);
+    CNRX_CUDA(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, plan->stream));
+    CNRX_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int cnrx_set_pilots(cnrx_plan* plan, int64_t T, int64_t F, const float* pilots, const uint8_t* mask) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    require(T > 0 && F > 0 && pilots && mask, "bad pilot grid");
+    DeviceGuard dg(plan->device);
+    build_pilot_tables(*plan, T, F, pilots, mask);
+    if (plan->gexec) {
+      cudaGraphExecDestroy(plan->gexec);
+      plan->gexec = nullptr;
+      plan->gkey.clear();
+    }
+  });
+}
+
+static void check_receive(cnrx_plan& p, int64_t B, int64_t T, int64_t F, int64_t N) {
+  require(p.has_pilots, "cnrx_set_pilots must be called before receive");
+  require(T == p.pT && F == p.pF, "received grid [T,F] does not match the pilot grid");
+  require(N >= 1 && 6 * N == p.in_ch, "network expects " + std::to_string(p.in_ch) + " input channels, i.e. " +
+                                          std::to_string(p.in_ch / 6) + " antennas, got N=" + std::to_string(N));
+  require(B > 0, "tensor dimensions must be positive");
+}
+
+int cnrx_receive_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t T, int64_t F, int64_t N,
+                        float* llr_dev, void* stream) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    check_receive(*plan, B, T, F, N);
+    require(y_dev && llr_dev, "null tensor pointer");
+    DeviceGuard dg(plan->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->stream;
+    run_forward(*plan, y_dev, B, T, F, llr_dev, 1, static_cast<int>(N), s);
+  });
+}
+
+int cnrx_receive(cnrx_plan* plan, const float* y, int64_t B, int64_t T, int64_t F, int64_t N, float* llr) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    check_receive(*plan, B, T, F, N);
+    require(y && llr, "null tensor pointer");
+    DeviceGuard dg(plan->device);
+    const size_t in_bytes = static_cast<size_t>(B * T * F * N) * 2 * sizeof(float);
+    const size_t out_bytes = static_cast<size_t>(B * T * F * plan->out_ch) * sizeof(float);
+    float* din = static_cast<float*>(ensure_dev(plan->ws.in_buf, plan->ws.in_bytes, in_bytes));
+    float* dout = static_cast<float*>(ensure_dev(plan->ws.out_buf, plan->ws.out_bytes, out_bytes));
+    CNRX_CUDA(cudaMemcpyAsync(din, y, in_bytes, cudaMemcpyHostToDevice, plan->stream));
+    run_forward(*plan, din, B, T, F, dout, 1, static_cast<int>(N), plan->stream);
+    CNRX_CUDA(cudaMemcpyAsync(llr, dout, out_bytes, cudaMemcpyDeviceToHost, plan->stream));
+    CNRX_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int cnrx_featurize_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t T, int64_t F, int64_t N,
+                          float* feat_dev, void* stream) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    require(plan->has_pilots, "cnrx_set_pilots must be called before featurize");
+    require(T == plan->pT && F == plan->pF && B > 0 && N >= 1, "received grid does not match the pilot grid");
+    DeviceGuard dg(plan->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->stream;
+    PlaneGeom g = make_geom(static_cast<int>(B), static_cast<int>(T), static_cast<int>(F), 1);
+    launch_featurize_ref(y_dev, g, static_cast<int>(N), plan->pt, feat_dev, s);
+  });
+}
+
+int cnrx_receive_sharded(cnrx_plan* const* plans, int32_t n_plans, const float* y, int64_t B, int64_t T, int64_t F,
+                         int64_t N, float* llr) {
+  if (!plans || n_plans < 1) return fail(CNRX_ERR_INVALID_ARGUMENT, "no plans");
+  const int64_t per = (B + n_plans - 1) / n_plans;
+  std::vector<int> rcs(static_cast<size_t>(n_plans), CNRX_OK);
+  std::vector<std::string> msgs(static_cast<size_t>(n_plans));
+  std::vector<std::thread> th;
+  for (int i = 0; i < n_plans; ++i) {
+    const int64_t b0 = i * per, b1 = std::min(B, b0 + per);
+    if (b0 >= b1) break;
+    th.emplace_back([&, i, b0, b1] {
+      const int out_ch = plans[i]->out_ch;
+      rcs[static_cast<size_t>(i)] =
+          cnrx_receive(plans[i], y + b0 * T * F * N * 2, b1 - b0, T, F, N, llr + b0 * T * F * out_ch);
+      if (rcs[static_cast<size_t>(i)] != CNRX_OK) msgs[static_cast<size_t>(i)] = cnrx_last_error();
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int i = 0; i < n_plans; ++i)
+    if (rcs[static_cast<size_t>(i)] != CNRX_OK)
+      return fail(rcs[static_cast<size_t>(i)], "shard " + std::to_string(i) + ": " + msgs[static_cast<size_t>(i)]);
+  return CNRX_OK;
+}
+
+int cnrx_get_plan_info(const cnrx_plan* plan, cnrx_plan_info* info) {
+  if (!plan || !info) return fail(CNRX_ERR_INVALID_ARGUMENT, "null argument");
+  std::memset(info, 0, sizeof(*info));
+  info->precision = plan->precision;
+  info->device = plan->device;
+  info->n_launches = static_cast<int32_t>(plan->launch_names.size());
+  info->n_tc_convs = static_cast<int32_t>(plan->tc.size());
+  info->input_channels = plan->in_ch;
+  info->output_channels = plan->out_ch;
+  info->macs_per_re = plan->macs;
+  info->rows_per_slot = plan->ws.geo.P;
+  size_t ws = 0;
+  if (plan->precision == CNRX_BF16) {
+    for (int c : plan->buf_channels) ws += static_cast<size_t>(plan->ws.geo.Nalloc) * c * 2;
+  } else {
+    for (int c : plan->f32_buf_channels) ws += static_cast<size_t>(plan->ws.B) * plan->ws.T * plan->ws.F * c * 4;
+  }
+  info->workspace_bytes = static_cast<int64_t>(ws);
+  return CNRX_OK;
+}
+
+int cnrx_set_graph_capture(cnrx_plan* plan, int32_t enable) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  std::lock_guard<std::mutex> lk(plan->mu);
+  plan->capture = enable != 0;
+  if (!plan->capture && plan->gexec) {
+    cudaGraphExecDestroy(plan->gexec);
+    plan->gexec = nullptr;
+    plan->gkey.clear();
+  }
+  return CNRX_OK;
+}
+
+int cnrx_set_profiling(cnrx_plan* plan, int32_t enable) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  std::lock_guard<std::mutex> lk(plan->mu);
+  plan->profile = enable != 0;
+  return CNRX_OK;
+}
+
+int cnrx_read_profile(cnrx_plan* plan, int32_t max_n, float* ms, int32_t* counts, int32_t* n_out) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    DeviceGuard dg(plan->device);
+    for (auto& evs : plan->prof_events) {
+      if (evs.empty()) continue;
+      CNRX_CUDA(cudaEventSynchronize(evs.back()));
+      for (size_t k = 1; k < evs.size(); ++k) {
+        float t = 0.f;
+        CNRX_CUDA(cudaEventElapsedTime(&t, evs[k - 1], evs[k]));
+        if (plan->prof_ms.size() < k) {
+          plan->prof_ms.resize(k, 0.0);
+          plan->prof_count.resize(k, 0);
+        }
+        plan->prof_ms[k - 1] += t;
+        plan->prof_count[k - 1] += 1;
+      }
+      for (auto e : evs) plan->event_pool.push_back(e);
+    }
+    plan->prof_events.clear();
+    const int n = static_cast<int>(plan->prof_ms.size());
+    if (n_out) *n_out = n;
+    for (int i = 0; i < n && i < max_n; ++i) {
+      if (ms) ms[i] = static_cast<float>(plan->prof_ms[static_cast<size_t>(i)]);
+      if (counts) counts[i] = plan->prof_count[static_cast<size_t>(i)];
+    }
+    plan->prof_ms.clear();
+    plan->prof_count.clear();
+  });
+}
+
+int64_t cnrx_launch_flops(const cnrx_plan* plan, int32_t i) {
+  if (!plan || i < 0 || i >= static_cast<int32_t>(plan->launch_flops.size())) return -1;
+  return plan->launch_flops[static_cast<size_t>(i)];
+}
+
+const char* cnrx_launch_name(const cnrx_plan* plan, int32_t i) {
+  if (!plan || i < 0 || i >= static_cast<int32_t>(plan->launch_names.size())) return nullptr;
+  return plan->launch_names[static_cast<size_t>(i)].c_str();
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// common.h — definitions shared by the host runtime (api.cpp) and the kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace cnrx {
+
+// ---------------------------------------------------------------------------------------------
+// Plane layout.  A bf16 activation "plane" stores one graph value
+// for a whole slot batch as rows of C channels.  Within a slot the grid is stored frequency-column
+// by column with the T symbols of a column contiguous, followed by one zero row, and each slot is
+// preceded by `npad` all-zero columns:
+//
+//     row(b, f, t) = b*P + (f + npad)*(T+1) + t,    P = (F + npad)*(T+1)
+//
+// plus npad trailing zero columns after the last slot.  With that padding a 3x3 "same" convolution
+// (dilation d <= npad along F) is a 1-D stencil over rows with offsets (dt-1) + (df-1)*d*(T+1): every
+// tap that falls outside the grid lands on a zero row, so the implicit GEMM needs no masking.
+// Rows that are padding are kept at zero by every kernel that writes a plane.
+// ---------------------------------------------------------------------------------------------
+struct PlaneGeom {
+  int32_t B, T, F, npad;
+  int32_t T1;       // T + 1 rows per frequency column
+  int64_t P;        // rows per slot
+  int64_t Npos;     // B*P + npad*T1
+  int64_t Nalloc;   // Npos rounded up to the 128-row GEMM tile
+  int64_t n_tiles;  // Nalloc / 128
+
+  __host__ __device__ bool valid(int64_t row) const {
+    if (row >= static_cast<int64_t>(B) * P) return false;
+    const int64_t r = row % P;
+    const int64_t c = r / T1;
+    const int64_t t = r - c * T1;
+    return t < T && c >= npad;
+  }
+  // (b, t, f) of a valid row
+  __host__ __device__ void coords(int64_t row, int32_t& b, int32_t& t, int32_t& f) const {
+    b = static_cast<int32_t>(row / P);
+    const int64_t r = row - static_cast<int64_t>(b) * P;
+    const int64_t c = r / T1;
+    t = static_cast<int32_t>(r - c * T1);
+    f = static_cast<int32_t>(c - npad);
+  }
+  __host__ __device__ int64_t row_of(int32_t b, int32_t t, int32_t f) const {
+    return static_cast<int64_t>(b) * P + static_cast<int64_t>(f + npad) * T1 + t;
+  }
+};
+
+inline PlaneGeom make_geom(int B, int T, int F, int npad) {
+  PlaneGeom g{};
+  g.B = B;
+  g.T = T;
+  g.F = F;
+  g.npad = npad;
+  g.T1 = T + 1;
+  g.P = static_cast<int64_t>(F + npad) * g.T1;
+  g.Npos = static_cast<int64_t>(B) * g.P + static_cast<int64_t>(npad) * g.T1;
+  g.Nalloc = (g.Npos + 127) / 128 * 128;
+  g.n_tiles = g.Nalloc / 128;
+  return g;
+}
+
+// Error type carrying a C-ABI status code.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CNRX_CUDA(call)                                                                                    \
+  do {                                                                                                     \
+    cudaError_t e_ = (call);                                                                               \
+    if (e_ != cudaSuccess)                                                                                 \
+      throw ::cnrx::Error(4, std::string("CUDA error in ") + #call + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+inline void require(bool cond, const std::string& msg) {
+  if (!cond) throw Error(1, msg);
+}
+
+}  // namespace cnrx

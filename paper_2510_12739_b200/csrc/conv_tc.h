@@ -1,0 +1,53 @@
+// conv_tc.h — launch interface of the tcgen05 implicit-GEMM convolution (conv_tc.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.h"
+
+namespace cnrx {
+
+constexpr int kTcMaxGroups = 4;
+
+// One convolution of a grouped launch (e.g. the same layer of the three CoNet subnetworks).
+struct TcGroup {
+  CUtensorMap map[2];               // input plane, K-chunk 0 (<=64 ch) and chunk 1 (remaining ch)
+  const uint8_t* wimg;              // weights, pre-swizzled smem image: [tap][chunk][COUT rows]
+  const float* bias;                // [COUT] (BN folded in)
+  const __nv_bfloat16* res;         // residual plane [Nalloc][COUT] or nullptr
+  __nv_bfloat16* out;               // primary output plane [Nalloc][COUT]
+  __nv_bfloat16* out2;              // optional pre-activated copy for the next conv, or nullptr
+  const float* s2;                  // out2 = relu(v*s2 + t2) (nullptr: relu(v))
+  const float* t2;
+  int32_t relu;                     // relu on the primary output (after bias / residual)
+  int32_t dil;                      // dilation along F
+  int32_t halo;                     // window halo rows = (T+1)*dil + 1 (0 for 1x1)
+  int32_t pad_;
+};
+
+struct TcLaunch {
+  TcGroup g[kTcMaxGroups];
+  PlaneGeom geo;
+  int32_t ngroups;
+  int32_t stages;                   // window pipeline depth
+  int32_t win_alloc;                // rows allocated per window stage (max over groups, 8-aligned)
+  int32_t pad_;
+};
+
+// Shared memory the kernel needs for (cin, cout, ks) with `stages` window stages of `win_alloc` rows.
+size_t conv_tc_smem_bytes(int cin, int cout, int ks, int stages, int win_alloc);
+bool conv_tc_supported(int cin, int cout, int ks);
+// Enqueue one grouped launch; grid = min(#SMs, ngroups * tiles).  Returns the kernel name.
+const char* conv_tc_launch(int cin, int cout, int ks, const TcLaunch& L, int num_sms, cudaStream_t stream);
+
+// Host helpers to build the operand layouts the kernel expects.
+// Byte size of the weight image for (cin, cout, ks).
+size_t conv_tc_wimg_bytes(int cin, int cout, int ks);
+// w: fp32 [ks,ks,cin_real,cout_real] (reference layout, kernels.hpp:32), scaled per output channel
+// by `scale` (nullable, folded BN); written as bf16 into `img` (host buffer of conv_tc_wimg_bytes).
+void conv_tc_pack_weights(const float* w, int ks, int cin_real, int cout_real, const float* scale, int cin,
+                          int cout, uint8_t* img);
+// Tensor maps for K-chunks of an input plane [nalloc][cin] bf16 with a window box of `box_rows` rows.
+void conv_tc_make_maps(const void* plane, int64_t nalloc, int cin, int box_rows, CUtensorMap* maps);
+
+}  // namespace cnrx

@@ -1,0 +1,99 @@
+// kernels.h — host-side launchers of the non-GEMM kernels (featurize, pointwise programs / head,
+// generic fp32 node kernels).  Every launcher enqueues on the given stream and returns the kernel's
+// name (recorded per forward for profiling and for the driver's native-code evidence).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.h"
+
+namespace cnrx {
+
+constexpr int kMaxPilotSyms = 8;
+
+// Interpolation tables for the LS estimate, precomputed once per plan from the pilot grid.
+struct PilotTablesDev {
+  int32_t n_sym;
+  int32_t sym[kMaxPilotSyms];   // pilot symbol indices (ascending)
+  const int32_t* flo;           // [n_sym][F] bracketing pilot subcarriers
+  const int32_t* fhi;
+  const float* wf;              // [n_sym][F] weight of fhi
+  const int32_t* jlo;           // [T] bracketing pilot symbols (index into sym)
+  const int32_t* jhi;
+  const float* wt;              // [T]
+  const float* x;               // [T][F] complex pilot grid (0 off-pilot)
+  const float* inv_x;           // [T][F] complex 1/x at pilot REs
+};
+
+const char* launch_featurize_plane(const float* y, const PlaneGeom& geo, int N, const PilotTablesDev& pt,
+                                   __nv_bfloat16* plane, int cpad, cudaStream_t s);
+const char* launch_featurize_ref(const float* y, const PlaneGeom& geo, int N, const PilotTablesDev& pt, float* feat,
+                                 cudaStream_t s);
+const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_bfloat16* plane, int cpad,
+                              cudaStream_t s);
+
+// ---------------------------------------------------------------------------------------------
+// Pointwise programs over bf16 planes (fusion nodes, the CoNet interaction and the LLR head).
+// A program is a linear chain evaluated per row on an 8-channel accumulator slice:
+//   LOAD k: acc = plane[k];  MUL k: acc *= plane[k];  ADD k: acc += plane[k];
+//   AFF k: acc = acc*s[k] + t[k] (eval BN);  RELU: acc = max(acc, 0)
+// and the result is either stored to a bf16 plane or fed to a 1x1 head GEMV
+// (llr[b,t,f,:] = acc . W + bias, fp32, reference layout [B,T,F,bits]).  build_conet's fusion tail
+// (network.hpp:534-553: mul -> norm -> mul -> norm ... -> main.out) is exactly such a chain.
+// ---------------------------------------------------------------------------------------------
+enum PwOp : int32_t { PW_LOAD = 0, PW_AFF = 1, PW_RELU = 2, PW_ADD = 3, PW_MUL = 4 };
+constexpr int kPwMaxIns = 24, kPwMaxPlanes = 8, kPwMaxAff = 8, kPwMaxBits = 16;
+
+struct PwIns {
+  int32_t op, k;
+};
+
+struct PwProgram {
+  int32_t n_ins;
+  int32_t C;                // channels of every operand (multiple of 8)
+  int32_t head_bits;        // 0: store plane; >0: head GEMV with this many outputs
+  int32_t pad_;
+  PwIns ins[kPwMaxIns];
+  const __nv_bfloat16* planes[kPwMaxPlanes];
+  const float* aff_s[kPwMaxAff];
+  const float* aff_t[kPwMaxAff];
+  __nv_bfloat16* out_plane; // [Nalloc][C]
+  const float* head_w;      // [C][head_bits] (reference layout of a 1x1 conv weight)
+  const float* head_b;      // [head_bits]
+  float* llr;               // [B,T,F,head_bits]
+};
+
+const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s);
+
+// ---------------------------------------------------------------------------------------------
+// Generic fp32 node kernels in the reference layout [B,T,F,C] (CNRX_FP32 plans).
+// ---------------------------------------------------------------------------------------------
+struct ConvF32 {
+  const float* x;       // [B,T,F,cin]
+  const float* w;       // [kh,kw,cin,cout]
+  const float* bias;    // [cout] or null
+  float* y;             // [B,T,F,cout]
+  int32_t B, T, F, cin, cout, kh, kw, dil_f;
+  // fused epilogue, applied in node order: y = conv+bias; [y = y*s+t]; [relu]; [y = y (op) other]
+  const float* aff_s;
+  const float* aff_t;
+  int32_t relu;
+  int32_t other_op;     // 0 none, 6 add, 7 mul (LayerOp values)
+  const float* other;
+};
+const char* launch_conv_f32(const ConvF32& p, cudaStream_t s);
+
+const char* launch_dwconv_f32(const float* x, const float* w, const float* bias, float* y, int B, int T, int F,
+                              int C, int kh, int kw, cudaStream_t s);
+// y = x*s + t per channel (eval BN, pre-folded exactly like norms.hpp:81-95), optional relu
+const char* launch_affine_f32(const float* x, const float* s_, const float* t_, int relu, float* y, int64_t rows,
+                              int C, cudaStream_t s);
+const char* launch_relu_f32(const float* x, float* y, int64_t n, cudaStream_t s);
+const char* launch_binary_f32(int op, const float* a, const float* b, float* y, int64_t n, cudaStream_t s);
+const char* launch_layernorm_f32(const float* x, const float* g, const float* b, float* y, int64_t rows, int C,
+                                 double eps, cudaStream_t s);
+const char* launch_concat_f32(const float* a, int ca, const float* b, int cb, float* y, int64_t rows, cudaStream_t s);
+
+}  // namespace cnrx

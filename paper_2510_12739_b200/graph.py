@@ -535,15 +535,16 @@ CONFIGS = {
                             snr_db=(0.0, 20.0)),
                    64, "fp32", "CoNet-small: 2 plain-CNN subnets x 4 conv3x3 @32, mul, 1x1 head -> 2 LLRs"),
     "cfg2": Config("cfg2", lambda: _conet_cfg(64, 2, 4, 12, 4),
-                   LinkSpec(T=14, F=612, N=2, mod_order=16, n_taps=12, rms_delay_s=300e-9, doppler_max_hz=200.0,
-                            snr_db=(0.0, 25.0)),
+                   LinkSpec(T=14, F=612, N=2, mod_order=16, n_taps=12, rms_delay_s=300e-9, tap_spacing_s=100e-9,
+                            doppler_max_hz=200.0, snr_db=(0.0, 25.0)),
                    256, "bf16", "CoNet-ResNet: 3 MRB subnets x 4 blocks @64, mul+BN fusion, 1x1 head -> 4 LLRs"),
     "cfg3": Config("cfg3", lambda: _conet_cfg(96, 3, 6, 24, 6, dil_subnets=(2, 3)),
-                   LinkSpec(T=14, F=3276, N=4, mod_order=64, n_taps=23, rms_delay_s=1e-6, doppler_max_hz=500.0,
+                   LinkSpec(T=14, F=3276, N=4, mod_order=64, n_taps=23, rms_delay_s=1e-6, tap_spacing_s=200e-9,
+                            doppler_max_hz=500.0,
                             snr_db=(0.0, 25.0), sir_db=(0.0, 15.0)),
                    64, "bf16", "CoNet-ResNet-large: 4 subnets x 6 MRB @96 (sup1, sup2 dilated x2 in F), 6 LLRs"),
     "cfg4": Config("cfg4", lambda: _resnet_cfg(96, 8, 12, 4),
-                   LinkSpec(T=14, F=612, N=2, mod_order=16, n_taps=12, rms_delay_s=300e-9, doppler_max_hz=200.0,
-                            snr_db=(0.0, 25.0)),
+                   LinkSpec(T=14, F=612, N=2, mod_order=16, n_taps=12, rms_delay_s=300e-9, tap_spacing_s=100e-9,
+                            doppler_max_hz=200.0, snr_db=(0.0, 25.0)),
                    256, "bf16", "plain ResNet (DeepRx-style RB x 8 @96), same inputs as cfg2"),
 }

@@ -1,0 +1,278 @@
+"""ctypes binding of the C ABI (include/conetrx_cuda.h) — the Python mirror of the reference-facing
+boundary.  `Plan(graph, precision)` compiles a network exactly as the reference describes it
+(GraphNode list, named params, BN-ready flags; network.hpp:19-33) and `Plan.forward(x)` is the drop-in
+for `Network<float>::forward(x, NormMode::eval)` (network.hpp:162): same input layout [B,T,F,C]
+fp32, same output [B,T,F,bits] fp32, same error behaviour (ValueError <- std::invalid_argument,
+RuntimeError <- std::runtime_error).
+
+There is no CPU fallback: if libconetrx_cuda.so is missing or no CUDA device is present, creating a
+plan raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from . import graph as G
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libconetrx_cuda.so")
+
+OK, ERR_INVALID_ARGUMENT, ERR_NOT_READY, ERR_UNSUPPORTED, ERR_CUDA = range(5)
+FP32, BF16 = 0, 1
+MODE_TRAIN, MODE_EVAL = 0, 1
+
+
+class CnrxError(RuntimeError):
+    """Base class; subclasses mirror the reference's exception types."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class CnrxInvalidArgument(CnrxError, ValueError):
+    pass
+
+
+class CnrxNotReady(CnrxError):
+    pass
+
+
+class CnrxUnsupported(CnrxError):
+    pass
+
+
+class CnrxCudaError(CnrxError):
+    pass
+
+
+_ERRS = {ERR_INVALID_ARGUMENT: CnrxInvalidArgument, ERR_NOT_READY: CnrxNotReady,
+         ERR_UNSUPPORTED: CnrxUnsupported, ERR_CUDA: CnrxCudaError}
+
+
+class cnrx_node(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in
+                ("op", "in0", "in1", "w", "b", "gamma", "beta", "rmean", "rvar", "bn_flag", "out_channels",
+                 "dilation_f")]
+
+
+class cnrx_param(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("rank", C.c_int32), ("learnable", C.c_int32), ("dims", C.c_int64 * 4),
+                ("data", C.POINTER(C.c_float))]
+
+
+class cnrx_plan_info(C.Structure):
+    _fields_ = [("precision", C.c_int32), ("device", C.c_int32), ("n_launches", C.c_int32),
+                ("n_tc_convs", C.c_int32), ("input_channels", C.c_int32), ("output_channels", C.c_int32),
+                ("macs_per_re", C.c_int64), ("rows_per_slot", C.c_int64), ("workspace_bytes", C.c_int64)]
+
+
+_lib = None
+
+EXPORTED = ["cnrx_plan_create", "cnrx_plan_destroy", "cnrx_last_error", "cnrx_forward", "cnrx_forward_device",
+            "cnrx_set_pilots", "cnrx_receive", "cnrx_receive_device", "cnrx_featurize_device",
+            "cnrx_receive_sharded", "cnrx_get_plan_info", "cnrx_set_graph_capture", "cnrx_launch_name",
+            "cnrx_set_profiling", "cnrx_read_profile", "cnrx_launch_flops"]
+
+
+def lib():
+    """Load libconetrx_cuda.so (build it first with paper_2510_12739_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2510_12739_b200.build` "
+                           "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, f32p, i64 = C.c_void_p, C.POINTER(C.c_float), C.c_int64
+    L.cnrx_plan_create.restype = C.c_int
+    L.cnrx_plan_create.argtypes = [C.POINTER(cnrx_node), C.c_int32, C.c_int32, C.c_int32, C.POINTER(cnrx_param),
+                                   C.c_int32, C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32,
+                                   C.POINTER(vp)]
+    L.cnrx_plan_destroy.argtypes = [vp]
+    L.cnrx_plan_destroy.restype = None
+    L.cnrx_last_error.restype = C.c_char_p
+    L.cnrx_forward.argtypes = [vp, f32p, i64, i64, i64, i64, C.c_int32, f32p]
+    L.cnrx_forward_device.argtypes = [vp, vp, i64, i64, i64, i64, C.c_int32, vp, vp]
+    L.cnrx_set_pilots.argtypes = [vp, i64, i64, f32p, C.POINTER(C.c_uint8)]
+    L.cnrx_receive.argtypes = [vp, f32p, i64, i64, i64, i64, f32p]
+    L.cnrx_receive_device.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp]
+    L.cnrx_featurize_device.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp]
+    L.cnrx_receive_sharded.argtypes = [C.POINTER(vp), C.c_int32, f32p, i64, i64, i64, i64, f32p]
+    L.cnrx_get_plan_info.argtypes = [vp, C.POINTER(cnrx_plan_info)]
+    L.cnrx_set_graph_capture.argtypes = [vp, C.c_int32]
+    L.cnrx_launch_name.restype = C.c_char_p
+    L.cnrx_launch_name.argtypes = [vp, C.c_int32]
+    L.cnrx_set_profiling.argtypes = [vp, C.c_int32]
+    L.cnrx_launch_flops.argtypes = [vp, C.c_int32]
+    L.cnrx_read_profile.argtypes = [vp, C.c_int32, C.POINTER(C.c_float), C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_int32)]
+    for fn in EXPORTED:
+        if fn not in ("cnrx_plan_destroy", "cnrx_last_error", "cnrx_launch_name"):
+            getattr(L, fn).restype = C.c_int
+    L.cnrx_launch_flops.restype = C.c_int64
+    _lib = L
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc != OK:
+        msg = lib().cnrx_last_error().decode()
+        raise _ERRS.get(rc, CnrxError)(rc, msg)
+
+
+def _f32p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _stream(stream: Optional[int]) -> C.c_void_p:
+    """None -> the plan's own stream (NULL at the ABI); 0 (torch's legacy default stream handle) ->
+    cudaStreamLegacy ((cudaStream_t)1); anything else is a cudaStream_t handle."""
+    if stream is None:
+        return C.c_void_p(0)
+    return C.c_void_p(1 if stream == 0 else stream)
+
+
+class Plan:
+    """A compiled CoNet-Rx network on one GPU."""
+
+    def __init__(self, g: "G.Graph", precision: str = "bf16", device: int = 0):
+        L = lib()
+        self.graph = g
+        self.precision = precision
+        self.device = device
+        nodes = (cnrx_node * len(g.nodes))(*[cnrx_node(*n.as_row()) for n in g.nodes])
+        self._keep = [np.ascontiguousarray(p.value, np.float32) for p in g.params]
+        self._names = [p.name.encode() for p in g.params]
+        params = (cnrx_param * max(1, len(g.params)))()
+        for i, (p, v) in enumerate(zip(g.params, self._keep)):
+            params[i].name = self._names[i]
+            params[i].rank = v.ndim
+            params[i].learnable = int(p.learnable)
+            for d in range(v.ndim):
+                params[i].dims[d] = v.shape[d]
+            params[i].data = _f32p(v)
+        ready = np.asarray(g.bn_ready if g.bn_ready else [0], np.uint8)
+        h = C.c_void_p()
+        prec = {"fp32": FP32, "bf16": BF16}[precision]
+        _check(L.cnrx_plan_create(nodes, len(g.nodes), g.input_node, g.output_node, params, len(g.params),
+                                  ready.ctypes.data_as(C.POINTER(C.c_uint8)), len(g.bn_ready), prec, device,
+                                  C.byref(h)))
+        self.h = h
+        self.out_channels = g.output_channels()
+        self.in_channels = g.in_channels
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            lib().cnrx_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- Network<float>::forward ------------------------------------------------------------
+    def forward(self, x: np.ndarray, mode: int = MODE_EVAL) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float32)
+        if x.ndim == 3:
+            x = x[None]
+        if x.ndim != 4:
+            raise CnrxInvalidArgument(ERR_INVALID_ARGUMENT,
+                                      f"activation tensor must be [T,F,C] or [B,T,F,C], got {list(x.shape)}")
+        B, T, F, Cc = x.shape
+        out = np.empty((B, T, F, self.out_channels), np.float32)
+        _check(lib().cnrx_forward(self.h, _f32p(x), B, T, F, Cc, mode, _f32p(out)))
+        return out
+
+    def forward_device(self, x, out, stream: Optional[int] = None, mode: int = MODE_EVAL) -> None:
+        """x, out: torch CUDA tensors (fp32, contiguous)."""
+        B, T, F, Cc = x.shape
+        _check(lib().cnrx_forward_device(self.h, C.c_void_p(x.data_ptr()), B, T, F, Cc, mode,
+                                         C.c_void_p(out.data_ptr()), _stream(stream)))
+
+    # ---- receiver path (featurize -> subnets -> fusion -> head) --------------------------------
+    def set_pilots(self, pilots: np.ndarray, mask: np.ndarray) -> None:
+        p = np.ascontiguousarray(pilots, np.complex64)
+        m = np.ascontiguousarray(mask, np.uint8)
+        T, F = m.shape
+        _check(lib().cnrx_set_pilots(self.h, T, F, p.view(np.float32).ctypes.data_as(C.POINTER(C.c_float)),
+                                     m.ctypes.data_as(C.POINTER(C.c_uint8))))
+
+    def receive(self, y: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """y: complex64 [B,T,F,N] host array -> LLRs fp32 [B,T,F,bits] (host, synchronous)."""
+        y = np.ascontiguousarray(y, np.complex64)
+        B, T, F, N = y.shape
+        if out is None:
+            out = np.empty((B, T, F, self.out_channels), np.float32)
+        _check(lib().cnrx_receive(self.h, y.view(np.float32).ctypes.data_as(C.POINTER(C.c_float)), B, T, F, N,
+                                  _f32p(out)))
+        return out
+
+    def receive_host_ptr(self, y_ptr: int, shape, out_ptr: int) -> None:
+        """Host-pointer variant (e.g. pinned torch tensors): y complex64 [B,T,F,N], out fp32."""
+        B, T, F, N = shape
+        _check(lib().cnrx_receive(self.h, C.cast(C.c_void_p(y_ptr), C.POINTER(C.c_float)), B, T, F, N,
+                                  C.cast(C.c_void_p(out_ptr), C.POINTER(C.c_float))))
+
+    def receive_device(self, y, out, stream: Optional[int] = None) -> None:
+        """y: torch complex64 CUDA tensor [B,T,F,N] (or float32 [...,2]); out: fp32 CUDA tensor."""
+        B, T, F, N = y.shape[:4]
+        _check(lib().cnrx_receive_device(self.h, C.c_void_p(y.data_ptr()), B, T, F, N,
+                                         C.c_void_p(out.data_ptr()), _stream(stream)))
+
+    def featurize_device(self, y, feat, stream: Optional[int] = None) -> None:
+        B, T, F, N = y.shape[:4]
+        _check(lib().cnrx_featurize_device(self.h, C.c_void_p(y.data_ptr()), B, T, F, N,
+                                           C.c_void_p(feat.data_ptr()), _stream(stream)))
+
+    # ---- introspection ----------------------------------------------------------------------------
+    def info(self) -> dict:
+        inf = cnrx_plan_info()
+        _check(lib().cnrx_get_plan_info(self.h, C.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in cnrx_plan_info._fields_}
+
+    def launch_names(self):
+        names, i = [], 0
+        while True:
+            n = lib().cnrx_launch_name(self.h, i)
+            if n is None:
+                return names
+            names.append(n.decode())
+            i += 1
+
+    def launch_flops_per_re(self):
+        return [int(lib().cnrx_launch_flops(self.h, i)) for i in range(len(self.launch_names()))]
+
+    def set_profiling(self, enable: bool) -> None:
+        _check(lib().cnrx_set_profiling(self.h, int(enable)))
+
+    def read_profile(self, max_n: int = 4096):
+        """[(kernel name, total ms, calls)] per launch position since the last read (single call: the
+        library clears its accumulators on every read)."""
+        n = C.c_int32()
+        ms = (C.c_float * max_n)()
+        cnt = (C.c_int32 * max_n)()
+        _check(lib().cnrx_read_profile(self.h, max_n, ms, cnt, C.byref(n)))
+        names = self.launch_names()
+        k = min(n.value, max_n)
+        return [(names[i] if i < len(names) else f"launch{i}", float(ms[i]), int(cnt[i])) for i in range(k)]
+
+    def set_graph_capture(self, enable: bool) -> None:
+        _check(lib().cnrx_set_graph_capture(self.h, int(enable)))
+
+
+def receive_sharded(plans, y: np.ndarray) -> np.ndarray:
+    """cnrx_receive_sharded: contiguous slot ranges over several single-GPU plans (one process)."""
+    y = np.ascontiguousarray(y, np.complex64)
+    B, T, F, N = y.shape
+    out = np.empty((B, T, F, plans[0].out_channels), np.float32)
+    arr = (C.c_void_p * len(plans))(*[p.h for p in plans])
+    _check(lib().cnrx_receive_sharded(arr, len(plans), y.view(np.float32).ctypes.data_as(C.POINTER(C.c_float)),
+                                      B, T, F, N, _f32p(out)))
+    return out

@@ -1,0 +1,133 @@
+"""Test helper: CPU (torch fp32) emulation of the CNRX_BF16 plan's arithmetic.
+
+The bf16 tensor-core plan rounds values to bf16 exactly where it stores activation planes (input
+features, every conv epilogue output, pre-activated copies, pointwise-program outputs) and folds an
+eval BN that follows a conv into bf16(W * scale) and bias*scale + shift.  This emulator applies the
+same rounding points with fp32 accumulation, so the GPU result can be checked tightly against it
+(deviation only from accumulation order), independent of how well bf16 tracks the fp32 reference.
+It mirrors the absorption rules of Bf16Compiler in paper_2510_12739_b200/csrc/api.cpp.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.nn.functional as Fn
+
+from paper_2510_12739_b200 import graph as G
+
+
+def bf16(t: torch.Tensor) -> torch.Tensor:
+    return t.to(torch.bfloat16).to(torch.float32)
+
+
+def bn_affine(g, n):
+    gamma, beta = g.params[n.gamma].value, g.params[n.beta].value
+    rm, rv = g.params[n.rmean].value, g.params[n.rvar].value
+    istd = (1.0 / np.sqrt(rv.astype(np.float64) + 1e-5)).astype(np.float32)
+    scale = (gamma * istd).astype(np.float32)
+    shift = (beta - rm * scale).astype(np.float32)
+    return torch.from_numpy(scale), torch.from_numpy(shift)
+
+
+def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
+    """x: [B,T,F,C] fp32 features -> LLRs [B,T,F,bits] as the bf16 plan computes them."""
+    nodes = g.nodes
+    consumers = [[] for _ in nodes]
+    for i, n in enumerate(nodes):
+        if n.in0 >= 0:
+            consumers[n.in0].append(i)
+        if n.in1 >= 0:
+            consumers[n.in1].append(i)
+    single = lambda i: consumers[i][0] if len(consumers[i]) == 1 else -1
+    planes, vals, nonneg, producer_relu = {}, {}, {}, {}
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float32)).permute(0, 3, 1, 2)  # [B,C,T,F]
+    planes[g.input_node] = bf16(xt)
+
+    def chain(u):
+        if u in planes:
+            return planes[u]
+        n = nodes[u]
+        if n.op == G.OP_RELU:
+            return torch.relu(chain(n.in0))
+        if n.op == G.OP_BN:
+            s, t = bn_affine(g, n)
+            return chain(n.in0) * s[None, :, None, None] + t[None, :, None, None]
+        if n.op in (G.OP_ADD, G.OP_MUL):
+            if n.in1 in planes:
+                leaf, rest = n.in1, n.in0
+            elif n.in0 in planes:
+                leaf, rest = n.in0, n.in1
+            else:
+                raise ValueError("not a linear chain")
+            r = chain(rest)
+            return r * planes[leaf] if n.op == G.OP_MUL else r + planes[leaf]
+        raise ValueError(f"op {n.op} not emulated")
+
+    def plane_for(u):
+        if u in planes:
+            return planes[u]
+        n = nodes[u]
+        if n.op == G.OP_RELU:
+            v, bn = n.in0, None
+            if v not in planes and nodes[v].op == G.OP_BN and nodes[v].in0 in planes:
+                bn, v = nodes[v], nodes[v].in0
+            if v in planes:
+                if bn is None and nonneg.get(v, False):
+                    planes[u] = planes[v]
+                    return planes[u]
+                if v in vals:
+                    z = vals[v]
+                    if bn is not None:
+                        s, t = bn_affine(g, bn)
+                        z = z * s[None, :, None, None] + t[None, :, None, None]
+                    planes[u] = bf16(torch.relu(z))
+                    return planes[u]
+        planes[u] = bf16(chain(u))
+        return planes[u]
+
+    absorbed = set()
+    for i, n in enumerate(nodes):
+        if n.op != G.OP_CONV or i in absorbed or i == g.output_node:
+            continue
+        inp = plane_for(n.in0)
+        w = torch.from_numpy(g.params[n.w].value)  # [kh,kw,cin,cout]
+        cout = w.shape[3]
+        bias = torch.from_numpy(g.params[n.b].value.copy()) if n.b >= 0 else torch.zeros(cout)
+        scale = None
+        end, relu, res = i, False, None
+        c = single(end)
+        if c >= 0 and nodes[c].op == G.OP_BN and c != g.output_node:
+            scale, shift = bn_affine(g, nodes[c])
+            bias = bias * scale + shift
+            absorbed.add(c)
+            end, c = c, single(c)
+        if c >= 0 and nodes[c].op == G.OP_RELU:
+            relu = True
+            absorbed.add(c)
+            end, c = c, single(c)
+        if not relu and c >= 0 and nodes[c].op == G.OP_ADD:
+            other = nodes[c].in1 if nodes[c].in0 == end else nodes[c].in0
+            if other != end and other < i:
+                res = plane_for(other)
+                absorbed.add(c)
+                end = c
+        wf = w * scale[None, None, None, :] if scale is not None else w
+        wk = bf16(wf.permute(3, 2, 0, 1).contiguous())  # [cout,cin,kh,kw]
+        kh, kw = w.shape[0], w.shape[1]
+        cin_plane = inp.shape[1]
+        if cin_plane > wk.shape[1]:  # zero-padded input channels
+            wk = torch.cat([wk, torch.zeros(cout, cin_plane - wk.shape[1], kh, kw)], 1)
+        v = Fn.conv2d(inp, wk, bias=bias, padding=(kh // 2, (kw // 2) * n.dilation_f), dilation=(1, n.dilation_f))
+        if relu:
+            v = torch.relu(v)
+        if res is not None:
+            v = v + res
+        vals[end] = v
+        planes[end] = bf16(v)
+        nonneg[end] = relu
+    on = nodes[g.output_node]
+    f = chain(on.in0)
+    hw = torch.from_numpy(g.params[on.w].value[0, 0])  # [C,bits]
+    hb = torch.from_numpy(g.params[on.b].value) if on.b >= 0 else torch.zeros(hw.shape[1])
+    out = torch.einsum("bctf,cj->btfj", f, hw) + hb
+    return out.numpy()
