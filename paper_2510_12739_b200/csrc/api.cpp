@@ -30,6 +30,7 @@
 #include "../../include/conetrx_cuda.h"
 #include "common.h"
 #include "conv_tc.h"
+#include "conv_ws.h"
 #include "kernels.h"
 
 using namespace cnrx;
@@ -127,6 +128,9 @@ struct TcOp {
   int node = -1;
   int cin = 0, cout = 0, ks = 1, dil = 1;
   int cin_real = 0, cout_real = 0;
+  bool ws = false;  // weights-stationary (A in TMEM) 64->64 3x3 kernel
+  bool stem = false;             // 1x1 conv on the network input, run by the fused stem kernel
+  float* stem_w = nullptr;       // fp32 [cin_real][cout_real], BN scale folded
   int in_plane = -1, res_plane = -1, out_plane = -1, out2_plane = -1;
   int relu = 0;
   void* wimg = nullptr;
@@ -154,7 +158,12 @@ struct Workspace {
   size_t out_bytes = 0;
   void* feat_buf = nullptr; // fp32 features when an FP32 plan runs the receive path
   size_t feat_bytes = 0;
-  std::vector<TcLaunch> launches;   // prepared tensor maps per TC group (bf16)
+  struct GroupLaunch {
+    bool ws = false;
+    TcLaunch tc;
+    WsLaunch wsl;
+  };
+  std::vector<GroupLaunch> launches;  // prepared tensor maps per TC group (bf16)
 };
 
 }  // namespace
@@ -189,6 +198,8 @@ struct cnrx_plan {
   std::vector<std::vector<int>> pw_by_level;
   int n_levels = 0;
   int npad = 1;
+  std::vector<int> stem_ops;   // TcOp indices run by the fused stem kernel
+  bool need_plane0 = true;     // some kernel reads the input-feature plane
   std::vector<int> buf_channels;  // plane buffers
 
   // pilots
@@ -551,6 +562,7 @@ struct Bf16Compiler {
 
   void finish_pw(PwStep& st, std::vector<std::vector<float>>& aff_tables, int C) {
     st.prog.C = C;
+    st.prog.n_planes_used = st.n_planes;
     for (size_t k = 0; k < aff_tables.size() / 2; ++k) {
       auto s = aff_tables[2 * k], t = aff_tables[2 * k + 1];
       s.resize(static_cast<size_t>(C), 0.f);
@@ -681,11 +693,28 @@ struct Bf16Compiler {
       use(op.in_plane, op.level);
       if (op.res_plane >= 0) use(op.res_plane, op.level);
       // weights (BN scale folded per output channel) and bias
-      std::vector<uint8_t> img(conv_tc_wimg_bytes(op.cin, op.cout, op.ks));
-      conv_tc_pack_weights(w.data.data(), op.ks, static_cast<int>(w.dims[2]), static_cast<int>(w.dims[3]),
-                           scale.empty() ? nullptr : scale.data(), op.cin, op.cout, img.data());
-      op.wimg = p.upload_bytes(img.data(), img.size());
+      static const bool no_ws = getenv("CNRX_NO_WS") != nullptr;
+      op.ws = !no_ws && op.ks == 3 && op.cin_real == 64 && op.cout_real == 64 && op.cin == 64 && op.cout == 64;
+      if (op.ws) {
+        std::vector<uint32_t> img(conv_ws64_wimg_bytes() / 4);
+        conv_ws64_pack_weights(w.data.data(), scale.empty() ? nullptr : scale.data(), img.data());
+        op.wimg = p.upload_bytes(img.data(), img.size() * 4);
+      } else {
+        std::vector<uint8_t> img(conv_tc_wimg_bytes(op.cin, op.cout, op.ks));
+        conv_tc_pack_weights(w.data.data(), op.ks, static_cast<int>(w.dims[2]), static_cast<int>(w.dims[3]),
+                             scale.empty() ? nullptr : scale.data(), op.cin, op.cout, img.data());
+        op.wimg = p.upload_bytes(img.data(), img.size());
+      }
       op.bias = p.upload(bias);
+      if (op.in_plane == 0 && op.ks == 1 && op.res_plane < 0 && stem_supported_cin(op.cin_real) &&
+          op.cout_real % 8 == 0 && op.cout_real <= 64 && op.cout == op.cout_real) {
+        std::vector<float> wf(static_cast<size_t>(op.cin_real) * op.cout_real);
+        for (int ci = 0; ci < op.cin_real; ++ci)
+          for (int co = 0; co < op.cout_real; ++co)
+            wf[static_cast<size_t>(ci) * op.cout_real + co] =
+                w.data[static_cast<size_t>(ci) * op.cout_real + co] * (scale.empty() ? 1.f : scale[static_cast<size_t>(co)]);
+        op.stem_w = p.upload(wf);
+      }
       op.out_plane = new_plane(op.cout, op.level, op.relu != 0);
       p.tc.push_back(op);
       plane_producer_tc[static_cast<size_t>(op.out_plane)] = static_cast<int>(p.tc.size()) - 1;
@@ -725,13 +754,32 @@ struct Bf16Compiler {
     p.n_levels = maxl + 1;
     p.tc_groups_by_level.assign(static_cast<size_t>(p.n_levels), {});
     p.pw_by_level.assign(static_cast<size_t>(p.n_levels), {});
+    // The CUDA-core fused featurize+stem kernel is opt-in (CNRX_STEM=1): measured slower than
+    // featurize + the tensor-core 1x1 conv at cfg2 sizes (profiles/r01_notes.md).
+    static const bool no_stem = getenv("CNRX_STEM") == nullptr;
+    for (int k = 0; k < static_cast<int>(p.tc.size()); ++k) {
+      TcOp& op = p.tc[static_cast<size_t>(k)];
+      if (!no_stem && op.stem_w && static_cast<int>(p.stem_ops.size()) < kStemMaxOps &&
+          (p.stem_ops.empty() || p.tc[static_cast<size_t>(p.stem_ops[0])].cin_real == op.cin_real)) {
+        op.stem = true;
+        p.stem_ops.push_back(k);
+      }
+    }
+    p.need_plane0 = false;
+    for (const auto& op : p.tc)
+      if (!op.stem && (op.in_plane == 0 || op.res_plane == 0)) p.need_plane0 = true;
+    for (const auto& st2 : p.pw)
+      for (int k = 0; k < st2.n_planes; ++k)
+        if (st2.plane_ids[k] == 0) p.need_plane0 = true;
     for (int k = 0; k < static_cast<int>(p.tc.size()); ++k) {
       const TcOp& op = p.tc[static_cast<size_t>(k)];
+      if (op.stem) continue;
       auto& groups = p.tc_groups_by_level[static_cast<size_t>(op.level)];
       bool placed = false;
       for (auto& g : groups) {
         const TcOp& o0 = p.tc[static_cast<size_t>(g[0])];
-        if (static_cast<int>(g.size()) < kTcMaxGroups && o0.cin == op.cin && o0.cout == op.cout && o0.ks == op.ks) {
+        if (static_cast<int>(g.size()) < kTcMaxGroups && o0.cin == op.cin && o0.cout == op.cout && o0.ks == op.ks &&
+            o0.ws == op.ws) {
           g.push_back(k);
           placed = true;
           break;
@@ -808,42 +856,76 @@ void ensure_workspace(cnrx_plan& p, int B, int T, int F) {
     ws.buffers.push_back(d);
   }
   // tensor maps / launch descriptors per TC group
+  auto plane_ptr = [&](int pl) -> __nv_bfloat16* {
+    return pl < 0 ? nullptr
+                  : static_cast<__nv_bfloat16*>(ws.buffers[static_cast<size_t>(p.planes[static_cast<size_t>(pl)].buffer)]);
+  };
   for (int lv = 0; lv < p.n_levels; ++lv)
     for (auto& grp : p.tc_groups_by_level[static_cast<size_t>(lv)]) {
-      TcLaunch L;
-      std::memset(&L, 0, sizeof(L));
-      L.geo = ws.geo;
-      L.ngroups = static_cast<int>(grp.size());
-      int win_alloc = 0;
-      for (size_t gi = 0; gi < grp.size(); ++gi) {
-        const TcOp& op = p.tc[static_cast<size_t>(grp[gi])];
-        TcGroup& g = L.g[gi];
-        auto plane_ptr = [&](int pl) -> __nv_bfloat16* {
-          return pl < 0 ? nullptr
-                        : static_cast<__nv_bfloat16*>(ws.buffers[static_cast<size_t>(p.planes[static_cast<size_t>(pl)].buffer)]);
-        };
-        g.halo = op.ks == 1 ? 0 : ws.geo.T1 * op.dil + 1;
-        g.dil = op.dil;
-        const int rows = 128 + 2 * g.halo;
-        win_alloc = std::max(win_alloc, (rows + 31) / 32 * 32);
-        conv_tc_make_maps(plane_ptr(op.in_plane), ws.geo.Nalloc, op.cin, 32, g.map);
-        g.wimg = static_cast<const uint8_t*>(op.wimg);
-        g.bias = op.bias;
-        g.res = plane_ptr(op.res_plane);
-        g.out = plane_ptr(op.out_plane);
-        g.out2 = plane_ptr(op.out2_plane);
-        g.s2 = op.s2;
-        g.t2 = op.t2;
-        g.relu = op.relu;
-      }
-      L.win_alloc = win_alloc;
+      Workspace::GroupLaunch GL;
       const TcOp& op0 = p.tc[static_cast<size_t>(grp[0])];
-      int stages = 4;
-      while (stages > 1 && conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc) > 227 * 1024) --stages;
-      if (conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc) > 227 * 1024)
-        throw Error(CNRX_ERR_UNSUPPORTED, "tcgen05 conv working set exceeds shared memory");
-      L.stages = stages;
-      ws.launches.push_back(L);
+      GL.ws = op0.ws;
+      if (op0.ws) {
+        WsLaunch& L = GL.wsl;
+        std::memset(&L, 0, sizeof(L));
+        L.geo = ws.geo;
+        L.ngroups = static_cast<int>(grp.size());
+        L.n_tiles = conv_ws64_tiles(ws.geo.Nalloc);
+        int win_alloc = 0;
+        for (size_t gi = 0; gi < grp.size(); ++gi) {
+          const TcOp& op = p.tc[static_cast<size_t>(grp[gi])];
+          WsGroup& g = L.g[gi];
+          g.halo = ws.geo.T1 * op.dil + 1;
+          g.dil = op.dil;
+          win_alloc = std::max(win_alloc, conv_ws64_win_alloc(g.halo));
+          conv_ws64_make_maps(plane_ptr(op.in_plane), plane_ptr(op.res_plane), plane_ptr(op.out_plane),
+                              plane_ptr(op.out2_plane), ws.geo.Nalloc, &g);
+          g.wimg = static_cast<const uint32_t*>(op.wimg);
+          g.bias = op.bias;
+          g.s2 = op.s2;
+          g.t2 = op.t2;
+          g.relu = op.relu;
+        }
+        L.win_alloc = win_alloc;
+        int stages = 4;
+        while (stages > 1 && conv_ws64_smem_bytes(stages, win_alloc) > 227 * 1024) --stages;
+        L.stages = stages;
+      } else {
+        TcLaunch& L = GL.tc;
+        std::memset(&L, 0, sizeof(L));
+        L.geo = ws.geo;
+        L.ngroups = static_cast<int>(grp.size());
+        int win_alloc = 0;
+        for (size_t gi = 0; gi < grp.size(); ++gi) {
+          const TcOp& op = p.tc[static_cast<size_t>(grp[gi])];
+          TcGroup& g = L.g[gi];
+          g.halo = op.ks == 1 ? 0 : ws.geo.T1 * op.dil + 1;
+          g.dil = op.dil;
+          const int rows = 128 + 2 * g.halo;
+          win_alloc = std::max(win_alloc, (rows + 31) / 32 * 32);
+          conv_tc_make_maps(plane_ptr(op.in_plane), ws.geo.Nalloc, op.cin, 32, g.map);
+          if (conv_tc_staged(op.cin, op.cout)) {
+            conv_tc_make_row_map(plane_ptr(op.res_plane), ws.geo.Nalloc, op.cout, &g.res_map);
+            conv_tc_make_row_map(plane_ptr(op.out_plane), ws.geo.Nalloc, op.cout, &g.out_map);
+            conv_tc_make_row_map(plane_ptr(op.out2_plane), ws.geo.Nalloc, op.cout, &g.out2_map);
+          }
+          g.wimg = static_cast<const uint8_t*>(op.wimg);
+          g.bias = op.bias;
+          g.res = plane_ptr(op.res_plane);
+          g.out = plane_ptr(op.out_plane);
+          g.out2 = plane_ptr(op.out2_plane);
+          g.s2 = op.s2;
+          g.t2 = op.t2;
+          g.relu = op.relu;
+        }
+        L.win_alloc = win_alloc;
+        int stages = 4;
+        while (stages > 1 && conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc) > 227 * 1024) --stages;
+        if (conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc) > 227 * 1024)
+          throw Error(CNRX_ERR_UNSUPPORTED, "tcgen05 conv working set exceeds shared memory");
+        L.stages = stages;
+      }
+      ws.launches.push_back(GL);
     }
 }
 
@@ -899,22 +981,92 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
   auto plane_ptr = [&](int pl) {
     return static_cast<__nv_bfloat16*>(ws.buffers[static_cast<size_t>(p.planes[static_cast<size_t>(pl)].buffer)]);
   };
-  __nv_bfloat16* in_plane = plane_ptr(0);
-  if (input_kind == 0)
-    p.note(launch_pack_plane(in, ws.geo, p.in_ch, in_plane, p.planes[0].C, s), s);
-  else
-    p.note(launch_featurize_plane(in, ws.geo, N, p.pt, in_plane, p.planes[0].C, s), s);
+  if (p.need_plane0) {
+    __nv_bfloat16* in_plane = plane_ptr(0);
+    if (input_kind == 0)
+      p.note(launch_pack_plane(in, ws.geo, p.in_ch, in_plane, p.planes[0].C, s), s);
+    else
+      p.note(launch_featurize_plane(in, ws.geo, N, p.pt, in_plane, p.planes[0].C, s), s);
+  }
+  if (!p.stem_ops.empty()) {
+    StemLaunch SL;
+    std::memset(&SL, 0, sizeof(SL));
+    SL.nops = static_cast<int>(p.stem_ops.size());
+    SL.cin = p.tc[static_cast<size_t>(p.stem_ops[0])].cin_real;
+    SL.N = N;
+    SL.mode = input_kind;
+    SL.x = input_kind == 0 ? in : nullptr;
+    SL.y = input_kind == 1 ? in : nullptr;
+    SL.pt = p.pt;
+    int64_t fl = 0;
+    for (int i = 0; i < SL.nops; ++i) {
+      const TcOp& op = p.tc[static_cast<size_t>(p.stem_ops[static_cast<size_t>(i)])];
+      StemOp& so = SL.op[i];
+      so.w = op.stem_w;
+      so.bias = op.bias;
+      so.out = plane_ptr(op.out_plane);
+      so.out2 = op.out2_plane >= 0 ? plane_ptr(op.out2_plane) : nullptr;
+      so.s2 = op.s2;
+      so.t2 = op.t2;
+      so.cout = op.cout_real;
+      so.relu = op.relu;
+      fl += 2ll * op.cin_real * op.cout_real;
+    }
+    p.note(launch_stem(SL, ws.geo, s), s, fl);
+  }
   size_t li = 0;
   for (int lv = 0; lv < p.n_levels; ++lv) {
     for (size_t gi = 0; gi < p.tc_groups_by_level[static_cast<size_t>(lv)].size(); ++gi) {
       const auto& grp = p.tc_groups_by_level[static_cast<size_t>(lv)][gi];
+      if (grp.empty()) continue;
       const TcOp& op0 = p.tc[static_cast<size_t>(grp[0])];
       int64_t fl = 0;
       for (int k : grp) {
         const TcOp& o = p.tc[static_cast<size_t>(k)];
         fl += 2ll * o.ks * o.ks * o.cin_real * o.cout_real;
       }
-      p.note(conv_tc_launch(op0.cin, op0.cout, op0.ks, ws.launches[li++], p.num_sms, s), s, fl);
+      Workspace::GroupLaunch& GL = ws.launches[li++];
+      static const bool trace = getenv("CNRX_TRACE") != nullptr;
+      static unsigned long long* dtrace = nullptr;
+      if (GL.ws) {
+        if (trace) {
+          if (!dtrace) CNRX_CUDA(cudaMalloc(&dtrace, 16 * sizeof(unsigned long long)));
+          CNRX_CUDA(cudaMemsetAsync(dtrace, 0, 16 * sizeof(unsigned long long), s));
+          GL.wsl.trace = dtrace;
+        }
+        p.note(conv_ws64_launch(GL.wsl, p.num_sms, s), s, fl);
+        if (trace) {
+          unsigned long long h[16];
+          CNRX_CUDA(cudaMemcpyAsync(h, dtrace, sizeof h, cudaMemcpyDeviceToHost, s));
+          CNRX_CUDA(cudaStreamSynchronize(s));
+          const double nt = static_cast<double>(h[kTraceTiles] ? h[kTraceTiles] : 1);
+          fprintf(stderr,
+                  "[trace] conv_ws64 tiles=%llu per-tile cycles: prod_wait %.0f mma_wait_full %.0f mma_wait_tmem %.0f "
+                  "mma_issue %.0f | epi_wait %.0f combine %.0f stage_wait %.0f write %.0f | total/tile %.0f\n",
+                  h[kTraceTiles], h[kTraceProdWaitEmpty] / nt, h[kTraceMmaWaitFull] / nt, h[kTraceMmaWaitTmem] / nt,
+                  h[kTraceMmaIssue] / nt, h[kTraceEpiWaitFull] / nt, h[kWsTraceCombine] / nt,
+                  h[kWsTraceStageWait] / nt, h[kWsTraceWrite] / nt, h[kTraceTotal] / nt);
+        }
+        continue;
+      }
+      if (trace) {
+        if (!dtrace) CNRX_CUDA(cudaMalloc(&dtrace, 16 * sizeof(unsigned long long)));
+        CNRX_CUDA(cudaMemsetAsync(dtrace, 0, kTraceN * sizeof(unsigned long long), s));
+        GL.tc.trace = dtrace;
+      }
+      p.note(conv_tc_launch(op0.cin, op0.cout, op0.ks, GL.tc, p.num_sms, s), s, fl);
+      if (trace) {
+        unsigned long long h[kTraceN];
+        CNRX_CUDA(cudaMemcpyAsync(h, dtrace, sizeof h, cudaMemcpyDeviceToHost, s));
+        CNRX_CUDA(cudaStreamSynchronize(s));
+        const double nct = static_cast<double>(h[kTraceTiles] ? h[kTraceTiles] : 1);
+        fprintf(stderr,
+                "[trace] %s tiles=%llu per-tile cycles: prod_wait_empty %.0f mma_wait_full %.0f mma_wait_tmem %.0f "
+                "mma_issue %.0f epi_wait %.0f epi_work %.0f | mma-thread total/tile %.0f\n",
+                p.launch_names.back().c_str(), h[kTraceTiles], h[kTraceProdWaitEmpty] / nct,
+                h[kTraceMmaWaitFull] / nct, h[kTraceMmaWaitTmem] / nct, h[kTraceMmaIssue] / nct,
+                h[kTraceEpiWaitFull] / nct, h[kTraceEpiWork] / nct, h[kTraceTotal] / nct);
+      }
     }
     for (int k : p.pw_by_level[static_cast<size_t>(lv)]) {
       PwStep& st = p.pw[static_cast<size_t>(k)];

@@ -52,8 +52,10 @@ __host__ __device__ inline uint32_t swz_offset(int rb, uint32_t r, uint32_t c) {
 }
 
 struct SmemLayout {
-  uint32_t w_off, win_off, win_stage_bytes, win_chunk1_off, bar_off, total;
+  uint32_t w_off, win_off, win_stage_bytes, win_chunk1_off;
+  uint32_t res_off, stg_off, par_off, bar_off, total;
 };
+__host__ __device__ constexpr bool staged_epi(int cin, int cout) { return cin <= 64 && cout <= 64; }
 __host__ __device__ inline SmemLayout smem_layout(int cin, int cout, int ks, int stages, int win_alloc) {
   SmemLayout s{};
   const uint32_t wbytes = static_cast<uint32_t>(ks * ks * cout * cin * 2);
@@ -63,7 +65,16 @@ __host__ __device__ inline SmemLayout smem_layout(int cin, int cout, int ks, int
   const uint32_t c1 = static_cast<uint32_t>(win_alloc * chunk1_ch(cin) * 2);
   s.win_chunk1_off = (c0 + 1023u) & ~1023u;
   s.win_stage_bytes = (s.win_chunk1_off + c1 + 1023u) & ~1023u;
-  s.bar_off = s.win_off + static_cast<uint32_t>(stages) * s.win_stage_bytes;
+  uint32_t off = s.win_off + static_cast<uint32_t>(stages) * s.win_stage_bytes;
+  if (staged_epi(cin, cout)) {
+    s.res_off = off;                                   // 2 x [128 rows][cout] residual tiles
+    off += 2u * 128u * static_cast<uint32_t>(cout) * 2u;
+    s.stg_off = off;                                   // 4 warps x 2 outputs x [32 rows][cout]
+    off += 4u * 2u * 32u * static_cast<uint32_t>(cout) * 2u;
+  }
+  s.par_off = off;                                     // bias, s2, t2 (fp32)
+  off += (3u * static_cast<uint32_t>(cout) * 4u + 15u) & ~15u;
+  s.bar_off = off;
   s.total = s.bar_off + 256 + 1024;  // barriers + alignment slack for the dynamic smem base
   return s;
 }
@@ -77,18 +88,25 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
   constexpr uint32_t WBYTES = TAPS * COUT * CIN * 2;
   constexpr uint32_t TMEM_COLS = tmem_cols_for(COUT);
   constexpr uint32_t IDESC = idesc_bf16_f32(128, COUT);
+  constexpr bool STAGED = staged_epi(CIN, COUT);
+  constexpr int ORB = COUT * 2;  // output row bytes (staged path: one swizzle chunk)
 
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   const SmemLayout lay = smem_layout(CIN, COUT, KS, L.stages, L.win_alloc);
   uint8_t* sW = smem + lay.w_off;
+  float* s_bias = reinterpret_cast<float*>(smem + lay.par_off);
+  float* s_s2 = s_bias + COUT;
+  float* s_t2 = s_s2 + COUT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.bar_off);
   uint64_t* w_full = bars;                  // [1]
   uint64_t* full = bars + 1;                // [stages]
   uint64_t* empty = full + L.stages;        // [stages]
   uint64_t* tfull = empty + L.stages;       // [2]
   uint64_t* tempty = tfull + 2;             // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;             // [2] residual tile landed
+  uint64_t* rempty = rfull + 2;             // [2] residual tile consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -98,6 +116,7 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
   const int nct = (static_cast<int>(gridDim.x) - g + G - 1) / G;
   const TcGroup& grp = L.g[g];
   const int64_t n_tiles = L.geo.n_tiles;
+  const bool has_res = grp.res != nullptr;
 
   if (threadIdx.x == 0) {
     mbar_init(w_full, 1);
@@ -108,8 +127,17 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
+      mbar_init(&rfull[a], 1);
+      mbar_init(&rempty[a], 4);
     }
     fence_barrier_init();
+  }
+  if (warp >= 2) {  // epilogue parameters to shared memory
+    for (int c = threadIdx.x - 64; c < COUT; c += 128) {
+      s_bias[c] = grp.bias[c];
+      s_s2[c] = grp.s2 ? grp.s2[c] : 1.f;
+      s_t2[c] = grp.t2 ? grp.t2[c] : 0.f;
+    }
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
@@ -120,6 +148,7 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------
     if (lane == 0) {
+      long long tr_prod = 0;
       prefetch_tmap(&grp.map[0]);
       if (CH1) prefetch_tmap(&grp.map[1]);
       mbar_arrive_expect_tx(w_full, WBYTES);
@@ -130,7 +159,9 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
       for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
         const int s = j % L.stages;
         const uint32_t k = static_cast<uint32_t>(j / L.stages);
+        const long long tw0 = L.trace ? clock64() : 0;
         mbar_wait(&empty[s], (k & 1u) ^ 1u);
+        if (L.trace) tr_prod += clock64() - tw0;
         mbar_arrive_expect_tx(&full[s], stage_tx);
         uint8_t* win = smem + lay.win_off + s * lay.win_stage_bytes;
         const int32_t r0 = static_cast<int32_t>(tile * 128 - grp.halo);
@@ -139,11 +170,22 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
           if (CH1) tma_load_2d(win + lay.win_chunk1_off + bx * kBoxRows * RB1, &grp.map[1], &full[s], 0,
                                r0 + bx * kBoxRows);
         }
+        if (STAGED && has_res) {
+          const int a = j & 1;
+          mbar_wait(&rempty[a], (static_cast<uint32_t>(j >> 1) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&rfull[a], 128u * ORB);
+          uint8_t* rb = smem + lay.res_off + a * 128 * ORB;
+          for (int bx = 0; bx < 4; ++bx)
+            tma_load_2d(rb + bx * 32 * ORB, &grp.res_map, &rfull[a], 0, static_cast<int32_t>(tile * 128 + bx * 32));
+        }
       }
+      if (L.trace) atomicAdd(&L.trace[kTraceProdWaitEmpty], static_cast<unsigned long long>(tr_prod));
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer --------------------------------
     if (lane == 0) {
+      long long tr_full = 0, tr_tmem = 0, tr_issue = 0;
+      const long long t_start = clock64();
       mbar_wait(w_full, 0);
       tc_fence_after();
       const uint32_t sW_addr = smem_u32(sW);
@@ -152,8 +194,15 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
       for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
         const int s = j % L.stages;
         const int a = j & 1;
+        const long long tm0 = L.trace ? clock64() : 0;
         mbar_wait(&full[s], static_cast<uint32_t>(j / L.stages) & 1u);
+        const long long tm1 = L.trace ? clock64() : 0;
         mbar_wait(&tempty[a], (static_cast<uint32_t>(j >> 1) & 1u) ^ 1u);
+        const long long tm2 = L.trace ? clock64() : 0;
+        if (L.trace) {
+          tr_full += tm1 - tm0;
+          tr_tmem += tm2 - tm1;
+        }
         tc_fence_after();
         const uint32_t win_addr = smem_u32(smem + lay.win_off + s * lay.win_stage_bytes);
         const uint32_t d_tmem = tbase + static_cast<uint32_t>(a * COUT);
@@ -184,81 +233,176 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
         }
         umma_commit(&empty[s]);   // window stage free once these MMAs have read it
         umma_commit(&tfull[a]);   // accumulator ready for the epilogue
+        if (L.trace) tr_issue += clock64() - tm2;
+      }
+      if (L.trace) {
+        atomicAdd(&L.trace[kTraceTotal], static_cast<unsigned long long>(clock64() - t_start));
+        atomicAdd(&L.trace[kTraceMmaWaitFull], static_cast<unsigned long long>(tr_full));
+        atomicAdd(&L.trace[kTraceMmaWaitTmem], static_cast<unsigned long long>(tr_tmem));
+        atomicAdd(&L.trace[kTraceMmaIssue], static_cast<unsigned long long>(tr_issue));
+        atomicAdd(&L.trace[kTraceTiles], static_cast<unsigned long long>(j));
       }
     }
   } else {
     // ------------------------------ epilogue (warps 2..5) ---------------------
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // s_bias / s_s2 / s_t2 visible to all epilogue warps
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = q * 32 + lane;
     const PlaneGeom geo = L.geo;
+    uint8_t* stg = STAGED ? smem + lay.stg_off + q * 2 * 32 * ORB : nullptr;  // [out | out2] x [32][COUT]
     int j = 0;
+    long long tr_ew = 0, tr_ework = 0;
     for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
       const int a = j & 1;
+      const long long te0 = L.trace ? clock64() : 0;
       mbar_wait(&tfull[a], static_cast<uint32_t>(j >> 1) & 1u);
+      const long long te1 = L.trace ? clock64() : 0;
+      if (L.trace) tr_ew += te1 - te0;
       tc_fence_after();
       const int64_t p = tile * 128 + row;
       const bool valid = geo.valid(p);
       const uint32_t taddr = tbase + static_cast<uint32_t>(a * COUT) + (static_cast<uint32_t>(q * 32) << 16);
-      __nv_bfloat16* orow = grp.out ? grp.out + p * COUT : nullptr;
-      __nv_bfloat16* orow2 = grp.out2 ? grp.out2 + p * COUT : nullptr;
-      const __nv_bfloat16* rrow = grp.res ? grp.res + p * COUT : nullptr;
-#pragma unroll 1
-      for (int cc = 0; cc < COUT / 32; ++cc) {
-        uint32_t r[32];
-        tmem_ld32(taddr + cc * 32, r);
-        tmem_ld_wait();
-        if (cc == COUT / 32 - 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[a]);
+      if constexpr (STAGED) {
+        const uint8_t* rrow = nullptr;
+        if (has_res) {
+          mbar_wait(&rfull[a], static_cast<uint32_t>(j >> 1) & 1u);
+          rrow = smem + lay.res_off + a * 128 * ORB;
         }
+        if (lane == 0) bulk_wait_read0();  // staging buffer free (previous tile's stores read it)
+        __syncwarp();
+#pragma unroll 1
+        for (int cc = 0; cc < COUT / 32; ++cc) {
+          uint32_t r[32];
+          tmem_ld32(taddr + cc * 32, r);
+          tmem_ld_wait();
+          if (cc == COUT / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);
+          }
 #pragma unroll
-        for (int v8 = 0; v8 < 4; ++v8) {
-          const int c0 = cc * 32 + v8 * 8;
-          float v[8];
+          for (int v8 = 0; v8 < 4; ++v8) {
+            const int c0 = cc * 32 + v8 * 8;
+            const uint32_t chunk = static_cast<uint32_t>(c0 / 8);
+            float v[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[v8 * 8 + i]) + __ldg(&grp.bias[c0 + i]);
-          if (rrow) {
-            const uint4 rv = *reinterpret_cast<const uint4*>(rrow + c0);
-            const __nv_bfloat162* rp = reinterpret_cast<const __nv_bfloat162*>(&rv);
+            for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[v8 * 8 + i]) + s_bias[c0 + i];
+            if (rrow) {
+              const uint4 rv = *reinterpret_cast<const uint4*>(rrow + swz_offset(ORB, static_cast<uint32_t>(row), chunk));
+              const __nv_bfloat162* rp = reinterpret_cast<const __nv_bfloat162*>(&rv);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float2 f = __bfloat1622float2(rp[i]);
-              v[2 * i] += f.x;
-              v[2 * i + 1] += f.y;
+              for (int i = 0; i < 4; ++i) {
+                const float2 f = __bfloat1622float2(rp[i]);
+                v[2 * i] += f.x;
+                v[2 * i + 1] += f.y;
+              }
+            }
+            if (grp.relu) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+            }
+            if (!valid) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = 0.f;
+            }
+            const uint32_t so = swz_offset(ORB, static_cast<uint32_t>(lane), chunk);
+            {
+              uint4 o;
+              __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) op[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+              *reinterpret_cast<uint4*>(stg + so) = o;
+            }
+            if (grp.out2) {
+              uint4 o;
+              __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float x0 = fmaxf(v[2 * i] * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
+                const float x1 = fmaxf(v[2 * i + 1] * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
+                op[i] = __floats2bfloat162_rn(valid ? x0 : 0.f, valid ? x1 : 0.f);
+              }
+              *reinterpret_cast<uint4*>(stg + 32 * ORB + so) = o;
             }
           }
-          if (grp.relu) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        if (has_res) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rempty[a]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int32_t r0 = static_cast<int32_t>(tile * 128 + q * 32);
+          tma_store_2d(&grp.out_map, stg, 0, r0);
+          if (grp.out2) tma_store_2d(&grp.out2_map, stg + 32 * ORB, 0, r0);
+          bulk_commit();
+        }
+      } else {
+        __nv_bfloat16* orow = grp.out ? grp.out + p * COUT : nullptr;
+        __nv_bfloat16* orow2 = grp.out2 ? grp.out2 + p * COUT : nullptr;
+        const __nv_bfloat16* rrow = grp.res ? grp.res + p * COUT : nullptr;
+#pragma unroll 1
+        for (int cc = 0; cc < COUT / 32; ++cc) {
+          uint32_t r[32];
+          tmem_ld32(taddr + cc * 32, r);
+          tmem_ld_wait();
+          if (cc == COUT / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);
           }
-          if (!valid) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = 0.f;
-          }
-          if (orow) {
-            uint4 o;
-            __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+          for (int v8 = 0; v8 < 4; ++v8) {
+            const int c0 = cc * 32 + v8 * 8;
+            float v[8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) op[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-            *reinterpret_cast<uint4*>(orow + c0) = o;
-          }
-          if (orow2) {
-            float u[8];
+            for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[v8 * 8 + i]) + s_bias[c0 + i];
+            if (rrow) {
+              const uint4 rv = *reinterpret_cast<const uint4*>(rrow + c0);
+              const __nv_bfloat162* rp = reinterpret_cast<const __nv_bfloat162*>(&rv);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              float x = v[i];
-              if (grp.s2) x = x * __ldg(&grp.s2[c0 + i]) + __ldg(&grp.t2[c0 + i]);
-              u[i] = valid ? fmaxf(x, 0.f) : 0.f;
+              for (int i = 0; i < 4; ++i) {
+                const float2 f = __bfloat1622float2(rp[i]);
+                v[2 * i] += f.x;
+                v[2 * i + 1] += f.y;
+              }
             }
-            uint4 o;
-            __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+            if (grp.relu) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) op[i] = __floats2bfloat162_rn(u[2 * i], u[2 * i + 1]);
-            *reinterpret_cast<uint4*>(orow2 + c0) = o;
+              for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+            }
+            if (!valid) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = 0.f;
+            }
+            if (orow) {
+              uint4 o;
+              __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) op[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+              *reinterpret_cast<uint4*>(orow + c0) = o;
+            }
+            if (orow2) {
+              uint4 o;
+              __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float x0 = fmaxf(v[2 * i] * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
+                const float x1 = fmaxf(v[2 * i + 1] * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
+                op[i] = __floats2bfloat162_rn(valid ? x0 : 0.f, valid ? x1 : 0.f);
+              }
+              *reinterpret_cast<uint4*>(orow2 + c0) = o;
+            }
           }
         }
       }
+      if (L.trace) tr_ework += clock64() - te1;
+    }
+    if (STAGED && lane == 0) bulk_wait0();  // all output stores complete before the CTA retires
+    if (L.trace && q == 0 && lane == 0) {
+      atomicAdd(&L.trace[kTraceEpiWaitFull], static_cast<unsigned long long>(tr_ew));
+      atomicAdd(&L.trace[kTraceEpiWork], static_cast<unsigned long long>(tr_ework));
     }
   }
 
@@ -317,6 +461,27 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }  // namespace
 
 bool conv_tc_supported(int cin, int cout, int ks) { return find_launch(cin, cout, ks) != nullptr; }
+
+bool conv_tc_staged(int cin, int cout) { return staged_epi(cin, cout); }
+
+void conv_tc_make_row_map(const void* plane, int64_t nalloc, int c, CUtensorMap* map) {
+  std::memset(map, 0, sizeof(CUtensorMap));
+  if (!plane) return;
+  if (c > 64) throw Error(3, "row map supports <= 64 channels");
+  const int rb = c * 2;
+  const CUtensorMapSwizzle sw = rb == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : rb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                           : CU_TENSOR_MAP_SWIZZLE_NONE;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(nalloc)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(c) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(c), 32u};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(plane), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
 
 size_t conv_tc_smem_bytes(int cin, int cout, int ks, int stages, int win_alloc) {
   return smem_layout(cin, cout, ks, stages, win_alloc).total;

@@ -12,6 +12,9 @@ constexpr int kTcMaxGroups = 4;
 // One convolution of a grouped launch (e.g. the same layer of the three CoNet subnetworks).
 struct TcGroup {
   CUtensorMap map[2];               // input plane, K-chunk 0 (<=64 ch) and chunk 1 (remaining ch)
+  CUtensorMap res_map;              // staged epilogue (COUT <= 64): residual plane, 32-row boxes
+  CUtensorMap out_map;              // staged epilogue: primary output plane, 32-row boxes
+  CUtensorMap out2_map;             // staged epilogue: pre-activated copy
   const uint8_t* wimg;              // weights, pre-swizzled smem image: [tap][chunk][COUT rows]
   const float* bias;                // [COUT] (BN folded in)
   const __nv_bfloat16* res;         // residual plane [Nalloc][COUT] or nullptr
@@ -32,7 +35,11 @@ struct TcLaunch {
   int32_t stages;                   // window pipeline depth
   int32_t win_alloc;                // rows allocated per window stage (max over groups, 8-aligned)
   int32_t pad_;
+  // debug: when non-null each CTA adds per-role clock64 totals (see kTrace* indices)
+  unsigned long long* trace;
 };
+enum : int { kTraceProdWaitEmpty = 0, kTraceMmaWaitFull, kTraceMmaWaitTmem, kTraceMmaIssue, kTraceEpiWaitFull,
+             kTraceEpiWork, kTraceTiles, kTraceTotal, kTraceN };
 
 // Shared memory the kernel needs for (cin, cout, ks) with `stages` window stages of `win_alloc` rows.
 size_t conv_tc_smem_bytes(int cin, int cout, int ks, int stages, int win_alloc);
@@ -49,5 +56,10 @@ void conv_tc_pack_weights(const float* w, int ks, int cin_real, int cout_real, c
                           int cout, uint8_t* img);
 // Tensor maps for K-chunks of an input plane [nalloc][cin] bf16 with a window box of `box_rows` rows.
 void conv_tc_make_maps(const void* plane, int64_t nalloc, int cin, int box_rows, CUtensorMap* maps);
+// Single-chunk (<= 64 channels) plane map with 32-row boxes for the staged epilogue (residual load,
+// output stores); a null plane yields a zeroed map.
+void conv_tc_make_row_map(const void* plane, int64_t nalloc, int c, CUtensorMap* map);
+// True when (cin, cout) uses the staged (TMA-load residual / TMA-store outputs) epilogue.
+bool conv_tc_staged(int cin, int cout);
 
 }  // namespace cnrx

@@ -1,0 +1,40 @@
+// conv_ws.h — launch interface of the weights-stationary (A in TMEM) 3x3 64->64 conv (conv_ws.cu).
+#pragma once
+#include <cuda.h>
+
+#include "common.h"
+
+namespace cnrx {
+
+struct WsGroup {
+  CUtensorMap in_map;    // input plane [Nalloc][64], 32-row boxes (activation window, B operand)
+  CUtensorMap res_map;   // residual plane, 32-row boxes
+  CUtensorMap out_map;   // output plane, 127-row boxes (TMA store of one tile)
+  CUtensorMap out2_map;  // pre-activated copy, 127-row boxes
+  const uint32_t* wimg;  // conv_ws64_pack_weights image: [24 blocks][128 lanes][8 x u32]
+  const float* bias;     // [64] (BN folded in)
+  const float* s2;       // out2 = relu(v*s2 + t2) (null: relu(v))
+  const float* t2;
+  int32_t relu, dil, halo, res_map_valid, out2_map_valid, pad_;
+};
+
+struct WsLaunch {
+  WsGroup g[4];
+  PlaneGeom geo;
+  int64_t n_tiles;   // 127-row output tiles
+  int32_t ngroups, stages, win_alloc, pad_;
+  unsigned long long* trace;  // debug: per-role clock64 totals (kTrace* in conv_tc.h + kWsTrace*)
+};
+enum : int { kWsTraceCombine = 8, kWsTraceStageWait, kWsTraceWrite, kWsTraceN };
+
+size_t conv_ws64_wimg_bytes();
+// w: fp32 [3,3,64,64] reference layout, scale: per-output-channel BN fold (nullable)
+void conv_ws64_pack_weights(const float* w, const float* scale, uint32_t* img);
+void conv_ws64_make_maps(const void* in, const void* res, const void* out, const void* out2, int64_t nalloc,
+                         WsGroup* g);
+size_t conv_ws64_smem_bytes(int stages, int win_alloc);
+int conv_ws64_win_alloc(int halo);
+int64_t conv_ws64_tiles(int64_t nalloc);
+const char* conv_ws64_launch(const WsLaunch& L, int num_sms, cudaStream_t stream);
+
+}  // namespace cnrx

@@ -13,6 +13,8 @@
 // ([B,T,F,N] complex, antenna fastest); plane writes are whole 32 B sectors per row.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.h"
 #include "kernels.h"
 
@@ -145,7 +147,178 @@ __global__ void pack_plane_kernel(const float* __restrict__ x, PlaneGeom geo, in
   }
 }
 
+// Features of plane row `row` (valid rows only): receive mode restates featurize_kernel per row.
+template <int CIN>
+__device__ __forceinline__ void row_features(const StemLaunch& L, const PlaneGeom& geo, int b, int t, int f,
+                                             float (&v)[CIN]) {
+  if (L.mode == 0) {
+    const float* src = L.x + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * CIN;
+#pragma unroll
+    for (int i = 0; i < CIN; ++i) v[i] = src[i];
+    return;
+  }
+  const PilotTablesDev& pt = L.pt;
+  constexpr int N = CIN / 6;
+  const int T = geo.T, F = geo.F;
+  const float2* y = reinterpret_cast<const float2*>(L.y);
+  const int j0 = pt.jlo[t], j1 = pt.jhi[t];
+  const float wt = pt.wt[t];
+  const float xr = pt.x[2 * (t * F + f)], xi = pt.x[2 * (t * F + f) + 1];
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    Cplx h[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int jj = q == 0 ? j0 : j1;
+      const int ts = pt.sym[jj];
+      const int flo = pt.flo[jj * F + f], fhi = pt.fhi[jj * F + f];
+      const float w = pt.wf[jj * F + f];
+      const Cplx ilo = {pt.inv_x[2 * (ts * F + flo)], pt.inv_x[2 * (ts * F + flo) + 1]};
+      const Cplx ihi = {pt.inv_x[2 * (ts * F + fhi)], pt.inv_x[2 * (ts * F + fhi) + 1]};
+      const float2 ylo = y[((static_cast<int64_t>(b) * T + ts) * F + flo) * N + a];
+      const float2 yhi = y[((static_cast<int64_t>(b) * T + ts) * F + fhi) * N + a];
+      const Cplx llo = cmul({ylo.x, ylo.y}, ilo), lhi = cmul({yhi.x, yhi.y}, ihi);
+      h[q] = {(1.f - w) * llo.re + w * lhi.re, (1.f - w) * llo.im + w * lhi.im};
+    }
+    const float2 yv = y[((static_cast<int64_t>(b) * T + t) * F + f) * N + a];
+    v[6 * a + 0] = yv.x;
+    v[6 * a + 1] = yv.y;
+    v[6 * a + 2] = xr;
+    v[6 * a + 3] = xi;
+    v[6 * a + 4] = (1.f - wt) * h[0].re + wt * h[1].re;
+    v[6 * a + 5] = (1.f - wt) * h[0].im + wt * h[1].im;
+  }
+}
+
+// Fused input stage.  grid.y = stem op; eight lanes share a plane row and lane g owns output
+// channels [8g, 8g+8) of the op, keeping its 8 x CIN weight slice in registers for the whole kernel,
+// so a row is written as one contiguous 128-byte line (a warp instruction stores 4 full rows).
+// The N antennas' 6 features are computed by the row's first N lanes and broadcast with shuffles.
+template <int CIN>
+__global__ void __launch_bounds__(256) stem_kernel(const __grid_constant__ StemLaunch L, PlaneGeom geo) {
+  constexpr int N = CIN / 6;
+  const StemOp& op = L.op[blockIdx.y];
+  const int cout = op.cout;
+  const int lane = threadIdx.x & 31;
+  const int g = lane & 7;         // 16-byte chunk of the row this lane writes
+  const int rsub = lane >> 3;     // row within the warp's 4-row group
+  const int base_lane = lane & ~7;
+  const int c0 = g * 8;
+  const bool active = c0 < cout;
+  float wr[CIN][8], bias[8], s2[8], t2[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = active ? c0 + k : 0;
+#pragma unroll
+    for (int i = 0; i < CIN; ++i) wr[i][k] = op.w[i * cout + c];
+    bias[k] = op.bias[c];
+    s2[k] = op.s2 ? op.s2[c] : 1.f;
+    t2[k] = op.t2 ? op.t2[c] : 0.f;
+  }
+  const int64_t groups = (geo.Nalloc + 3) / 4;
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  for (int64_t wg = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); wg < groups;
+       wg += wstride) {
+    const int64_t row = wg * 4 + rsub;
+    const bool in_range = row < geo.Nalloc;
+    const bool valid = in_range && geo.valid(row);
+    float mine[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) mine[k] = 0.f;
+    if (valid && g < N) {
+      int b, t, f;
+      geo.coords(row, b, t, f);
+      if (L.mode == 0) {
+        const float* src = L.x + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * CIN + 6 * g;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) mine[k] = src[k];
+      } else {
+        const PilotTablesDev& pt = L.pt;
+        const int T = geo.T, F = geo.F;
+        const float2* y = reinterpret_cast<const float2*>(L.y);
+        const int j0 = pt.jlo[t], j1 = pt.jhi[t];
+        const float wt = pt.wt[t];
+        Cplx h[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int jj = q == 0 ? j0 : j1;
+          const int ts = pt.sym[jj];
+          const int flo = pt.flo[jj * F + f], fhi = pt.fhi[jj * F + f];
+          const float w = pt.wf[jj * F + f];
+          const Cplx ilo = {pt.inv_x[2 * (ts * F + flo)], pt.inv_x[2 * (ts * F + flo) + 1]};
+          const Cplx ihi = {pt.inv_x[2 * (ts * F + fhi)], pt.inv_x[2 * (ts * F + fhi) + 1]};
+          const float2 ylo = y[((static_cast<int64_t>(b) * T + ts) * F + flo) * N + g];
+          const float2 yhi = y[((static_cast<int64_t>(b) * T + ts) * F + fhi) * N + g];
+          const Cplx llo = cmul({ylo.x, ylo.y}, ilo), lhi = cmul({yhi.x, yhi.y}, ihi);
+          h[q] = {(1.f - w) * llo.re + w * lhi.re, (1.f - w) * llo.im + w * lhi.im};
+        }
+        const float2 yv = y[((static_cast<int64_t>(b) * T + t) * F + f) * N + g];
+        mine[0] = yv.x;
+        mine[1] = yv.y;
+        mine[2] = pt.x[2 * (t * F + f)];
+        mine[3] = pt.x[2 * (t * F + f) + 1];
+        mine[4] = (1.f - wt) * h[0].re + wt * h[1].re;
+        mine[5] = (1.f - wt) * h[0].im + wt * h[1].im;
+      }
+    }
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = bias[k];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+      for (int k6 = 0; k6 < 6; ++k6) {
+        const float xi = __shfl_sync(0xffffffffu, mine[k6], base_lane + a);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = fmaf(xi, wr[6 * a + k6][k], acc[k]);
+      }
+    if (!active || !in_range) continue;
+    uint4 o1, o2;
+    __nv_bfloat162* p1 = reinterpret_cast<__nv_bfloat162*>(&o1);
+    __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&o2);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float a0 = acc[2 * k], a1 = acc[2 * k + 1];
+      if (op.relu) {
+        a0 = fmaxf(a0, 0.f);
+        a1 = fmaxf(a1, 0.f);
+      }
+      if (!valid) a0 = a1 = 0.f;
+      p1[k] = __floats2bfloat162_rn(a0, a1);
+      const float u0 = valid ? fmaxf(a0 * s2[2 * k] + t2[2 * k], 0.f) : 0.f;
+      const float u1 = valid ? fmaxf(a1 * s2[2 * k + 1] + t2[2 * k + 1], 0.f) : 0.f;
+      p2[k] = __floats2bfloat162_rn(u0, u1);
+    }
+    *reinterpret_cast<uint4*>(op.out + row * cout + c0) = o1;
+    if (op.out2) *reinterpret_cast<uint4*>(op.out2 + row * cout + c0) = o2;
+  }
+}
+
 }  // namespace
+
+bool stem_supported_cin(int cin) { return cin == 6 || cin == 12 || cin == 24 || cin == 48; }
+
+const char* launch_stem(const StemLaunch& L, const PlaneGeom& geo, cudaStream_t s) {
+  require(L.cin <= kStemMaxIn && L.nops >= 1 && L.nops <= kStemMaxOps, "stem launch out of range");
+  for (int i = 0; i < L.nops; ++i)
+    require(L.op[i].cout <= 64 && L.op[i].cout % 8 == 0, "stem kernel writes <= 64 channels per op");
+  const size_t smem = 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t groups = (geo.Nalloc + 3) / 4;
+  const dim3 blocks(static_cast<unsigned>(std::min<int64_t>((groups + 7) / 8, static_cast<int64_t>(sms) * 4)),
+                    static_cast<unsigned>(L.nops));
+  switch (L.cin) {
+    case 6: stem_kernel<6><<<blocks, 256, smem, s>>>(L, geo); break;
+    case 12: stem_kernel<12><<<blocks, 256, smem, s>>>(L, geo); break;
+    case 24: stem_kernel<24><<<blocks, 256, smem, s>>>(L, geo); break;
+    case 48: stem_kernel<48><<<blocks, 256, smem, s>>>(L, geo); break;
+    default: throw Error(3, "stem kernel supports 6/12/24/48 input channels");
+  }
+  CNRX_CUDA(cudaGetLastError());
+  return L.mode == 1 ? "stem_kernel<featurize>" : "stem_kernel<features>";
+}
 
 const char* launch_featurize_plane(const float* y, const PlaneGeom& geo, int N, const PilotTablesDev& pt,
                                    __nv_bfloat16* plane, int cpad, cudaStream_t s) {

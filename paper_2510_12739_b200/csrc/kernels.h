@@ -35,6 +35,34 @@ const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_
                               cudaStream_t s);
 
 // ---------------------------------------------------------------------------------------------
+// Fused input stage: network input features (computed from the received grid, or read from the
+// caller's fp32 [B,T,F,C] tensor) -> every 1x1 "stem" conv on the network input, on CUDA cores
+// (12 -> 3 x 64 is 768 FMA per row; a tensor-core launch would be epilogue-bound).
+// out = [relu](W . x + bias) (BN folded), optional out2 = relu(out*s2 + t2), padding rows zeroed.
+// ---------------------------------------------------------------------------------------------
+constexpr int kStemMaxOps = 4, kStemMaxIn = 48;
+struct StemOp {
+  const float* w;        // [cin][cout] fp32 (reference [1,1,cin,cout], BN scale folded)
+  const float* bias;     // [cout]
+  __nv_bfloat16* out;    // plane [Nalloc][cout]
+  __nv_bfloat16* out2;   // nullable
+  const float* s2;       // nullable (out2 = relu(out))
+  const float* t2;
+  int32_t cout, relu;
+};
+struct StemLaunch {
+  StemOp op[kStemMaxOps];
+  int32_t nops, cin;
+  int32_t N;             // receive mode: antennas (cin = 6N)
+  int32_t mode;          // 0: x fp32 [B,T,F,cin]; 1: received grid y
+  const float* x;
+  const float* y;        // complex [B,T,F,N]
+  PilotTablesDev pt;
+};
+const char* launch_stem(const StemLaunch& L, const PlaneGeom& geo, cudaStream_t s);
+bool stem_supported_cin(int cin);
+
+// ---------------------------------------------------------------------------------------------
 // Pointwise programs over bf16 planes (fusion nodes, the CoNet interaction and the LLR head).
 // A program is a linear chain evaluated per row on an 8-channel accumulator slice:
 //   LOAD k: acc = plane[k];  MUL k: acc *= plane[k];  ADD k: acc += plane[k];
@@ -54,7 +82,7 @@ struct PwProgram {
   int32_t n_ins;
   int32_t C;                // channels of every operand (multiple of 8)
   int32_t head_bits;        // 0: store plane; >0: head GEMV with this many outputs
-  int32_t pad_;
+  int32_t n_planes_used;    // planes[0 .. n_planes_used) are operands
   PwIns ins[kPwMaxIns];
   const __nv_bfloat16* planes[kPwMaxPlanes];
   const float* aff_s[kPwMaxAff];
@@ -66,6 +94,12 @@ struct PwProgram {
 };
 
 const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s);
+
+// Specialised form of the common program shape, a left fold over operand planes:
+//   acc = P[0]; [aff_0]; [relu_0];  for i >= 1: acc = acc (mul|add) P[i]; [aff_i]; [relu_i]
+// (build_conet's fusion tail).  Returns false if the program is not a fold (caller uses the
+// generic interpreter).
+bool pw_as_fold(const PwProgram& prog, int* nsteps, int* ops, int* affs, int* relus);
 
 // ---------------------------------------------------------------------------------------------
 // Generic fp32 node kernels in the reference layout [B,T,F,C] (CNRX_FP32 plans).

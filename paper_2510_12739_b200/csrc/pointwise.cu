@@ -8,6 +8,8 @@
 // rows produce no output.  HBM-bound: it reads C*2 bytes per operand plane and writes 4*bits bytes.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace cnrx {
@@ -93,21 +95,393 @@ __global__ void __launch_bounds__(256) pw_program_kernel(const __grid_constant__
   }
 }
 
+// Coalesced variant for C in {16, 32, 64, 128}: LPR = C/8 lanes share a row (each lane owns one
+// 16-byte, 8-channel slice), so a warp instruction reads 32 consecutive 16-byte slices of 32/LPR rows.
+// The head GEMV partial sums are reduced across the row's lanes with shuffles.
+template <int HEAD, int LPR>
+__global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ PwProgram prog, PlaneGeom geo) {
+  extern __shared__ float smem_f[];
+  const int C = prog.C, NB = prog.head_bits;
+  float* s_w = smem_f;                               // [C][NB]
+  float* s_b = s_w + (HEAD ? C * NB : 0);            // [NB]
+  float* s_aff = s_b + (HEAD ? ((NB + 3) & ~3) : 0); // [n_aff][2][C]
+  int n_aff = 0;
+  for (int n = 0; n < prog.n_ins; ++n)
+    if (prog.ins[n].op == PW_AFF) n_aff = max(n_aff, prog.ins[n].k + 1);
+  // Tables are stored with the lane's channel group (cg = c / 8) innermost so the LPR lanes of a row,
+  // which read the same (i, j) for different cg, hit distinct banks:
+  //   s_w[(i * NB + j) * LPR + cg] = W[8 cg + i][j],  s_aff[((2k + st) * 8 + i) * LPR + cg]
+  if (HEAD) {
+    for (int e = threadIdx.x; e < C * NB; e += blockDim.x) {
+      const int c = e / NB, jj = e % NB;
+      s_w[((c % 8) * NB + jj) * LPR + c / 8] = prog.head_w[e];
+    }
+    for (int e = threadIdx.x; e < NB; e += blockDim.x) s_b[e] = prog.head_b[e];
+  }
+  for (int e = threadIdx.x; e < n_aff * C; e += blockDim.x) {
+    const int k = e / C, c = e % C;
+    s_aff[((2 * k) * 8 + c % 8) * LPR + c / 8] = prog.aff_s[k][c];
+    s_aff[((2 * k + 1) * 8 + c % 8) * LPR + c / 8] = prog.aff_t[k][c];
+  }
+  __syncthreads();
+  constexpr int RPW = 32 / LPR;  // rows per warp pass
+  constexpr int U = 2;           // row groups per iteration (loads of both issued before compute)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cg = lane % LPR;
+  const int c0 = cg * 8;
+  const int np = prog.n_planes_used;
+  const int64_t groups = (geo.Nalloc + RPW - 1) / RPW;
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * 8;
+  for (int64_t grp0 = (static_cast<int64_t>(blockIdx.x) * 8 + warp) * U; grp0 < groups; grp0 += wstride * U) {
+    int64_t row[U];
+    bool in_range[U], valid[U];
+    uint4 raw[U][kPwMaxPlanes];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      row[u] = (grp0 + u) * RPW + lane / LPR;
+      in_range[u] = row[u] < geo.Nalloc;
+      valid[u] = in_range[u] && geo.valid(row[u]);
+#pragma unroll
+      for (int k = 0; k < kPwMaxPlanes; ++k)
+        if (k < np) raw[u][k] = valid[u] ? *reinterpret_cast<const uint4*>(prog.planes[k] + row[u] * C + c0)
+                                          : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+      for (int n = 0; n < prog.n_ins; ++n) {
+        const PwIns ins = prog.ins[n];
+        if (ins.op == PW_LOAD || ins.op == PW_MUL || ins.op == PW_ADD) {
+          uint4 r4 = raw[u][0];
+#pragma unroll
+          for (int k = 1; k < kPwMaxPlanes; ++k)
+            if (k == ins.k) r4 = raw[u][k];
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r4);
+          float v[8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(h[i]);
+            v[2 * i] = f.x;
+            v[2 * i + 1] = f.y;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            acc[i] = ins.op == PW_LOAD ? v[i] : ins.op == PW_MUL ? acc[i] * v[i] : acc[i] + v[i];
+        } else if (ins.op == PW_AFF) {
+          const float* sa = s_aff + (2 * ins.k) * 8 * LPR + cg;
+          const float* ta = s_aff + (2 * ins.k + 1) * 8 * LPR + cg;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = acc[i] * sa[i * LPR] + ta[i * LPR];
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = fmaxf(acc[i], 0.f);
+        }
+      }
+      if (!valid[u]) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+      }
+      if (HEAD) {
+        float part[kPwMaxBits];
+#pragma unroll
+        for (int j = 0; j < kPwMaxBits; ++j) part[j] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float* wr = s_w + (i * NB) * LPR + cg;
+#pragma unroll
+          for (int j = 0; j < kPwMaxBits; ++j)
+            if (j < NB) part[j] += acc[i] * wr[j * LPR];
+        }
+#pragma unroll
+        for (int off = LPR / 2; off >= 1; off >>= 1)
+#pragma unroll
+          for (int j = 0; j < kPwMaxBits; ++j)
+            if (j < NB) part[j] += __shfl_xor_sync(0xffffffffu, part[j], off);
+        if (valid[u] && cg == 0) {
+          int b, t, f;
+          geo.coords(row[u], b, t, f);
+          float* dst = prog.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * NB;
+          if (NB == 4) {
+            *reinterpret_cast<float4*>(dst) = make_float4(part[0] + s_b[0], part[1] + s_b[1], part[2] + s_b[2],
+                                                          part[3] + s_b[3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kPwMaxBits; ++j)
+              if (j < NB) dst[j] = part[j] + s_b[j];
+          }
+        }
+      } else if (in_range[u]) {
+        uint4 o;
+        __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) op[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+        *reinterpret_cast<uint4*>(prog.out_plane + row[u] * C + c0) = o;
+      }
+    }
+  }
+}
+
+
+// Fold kernel: LPR = C/8 lanes per row (lane cg owns channels [8cg, 8cg+8)); all NS operand loads of
+// the row are issued before any arithmetic; BN tables and head weights are read from shared memory
+// laid out [.][cg][8] so the lanes of a row read distinct banks and rows of a warp broadcast.
+struct FoldSteps {
+  int32_t op[kPwMaxPlanes];    // PW_MUL / PW_ADD for steps >= 1
+  int32_t aff[kPwMaxPlanes];   // affine table index or -1
+  int32_t relu[kPwMaxPlanes];
+};
+
+template <int HEAD, int LPR, int NS>
+__global__ void __launch_bounds__(256) pw_fold_kernel(const __grid_constant__ PwProgram prog, const FoldSteps fs,
+                                                      PlaneGeom geo) {
+  extern __shared__ float smem_f[];
+  constexpr int C = LPR * 8;
+  constexpr int NB = HEAD;  // LLR outputs per RE (0: the program stores a plane)
+  float* s_aff = smem_f;                              // [NS][2][LPR][8]
+  float* s_w = s_aff + NS * 2 * C;                    // [8][NB][LPR]
+  float* s_b = s_w + C * NB;                          // [NB]
+  for (int e = threadIdx.x; e < NS * C; e += blockDim.x) {
+    const int i = e / C, c = e % C;
+    const int a = fs.aff[i];
+    s_aff[(i * 2) * C + c] = a >= 0 ? prog.aff_s[a][c] : 1.f;
+    s_aff[(i * 2 + 1) * C + c] = a >= 0 ? prog.aff_t[a][c] : 0.f;
+  }
+  if (NB > 0) {
+    for (int e = threadIdx.x; e < C * NB; e += blockDim.x) {  // [e][j][cg]: lanes of a row hit distinct banks
+      const int c = e / NB, j = e % NB;
+      s_w[((c % 8) * NB + j) * LPR + c / 8] = prog.head_w[e];
+    }
+    for (int e = threadIdx.x; e < NB; e += blockDim.x) s_b[e] = prog.head_b[e];
+  }
+  __syncthreads();
+  constexpr int RPW = 32 / LPR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cg = lane % LPR;
+  const int c0 = cg * 8;
+  const int64_t groups = (geo.Nalloc + RPW - 1) / RPW;
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * 8;
+  constexpr int U = 4;  // row groups per warp iteration: U * NS 16-byte loads in flight per lane
+  for (int64_t grp0 = (static_cast<int64_t>(blockIdx.x) * 8 + warp) * U; grp0 < groups; grp0 += wstride * U) {
+    int64_t row[U];
+    bool in_range[U], valid[U];
+    uint4 raw[U][NS];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      row[u] = (grp0 + u) * RPW + lane / LPR;
+      in_range[u] = row[u] < geo.Nalloc;
+      valid[u] = in_range[u] && geo.valid(row[u]);
+#pragma unroll
+      for (int i = 0; i < NS; ++i)
+        raw[u][i] = valid[u] ? __ldg(reinterpret_cast<const uint4*>(prog.planes[i] + row[u] * C + c0))
+                             : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < NS; ++i) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[u][i]);
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+          v[2 * e] = f.x;
+          v[2 * e + 1] = f.y;
+        }
+        if (i == 0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = v[e];
+        } else if (fs.op[i] == PW_MUL) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] *= v[e];
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += v[e];
+        }
+        if (fs.aff[i] >= 0) {
+          const float4 s0 = *reinterpret_cast<const float4*>(s_aff + (i * 2) * C + c0);
+          const float4 s1 = *reinterpret_cast<const float4*>(s_aff + (i * 2) * C + c0 + 4);
+          const float4 t0 = *reinterpret_cast<const float4*>(s_aff + (i * 2 + 1) * C + c0);
+          const float4 t1 = *reinterpret_cast<const float4*>(s_aff + (i * 2 + 1) * C + c0 + 4);
+          acc[0] = acc[0] * s0.x + t0.x;
+          acc[1] = acc[1] * s0.y + t0.y;
+          acc[2] = acc[2] * s0.z + t0.z;
+          acc[3] = acc[3] * s0.w + t0.w;
+          acc[4] = acc[4] * s1.x + t1.x;
+          acc[5] = acc[5] * s1.y + t1.y;
+          acc[6] = acc[6] * s1.z + t1.z;
+          acc[7] = acc[7] * s1.w + t1.w;
+        }
+        if (fs.relu[i]) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = fmaxf(acc[e], 0.f);
+        }
+      }
+      if constexpr (NB > 0) {
+        float part[NB > 0 ? NB : 1];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) part[j] = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float* wr = s_w + (e * NB) * LPR + cg;
+#pragma unroll
+          for (int j = 0; j < NB; ++j) part[j] = fmaf(acc[e], wr[j * LPR], part[j]);
+        }
+#pragma unroll
+        for (int off = LPR / 2; off >= 1; off >>= 1)
+#pragma unroll
+          for (int j = 0; j < NB; ++j) part[j] += __shfl_xor_sync(0xffffffffu, part[j], off);
+        if (valid[u] && cg == 0) {
+          int b, t, f;
+          geo.coords(row[u], b, t, f);
+          float* dst = prog.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * NB;
+          if constexpr (NB == 4) {
+            *reinterpret_cast<float4*>(dst) =
+                make_float4(part[0] + s_b[0], part[1] + s_b[1], part[2] + s_b[2], part[3] + s_b[3]);
+          } else if constexpr (NB == 2) {
+            *reinterpret_cast<float2*>(dst) = make_float2(part[0] + s_b[0], part[1] + s_b[1]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < NB; ++j) dst[j] = part[j] + s_b[j];
+          }
+        }
+      } else if (in_range[u]) {
+        if (!valid[u]) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+        }
+        uint4 o;
+        __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) op[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+        *reinterpret_cast<uint4*>(prog.out_plane + row[u] * C + c0) = o;
+      }
+    }
+  }
+}
+
+template <int HEAD, int LPR, int NS>
+void launch_fold_t(const PwProgram& prog, const FoldSteps& fs, const PlaneGeom& geo, cudaStream_t s) {
+  constexpr int C = LPR * 8;
+  const size_t smem = sizeof(float) * (NS * 2 * C + (HEAD ? C * HEAD + HEAD : 0));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t groups = (geo.Nalloc + (32 / LPR) - 1) / (32 / LPR);
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((groups + 31) / 32, static_cast<int64_t>(sms) * 8));
+  pw_fold_kernel<HEAD, LPR, NS><<<blocks, 256, smem, s>>>(prog, fs, geo);
+  CNRX_CUDA(cudaGetLastError());
+}
+
+template <int HEAD, int LPR>
+bool launch_fold_ns(const PwProgram& prog, const FoldSteps& fs, int ns, const PlaneGeom& geo, cudaStream_t s) {
+  switch (ns) {
+    case 1: launch_fold_t<HEAD, LPR, 1>(prog, fs, geo, s); return true;
+    case 2: launch_fold_t<HEAD, LPR, 2>(prog, fs, geo, s); return true;
+    case 3: launch_fold_t<HEAD, LPR, 3>(prog, fs, geo, s); return true;
+    case 4: launch_fold_t<HEAD, LPR, 4>(prog, fs, geo, s); return true;
+    default: return false;
+  }
+}
+
+template <int HEAD>
+bool launch_fold_c(const PwProgram& prog, const FoldSteps& fs, int ns, const PlaneGeom& geo, cudaStream_t s) {
+  switch (prog.C) {
+    case 16: return launch_fold_ns<HEAD, 2>(prog, fs, ns, geo, s);
+    case 32: return launch_fold_ns<HEAD, 4>(prog, fs, ns, geo, s);
+    case 64: return launch_fold_ns<HEAD, 8>(prog, fs, ns, geo, s);
+    case 128: return launch_fold_ns<HEAD, 16>(prog, fs, ns, geo, s);
+    default: return false;
+  }
+}
+
+// HEAD = LLR outputs per RE (compile-time: the GEMV and its shuffle reduction are fully unrolled)
+bool launch_fold_any(const PwProgram& prog, const FoldSteps& fs, int ns, const PlaneGeom& geo, cudaStream_t s) {
+  switch (prog.head_bits) {
+    case 0: return launch_fold_c<0>(prog, fs, ns, geo, s);
+    case 1: return launch_fold_c<1>(prog, fs, ns, geo, s);
+    case 2: return launch_fold_c<2>(prog, fs, ns, geo, s);
+    case 4: return launch_fold_c<4>(prog, fs, ns, geo, s);
+    case 6: return launch_fold_c<6>(prog, fs, ns, geo, s);
+    case 8: return launch_fold_c<8>(prog, fs, ns, geo, s);
+    default: return false;
+  }
+}
+
 }  // namespace
 
-const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s) {
-  const int threads = 256;
-  const unsigned blocks = static_cast<unsigned>((geo.Nalloc + threads - 1) / threads);
-  if (prog.head_bits > 0) {
-    require(prog.head_bits <= kPwMaxBits, "head with more than 16 outputs");
-    const size_t smem = sizeof(float) * (static_cast<size_t>(prog.C) * prog.head_bits + prog.head_bits);
-    pw_program_kernel<1><<<blocks, threads, smem, s>>>(prog, geo);
-    CNRX_CUDA(cudaGetLastError());
-    return "pw_program_kernel<head>";
+bool pw_as_fold(const PwProgram& prog, int* nsteps, int* ops, int* affs, int* relus) {
+  int ns = 0;
+  for (int n = 0; n < prog.n_ins; ++n) {
+    const PwIns& in = prog.ins[n];
+    if (in.op == PW_LOAD || in.op == PW_MUL || in.op == PW_ADD) {
+      if ((in.op == PW_LOAD) != (ns == 0) || in.k != ns || ns >= kPwMaxPlanes) return false;
+      ops[ns] = in.op;
+      affs[ns] = -1;
+      relus[ns] = 0;
+      ++ns;
+    } else if (ns == 0) {
+      return false;
+    } else if (in.op == PW_AFF) {
+      if (affs[ns - 1] >= 0 || relus[ns - 1]) return false;
+      affs[ns - 1] = in.k;
+    } else if (in.op == PW_RELU) {
+      relus[ns - 1] = 1;
+    }
   }
-  pw_program_kernel<0><<<blocks, threads, 0, s>>>(prog, geo);
+  *nsteps = ns;
+  return ns > 0;
+}
+
+template <int HEAD, int LPR>
+static void launch_rows(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s) {
+  int n_aff = 0;
+  for (int n = 0; n < prog.n_ins; ++n)
+    if (prog.ins[n].op == PW_AFF) n_aff = std::max(n_aff, prog.ins[n].k + 1);
+  const size_t smem = sizeof(float) * ((HEAD ? prog.C * prog.head_bits + ((prog.head_bits + 3) & ~3) : 0) +
+                                       2 * n_aff * prog.C);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t groups = (geo.Nalloc + (32 / LPR) - 1) / (32 / LPR);
+  const int64_t want = (groups + 15) / 16;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(sms) * 8));
+  pw_rows_kernel<HEAD, LPR><<<blocks, 256, smem, s>>>(prog, geo);
   CNRX_CUDA(cudaGetLastError());
-  return "pw_program_kernel<plane>";
+}
+
+const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s) {
+  if (prog.head_bits > 0) require(prog.head_bits <= kPwMaxBits, "head with more than 16 outputs");
+  const bool head = prog.head_bits > 0;
+  {
+    FoldSteps fs{};
+    int ns = 0;
+    if (pw_as_fold(prog, &ns, fs.op, fs.aff, fs.relu) && prog.n_planes_used == ns) {
+      const bool ok = launch_fold_any(prog, fs, ns, geo, s);
+      if (ok) return head ? "pw_fold_kernel<head>" : "pw_fold_kernel<plane>";
+    }
+  }
+  switch (prog.C) {
+    case 16: head ? launch_rows<1, 2>(prog, geo, s) : launch_rows<0, 2>(prog, geo, s); break;
+    case 32: head ? launch_rows<1, 4>(prog, geo, s) : launch_rows<0, 4>(prog, geo, s); break;
+    case 64: head ? launch_rows<1, 8>(prog, geo, s) : launch_rows<0, 8>(prog, geo, s); break;
+    case 128: head ? launch_rows<1, 16>(prog, geo, s) : launch_rows<0, 16>(prog, geo, s); break;
+    default: {
+      const int threads = 256;
+      const unsigned blocks = static_cast<unsigned>((geo.Nalloc + threads - 1) / threads);
+      if (head) {
+        const size_t smem = sizeof(float) * (static_cast<size_t>(prog.C) * prog.head_bits + prog.head_bits);
+        pw_program_kernel<1><<<blocks, threads, smem, s>>>(prog, geo);
+      } else {
+        pw_program_kernel<0><<<blocks, threads, 0, s>>>(prog, geo);
+      }
+      CNRX_CUDA(cudaGetLastError());
+      return head ? "pw_program_kernel<head>" : "pw_program_kernel<plane>";
+    }
+  }
+  return head ? "pw_rows_kernel<head>" : "pw_rows_kernel<plane>";
 }
 
 }  // namespace cnrx

@@ -16,6 +16,11 @@ import torch.nn.functional as Fn
 from paper_2510_12739_b200 import graph as G
 
 
+import os
+
+STEM_ENABLED = os.environ.get("CNRX_STEM") is not None  # mirrors api.cpp: fused CUDA-core stem is opt-in
+
+
 def bf16(t: torch.Tensor) -> torch.Tensor:
     return t.to(torch.bfloat16).to(torch.float32)
 
@@ -86,10 +91,21 @@ def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
         return planes[u]
 
     absorbed = set()
+    stem_cin = None
+    n_stems = 0
     for i, n in enumerate(nodes):
         if n.op != G.OP_CONV or i in absorbed or i == g.output_node:
             continue
-        inp = plane_for(n.in0)
+        w0 = g.params[n.w].value
+        # 1x1 convs on the network input run on CUDA cores in fp32 (fused stem kernel): no bf16
+        # rounding of the features or the weights (mirrors Bf16Compiler's stem selection)
+        stem = (STEM_ENABLED and n.in0 == g.input_node and w0.shape[0] == 1 and w0.shape[2] in (6, 12, 24, 48)
+                and w0.shape[3] % 8 == 0 and w0.shape[3] <= 64 and n_stems < 4
+                and (stem_cin is None or stem_cin == w0.shape[2]))
+        if stem:
+            n_stems += 1
+            stem_cin = w0.shape[2]
+        inp = xt if stem else plane_for(n.in0)
         w = torch.from_numpy(g.params[n.w].value)  # [kh,kw,cin,cout]
         cout = w.shape[3]
         bias = torch.from_numpy(g.params[n.b].value.copy()) if n.b >= 0 else torch.zeros(cout)
@@ -111,8 +127,12 @@ def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
                 res = plane_for(other)
                 absorbed.add(c)
                 end = c
+        if res is not None and stem:
+            raise ValueError("stem with residual is not emulated")
         wf = w * scale[None, None, None, :] if scale is not None else w
-        wk = bf16(wf.permute(3, 2, 0, 1).contiguous())  # [cout,cin,kh,kw]
+        wk = wf.permute(3, 2, 0, 1).contiguous()  # [cout,cin,kh,kw]
+        if not stem:
+            wk = bf16(wk)
         kh, kw = w.shape[0], w.shape[1]
         cin_plane = inp.shape[1]
         if cin_plane > wk.shape[1]:  # zero-padded input channels

@@ -66,13 +66,13 @@ def main():
     yd = torch.from_numpy(full.y).cuda()
     out = torch.empty((B, 14, link.F, 4), dtype=torch.float32, device="cuda")
     for _ in range(3):
-        pb.receive_device(yd, out)
+        pb.receive_device(yd, out, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     n = 10
     for _ in range(n):
-        pb.receive_device(yd, out)
+        pb.receive_device(yd, out, torch.cuda.current_stream().cuda_stream)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
