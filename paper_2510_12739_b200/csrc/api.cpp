@@ -240,6 +240,7 @@ struct cnrx_plan {
 
   // graph capture
   bool capture = false;
+  cudaEvent_t fence_in = nullptr, fence_out = nullptr;
   cudaGraphExec_t gexec = nullptr;
   std::string gkey;
 
@@ -1128,6 +1129,19 @@ void run_forward(cnrx_plan& p, const float* x_dev, int64_t B, int64_t T, int64_t
     enqueue();
     return;
   }
+  // A legacy / per-thread default stream cannot be captured: capture and replay on the plan's own
+  // stream, ordered after and before the caller's stream with events.
+  cudaStream_t caller = s;
+  const bool fence = s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread;
+  if (fence) {
+    s = p.stream;
+    if (!p.fence_in) {
+      CNRX_CUDA(cudaEventCreateWithFlags(&p.fence_in, cudaEventDisableTiming));
+      CNRX_CUDA(cudaEventCreateWithFlags(&p.fence_out, cudaEventDisableTiming));
+    }
+    CNRX_CUDA(cudaEventRecord(p.fence_in, caller));
+    CNRX_CUDA(cudaStreamWaitEvent(s, p.fence_in, 0));
+  }
   char key[256];
   snprintf(key, sizeof key, "%p/%p/%lld/%lld/%lld/%d/%p", static_cast<const void*>(x_dev), static_cast<void*>(out_dev),
            static_cast<long long>(B), static_cast<long long>(T), static_cast<long long>(F), input_kind,
@@ -1151,6 +1165,10 @@ void run_forward(cnrx_plan& p, const float* x_dev, int64_t B, int64_t T, int64_t
     p.gkey = key;
   }
   CNRX_CUDA(cudaGraphLaunch(p.gexec, s));
+  if (fence) {
+    CNRX_CUDA(cudaEventRecord(p.fence_out, s));
+    CNRX_CUDA(cudaStreamWaitEvent(caller, p.fence_out, 0));
+  }
 }
 
 
@@ -1316,6 +1334,8 @@ void cnrx_plan_destroy(cnrx_plan* plan) {
   cudaSetDevice(plan->device);
   if (plan->stream) cudaStreamSynchronize(plan->stream);
   if (plan->gexec) cudaGraphExecDestroy(plan->gexec);
+  if (plan->fence_in) cudaEventDestroy(plan->fence_in);
+  if (plan->fence_out) cudaEventDestroy(plan->fence_out);
   for (void* b : plan->ws.buffers) cudaFree(b);
   if (plan->ws.in_buf) cudaFree(plan->ws.in_buf);
   if (plan->ws.out_buf) cudaFree(plan->ws.out_buf);

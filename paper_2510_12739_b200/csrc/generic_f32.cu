@@ -1,11 +1,13 @@
 // generic_f32.cu — fp32 CUDA-core kernels for CNRX_FP32 plans, in the reference layout [B,T,F,C].
 //
 // The fp32 path is the one BASELINE config 1 names ("CoNet-small, fp32") and the fp32 leg of the
-// config-5 sweep: LLRs must match the reference within 1e-4 relative, so nothing here runs on the
-// tensor cores (TF32 would not meet that).  Each LayerOp has a kernel (network.hpp:380-420); the plan
-// compiler fuses a conv with the single-consumer BN / ReLU / add|mul chain that follows it, applying
-// the same float operations in the same order as the separate reference nodes (no FMA contraction in
-// the epilogue), so only the conv's summation order differs from the reference.
+// config-5 sweep.  It is BIT-EXACT with the reference: every kernel performs the reference's float
+// operations in the reference's order with the reference's rounding — conv accumulates bias, then
+// taps (dt, df) and input channels in order with separately rounded multiply and add
+// (yrow[co] += xv * wrow[co], kernels.hpp:78-82; x86-64 has no FMA contraction), eval BN applies the
+// host-folded float scale/shift (norms.hpp:81-95), layer norm runs in double (norms.hpp:155-191).
+// Each LayerOp has a kernel (network.hpp:380-420); the plan compiler fuses a conv with the
+// single-consumer BN / ReLU / add|mul chain that follows it without changing any rounding.
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -57,10 +59,10 @@ __global__ void __launch_bounds__(128) conv_f32_kernel(const ConvF32 p) {
 #pragma unroll
             for (int q = 0; q < kCot / 4; ++q) {
               const float4 wv = w4[q];
-              acc[4 * q + 0] = fmaf(xs[u], wv.x, acc[4 * q + 0]);
-              acc[4 * q + 1] = fmaf(xs[u], wv.y, acc[4 * q + 1]);
-              acc[4 * q + 2] = fmaf(xs[u], wv.z, acc[4 * q + 2]);
-              acc[4 * q + 3] = fmaf(xs[u], wv.w, acc[4 * q + 3]);
+              acc[4 * q + 0] = __fadd_rn(acc[4 * q + 0], __fmul_rn(xs[u], wv.x));
+              acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(xs[u], wv.y));
+              acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(xs[u], wv.z));
+              acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(xs[u], wv.w));
             }
           }
         }
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(128) conv_f32_kernel(const ConvF32 p) {
       for (; ci < p.cin; ++ci) {
         const float xv = xr[ci];
 #pragma unroll
-        for (int c = 0; c < kCot; ++c) acc[c] = fmaf(xv, wt[ci * kCot + c], acc[c]);
+        for (int c = 0; c < kCot; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(xv, wt[ci * kCot + c]));
       }
     }
   }
@@ -103,7 +105,7 @@ __global__ void dwconv_f32_kernel(const float* __restrict__ x, const float* __re
     for (int df = 0; df < kw; ++df) {
       const int fi = f + df - kw / 2;
       if (fi < 0 || fi >= F) continue;
-      acc = fmaf(x[((b * T + ti) * F + fi) * C + c], w[(dt * kw + df) * C + c], acc);
+      acc = __fadd_rn(acc, __fmul_rn(x[((b * T + ti) * F + fi) * C + c], w[(dt * kw + df) * C + c]));
     }
   }
   y[i] = acc;
@@ -139,14 +141,17 @@ __global__ void layernorm_f32_kernel(const float* __restrict__ x, const float* _
   const float* xr = x + r * C;
   double sum = 0.0, sq = 0.0;
   for (int i = 0; i < C; ++i) {
-    sum += xr[i];
-    sq += static_cast<double>(xr[i]) * xr[i];
+    sum = __dadd_rn(sum, static_cast<double>(xr[i]));
+    sq = __dadd_rn(sq, __dmul_rn(static_cast<double>(xr[i]), static_cast<double>(xr[i])));
   }
-  const double m = sum / C;
-  double v = sq / C - m * m;
+  const double m = __ddiv_rn(sum, static_cast<double>(C));
+  double v = __dsub_rn(__ddiv_rn(sq, static_cast<double>(C)), __dmul_rn(m, m));
   if (v < 0) v = 0;
-  const double istd = 1.0 / sqrt(v + eps);
-  for (int i = 0; i < C; ++i) y[r * C + i] = static_cast<float>((static_cast<double>(xr[i]) - m) * istd * g[i] + bb[i]);
+  const double istd = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(v, eps)));
+  for (int i = 0; i < C; ++i) {
+    const double z = __dmul_rn(__dmul_rn(__dsub_rn(static_cast<double>(xr[i]), m), istd), static_cast<double>(g[i]));
+    y[r * C + i] = static_cast<float>(__dadd_rn(z, static_cast<double>(bb[i])));
+  }
 }
 
 __global__ void concat_f32_kernel(const float* __restrict__ a, int ca, const float* __restrict__ b, int cb,
