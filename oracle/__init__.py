@@ -41,6 +41,10 @@ def build(reference: bool = True) -> None:
     subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
     if reference and os.path.isdir(os.environ.get("CNRX_REFERENCE", "/root/reference")):
         subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+        # reference-side C++ integration example (needs libconetrx_cuda.so built first)
+        integ = os.path.join(os.path.dirname(HERE), "tools", "integration")
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_2510_12739_b200", "libconetrx_cuda.so")):
+            subprocess.run(["make", "-s", "-C", integ], check=True)
 
 
 def lib():

@@ -259,3 +259,17 @@ def test_tensor_core_kernels_are_used():
     assert sum("conv_ws64" in n for n in names) == 8, names
     info = p.info()
     assert info["n_tc_convs"] == 27 and info["macs_per_re"] == 887296
+
+
+def test_cpp_drop_in_example():
+    """Reference-side C++ integration (include/conetrx/gpu_plan.hpp): a conetrx::Network<float> built by
+    the reference's own builders runs through the plan; fp32 bit-exact, bf16 within tolerance, same
+    exception type on a bad input (tools/integration/drop_in_example.cpp)."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "drop_in_example")
+    if not os.path.exists(exe):
+        pytest.skip("drop_in_example not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "drop-in OK" in r.stdout
