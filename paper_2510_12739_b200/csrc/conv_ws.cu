@@ -16,11 +16,11 @@
 // q in [p0, p0+127) is A[q-p0] + B[q-p0+1].  Pairs: (dt=-1,0) for df in {-1,0,1} and (dt=+1, zero) for
 // df in {-1,0,1} -> 6 UMMAs per 16-channel K step, 24 per tile, 75% of the issued MACs useful.
 //
-// Warp roles (320 threads, persistent, 1 CTA/SM, TMEM: 224 weight/identity columns + 2 x 128 accumulator):
+// Warp roles (576 threads, persistent, 1 CTA/SM, TMEM: 224 weight/identity columns + 2 x 128 accumulator):
 //   warp 0     TMA producer: activation windows (4-stage ring) + residual tiles (2-deep ring)
 //   warp 1     TMEM allocator + MMA issuer
-//   warps 2-9  weights -> TMEM at start (2-5); epilogue: two warps per TMEM lane quadrant, each owning
-//              64 accumulator columns: TMEM -> registers, lane-pair shuffle combine,
+//   warps 2-17 weights -> TMEM at start (2-5); epilogue: four warps per TMEM lane quadrant, each owning
+//              32 accumulator columns: TMEM -> registers, lane-pair shuffle combine,
 //              bias / ReLU / validity, bf16 pack, 8x8 lane-butterfly transpose so every lane writes
 //              16-byte rows (8 channels of one plane row) to swizzled smem, TMA store of 127 rows.
 // The residual add is done by the tensor core: an identity A block (TMEM columns 192..223) times
@@ -73,7 +73,7 @@ __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t byte_in_row) {
   return row * 128u + ((((byte_in_row >> 4) ^ (row & 7u)) << 4) | (byte_in_row & 15u));
 }
 
-__global__ void __launch_bounds__(320, 1) conv_ws64_kernel(const __grid_constant__ WsLaunch L) {
+__global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant__ WsLaunch L) {
   constexpr uint32_t IDESC = idesc_bf16_f32(128, kN);
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
@@ -108,14 +108,14 @@ __global__ void __launch_bounds__(320, 1) conv_ws64_kernel(const __grid_constant
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
+      mbar_init(&tempty[a], 16);
       mbar_init(&rfull[a], 1);
       mbar_init(&rempty[a], 1);
     }
     fence_barrier_init();
   }
   if (warp >= 2) {
-    for (int c = threadIdx.x - 64; c < kC; c += 256) {
+    for (int c = threadIdx.x - 64; c < kC; c += 512) {
       s_bias[c] = grp.bias[c];
       s_s2[c] = grp.s2 ? grp.s2[c] : 1.f;
       s_t2[c] = grp.t2 ? grp.t2[c] : 0.f;
@@ -256,16 +256,16 @@ __global__ void __launch_bounds__(320, 1) conv_ws64_kernel(const __grid_constant
       atomicAdd(&L.trace[kTraceTiles], static_cast<unsigned long long>(j));
     }
   } else {
-    // ------------------------------ epilogue (warps 2..9) ---------------------
+    // ------------------------------ epilogue (warps 2..17) --------------------
     const int q = warp & 3;            // TMEM lane quadrant
-    const int H = (warp - 2) >> 2;     // column half: accumulator columns [64H, 64H + 64)
-    const int cb = 64 * H;
+    const int H = (warp - 2) >> 2;     // column quarter: accumulator columns [32H, 32H + 32)
+    const int cb = 32 * H;
     const int Ln = q * 32 + lane;      // accumulator lane
     const int co = Ln >> 1;            // output channel of this lane
     const bool odd = (lane & 1) != 0;  // B-half lane
     const int idx = (lane >> 1) & 7;   // position in the 8-lane transpose group (same parity, same half-warp)
     const int c0 = q * 16 + (lane >> 4) * 8;  // first of the 8 channels this lane writes after the transpose
-    const int rbase = cb + (odd ? 32 : 0);    // this lane finalises rows rbase .. rbase + 31
+    const int rbase = cb + (odd ? 16 : 0);    // this lane finalises rows rbase .. rbase + 15
     const PlaneGeom geo = L.geo;
     uint8_t* stg = smem + lay.stg_off;
     const float bias = s_bias[co];
@@ -281,12 +281,11 @@ __global__ void __launch_bounds__(320, 1) conv_ws64_kernel(const __grid_constant
       const long long te1 = clock64();
       tr_ew += te1 - te0;
       tc_fence_after();
-      uint32_t ra[32], rb[32], rx[1];  // accumulator columns cb..cb+31, cb+32..cb+63, cb+64
+      uint32_t ra[32], rx[1];  // accumulator columns cb..cb+31, cb+32
       const uint32_t taddr = tbase + kAcc0 + static_cast<uint32_t>(a * kN + cb) + (static_cast<uint32_t>(q * 32) << 16);
       tmem_ld32(taddr, ra);
-      tmem_ld32(taddr + 32, rb);
-      if (H == 0) {
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(rx[0]) : "r"(taddr + 64) : "memory");
+      if (H < 3) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(rx[0]) : "r"(taddr + 32) : "memory");
       } else {
         rx[0] = 0;
       }
@@ -294,15 +293,15 @@ __global__ void __launch_bounds__(320, 1) conv_ws64_kernel(const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
-#define CNRX_R(i) ((i) < 32 ? ra[(i)] : (i) < 64 ? rb[(i) - 32] : rx[0])
-      // row cb + k = A[k] + B[k+1]: even lanes finalise k in [0,32), odd lanes k in [32,64).
-      // pk[i] packs rows (2i, 2i+1) of this lane's 32 rows, channel co.
-      uint32_t pk[16];
+#define CNRX_R(i) ((i) < 32 ? ra[(i)] : rx[0])
+      // row cb + k = A[k] + B[k+1]: even lanes finalise k in [0,16), odd lanes k in [16,32).
+      // pk[i] packs rows (2i, 2i+1) of this lane's 16 rows, channel co.
+      uint32_t pk[8];
 #pragma unroll
-      for (int m = 0; m < 32; ++m) {
-        const uint32_t send = odd ? CNRX_R(m + 1) : CNRX_R(32 + m);
+      for (int m = 0; m < 16; ++m) {
+        const uint32_t send = odd ? CNRX_R(m + 1) : CNRX_R(16 + m);
         const float recv = __uint_as_float(__shfl_xor_sync(0xffffffffu, send, 1));
-        const float mine = __uint_as_float(odd ? CNRX_R(33 + m) : CNRX_R(m));
+        const float mine = __uint_as_float(odd ? CNRX_R(17 + m) : CNRX_R(m));
         float v = mine + recv + bias;
         if (grp.relu) v = fmaxf(v, 0.f);
         const uint32_t h = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
@@ -313,7 +312,7 @@ __global__ void __launch_bounds__(320, 1) conv_ws64_kernel(const __grid_constant
       // 8x8 transpose (16-bit elements) inside each group of 8 lanes (lane bits 1..3), per block of 8 rows:
       // afterwards pk[4b .. 4b+3] of lane idx = channels c0..c0+7 of row rbase + 8b + idx.
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < 2; ++b) {
         uint32_t& r0 = pk[4 * b + 0];
         uint32_t& r1 = pk[4 * b + 1];
         uint32_t& r2 = pk[4 * b + 2];
@@ -344,11 +343,11 @@ __global__ void __launch_bounds__(320, 1) conv_ws64_kernel(const __grid_constant
       tr_comb += te2 - te1;
       // staging buffer free? (previous tile's TMA store has read it)
       if (lead) bulk_wait_read0();
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, 512;" ::: "memory");
       const long long te3 = clock64();
       tr_sw += te3 - te2;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < 2; ++b) {
         const uint32_t row = static_cast<uint32_t>(rbase + 8 * b + idx);  // 0..127 (127 is never stored)
         const bool valid = geo.valid(p0 + row);
         uint4 o = make_uint4(pk[4 * b], pk[4 * b + 1], pk[4 * b + 2], pk[4 * b + 3]);
@@ -379,7 +378,7 @@ __global__ void __launch_bounds__(320, 1) conv_ws64_kernel(const __grid_constant
       }
       tr_wr += clock64() - te3;
       fence_proxy_async_smem();
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, 512;" ::: "memory");
       if (lead) {
         tma_store_2d(&grp.out_map, stg, 0, static_cast<int32_t>(p0));
         if (has_out2) tma_store_2d(&grp.out2_map, stg + 128 * kRB, 0, static_cast<int32_t>(p0));
@@ -485,7 +484,7 @@ const char* conv_ws64_launch(const WsLaunch& L, int num_sms, cudaStream_t stream
   const int64_t work = static_cast<int64_t>(L.ngroups) * L.n_tiles;
   int grid = static_cast<int>(work < num_sms ? work : num_sms);
   if (grid < L.ngroups) grid = L.ngroups;
-  conv_ws64_kernel<<<grid, 320, lay.total, stream>>>(L);
+  conv_ws64_kernel<<<grid, 576, lay.total, stream>>>(L);
   CNRX_CUDA(cudaGetLastError());
   return "conv_ws64_kernel";
 }
