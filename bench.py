@@ -184,6 +184,7 @@ def main():
     ap.add_argument("--precision", default="")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling runs only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -278,16 +279,16 @@ def main():
     # ---------------- e2e leg: C-ABI host call, pinned host buffers ----------------
     y_host = torch.from_numpy(batch.y).pin_memory()
     out_host = torch.empty((B, link.T, link.F, nb), dtype=torch.float32).pin_memory()
-    for _ in range(max(2, args.warmup // 2)):
+    for _ in range(0 if args.no_e2e else max(2, args.warmup // 2)):
         plan.receive_host_ptr(y_host.data_ptr(), batch.y.shape, out_host.data_ptr())
-    e2e_steps = max(5, args.steps // 4)
+    e2e_steps = 0 if args.no_e2e else max(5, args.steps // 4)
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         plan.receive_host_ptr(y_host.data_ptr(), batch.y.shape, out_host.data_ptr())
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     barrier()
-    e2e_value = world * B * e2e_steps / e2e_s
+    e2e_value = world * B * e2e_steps / e2e_s if e2e_steps else None
     h2d = batch.y.nbytes
     d2h = out_host.numel() * 4
 

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -149,6 +150,7 @@ struct PwStep {
 
 struct Workspace {
   int B = -1, T = -1, F = -1;
+  int cap_B = 0;  // batch the buffers were allocated for
   PlaneGeom geo{};
   std::vector<void*> buffers;
   std::vector<size_t> sizes;
@@ -173,6 +175,8 @@ struct cnrx_plan {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host APIs
+  std::vector<cudaEvent_t> pipe_ev;            // [2 * chunks]: input landed / chunk computed
   std::vector<cnrx_node> nodes;
   int in_node = -1, out_node = -1;
   std::vector<HostParam> params;
@@ -827,19 +831,27 @@ struct Bf16Compiler {
 void ensure_workspace(cnrx_plan& p, int B, int T, int F) {
   Workspace& ws = p.ws;
   if (ws.B == B && ws.T == T && ws.F == F) return;
-  for (void* b : ws.buffers) cudaFree(b);
-  ws.buffers.clear();
-  ws.sizes.clear();
+  // A smaller batch of the same grid reuses the buffers (capacity cap_B): only the geometry and the
+  // launch descriptors change.  Every producer writes all rows of [0, Nalloc) (zeros on padding rows)
+  // and TMA zero-fills past the descriptor's Nalloc, so stale rows beyond it are never read.
+  const bool reuse = ws.T == T && ws.F == F && B <= ws.cap_B;
   ws.launches.clear();
   if (p.gexec) {
     cudaGraphExecDestroy(p.gexec);
     p.gexec = nullptr;
     p.gkey.clear();
   }
+  if (!reuse) {
+    for (void* b : ws.buffers) cudaFree(b);
+    ws.buffers.clear();
+    ws.sizes.clear();
+    ws.cap_B = B;
+  }
   ws.B = B;
   ws.T = T;
   ws.F = F;
   if (p.precision == CNRX_FP32) {
+    if (reuse) return;
     const int64_t rows = static_cast<int64_t>(B) * T * F;
     for (int c : p.f32_buf_channels) {
       void* d = nullptr;
@@ -849,13 +861,14 @@ void ensure_workspace(cnrx_plan& p, int B, int T, int F) {
     return;
   }
   ws.geo = make_geom(B, T, F, p.npad);
-  for (int c : p.buf_channels) {
-    void* d = nullptr;
-    const size_t bytes = static_cast<size_t>(ws.geo.Nalloc) * c * 2;
-    CNRX_CUDA(cudaMalloc(&d, bytes));
-    CNRX_CUDA(cudaMemset(d, 0, bytes));
-    ws.buffers.push_back(d);
-  }
+  if (!reuse)
+    for (int c : p.buf_channels) {
+      void* d = nullptr;
+      const size_t bytes = static_cast<size_t>(ws.geo.Nalloc) * c * 2;
+      CNRX_CUDA(cudaMalloc(&d, bytes));
+      CNRX_CUDA(cudaMemset(d, 0, bytes));
+      ws.buffers.push_back(d);
+    }
   // tensor maps / launch descriptors per TC group
   auto plane_ptr = [&](int pl) -> __nv_bfloat16* {
     return pl < 0 ? nullptr
@@ -1270,6 +1283,71 @@ struct DeviceGuard {
 
 }  // namespace
 
+namespace {
+
+// Host-buffer entry points: the slot batch is cut into chunks so that the host->device copy of chunk
+// k+1 and the device->host copy of chunk k-1 run on the copy engines while chunk k computes (full
+// overlap needs page-locked host buffers; pageable ones still give correct results).  Slots are
+// independent, so chunking changes nothing in the results.
+int pipeline_chunks(const cnrx_plan& p, int64_t B) {
+  if (p.capture) return 1;  // a captured graph is keyed on its pointers: keep one launch
+  if (const char* e = std::getenv("CNRX_PIPELINE_CHUNKS")) {
+    const int n = std::atoi(e);
+    if (n >= 1) return static_cast<int>(std::min<int64_t>(n, B));
+  }
+  return B >= 64 ? 8 : (B >= 8 ? 2 : 1);
+}
+
+template <class Run>
+void host_pipeline(cnrx_plan& p, const float* in, size_t in_per_slot, float* out, size_t out_per_slot, int64_t B,
+                   Run&& run) {
+  const size_t in_bytes = static_cast<size_t>(B) * in_per_slot;
+  const size_t out_bytes = static_cast<size_t>(B) * out_per_slot;
+  char* din = static_cast<char*>(ensure_dev(p.ws.in_buf, p.ws.in_bytes, in_bytes));
+  char* dout = static_cast<char*>(ensure_dev(p.ws.out_buf, p.ws.out_bytes, out_bytes));
+  const int n = pipeline_chunks(p, B);
+  if (n == 1) {
+    CNRX_CUDA(cudaMemcpyAsync(din, in, in_bytes, cudaMemcpyHostToDevice, p.stream));
+    run(reinterpret_cast<const float*>(din), B, reinterpret_cast<float*>(dout), p.stream);
+    CNRX_CUDA(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, p.stream));
+    CNRX_CUDA(cudaStreamSynchronize(p.stream));
+    return;
+  }
+  if (!p.h2d) {
+    CNRX_CUDA(cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking));
+    CNRX_CUDA(cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking));
+  }
+  while (p.pipe_ev.size() < static_cast<size_t>(2 * n)) {
+    cudaEvent_t e;
+    CNRX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p.pipe_ev.push_back(e);
+  }
+  // the previous call's work on the plan stream (and its buffers) is finished before we return, but
+  // order the copy streams after anything the caller queued on the plan stream anyway
+  CNRX_CUDA(cudaEventRecord(p.pipe_ev[0], p.stream));
+  CNRX_CUDA(cudaStreamWaitEvent(p.h2d, p.pipe_ev[0], 0));
+  const int64_t per = (B + n - 1) / n;
+  for (int k = 0; k < n; ++k) {
+    const int64_t b0 = k * per, nb = std::min(B, b0 + per) - b0;
+    if (nb <= 0) break;
+    cudaEvent_t landed = p.pipe_ev[static_cast<size_t>(2 * k)], done = p.pipe_ev[static_cast<size_t>(2 * k + 1)];
+    CNRX_CUDA(cudaMemcpyAsync(din + b0 * in_per_slot, reinterpret_cast<const char*>(in) + b0 * in_per_slot,
+                              static_cast<size_t>(nb) * in_per_slot, cudaMemcpyHostToDevice, p.h2d));
+    CNRX_CUDA(cudaEventRecord(landed, p.h2d));
+    CNRX_CUDA(cudaStreamWaitEvent(p.stream, landed, 0));
+    run(reinterpret_cast<const float*>(din + b0 * in_per_slot), nb, reinterpret_cast<float*>(dout + b0 * out_per_slot),
+        p.stream);
+    CNRX_CUDA(cudaEventRecord(done, p.stream));
+    CNRX_CUDA(cudaStreamWaitEvent(p.d2h, done, 0));
+    CNRX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(out) + b0 * out_per_slot, dout + b0 * out_per_slot,
+                              static_cast<size_t>(nb) * out_per_slot, cudaMemcpyDeviceToHost, p.d2h));
+  }
+  CNRX_CUDA(cudaStreamSynchronize(p.d2h));
+  CNRX_CUDA(cudaStreamSynchronize(p.stream));
+}
+
+}  // namespace
+
 // ================================================================================================
 // C ABI
 // ================================================================================================
@@ -1344,6 +1422,9 @@ void cnrx_plan_destroy(cnrx_plan* plan) {
   for (auto& evs : plan->prof_events)
     for (auto e : evs) cudaEventDestroy(e);
   for (auto e : plan->event_pool) cudaEventDestroy(e);
+  for (auto e : plan->pipe_ev) cudaEventDestroy(e);
+  if (plan->h2d) cudaStreamDestroy(plan->h2d);
+  if (plan->d2h) cudaStreamDestroy(plan->d2h);
   if (plan->stream) cudaStreamDestroy(plan->stream);
   if (prev >= 0) cudaSetDevice(prev);
   delete plan;
@@ -1374,14 +1455,11 @@ int cnrx_forward(cnrx_plan* plan, const float* x, int64_t B, int64_t T, int64_t 
     check_shape(*plan, B, T, F, C);
     require(x && out, "null tensor pointer");
     DeviceGuard dg(plan->device);
-    const size_t in_bytes = static_cast<size_t>(B * T * F * C) * sizeof(float);
-    const size_t out_bytes = static_cast<size_t>(B * T * F * plan->out_ch) * sizeof(float);
-    float* din = static_cast<float*>(ensure_dev(plan->ws.in_buf, plan->ws.in_bytes, in_bytes));
-    float* dout = static_cast<float*>(ensure_dev(plan->ws.out_buf, plan->ws.out_bytes, out_bytes));
-    CNRX_CUDA(cudaMemcpyAsync(din, x, in_bytes, cudaMemcpyHostToDevice, plan->stream));
-    run_forward(*plan, din, B, T, F, dout, 0, 0, plan->stream);
-    CNRX_CUDA(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, plan->stream));
-    CNRX_CUDA(cudaStreamSynchronize(plan->stream));
+    host_pipeline(*plan, x, static_cast<size_t>(T * F * C) * sizeof(float), out,
+                  static_cast<size_t>(T * F * plan->out_ch) * sizeof(float), B,
+                  [&](const float* xi, int64_t nb, float* yo, cudaStream_t s) {
+                    run_forward(*plan, xi, nb, T, F, yo, 0, 0, s);
+                  });
   });
 }
 
@@ -1428,14 +1506,11 @@ int cnrx_receive(cnrx_plan* plan, const float* y, int64_t B, int64_t T, int64_t 
     check_receive(*plan, B, T, F, N);
     require(y && llr, "null tensor pointer");
     DeviceGuard dg(plan->device);
-    const size_t in_bytes = static_cast<size_t>(B * T * F * N) * 2 * sizeof(float);
-    const size_t out_bytes = static_cast<size_t>(B * T * F * plan->out_ch) * sizeof(float);
-    float* din = static_cast<float*>(ensure_dev(plan->ws.in_buf, plan->ws.in_bytes, in_bytes));
-    float* dout = static_cast<float*>(ensure_dev(plan->ws.out_buf, plan->ws.out_bytes, out_bytes));
-    CNRX_CUDA(cudaMemcpyAsync(din, y, in_bytes, cudaMemcpyHostToDevice, plan->stream));
-    run_forward(*plan, din, B, T, F, dout, 1, static_cast<int>(N), plan->stream);
-    CNRX_CUDA(cudaMemcpyAsync(llr, dout, out_bytes, cudaMemcpyDeviceToHost, plan->stream));
-    CNRX_CUDA(cudaStreamSynchronize(plan->stream));
+    host_pipeline(*plan, y, static_cast<size_t>(T * F * N) * 2 * sizeof(float), llr,
+                  static_cast<size_t>(T * F * plan->out_ch) * sizeof(float), B,
+                  [&](const float* yi, int64_t nb, float* lo, cudaStream_t s) {
+                    run_forward(*plan, yi, nb, T, F, lo, 1, static_cast<int>(N), s);
+                  });
   });
 }
 

@@ -19,8 +19,8 @@
 // Warp roles (576 threads, persistent, 1 CTA/SM, TMEM: 224 weight/identity columns + 2 x 128 accumulator):
 //   warp 0     TMA producer: activation windows (4-stage ring) + residual tiles (2-deep ring)
 //   warp 1     TMEM allocator + MMA issuer
-//   warps 2-17 weights -> TMEM at start (2-5); epilogue: four warps per TMEM lane quadrant, each owning
-//              32 accumulator columns: TMEM -> registers, lane-pair shuffle combine,
+//   warps 2-17 weights -> TMEM at start (2-5); epilogue in two groups of eight warps, one per
+//              accumulator stage (alternate tiles): TMEM -> registers, lane-pair shuffle combine,
 //              bias / ReLU / validity, bf16 pack, 8x8 lane-butterfly transpose so every lane writes
 //              16-byte rows (8 channels of one plane row) to swizzled smem, TMA store of 127 rows.
 // The residual add is done by the tensor core: an identity A block (TMEM columns 192..223) times
@@ -60,8 +60,8 @@ __host__ __device__ inline WsLayout ws_layout(int stages, int win_alloc) {
   uint32_t off = s.win_stage * static_cast<uint32_t>(stages);
   s.res_off = off;                       // 2 x [128 rows][128 B]
   off += 2u * 128u * kRB;
-  s.stg_off = off;                       // [out | out2] x [128 rows][128 B]
-  off += 2u * 128u * kRB;
+  s.stg_off = off;                       // per epilogue group: [out | out2] x [128 rows][128 B]
+  off += 2u * 2u * 128u * kRB;
   s.par_off = off;                       // bias, s2, t2
   off += 3u * kC * 4u;
   s.bar_off = off;
@@ -71,6 +71,12 @@ __host__ __device__ inline WsLayout ws_layout(int stages, int win_alloc) {
 
 __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t byte_in_row) {
   return row * 128u + ((((byte_in_row >> 4) ^ (row & 7u)) << 4) | (byte_in_row & 15u));
+}
+
+// named barrier of one 256-thread epilogue group (constant ids: a register id makes ptxas reserve all 16)
+__device__ __forceinline__ void epi_group_sync(int e) {
+  if (e == 0) asm volatile("bar.sync 1, 256;" ::: "memory");
+  else asm volatile("bar.sync 2, 256;" ::: "memory");
 }
 
 __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant__ WsLaunch L) {
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 16);
+      mbar_init(&tempty[a], 8);
       mbar_init(&rfull[a], 1);
       mbar_init(&rempty[a], 1);
     }
@@ -257,66 +263,74 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
     }
   } else {
     // ------------------------------ epilogue (warps 2..17) --------------------
+    // Two groups of eight warps, group e owning accumulator stage e (tiles j with j % 2 == e), so one
+    // group's TMEM reads overlap the other group's shared-memory writes and TMA stores.  In a group,
+    // warp (q, H) covers TMEM lane quadrant q and accumulator columns [64H, 64H + 64) as two 32-column
+    // chunks.
+    const int e = (warp - 2) >> 3;     // epilogue group == accumulator stage
     const int q = warp & 3;            // TMEM lane quadrant
-    const int H = (warp - 2) >> 2;     // column quarter: accumulator columns [32H, 32H + 32)
-    const int cb = 32 * H;
+    const int H = ((warp - 2) >> 2) & 1;
     const int Ln = q * 32 + lane;      // accumulator lane
     const int co = Ln >> 1;            // output channel of this lane
     const bool odd = (lane & 1) != 0;  // B-half lane
     const int idx = (lane >> 1) & 7;   // position in the 8-lane transpose group (same parity, same half-warp)
     const int c0 = q * 16 + (lane >> 4) * 8;  // first of the 8 channels this lane writes after the transpose
-    const int rbase = cb + (odd ? 16 : 0);    // this lane finalises rows rbase .. rbase + 15
     const PlaneGeom geo = L.geo;
-    uint8_t* stg = smem + lay.stg_off;
+    uint8_t* stg = smem + lay.stg_off + e * 2 * 128 * kRB;
     const float bias = s_bias[co];
     const bool relu2_only = grp.s2 == nullptr;
-    const bool lead = threadIdx.x == 64;
+    const bool lead = ((warp - 2) & 7) == 0 && lane == 0;
     long long tr_ew = 0, tr_comb = 0, tr_sw = 0, tr_wr = 0;
-    int j = 0;
-    for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
-      const int a = j & 1;
+    int j = e;
+    for (int64_t tile = local + static_cast<int64_t>(e) * nct; tile < n_tiles; tile += 2 * static_cast<int64_t>(nct), j += 2) {
       const int64_t p0 = tile * kTileRows;
       const long long te0 = clock64();
-      mbar_wait(&tfull[a], static_cast<uint32_t>(j >> 1) & 1u);
+      mbar_wait(&tfull[e], static_cast<uint32_t>(j >> 1) & 1u);
       const long long te1 = clock64();
       tr_ew += te1 - te0;
       tc_fence_after();
-      uint32_t ra[32], rx[1];  // accumulator columns cb..cb+31, cb+32
-      const uint32_t taddr = tbase + kAcc0 + static_cast<uint32_t>(a * kN + cb) + (static_cast<uint32_t>(q * 32) << 16);
-      tmem_ld32(taddr, ra);
-      if (H < 3) {
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(rx[0]) : "r"(taddr + 32) : "memory");
-      } else {
-        rx[0] = 0;
-      }
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[a]);
-#define CNRX_R(i) ((i) < 32 ? ra[(i)] : rx[0])
-      // row cb + k = A[k] + B[k+1]: even lanes finalise k in [0,16), odd lanes k in [16,32).
-      // pk[i] packs rows (2i, 2i+1) of this lane's 16 rows, channel co.
-      uint32_t pk[8];
+      // chunk h (accumulator columns 64H + 32h .. +31, plus the next column): row 64H + 32h + k is
+      // A[k] + B[k+1]; even lanes finalise k in [0,16), odd lanes k in [16,32).  pk[h][i] packs rows
+      // (2i, 2i+1) of this lane's 16 rows, channel co.  The stage is released after the second load.
+      const uint32_t taddr = tbase + kAcc0 + static_cast<uint32_t>(e * kN + 64 * H) + (static_cast<uint32_t>(q * 32) << 16);
+      uint32_t pk[2][8];
 #pragma unroll
-      for (int m = 0; m < 16; ++m) {
-        const uint32_t send = odd ? CNRX_R(m + 1) : CNRX_R(16 + m);
-        const float recv = __uint_as_float(__shfl_xor_sync(0xffffffffu, send, 1));
-        const float mine = __uint_as_float(odd ? CNRX_R(17 + m) : CNRX_R(m));
-        float v = mine + recv + bias;
-        if (grp.relu) v = fmaxf(v, 0.f);
-        const uint32_t h = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
-        if ((m & 1) == 0) pk[m >> 1] = h;
-        else pk[m >> 1] |= h << 16;
-      }
+      for (int h = 0; h < 2; ++h) {
+        uint32_t ra[32], rx[1];
+        tmem_ld32(taddr + 32 * h, ra);
+        if (H == 0 || h == 0) {
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(rx[0]) : "r"(taddr + 32 * h + 32) : "memory");
+        } else {
+          rx[0] = 0;
+        }
+        tmem_ld_wait();
+        if (h == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[e]);
+        }
+#define CNRX_R(i) ((i) < 32 ? ra[(i) & 31] : rx[0])
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          const uint32_t send = odd ? CNRX_R(m + 1) : CNRX_R(16 + m);
+          const float recv = __uint_as_float(__shfl_xor_sync(0xffffffffu, send, 1));
+          const float mine = __uint_as_float(odd ? CNRX_R(17 + m) : CNRX_R(m));
+          float v = mine + recv + bias;
+          if (grp.relu) v = fmaxf(v, 0.f);
+          const uint32_t hv = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
+          if ((m & 1) == 0) pk[h][m >> 1] = hv;
+          else pk[h][m >> 1] |= hv << 16;
+        }
 #undef CNRX_R
+      }
       // 8x8 transpose (16-bit elements) inside each group of 8 lanes (lane bits 1..3), per block of 8 rows:
-      // afterwards pk[4b .. 4b+3] of lane idx = channels c0..c0+7 of row rbase + 8b + idx.
+      // afterwards pk[h][4b .. 4b+3] of lane idx = channels c0..c0+7 of row 64H + 32h + (odd ? 16 : 0) + 8b + idx.
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        uint32_t& r0 = pk[4 * b + 0];
-        uint32_t& r1 = pk[4 * b + 1];
-        uint32_t& r2 = pk[4 * b + 2];
-        uint32_t& r3 = pk[4 * b + 3];
+      for (int hb = 0; hb < 4; ++hb) {
+        uint32_t& r0 = pk[hb >> 1][4 * (hb & 1) + 0];
+        uint32_t& r1 = pk[hb >> 1][4 * (hb & 1) + 1];
+        uint32_t& r2 = pk[hb >> 1][4 * (hb & 1) + 2];
+        uint32_t& r3 = pk[hb >> 1][4 * (hb & 1) + 3];
         {  // level 1: swap off-diagonal 4x4 blocks between idx and idx^4
           const bool lo = (idx & 4) == 0;
           const uint32_t s0 = lo ? r2 : r0, s1 = lo ? r3 : r1;
@@ -341,16 +355,17 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
       }
       const long long te2 = clock64();
       tr_comb += te2 - te1;
-      // staging buffer free? (previous tile's TMA store has read it)
+      // staging buffer free? (this group's previous TMA store has read it)
       if (lead) bulk_wait_read0();
-      asm volatile("bar.sync 1, 512;" ::: "memory");
+      epi_group_sync(e);
       const long long te3 = clock64();
       tr_sw += te3 - te2;
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const uint32_t row = static_cast<uint32_t>(rbase + 8 * b + idx);  // 0..127 (127 is never stored)
-        const bool valid = geo.valid(p0 + row);
-        uint4 o = make_uint4(pk[4 * b], pk[4 * b + 1], pk[4 * b + 2], pk[4 * b + 3]);
+      for (int hb = 0; hb < 4; ++hb) {
+        const uint32_t row = static_cast<uint32_t>(64 * H + 32 * (hb >> 1) + (odd ? 16 : 0) + 8 * (hb & 1) + idx);
+        const bool valid = geo.valid(p0 + row);  // row 127 is never stored
+        const uint32_t* pr = &pk[hb >> 1][4 * (hb & 1)];
+        uint4 o = make_uint4(pr[0], pr[1], pr[2], pr[3]);
         if (!valid) o = make_uint4(0, 0, 0, 0);
         const uint32_t off = row * 128u + (((static_cast<uint32_t>(c0 >> 3)) ^ (row & 7u)) << 4);
         *reinterpret_cast<uint4*>(stg + off) = o;
@@ -378,7 +393,7 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
       }
       tr_wr += clock64() - te3;
       fence_proxy_async_smem();
-      asm volatile("bar.sync 1, 512;" ::: "memory");
+      epi_group_sync(e);
       if (lead) {
         tma_store_2d(&grp.out_map, stg, 0, static_cast<int32_t>(p0));
         if (has_out2) tma_store_2d(&grp.out2_map, stg + 128 * kRB, 0, static_cast<int32_t>(p0));
@@ -386,7 +401,7 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
       }
     }
     if (lead) bulk_wait0();
-    if (L.trace && lead) {
+    if (L.trace && lead && e == 0) {
       atomicAdd(&L.trace[kTraceEpiWaitFull], static_cast<unsigned long long>(tr_ew));
       atomicAdd(&L.trace[kWsTraceCombine], static_cast<unsigned long long>(tr_comb));
       atomicAdd(&L.trace[kWsTraceStageWait], static_cast<unsigned long long>(tr_sw));
@@ -485,7 +500,15 @@ const char* conv_ws64_launch(const WsLaunch& L, int num_sms, cudaStream_t stream
   int grid = static_cast<int>(work < num_sms ? work : num_sms);
   if (grid < L.ngroups) grid = L.ngroups;
   conv_ws64_kernel<<<grid, 576, lay.total, stream>>>(L);
-  CNRX_CUDA(cudaGetLastError());
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, conv_ws64_kernel);
+    throw Error(4, std::string("conv_ws64 launch failed: ") + cudaGetErrorString(err) + " (regs " +
+                       std::to_string(fa.numRegs) + ", max threads " + std::to_string(fa.maxThreadsPerBlock) +
+                       ", static smem " + std::to_string(fa.sharedSizeBytes) + ", dynamic " +
+                       std::to_string(lay.total) + ")");
+  }
   return "conv_ws64_kernel";
 }
 
