@@ -933,9 +933,15 @@ void ensure_workspace(cnrx_plan& p, int B, int T, int F) {
           g.relu = op.relu;
         }
         L.win_alloc = win_alloc;
+        for (size_t gi = 0; gi < grp.size(); ++gi) {
+          const TcOp& op = p.tc[static_cast<size_t>(grp[gi])];
+          if (op.res_plane >= 0) L.flags |= 1;
+          if (op.out2_plane >= 0) L.flags |= 2;
+        }
         int stages = 4;
-        while (stages > 1 && conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc) > 227 * 1024) --stages;
-        if (conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc) > 227 * 1024)
+        while (stages > 1 && conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc, L.flags) > 227 * 1024)
+          --stages;
+        if (conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc, L.flags) > 227 * 1024)
           throw Error(CNRX_ERR_UNSUPPORTED, "tcgen05 conv working set exceeds shared memory");
         L.stages = stages;
       }
@@ -990,6 +996,12 @@ void run_f32(cnrx_plan& p, const float* x, float* out, cudaStream_t s) {
 }
 
 // input_kind: 0 = features [B,T,F,C] fp32, 1 = received grid y [B,T,F,N] complex
+void trace_window(const unsigned long long* h) {
+  const double span_us = (h[14] - ~h[13]) * 1e-3;
+  const double mhz = h[15] ? static_cast<double>(h[kTraceTotal]) / static_cast<double>(h[15]) * 1e3 : 0.0;
+  fprintf(stderr, "[trace]   CTAs %llu, MMA-loop span %.1f us, effective SM clock %.0f MHz\n", h[12], span_us, mhz);
+}
+
 void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, cudaStream_t s) {
   Workspace& ws = p.ws;
   auto plane_ptr = [&](int pl) {
@@ -1060,17 +1072,18 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
                   h[kTraceTiles], h[kTraceProdWaitEmpty] / nt, h[kTraceMmaWaitFull] / nt, h[kTraceMmaWaitTmem] / nt,
                   h[kTraceMmaIssue] / nt, h[kTraceEpiWaitFull] / nt, h[kWsTraceCombine] / nt,
                   h[kWsTraceStageWait] / nt, h[kWsTraceWrite] / nt, h[kTraceTotal] / nt);
+          trace_window(h);
         }
         continue;
       }
       if (trace) {
         if (!dtrace) CNRX_CUDA(cudaMalloc(&dtrace, 16 * sizeof(unsigned long long)));
-        CNRX_CUDA(cudaMemsetAsync(dtrace, 0, kTraceN * sizeof(unsigned long long), s));
+        CNRX_CUDA(cudaMemsetAsync(dtrace, 0, 16 * sizeof(unsigned long long), s));
         GL.tc.trace = dtrace;
       }
       p.note(conv_tc_launch(op0.cin, op0.cout, op0.ks, GL.tc, p.num_sms, s), s, fl);
       if (trace) {
-        unsigned long long h[kTraceN];
+        unsigned long long h[16];
         CNRX_CUDA(cudaMemcpyAsync(h, dtrace, sizeof h, cudaMemcpyDeviceToHost, s));
         CNRX_CUDA(cudaStreamSynchronize(s));
         const double nct = static_cast<double>(h[kTraceTiles] ? h[kTraceTiles] : 1);
@@ -1080,6 +1093,7 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
                 p.launch_names.back().c_str(), h[kTraceTiles], h[kTraceProdWaitEmpty] / nct,
                 h[kTraceMmaWaitFull] / nct, h[kTraceMmaWaitTmem] / nct, h[kTraceMmaIssue] / nct,
                 h[kTraceEpiWaitFull] / nct, h[kTraceEpiWork] / nct, h[kTraceTotal] / nct);
+        trace_window(h);
       }
     }
     for (int k : p.pw_by_level[static_cast<size_t>(lv)]) {

@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -56,7 +58,8 @@ struct SmemLayout {
   uint32_t res_off, stg_off, par_off, bar_off, total;
 };
 __host__ __device__ constexpr bool staged_epi(int cin, int cout) { return cin <= 64 && cout <= 64; }
-__host__ __device__ inline SmemLayout smem_layout(int cin, int cout, int ks, int stages, int win_alloc) {
+// flags: bit 0 = some group has a residual, bit 1 = some group writes a second output
+__host__ __device__ inline SmemLayout smem_layout(int cin, int cout, int ks, int stages, int win_alloc, int flags) {
   SmemLayout s{};
   const uint32_t wbytes = static_cast<uint32_t>(ks * ks * cout * cin * 2);
   s.w_off = 0;
@@ -68,7 +71,7 @@ __host__ __device__ inline SmemLayout smem_layout(int cin, int cout, int ks, int
   uint32_t off = s.win_off + static_cast<uint32_t>(stages) * s.win_stage_bytes;
   if (staged_epi(cin, cout)) {
     s.res_off = off;                                   // 2 x [128 rows][cout] residual tiles
-    off += 2u * 128u * static_cast<uint32_t>(cout) * 2u;
+    if (flags & 1) off += 2u * 128u * static_cast<uint32_t>(cout) * 2u;
     s.stg_off = off;                                   // 4 warps x 2 outputs x [32 rows][cout]
     off += 4u * 2u * 32u * static_cast<uint32_t>(cout) * 2u;
   }
@@ -79,8 +82,12 @@ __host__ __device__ inline SmemLayout smem_layout(int cin, int cout, int ks, int
   return s;
 }
 
+// 1x1 convs with few input channels (the stem) are epilogue-latency bound: let three CTAs share an SM.
 template <int CIN, int COUT, int KS>
-__global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__ TcLaunch L) {
+constexpr int min_ctas() { return KS == 1 && CIN <= 32 && COUT <= 64 ? 3 : 1; }
+
+template <int CIN, int COUT, int KS>
+__global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel(const __grid_constant__ TcLaunch L) {
   constexpr int CH0 = chunk0_ch(CIN), CH1 = chunk1_ch(CIN);
   constexpr int RB0 = CH0 * 2, RB1 = CH1 * 2;
   constexpr uint32_t SW0 = swz_of_rowbytes(RB0), SW1 = swz_of_rowbytes(RB1);
@@ -93,7 +100,7 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
 
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  const SmemLayout lay = smem_layout(CIN, COUT, KS, L.stages, L.win_alloc);
+  const SmemLayout lay = smem_layout(CIN, COUT, KS, L.stages, L.win_alloc, L.flags);
   uint8_t* sW = smem + lay.w_off;
   float* s_bias = reinterpret_cast<float*>(smem + lay.par_off);
   float* s_s2 = s_bias + COUT;
@@ -186,6 +193,7 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
     if (lane == 0) {
       long long tr_full = 0, tr_tmem = 0, tr_issue = 0;
       const long long t_start = clock64();
+    const unsigned long long g_start = globaltimer_ns();
       mbar_wait(w_full, 0);
       tc_fence_after();
       const uint32_t sW_addr = smem_u32(sW);
@@ -237,6 +245,7 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
       }
       if (L.trace) {
         atomicAdd(&L.trace[kTraceTotal], static_cast<unsigned long long>(clock64() - t_start));
+      trace_cta_window(L.trace, g_start);
         atomicAdd(&L.trace[kTraceMmaWaitFull], static_cast<unsigned long long>(tr_full));
         atomicAdd(&L.trace[kTraceMmaWaitTmem], static_cast<unsigned long long>(tr_tmem));
         atomicAdd(&L.trace[kTraceMmaIssue], static_cast<unsigned long long>(tr_issue));
@@ -415,15 +424,34 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(const __grid_constant__
 template <int CIN, int COUT, int KS>
 const char* launch_t(const TcLaunch& L, int num_sms, cudaStream_t stream) {
   auto kern = conv_tc_kernel<CIN, COUT, KS>;
-  const SmemLayout lay = smem_layout(CIN, COUT, KS, L.stages, L.win_alloc);
+  const SmemLayout lay = smem_layout(CIN, COUT, KS, L.stages, L.win_alloc, L.flags);
   static thread_local int configured_bytes = -1;
   if (configured_bytes < static_cast<int>(lay.total)) {
     CNRX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lay.total)));
+    CNRX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     configured_bytes = static_cast<int>(lay.total);
   }
+  // Several CTAs per SM when shared memory and TMEM allow (small-K convs, e.g. the 1x1 stem, are
+  // bound by their epilogue; more resident epilogue warps hide its latency chains).
+  // (the occupancy API under-reports here, so count registers / shared memory / TMEM directly)
+  static thread_local int regs = -1;
+  if (regs < 0) {
+    cudaFuncAttributes fa{};
+    CNRX_CUDA(cudaFuncGetAttributes(&fa, kern));
+    regs = fa.numRegs;
+  }
+  const int by_regs = 65536 / (192 * ((regs + 7) / 8 * 8));
+  const int by_smem = static_cast<int>((228u * 1024u) / (lay.total + 2048u));
+  const int by_tmem = static_cast<int>(512 / tmem_cols_for(COUT));
+  int per_sm = by_regs < by_smem ? by_regs : by_smem;
+  if (per_sm > by_tmem) per_sm = by_tmem;
+  if (per_sm > min_ctas<CIN, COUT, KS>()) per_sm = min_ctas<CIN, COUT, KS>();
+  if (per_sm < 1) per_sm = 1;
   const int64_t work = static_cast<int64_t>(L.ngroups) * L.geo.n_tiles;
-  int grid = static_cast<int>(work < num_sms ? work : num_sms);
+  const int64_t slots = static_cast<int64_t>(num_sms) * per_sm;
+  int grid = static_cast<int>(work < slots ? work : slots);
   if (grid < L.ngroups) grid = L.ngroups;
+  if (L.trace) fprintf(stderr, "[trace] conv_tc %d CTAs/SM (regs %d, smem %u B), grid %d\n", per_sm, regs, lay.total, grid);
   kern<<<grid, 192, lay.total, stream>>>(L);
   CNRX_CUDA(cudaGetLastError());
   static char name[96];
@@ -483,8 +511,8 @@ void conv_tc_make_row_map(const void* plane, int64_t nalloc, int c, CUtensorMap*
   if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
-size_t conv_tc_smem_bytes(int cin, int cout, int ks, int stages, int win_alloc) {
-  return smem_layout(cin, cout, ks, stages, win_alloc).total;
+size_t conv_tc_smem_bytes(int cin, int cout, int ks, int stages, int win_alloc, int flags) {
+  return smem_layout(cin, cout, ks, stages, win_alloc, flags).total;
 }
 
 size_t conv_tc_wimg_bytes(int cin, int cout, int ks) { return static_cast<size_t>(ks) * ks * cout * cin * 2; }

@@ -34,7 +34,7 @@ struct TcLaunch {
   int32_t ngroups;
   int32_t stages;                   // window pipeline depth
   int32_t win_alloc;                // rows allocated per window stage (max over groups, 8-aligned)
-  int32_t pad_;
+  int32_t flags;                    // bit 0: a group has a residual, bit 1: a group writes out2
   // debug: when non-null each CTA adds per-role clock64 totals (see kTrace* indices)
   unsigned long long* trace;
 };
@@ -42,7 +42,7 @@ enum : int { kTraceProdWaitEmpty = 0, kTraceMmaWaitFull, kTraceMmaWaitTmem, kTra
              kTraceEpiWork, kTraceTiles, kTraceTotal, kTraceN };
 
 // Shared memory the kernel needs for (cin, cout, ks) with `stages` window stages of `win_alloc` rows.
-size_t conv_tc_smem_bytes(int cin, int cout, int ks, int stages, int win_alloc);
+size_t conv_tc_smem_bytes(int cin, int cout, int ks, int stages, int win_alloc, int flags);
 bool conv_tc_supported(int cin, int cout, int ks);
 // Enqueue one grouped launch; grid = min(#SMs, ngroups * tiles).  Returns the kernel name.
 const char* conv_tc_launch(int cin, int cout, int ks, const TcLaunch& L, int num_sms, cudaStream_t stream);

@@ -16,15 +16,17 @@
 // q in [p0, p0+127) is A[q-p0] + B[q-p0+1].  Pairs: (dt=-1,0) for df in {-1,0,1} and (dt=+1, zero) for
 // df in {-1,0,1} -> 6 UMMAs per 16-channel K step, 24 per tile, 75% of the issued MACs useful.
 //
-// Warp roles (576 threads, persistent, 1 CTA/SM, TMEM: 224 weight/identity columns + 2 x 128 accumulator):
-//   warp 0     TMA producer: activation windows (4-stage ring) + residual tiles (2-deep ring)
+// Warp roles (576 threads, persistent, 1 CTA/SM, TMEM: 192 weight columns + 2 x 128 accumulator):
+//   warp 0     TMA producer: activation windows (4-stage ring); residual tiles are streamed by the
+//              epilogue group that consumes them
 //   warp 1     TMEM allocator + MMA issuer
 //   warps 2-17 weights -> TMEM at start (2-5); epilogue in two groups of eight warps, one per
 //              accumulator stage (alternate tiles): TMEM -> registers, lane-pair shuffle combine,
 //              bias / ReLU / validity, bf16 pack, 8x8 lane-butterfly transpose so every lane writes
 //              16-byte rows (8 channels of one plane row) to swizzled smem, TMA store of 127 rows.
-// The residual add is done by the tensor core: an identity A block (TMEM columns 192..223) times
-// the TMA-loaded residual tile accumulates R[p][c] into lane 2c, so the epilogue never reads it.
+// With a residual the epilogue transposes the combined fp32 values (8x8 lane butterflies) so each
+// lane holds 8 channels of one row, adds the TMA-staged residual row chunk with one 16-byte shared
+// load, then rounds to bf16 (fp32 conv + bias + residual, a single rounding as the reference).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -46,7 +48,6 @@ constexpr int kN = 128;           // UMMA N (plane rows per instruction)
 constexpr int kPairs = 6;
 constexpr int kKSteps = kC / 16;  // 4
 constexpr int kWCols = kPairs * kKSteps * 8;  // 192 TMEM columns of weights
-constexpr int kIdCol = kWCols;                // identity block for the residual: 4 K steps x 8 columns
 constexpr int kAcc0 = 256;        // accumulator columns [256,384) and [384,512)
 constexpr int kBox = 32;
 
@@ -58,8 +59,8 @@ __host__ __device__ inline WsLayout ws_layout(int stages, int win_alloc) {
   s.win_off = 0;
   s.win_stage = static_cast<uint32_t>(win_alloc * kRB);  // multiple of 4 KB (32-row boxes)
   uint32_t off = s.win_stage * static_cast<uint32_t>(stages);
-  s.res_off = off;                       // 2 x [128 rows][128 B]
-  off += 2u * 128u * kRB;
+  s.res_off = off;                       // 2 groups x 2 buffers x [128 rows][128 B]
+  off += 4u * 128u * kRB;
   s.stg_off = off;                       // per epilogue group: [out | out2] x [128 rows][128 B]
   off += 2u * 2u * 128u * kRB;
   s.par_off = off;                       // bias, s2, t2
@@ -92,9 +93,8 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
   uint64_t* empty = full + L.stages;      // [stages]
   uint64_t* tfull = empty + L.stages;     // [2]
   uint64_t* tempty = tfull + 2;           // [2]
-  uint64_t* rfull = tempty + 2;           // [2]
-  uint64_t* rempty = rfull + 2;           // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 2);
+  uint64_t* rfull = tempty + 2;           // [2 groups][2 buffers] residual tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 4);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -115,8 +115,8 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);
-      mbar_init(&rfull[a], 1);
-      mbar_init(&rempty[a], 1);
+      mbar_init(&rfull[2 * a], 1);
+      mbar_init(&rfull[2 * a + 1], 1);
     }
     fence_barrier_init();
   }
@@ -146,22 +146,6 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
       r[4] = v1.x; r[5] = v1.y; r[6] = v1.z; r[7] = v1.w;
       tmem_st8(tbase + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * 8), r);
     }
-    // identity (residual) block: lane 2c has a 1.0 at K index c
-    const int Ln = q * 32 + lane;
-#pragma unroll 1
-    for (int kk = 0; kk < kKSteps; ++kk) {
-      uint32_t r[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) r[e] = 0;
-      if ((Ln & 1) == 0) {
-        const int c = Ln >> 1;
-        if (c / 16 == kk) {
-          const int k = c % 16;
-          r[k / 2] = 0x3F80u << ((k & 1) * 16);  // bf16 1.0
-        }
-      }
-      tmem_st8(tbase + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kIdCol + kk * 8), r);
-    }
     tmem_st_wait();
   }
   tc_fence_before();
@@ -188,16 +172,6 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
         const int32_t r0 = static_cast<int32_t>(p0 - grp.halo);
         for (int bx = 0; bx < nboxes; ++bx)
           tma_load_2d(win + bx * kBox * kRB, &grp.in_map, &full[s], 0, r0 + bx * kBox);
-        if (has_res) {
-          const int a = j & 1;
-          const long long tp1 = L.trace ? clock64() : 0;
-          mbar_wait(&rempty[a], (static_cast<uint32_t>(j >> 1) & 1u) ^ 1u);
-          if (L.trace) tr_prod += clock64() - tp1;
-          mbar_arrive_expect_tx(&rfull[a], 128u * kRB);
-          uint8_t* rb = smem + lay.res_off + a * 128 * kRB;
-          for (int bx = 0; bx < 4; ++bx)
-            tma_load_2d(rb + bx * kBox * kRB, &grp.res_map, &rfull[a], 0, static_cast<int32_t>(p0 + bx * kBox));
-        }
       }
       if (L.trace) atomicAdd(&L.trace[kTraceProdWaitEmpty], static_cast<unsigned long long>(tr_prod));
     }
@@ -213,6 +187,7 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
     }
     long long tr_full = 0, tr_tmem = 0, tr_issue = 0;
     const long long t_start = clock64();
+    const unsigned long long g_start = globaltimer_ns();
     int j = 0;
     for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
       const int s = j % L.stages;
@@ -238,16 +213,6 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
                          (p | kk) != 0 ? 1u : 0u);
           }
         }
-        if (has_res) {
-          mbar_wait(&rfull[a], static_cast<uint32_t>(j >> 1) & 1u);
-          tc_fence_after();
-          const uint64_t rdesc0 = make_sdesc(smem_u32(smem + lay.res_off + a * 128 * kRB), 8 * kRB, kSwizzle128, 0);
-#pragma unroll
-          for (int kk = 0; kk < kKSteps; ++kk)
-            umma_bf16_ts(d_tmem, tbase + static_cast<uint32_t>(kIdCol + kk * 8),
-                         rdesc0 + static_cast<uint64_t>((kk * 32) >> 4), IDESC, 1u);
-          umma_commit(&rempty[a]);
-        }
         umma_commit(&empty[s]);
         umma_commit(&tfull[a]);
       }
@@ -256,6 +221,7 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
     }
     if (L.trace && lane == 0) {
       atomicAdd(&L.trace[kTraceTotal], static_cast<unsigned long long>(clock64() - t_start));
+      trace_cta_window(L.trace, g_start);
       atomicAdd(&L.trace[kTraceMmaWaitFull], static_cast<unsigned long long>(tr_full));
       atomicAdd(&L.trace[kTraceMmaWaitTmem], static_cast<unsigned long long>(tr_tmem));
       atomicAdd(&L.trace[kTraceMmaIssue], static_cast<unsigned long long>(tr_issue));
@@ -268,19 +234,43 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
     // warp (q, H) covers TMEM lane quadrant q and accumulator columns [64H, 64H + 64) as two 32-column
     // chunks.
     const int e = (warp - 2) >> 3;     // epilogue group == accumulator stage
-    const int q = warp & 3;            // TMEM lane quadrant
+    const int q = warp & 3;            // TMEM lane quadrant: channels 16q .. 16q+15 (two 16-lane blocks)
     const int H = ((warp - 2) >> 2) & 1;
-    const int Ln = q * 32 + lane;      // accumulator lane
-    const int co = Ln >> 1;            // output channel of this lane
-    const bool odd = (lane & 1) != 0;  // B-half lane
-    const int idx = (lane >> 1) & 7;   // position in the 8-lane transpose group (same parity, same half-warp)
-    const int c0 = q * 16 + (lane >> 4) * 8;  // first of the 8 channels this lane writes after the transpose
+    const int t0 = lane & 3;           // column pair within an 8-column group
+    const int ci = lane >> 2;          // channel within a 16-lane block
     const PlaneGeom geo = L.geo;
     uint8_t* stg = smem + lay.stg_off + e * 2 * 128 * kRB;
-    const float bias = s_bias[co];
+    const uint32_t stg_a = smem_u32(stg);
+    float bias[2], s2v[2], t2v[2];
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      const int ch = 16 * q + 8 * blk + ci;
+      bias[blk] = s_bias[ch];
+      s2v[blk] = s_s2[ch];
+      t2v[blk] = s_t2[ch];
+    }
     const bool relu2_only = grp.s2 == nullptr;
     const bool lead = ((warp - 2) & 7) == 0 && lane == 0;
+    // ldmatrix / stmatrix row addresses: thread a -> matrix a/8 (8-row group), row a%8
+    const int arow = ((lane >> 3) << 3) + (lane & 7);
     long long tr_ew = 0, tr_comb = 0, tr_sw = 0, tr_wr = 0;
+    // The group's lead thread streams its own residual tiles through two buffers: the load for the
+    // group's tile k+2 is issued once every warp of the group has read tile k's, two group tiles
+    // (four tile periods) ahead of its use.
+    uint8_t* rbuf0 = smem + lay.res_off + e * 2 * 128 * kRB;
+    auto load_res = [&](int64_t t, int b) {
+      uint8_t* dst = rbuf0 + b * 128 * kRB;
+      mbar_arrive_expect_tx(&rfull[2 * e + b], 128u * kRB);
+      for (int bx = 0; bx < 4; ++bx)
+        tma_load_2d(dst + bx * kBox * kRB, &grp.res_map, &rfull[2 * e + b], 0, static_cast<int32_t>(t * kTileRows + bx * kBox));
+    };
+    const int64_t gstride = 2 * static_cast<int64_t>(nct);
+    if (has_res && lead) {
+      prefetch_tmap(&grp.res_map);
+      const int64_t t0_ = local + static_cast<int64_t>(e) * nct;
+      if (t0_ < n_tiles) load_res(t0_, 0);
+      if (t0_ + gstride < n_tiles) load_res(t0_ + gstride, 1);
+    }
     int j = e;
     for (int64_t tile = local + static_cast<int64_t>(e) * nct; tile < n_tiles; tile += 2 * static_cast<int64_t>(nct), j += 2) {
       const int64_t p0 = tile * kTileRows;
@@ -288,20 +278,32 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
       mbar_wait(&tfull[e], static_cast<uint32_t>(j >> 1) & 1u);
       const long long te1 = clock64();
       tr_ew += te1 - te0;
+      // staging buffer free? (this group's previous TMA store has read it)
+      if (lead) bulk_wait_read0();
+      epi_group_sync(e);
+      const int kb = (j >> 1) & 1;  // residual buffer of this group tile
+      if (has_res) mbar_wait(&rfull[2 * e + kb], static_cast<uint32_t>(j >> 2) & 1u);
+      const uint32_t rbuf_a = smem_u32(rbuf0 + kb * 128 * kRB);
+      const long long te2 = clock64();
+      tr_sw += te2 - te1;
       tc_fence_after();
-      // chunk h (accumulator columns 64H + 32h .. +31, plus the next column): row 64H + 32h + k is
-      // A[k] + B[k+1]; even lanes finalise k in [0,16), odd lanes k in [16,32).  pk[h][i] packs rows
-      // (2i, 2i+1) of this lane's 16 rows, channel co.  The stage is released after the second load.
-      const uint32_t taddr = tbase + kAcc0 + static_cast<uint32_t>(e * kN + 64 * H) + (static_cast<uint32_t>(q * 32) << 16);
-      uint32_t pk[2][8];
+      // Chunk h = accumulator columns c = 64H + 32h + [0, 32).  Lanes 16k + i / 16k + 8 + i hold the
+      // A / B tap partial sums of channel 8k + i, so output row c = A[c] + B[c+1] needs one shuffle
+      // for odd c (B[c+1] sits with the neighbouring column pair) and none for even c.
+      // validity of this warp's 64 rows (padding rows are stored as zeros): one bit per row
+      uint32_t vmask[2];
+#pragma unroll
+      for (int w = 0; w < 2; ++w) vmask[w] = __ballot_sync(0xffffffffu, geo.valid(p0 + 64 * H + 32 * w + lane));
+      const uint32_t tq = tbase + kAcc0 + static_cast<uint32_t>(e * kN + 64 * H) + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        uint32_t ra[32], rx[1];
-        tmem_ld32(taddr + 32 * h, ra);
+        uint32_t a0[16], a1[16], xb;
+        tmem_ld16x256b_x4(tq + 32 * h, a0);
+        tmem_ld16x256b_x4(tq + (16u << 16) + 32 * h, a1);
         if (H == 0 || h == 0) {
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(rx[0]) : "r"(taddr + 32 * h + 32) : "memory");
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(xb) : "r"(tq + 32 * h + 32) : "memory");
         } else {
-          rx[0] = 0;
+          xb = 0;  // column 128 would only feed row 127, which is never stored
         }
         tmem_ld_wait();
         if (h == 1) {
@@ -309,96 +311,69 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[e]);
         }
-#define CNRX_R(i) ((i) < 32 ? ra[(i) & 31] : rx[0])
 #pragma unroll
-        for (int m = 0; m < 16; ++m) {
-          const uint32_t send = odd ? CNRX_R(m + 1) : CNRX_R(16 + m);
-          const float recv = __uint_as_float(__shfl_xor_sync(0xffffffffu, send, 1));
-          const float mine = __uint_as_float(odd ? CNRX_R(17 + m) : CNRX_R(m));
-          float v = mine + recv + bias;
-          if (grp.relu) v = fmaxf(v, 0.f);
-          const uint32_t hv = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
-          if ((m & 1) == 0) pk[h][m >> 1] = hv;
-          else pk[h][m >> 1] |= hv << 16;
-        }
-#undef CNRX_R
-      }
-      // 8x8 transpose (16-bit elements) inside each group of 8 lanes (lane bits 1..3), per block of 8 rows:
-      // afterwards pk[h][4b .. 4b+3] of lane idx = channels c0..c0+7 of row 64H + 32h + (odd ? 16 : 0) + 8b + idx.
+        for (int blk = 0; blk < 2; ++blk) {
+          uint32_t (&a)[16] = blk == 0 ? a0 : a1;
+          uint32_t rres[4] = {0u, 0u, 0u, 0u};
+          if (has_res) {
+            // residual rows 64H + 32h + 8i + arow%8 (matrix i), channel chunk 2q + blk
+            const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
+            ldsm_x4_trans(rbuf_a + sw128(row, static_cast<uint32_t>((2 * q + blk) * 16)), rres);
+          }
+          const float bnd = __uint_as_float(__shfl_sync(0xffffffffu, xb, 16 * blk + 8 + ci));
+          uint32_t o[4], o2[4];
 #pragma unroll
-      for (int hb = 0; hb < 4; ++hb) {
-        uint32_t& r0 = pk[hb >> 1][4 * (hb & 1) + 0];
-        uint32_t& r1 = pk[hb >> 1][4 * (hb & 1) + 1];
-        uint32_t& r2 = pk[hb >> 1][4 * (hb & 1) + 2];
-        uint32_t& r3 = pk[hb >> 1][4 * (hb & 1) + 3];
-        {  // level 1: swap off-diagonal 4x4 blocks between idx and idx^4
-          const bool lo = (idx & 4) == 0;
-          const uint32_t s0 = lo ? r2 : r0, s1 = lo ? r3 : r1;
-          const uint32_t g0 = __shfl_xor_sync(0xffffffffu, s0, 8), g1 = __shfl_xor_sync(0xffffffffu, s1, 8);
-          if (lo) { r2 = g0; r3 = g1; } else { r0 = g0; r1 = g1; }
-        }
-        {  // level 2: swap off-diagonal 2x2 blocks between idx and idx^2
-          const bool lo = (idx & 2) == 0;
-          const uint32_t s0 = lo ? r1 : r0, s1 = lo ? r3 : r2;
-          const uint32_t g0 = __shfl_xor_sync(0xffffffffu, s0, 4), g1 = __shfl_xor_sync(0xffffffffu, s1, 4);
-          if (lo) { r1 = g0; r3 = g1; } else { r0 = g0; r2 = g1; }
-        }
-        {  // level 3: swap off-diagonal elements between idx and idx^1
-          const bool lo = (idx & 1) == 0;
-          const uint32_t g0 = __shfl_xor_sync(0xffffffffu, r0, 2), g1 = __shfl_xor_sync(0xffffffffu, r1, 2);
-          const uint32_t g2 = __shfl_xor_sync(0xffffffffu, r2, 2), g3 = __shfl_xor_sync(0xffffffffu, r3, 2);
-          r0 = lo ? __byte_perm(r0, g0, 0x5410) : __byte_perm(g0, r0, 0x7632);
-          r1 = lo ? __byte_perm(r1, g1, 0x5410) : __byte_perm(g1, r1, 0x7632);
-          r2 = lo ? __byte_perm(r2, g2, 0x5410) : __byte_perm(g2, r2, 0x7632);
-          r3 = lo ? __byte_perm(r3, g3, 0x5410) : __byte_perm(g3, r3, 0x7632);
-        }
-      }
-      const long long te2 = clock64();
-      tr_comb += te2 - te1;
-      // staging buffer free? (this group's previous TMA store has read it)
-      if (lead) bulk_wait_read0();
-      epi_group_sync(e);
-      const long long te3 = clock64();
-      tr_sw += te3 - te2;
-#pragma unroll
-      for (int hb = 0; hb < 4; ++hb) {
-        const uint32_t row = static_cast<uint32_t>(64 * H + 32 * (hb >> 1) + (odd ? 16 : 0) + 8 * (hb & 1) + idx);
-        const bool valid = geo.valid(p0 + row);  // row 127 is never stored
-        const uint32_t* pr = &pk[hb >> 1][4 * (hb & 1)];
-        uint4 o = make_uint4(pr[0], pr[1], pr[2], pr[3]);
-        if (!valid) o = make_uint4(0, 0, 0, 0);
-        const uint32_t off = row * 128u + (((static_cast<uint32_t>(c0 >> 3)) ^ (row & 7u)) << 4);
-        *reinterpret_cast<uint4*>(stg + off) = o;
-        if (has_out2) {
-          uint4 u;
-          if (relu2_only) {
-            const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
-            __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
-            __nv_bfloat162* up = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) up[i] = __hmax2(op[i], z);
-          } else {
-            const __nv_bfloat162* op = reinterpret_cast<const __nv_bfloat162*>(&o);
-            __nv_bfloat162* up = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float2 f = __bfloat1622float2(op[i]);
-              const float x0 = fmaxf(f.x * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
-              const float x1 = fmaxf(f.y * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
-              up[i] = __floats2bfloat162_rn(valid ? x0 : 0.f, valid ? x1 : 0.f);
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t snd = t0 == 0 ? (i < 3 ? a[4 * (i + 1) + 2] : 0u) : a[4 * i + 2];
+            float got = __uint_as_float(__shfl_sync(0xffffffffu, snd, t0 == 3 ? lane - 3 : lane + 1));
+            if (i == 3 && t0 == 3) got = bnd;
+            float y0 = __uint_as_float(a[4 * i + 0]) + __uint_as_float(a[4 * i + 3]) + bias[blk];
+            float y1 = __uint_as_float(a[4 * i + 1]) + got + bias[blk];
+            if (has_res) {
+              const float2 rf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rres[i]));
+              y0 += rf.x;
+              y1 += rf.y;
+            }
+            if (grp.relu) {
+              y0 = fmaxf(y0, 0.f);
+              y1 = fmaxf(y1, 0.f);
+            }
+            const int rb = 8 * i + 2 * t0;  // row 64H + 32h + rb
+            const bool v0 = (vmask[h] >> rb) & 1u, v1 = (vmask[h] >> (rb + 1)) & 1u;
+            if (!v0) y0 = 0.f;
+            if (!v1) y1 = 0.f;
+            const __nv_bfloat162 ob = __floats2bfloat162_rn(y0, y1);
+            o[i] = *reinterpret_cast<const uint32_t*>(&ob);
+            if (has_out2) {
+              __nv_bfloat162 u;
+              if (relu2_only) {
+                u = __hmax2(ob, __float2bfloat162_rn(0.f));
+              } else {
+                const float2 f = __bfloat1622float2(ob);
+                const float x0 = fmaxf(f.x * s2v[blk] + t2v[blk], 0.f);
+                const float x1 = fmaxf(f.y * s2v[blk] + t2v[blk], 0.f);
+                u = __floats2bfloat162_rn(v0 ? x0 : 0.f, v1 ? x1 : 0.f);
+              }
+              o2[i] = *reinterpret_cast<const uint32_t*>(&u);
             }
           }
-          *reinterpret_cast<uint4*>(stg + 128 * kRB + off) = u;
+          const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
+          const uint32_t off = sw128(row, static_cast<uint32_t>((2 * q + blk) * 16));
+          stsm_x4_trans(stg_a + off, o);
+          if (has_out2) stsm_x4_trans(stg_a + 128 * kRB + off, o2);
         }
       }
-      tr_wr += clock64() - te3;
+      const long long te3 = clock64();
+      tr_comb += te3 - te2;
       fence_proxy_async_smem();
       epi_group_sync(e);
       if (lead) {
         tma_store_2d(&grp.out_map, stg, 0, static_cast<int32_t>(p0));
         if (has_out2) tma_store_2d(&grp.out2_map, stg + 128 * kRB, 0, static_cast<int32_t>(p0));
         bulk_commit();
+        if (has_res && tile + 2 * gstride < n_tiles) load_res(tile + 2 * gstride, kb);
       }
+      tr_wr += clock64() - te3;
     }
     if (lead) bulk_wait0();
     if (L.trace && lead && e == 0) {
@@ -453,7 +428,7 @@ void conv_ws64_pack_weights(const float* w, const float* scale, uint32_t* img) {
       const int dt = dtA + half;
       const bool real = half == 0 || p < 3;
       for (int co = 0; co < kC; ++co) {
-        const int lane = 2 * co + half;
+        const int lane = 16 * (co / 8) + 8 * half + co % 8;
         for (int ci = 0; ci < kC; ++ci) {
           float v = 0.f;
           if (real) {

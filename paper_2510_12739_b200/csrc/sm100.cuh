@@ -232,4 +232,45 @@ __host__ __device__ __forceinline__ uint32_t sw64_offset(uint32_t row, uint32_t 
   return row * 64u + ((chunk ^ ((row >> 1) & 3u)) << 4);
 }
 
+
+// %globaltimer in ns (debug tracing: effective SM clock = clock64 cycles / elapsed ns)
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// trace slots 12..15: CTA count, ~min start, max end, summed CTA ns (see api.cpp trace printing)
+__device__ __forceinline__ void trace_cta_window(unsigned long long* tr, unsigned long long g_start) {
+  const unsigned long long g_end = globaltimer_ns();
+  atomicAdd(&tr[12], 1ull);
+  atomicMax(&tr[13], ~g_start);
+  atomicMax(&tr[14], g_end);
+  atomicAdd(&tr[15], g_end - g_start);
+}
+
+// TMEM -> registers, 16 lanes x 256 bit, 4 repetitions along columns (CuTe SM100_TMEM_LOAD_16dp256b4x):
+// thread t gets r[4i + 0/1] = (lane t/4, columns 8i + 2(t%4) + 0/1), r[4i + 2/3] = lane t/4 + 8, same columns.
+__device__ __forceinline__ void tmem_ld16x256b_x4(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+// Four 8x8 b16 matrices, transposed: thread a supplies the address of row a%8 of matrix a/8 (16 bytes);
+// thread t gets r[i] = (rows 2(t%4), 2(t%4)+1 ; column t/4) of matrix i, low half = the even row.
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t saddr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(saddr)
+               : "memory");
+}
+// Inverse of ldsm_x4_trans: r[i] holds (rows 2(t%4), 2(t%4)+1 ; column t/4) of matrix i.
+__device__ __forceinline__ void stsm_x4_trans(uint32_t saddr, const uint32_t (&r)[4]) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1,%2,%3,%4};"
+               :
+               : "r"(saddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+               : "memory");
+}
 }  // namespace cnrx

@@ -1,0 +1,23 @@
+"""Per-launch device times (CUDA events inside the library) for one config, averaged over a few runs."""
+import os, sys
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import torch
+from paper_2510_12739_b200 import graph as G, plan as P, slots
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+cfg = G.CONFIGS[name]; g = cfg.graph(); B = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.batch
+b = slots.generate(cfg.link, B, 1)
+p = P.Plan(g, cfg.precision if hasattr(cfg, "precision") else "bf16"); p.set_pilots(b.pilots, b.pilot_mask)
+y = torch.from_numpy(b.y).cuda(); out = torch.empty((B, cfg.link.T, cfg.link.F, p.out_channels), device="cuda")
+for _ in range(3):
+    p.receive_device(y, out, 0)
+torch.cuda.synchronize()
+p.set_profiling(True)
+reps = 10
+for _ in range(reps):
+    p.receive_device(y, out, 0)
+torch.cuda.synchronize()
+tot = 0.0
+for n, ms, c in p.read_profile():
+    tot += ms / reps
+    print(f"{n:40s} {ms / reps * 1e3:9.1f} us")
+print(f"{'total':40s} {tot * 1e3:9.1f} us")
