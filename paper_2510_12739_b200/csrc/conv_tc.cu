@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
   constexpr int ORB = COUT * 2;  // output row bytes (staged path: one swizzle chunk)
 
   extern __shared__ uint8_t smem_dyn[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_dyn);
   const SmemLayout lay = smem_layout(CIN, COUT, KS, L.stages, L.win_alloc, L.flags);
   uint8_t* sW = smem + lay.w_off;
   float* s_bias = reinterpret_cast<float*>(smem + lay.par_off);

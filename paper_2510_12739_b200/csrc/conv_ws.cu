@@ -80,10 +80,15 @@ __device__ __forceinline__ void epi_group_sync(int e) {
   else asm volatile("bar.sync 2, 256;" ::: "memory");
 }
 
+// Epilogue variant flags (compile-time so the unrolled epilogue carries no per-element branches);
+// kWsDynamic reads them from the launch instead.
+enum : int { kWsRes = 1, kWsOut2 = 2, kWsOut2Bn = 4, kWsRelu = 8, kWsDynamic = -1 };
+
+template <int FL>
 __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant__ WsLaunch L) {
   constexpr uint32_t IDESC = idesc_bf16_f32(128, kN);
   extern __shared__ uint8_t smem_dyn[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_dyn);
   const WsLayout lay = ws_layout(L.stages, L.win_alloc);
   float* s_bias = reinterpret_cast<float*>(smem + lay.par_off);
   float* s_s2 = s_bias + kC;
@@ -104,8 +109,9 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
   const int nct = (static_cast<int>(gridDim.x) - g + G - 1) / G;
   const WsGroup& grp = L.g[g];
   const int64_t n_tiles = L.n_tiles;
-  const bool has_res = grp.res_map_valid != 0;
-  const bool has_out2 = grp.out2_map_valid != 0;
+  const bool has_res = FL < 0 ? grp.res_map_valid != 0 : (FL & kWsRes) != 0;
+  const bool has_out2 = FL < 0 ? grp.out2_map_valid != 0 : (FL & kWsOut2) != 0;
+  const bool relu_main = FL < 0 ? grp.relu != 0 : (FL & kWsRelu) != 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < L.stages; ++s) {
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
       s2v[blk] = s_s2[ch];
       t2v[blk] = s_t2[ch];
     }
-    const bool relu2_only = grp.s2 == nullptr;
+    const bool relu2_only = FL < 0 ? grp.s2 == nullptr : (FL & kWsOut2Bn) == 0;
     const bool lead = ((warp - 2) & 7) == 0 && lane == 0;
     // ldmatrix / stmatrix row addresses: thread a -> matrix a/8 (8-row group), row a%8
     const int arow = ((lane >> 3) << 3) + (lane & 7);
@@ -334,7 +340,7 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
               y0 += rf.x;
               y1 += rf.y;
             }
-            if (grp.relu) {
+            if (relu_main) {
               y0 = fmaxf(y0, 0.f);
               y1 = fmaxf(y1, 0.f);
             }
@@ -463,26 +469,50 @@ int conv_ws64_win_alloc(int halo) { return (kN + 1 + 2 * halo + kBox - 1) / kBox
 
 int64_t conv_ws64_tiles(int64_t nalloc) { return (nalloc + kTileRows - 1) / kTileRows; }
 
-const char* conv_ws64_launch(const WsLaunch& L, int num_sms, cudaStream_t stream) {
-  const WsLayout lay = ws_layout(L.stages, L.win_alloc);
+namespace {
+
+int group_flags(const WsGroup& g) {
+  return (g.res_map_valid ? kWsRes : 0) | (g.out2_map_valid ? kWsOut2 : 0) | (g.s2 ? kWsOut2Bn : 0) |
+         (g.relu ? kWsRelu : 0);
+}
+
+template <int FL>
+void launch_fl(const WsLaunch& L, const WsLayout& lay, int grid, cudaStream_t stream) {
   static thread_local int configured = -1;
   if (configured < static_cast<int>(lay.total)) {
-    CNRX_CUDA(cudaFuncSetAttribute(conv_ws64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CNRX_CUDA(cudaFuncSetAttribute(conv_ws64_kernel<FL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(lay.total)));
     configured = static_cast<int>(lay.total);
   }
-  const int64_t work = static_cast<int64_t>(L.ngroups) * L.n_tiles;
-  int grid = static_cast<int>(work < num_sms ? work : num_sms);
-  if (grid < L.ngroups) grid = L.ngroups;
-  conv_ws64_kernel<<<grid, 576, lay.total, stream>>>(L);
+  conv_ws64_kernel<FL><<<grid, 576, lay.total, stream>>>(L);
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, conv_ws64_kernel);
+    cudaFuncGetAttributes(&fa, conv_ws64_kernel<FL>);
     throw Error(4, std::string("conv_ws64 launch failed: ") + cudaGetErrorString(err) + " (regs " +
                        std::to_string(fa.numRegs) + ", max threads " + std::to_string(fa.maxThreadsPerBlock) +
                        ", static smem " + std::to_string(fa.sharedSizeBytes) + ", dynamic " +
                        std::to_string(lay.total) + ")");
+  }
+}
+
+}  // namespace
+
+const char* conv_ws64_launch(const WsLaunch& L, int num_sms, cudaStream_t stream) {
+  const WsLayout lay = ws_layout(L.stages, L.win_alloc);
+  const int64_t work = static_cast<int64_t>(L.ngroups) * L.n_tiles;
+  int grid = static_cast<int>(work < num_sms ? work : num_sms);
+  if (grid < L.ngroups) grid = L.ngroups;
+  int fl = group_flags(L.g[0]);
+  for (int i = 1; i < L.ngroups; ++i)
+    if (group_flags(L.g[i]) != fl) fl = kWsDynamic;
+  switch (fl) {
+    case kWsRelu: launch_fl<kWsRelu>(L, lay, grid, stream); break;                         // block conv 1
+    case kWsRes | kWsOut2: launch_fl<kWsRes | kWsOut2>(L, lay, grid, stream); break;       // block conv 2
+    case kWsRes: launch_fl<kWsRes>(L, lay, grid, stream); break;                           // last block conv 2
+    case kWsRes | kWsOut2 | kWsOut2Bn: launch_fl<kWsRes | kWsOut2 | kWsOut2Bn>(L, lay, grid, stream); break;
+    case 0: launch_fl<0>(L, lay, grid, stream); break;
+    default: launch_fl<kWsDynamic>(L, lay, grid, stream); break;
   }
   return "conv_ws64_kernel";
 }

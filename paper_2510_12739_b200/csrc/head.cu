@@ -1,0 +1,266 @@
+// head.cu — CoNet-Rx fusion tail + LLR head over 64-channel bf16 planes, TMA-streamed.
+//
+// Replaces the reference's tail of build_conet (network.hpp:520-560): the interaction fusion of the
+// main and supplementary subnetwork outputs (elementwise mul / add, network.hpp:526-532, each
+// optionally followed by an eval BN, norms.hpp:81-95, and ReLU) and the 1x1 output conv to the LLRs
+// (kernels.hpp:47-91 with k = 1), for the left-fold program shape pw_as_fold() recognises.
+//
+// HBM-bound (it reads every subnet's final plane once: NS x 128 B per plane row, writes NB fp32 LLRs per
+// RE), so the operand rows are streamed by TMA (128-row boxes, 128-byte swizzle) into a shared-memory
+// ring instead of per-thread global loads, which saturated the L1 path at ~3 TB/s.  Two threads per
+// plane row (32 channels each) do the fold and the GEMV in fp32 and combine with one shuffle.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
+#include "head.h"
+#include "sm100.cuh"
+
+namespace cnrx {
+
+namespace {
+
+constexpr int kHC = 64;                  // channels
+constexpr int kHRows = 128;              // rows per tile
+constexpr uint32_t kPlaneBox = kHRows * kHC * 2;  // 16 KB per operand tile
+constexpr int kConsumers = 256;          // two threads per row
+constexpr int kThreads = kConsumers + 32;
+
+struct HeadLayout {
+  uint32_t ring_off, stage_bytes, aff_off, w_off, b_off, bar_off, total;
+};
+__host__ __device__ inline HeadLayout head_layout(int ns, int nb, int stages) {
+  HeadLayout l{};
+  l.ring_off = 0;
+  l.stage_bytes = static_cast<uint32_t>(ns) * kPlaneBox;
+  uint32_t off = l.stage_bytes * static_cast<uint32_t>(stages);
+  l.aff_off = off;
+  off += static_cast<uint32_t>(ns) * 2u * kHC * 4u;
+  l.w_off = off;
+  off += static_cast<uint32_t>(kHC * nb) * 4u;
+  l.b_off = off;
+  off += 64u;
+  l.bar_off = (off + 15u) & ~15u;
+  l.total = l.bar_off + 2u * 8u * static_cast<uint32_t>(stages) + 1024u;
+  return l;
+}
+
+__device__ __forceinline__ uint32_t hsw128(uint32_t row, uint32_t chunk) {
+  return row * 128u + ((chunk ^ (row & 7u)) << 4);
+}
+
+template <int NB, int NS>
+__global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_constant__ HeadLaunch L) {
+  extern __shared__ uint8_t smem_dyn[];
+  uint8_t* smem = smem_align1024(smem_dyn);
+  const HeadLayout lay = head_layout(NS, NB, L.stages);
+  float* s_aff = reinterpret_cast<float*>(smem + lay.aff_off);  // [NS][2][64]
+  float* s_w = reinterpret_cast<float*>(smem + lay.w_off);      // [64][NB]
+  float* s_b = reinterpret_cast<float*>(smem + lay.b_off);      // [NB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + lay.bar_off);
+  uint64_t* empty = full + L.stages;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < L.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers / 32);
+    }
+    fence_barrier_init();
+  }
+  for (int e = tid; e < NS * kHC; e += kThreads) {
+    const int i = e / kHC, c = e % kHC;
+    s_aff[(2 * i) * kHC + c] = L.aff_s[i] ? L.aff_s[i][c] : 1.f;
+    s_aff[(2 * i + 1) * kHC + c] = L.aff_t[i] ? L.aff_t[i][c] : 0.f;
+  }
+  for (int e = tid; e < kHC * NB; e += kThreads) s_w[e] = L.head_w[e];
+  if (tid < NB) s_b[tid] = L.head_b[tid];
+  __syncthreads();
+
+  const int64_t n_tiles = L.geo.Nalloc / kHRows;
+  if (tid >= kConsumers) {
+    // ------------------------------ TMA producer ------------------------------
+    if (tid == kConsumers) {
+      for (int i = 0; i < NS; ++i) prefetch_tmap(&L.maps[i]);
+      int j = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
+        const int s = j % L.stages;
+        mbar_wait(&empty[s], (static_cast<uint32_t>(j / L.stages) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(NS) * kPlaneBox);
+        uint8_t* dst = smem + lay.ring_off + s * lay.stage_bytes;
+        for (int i = 0; i < NS; ++i)
+          tma_load_2d(dst + i * kPlaneBox, &L.maps[i], &full[s], 0, static_cast<int32_t>(tile * kHRows));
+      }
+    }
+    return;
+  }
+  // ------------------------------ consumers: two threads per row ------------------
+  const int r = tid >> 1, hf = tid & 1;
+  const PlaneGeom geo = L.geo;
+  int j = 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
+    const int s = j % L.stages;
+    mbar_wait(&full[s], static_cast<uint32_t>(j / L.stages) & 1u);
+    const uint8_t* st = smem + lay.ring_off + s * lay.stage_bytes;
+    float acc[32];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(st + i * kPlaneBox + hsw128(r, 4 * hf + k));
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(hv[e]);
+          const int c = 8 * k + 2 * e;
+          if (i == 0) {
+            acc[c] = f.x;
+            acc[c + 1] = f.y;
+          } else if (L.op[i] == PW_MUL) {
+            acc[c] *= f.x;
+            acc[c + 1] *= f.y;
+          } else {
+            acc[c] += f.x;
+            acc[c + 1] += f.y;
+          }
+        }
+      }
+      if (L.aff_s[i]) {
+        const float* ps = s_aff + (2 * i) * kHC + 32 * hf;
+        const float* pt = s_aff + (2 * i + 1) * kHC + 32 * hf;
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          const float4 sv = *reinterpret_cast<const float4*>(ps + c);
+          const float4 tv = *reinterpret_cast<const float4*>(pt + c);
+          acc[c] = acc[c] * sv.x + tv.x;
+          acc[c + 1] = acc[c + 1] * sv.y + tv.y;
+          acc[c + 2] = acc[c + 2] * sv.z + tv.z;
+          acc[c + 3] = acc[c + 3] * sv.w + tv.w;
+        }
+      }
+      if (L.relu[i]) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] = fmaxf(acc[c], 0.f);
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    float part[NB];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) part[q] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const float* wr = s_w + (32 * hf + c) * NB;
+#pragma unroll
+      for (int q = 0; q < NB; ++q) part[q] = fmaf(acc[c], wr[q], part[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < NB; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], 1);
+    const int64_t row = tile * kHRows + r;
+    if (hf == 0 && geo.valid(row)) {
+      int b, t, f;
+      geo.coords(row, b, t, f);
+      float* dst = L.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * NB;
+      if constexpr (NB == 4) {
+        *reinterpret_cast<float4*>(dst) =
+            make_float4(part[0] + s_b[0], part[1] + s_b[1], part[2] + s_b[2], part[3] + s_b[3]);
+      } else if constexpr (NB == 2) {
+        *reinterpret_cast<float2*>(dst) = make_float2(part[0] + s_b[0], part[1] + s_b[1]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NB; ++q) dst[q] = part[q] + s_b[q];
+      }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_head() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void* p = nullptr;
+    CNRX_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr));
+    if (!p) throw Error(4, "cuTensorMapEncodeTiled not available");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <int NB, int NS>
+void launch_t(const HeadLaunch& L, int stages_bytes_total, cudaStream_t s) {
+  static thread_local int configured = -1;
+  if (configured < stages_bytes_total) {
+    CNRX_CUDA(cudaFuncSetAttribute(head_tma_kernel<NB, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   stages_bytes_total));
+    configured = stages_bytes_total;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n_tiles = L.geo.Nalloc / kHRows;
+  const int64_t slots = 2ll * sms;  // two CTAs per SM (16 consumer warps) to hide the per-row latency chain
+  const unsigned grid = static_cast<unsigned>(n_tiles < slots ? n_tiles : slots);
+  head_tma_kernel<NB, NS><<<grid, kThreads, stages_bytes_total, s>>>(L);
+  CNRX_CUDA(cudaGetLastError());
+}
+
+template <int NB>
+bool launch_ns(const HeadLaunch& L, int total, cudaStream_t s) {
+  switch (L.ns) {
+    case 1: launch_t<NB, 1>(L, total, s); return true;
+    case 2: launch_t<NB, 2>(L, total, s); return true;
+    case 3: launch_t<NB, 3>(L, total, s); return true;
+    case 4: launch_t<NB, 4>(L, total, s); return true;
+    default: return false;
+  }
+}
+
+}  // namespace
+
+const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const int* affs, const int* relus,
+                            const PlaneGeom& geo, cudaStream_t s) {
+  if (prog.C != kHC || ns < 1 || ns > kHeadMaxPlanes || geo.Nalloc % kHRows != 0) return nullptr;
+  const int nb = prog.head_bits;
+  if (nb != 1 && nb != 2 && nb != 4 && nb != 6 && nb != 8) return nullptr;
+  HeadLaunch L;
+  std::memset(&L, 0, sizeof(L));
+  L.geo = geo;
+  L.ns = ns;
+  L.nb = nb;
+  for (int i = 0; i < ns; ++i) {
+    L.op[i] = ops[i];
+    L.relu[i] = relus[i];
+    L.aff_s[i] = affs[i] >= 0 ? prog.aff_s[affs[i]] : nullptr;
+    L.aff_t[i] = affs[i] >= 0 ? prog.aff_t[affs[i]] : nullptr;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(kHC), static_cast<cuuint64_t>(geo.Nalloc)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(kHC * 2)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kHC), static_cast<cuuint32_t>(kHRows)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn_head()(&L.maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                  const_cast<__nv_bfloat16*>(prog.planes[i]), dims, strides, box, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  }
+  L.head_w = prog.head_w;
+  L.head_b = prog.head_b;
+  L.llr = prog.llr;
+  int stages = 3;
+  while (stages > 2 && head_layout(ns, nb, stages).total > 113u * 1024u) --stages;
+  L.stages = stages;
+  const int total = static_cast<int>(head_layout(ns, nb, stages).total);
+  bool ok = false;
+  switch (nb) {
+    case 1: ok = launch_ns<1>(L, total, s); break;
+    case 2: ok = launch_ns<2>(L, total, s); break;
+    case 4: ok = launch_ns<4>(L, total, s); break;
+    case 6: ok = launch_ns<6>(L, total, s); break;
+    case 8: ok = launch_ns<8>(L, total, s); break;
+    default: break;
+  }
+  return ok ? "head_tma_kernel" : nullptr;
+}
+
+}  // namespace cnrx

@@ -9,7 +9,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
+#include "head.h"
 #include "kernels.h"
 
 namespace cnrx {
@@ -459,6 +461,11 @@ const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaS
     FoldSteps fs{};
     int ns = 0;
     if (pw_as_fold(prog, &ns, fs.op, fs.aff, fs.relu) && prog.n_planes_used == ns) {
+      static const bool no_tma_head = getenv("CNRX_NO_TMA_HEAD") != nullptr;
+      if (head && !no_tma_head) {
+        const char* name = launch_head_tma(prog, ns, fs.op, fs.aff, fs.relu, geo, s);
+        if (name) return name;
+      }
       const bool ok = launch_fold_any(prog, fs, ns, geo, s);
       if (ok) return head ? "pw_fold_kernel<head>" : "pw_fold_kernel<plane>";
     }

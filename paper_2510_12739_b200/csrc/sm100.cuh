@@ -273,4 +273,12 @@ __device__ __forceinline__ void stsm_x4_trans(uint32_t saddr, const uint32_t (&r
                : "r"(saddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
                : "memory");
 }
+
+// 1024-byte aligned base inside the dynamic shared-memory array.  Offsetting the __shared__ array itself
+// (instead of round-tripping through an integer) keeps the pointer in the shared state space, so
+// plain loads / stores through it compile to LDS / STS rather than generic LD / ST.
+__device__ __forceinline__ uint8_t* smem_align1024(uint8_t* smem_dyn) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dyn));
+  return smem_dyn + ((1024u - (a & 1023u)) & 1023u);
+}
 }  // namespace cnrx
