@@ -134,6 +134,7 @@ struct TcOp {
   float* stem_w = nullptr;       // fp32 [cin_real][cout_real], BN scale folded
   int in_plane = -1, res_plane = -1, out_plane = -1, out2_plane = -1;
   int relu = 0;
+  int relu_in = 0;  // ws kernels: input is relu(in_plane), applied to the window on load
   void* wimg = nullptr;
   float* bias = nullptr;
   float* s2 = nullptr;
@@ -650,7 +651,22 @@ struct Bf16Compiler {
       if (op.ks != 1 && op.ks != 3)
         throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan supports 1x1 and 3x3 convolutions");
       op.dil = nd.dilation_f;
-      op.in_plane = plane_for(nd.in0);
+      // relu(v) feeding a 64->64 3x3 conv: the weights-stationary kernel applies the ReLU to its input
+      // window in shared memory, so v's producer need not store a second, pre-activated plane
+      // (relu commutes with the bf16 rounding: identical values).
+      static const bool no_relu_in = getenv("CNRX_NO_RELU_IN") != nullptr;
+      {
+        const cnrx_node& in = p.N(nd.in0);
+        const int v = in.op == CNRX_OP_RELU ? in.in0 : -1;
+        if (!no_relu_in && v >= 0 && node_plane[static_cast<size_t>(nd.in0)] < 0 && node_plane[static_cast<size_t>(v)] >= 0 &&
+            !p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].nonneg && op.ks == 3 && w.dims[2] == 64 &&
+            w.dims[3] == 64 && p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].C == 64 && !getenv("CNRX_NO_WS")) {
+          op.relu_in = 1;
+          op.in_plane = node_plane[static_cast<size_t>(v)];
+        } else {
+          op.in_plane = plane_for(nd.in0);
+        }
+      }
       op.cin = p.planes[static_cast<size_t>(op.in_plane)].C;
       op.cout = round_cout(nd.out_channels);
       op.cin_real = static_cast<int>(w.dims[2]);
@@ -700,6 +716,7 @@ struct Bf16Compiler {
       // weights (BN scale folded per output channel) and bias
       static const bool no_ws = getenv("CNRX_NO_WS") != nullptr;
       op.ws = !no_ws && op.ks == 3 && op.cin_real == 64 && op.cout_real == 64 && op.cin == 64 && op.cout == 64;
+      if (op.relu_in && !op.ws) throw Error(CNRX_ERR_UNSUPPORTED, "internal: relu-on-load needs the ws conv kernel");
       if (op.ws) {
         std::vector<uint32_t> img(conv_ws64_wimg_bytes() / 4);
         conv_ws64_pack_weights(w.data.data(), scale.empty() ? nullptr : scale.data(), img.data());
@@ -899,6 +916,7 @@ void ensure_workspace(cnrx_plan& p, int B, int T, int F) {
           g.s2 = op.s2;
           g.t2 = op.t2;
           g.relu = op.relu;
+          g.relu_in = op.relu_in;
         }
         L.win_alloc = win_alloc;
         int stages = 4;

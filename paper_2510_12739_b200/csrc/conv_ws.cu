@@ -20,6 +20,7 @@
 //   warp 0     TMA producer: activation windows (4-stage ring); residual tiles are streamed by the
 //              epilogue group that consumes them
 //   warp 1     TMEM allocator + MMA issuer
+//   warp 18    input ReLU of the window in shared memory when the plan asks for it (relu_in)
 //   warps 2-17 weights -> TMEM at start (2-5); epilogue in two groups of eight warps, one per
 //              accumulator stage (alternate tiles): TMEM -> registers, lane-pair shuffle combine,
 //              bias / ReLU / validity, bf16 pack, 8x8 lane-butterfly transpose so every lane writes
@@ -82,10 +83,11 @@ __device__ __forceinline__ void epi_group_sync(int e) {
 
 // Epilogue variant flags (compile-time so the unrolled epilogue carries no per-element branches);
 // kWsDynamic reads them from the launch instead.
-enum : int { kWsRes = 1, kWsOut2 = 2, kWsOut2Bn = 4, kWsRelu = 8, kWsDynamic = -1 };
+enum : int { kWsRes = 1, kWsOut2 = 2, kWsOut2Bn = 4, kWsRelu = 8, kWsReluIn = 16, kWsDynamic = -1 };
+constexpr int kWsThreads = 608;  // 19 warps: producer, MMA, 16 epilogue, input-ReLU
 
 template <int FL>
-__global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant__ WsLaunch L) {
+__global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_constant__ WsLaunch L) {
   constexpr uint32_t IDESC = idesc_bf16_f32(128, kN);
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
@@ -99,7 +101,8 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
   uint64_t* tfull = empty + L.stages;     // [2]
   uint64_t* tempty = tfull + 2;           // [2]
   uint64_t* rfull = tempty + 2;           // [2 groups][2 buffers] residual tile landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 4);
+  uint64_t* ready = rfull + 4;            // [stages] window ReLU'd in place (relu_in only)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + L.stages);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -112,11 +115,13 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
   const bool has_res = FL < 0 ? grp.res_map_valid != 0 : (FL & kWsRes) != 0;
   const bool has_out2 = FL < 0 ? grp.out2_map_valid != 0 : (FL & kWsOut2) != 0;
   const bool relu_main = FL < 0 ? grp.relu != 0 : (FL & kWsRelu) != 0;
+  const bool relu_in = FL < 0 ? grp.relu_in != 0 : (FL & kWsReluIn) != 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < L.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&ready[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
       const int s = j % L.stages;
       const int a = j & 1;
       const long long tm0 = clock64();
-      mbar_wait(&full[s], static_cast<uint32_t>(j / L.stages) & 1u);
+      mbar_wait(relu_in ? &ready[s] : &full[s], static_cast<uint32_t>(j / L.stages) & 1u);
       const long long tm1 = clock64();
       mbar_wait(&tempty[a], (static_cast<uint32_t>(j >> 1) & 1u) ^ 1u);
       const long long tm2 = clock64();
@@ -232,6 +237,32 @@ __global__ void __launch_bounds__(576, 1) conv_ws64_kernel(const __grid_constant
       atomicAdd(&L.trace[kTraceMmaWaitTmem], static_cast<unsigned long long>(tr_tmem));
       atomicAdd(&L.trace[kTraceMmaIssue], static_cast<unsigned long long>(tr_issue));
       atomicAdd(&L.trace[kTraceTiles], static_cast<unsigned long long>(j));
+    }
+  } else if (warp == 18) {
+    // ------------------------------ input ReLU (relu_in) ----------------------
+    // The window is the B operand of the tensor core (async proxy): ReLU it in place with generic
+    // 16-byte shared accesses, then fence the generic writes to the async proxy before the MMA warp
+    // may read them.
+    if (relu_in) {
+      const int nchunks = (kN + 1 + 2 * grp.halo) * (kRB / 16);  // only the rows the UMMAs read
+      const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
+      int j = 0;
+      for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
+        const int s = j % L.stages;
+        mbar_wait(&full[s], static_cast<uint32_t>(j / L.stages) & 1u);
+        uint4* win = reinterpret_cast<uint4*>(smem + lay.win_off + s * lay.win_stage);
+#pragma unroll 4
+        for (int c = lane; c < nchunks; c += 32) {
+          uint4 v = win[c];
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) h[i] = __hmax2(h[i], z);
+          win[c] = v;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ready[s]);
+      }
     }
   } else {
     // ------------------------------ epilogue (warps 2..17) --------------------
@@ -473,7 +504,7 @@ namespace {
 
 int group_flags(const WsGroup& g) {
   return (g.res_map_valid ? kWsRes : 0) | (g.out2_map_valid ? kWsOut2 : 0) | (g.s2 ? kWsOut2Bn : 0) |
-         (g.relu ? kWsRelu : 0);
+         (g.relu ? kWsRelu : 0) | (g.relu_in ? kWsReluIn : 0);
 }
 
 template <int FL>
@@ -484,7 +515,7 @@ void launch_fl(const WsLaunch& L, const WsLayout& lay, int grid, cudaStream_t st
                                    static_cast<int>(lay.total)));
     configured = static_cast<int>(lay.total);
   }
-  conv_ws64_kernel<FL><<<grid, 576, lay.total, stream>>>(L);
+  conv_ws64_kernel<FL><<<grid, kWsThreads, lay.total, stream>>>(L);
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {
     cudaFuncAttributes fa{};
@@ -508,6 +539,7 @@ const char* conv_ws64_launch(const WsLaunch& L, int num_sms, cudaStream_t stream
     if (group_flags(L.g[i]) != fl) fl = kWsDynamic;
   switch (fl) {
     case kWsRelu: launch_fl<kWsRelu>(L, lay, grid, stream); break;                         // block conv 1
+    case kWsRelu | kWsReluIn: launch_fl<kWsRelu | kWsReluIn>(L, lay, grid, stream); break; // conv 1, ReLU on load
     case kWsRes | kWsOut2: launch_fl<kWsRes | kWsOut2>(L, lay, grid, stream); break;       // block conv 2
     case kWsRes: launch_fl<kWsRes>(L, lay, grid, stream); break;                           // last block conv 2
     case kWsRes | kWsOut2 | kWsOut2Bn: launch_fl<kWsRes | kWsOut2 | kWsOut2Bn>(L, lay, grid, stream); break;

@@ -15,7 +15,8 @@ struct WsGroup {
   const float* bias;     // [64] (BN folded in)
   const float* s2;       // out2 = relu(v*s2 + t2) (null: relu(v))
   const float* t2;
-  int32_t relu, dil, halo, res_map_valid, out2_map_valid, pad_;
+  int32_t relu, dil, halo, res_map_valid, out2_map_valid;
+  int32_t relu_in;       // apply ReLU to the input window in shared memory (consumer-side pre-activation)
 };
 
 struct WsLaunch {
