@@ -5,10 +5,11 @@
 // optionally followed by an eval BN, norms.hpp:81-95, and ReLU) and the 1x1 output conv to the LLRs
 // (kernels.hpp:47-91 with k = 1), for the left-fold program shape pw_as_fold() recognises.
 //
-// HBM-bound (it reads every subnet's final plane once: NS x 128 B per plane row, writes NB fp32 LLRs per
-// RE), so the operand rows are streamed by TMA (128-row boxes, 128-byte swizzle) into a shared-memory
-// ring instead of per-thread global loads, which saturated the L1 path at ~3 TB/s.  Two threads per
-// plane row (32 channels each) do the fold and the GEMV in fp32 and combine with one shuffle.
+// HBM-bound (it reads every subnet's final plane once: NS x 2C bytes per plane row, writes NB fp32 LLRs
+// per RE), so the operand rows are streamed by TMA (128-row boxes; 128-byte swizzle for 64 channels)
+// into a shared-memory ring instead of per-thread global loads, which saturated the L1 path at ~3 TB/s.
+// Two threads per plane row (C/2 channels each) do the fold and the GEMV in fp32 and combine with one
+// shuffle.  C in {64, 96, 128}.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -22,17 +23,17 @@ namespace cnrx {
 
 namespace {
 
-constexpr int kHC = 64;                  // channels
 constexpr int kHRows = 128;              // rows per tile
-constexpr uint32_t kPlaneBox = kHRows * kHC * 2;  // 16 KB per operand tile
-constexpr int kConsumers = 256;          // two threads per row
+constexpr int kConsumers = 256;          // two threads per row, C/2 channels each
 constexpr int kThreads = kConsumers + 32;
 
 struct HeadLayout {
   uint32_t ring_off, stage_bytes, aff_off, w_off, b_off, bar_off, total;
 };
-__host__ __device__ inline HeadLayout head_layout(int ns, int nb, int stages) {
+__host__ __device__ inline HeadLayout head_layout(int c, int ns, int nb, int stages) {
   HeadLayout l{};
+  const int kHC = c;
+  const uint32_t kPlaneBox = static_cast<uint32_t>(kHRows * c * 2);
   l.ring_off = 0;
   l.stage_bytes = static_cast<uint32_t>(ns) * kPlaneBox;
   uint32_t off = l.stage_bytes * static_cast<uint32_t>(stages);
@@ -47,17 +48,24 @@ __host__ __device__ inline HeadLayout head_layout(int ns, int nb, int stages) {
   return l;
 }
 
-__device__ __forceinline__ uint32_t hsw128(uint32_t row, uint32_t chunk) {
-  return row * 128u + ((chunk ^ (row & 7u)) << 4);
+// byte offset of 16-byte chunk `chunk` of row `row` in a TMA tile: 128-byte swizzle for 64-channel
+// rows, plain row-major otherwise (96 / 128 channels: rows wider than the swizzle span)
+template <int C>
+__device__ __forceinline__ uint32_t hoff(uint32_t row, uint32_t chunk) {
+  if constexpr (C == 64) return row * 128u + ((chunk ^ (row & 7u)) << 4);
+  else return row * static_cast<uint32_t>(C * 2) + (chunk << 4);
 }
 
-template <int NB, int NS>
+template <int C, int NB, int NS>
 __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_constant__ HeadLaunch L) {
+  constexpr int kHC = C;
+  constexpr int CPT = C / 2;  // channels per thread
+  constexpr uint32_t kPlaneBox = kHRows * C * 2;
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
-  const HeadLayout lay = head_layout(NS, NB, L.stages);
-  float* s_aff = reinterpret_cast<float*>(smem + lay.aff_off);  // [NS][2][64]
-  float* s_w = reinterpret_cast<float*>(smem + lay.w_off);      // [64][NB]
+  const HeadLayout lay = head_layout(C, NS, NB, L.stages);
+  float* s_aff = reinterpret_cast<float*>(smem + lay.aff_off);  // [NS][2][C]
+  float* s_w = reinterpret_cast<float*>(smem + lay.w_off);      // [C][NB]
   float* s_b = reinterpret_cast<float*>(smem + lay.b_off);      // [NB]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + lay.bar_off);
   uint64_t* empty = full + L.stages;
@@ -104,12 +112,12 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
     const int s = j % L.stages;
     mbar_wait(&full[s], static_cast<uint32_t>(j / L.stages) & 1u);
     const uint8_t* st = smem + lay.ring_off + s * lay.stage_bytes;
-    float acc[32];
+    float acc[CPT];
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(st + i * kPlaneBox + hsw128(r, 4 * hf + k));
+      for (int k = 0; k < CPT / 8; ++k) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(st + i * kPlaneBox + hoff<C>(r, (CPT / 8) * hf + k));
         const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -128,10 +136,10 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
         }
       }
       if (L.aff_s[i]) {
-        const float* ps = s_aff + (2 * i) * kHC + 32 * hf;
-        const float* pt = s_aff + (2 * i + 1) * kHC + 32 * hf;
+        const float* ps = s_aff + (2 * i) * kHC + CPT * hf;
+        const float* pt = s_aff + (2 * i + 1) * kHC + CPT * hf;
 #pragma unroll
-        for (int c = 0; c < 32; c += 4) {
+        for (int c = 0; c < CPT; c += 4) {
           const float4 sv = *reinterpret_cast<const float4*>(ps + c);
           const float4 tv = *reinterpret_cast<const float4*>(pt + c);
           acc[c] = acc[c] * sv.x + tv.x;
@@ -142,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
       }
       if (L.relu[i]) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] = fmaxf(acc[c], 0.f);
+        for (int c = 0; c < CPT; ++c) acc[c] = fmaxf(acc[c], 0.f);
       }
     }
     __syncwarp();
@@ -151,8 +159,8 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
 #pragma unroll
     for (int q = 0; q < NB; ++q) part[q] = 0.f;
 #pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const float* wr = s_w + (32 * hf + c) * NB;
+    for (int c = 0; c < CPT; ++c) {
+      const float* wr = s_w + (CPT * hf + c) * NB;
 #pragma unroll
       for (int q = 0; q < NB; ++q) part[q] = fmaf(acc[c], wr[q], part[q]);
     }
@@ -188,11 +196,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn_head() {
   return fn;
 }
 
-template <int NB, int NS>
+template <int C, int NB, int NS>
 void launch_t(const HeadLaunch& L, int stages_bytes_total, cudaStream_t s) {
   static thread_local int configured = -1;
   if (configured < stages_bytes_total) {
-    CNRX_CUDA(cudaFuncSetAttribute(head_tma_kernel<NB, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CNRX_CUDA(cudaFuncSetAttribute(head_tma_kernel<C, NB, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    stages_bytes_total));
     configured = stages_bytes_total;
   }
@@ -200,19 +208,32 @@ void launch_t(const HeadLaunch& L, int stages_bytes_total, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t n_tiles = L.geo.Nalloc / kHRows;
-  const int64_t slots = 2ll * sms;  // two CTAs per SM (16 consumer warps) to hide the per-row latency chain
+  // two CTAs per SM (16 consumer warps) when they fit, to hide the per-row latency chain
+  const int per_sm = stages_bytes_total * 2 + 4096 <= 228 * 1024 ? 2 : 1;
+  const int64_t slots = static_cast<int64_t>(per_sm) * sms;
   const unsigned grid = static_cast<unsigned>(n_tiles < slots ? n_tiles : slots);
-  head_tma_kernel<NB, NS><<<grid, kThreads, stages_bytes_total, s>>>(L);
+  head_tma_kernel<C, NB, NS><<<grid, kThreads, stages_bytes_total, s>>>(L);
   CNRX_CUDA(cudaGetLastError());
 }
 
-template <int NB>
+template <int C, int NB>
 bool launch_ns(const HeadLaunch& L, int total, cudaStream_t s) {
   switch (L.ns) {
-    case 1: launch_t<NB, 1>(L, total, s); return true;
-    case 2: launch_t<NB, 2>(L, total, s); return true;
-    case 3: launch_t<NB, 3>(L, total, s); return true;
-    case 4: launch_t<NB, 4>(L, total, s); return true;
+    case 1: launch_t<C, NB, 1>(L, total, s); return true;
+    case 2: launch_t<C, NB, 2>(L, total, s); return true;
+    case 3: launch_t<C, NB, 3>(L, total, s); return true;
+    case 4: launch_t<C, NB, 4>(L, total, s); return true;
+    default: return false;
+  }
+}
+
+template <int C>
+bool launch_nb(const HeadLaunch& L, int total, cudaStream_t s) {
+  switch (L.nb) {
+    case 2: return launch_ns<C, 2>(L, total, s);
+    case 4: return launch_ns<C, 4>(L, total, s);
+    case 6: return launch_ns<C, 6>(L, total, s);
+    case 8: return launch_ns<C, 8>(L, total, s);
     default: return false;
   }
 }
@@ -221,9 +242,10 @@ bool launch_ns(const HeadLaunch& L, int total, cudaStream_t s) {
 
 const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const int* affs, const int* relus,
                             const PlaneGeom& geo, cudaStream_t s) {
-  if (prog.C != kHC || ns < 1 || ns > kHeadMaxPlanes || geo.Nalloc % kHRows != 0) return nullptr;
+  const int C = prog.C;
+  if ((C != 64 && C != 96 && C != 128) || ns < 1 || ns > kHeadMaxPlanes || geo.Nalloc % kHRows != 0) return nullptr;
   const int nb = prog.head_bits;
-  if (nb != 1 && nb != 2 && nb != 4 && nb != 6 && nb != 8) return nullptr;
+  if (nb != 2 && nb != 4 && nb != 6 && nb != 8) return nullptr;
   HeadLaunch L;
   std::memset(&L, 0, sizeof(L));
   L.geo = geo;
@@ -234,13 +256,14 @@ const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const
     L.relu[i] = relus[i];
     L.aff_s[i] = affs[i] >= 0 ? prog.aff_s[affs[i]] : nullptr;
     L.aff_t[i] = affs[i] >= 0 ? prog.aff_t[affs[i]] : nullptr;
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(kHC), static_cast<cuuint64_t>(geo.Nalloc)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(kHC * 2)};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(kHC), static_cast<cuuint32_t>(kHRows)};
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(geo.Nalloc)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(C * 2)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(C), static_cast<cuuint32_t>(kHRows)};
     cuuint32_t es[2] = {1, 1};
     CUresult r = encode_fn_head()(&L.maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                                   const_cast<__nv_bfloat16*>(prog.planes[i]), dims, strides, box, es,
-                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  C == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
   }
@@ -248,16 +271,15 @@ const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const
   L.head_b = prog.head_b;
   L.llr = prog.llr;
   int stages = 3;
-  while (stages > 2 && head_layout(ns, nb, stages).total > 113u * 1024u) --stages;
+  while (stages > 2 && head_layout(C, ns, nb, stages).total > 113u * 1024u) --stages;
   L.stages = stages;
-  const int total = static_cast<int>(head_layout(ns, nb, stages).total);
+  const int total = static_cast<int>(head_layout(C, ns, nb, stages).total);
+  if (total > 227 * 1024) return nullptr;
   bool ok = false;
-  switch (nb) {
-    case 1: ok = launch_ns<1>(L, total, s); break;
-    case 2: ok = launch_ns<2>(L, total, s); break;
-    case 4: ok = launch_ns<4>(L, total, s); break;
-    case 6: ok = launch_ns<6>(L, total, s); break;
-    case 8: ok = launch_ns<8>(L, total, s); break;
+  switch (C) {
+    case 64: ok = launch_nb<64>(L, total, s); break;
+    case 96: ok = launch_nb<96>(L, total, s); break;
+    case 128: ok = launch_nb<128>(L, total, s); break;
     default: break;
   }
   return ok ? "head_tma_kernel" : nullptr;

@@ -10,20 +10,20 @@ namespace cnrx {
 constexpr int kHeadMaxPlanes = 4;
 
 struct HeadLaunch {
-  CUtensorMap maps[kHeadMaxPlanes];  // operand planes [Nalloc][64] bf16, 128-row boxes, 128B swizzle
+  CUtensorMap maps[kHeadMaxPlanes];  // operand planes [Nalloc][C] bf16, 128-row boxes
   PlaneGeom geo;
   const float* aff_s[kHeadMaxPlanes];  // per fold step: eval BN scale / shift, or null
   const float* aff_t[kHeadMaxPlanes];
   int32_t op[kHeadMaxPlanes];          // PW_MUL / PW_ADD for steps >= 1
   int32_t relu[kHeadMaxPlanes];
-  const float* head_w;                 // [64][nb]
+  const float* head_w;                 // [C][nb]
   const float* head_b;                 // [nb]
   float* llr;                          // [B,T,F,nb]
   int32_t ns, nb, stages, pad_;
 };
 
 // Launch the fold program (ns steps, ops/affs/relus as pw_as_fold returns them) + head GEMV when it
-// fits this kernel (64 channels, nb in {1,2,4,6,8}); returns the kernel name, or nullptr if the caller
+// fits this kernel (C in {64, 96, 128}, nb in {2,4,6,8}); returns the kernel name, or nullptr if the caller
 // must use another kernel.
 const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const int* affs, const int* relus,
                             const PlaneGeom& geo, cudaStream_t s);
