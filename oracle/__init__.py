@@ -132,6 +132,10 @@ def ref():
         R.ref_threads.restype = C.c_int
         R.ref_save_checkpoint.argtypes = [vp, C.c_char_p]
         R.ref_load_checkpoint.argtypes = [vp, C.c_char_p]
+        R.ref_spec_to_json.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        R.ref_net_from_spec.restype = vp
+        R.ref_net_from_spec.argtypes = [C.c_char_p]
+        R.ref_solve_spec_width.argtypes = [C.c_char_p, C.c_longlong, C.c_double, _i32p, _i32p, _i64p, _i32p, _i32p]
         R.ref_rng_u64.argtypes = [C.c_uint64, C.c_int, C.POINTER(C.c_uint64)]
         R.ref_rng_uniform.argtypes = [C.c_uint64, C.c_int, _f64p]
         R.ref_rng_normal.argtypes = [C.c_uint64, C.c_int, _f64p]
@@ -223,6 +227,35 @@ class RefNet:
     def deeprx(cls, width, blocks, in_ch, bits, block_kind=0, io_kernel=1, block_kernel=3) -> "RefNet":
         return cls(ref().ref_build_deeprx_k(width, blocks, in_ch, bits, block_kind, io_kernel, block_kernel))
 
+    @classmethod
+    def from_spec(cls, text: str) -> "RefNet":
+        """parse_spec_file_json + build_conet / build_net (netspec.cpp:202-228, network.hpp:470-562)."""
+        return cls(ref().ref_net_from_spec(text.encode()))
+
+    # -- checkpoints (checkpoint.cpp:47-99) ------------------------------------------------------
+    def save_checkpoint(self, path: str) -> None:
+        if ref().ref_save_checkpoint(self.h, path.encode()):
+            raise RefError(1, ref().ref_last_error().decode())
+
+    def load_checkpoint(self, path: str) -> None:
+        rc = ref().ref_load_checkpoint(self.h, path.encode())
+        if rc:
+            raise RefError(rc, ref().ref_last_error().decode())
+
+    def param_values(self):
+        """[(name, fp32 array)] in params() order, copied out of the reference network."""
+        R = ref()
+        out = []
+        for i, (name, shape, _) in enumerate(self.params()):
+            n = int(np.prod(shape)) if shape else 1
+            ptr = R.ref_param_data(self.h, i)
+            out.append((name, np.ctypeslib.as_array(ptr, shape=(n,)).copy().reshape(shape)))
+        return out
+
+    def bn_ready(self):
+        R = ref()
+        return [int(R.ref_get_bn_ready(self.h, k)) for k in range(R.ref_n_bn(self.h))]
+
     # -- parameters ------------------------------------------------------------------------------
     def load_params(self, g) -> None:
         R = ref()
@@ -291,6 +324,24 @@ class RefNet:
         out = np.zeros((B, T, F, self.output_channels()), np.float32)
         return float(ref().ref_time_forward(self.h, _ptr(x, _f32p), B, T, F, Cin, _ptr(out, _f32p),
                                             int(concurrent), reps))
+
+
+def spec_to_json(text: str) -> str:
+    """The reference's canonical spec JSON: spec_file_to_json(parse_spec_file_json(text))."""
+    buf = C.create_string_buffer(1 << 16)
+    if ref().ref_spec_to_json(text.encode(), buf, len(buf)):
+        raise RefError(1, ref().ref_last_error().decode())
+    return buf.value.decode()
+
+
+def solve_spec_width(text: str, target: int, tol: float = 0.01):
+    """solve_spec_width (netspec.cpp:147-153) -> (found, width, params, lo_width, hi_width)."""
+    found, width, lo, hi = (C.c_int32() for _ in range(4))
+    params = C.c_int64()
+    if ref().ref_solve_spec_width(text.encode(), target, tol, C.byref(found), C.byref(width), C.byref(params),
+                                  C.byref(lo), C.byref(hi)):
+        raise RefError(1, ref().ref_last_error().decode())
+    return bool(found.value), width.value, params.value, lo.value, hi.value
 
 
 # ---------------------------------------------------------------------------------------------

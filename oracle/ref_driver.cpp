@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "conetrx/channel.hpp"
+#include "conetrx/netspec.hpp"
 #include "conetrx/network.hpp"
 #include "conetrx/pilots.hpp"
 #include "conetrx/qam.hpp"
@@ -252,6 +253,38 @@ int ref_save_checkpoint(void* h, const char* path) {
 }
 int ref_load_checkpoint(void* h, const char* path) {
   return guarded([&] { conetrx::load_checkpoint(*net(h), path); });
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Spec files (netspec.cpp:160-257): JSON -> SpecFile -> canonical JSON / network / width solve
+// ---------------------------------------------------------------------------------------------
+int ref_spec_to_json(const char* text, char* out, int cap) {
+  return guarded([&] {
+    const std::string j = conetrx::spec_file_to_json(conetrx::parse_spec_file_json(text));
+    if (static_cast<int>(j.size()) + 1 > cap) throw std::runtime_error("output buffer too small");
+    std::memcpy(out, j.c_str(), j.size() + 1);
+  });
+}
+void* ref_net_from_spec(const char* text) {
+  Network<float>* out = nullptr;
+  int rc = guarded([&] {
+    const conetrx::SpecFile f = conetrx::parse_spec_file_json(text);
+    out = f.is_conet() ? new Network<float>(conetrx::build_conet<float>(f.to_conet()))
+                       : new Network<float>(conetrx::build_net<float>(f.to_deeprx()));
+  });
+  return rc ? nullptr : out;
+}
+int ref_solve_spec_width(const char* text, long long target, double tol, int* found, int* width,
+                         long long* params, int* lo_w, int* hi_w) {
+  return guarded([&] {
+    const auto r = conetrx::solve_spec_width(conetrx::parse_spec_file_json(text), target, tol);
+    *found = r.found ? 1 : 0;
+    *width = r.width;
+    *params = r.params;
+    *lo_w = r.lo_width;
+    *hi_w = r.hi_width;
+  });
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -67,7 +67,10 @@ class Param:
 class Graph:
     """Restatement of `conetrx::Network<float>`'s construction API (network.hpp:49-112)."""
 
-    def __init__(self) -> None:
+    def __init__(self, shape_only: bool = False) -> None:
+        # shape_only: parameters are zero-stride views with the right shapes (parameter counting for
+        # width solving without allocating; such a graph cannot be run)
+        self.shape_only = shape_only
         self.nodes: List[Node] = []
         self.params: List[Param] = []
         self.bn_ready: List[int] = []
@@ -84,9 +87,13 @@ class Graph:
         self.nodes.append(n)
         return len(self.nodes) - 1
 
-    def _push_param(self, name: str, value: np.ndarray, learnable: bool) -> int:
+    def _push_param(self, name: str, shape: tuple, learnable: bool, fill: float = 0.0) -> int:
         require(self.find_param(name) < 0, "duplicate parameter name " + name)
-        self.params.append(Param(name, np.ascontiguousarray(value, dtype=np.float32), learnable))
+        if self.shape_only:
+            value = np.broadcast_to(np.float32(fill), shape)
+        else:
+            value = np.full(shape, fill, np.float32)
+        self.params.append(Param(name, value, learnable))
         return len(self.params) - 1
 
     def _check_in(self, inp: int, expected: int) -> None:
@@ -110,17 +117,17 @@ class Graph:
                  dilation_f: int = 1) -> int:
         self._check_in(inp, cin)
         n = Node(OP_CONV, in0=inp, out_channels=cout, dilation_f=dilation_f)
-        n.w = self._push_param(name + ".w", np.zeros((kernel, kernel, cin, cout), np.float32), True)
+        n.w = self._push_param(name + ".w", (kernel, kernel, cin, cout), True)
         if bias:
-            n.b = self._push_param(name + ".b", np.zeros((cout,), np.float32), True)
+            n.b = self._push_param(name + ".b", (cout,), True)
         return self._push(n)
 
     def add_dwconv(self, inp: int, name: str, kernel: int, c: int, bias: bool) -> int:
         self._check_in(inp, c)
         n = Node(OP_DWCONV, in0=inp, out_channels=c)
-        n.w = self._push_param(name + ".w", np.zeros((kernel, kernel, c, 1), np.float32), True)
+        n.w = self._push_param(name + ".w", (kernel, kernel, c, 1), True)
         if bias:
-            n.b = self._push_param(name + ".b", np.zeros((c,), np.float32), True)
+            n.b = self._push_param(name + ".b", (c,), True)
         return self._push(n)
 
     def add_relu(self, inp: int) -> int:
@@ -129,11 +136,11 @@ class Graph:
     def add_norm(self, inp: int, kind: str, name: str, channels: int) -> int:
         self._check_in(inp, channels)
         n = Node(OP_BN if kind == "bn" else OP_LN, in0=inp, out_channels=channels)
-        n.gamma = self._push_param(name + ".g", np.ones((channels,), np.float32), True)
-        n.beta = self._push_param(name + ".s", np.zeros((channels,), np.float32), True)
+        n.gamma = self._push_param(name + ".g", (channels,), True, 1.0)
+        n.beta = self._push_param(name + ".s", (channels,), True)
         if kind == "bn":
-            n.rmean = self._push_param(name + ".rm", np.zeros((channels,), np.float32), False)
-            n.rvar = self._push_param(name + ".rv", np.ones((channels,), np.float32), False)
+            n.rmean = self._push_param(name + ".rm", (channels,), False)
+            n.rvar = self._push_param(name + ".rv", (channels,), False, 1.0)
             n.bn_flag = len(self.bn_ready)
             self.bn_ready.append(0)
             self.bn_flag_names.append(name + ".rm")
@@ -357,10 +364,10 @@ def _append_block(g: Graph, cur: int, cur_ch: int, blk: BlockSpec, prefix: str) 
     return g.add_binary(OP_ADD, t, skip), f
 
 
-def build_net(spec: NetSpec, prefix: str = "main") -> Graph:
+def build_net(spec: NetSpec, prefix: str = "main", shape_only: bool = False) -> Graph:
     """build_net (network.hpp:470-483)"""
     require(len(spec.blocks) > 0, "net spec needs at least one block")
-    g = Graph()
+    g = Graph(shape_only)
     inp = g.add_input(spec.in_channels)
     cur = g.add_relu(g.add_conv(inp, prefix + ".in", spec.kernel, spec.in_channels, spec.input_filters, True))
     ch = spec.input_filters
@@ -371,11 +378,11 @@ def build_net(spec: NetSpec, prefix: str = "main") -> Graph:
     return g
 
 
-def build_conet(spec: CoNetSpec) -> Graph:
+def build_conet(spec: CoNetSpec, shape_only: bool = False) -> Graph:
     """build_conet (network.hpp:490-562)"""
     spec.validate()
     m_count = len(spec.supports)
-    g = Graph()
+    g = Graph(shape_only)
     inp = g.add_input(spec.main.in_channels)
     mcur = g.add_relu(g.add_conv(inp, "main.in", spec.main.kernel, spec.main.in_channels,
                                  spec.main.input_filters, True))
