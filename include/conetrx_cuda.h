@@ -141,6 +141,38 @@ int cnrx_read_profile(cnrx_plan* plan, int32_t max_n, float* ms, int32_t* counts
 const char* cnrx_launch_name(const cnrx_plan* plan, int32_t i);
 int64_t cnrx_launch_flops(const cnrx_plan* plan, int32_t i);
 
+/* ---------------------------------------------------------------------------------------------
+ * On-GPU synthetic slots and BER.  The reference's slot model (SPEC.md:212-220
+ * generate_tti, qam.cpp:10-52, pilots.cpp:13-31, TDL/Jakes channel.cpp:37-111, AWGN, optional
+ * co-channel QPSK interferer) with Philox4x32-10 random draws addressed by (index, purpose, slot) under
+ * `seed`, so any slot range is reproducible independently (slot numbers slot0 .. slot0+B-1).
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t T, F, N;
+  int32_t mod_order;          /* 4, 16 or 64 (Gray, qam.cpp:42-52) */
+  int32_t n_taps;
+  int32_t pilot_spacing;      /* pilot every `spacing`-th subcarrier on the pilot symbols */
+  int32_t n_pilot_symbols;    /* <= 8 */
+  int32_t has_interferer;     /* config 3: QPSK interferer through an independent channel */
+  int32_t pilot_symbols[8];
+  double rms_delay_s;         /* 0: exponential PDP e^{-l} over the taps */
+  double tap_spacing_s;       /* 0: rms/3, or 1/(F scs) when rms is 0 */
+  double doppler_max_hz;      /* per-slot Doppler ~ U[0, max] */
+  double scs_hz;
+  double cp_fraction;
+  double snr_db_lo, snr_db_hi;
+  double sir_db_lo, sir_db_hi;
+} cnrx_link;
+
+/* y_dev: [B,T,F,N] complex (re,im) fp32; bits_dev: [B,T,F,bits] u8 (0 on pilot REs); h_dev (nullable):
+ * [B,T,F,N] complex user channel.  Asynchronous on `stream` (NULL: the legacy default stream). */
+int cnrx_generate_slots(const cnrx_link* link, int64_t B, uint64_t seed, uint64_t slot0, float* y_dev,
+                        uint8_t* bits_dev, float* h_dev, void* stream);
+/* Per-slot hard-decision bit errors (LLR > 0 => bit 1) over data REs (data_mask_dev [T,F]
+ * u8, 1 = data; pilots excluded): errors_dev [B] u64.  Asynchronous on `stream`. */
+int cnrx_count_bit_errors(const float* llr_dev, const uint8_t* bits_dev, const uint8_t* data_mask_dev, int64_t B,
+                          int64_t T, int64_t F, int32_t bits, unsigned long long* errors_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

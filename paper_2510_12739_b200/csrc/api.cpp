@@ -32,6 +32,7 @@
 #include "common.h"
 #include "conv_tc.h"
 #include "conv_ws.h"
+#include "slotgen.h"
 #include "kernels.h"
 
 using namespace cnrx;
@@ -1582,6 +1583,74 @@ int cnrx_receive_sharded(cnrx_plan* const* plans, int32_t n_plans, const float* 
     if (rcs[static_cast<size_t>(i)] != CNRX_OK)
       return fail(rcs[static_cast<size_t>(i)], "shard " + std::to_string(i) + ": " + msgs[static_cast<size_t>(i)]);
   return CNRX_OK;
+}
+
+
+int cnrx_generate_slots(const cnrx_link* link, int64_t B, uint64_t seed, uint64_t slot0, float* y_dev,
+                        uint8_t* bits_dev, float* h_dev, void* stream) {
+  return guarded([&] {
+    require(link != nullptr, "null link");
+    require(B > 0, "batch must be positive");
+    require(y_dev && bits_dev, "null output pointer");
+    SlotGenHost host;
+    slotgen_prepare(*link, &host);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int L = link->n_taps, nch = link->has_interferer ? 2 : 1;
+    const size_t tf = static_cast<size_t>(link->T) * link->F;
+    // small per-call device scratch: pilots, tap profile, Jakes taps
+    const size_t taps_bytes = static_cast<size_t>(B) * nch * link->T * link->N * L * sizeof(float2);
+    const size_t bytes = tf + tf * sizeof(float2) + L * sizeof(float) + L * sizeof(double) + taps_bytes + 64;
+    char* scratch = nullptr;
+    CNRX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes + 256, s));
+    char* q = scratch;
+    auto take = [&](size_t n) {
+      char* r = q;
+      q += (n + 15) & ~size_t(15);
+      return r;
+    };
+    uint8_t* pmask = reinterpret_cast<uint8_t*>(take(tf));
+    float2* pvals = reinterpret_cast<float2*>(take(tf * sizeof(float2)));
+    float* gain = reinterpret_cast<float*>(take(L * sizeof(float)));
+    double* tau = reinterpret_cast<double*>(take(L * sizeof(double)));
+    float2* taps = reinterpret_cast<float2*>(take(taps_bytes));
+    CNRX_CUDA(cudaMemcpyAsync(pmask, host.pmask.data(), tf, cudaMemcpyHostToDevice, s));
+    CNRX_CUDA(cudaMemcpyAsync(pvals, host.pvals.data(), tf * sizeof(float2), cudaMemcpyHostToDevice, s));
+    CNRX_CUDA(cudaMemcpyAsync(gain, host.gain.data(), L * sizeof(float), cudaMemcpyHostToDevice, s));
+    CNRX_CUDA(cudaMemcpyAsync(tau, host.tau.data(), L * sizeof(double), cudaMemcpyHostToDevice, s));
+    SlotGenArgs a{};
+    a.B = B;
+    a.T = link->T;
+    a.F = link->F;
+    a.N = link->N;
+    a.L = L;
+    a.nb = host.nb;
+    a.has_interferer = link->has_interferer ? 1 : 0;
+    a.scs = link->scs_hz;
+    a.tsym = (1.0 + link->cp_fraction) / link->scs_hz;
+    a.doppler_max = link->doppler_max_hz;
+    a.snr_lo = link->snr_db_lo;
+    a.snr_hi = link->snr_db_hi;
+    a.sir_lo = link->sir_db_lo;
+    a.sir_hi = link->sir_db_hi;
+    a.seed = seed;
+    a.slot0 = slot0;
+    a.pmask = pmask;
+    a.pvals = pvals;
+    a.tap_gain = gain;
+    a.tau = tau;
+    slotgen_launch(a, taps, reinterpret_cast<float2*>(y_dev), bits_dev, reinterpret_cast<float2*>(h_dev), s);
+    CNRX_CUDA(cudaFreeAsync(scratch, s));
+    // host vectors of `host` are pageable: the copies above completed before cudaMemcpyAsync returned
+  });
+}
+
+int cnrx_count_bit_errors(const float* llr_dev, const uint8_t* bits_dev, const uint8_t* data_mask_dev, int64_t B,
+                          int64_t T, int64_t F, int32_t bits, unsigned long long* errors_dev, void* stream) {
+  return guarded([&] {
+    require(llr_dev && bits_dev && data_mask_dev && errors_dev, "null pointer");
+    require(B > 0 && T > 0 && F > 0 && bits > 0, "dimensions must be positive");
+    ber_launch(llr_dev, bits_dev, data_mask_dev, B, T * F * bits, bits, errors_dev, static_cast<cudaStream_t>(stream));
+  });
 }
 
 int cnrx_get_plan_info(const cnrx_plan* plan, cnrx_plan_info* info) {

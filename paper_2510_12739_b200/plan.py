@@ -71,12 +71,22 @@ class cnrx_plan_info(C.Structure):
                 ("macs_per_re", C.c_int64), ("rows_per_slot", C.c_int64), ("workspace_bytes", C.c_int64)]
 
 
+class cnrx_link(C.Structure):
+    _fields_ = [("T", C.c_int32), ("F", C.c_int32), ("N", C.c_int32), ("mod_order", C.c_int32),
+                ("n_taps", C.c_int32), ("pilot_spacing", C.c_int32), ("n_pilot_symbols", C.c_int32),
+                ("has_interferer", C.c_int32), ("pilot_symbols", C.c_int32 * 8), ("rms_delay_s", C.c_double),
+                ("tap_spacing_s", C.c_double), ("doppler_max_hz", C.c_double), ("scs_hz", C.c_double),
+                ("cp_fraction", C.c_double), ("snr_db_lo", C.c_double), ("snr_db_hi", C.c_double),
+                ("sir_db_lo", C.c_double), ("sir_db_hi", C.c_double)]
+
+
 _lib = None
 
 EXPORTED = ["cnrx_plan_create", "cnrx_plan_destroy", "cnrx_last_error", "cnrx_forward", "cnrx_forward_device",
             "cnrx_set_pilots", "cnrx_receive", "cnrx_receive_device", "cnrx_featurize_device",
             "cnrx_receive_sharded", "cnrx_get_plan_info", "cnrx_set_graph_capture", "cnrx_launch_name",
-            "cnrx_set_profiling", "cnrx_read_profile", "cnrx_launch_flops"]
+            "cnrx_set_profiling", "cnrx_read_profile", "cnrx_launch_flops", "cnrx_generate_slots",
+            "cnrx_count_bit_errors"]
 
 
 def lib():
@@ -111,6 +121,8 @@ def lib():
     L.cnrx_launch_flops.argtypes = [vp, C.c_int32]
     L.cnrx_read_profile.argtypes = [vp, C.c_int32, C.POINTER(C.c_float), C.POINTER(C.c_int32),
                                     C.POINTER(C.c_int32)]
+    L.cnrx_generate_slots.argtypes = [C.POINTER(cnrx_link), i64, C.c_uint64, C.c_uint64, vp, vp, vp, vp]
+    L.cnrx_count_bit_errors.argtypes = [vp, vp, vp, i64, i64, i64, C.c_int32, vp, vp]
     for fn in EXPORTED:
         if fn not in ("cnrx_plan_destroy", "cnrx_last_error", "cnrx_launch_name"):
             getattr(L, fn).restype = C.c_int
@@ -276,3 +288,55 @@ def receive_sharded(plans, y: np.ndarray) -> np.ndarray:
     _check(lib().cnrx_receive_sharded(arr, len(plans), y.view(np.float32).ctypes.data_as(C.POINTER(C.c_float)),
                                       B, T, F, N, _f32p(out)))
     return out
+
+
+# ---------------------------------------------------------------------------------------------
+# On-GPU synthetic slots + BER (cnrx_generate_slots / cnrx_count_bit_errors)
+# ---------------------------------------------------------------------------------------------
+def link_struct(link) -> cnrx_link:
+    """A paper_2510_12739_b200.graph.LinkSpec as the C ABI's cnrx_link."""
+    require_ps = list(link.pilot_symbols)
+    if len(require_ps) > 8:
+        raise ValueError("at most 8 pilot symbols")
+    ln = cnrx_link()
+    ln.T, ln.F, ln.N, ln.mod_order, ln.n_taps = link.T, link.F, link.N, link.mod_order, link.n_taps
+    ln.pilot_spacing, ln.n_pilot_symbols = link.pilot_spacing, len(require_ps)
+    for i, t in enumerate(require_ps):
+        ln.pilot_symbols[i] = t
+    ln.has_interferer = 1 if link.sir_db is not None else 0
+    ln.rms_delay_s, ln.tap_spacing_s, ln.doppler_max_hz = link.rms_delay_s, link.tap_spacing_s, link.doppler_max_hz
+    ln.scs_hz, ln.cp_fraction = link.scs_hz, link.cp_fraction
+    ln.snr_db_lo, ln.snr_db_hi = link.snr_db
+    if link.sir_db is not None:
+        ln.sir_db_lo, ln.sir_db_hi = link.sir_db
+    return ln
+
+
+def generate_slots_device(link, B: int, seed: int, slot0: int = 0, with_h: bool = False,
+                          stream: Optional[int] = None):
+    """Synthetic slots generated on the current CUDA device -> (y complex64 [B,T,F,N], bits uint8
+    [B,T,F,b][, h complex64 [B,T,F,N]]) torch tensors.  Asynchronous on `stream` (default: torch's
+    current stream)."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    y = torch.empty((B, link.T, link.F, link.N), dtype=torch.complex64, device=dev)
+    bits = torch.empty((B, link.T, link.F, link.bits), dtype=torch.uint8, device=dev)
+    h = torch.empty_like(y) if with_h else None
+    st = torch.cuda.current_stream().cuda_stream if stream is None else stream
+    ln = link_struct(link)
+    _check(lib().cnrx_generate_slots(C.byref(ln), B, seed, slot0, y.data_ptr(), bits.data_ptr(),
+                                     h.data_ptr() if h is not None else None, _stream(st)))
+    return (y, bits, h) if with_h else (y, bits)
+
+
+def count_bit_errors(llr, bits, data_mask, stream: Optional[int] = None):
+    """Per-slot hard-decision bit errors over data REs, on the device: llr [B,T,F,b] fp32, bits
+    [B,T,F,b] uint8, data_mask [T,F] (bool/uint8, 1 = data RE) -> int64 tensor [B]."""
+    import torch
+    B, T, F, nb = llr.shape
+    mask = data_mask.to(device=llr.device, dtype=torch.uint8).contiguous()
+    err = torch.empty((B,), dtype=torch.int64, device=llr.device)
+    st = torch.cuda.current_stream().cuda_stream if stream is None else stream
+    _check(lib().cnrx_count_bit_errors(llr.contiguous().data_ptr(), bits.contiguous().data_ptr(), mask.data_ptr(),
+                                       B, T, F, nb, err.data_ptr(), _stream(st)))
+    return err
