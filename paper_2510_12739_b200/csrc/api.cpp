@@ -1075,16 +1075,20 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
       static unsigned long long* dtrace = nullptr;
       if (GL.ws) {
         if (trace) {
-          if (!dtrace) CNRX_CUDA(cudaMalloc(&dtrace, 16 * sizeof(unsigned long long)));
-          CNRX_CUDA(cudaMemsetAsync(dtrace, 0, 16 * sizeof(unsigned long long), s));
+          if (!dtrace) CNRX_CUDA(cudaMalloc(&dtrace, 32 * sizeof(unsigned long long)));
+          CNRX_CUDA(cudaMemsetAsync(dtrace, 0, 32 * sizeof(unsigned long long), s));
           GL.wsl.trace = dtrace;
         }
+        static const int ws_debug = getenv("CNRX_WS_DEBUG") ? atoi(getenv("CNRX_WS_DEBUG")) : 0;
+        GL.wsl.debug = ws_debug;
         p.note(conv_ws64_launch(GL.wsl, p.num_sms, s), s, fl);
         if (trace) {
-          unsigned long long h[16];
+          unsigned long long h[kWsTraceSlots];
           CNRX_CUDA(cudaMemcpyAsync(h, dtrace, sizeof h, cudaMemcpyDeviceToHost, s));
           CNRX_CUDA(cudaStreamSynchronize(s));
           const double nt = static_cast<double>(h[kTraceTiles] ? h[kTraceTiles] : 1);
+          fprintf(stderr, "[trace] conv_ws64 MMA loop-back %.0f commit %.0f cycles/tile\n", h[kWsTraceLoop] / nt,
+                  h[kWsTraceCommit] / nt);
           fprintf(stderr,
                   "[trace] conv_ws64 tiles=%llu per-tile cycles: prod_wait %.0f mma_wait_full %.0f mma_wait_tmem %.0f "
                   "mma_issue %.0f | epi_wait %.0f combine %.0f stage_wait %.0f write %.0f | total/tile %.0f\n",
@@ -1096,8 +1100,8 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
         continue;
       }
       if (trace) {
-        if (!dtrace) CNRX_CUDA(cudaMalloc(&dtrace, 16 * sizeof(unsigned long long)));
-        CNRX_CUDA(cudaMemsetAsync(dtrace, 0, 16 * sizeof(unsigned long long), s));
+        if (!dtrace) CNRX_CUDA(cudaMalloc(&dtrace, 32 * sizeof(unsigned long long)));
+        CNRX_CUDA(cudaMemsetAsync(dtrace, 0, 32 * sizeof(unsigned long long), s));
         GL.tc.trace = dtrace;
       }
       p.note(conv_tc_launch(op0.cin, op0.cout, op0.ks, GL.tc, p.num_sms, s), s, fl);

@@ -84,7 +84,30 @@ __device__ __forceinline__ void epi_group_sync(int e) {
 // Epilogue variant flags (compile-time so the unrolled epilogue carries no per-element branches);
 // kWsDynamic reads them from the launch instead.
 enum : int { kWsRes = 1, kWsOut2 = 2, kWsOut2Bn = 4, kWsRelu = 8, kWsReluIn = 16, kWsDynamic = -1 };
-constexpr int kWsThreads = 608;  // 19 warps: producer, MMA, 16 epilogue, input-ReLU
+constexpr int kWsThreads = 640;  // 20 warps: producer, MMA (stage 0), 16 epilogue, input-ReLU, MMA (stage 1)
+
+// In-place ReLU of 16-byte chunks [lo, hi) of a shared-memory window, one warp, batches of 16 chunks per
+// lane so all loads are in flight before the first store (shared-memory latency is long while the
+// tensor core streams the other stages).
+__device__ __forceinline__ void relu_chunks(uint32_t win, int lo, int hi, int lane) {
+  const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
+  for (int c0 = lo; c0 < hi; c0 += 32 * 16) {
+    uint4 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int c = c0 + u * 32 + lane;
+      if (c < hi) v[u] = lds128(win + static_cast<uint32_t>(c) * 16u);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int c = c0 + u * 32 + lane;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v[u]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __hmax2(h[i], z);
+      if (c < hi) sts128(win + static_cast<uint32_t>(c) * 16u, v[u]);
+    }
+  }
+}
 
 template <int FL>
 __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_constant__ WsLaunch L) {
@@ -121,7 +144,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
     for (int s = 0; s < L.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&ready[s], 1);
+      mbar_init(&ready[s], 1);  // input ReLU done (warp 18)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -163,15 +186,26 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
   __syncthreads();
   tc_fence_after();
 
+  // input ReLU of one window (relu_in), by warp 18
+  const int relu_n = (kN + 1 + 2 * grp.halo) * (kRB / 16);  // only the rows the UMMAs read
+  auto relu_stage = [&](int jr, int lo, int hi) {
+    const int s = jr % L.stages;
+    mbar_wait(&full[s], static_cast<uint32_t>(jr / L.stages) & 1u);
+    if (!(L.debug & 2)) relu_chunks(smem_u32(smem + lay.win_off + s * lay.win_stage), lo, hi, lane);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ready[s]);
+  };
+
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------
-    if (lane == 0) {
-      prefetch_tmap(&grp.in_map);
-      const int nboxes = (kN + 1 + 2 * grp.halo + kBox - 1) / kBox;
-      const uint32_t stage_tx = static_cast<uint32_t>(nboxes * kBox * kRB);
-      long long tr_prod = 0;
-      int j = 0;
-      for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
+    if (lane == 0) prefetch_tmap(&grp.in_map);
+    const int nboxes = (kN + 1 + 2 * grp.halo + kBox - 1) / kBox;
+    const uint32_t stage_tx = static_cast<uint32_t>(nboxes * kBox * kRB);
+    long long tr_prod = 0;
+    int j = 0;
+    for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
+      if (lane == 0) {
         const int s = j % L.stages;
         const uint32_t k = static_cast<uint32_t>(j / L.stages);
         const int64_t p0 = tile * kTileRows;
@@ -184,11 +218,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
         for (int bx = 0; bx < nboxes; ++bx)
           tma_load_2d(win + bx * kBox * kRB, &grp.in_map, &full[s], 0, r0 + bx * kBox);
       }
-      if (L.trace) atomicAdd(&L.trace[kTraceProdWaitEmpty], static_cast<unsigned long long>(tr_prod));
     }
-  } else if (warp == 1) {
-    // ------------------------------ MMA issuer --------------------------------
+    if (L.trace && lane == 0) atomicAdd(&L.trace[kTraceProdWaitEmpty], static_cast<unsigned long long>(tr_prod));
+  } else if (warp == 1 || warp == 19) {
+    // ------------------------------ MMA issuers --------------------------------
+    // Two issuing warps, one per accumulator stage (alternate tiles): the UMMA queue is shallow, so a
+    // single issuer's per-tile barrier waits, commits and loop overhead leave the tensor pipe idle;
+    // with two, one warp's tile keeps the pipe fed while the other does its bookkeeping.  Each warp's
+    // tcgen05.commit tracks only its own UMMAs.
     // pair p: A-half tap (dt = -1 or +1, df), B-half tap dt + 1 (real for the first three pairs)
+    const int me = warp == 1 ? 0 : 1;
     int32_t shift[kPairs];
 #pragma unroll
     for (int p = 0; p < kPairs; ++p) {
@@ -196,14 +235,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
       const int dt = p < 3 ? -1 : 1;
       shift[p] = grp.halo + dt + df * grp.dil * L.geo.T1;
     }
-    long long tr_full = 0, tr_tmem = 0, tr_issue = 0;
+    long long tr_full = 0, tr_tmem = 0, tr_issue = 0, tr_loop = 0, tr_commit = 0;
     const long long t_start = clock64();
     const unsigned long long g_start = globaltimer_ns();
-    int j = 0;
-    for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
+    long long t_prev_end = t_start;
+    int j = me;
+    for (int64_t tile = local + static_cast<int64_t>(me) * nct; tile < n_tiles; tile += 2 * static_cast<int64_t>(nct), j += 2) {
       const int s = j % L.stages;
       const int a = j & 1;
       const long long tm0 = clock64();
+      tr_loop += tm0 - t_prev_end;
       mbar_wait(relu_in ? &ready[s] : &full[s], static_cast<uint32_t>(j / L.stages) & 1u);
       const long long tm1 = clock64();
       mbar_wait(&tempty[a], (static_cast<uint32_t>(j >> 1) & 1u) ^ 1u);
@@ -224,19 +265,25 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
                          (p | kk) != 0 ? 1u : 0u);
           }
         }
+        const long long tc0 = clock64();
         umma_commit(&empty[s]);
         umma_commit(&tfull[a]);
+        tr_commit += clock64() - tc0;
       }
       __syncwarp();
-      tr_issue += clock64() - tm2;
+      t_prev_end = clock64();
+      tr_issue += t_prev_end - tm2;
     }
-    if (L.trace && lane == 0) {
+    if (L.trace && lane == 0 && me == 0) {  // per-tile figures of stage 0's issuer (half the tiles)
+      j >>= 1;
       atomicAdd(&L.trace[kTraceTotal], static_cast<unsigned long long>(clock64() - t_start));
       trace_cta_window(L.trace, g_start);
       atomicAdd(&L.trace[kTraceMmaWaitFull], static_cast<unsigned long long>(tr_full));
       atomicAdd(&L.trace[kTraceMmaWaitTmem], static_cast<unsigned long long>(tr_tmem));
       atomicAdd(&L.trace[kTraceMmaIssue], static_cast<unsigned long long>(tr_issue));
       atomicAdd(&L.trace[kTraceTiles], static_cast<unsigned long long>(j));
+      atomicAdd(&L.trace[kWsTraceLoop], static_cast<unsigned long long>(tr_loop));
+      atomicAdd(&L.trace[kWsTraceCommit], static_cast<unsigned long long>(tr_commit));
     }
   } else if (warp == 18) {
     // ------------------------------ input ReLU (relu_in) ----------------------
@@ -244,25 +291,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
     // 16-byte shared accesses, then fence the generic writes to the async proxy before the MMA warp
     // may read them.
     if (relu_in) {
-      const int nchunks = (kN + 1 + 2 * grp.halo) * (kRB / 16);  // only the rows the UMMAs read
-      const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
       int j = 0;
-      for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
-        const int s = j % L.stages;
-        mbar_wait(&full[s], static_cast<uint32_t>(j / L.stages) & 1u);
-        uint4* win = reinterpret_cast<uint4*>(smem + lay.win_off + s * lay.win_stage);
-#pragma unroll 4
-        for (int c = lane; c < nchunks; c += 32) {
-          uint4 v = win[c];
-          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) h[i] = __hmax2(h[i], z);
-          win[c] = v;
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ready[s]);
-      }
+      for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) relu_stage(j, 0, relu_n);
     }
   } else {
     // ------------------------------ epilogue (warps 2..17) --------------------
@@ -396,15 +426,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
           }
           const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
           const uint32_t off = sw128(row, static_cast<uint32_t>((2 * q + blk) * 16));
-          stsm_x4_trans(stg_a + off, o);
-          if (has_out2) stsm_x4_trans(stg_a + 128 * kRB + off, o2);
+          if (!(L.debug & 1)) {
+            stsm_x4_trans(stg_a + off, o);
+            if (has_out2) stsm_x4_trans(stg_a + 128 * kRB + off, o2);
+          }
         }
       }
       const long long te3 = clock64();
       tr_comb += te3 - te2;
       fence_proxy_async_smem();
       epi_group_sync(e);
-      if (lead) {
+      if (lead && !(L.debug & 1)) {
         tma_store_2d(&grp.out_map, stg, 0, static_cast<int32_t>(p0));
         if (has_out2) tma_store_2d(&grp.out2_map, stg + 128 * kRB, 0, static_cast<int32_t>(p0));
         bulk_commit();

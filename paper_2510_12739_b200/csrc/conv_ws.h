@@ -23,10 +23,13 @@ struct WsLaunch {
   WsGroup g[4];
   PlaneGeom geo;
   int64_t n_tiles;   // 127-row output tiles
-  int32_t ngroups, stages, win_alloc, pad_;
+  int32_t ngroups, stages, win_alloc;
+  int32_t debug;     // experiments only (CNRX_WS_DEBUG): bit 0 skip staging writes + stores, bit 1 skip input ReLU pass
   unsigned long long* trace;  // debug: per-role clock64 totals (kTrace* in conv_tc.h + kWsTrace*)
 };
 enum : int { kWsTraceCombine = 8, kWsTraceStageWait, kWsTraceWrite, kWsTraceN };
+// slots 12..15 hold the CTA window (sm100.cuh trace_cta_window); 16, 17: MMA loop-back and commit cycles
+enum : int { kWsTraceLoop = 16, kWsTraceCommit = 17, kWsTraceSlots = 18 };
 
 size_t conv_ws64_wimg_bytes();
 // w: fp32 [3,3,64,64] reference layout, scale: per-output-channel BN fold (nullable)

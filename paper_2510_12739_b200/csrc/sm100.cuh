@@ -281,4 +281,14 @@ __device__ __forceinline__ uint8_t* smem_align1024(uint8_t* smem_dyn) {
   const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dyn));
   return smem_dyn + ((1024u - (a & 1023u)) & 1023u);
 }
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 }  // namespace cnrx
