@@ -1332,7 +1332,8 @@ int pipeline_chunks(const cnrx_plan& p, int64_t B) {
     const int n = std::atoi(e);
     if (n >= 1) return static_cast<int>(std::min<int64_t>(n, B));
   }
-  return B >= 64 ? 8 : (B >= 8 ? 2 : 1);
+  // measured on cfg2 (B=256): 3-4 chunks maximise e2e; more chunks pay each launch's fixed cost again
+  return static_cast<int>(std::min<int64_t>(4, std::max<int64_t>(1, B / 48)));
 }
 
 template <class Run>
