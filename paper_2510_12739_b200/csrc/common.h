@@ -5,7 +5,9 @@
 
 #include <cstdint>
 #include <stdexcept>
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 namespace cnrx {
 
@@ -113,4 +115,23 @@ inline void require(bool cond, const std::string& msg) {
   if (!cond) throw Error(1, msg);
 }
 
+
+// Launch `kernel` with programmatic stream serialization (PDL) unless CNRX_NO_PDL is set; the kernel
+// must call pdl_wait() (sm100.cuh) before reading or writing activations.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  static const bool no_pdl = std::getenv("CNRX_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CNRX_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 }  // namespace cnrx

@@ -151,6 +151,8 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // PDL: the prologue above overlapped the previous kernel's tail
 
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------
@@ -452,8 +454,7 @@ const char* launch_t(const TcLaunch& L, int num_sms, cudaStream_t stream) {
   int grid = static_cast<int>(work < slots ? work : slots);
   if (grid < L.ngroups) grid = L.ngroups;
   if (L.trace) fprintf(stderr, "[trace] conv_tc %d CTAs/SM (regs %d, smem %u B), grid %d\n", per_sm, regs, lay.total, grid);
-  kern<<<grid, 192, lay.total, stream>>>(L);
-  CNRX_CUDA(cudaGetLastError());
+  launch_pdl(kern, dim3(grid), dim3(192), lay.total, stream, L);
   static char name[96];
   snprintf(name, sizeof name, "conv_tc_kernel<%d,%d,%d>", CIN, COUT, KS);
   return name;

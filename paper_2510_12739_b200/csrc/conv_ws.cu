@@ -185,6 +185,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // everything above is independent of the previous kernel (PDL: it overlapped that kernel's tail)
+  pdl_trigger();
+  pdl_wait();
 
   // input ReLU of one window (relu_in), by warp 18
   const int relu_n = (kN + 1 + 2 * grp.halo) * (kRB / 16);  // only the rows the UMMAs read
@@ -547,9 +550,9 @@ void launch_fl(const WsLaunch& L, const WsLayout& lay, int grid, cudaStream_t st
                                    static_cast<int>(lay.total)));
     configured = static_cast<int>(lay.total);
   }
-  conv_ws64_kernel<FL><<<grid, kWsThreads, lay.total, stream>>>(L);
+  launch_pdl(conv_ws64_kernel<FL>, dim3(grid), dim3(kWsThreads), lay.total, stream, L);
   const cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) {
+  if (err != cudaSuccess) {  // (launch_pdl throws on launch errors; this catches sticky ones)
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, conv_ws64_kernel<FL>);
     throw Error(4, std::string("conv_ws64 launch failed: ") + cudaGetErrorString(err) + " (regs " +

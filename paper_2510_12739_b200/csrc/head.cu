@@ -86,6 +86,8 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
   for (int e = tid; e < kHC * NB; e += kThreads) s_w[e] = L.head_w[e];
   if (tid < NB) s_b[tid] = L.head_b[tid];
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();  // PDL: the prologue above overlapped the previous kernel's tail
 
   const int64_t n_tiles = L.geo.Nalloc / kHRows;
   if (tid >= kConsumers) {
@@ -212,8 +214,7 @@ void launch_t(const HeadLaunch& L, int stages_bytes_total, cudaStream_t s) {
   const int per_sm = stages_bytes_total * 2 + 4096 <= 228 * 1024 ? 2 : 1;
   const int64_t slots = static_cast<int64_t>(per_sm) * sms;
   const unsigned grid = static_cast<unsigned>(n_tiles < slots ? n_tiles : slots);
-  head_tma_kernel<C, NB, NS><<<grid, kThreads, stages_bytes_total, s>>>(L);
-  CNRX_CUDA(cudaGetLastError());
+  launch_pdl(head_tma_kernel<C, NB, NS>, dim3(grid), dim3(kThreads), static_cast<size_t>(stages_bytes_total), s, L);
 }
 
 template <int C, int NB>

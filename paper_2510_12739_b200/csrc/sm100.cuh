@@ -291,4 +291,11 @@ __device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
+
+// Programmatic dependent launch: let the next kernel in the stream start its prologue (barrier init,
+// TMEM allocation, weight staging) on SMs this grid has left, and wait for this grid before touching
+// its outputs.  Kernels launched with the PDL attribute must call pdl_wait() before their first
+// global read or write of activation data.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 }  // namespace cnrx

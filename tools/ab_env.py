@@ -19,7 +19,7 @@ for _ in range(reps):
                 env[k] = val
         out = subprocess.run([sys.executable, os.path.join(here, "prof_run.py")], env=env, capture_output=True,
                              text=True).stdout
-        tot = [l for l in out.splitlines() if l.startswith("total")]
+        tot = [l for l in out.splitlines() if l.startswith("step")]
         res[v].append(float(tot[-1].split()[1]) / 1e3)
 for v, xs in res.items():
     print(f"{v:40s} min {min(xs):.3f} ms  median {statistics.median(xs):.3f} ms  ({len(xs)} runs)")

@@ -11,6 +11,14 @@ y = torch.from_numpy(b.y).cuda(); out = torch.empty((B, cfg.link.T, cfg.link.F, 
 for _ in range(3):
     p.receive_device(y, out, 0)
 torch.cuda.synchronize()
+# whole-step time without per-kernel events (those would break programmatic dependent launches)
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(10):
+    p.receive_device(y, out, 0)
+b.record()
+b.synchronize()
+step_ms = a.elapsed_time(b) / 10
 p.set_profiling(True)
 reps = 10
 for _ in range(reps):
@@ -20,4 +28,5 @@ tot = 0.0
 for n, ms, c in p.read_profile():
     tot += ms / reps
     print(f"{n:40s} {ms / reps * 1e3:9.1f} us")
-print(f"{'total':40s} {tot * 1e3:9.1f} us")
+print(f"{'total (sum of kernels)':40s} {tot * 1e3:9.1f} us")
+print(f"{'step':40s} {step_ms * 1e3:9.1f} us")
