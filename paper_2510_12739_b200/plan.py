@@ -19,7 +19,7 @@ import numpy as np
 from . import graph as G
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libconetrx_cuda.so")
+LIB_PATH = os.environ.get("CNRX_LIB") or os.path.join(HERE, "libconetrx_cuda.so")  # CNRX_LIB: A/B builds only
 
 OK, ERR_INVALID_ARGUMENT, ERR_NOT_READY, ERR_UNSUPPORTED, ERR_CUDA = range(5)
 FP32, BF16 = 0, 1
