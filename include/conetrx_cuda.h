@@ -173,6 +173,19 @@ int cnrx_generate_slots(const cnrx_link* link, int64_t B, uint64_t seed, uint64_
 int cnrx_count_bit_errors(const float* llr_dev, const uint8_t* bits_dev, const uint8_t* data_mask_dev, int64_t B,
                           int64_t T, int64_t F, int32_t bits, unsigned long long* errors_dev, void* stream);
 
+/* Per-slot total noise-plus-interference variance of the generated slots (interference as noise:
+ * 10^(-SNR/10) + 10^(-SIR/10) with the interferer's unit-power channel), host output [B]. */
+int cnrx_slot_noise_var(const cnrx_link* link, int64_t B, uint64_t seed, uint64_t slot0, float* noise_var);
+
+/* Classical baseline receiver: LMMSE combining over the N
+ * antennas + exact max-log demapping (Gray QAM, positive LLR => bit 1).  h_dev == NULL: LS estimate with
+ * the plan's pilot grid and the featurizer's interpolation (ls_lmmse); otherwise h_dev [B,T,F,N] complex
+ * is the true channel (perfect_csi_lmmse).  noise_var_dev [B]: total noise(+interference) variance.
+ * llr_dev [B,T,F,bits] fp32.  Asynchronous on `stream` (NULL: the plan's stream). */
+int cnrx_classical_receive(cnrx_plan* plan, const float* y_dev, const float* h_dev, const float* noise_var_dev,
+                           int64_t B, int64_t T, int64_t F, int64_t N, int32_t mod_order, float* llr_dev,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

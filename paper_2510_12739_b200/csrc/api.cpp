@@ -1658,6 +1658,42 @@ int cnrx_count_bit_errors(const float* llr_dev, const uint8_t* bits_dev, const u
   });
 }
 
+int cnrx_slot_noise_var(const cnrx_link* link, int64_t B, uint64_t seed, uint64_t slot0, float* noise_var) {
+  return guarded([&] {
+    require(link != nullptr && noise_var != nullptr, "null pointer");
+    require(B > 0, "batch must be positive");
+    slot_noise_var(*link, B, seed, slot0, noise_var);
+  });
+}
+
+int cnrx_classical_receive(cnrx_plan* plan, const float* y_dev, const float* h_dev, const float* noise_var_dev,
+                           int64_t B, int64_t T, int64_t F, int64_t N, int32_t mod_order, float* llr_dev,
+                           void* stream) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    require(y_dev && noise_var_dev && llr_dev, "null tensor pointer");
+    require(B > 0 && T > 0 && F > 0 && N >= 1 && N <= 8, "bad grid dimensions");
+    require(mod_order == 4 || mod_order == 16 || mod_order == 64, "modulation order must be 4, 16 or 64");
+    const int bits = mod_order == 4 ? 2 : mod_order == 16 ? 4 : 6;
+    DeviceGuard dg(plan->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : plan->stream;
+    const float* feat = nullptr;
+    if (!h_dev) {
+      require(plan->has_pilots, "cnrx_set_pilots must be called before the LS-LMMSE receiver");
+      require(T == plan->pT && F == plan->pF, "received grid does not match the pilot grid");
+      const size_t bytes = static_cast<size_t>(B * T * F * 6 * N) * sizeof(float);
+      float* f = static_cast<float*>(ensure_dev(plan->ws.feat_buf, plan->ws.feat_bytes, bytes));
+      PlaneGeom g = make_geom(static_cast<int>(B), static_cast<int>(T), static_cast<int>(F), 1);
+      launch_featurize_ref(y_dev, g, static_cast<int>(N), plan->pt, f, s);
+      feat = f;
+    }
+    launch_lmmse_demap(feat, reinterpret_cast<const float2*>(y_dev), reinterpret_cast<const float2*>(h_dev),
+                       noise_var_dev, B, static_cast<int>(T), static_cast<int>(F), static_cast<int>(N), bits, llr_dev,
+                       s);
+  });
+}
+
 int cnrx_get_plan_info(const cnrx_plan* plan, cnrx_plan_info* info) {
   if (!plan || !info) return fail(CNRX_ERR_INVALID_ARGUMENT, "null argument");
   std::memset(info, 0, sizeof(*info));

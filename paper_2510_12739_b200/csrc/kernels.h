@@ -29,6 +29,10 @@ struct PilotTablesDev {
 
 const char* launch_featurize_plane(const float* y, const PlaneGeom& geo, int N, const PilotTablesDev& pt,
                                    __nv_bfloat16* plane, int cpad, cudaStream_t s);
+// Classical receiver (classic.cu): LMMSE combining + exact max-log demapping per RE.  Either feat
+// ([B,T,F,6N] featurizer output: y and the LS-interpolated estimate) or y and h ([B,T,F,N] complex).
+const char* launch_lmmse_demap(const float* feat, const float2* y, const float2* h, const float* noise_var, int64_t B,
+                               int T, int F, int N, int bits, float* llr, cudaStream_t s);
 const char* launch_featurize_ref(const float* y, const PlaneGeom& geo, int N, const PilotTablesDev& pt, float* feat,
                                  cudaStream_t s);
 const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_bfloat16* plane, int cpad,

@@ -33,11 +33,12 @@ struct U4 {
   uint32_t x, y, z, w;
 };
 
-__device__ __forceinline__ U4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
+__host__ __device__ __forceinline__ U4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
-    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint64_t p0 = 0xD2511F53ull * c0, p1 = 0xCD9E8D57ull * c2;
+    const uint32_t lo0 = static_cast<uint32_t>(p0), hi0 = static_cast<uint32_t>(p0 >> 32);
+    const uint32_t lo1 = static_cast<uint32_t>(p1), hi1 = static_cast<uint32_t>(p1 >> 32);
     const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
     c0 = n0;
     c1 = lo1;
@@ -54,7 +55,7 @@ struct Draw {
   __device__ U4 operator()(uint32_t purpose, uint32_t index) const { return philox(index, purpose, s0, s1, k0, k1); }
 };
 
-__device__ __forceinline__ float unif(uint32_t w) { return static_cast<float>(w >> 8) * 5.9604644775390625e-8f; }
+__host__ __device__ __forceinline__ float unif(uint32_t w) { return static_cast<float>(w >> 8) * 5.9604644775390625e-8f; }
 
 __device__ __forceinline__ Draw draw_for(const SlotGenArgs& a, int64_t b) {
   const uint64_t slot = a.slot0 + static_cast<uint64_t>(b);
@@ -281,6 +282,23 @@ void slotgen_prepare(const cnrx_link& link, SlotGenHost* h) {
   for (int l = 0; l < L; ++l) {
     h->gain[static_cast<size_t>(l)] = static_cast<float>(std::sqrt(p[static_cast<size_t>(l)] / kSin));
     h->tau[static_cast<size_t>(l)] = l * spacing;
+  }
+}
+
+
+void slot_noise_var(const cnrx_link& link, int64_t B, uint64_t seed, uint64_t slot0, float* out) {
+  for (int64_t b = 0; b < B; ++b) {
+    const uint64_t slot = slot0 + static_cast<uint64_t>(b);
+    const U4 ws = philox(0u, P_SLOT, static_cast<uint32_t>(slot), static_cast<uint32_t>(slot >> 32),
+                         static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+    // same float arithmetic as re_kernel
+    const float snr = static_cast<float>(link.snr_db_lo + (link.snr_db_hi - link.snr_db_lo) * static_cast<double>(unif(ws.x)));
+    float v = std::pow(10.f, -snr / 10.f);
+    if (link.has_interferer) {
+      const float sir = static_cast<float>(link.sir_db_lo + (link.sir_db_hi - link.sir_db_lo) * static_cast<double>(unif(ws.z)));
+      v += std::pow(10.f, -sir / 10.f);
+    }
+    out[b] = v;
   }
 }
 

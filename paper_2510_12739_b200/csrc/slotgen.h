@@ -30,6 +30,8 @@ struct SlotGenArgs {
 };
 
 void slotgen_prepare(const cnrx_link& link, SlotGenHost* h);
+// host restatement of the per-slot draws: total noise + interference variance of slots slot0 .. slot0+B-1
+void slot_noise_var(const cnrx_link& link, int64_t B, uint64_t seed, uint64_t slot0, float* out);
 // taps: device scratch of B * (1 + has_interferer) * T * N * L float2
 void slotgen_launch(const SlotGenArgs& a, float2* taps, float2* y, uint8_t* bits, float2* h, cudaStream_t s);
 void ber_launch(const float* llr, const uint8_t* bits, const uint8_t* data_mask, int64_t B, int64_t per_slot, int nb,

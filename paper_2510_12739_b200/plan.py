@@ -86,7 +86,7 @@ EXPORTED = ["cnrx_plan_create", "cnrx_plan_destroy", "cnrx_last_error", "cnrx_fo
             "cnrx_set_pilots", "cnrx_receive", "cnrx_receive_device", "cnrx_featurize_device",
             "cnrx_receive_sharded", "cnrx_get_plan_info", "cnrx_set_graph_capture", "cnrx_launch_name",
             "cnrx_set_profiling", "cnrx_read_profile", "cnrx_launch_flops", "cnrx_generate_slots",
-            "cnrx_count_bit_errors"]
+            "cnrx_count_bit_errors", "cnrx_slot_noise_var", "cnrx_classical_receive"]
 
 
 def lib():
@@ -123,6 +123,8 @@ def lib():
                                     C.POINTER(C.c_int32)]
     L.cnrx_generate_slots.argtypes = [C.POINTER(cnrx_link), i64, C.c_uint64, C.c_uint64, vp, vp, vp, vp]
     L.cnrx_count_bit_errors.argtypes = [vp, vp, vp, i64, i64, i64, C.c_int32, vp, vp]
+    L.cnrx_slot_noise_var.argtypes = [C.POINTER(cnrx_link), i64, C.c_uint64, C.c_uint64, f32p]
+    L.cnrx_classical_receive.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, C.c_int32, vp, vp]
     for fn in EXPORTED:
         if fn not in ("cnrx_plan_destroy", "cnrx_last_error", "cnrx_launch_name"):
             getattr(L, fn).restype = C.c_int
@@ -340,3 +342,28 @@ def count_bit_errors(llr, bits, data_mask, stream: Optional[int] = None):
     _check(lib().cnrx_count_bit_errors(llr.contiguous().data_ptr(), bits.contiguous().data_ptr(), mask.data_ptr(),
                                        B, T, F, nb, err.data_ptr(), _stream(st)))
     return err
+
+
+def slot_noise_var(link, B: int, seed: int, slot0: int = 0) -> np.ndarray:
+    """Per-slot noise-plus-interference variance of generate_slots_device's slots (host, fp32 [B])."""
+    out = np.empty(B, np.float32)
+    ln = link_struct(link)
+    _check(lib().cnrx_slot_noise_var(C.byref(ln), B, seed, slot0, _f32p(out)))
+    return out
+
+
+def classical_receive_device(plan: "Plan", y, noise_var, mod_order: int, h=None, out=None,
+                             stream: Optional[int] = None):
+    """LS-LMMSE (h=None, the plan's pilot grid) or perfect-CSI LMMSE + max-log LLRs on the device:
+    y / h complex64 [B,T,F,N] torch tensors, noise_var fp32 [B] -> llr fp32 [B,T,F,bits]."""
+    import torch
+    B, T, F, N = y.shape
+    bits = {4: 2, 16: 4, 64: 6}[mod_order]
+    if out is None:
+        out = torch.empty((B, T, F, bits), dtype=torch.float32, device=y.device)
+    nv = torch.as_tensor(noise_var, dtype=torch.float32).to(y.device).contiguous()
+    st = torch.cuda.current_stream().cuda_stream if stream is None else stream
+    _check(lib().cnrx_classical_receive(plan.h, y.contiguous().data_ptr(),
+                                        h.contiguous().data_ptr() if h is not None else None, nv.data_ptr(), B, T, F, N,
+                                        mod_order, out.data_ptr(), _stream(st)))
+    return out

@@ -34,7 +34,7 @@ rows = []
 t_total, slots_total = 0.0, 0
 for lo, hi in zip(bins[:-1], bins[1:]):
     link = dataclasses.replace(cfg.link, snr_db=(float(lo), float(hi)))
-    errs, nbits = 0, 0
+    errs, nbits, e_ls, e_pc = 0, 0, 0, 0
     for k in range(n_batches + 1):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -50,6 +50,13 @@ for lo, hi in zip(bins[:-1], bins[1:]):
         slots_total += B
         errs += int(e.sum().item())
         nbits += B * int(pmask.size - pmask.sum()) * cfg.link.bits
-    rows.append({"snr_db": [float(lo), float(hi)], "ber": errs / nbits, "bits": nbits})
+        # classical baselines on the same slots: LS-LMMSE and perfect-CSI LMMSE
+        yh, _, hh = P.generate_slots_device(link, B, seed=2024, slot0=k * B, with_h=True)
+        nv = P.slot_noise_var(link, B, 2024, k * B)
+        e_ls += int(P.count_bit_errors(P.classical_receive_device(p, yh, nv, link.mod_order), bits, data).sum())
+        e_pc += int(P.count_bit_errors(P.classical_receive_device(p, yh, nv, link.mod_order, h=hh), bits,
+                                       data).sum())
+    rows.append({"snr_db": [float(lo), float(hi)], "ber": errs / nbits, "ber_ls_lmmse": e_ls / nbits,
+                 "ber_perfect_csi_lmmse": e_pc / nbits, "bits": nbits})
 print(json.dumps({"config": name, "batch": B, "device_pipeline_slots_per_s": slots_total / t_total,
-                  "note": "random weights unless a checkpoint is given", "sweep": rows}))
+                  "note": "network: random weights unless a checkpoint is given; LMMSE baselines on the same slots", "sweep": rows}))
