@@ -28,7 +28,7 @@ constexpr int kConsumers = 256;          // two threads per row, C/2 channels ea
 constexpr int kThreads = kConsumers + 32;
 
 struct HeadLayout {
-  uint32_t ring_off, stage_bytes, aff_off, w_off, b_off, bar_off, total;
+  uint32_t ring_off, stage_bytes, aff_off, w_off, b_off, part_off, bar_off, total;
 };
 __host__ __device__ inline HeadLayout head_layout(int c, int ns, int nb, int stages) {
   HeadLayout l{};
@@ -43,6 +43,8 @@ __host__ __device__ inline HeadLayout head_layout(int c, int ns, int nb, int sta
   off += static_cast<uint32_t>(kHC * nb) * 4u;
   l.b_off = off;
   off += 64u;
+  l.part_off = off;  // [2][128 rows][nb] partial GEMV sums of the upper channel half
+  off += 2u * kHRows * static_cast<uint32_t>(nb) * 4u;
   l.bar_off = (off + 15u) & ~15u;
   l.total = l.bar_off + 2u * 8u * static_cast<uint32_t>(stages) + 1024u;
   return l;
@@ -107,7 +109,10 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
     return;
   }
   // ------------------------------ consumers: two threads per row ------------------
-  const int r = tid >> 1, hf = tid & 1;
+  // warp w covers rows 32*(w/2) .. +31 and channel half w%2, so every shared-memory parameter load
+  // (BN tables, head weights) is one broadcast address per warp; the halves meet through smem.
+  const int hf = (tid >> 5) & 1, r = (tid & 31) + 32 * (tid >> 6);
+  float* s_part = reinterpret_cast<float*>(smem + lay.part_off);
   const PlaneGeom geo = L.geo;
   int j = 0;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
@@ -166,10 +171,17 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
 #pragma unroll
       for (int q = 0; q < NB; ++q) part[q] = fmaf(acc[c], wr[q], part[q]);
     }
+    float* pb = s_part + ((j & 1) * kHRows + r) * NB;
+    if (hf == 1) {
 #pragma unroll
-    for (int q = 0; q < NB; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], 1);
+      for (int q = 0; q < NB; ++q) pb[q] = part[q];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+    if (hf == 1) continue;
+#pragma unroll
+    for (int q = 0; q < NB; ++q) part[q] += pb[q];
     const int64_t row = tile * kHRows + r;
-    if (hf == 0 && geo.valid(row)) {
+    if (geo.valid(row)) {
       int b, t, f;
       geo.coords(row, b, t, f);
       float* dst = L.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * NB;
