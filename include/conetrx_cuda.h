@@ -104,9 +104,11 @@ int cnrx_receive_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t 
 int cnrx_featurize_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t T, int64_t F, int64_t N,
                           float* feat_dev, void* stream);
 
-/* Slot-sharded receive across several plans (one per GPU, built from the same network): slots are
+/* Slot-sharded forward / receive across several plans (one per GPU, built from the same network): slots are
  * split into contiguous ranges, each GPU runs its range from host memory on its own thread, LLRs land
  * in the caller's buffer.  No collective on the data path. */
+int cnrx_forward_sharded(cnrx_plan* const* plans, int32_t n_plans, const float* x, int64_t B, int64_t T,
+                         int64_t F, int64_t C, int32_t mode, float* out);
 int cnrx_receive_sharded(cnrx_plan* const* plans, int32_t n_plans, const float* y, int64_t B, int64_t T,
                          int64_t F, int64_t N, float* llr);
 

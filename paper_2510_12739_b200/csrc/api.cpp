@@ -1389,6 +1389,31 @@ void host_pipeline(cnrx_plan& p, const float* in, size_t in_per_slot, float* out
 // ================================================================================================
 // C ABI
 // ================================================================================================
+namespace {
+// contiguous slot ranges, one host thread per plan (no collective on the data path)
+template <class Call>
+int run_sharded(cnrx_plan* const* plans, int32_t n_plans, int64_t B, Call&& call) {
+  if (!plans || n_plans < 1) return fail(CNRX_ERR_INVALID_ARGUMENT, "no plans");
+  const int64_t per = (B + n_plans - 1) / n_plans;
+  std::vector<int> rcs(static_cast<size_t>(n_plans), CNRX_OK);
+  std::vector<std::string> msgs(static_cast<size_t>(n_plans));
+  std::vector<std::thread> th;
+  for (int i = 0; i < n_plans; ++i) {
+    const int64_t b0 = i * per, b1 = std::min(B, b0 + per);
+    if (b0 >= b1) break;
+    th.emplace_back([&, i, b0, b1] {
+      rcs[static_cast<size_t>(i)] = call(plans[i], b0, b1 - b0);
+      if (rcs[static_cast<size_t>(i)] != CNRX_OK) msgs[static_cast<size_t>(i)] = cnrx_last_error();
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int i = 0; i < n_plans; ++i)
+    if (rcs[static_cast<size_t>(i)] != CNRX_OK)
+      return fail(rcs[static_cast<size_t>(i)], "shard " + std::to_string(i) + ": " + msgs[static_cast<size_t>(i)]);
+  return CNRX_OK;
+}
+}  // namespace
+
 extern "C" {
 
 const char* cnrx_last_error(void) { return g_last_error.c_str(); }
@@ -1566,28 +1591,19 @@ int cnrx_featurize_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_
   });
 }
 
+
+int cnrx_forward_sharded(cnrx_plan* const* plans, int32_t n_plans, const float* x, int64_t B, int64_t T, int64_t F,
+                         int64_t C, int32_t mode, float* out) {
+  return run_sharded(plans, n_plans, B, [&](cnrx_plan* p, int64_t b0, int64_t nb) {
+    return cnrx_forward(p, x + b0 * T * F * C, nb, T, F, C, mode, out + b0 * T * F * p->out_ch);
+  });
+}
+
 int cnrx_receive_sharded(cnrx_plan* const* plans, int32_t n_plans, const float* y, int64_t B, int64_t T, int64_t F,
                          int64_t N, float* llr) {
-  if (!plans || n_plans < 1) return fail(CNRX_ERR_INVALID_ARGUMENT, "no plans");
-  const int64_t per = (B + n_plans - 1) / n_plans;
-  std::vector<int> rcs(static_cast<size_t>(n_plans), CNRX_OK);
-  std::vector<std::string> msgs(static_cast<size_t>(n_plans));
-  std::vector<std::thread> th;
-  for (int i = 0; i < n_plans; ++i) {
-    const int64_t b0 = i * per, b1 = std::min(B, b0 + per);
-    if (b0 >= b1) break;
-    th.emplace_back([&, i, b0, b1] {
-      const int out_ch = plans[i]->out_ch;
-      rcs[static_cast<size_t>(i)] =
-          cnrx_receive(plans[i], y + b0 * T * F * N * 2, b1 - b0, T, F, N, llr + b0 * T * F * out_ch);
-      if (rcs[static_cast<size_t>(i)] != CNRX_OK) msgs[static_cast<size_t>(i)] = cnrx_last_error();
-    });
-  }
-  for (auto& t : th) t.join();
-  for (int i = 0; i < n_plans; ++i)
-    if (rcs[static_cast<size_t>(i)] != CNRX_OK)
-      return fail(rcs[static_cast<size_t>(i)], "shard " + std::to_string(i) + ": " + msgs[static_cast<size_t>(i)]);
-  return CNRX_OK;
+  return run_sharded(plans, n_plans, B, [&](cnrx_plan* p, int64_t b0, int64_t nb) {
+    return cnrx_receive(p, y + b0 * T * F * N * 2, nb, T, F, N, llr + b0 * T * F * p->out_ch);
+  });
 }
 
 

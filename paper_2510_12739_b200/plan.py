@@ -84,7 +84,7 @@ _lib = None
 
 EXPORTED = ["cnrx_plan_create", "cnrx_plan_destroy", "cnrx_last_error", "cnrx_forward", "cnrx_forward_device",
             "cnrx_set_pilots", "cnrx_receive", "cnrx_receive_device", "cnrx_featurize_device",
-            "cnrx_receive_sharded", "cnrx_get_plan_info", "cnrx_set_graph_capture", "cnrx_launch_name",
+            "cnrx_receive_sharded", "cnrx_forward_sharded", "cnrx_get_plan_info", "cnrx_set_graph_capture", "cnrx_launch_name",
             "cnrx_set_profiling", "cnrx_read_profile", "cnrx_launch_flops", "cnrx_generate_slots",
             "cnrx_count_bit_errors", "cnrx_slot_noise_var", "cnrx_classical_receive"]
 
@@ -113,6 +113,7 @@ def lib():
     L.cnrx_receive_device.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp]
     L.cnrx_featurize_device.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp]
     L.cnrx_receive_sharded.argtypes = [C.POINTER(vp), C.c_int32, f32p, i64, i64, i64, i64, f32p]
+    L.cnrx_forward_sharded.argtypes = [C.POINTER(vp), C.c_int32, f32p, i64, i64, i64, i64, C.c_int32, f32p]
     L.cnrx_get_plan_info.argtypes = [vp, C.POINTER(cnrx_plan_info)]
     L.cnrx_set_graph_capture.argtypes = [vp, C.c_int32]
     L.cnrx_launch_name.restype = C.c_char_p
@@ -279,6 +280,16 @@ class Plan:
 
     def set_graph_capture(self, enable: bool) -> None:
         _check(lib().cnrx_set_graph_capture(self.h, int(enable)))
+
+
+def forward_sharded(plans, x: np.ndarray, mode: int = MODE_EVAL) -> np.ndarray:
+    """cnrx_forward_sharded: Network::forward over contiguous slot ranges of several single-GPU plans."""
+    x = np.ascontiguousarray(x, np.float32)
+    B, T, F, Cc = x.shape
+    out = np.empty((B, T, F, plans[0].out_channels), np.float32)
+    arr = (C.c_void_p * len(plans))(*[p.h for p in plans])
+    _check(lib().cnrx_forward_sharded(arr, len(plans), _f32p(x), B, T, F, Cc, mode, _f32p(out)))
+    return out
 
 
 def receive_sharded(plans, y: np.ndarray) -> np.ndarray:

@@ -249,6 +249,8 @@ def test_device_api_graph_capture_and_sharded():
     q = P.Plan(g, "bf16")
     q.set_pilots(b.pilots, b.pilot_mask)
     assert np.array_equal(P.receive_sharded([p, q], b.y), ref)
+    feat = np.ascontiguousarray(oracle.featurize(b.y, b.pilots, b.pilot_mask))
+    assert np.array_equal(P.forward_sharded([p, q], feat), p.forward(feat))
 
 
 def test_tensor_core_kernels_are_used():
