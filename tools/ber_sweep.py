@@ -1,7 +1,7 @@
 """Device-resident BER sweep: slots generated on the GPU (cnrx_generate_slots), received by the plan and
 scored on the GPU (cnrx_count_bit_errors) — nothing crosses PCIe but the per-slot error counts.
 
-usage: python tools/ber_sweep.py [cfg2] [batches] [batch] [checkpoint.cnck spec.json]
+usage: python tools/ber_sweep.py [cfg2] [batches] [batch] [checkpoint.cnck [spec.json]]
 Without a trained checkpoint the network has random weights and the BER sits near 0.5; the sweep is
 then a throughput run of the whole device pipeline (generate + receive + count)."""
 import dataclasses
@@ -22,6 +22,10 @@ cfg = G.CONFIGS[name]
 B = int(sys.argv[3]) if len(sys.argv) > 3 else cfg.batch
 if len(sys.argv) > 5:
     p = Fi.plan_from_files(sys.argv[5], sys.argv[4], cfg.precision)
+elif len(sys.argv) > 4:  # a checkpoint of this config's own graph (e.g. tests/golden/cfg2_trained.cnck)
+    g = cfg.graph_fn()
+    Fi.load_checkpoint(g, sys.argv[4])
+    p = P.Plan(g, cfg.precision)
 else:
     p = P.Plan(cfg.graph(seed=1), cfg.precision)
 pmask, pvals = slots.pilot_pattern(cfg.link.T, cfg.link.F, cfg.link.pilot_symbols, cfg.link.pilot_spacing)
