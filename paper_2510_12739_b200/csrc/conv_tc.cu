@@ -265,6 +265,17 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
     long long tr_ew = 0, tr_ework = 0;
     for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
       const int a = j & 1;
+      // unstaged epilogue: this row's residual is fetched before waiting for the accumulator, so its
+      // global-memory latency hides behind the tile's MMAs (one batch of COUT/8 16-byte loads)
+      constexpr int NRES = STAGED ? 1 : COUT / 8;
+      uint4 rres[NRES];
+      if constexpr (!STAGED) {
+        if (grp.res) {
+          const uint4* rrow = reinterpret_cast<const uint4*>(grp.res + (tile * 128 + q * 32 + lane) * COUT);
+#pragma unroll
+          for (int i = 0; i < NRES; ++i) rres[i] = __ldg(rrow + i);
+        }
+      }
       const long long te0 = L.trace ? clock64() : 0;
       mbar_wait(&tfull[a], static_cast<uint32_t>(j >> 1) & 1u);
       const long long te1 = L.trace ? clock64() : 0;
@@ -352,8 +363,8 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
       } else {
         __nv_bfloat16* orow = grp.out ? grp.out + p * COUT : nullptr;
         __nv_bfloat16* orow2 = grp.out2 ? grp.out2 + p * COUT : nullptr;
-        const __nv_bfloat16* rrow = grp.res ? grp.res + p * COUT : nullptr;
-#pragma unroll 1
+        const bool has_r = grp.res != nullptr;
+#pragma unroll
         for (int cc = 0; cc < COUT / 32; ++cc) {
           uint32_t r[32];
           tmem_ld32(taddr + cc * 32, r);
@@ -369,8 +380,8 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
             float v[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[v8 * 8 + i]) + s_bias[c0 + i];
-            if (rrow) {
-              const uint4 rv = *reinterpret_cast<const uint4*>(rrow + c0);
+            if (has_r) {
+              const uint4 rv = rres[(cc * 32 + v8 * 8) / 8 < NRES ? (cc * 32 + v8 * 8) / 8 : 0];
               const __nv_bfloat162* rp = reinterpret_cast<const __nv_bfloat162*>(&rv);
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
