@@ -267,13 +267,13 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
       const int a = j & 1;
       // unstaged epilogue: this row's residual is fetched before waiting for the accumulator, so its
       // global-memory latency hides behind the tile's MMAs (one batch of COUT/8 16-byte loads)
-      constexpr int NRES = STAGED ? 1 : COUT / 8;
-      uint4 rres[NRES];
+      constexpr int NRES = STAGED ? 1 : COUT / 16;  // 32-byte (16-channel) pieces
+      u32x8 rres[NRES];
       if constexpr (!STAGED) {
         if (grp.res) {
-          const uint4* rrow = reinterpret_cast<const uint4*>(grp.res + (tile * 128 + q * 32 + lane) * COUT);
+          const __nv_bfloat16* rrow = grp.res + (tile * 128 + q * 32 + lane) * COUT;
 #pragma unroll
-          for (int i = 0; i < NRES; ++i) rres[i] = __ldg(rrow + i);
+          for (int i = 0; i < NRES; ++i) rres[i] = ldg256(rrow + 16 * i);
         }
       }
       const long long te0 = L.trace ? clock64() : 0;
@@ -374,47 +374,49 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[a]);
           }
+          // two 16-channel pieces per 32-column chunk, each stored with one 256-bit access
 #pragma unroll
-          for (int v8 = 0; v8 < 4; ++v8) {
-            const int c0 = cc * 32 + v8 * 8;
-            float v[8];
+          for (int hp = 0; hp < 2; ++hp) {
+            const int c0 = cc * 32 + hp * 16;
+            float v[16];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[v8 * 8 + i]) + s_bias[c0 + i];
+            for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[hp * 16 + i]) + s_bias[c0 + i];
             if (has_r) {
-              const uint4 rv = rres[(cc * 32 + v8 * 8) / 8 < NRES ? (cc * 32 + v8 * 8) / 8 : 0];
-              const __nv_bfloat162* rp = reinterpret_cast<const __nv_bfloat162*>(&rv);
+              const u32x8& rv = rres[(c0 / 16) < NRES ? c0 / 16 : 0];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float2 f = __bfloat1622float2(rp[i]);
+              for (int i = 0; i < 8; ++i) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.v[i]));
                 v[2 * i] += f.x;
                 v[2 * i + 1] += f.y;
               }
             }
             if (grp.relu) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+              for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
             }
             if (!valid) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = 0.f;
+              for (int i = 0; i < 16; ++i) v[i] = 0.f;
             }
             if (orow) {
-              uint4 o;
-              __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+              u32x8 o;
 #pragma unroll
-              for (int i = 0; i < 4; ++i) op[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-              *reinterpret_cast<uint4*>(orow + c0) = o;
+              for (int i = 0; i < 8; ++i) {
+                const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+                o.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
+              }
+              stg256(orow + c0, o);
             }
             if (orow2) {
-              uint4 o;
-              __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+              u32x8 o;
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
+              for (int i = 0; i < 8; ++i) {
                 const float x0 = fmaxf(v[2 * i] * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
                 const float x1 = fmaxf(v[2 * i + 1] * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
-                op[i] = __floats2bfloat162_rn(valid ? x0 : 0.f, valid ? x1 : 0.f);
+                const __nv_bfloat162 b2 = __floats2bfloat162_rn(valid ? x0 : 0.f, valid ? x1 : 0.f);
+                o.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
               }
-              *reinterpret_cast<uint4*>(orow2 + c0) = o;
+              stg256(orow2 + c0, o);
             }
           }
         }
