@@ -17,6 +17,7 @@
 
 #include "common.h"
 #include "kernels.h"
+#include "sm100.cuh"
 
 namespace cnrx {
 
@@ -102,7 +103,16 @@ __global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, in
     } else {
       for (int i = 0; i < C; ++i) v[i] = 0.f;
     }
-    if (OUT_PLANE) {
+    if (OUT_PLANE && cpad == 16) {  // one 32-byte row: a single 256-bit store
+      u32x8 o;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k = 2 * i;
+        const __nv_bfloat162 b2 = __floats2bfloat162_rn(k < C ? v[k] : 0.f, k + 1 < C ? v[k + 1] : 0.f);
+        o.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
+      }
+      stg256(plane + geo.row_of(b, t, f) * cpad, o);
+    } else if (OUT_PLANE) {
       __nv_bfloat16* dst = plane + geo.row_of(b, t, f) * cpad;
       for (int i0 = 0; i0 < cpad; i0 += 8) {
         uint4 o;
