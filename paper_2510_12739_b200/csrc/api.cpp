@@ -147,6 +147,7 @@ struct PwStep {
   int plane_ids[kPwMaxPlanes];
   int n_planes = 0;
   int out_plane = -1;  // -1: head
+  int out2_plane = -1; // relu(out) copy (fold programs): the next block's pre-activation
   int level = 0;
 };
 
@@ -495,6 +496,7 @@ struct Bf16Compiler {
   cnrx_plan& p;
   std::vector<int> node_plane;    // node -> plane holding its value
   std::vector<int> plane_producer_tc;  // plane -> tc op index that writes it as primary/out2 (-1 none)
+  std::vector<int> plane_producer_pw;  // plane -> pointwise step that writes it as primary (-1 none)
 
   explicit Bf16Compiler(cnrx_plan& pl) : p(pl) {}
 
@@ -505,6 +507,7 @@ struct Bf16Compiler {
     pi.nonneg = nonneg;
     p.planes.push_back(pi);
     plane_producer_tc.push_back(-1);
+    plane_producer_pw.push_back(-1);
     return static_cast<int>(p.planes.size()) - 1;
   }
   void use(int plane, int level) {
@@ -600,6 +603,17 @@ struct Bf16Compiler {
           node_plane[static_cast<size_t>(u)] = vp;
           return vp;
         }
+        const int pprod = plane_producer_pw[static_cast<size_t>(vp)];
+        if (!bn && pprod >= 0 && p.pw[static_cast<size_t>(pprod)].out2_plane < 0) {
+          PwStep& ps = p.pw[static_cast<size_t>(pprod)];
+          int ns = 0, ops[kPwMaxPlanes], affs[kPwMaxPlanes], relus[kPwMaxPlanes];
+          if (pw_as_fold(ps.prog, &ns, ops, affs, relus) && ps.prog.n_planes_used == ns) {
+            const int np = new_plane(p.planes[static_cast<size_t>(vp)].C, ps.level, true);
+            ps.out2_plane = np;
+            node_plane[static_cast<size_t>(u)] = np;
+            return np;
+          }
+        }
         const int prod = plane_producer_tc[static_cast<size_t>(vp)];
         if (prod >= 0 && p.tc[static_cast<size_t>(prod)].out_plane == vp && p.tc[static_cast<size_t>(prod)].out2_plane < 0) {
           TcOp& op = p.tc[static_cast<size_t>(prod)];
@@ -631,6 +645,7 @@ struct Bf16Compiler {
     st.out_plane = new_plane(C, st.level, false);
     finish_pw(st, aff, C);
     p.pw.push_back(st);
+    plane_producer_pw[static_cast<size_t>(st.out_plane)] = static_cast<int>(p.pw.size()) - 1;
     node_plane[static_cast<size_t>(u)] = st.out_plane;
     return st.out_plane;
   }
@@ -815,6 +830,9 @@ struct Bf16Compiler {
     // out2 planes share their producer's level; every plane is live from its level to last use
     for (auto& op : p.tc) {
       if (op.out2_plane >= 0) p.planes[static_cast<size_t>(op.out2_plane)].level = op.level;
+    }
+    for (auto& st2 : p.pw) {
+      if (st2.out2_plane >= 0) p.planes[static_cast<size_t>(st2.out2_plane)].level = st2.level;
     }
     // buffer assignment by liveness over levels (a buffer is reusable once every reader's level passed)
     std::vector<int> order(p.planes.size());
@@ -1127,6 +1145,7 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
         prog.out_plane = plane_ptr(st.out_plane);
       else
         prog.llr = out;
+      prog.out2_plane = st.out2_plane >= 0 ? plane_ptr(st.out2_plane) : nullptr;
       p.note(launch_pw_program(prog, ws.geo, s), s);
     }
   }

@@ -92,6 +92,7 @@ struct PwProgram {
   const float* aff_s[kPwMaxAff];
   const float* aff_t[kPwMaxAff];
   __nv_bfloat16* out_plane; // [Nalloc][C]
+  __nv_bfloat16* out2_plane; // optional relu(out) copy [Nalloc][C] (fold programs only), or null
   const float* head_w;      // [C][head_bits] (reference layout of a 1x1 conv weight)
   const float* head_b;      // [head_bits]
   float* llr;               // [B,T,F,head_bits]

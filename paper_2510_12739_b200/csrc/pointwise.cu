@@ -412,6 +412,89 @@ bool launch_fold_any(const PwProgram& prog, const FoldSteps& fs, int ns, const P
   }
 }
 
+// Fold program storing a plane (any C, multiple of 8): one thread per (row, 8-channel chunk), so
+// consecutive threads touch consecutive 16-byte chunks (fully coalesced) and small batches still fill
+// the GPU; optionally also writes relu(result) as a second plane (the next block's pre-activation).
+template <int NS>
+__global__ void __launch_bounds__(256) pw_fold_plane_kernel(const __grid_constant__ PwProgram prog,
+                                                            const FoldSteps fs, PlaneGeom geo) {
+  const int CC = prog.C / 8;  // chunks per row
+  const int64_t total = geo.Nalloc * CC;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / CC;
+    const int c0 = static_cast<int>(i - row * CC) * 8;
+    const bool valid = geo.valid(row);
+    uint4 raw[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      raw[k] = valid ? __ldg(reinterpret_cast<const uint4*>(prog.planes[k] + row * prog.C + c0)) : make_uint4(0, 0, 0, 0);
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        if (k == 0) {
+          acc[2 * e] = f.x;
+          acc[2 * e + 1] = f.y;
+        } else if (fs.op[k] == PW_MUL) {
+          acc[2 * e] *= f.x;
+          acc[2 * e + 1] *= f.y;
+        } else {
+          acc[2 * e] += f.x;
+          acc[2 * e + 1] += f.y;
+        }
+      }
+      if (fs.aff[k] >= 0) {
+        const float* sv = prog.aff_s[fs.aff[k]] + c0;
+        const float* tv = prog.aff_t[fs.aff[k]] + c0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = acc[e] * __ldg(sv + e) + __ldg(tv + e);
+      }
+      if (fs.relu[k]) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = fmaxf(acc[e], 0.f);
+      }
+    }
+    if (!valid) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    }
+    uint4 o;
+    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) op[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+    *reinterpret_cast<uint4*>(prog.out_plane + row * prog.C + c0) = o;
+    if (prog.out2_plane) {
+      const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) op[e] = __hmax2(op[e], z);  // relu commutes with the bf16 rounding
+      *reinterpret_cast<uint4*>(prog.out2_plane + row * prog.C + c0) = o;
+    }
+  }
+}
+
+template <int NS>
+void launch_fold_plane_t(const PwProgram& prog, const FoldSteps& fs, const PlaneGeom& geo, cudaStream_t s) {
+  const int64_t total = geo.Nalloc * (prog.C / 8);
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+  pw_fold_plane_kernel<NS><<<blocks, 256, 0, s>>>(prog, fs, geo);
+  CNRX_CUDA(cudaGetLastError());
+}
+
+bool launch_fold_plane(const PwProgram& prog, const FoldSteps& fs, int ns, const PlaneGeom& geo, cudaStream_t s) {
+  if (prog.C % 8 != 0) return false;
+  switch (ns) {
+    case 1: launch_fold_plane_t<1>(prog, fs, geo, s); return true;
+    case 2: launch_fold_plane_t<2>(prog, fs, geo, s); return true;
+    case 3: launch_fold_plane_t<3>(prog, fs, geo, s); return true;
+    case 4: launch_fold_plane_t<4>(prog, fs, geo, s); return true;
+    default: return false;
+  }
+}
+
 }  // namespace
 
 bool pw_as_fold(const PwProgram& prog, int* nsteps, int* ops, int* affs, int* relus) {
@@ -456,6 +539,7 @@ static void launch_rows(const PwProgram& prog, const PlaneGeom& geo, cudaStream_
 
 const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s) {
   if (prog.head_bits > 0) require(prog.head_bits <= kPwMaxBits, "head with more than 16 outputs");
+  require(prog.out2_plane == nullptr || prog.head_bits == 0, "second output needs a plane program");
   const bool head = prog.head_bits > 0;
   {
     FoldSteps fs{};
@@ -466,10 +550,12 @@ const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaS
         const char* name = launch_head_tma(prog, ns, fs.op, fs.aff, fs.relu, geo, s);
         if (name) return name;
       }
+      if (!head && launch_fold_plane(prog, fs, ns, geo, s)) return "pw_fold_plane_kernel";
       const bool ok = launch_fold_any(prog, fs, ns, geo, s);
       if (ok) return head ? "pw_fold_kernel<head>" : "pw_fold_kernel<plane>";
     }
   }
+  require(prog.out2_plane == nullptr, "internal: a second pointwise output needs a fold program");
   switch (prog.C) {
     case 16: head ? launch_rows<1, 2>(prog, geo, s) : launch_rows<0, 2>(prog, geo, s); break;
     case 32: head ? launch_rows<1, 4>(prog, geo, s) : launch_rows<0, 4>(prog, geo, s); break;
