@@ -35,6 +35,22 @@
 #include "slotgen.h"
 #include "kernels.h"
 
+
+namespace cnrx {
+void ensure_smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  CNRX_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{dev, func}];
+  if (have >= bytes) return;
+  CNRX_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CNRX_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+  have = bytes;
+}
+}  // namespace cnrx
+
 using namespace cnrx;
 
 namespace {

@@ -134,4 +134,9 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.numAttrs = 1;
   CNRX_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
+
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` on the CURRENT device (function
+// attributes are per device: a plan on another device, or another thread, must not rely on a cache
+// filled elsewhere).  Process-wide cache keyed by (device, function).
+void ensure_smem_attr(const void* func, int bytes);
 }  // namespace cnrx

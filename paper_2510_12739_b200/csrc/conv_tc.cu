@@ -440,12 +440,7 @@ template <int CIN, int COUT, int KS>
 const char* launch_t(const TcLaunch& L, int num_sms, cudaStream_t stream) {
   auto kern = conv_tc_kernel<CIN, COUT, KS>;
   const SmemLayout lay = smem_layout(CIN, COUT, KS, L.stages, L.win_alloc, L.flags);
-  static thread_local int configured_bytes = -1;
-  if (configured_bytes < static_cast<int>(lay.total)) {
-    CNRX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lay.total)));
-    CNRX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-    configured_bytes = static_cast<int>(lay.total);
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(lay.total));
   // Several CTAs per SM when shared memory and TMEM allow (small-K convs, e.g. the 1x1 stem, are
   // bound by their epilogue; more resident epilogue warps hide its latency chains).
   // (the occupancy API under-reports here, so count registers / shared memory / TMEM directly)

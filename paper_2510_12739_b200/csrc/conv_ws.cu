@@ -544,12 +544,7 @@ int group_flags(const WsGroup& g) {
 
 template <int FL>
 void launch_fl(const WsLaunch& L, const WsLayout& lay, int grid, cudaStream_t stream) {
-  static thread_local int configured = -1;
-  if (configured < static_cast<int>(lay.total)) {
-    CNRX_CUDA(cudaFuncSetAttribute(conv_ws64_kernel<FL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(lay.total)));
-    configured = static_cast<int>(lay.total);
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(conv_ws64_kernel<FL>), static_cast<int>(lay.total));
   launch_pdl(conv_ws64_kernel<FL>, dim3(grid), dim3(kWsThreads), lay.total, stream, L);
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {  // (launch_pdl throws on launch errors; this catches sticky ones)

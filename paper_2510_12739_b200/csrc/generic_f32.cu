@@ -171,11 +171,7 @@ inline unsigned nblk(int64_t n, int t) { return static_cast<unsigned>((n + t - 1
 const char* launch_conv_f32(const ConvF32& p, cudaStream_t s) {
   const int64_t npix = static_cast<int64_t>(p.B) * p.T * p.F;
   const size_t smem = sizeof(float) * p.kh * p.kw * p.cin * kCot;
-  static thread_local size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    CNRX_CUDA(cudaFuncSetAttribute(conv_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    configured = smem;
-  }
+  if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(conv_f32_kernel), static_cast<int>(smem));
   require(smem <= 227 * 1024, "fp32 conv weights tile exceeds shared memory");
   dim3 grid(nblk(npix, 128), static_cast<unsigned>((p.cout + kCot - 1) / kCot));
   conv_f32_kernel<<<grid, 128, smem, s>>>(p);

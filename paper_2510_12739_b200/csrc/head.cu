@@ -212,12 +212,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn_head() {
 
 template <int C, int NB, int NS>
 void launch_t(const HeadLaunch& L, int stages_bytes_total, cudaStream_t s) {
-  static thread_local int configured = -1;
-  if (configured < stages_bytes_total) {
-    CNRX_CUDA(cudaFuncSetAttribute(head_tma_kernel<C, NB, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   stages_bytes_total));
-    configured = stages_bytes_total;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(head_tma_kernel<C, NB, NS>), stages_bytes_total);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
