@@ -264,6 +264,9 @@ struct cnrx_plan {
   // graph capture
   bool capture = false;
   cudaEvent_t fence_in = nullptr, fence_out = nullptr;
+  cudaEvent_t ws_done = nullptr;       // end of the last forward's work on the shared workspace
+  cudaStream_t ws_stream = nullptr;    // stream that forward ran on
+  bool ws_used = false;
   cudaGraphExec_t gexec = nullptr;
   std::string gkey;
 
@@ -1210,8 +1213,21 @@ void run_forward(cnrx_plan& p, const float* x_dev, int64_t B, int64_t T, int64_t
       run_bf16(p, x_dev, input_kind, N, out_dev, s);
     }
   };
+  // The workspace planes are shared by every call of this plan: a call on a different stream than the
+  // previous one first waits for that call's kernels (calls on one stream are ordered already).
+  auto order_in = [&](cudaStream_t st) {
+    if (p.ws_used && p.ws_stream != st) CNRX_CUDA(cudaStreamWaitEvent(st, p.ws_done, 0));
+  };
+  auto order_out = [&](cudaStream_t st) {
+    if (!p.ws_done) CNRX_CUDA(cudaEventCreateWithFlags(&p.ws_done, cudaEventDisableTiming));
+    CNRX_CUDA(cudaEventRecord(p.ws_done, st));
+    p.ws_stream = st;
+    p.ws_used = true;
+  };
   if (!p.capture) {
+    order_in(s);
     enqueue();
+    order_out(s);
     return;
   }
   // A legacy / per-thread default stream cannot be captured: capture and replay on the plan's own
@@ -1249,7 +1265,9 @@ void run_forward(cnrx_plan& p, const float* x_dev, int64_t B, int64_t T, int64_t
     cudaGraphDestroy(graph);
     p.gkey = key;
   }
+  order_in(s);
   CNRX_CUDA(cudaGraphLaunch(p.gexec, s));
+  order_out(s);
   if (fence) {
     CNRX_CUDA(cudaEventRecord(p.fence_out, s));
     CNRX_CUDA(cudaStreamWaitEvent(caller, p.fence_out, 0));
@@ -1521,6 +1539,7 @@ void cnrx_plan_destroy(cnrx_plan* plan) {
     for (auto e : evs) cudaEventDestroy(e);
   for (auto e : plan->event_pool) cudaEventDestroy(e);
   for (auto e : plan->pipe_ev) cudaEventDestroy(e);
+  if (plan->ws_done) cudaEventDestroy(plan->ws_done);
   if (plan->h2d) cudaStreamDestroy(plan->h2d);
   if (plan->d2h) cudaStreamDestroy(plan->d2h);
   if (plan->stream) cudaStreamDestroy(plan->stream);

@@ -301,3 +301,26 @@ def test_pipelined_host_api_matches_one_shot(prec, monkeypatch):
             fwd1 = p.forward(x)
             monkeypatch.setenv("CNRX_PIPELINE_CHUNKS", "1")
             assert np.array_equal(p.forward(x), fwd1)
+
+
+def test_calls_on_different_streams_share_the_workspace_safely():
+    """The plan's activation planes are shared by all calls: back-to-back device calls on two streams
+    (no host sync in between) must still produce each call's own result."""
+    import dataclasses
+    import torch
+    link = dataclasses.replace(G.CONFIGS["cfg2"].link, F=96)
+    g = G.CONFIGS["cfg2"].graph(seed=13)
+    p = P.Plan(g, "bf16")
+    ba, bb = slots.generate(link, 6, 1), slots.generate(link, 6, 2)
+    p.set_pilots(ba.pilots, ba.pilot_mask)
+    want_a, want_b = p.receive(ba.y), p.receive(bb.y)
+    ya, yb = torch.from_numpy(ba.y).cuda(), torch.from_numpy(bb.y).cuda()
+    oa = torch.empty((6, link.T, link.F, p.out_channels), device="cuda")
+    ob = torch.empty_like(oa)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        p.receive_device(ya, oa, s1.cuda_stream)
+        p.receive_device(yb, ob, s2.cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(oa.cpu().numpy(), want_a) and np.array_equal(ob.cpu().numpy(), want_b)
