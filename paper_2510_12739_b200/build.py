@@ -42,7 +42,8 @@ def flags(verbose_ptxas: bool = False):
          "--expt-relaxed-constexpr", "-I", CSRC, "-I", INCLUDE] + ARCH
     if verbose_ptxas:
         f += ["-Xptxas", "-v"]
-    return f
+    extra = os.environ.get("CNRX_EXTRA_NVCC_FLAGS", "")  # experiments / A-B builds only
+    return f + extra.split()
 
 
 def _compile(src: str, verbose: bool) -> str:
