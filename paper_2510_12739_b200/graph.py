@@ -554,4 +554,10 @@ CONFIGS = {
                    LinkSpec(T=14, F=612, N=2, mod_order=16, n_taps=12, rms_delay_s=300e-9, tap_spacing_s=100e-9,
                             doppler_max_hz=200.0, snr_db=(0.0, 25.0)),
                    256, "bf16", "plain ResNet (DeepRx-style RB x 8 @96), same inputs as cfg2"),
+    # "96 ch" and "MAC-matched to cfg2" disagree; run both.  W=78 gives 877,344 MACs/RE
+    # (cfg2: 887,296); the bf16 plan pads 78 channels to 96 internally.
+    "cfg4m": Config("cfg4m", lambda: _resnet_cfg(78, 8, 12, 4),
+                    LinkSpec(T=14, F=612, N=2, mod_order=16, n_taps=12, rms_delay_s=300e-9, tap_spacing_s=100e-9,
+                             doppler_max_hz=200.0, snr_db=(0.0, 25.0)),
+                    256, "bf16", "plain ResNet (DeepRx-style RB x 8 @78, MAC-matched to cfg2), same inputs as cfg2"),
 }

@@ -103,7 +103,7 @@ def test_bf16_matches_reference_golden(name, wseed):
 # ------------------------------------------------------------------------------------------------
 # live oracle comparisons: configs, shapes, ragged edges
 # ------------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("name,B,F", [("cfg1", 3, 72), ("cfg2", 2, 37), ("cfg2", 1, 612), ("cfg4", 2, 29),
+@pytest.mark.parametrize("name,B,F", [("cfg1", 3, 72), ("cfg2", 2, 37), ("cfg2", 1, 612), ("cfg4", 2, 29), ("cfg4m", 1, 33),
                                       ("cfg3", 1, 40)])
 def test_fp32_vs_oracle(name, B, F):
     g = G.CONFIGS[name].graph(seed=7)
@@ -112,7 +112,7 @@ def test_fp32_vs_oracle(name, B, F):
     assert np.array_equal(got, ref), np.abs(got - ref).max()
 
 
-@pytest.mark.parametrize("name,B,F", [("cfg1", 3, 72), ("cfg2", 2, 37), ("cfg2", 1, 612), ("cfg4", 2, 29),
+@pytest.mark.parametrize("name,B,F", [("cfg1", 3, 72), ("cfg2", 2, 37), ("cfg2", 1, 612), ("cfg4", 2, 29), ("cfg4m", 1, 33),
                                       ("cfg3", 1, 40), ("cfg2", 5, 5)])
 def test_bf16_vs_emulation_and_oracle(name, B, F):
     g = G.CONFIGS[name].graph(seed=7)
