@@ -1189,6 +1189,11 @@ void* ensure_dev(void*& buf, size_t& cap, size_t bytes) {
 void run_forward(cnrx_plan& p, const float* x_dev, int64_t B, int64_t T, int64_t F, float* out_dev, int input_kind,
                  int N, cudaStream_t s) {
   ensure_workspace(p, static_cast<int>(B), static_cast<int>(T), static_cast<int>(F));
+  float* feat = nullptr;  // fp32 plans on the receive path: features in the reference layout
+  if (p.precision == CNRX_FP32 && input_kind == 1) {  // allocated outside any graph capture
+    const size_t bytes = static_cast<size_t>(B * T * F * p.in_ch) * sizeof(float);
+    feat = static_cast<float*>(ensure_dev(p.ws.feat_buf, p.ws.feat_bytes, bytes));
+  }
   auto enqueue = [&]() {
     p.launch_names.clear();
     p.launch_flops.clear();
@@ -1201,8 +1206,6 @@ void run_forward(cnrx_plan& p, const float* x_dev, int64_t B, int64_t T, int64_t
     if (p.precision == CNRX_FP32) {
       if (input_kind == 1) {
         // featurize into an fp32 reference-layout buffer, then run the node program on it
-        const size_t bytes = static_cast<size_t>(B * T * F * p.in_ch) * sizeof(float);
-        float* feat = static_cast<float*>(ensure_dev(p.ws.feat_buf, p.ws.feat_bytes, bytes));
         PlaneGeom g = make_geom(static_cast<int>(B), static_cast<int>(T), static_cast<int>(F), 1);
         p.note(launch_featurize_ref(x_dev, g, N, p.pt, feat, s), s);
         run_f32(p, feat, out_dev, s);
