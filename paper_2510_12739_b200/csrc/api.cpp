@@ -1420,10 +1420,20 @@ void host_pipeline(cnrx_plan& p, const float* in, size_t in_per_slot, float* out
   // order the copy streams after anything the caller queued on the plan stream anyway
   CNRX_CUDA(cudaEventRecord(p.pipe_ev[0], p.stream));
   CNRX_CUDA(cudaStreamWaitEvent(p.h2d, p.pipe_ev[0], 0));
-  const int64_t per = (B + n - 1) / n;
+  // tapered chunks (half-size first and last): the first upload and the last download are the only
+  // copies not hidden behind a chunk's kernels
+  static const bool taper = !(std::getenv("CNRX_PIPELINE_TAPER") && std::atoi(std::getenv("CNRX_PIPELINE_TAPER")) == 0);
+  std::vector<int64_t> bounds(static_cast<size_t>(n) + 1, 0);
+  const double units = taper && n > 2 ? n - 1.0 : static_cast<double>(n);
+  double acc = 0;
   for (int k = 0; k < n; ++k) {
-    const int64_t b0 = k * per, nb = std::min(B, b0 + per) - b0;
-    if (nb <= 0) break;
+    acc += (taper && n > 2 && (k == 0 || k == n - 1)) ? 0.5 : 1.0;
+    bounds[static_cast<size_t>(k) + 1] = std::min<int64_t>(B, static_cast<int64_t>(std::llround(acc / units * B)));
+  }
+  bounds[static_cast<size_t>(n)] = B;
+  for (int k = 0; k < n; ++k) {
+    const int64_t b0 = bounds[static_cast<size_t>(k)], nb = bounds[static_cast<size_t>(k) + 1] - b0;
+    if (nb <= 0) continue;
     cudaEvent_t landed = p.pipe_ev[static_cast<size_t>(2 * k)], done = p.pipe_ev[static_cast<size_t>(2 * k + 1)];
     CNRX_CUDA(cudaMemcpyAsync(din + b0 * in_per_slot, reinterpret_cast<const char*>(in) + b0 * in_per_slot,
                               static_cast<size_t>(nb) * in_per_slot, cudaMemcpyHostToDevice, p.h2d));
