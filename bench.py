@@ -65,7 +65,8 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                ["nvidia-smi", "-i", str(self.idx),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw,power.limit",
                  "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
@@ -87,7 +88,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
+        sm, mx, reasons, pw, pl = [], [], set(), [], []
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 3:
@@ -98,13 +99,22 @@ class ClockSampler:
                 bits = int(parts[2], 16)
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[3]))
+                pl.append(float(parts[4]))
+            except (ValueError, IndexError):
+                pass
             for b, name in REASON_BITS.items():
                 if bits & b and name != "gpu_idle":
                     reasons.add(name)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if pw:
+            out["power_w"] = float(np.median(pw))
+            out["power_limit_w"] = float(max(pl)) if pl else None
+        return out
 
 
 def cpu_baseline(cfg, g, batch, sample_slots=None, reps=1):
