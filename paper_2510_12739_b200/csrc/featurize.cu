@@ -304,6 +304,60 @@ __global__ void __launch_bounds__(256) stem_kernel(const __grid_constant__ StemL
   }
 }
 
+// Small batches: one thread per plane row (slot, column, symbol) instead of per column, so a single
+// slot still spreads over the GPU; each thread recomputes its column's LS values at the two pilot
+// symbols it interpolates between (a handful of L1/L2-resident loads).
+__global__ void featurize_row_kernel(const float2* __restrict__ y, PlaneGeom geo, int N, PilotTablesDev pt,
+                                     __nv_bfloat16* __restrict__ plane, int cpad) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= geo.Nalloc) return;
+  float v[6 * kMaxN];
+  const int C = 6 * N;
+  for (int i = 0; i < C; ++i) v[i] = 0.f;
+  if (geo.valid(row)) {
+    int b, t, f;
+    geo.coords(row, b, t, f);
+    const int T = geo.T, F = geo.F;
+    const int j0 = pt.jlo[t], j1 = pt.jhi[t];
+    const float wt = pt.wt[t];
+    Cplx hs[2][kMaxN];
+    for (int jj = 0; jj < 2; ++jj) {
+      const int j = jj == 0 ? j0 : j1;
+      const int ts = pt.sym[j];
+      const int flo = pt.flo[j * F + f], fhi = pt.fhi[j * F + f];
+      const float w = pt.wf[j * F + f];
+      const Cplx ilo = {pt.inv_x[2 * (ts * F + flo)], pt.inv_x[2 * (ts * F + flo) + 1]};
+      const Cplx ihi = {pt.inv_x[2 * (ts * F + fhi)], pt.inv_x[2 * (ts * F + fhi) + 1]};
+      for (int a = 0; a < N; ++a) {
+        const float2 ylo = y[((static_cast<int64_t>(b) * T + ts) * F + flo) * N + a];
+        const float2 yhi = y[((static_cast<int64_t>(b) * T + ts) * F + fhi) * N + a];
+        const Cplx llo = cmul({ylo.x, ylo.y}, ilo), lhi = cmul({yhi.x, yhi.y}, ihi);
+        hs[jj][a] = {(1.f - w) * llo.re + w * lhi.re, (1.f - w) * llo.im + w * lhi.im};
+      }
+    }
+    const float xr = pt.x[2 * (t * F + f)], xi = pt.x[2 * (t * F + f) + 1];
+    for (int a = 0; a < N; ++a) {
+      const float2 yv = y[((static_cast<int64_t>(b) * T + t) * F + f) * N + a];
+      v[6 * a + 0] = yv.x;
+      v[6 * a + 1] = yv.y;
+      v[6 * a + 2] = xr;
+      v[6 * a + 3] = xi;
+      v[6 * a + 4] = (1.f - wt) * hs[0][a].re + wt * hs[1][a].re;
+      v[6 * a + 5] = (1.f - wt) * hs[0][a].im + wt * hs[1][a].im;
+    }
+  }
+  __nv_bfloat16* dst = plane + row * cpad;
+  for (int i0 = 0; i0 < cpad; i0 += 8) {
+    uint4 o;
+    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+    for (int i = 0; i < 4; ++i) {
+      const int k = i0 + 2 * i;
+      op[i] = __floats2bfloat162_rn(k < C ? v[k] : 0.f, k + 1 < C ? v[k + 1] : 0.f);
+    }
+    *reinterpret_cast<uint4*>(dst + i0) = o;
+  }
+}
+
 }  // namespace
 
 bool stem_supported_cin(int cin) { return cin == 6 || cin == 12 || cin == 24 || cin == 48; }
@@ -335,6 +389,12 @@ const char* launch_featurize_plane(const float* y, const PlaneGeom& geo, int N, 
   require(N <= kMaxN, "featurize supports at most 8 receive antennas");
   const int64_t n = static_cast<int64_t>(geo.B) * (geo.F + geo.npad) + (geo.Nalloc - static_cast<int64_t>(geo.B) * geo.P);
   const int threads = 128;
+  if (n < 148 * 128 && pt.n_sym >= 1) {  // too few columns to fill the GPU: one thread per row
+    featurize_row_kernel<<<static_cast<unsigned>((geo.Nalloc + threads - 1) / threads), threads, 0, s>>>(
+        reinterpret_cast<const float2*>(y), geo, N, pt, plane, cpad);
+    CNRX_CUDA(cudaGetLastError());
+    return "featurize_row_kernel";
+  }
   featurize_kernel<1><<<static_cast<unsigned>((n + threads - 1) / threads), threads, 0, s>>>(
       reinterpret_cast<const float2*>(y), geo, N, pt, nullptr, plane, cpad);
   CNRX_CUDA(cudaGetLastError());
