@@ -324,3 +324,29 @@ def test_calls_on_different_streams_share_the_workspace_safely():
         p.receive_device(yb, ob, s2.cuda_stream)
     torch.cuda.synchronize()
     assert np.array_equal(oa.cpu().numpy(), want_a) and np.array_equal(ob.cpu().numpy(), want_b)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+@pytest.mark.parametrize("T,F,N,pilots,spacing", [(12, 50, 1, (2, 9), 2), (14, 33, 4, (3,), 3), (7, 61, 2, (0, 6), 4)])
+def test_receive_other_grids(prec, T, F, N, pilots, spacing):
+    """Grids other than the BASELINE ones: symbol count, odd subcarrier counts, 1/4 antennas, one or two
+    pilot symbols at other positions and spacings — the plane layout, the featurizer's interpolation and
+    the padded tiles must all follow."""
+    import dataclasses
+    link = dataclasses.replace(G.CONFIGS["cfg2"].link, T=T, F=F, N=N, pilot_symbols=pilots, pilot_spacing=spacing)
+    spec = G.conet_template(64, 2, [2], "mul", "bn", False, 6 * N, 4, "standard", 3, [1])
+    for ns in [spec.main] + spec.supports:
+        ns.kernel = 1  # 1x1 stem / head as in the BASELINE configs (the bf16 head is a pointwise GEMV)
+    g = G.build_conet(spec)
+    g.init_he_normal(5, randomize_aux=True)
+    b = slots.generate(link, 2, 17)
+    p = P.Plan(g, prec)
+    p.set_pilots(b.pilots, b.pilot_mask)
+    got = p.receive(b.y)
+    feat = oracle.featurize(b.y, b.pilots, b.pilot_mask)
+    ref = oracle.forward(g, feat)
+    if prec == "fp32":
+        assert_fp32(got, ref)
+    else:
+        assert_bf16_vs_emu(got, E.emulate(g, feat))
+        assert_bf16_vs_ref(got, ref)
