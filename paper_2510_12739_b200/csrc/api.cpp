@@ -31,6 +31,7 @@
 #include "../../include/conetrx_cuda.h"
 #include "common.h"
 #include "conv_tc.h"
+#include "conv_blk.h"
 #include "conv_ws.h"
 #include "slotgen.h"
 #include "kernels.h"
@@ -141,6 +142,7 @@ struct PlaneInfo {
   int level = 0;       // level of its producer
   int last_use = 0;    // last level reading it
   int buffer = -1;     // workspace buffer index
+  bool dead = false;   // conv1 output inside a fused block: never written, no buffer
 };
 struct TcOp {
   int node = -1;
@@ -152,6 +154,10 @@ struct TcOp {
   int in_plane = -1, res_plane = -1, out_plane = -1, out2_plane = -1;
   int relu = 0;
   int relu_in = 0;  // ws kernels: input is relu(in_plane), applied to the window on load
+  // fused residual block (conv_blk.cu): this op is conv2 and `blk_c1` its conv1, whose output plane is
+  // never materialised; the conv1 op is then `fused_away` (not launched)
+  int blk_c1 = -1;
+  bool fused_away = false;
   void* wimg = nullptr;
   float* bias = nullptr;
   float* s2 = nullptr;
@@ -181,8 +187,10 @@ struct Workspace {
   size_t feat_bytes = 0;
   struct GroupLaunch {
     bool ws = false;
+    bool blk = false;
     TcLaunch tc;
     WsLaunch wsl;
+    BlkLaunch blkl;
   };
   std::vector<GroupLaunch> launches;  // prepared tensor maps per TC group (bf16)
 };
@@ -669,6 +677,36 @@ struct Bf16Compiler {
     return st.out_plane;
   }
 
+  // Opt-in (CNRX_BLK=1): pre-activation residual blocks y = conv2(relu(bn(conv1(relu?(x))))) + x over
+  // 64-channel planes as one kernel (conv_blk.cu) when conv1's output feeds nothing but conv2.  Same
+  // values as the two-kernel path (conv1's output is rounded to bf16 either way); measured no faster at
+  // cfg2 sizes, so the two-kernel path stays the default.
+  void fuse_blocks() {
+    const char* e = getenv("CNRX_BLK");
+    if (!e || atoi(e) == 0) return;
+    std::vector<int> readers(p.planes.size(), 0);
+    for (const auto& op : p.tc) {
+      if (op.in_plane >= 0) ++readers[static_cast<size_t>(op.in_plane)];
+      if (op.res_plane >= 0) ++readers[static_cast<size_t>(op.res_plane)];
+    }
+    for (const auto& st : p.pw)
+      for (int k = 0; k < st.n_planes; ++k) ++readers[static_cast<size_t>(st.plane_ids[k])];
+    for (size_t bi = 0; bi < p.tc.size(); ++bi) {
+      TcOp& b = p.tc[bi];
+      if (!b.ws || b.relu || b.relu_in || b.res_plane < 0 || b.out2_plane >= 0 || b.stem) continue;
+      const int ai = plane_producer_tc[static_cast<size_t>(b.in_plane)];
+      if (ai < 0) continue;
+      TcOp& a = p.tc[static_cast<size_t>(ai)];
+      if (!a.ws || a.fused_away || a.blk_c1 >= 0 || a.out_plane != b.in_plane || !a.relu || a.res_plane >= 0 ||
+          a.out2_plane >= 0 || a.dil != b.dil || a.in_plane != b.res_plane || a.stem)
+        continue;
+      if (readers[static_cast<size_t>(a.out_plane)] != 1) continue;
+      b.blk_c1 = ai;
+      a.fused_away = true;
+      p.planes[static_cast<size_t>(a.out_plane)].dead = true;
+    }
+  }
+
   void compile() {
     const int n = static_cast<int>(p.nodes.size());
     node_plane.assign(static_cast<size_t>(n), -1);
@@ -804,6 +842,7 @@ struct Bf16Compiler {
     st.prog.head_b = p.upload(hb);
     finish_pw(st, aff, C);
     p.pw.push_back(st);
+    fuse_blocks();
     // level schedule
     int maxl = 0;
     for (auto& op : p.tc) maxl = std::max(maxl, op.level);
@@ -816,6 +855,7 @@ struct Bf16Compiler {
     static const bool no_stem = getenv("CNRX_STEM") == nullptr;
     for (int k = 0; k < static_cast<int>(p.tc.size()); ++k) {
       TcOp& op = p.tc[static_cast<size_t>(k)];
+      if (op.fused_away) continue;
       if (!no_stem && op.stem_w && static_cast<int>(p.stem_ops.size()) < kStemMaxOps &&
           (p.stem_ops.empty() || p.tc[static_cast<size_t>(p.stem_ops[0])].cin_real == op.cin_real)) {
         op.stem = true;
@@ -824,19 +864,21 @@ struct Bf16Compiler {
     }
     p.need_plane0 = false;
     for (const auto& op : p.tc)
-      if (!op.stem && (op.in_plane == 0 || op.res_plane == 0)) p.need_plane0 = true;
+      if (!op.stem && !op.fused_away && (op.in_plane == 0 || op.res_plane == 0)) p.need_plane0 = true;
     for (const auto& st2 : p.pw)
       for (int k = 0; k < st2.n_planes; ++k)
         if (st2.plane_ids[k] == 0) p.need_plane0 = true;
     for (int k = 0; k < static_cast<int>(p.tc.size()); ++k) {
       const TcOp& op = p.tc[static_cast<size_t>(k)];
-      if (op.stem) continue;
+      if (op.stem || op.fused_away) continue;
       auto& groups = p.tc_groups_by_level[static_cast<size_t>(op.level)];
       bool placed = false;
       for (auto& g : groups) {
         const TcOp& o0 = p.tc[static_cast<size_t>(g[0])];
+        const bool blk0 = o0.blk_c1 >= 0, blk = op.blk_c1 >= 0;
         if (static_cast<int>(g.size()) < kTcMaxGroups && o0.cin == op.cin && o0.cout == op.cout && o0.ks == op.ks &&
-            o0.ws == op.ws) {
+            o0.ws == op.ws && blk0 == blk &&
+            (!blk || p.tc[static_cast<size_t>(o0.blk_c1)].relu_in == p.tc[static_cast<size_t>(op.blk_c1)].relu_in)) {
           g.push_back(k);
           placed = true;
           break;
@@ -862,6 +904,7 @@ struct Bf16Compiler {
     std::vector<int> buf_free_after;
     for (int pl : order) {
       auto& pi = p.planes[static_cast<size_t>(pl)];
+      if (pi.dead) continue;
       if (pi.last_use < pi.level) pi.last_use = pi.level;
       int chosen = -1;
       for (size_t b = 0; b < p.buf_channels.size(); ++b)
@@ -934,7 +977,35 @@ void ensure_workspace(cnrx_plan& p, int B, int T, int F) {
       Workspace::GroupLaunch GL;
       const TcOp& op0 = p.tc[static_cast<size_t>(grp[0])];
       GL.ws = op0.ws;
-      if (op0.ws) {
+      GL.blk = op0.blk_c1 >= 0;
+      if (GL.blk) {
+        BlkLaunch& L = GL.blkl;
+        std::memset(&L, 0, sizeof(L));
+        L.geo = ws.geo;
+        L.ngroups = static_cast<int>(grp.size());
+        L.n_tiles = conv_blk64_tiles(ws.geo.Nalloc);
+        L.relu_in = p.tc[static_cast<size_t>(op0.blk_c1)].relu_in;
+        int win_alloc = 0;
+        for (size_t gi = 0; gi < grp.size(); ++gi) {
+          const TcOp& c2 = p.tc[static_cast<size_t>(grp[gi])];
+          const TcOp& c1 = p.tc[static_cast<size_t>(c2.blk_c1)];
+          BlkGroup& g = L.g[gi];
+          g.dil = c1.dil;
+          g.halo = ws.geo.T1 * c1.dil + 1;
+          if (!conv_blk64_supported_halo(g.halo))
+            throw Error(CNRX_ERR_UNSUPPORTED, "fused residual block: T+1 = " + std::to_string(ws.geo.T1) + " with dilation " +
+                                                  std::to_string(c1.dil) + " exceeds its window (unset CNRX_BLK)");
+          win_alloc = std::max(win_alloc, conv_blk64_win_alloc(g.halo));
+          conv_blk64_make_maps(plane_ptr(c1.in_plane), plane_ptr(c2.out_plane), ws.geo.Nalloc, &g);
+          g.wimg1 = static_cast<const uint32_t*>(c1.wimg);
+          g.wimg2 = static_cast<const uint32_t*>(c2.wimg);
+          g.bias1 = c1.bias;
+          g.bias2 = c2.bias;
+        }
+        L.win_alloc = win_alloc;
+        L.xstages = conv_blk64_xstages(win_alloc, L.relu_in);
+        if (L.xstages == 0) throw Error(CNRX_ERR_UNSUPPORTED, "fused residual block exceeds shared memory (unset CNRX_BLK)");
+      } else if (op0.ws) {
         WsLaunch& L = GL.wsl;
         std::memset(&L, 0, sizeof(L));
         L.geo = ws.geo;
@@ -1106,10 +1177,41 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
       for (int k : grp) {
         const TcOp& o = p.tc[static_cast<size_t>(k)];
         fl += 2ll * o.ks * o.ks * o.cin_real * o.cout_real;
+        if (o.blk_c1 >= 0) {
+          const TcOp& o1 = p.tc[static_cast<size_t>(o.blk_c1)];
+          fl += 2ll * o1.ks * o1.ks * o1.cin_real * o1.cout_real;
+        }
       }
       Workspace::GroupLaunch& GL = ws.launches[li++];
       static const bool trace = getenv("CNRX_TRACE") != nullptr;
       static unsigned long long* dtrace = nullptr;
+      if (GL.blk) {
+        if (trace) {
+          if (!dtrace) CNRX_CUDA(cudaMalloc(&dtrace, 32 * sizeof(unsigned long long)));
+          CNRX_CUDA(cudaMemsetAsync(dtrace, 0, 32 * sizeof(unsigned long long), s));
+          GL.blkl.trace = dtrace;
+        }
+        p.note(conv_blk64_launch(GL.blkl, p.num_sms, s), s, fl);
+        if (trace) {
+          unsigned long long h[kBlkTraceSlots];
+          CNRX_CUDA(cudaMemcpyAsync(h, dtrace, sizeof h, cudaMemcpyDeviceToHost, s));
+          CNRX_CUDA(cudaStreamSynchronize(s));
+          const double nt = static_cast<double>(h[kBlkTraceTiles] ? h[kBlkTraceTiles] : 1);
+          fprintf(stderr,
+                  "[trace] conv_blk64 relu_in=%d tiles=%llu per-tile cycles: prod_wait %.0f | mma1 wait_in %.0f wait_acc %.0f | "
+                  "mma2 wait_in %.0f wait_acc %.0f | epi1 wait_full %.0f wait_w %.0f | epi2 wait_full %.0f | relu_wait %.0f | "
+                  "total/tile %.0f\n",
+                  GL.blkl.relu_in, h[kBlkTraceTiles], h[kBlkTraceProd] / nt, h[kBlkTraceM1In] / nt, h[kBlkTraceM1Acc] / nt,
+                  h[kBlkTraceM2In] / nt, h[kBlkTraceM2Acc] / nt, h[kBlkTraceE1Full] / nt, h[kBlkTraceE1W] / nt,
+                  h[kBlkTraceE2Full] / nt, h[kBlkTraceRelu] / nt, h[kBlkTraceTotal] / nt);
+          fprintf(stderr, "[trace]   epi1 drain %.0f combine %.0f store %.0f | epi2 drain %.0f combine %.0f store %.0f\n",
+                  h[kBlkTraceE1Drain] / nt, h[kBlkTraceE1Comb] / nt, h[kBlkTraceE1Store] / nt, h[kBlkTraceE2Drain] / nt,
+                  h[kBlkTraceE2Comb] / nt, h[kBlkTraceE2Store] / nt);
+          fprintf(stderr, "[trace]   CTAs %llu, span %.1f us, effective SM clock %.0f MHz\n", h[12], (h[14] - ~h[13]) * 1e-3,
+                  h[15] ? static_cast<double>(h[kBlkTraceTotal]) / static_cast<double>(h[15]) * 1e3 : 0.0);
+        }
+        continue;
+      }
       if (GL.ws) {
         if (trace) {
           if (!dtrace) CNRX_CUDA(cudaMalloc(&dtrace, 32 * sizeof(unsigned long long)));

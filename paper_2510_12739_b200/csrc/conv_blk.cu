@@ -1,0 +1,614 @@
+// conv_blk.cu — one pre-activation residual block in one kernel, conv1's output never leaving the SM:
+//
+//     h = relu(conv1(relu?(x)) * s2 + t2)        (BN2 folded into conv1's weights and bias)
+//     y = conv2(h) + b2 + x
+//
+// i.e. the MRB block of build_net / append_block (reference network.hpp:451-465: ReLU -> C1 -> BN ->
+// ReLU -> C2 -> + skip) over 64-channel bf16 planes, 3x3 "same" convolutions (kernels.hpp:47-91).
+// The separate-kernel path (conv_ws.cu twice) moves x, h, h, x, y through HBM (4.4 GB per cfg2 block
+// at B = 256, conv2 running at ~87 % of the HBM roofline); here only x in and y out (1.8 GB) remain,
+// and the block is tensor-core bound.
+//
+// Both convolutions use conv_ws.cu's weights-stationary form (weights = A operand resident in TMEM,
+// two 3x3 taps per UMMA in lane halves, activation window = B operand, partial sums combined in the
+// epilogue); see conv_ws.cu and DESIGN.md.  TMEM holds both weight sets (2 x 192 columns), so the
+// accumulators are N = 64 columns each (one per convolution, single-buffered): tiles are 63 output rows
+// and the tensor core alternates conv1 of one tile with conv2 of an earlier tile, each convolution's
+// epilogue draining its accumulator while the other convolution's UMMAs run.
+//
+// Every CTA owns a contiguous range of tiles, so conv1's output tiles are reused by the conv2 windows
+// of neighbouring tiles straight from shared memory: conv1 runs on the range plus one halo tile on each
+// side (0.3 % recompute at cfg2 sizes), and its epilogue writes each h row into every conv2 window
+// (`W` buffers, 96 rows for T = 14) that contains it.  The residual is read from the x window conv1
+// already loaded.
+//
+// Warp roles (21 warps, 1 CTA per SM):
+//   warp 0        TMA producer: x windows (ring of `xstages`)
+//   warp 1        conv1 UMMA issuer        warp 19   conv2 UMMA issuer
+//   warps 2-9     conv1 epilogue (+ weights -> TMEM at start): TMEM -> combine -> bias, ReLU, zero
+//                 padding rows -> bf16 -> stmatrix into the W windows
+//   warps 10-17   conv2 epilogue: TMEM -> combine -> bias + residual (ldmatrix from the x window) ->
+//                 bf16 -> staging -> TMA store of 63 rows
+//   warps 18, 20  input ReLU (x window -> relu'd copy, the conv1 B operand) when x is not already
+//                 non-negative
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "conv_blk.h"
+#include "sm100.cuh"
+
+namespace cnrx {
+
+namespace {
+
+constexpr int kC = 64;
+constexpr int kRB = 128;          // bytes per plane row
+constexpr int kN = 64;            // UMMA N: window rows per instruction
+constexpr int kTile = kN - 1;     // output rows per tile (tap B of a pair lands one column later)
+constexpr int kPairs = 6;
+constexpr int kKSteps = kC / 16;
+constexpr int kWCols = kPairs * kKSteps * 8;  // 192 TMEM columns per weight set
+constexpr int kAcc1 = 2 * kWCols;              // 384
+constexpr int kAcc2 = kAcc1 + kN;              // 448
+constexpr int kBox = 32;
+constexpr int kWSlots = 5;        // conv2 windows in flight
+// warp roles: 0 TMA producer, 1 conv1 UMMA, 2-9 conv1 epilogue, 10-17 conv2 epilogue, 18 and 20 input
+// ReLU, 19 conv2 UMMA
+constexpr int kWarpE2 = 10, kWarpRelu0 = 18, kWarpMma2 = 19, kWarpRelu1 = 20;
+constexpr int kThreads = 21 * 32;
+constexpr int kMaxXStages = 6;
+
+struct BlkLayout {
+  uint32_t x_off, stage, xr_off, w_off, stg_off, trash_off, par_off, bar_off, total;
+};
+__host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int relu_in) {
+  BlkLayout s{};
+  s.stage = static_cast<uint32_t>(win_alloc * kRB);  // multiple of 4 KB
+  s.x_off = 0;
+  uint32_t off = s.stage * static_cast<uint32_t>(xstages);
+  s.xr_off = off;
+  if (relu_in) off += 2u * s.stage;
+  s.w_off = off;
+  off += static_cast<uint32_t>(kWSlots) * s.stage;
+  s.stg_off = off;                 // 2 x [64 rows][128 B]
+  off += 2u * 64u * kRB;
+  s.trash_off = off;               // 32 rows: destination of stmatrix rows that belong to no window
+  off += 32u * kRB;
+  s.par_off = off;                 // bias1, bias2
+  off += 2u * kC * 4u;
+  s.bar_off = off;                 // 34 mbarriers + the TMEM address slot
+  s.total = off + 512 + 1024;
+  return s;
+}
+
+__device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t byte_in_row) {
+  return row * 128u + ((((byte_in_row >> 4) ^ (row & 7u)) << 4) | (byte_in_row & 15u));
+}
+
+// Copy 16-byte chunks [lo, hi) of a window with ReLU applied (both buffers 1024-byte aligned, same row
+// phase, so the 128B swizzle is identical and the copy is chunk for chunk).
+__device__ __forceinline__ void relu_copy(uint32_t src, uint32_t dst, int lo, int hi, int lane) {
+  const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
+  for (int c0 = lo; c0 < hi; c0 += 32 * 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u * 32 + lane;
+      if (c < hi) v[u] = lds128(src + static_cast<uint32_t>(c) * 16u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u * 32 + lane;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v[u]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __hmax2(h[i], z);
+      if (c < hi) sts128(dst + static_cast<uint32_t>(c) * 16u, v[u]);
+    }
+  }
+}
+
+// Pair-combined accumulator chunk -> four bf16x2 stmatrix fragments (per 8-channel block `blk`).
+// Lanes 16k+i / 16k+8+i of the accumulator hold the tap-A / tap-B partial sums of channel 8k+i; output
+// row c = A[c] + B[c+1] (conv_ws.cu).  `xb` is column 32 of this warp's chunk (B of the chunk's last
+// row), `res` the residual fragments (or null), `vm` one validity bit per row of the chunk.
+template <bool RES, bool RELU>
+__device__ __forceinline__ void combine_chunk(const uint32_t (&a)[16], uint32_t xb, int blk, float bias,
+                                              const uint32_t* res, uint32_t vm, int lane, uint32_t (&o)[4]) {
+  const int t0 = lane & 3, ci = lane >> 2;
+  const float bnd = __uint_as_float(__shfl_sync(0xffffffffu, xb, 16 * blk + 8 + ci));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t snd = t0 == 0 ? (i < 3 ? a[4 * (i + 1) + 2] : 0u) : a[4 * i + 2];
+    float got = __uint_as_float(__shfl_sync(0xffffffffu, snd, t0 == 3 ? lane - 3 : lane + 1));
+    if (i == 3 && t0 == 3) got = bnd;
+    float y0 = __uint_as_float(a[4 * i + 0]) + __uint_as_float(a[4 * i + 3]) + bias;
+    float y1 = __uint_as_float(a[4 * i + 1]) + got + bias;
+    if (RES) {
+      const float2 rf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&res[i]));
+      y0 += rf.x;
+      y1 += rf.y;
+    }
+    if (RELU) {
+      y0 = fmaxf(y0, 0.f);
+      y1 = fmaxf(y1, 0.f);
+    }
+    const int rb = 8 * i + 2 * t0;
+    if (!((vm >> rb) & 1u)) y0 = 0.f;
+    if (!((vm >> (rb + 1)) & 1u)) y1 = 0.f;
+    const __nv_bfloat162 ob = __floats2bfloat162_rn(y0, y1);
+    o[i] = *reinterpret_cast<const uint32_t*>(&ob);
+  }
+}
+
+__device__ __forceinline__ void tmem_ld_x1(uint32_t taddr, uint32_t& r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr) : "memory");
+}
+
+__device__ __forceinline__ bool row_valid(const PlaneGeom& geo, int64_t row) { return row >= 0 && geo.valid(row); }
+
+template <bool RELU_IN>
+__global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_constant__ BlkLaunch L) {
+  constexpr uint32_t IDESC = idesc_bf16_f32(128, kN);
+  extern __shared__ uint8_t smem_dyn[];
+  uint8_t* smem = smem_align1024(smem_dyn);
+  const int XS = L.xstages;
+  const BlkLayout lay = blk_layout(XS, L.win_alloc, RELU_IN);
+  float* s_bias1 = reinterpret_cast<float*>(smem + lay.par_off);
+  float* s_bias2 = s_bias1 + kC;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.bar_off);
+  uint64_t* xfull = bars;                   // [XS] x window landed
+  uint64_t* xempty = xfull + kMaxXStages;   // [XS] x window consumed (residual read / halo conv1 done)
+  uint64_t* xrfull = xempty + kMaxXStages;  // [2] relu'd copy written
+  uint64_t* xrempty = xrfull + 2;           // [2] relu'd copy read by conv1
+  uint64_t* wfull = xrempty + 2;            // [kWSlots] conv2 window complete
+  uint64_t* wempty = wfull + kWSlots;       // [kWSlots] conv2 window read
+  uint64_t* t1full = wempty + kWSlots;
+  uint64_t* t1empty = t1full + 1;
+  uint64_t* t2full = t1empty + 1;
+  uint64_t* t2empty = t2full + 1;
+  uint64_t* sfull = t2empty + 1;            // [2] staging buffer written by all conv2-epilogue warps
+  uint64_t* sfree = sfull + 2;              // [2] staging buffer read by its TMA store
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int G = L.ngroups;
+  const int g = blockIdx.x % G;
+  const int local = blockIdx.x / G;
+  const int nct = (static_cast<int>(gridDim.x) - g + G - 1) / G;
+  const BlkGroup& grp = L.g[g];
+  // contiguous tile range of this CTA; conv1 runs on it plus one tile either side
+  const int64_t t_begin = L.n_tiles * local / nct;
+  const int64_t t_end = L.n_tiles * (local + 1) / nct;
+  const int n_local = static_cast<int>(t_end - t_begin);
+  const int U = n_local > 0 ? n_local + 2 : 0;
+  const int halo = grp.halo;
+  const int win_rows = kN + 2 * halo;  // rows the UMMAs of one window read
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMaxXStages; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1);  // conv2's store thread (residual read) or, for halo tiles, conv1's commit
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&xrfull[s], 2);  // both ReLU warps
+      mbar_init(&xrempty[s], 1);
+      mbar_init(&sfull[s], 8);
+      mbar_init(&sfree[s], 1);
+    }
+    for (int s = 0; s < kWSlots; ++s) {
+      mbar_init(&wfull[s], 8 * 3);  // 8 conv1-epilogue warps x the 3 conv1 tiles a window spans
+      mbar_init(&wempty[s], 1);
+    }
+    mbar_init(t1full, 1);
+    mbar_init(t1empty, 8);
+    mbar_init(t2full, 1);
+    mbar_init(t2empty, 8);
+    fence_barrier_init();
+  }
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + kC) {
+    s_bias1[threadIdx.x - 64] = grp.bias1[threadIdx.x - 64];
+    s_bias2[threadIdx.x - 64] = grp.bias2[threadIdx.x - 64];
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp >= 2 && warp < 10) {
+    // weights -> TMEM: warps 2-5 conv1 (columns [0,192)), warps 6-9 conv2 ([192,384))
+    const int q = warp & 3;
+    const int set = (warp - 2) >> 2;
+    const uint32_t* src = (set == 0 ? grp.wimg1 : grp.wimg2) + static_cast<size_t>(q * 32 + lane) * 8;
+#pragma unroll 1
+    for (int b = 0; b < kPairs * kKSteps; ++b) {
+      uint32_t r[8];
+      const uint4* p4 = reinterpret_cast<const uint4*>(src + static_cast<size_t>(b) * 128 * 8);
+      const uint4 v0 = p4[0], v1 = p4[1];
+      r[0] = v0.x; r[1] = v0.y; r[2] = v0.z; r[3] = v0.w;
+      r[4] = v1.x; r[5] = v1.y; r[6] = v1.z; r[7] = v1.w;
+      tmem_st8(tbase + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(set * kWCols + b * 8), r);
+    }
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_trigger();
+  pdl_wait();
+
+  const uint32_t x_a = smem_u32(smem + lay.x_off);
+  const uint32_t xr_a = smem_u32(smem + lay.xr_off);
+  const uint32_t w_a = smem_u32(smem + lay.w_off);
+  const bool tr = L.trace != nullptr;
+  // ring positions advance incrementally (the ring depth XS is a runtime value: no division in the loops)
+  auto ring_next = [&](int& slot, uint32_t& phase) {
+    if (++slot == XS) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  };
+
+  if (warp == 0) {
+    // ------------------------------ TMA producer ------------------------------
+    if (lane == 0 && U > 0) {
+      prefetch_tmap(&grp.in_map);
+      const int nboxes = L.win_alloc / kBox;
+      const uint32_t stage_tx = static_cast<uint32_t>(L.win_alloc * kRB);
+      long long t_wait = 0;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = 0; u < U; ++u, ring_next(s, ph)) {
+        const long long t0 = tr ? clock64() : 0;
+        mbar_wait(&xempty[s], ph ^ 1u);
+        if (tr) t_wait += clock64() - t0;
+        mbar_arrive_expect_tx(&xfull[s], stage_tx);
+        const int32_t r0 = static_cast<int32_t>((t_begin + u - 1) * kTile - halo);
+        uint8_t* win = smem + lay.x_off + s * lay.stage;
+        for (int bx = 0; bx < nboxes; ++bx) tma_load_2d(win + bx * kBox * kRB, &grp.in_map, &xfull[s], 0, r0 + bx * kBox);
+      }
+      if (tr) atomicAdd(&L.trace[kBlkTraceProd], static_cast<unsigned long long>(t_wait));
+    }
+  } else if (warp == 1 || warp == kWarpMma2) {
+    // ------------------------------ UMMA issuers ------------------------------
+    // warp 1: conv1 of tiles u = 0 .. U-1; kWarpMma2: conv2 of tiles v = 0 .. n_local-1.  Each warp's
+    // tcgen05.commit tracks only its own UMMAs.
+    const bool c1 = warp == 1;
+    int32_t shift[kPairs];
+#pragma unroll
+    for (int p = 0; p < kPairs; ++p) {
+      const int df = p % 3 - 1;
+      const int dt = p < 3 ? -1 : 1;
+      shift[p] = halo + dt + df * grp.dil * L.geo.T1;
+    }
+    const uint32_t a_base = tbase + static_cast<uint32_t>(c1 ? 0 : kWCols);
+    const uint32_t d_tmem = tbase + static_cast<uint32_t>(c1 ? kAcc1 : kAcc2);
+    uint64_t* tfull = c1 ? t1full : t2full;
+    uint64_t* tempty = c1 ? t1empty : t2empty;
+    const int n = c1 ? U : n_local;
+    long long t_in = 0, t_acc = 0;
+    const long long t_start = clock64();
+    const unsigned long long g_start = globaltimer_ns();
+    int s = 0;
+    uint32_t ph = 0;
+    for (int k = 0; k < n; ++k) {
+      uint32_t src;
+      uint64_t* release;
+      const long long ta = tr ? clock64() : 0;
+      if (c1) {
+        if (RELU_IN) {
+          const int r2 = k & 1;
+          mbar_wait(&xrfull[r2], static_cast<uint32_t>(k >> 1) & 1u);
+          src = xr_a + static_cast<uint32_t>(r2) * lay.stage;
+          release = &xrempty[r2];
+        } else {
+          mbar_wait(&xfull[s], ph);
+          src = x_a + static_cast<uint32_t>(s) * lay.stage;
+          release = nullptr;
+        }
+      } else {
+        const int w = k % kWSlots;
+        mbar_wait(&wfull[w], static_cast<uint32_t>(k / kWSlots) & 1u);
+        src = w_a + static_cast<uint32_t>(w) * lay.stage;
+        release = &wempty[w];
+      }
+      const long long tb = tr ? clock64() : 0;
+      mbar_wait(tempty, (static_cast<uint32_t>(k) & 1u) ^ 1u);
+      if (tr) {
+        t_in += tb - ta;
+        t_acc += clock64() - tb;
+      }
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t bdesc0 = make_sdesc(src, 8 * kRB, kSwizzle128, 0);
+#pragma unroll
+        for (int p = 0; p < kPairs; ++p) {
+#pragma unroll
+          for (int kk = 0; kk < kKSteps; ++kk) {
+            const uint64_t bd = bdesc0 + static_cast<uint64_t>((shift[p] * kRB + kk * 32) >> 4);
+            umma_bf16_ts(d_tmem, a_base + static_cast<uint32_t>((p * kKSteps + kk) * 8), bd, IDESC,
+                         (p | kk) != 0 ? 1u : 0u);
+          }
+        }
+        if (release) umma_commit(release);
+        // halo tiles have no residual reader: their x stage is free once conv1 has read it
+        if (c1 && (k == 0 || k == U - 1)) umma_commit(&xempty[s]);
+        umma_commit(tfull);
+      }
+      __syncwarp();
+      if (c1) ring_next(s, ph);
+    }
+    if (tr && lane == 0) {
+      atomicAdd(&L.trace[c1 ? kBlkTraceM1In : kBlkTraceM2In], static_cast<unsigned long long>(t_in));
+      atomicAdd(&L.trace[c1 ? kBlkTraceM1Acc : kBlkTraceM2Acc], static_cast<unsigned long long>(t_acc));
+      if (c1) {
+        atomicAdd(&L.trace[kBlkTraceTiles], static_cast<unsigned long long>(n_local));
+        atomicAdd(&L.trace[kBlkTraceTotal], static_cast<unsigned long long>(clock64() - t_start));
+        trace_cta_window(L.trace, g_start);
+      }
+    }
+  } else if (warp == kWarpRelu0 || warp == kWarpRelu1) {
+    // ------------------------------ input ReLU --------------------------------
+    if (RELU_IN) {
+      const int nchunks = win_rows * (kRB / 16);
+      const int half = (nchunks / 2 + 31) / 32 * 32;
+      const int lo = warp == kWarpRelu0 ? 0 : half, hi = warp == kWarpRelu0 ? half : nchunks;
+      long long t_w = 0;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = 0; u < U; ++u, ring_next(s, ph)) {
+        const int r2 = u & 1;
+        const long long t0 = tr ? clock64() : 0;
+        mbar_wait(&xfull[s], ph);
+        mbar_wait(&xrempty[r2], (static_cast<uint32_t>(u >> 1) & 1u) ^ 1u);
+        if (tr) t_w += clock64() - t0;
+        relu_copy(x_a + static_cast<uint32_t>(s) * lay.stage, xr_a + static_cast<uint32_t>(r2) * lay.stage, lo, hi, lane);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xrfull[r2]);
+      }
+      if (tr && lane == 0 && warp == kWarpRelu0) atomicAdd(&L.trace[kBlkTraceRelu], static_cast<unsigned long long>(t_w));
+    }
+  } else if (warp < kWarpE2) {
+    // ------------------------------ conv1 epilogue (warps 2-9) ----------------
+    // warp (q, H): TMEM lane quadrant q (channels 16q .. 16q+15), accumulator columns [32H, 32H+32)
+    const int q = warp & 3;
+    const int H = ((warp - 2) >> 2) & 1;
+    const int ci = lane >> 2;
+    const PlaneGeom geo = L.geo;
+    float bias[2];
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) bias[blk] = s_bias1[16 * q + 8 * blk + ci];
+    const uint32_t trash = smem_u32(smem + lay.trash_off);
+    const int r = 32 * H + lane;  // this lane's stmatrix row within the tile
+    const uint32_t tq = tbase + kAcc1 + static_cast<uint32_t>(32 * H) + (static_cast<uint32_t>(q * 32) << 16);
+    long long t_full = 0, t_w = 0, e1_drain = 0, e1_comb = 0, e1_store = 0;
+    for (int u = 0; u < U; ++u) {
+      const int64_t p0 = (t_begin + u - 1) * kTile;
+      const uint32_t vm = __ballot_sync(0xffffffffu, row_valid(geo, p0 + r));
+      const long long ta = tr ? clock64() : 0;
+      mbar_wait(t1full, static_cast<uint32_t>(u) & 1u);
+      const long long t1 = tr ? clock64() : 0;
+      if (tr) t_full += t1 - ta;
+      tc_fence_after();
+      uint32_t a0[16], a1[16], xb = 0;
+      tmem_ld16x256b_x4(tq, a0);
+      tmem_ld16x256b_x4(tq + (16u << 16), a1);
+      if (H == 0) tmem_ld_x1(tq + 32, xb);  // column 64 would only feed row 63, which no tile owns
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(t1empty);
+      const long long t2 = tr ? clock64() : 0;
+      uint32_t o[2][4];
+      combine_chunk<false, true>(a0, xb, 0, bias[0], nullptr, vm, lane, o[0]);
+      combine_chunk<false, true>(a1, xb, 1, bias[1], nullptr, vm, lane, o[1]);
+      if (tr) {
+        asm volatile("" ::"r"(o[0][0]), "r"(o[1][3]));  // time the combine, not a sunk copy of it
+        const long long t3 = clock64();
+        e1_drain += t2 - t1;
+        e1_comb += t3 - t2;
+      }
+      // window u (first written by this tile) must have been released by conv2 of tile u - kWSlots
+      const long long tb = tr ? clock64() : 0;
+      if (u < n_local) mbar_wait(&wempty[u % kWSlots], (static_cast<uint32_t>(u / kWSlots) & 1u) ^ 1u);
+      const long long tc = tr ? clock64() : 0;
+      if (tr) t_w += tc - tb;
+      // h row p0 + r belongs to windows v = u-2, u-1, u at window row r + 63 (u-1-v) + halo
+#pragma unroll
+      for (int dv = -1; dv <= 1; ++dv) {
+        const int v = u - 1 + dv;  // dv = -1: v = u - 2 ... dv = +1: v = u
+        if (v < 0 || v >= n_local) continue;
+        const int wrow = r - dv * kTile + halo;
+        const bool mine = r < kTile && wrow >= 0 && wrow < win_rows;
+        if (!__any_sync(0xffffffffu, mine)) continue;
+        const uint32_t wbase = w_a + static_cast<uint32_t>(v % kWSlots) * lay.stage;
+#pragma unroll
+        for (int blk = 0; blk < 2; ++blk) {
+          const uint32_t cb = static_cast<uint32_t>((2 * q + blk) * 16);
+          const uint32_t addr = mine ? wbase + sw128(static_cast<uint32_t>(wrow), cb) : trash + sw128(static_cast<uint32_t>(lane), cb);
+          stsm_x4_trans(addr, o[blk]);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int dv = -1; dv <= 1; ++dv) {
+          const int v = u - 1 + dv;
+          if (v >= 0 && v < n_local) mbar_arrive(&wfull[v % kWSlots]);
+        }
+      }
+      if (tr) e1_store += clock64() - tc;
+    }
+    if (tr && lane == 0 && warp == 2) {
+      atomicAdd(&L.trace[kBlkTraceE1Full], static_cast<unsigned long long>(t_full));
+      atomicAdd(&L.trace[kBlkTraceE1W], static_cast<unsigned long long>(t_w));
+      atomicAdd(&L.trace[kBlkTraceE1Drain], static_cast<unsigned long long>(e1_drain));
+      atomicAdd(&L.trace[kBlkTraceE1Comb], static_cast<unsigned long long>(e1_comb));
+      atomicAdd(&L.trace[kBlkTraceE1Store], static_cast<unsigned long long>(e1_store));
+    }
+  } else {
+    // ------------------------------ conv2 epilogue (warps 10-17) --------------
+    // Staging buffers are handed over by mbarriers (no group-wide bar.sync): each warp waits for its
+    // buffer to be free, writes its 32 rows x 16 channels, arrives; one thread issues the TMA store.
+    const int e = warp - kWarpE2;
+    const int q = warp & 3;
+    const int H = (e >> 2) & 1;
+    const int ci = lane >> 2;
+    const PlaneGeom geo = L.geo;
+    float bias[2];
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) bias[blk] = s_bias2[16 * q + 8 * blk + ci];
+    const bool lead = e == 0 && lane == 0;
+    const uint32_t stg_a = smem_u32(smem + lay.stg_off);
+    const uint32_t tq = tbase + kAcc2 + static_cast<uint32_t>(32 * H) + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t xrow = static_cast<uint32_t>(halo + 32 * H + lane);
+    const uint32_t srow = static_cast<uint32_t>(32 * H + lane);
+    const int r = 32 * H + lane;
+    if (lead) prefetch_tmap(&grp.out_map);
+    long long t_full = 0, e2_drain = 0, e2_comb = 0, e2_store = 0;
+    int s = XS > 1 ? 1 : 0;  // x stage of conv1 tile u = v + 1
+    uint32_t ph = XS > 1 ? 0u : 1u;
+    for (int v = 0; v < n_local; ++v, ring_next(s, ph)) {
+      const int64_t p0 = (t_begin + v) * kTile;
+      const int sb = v & 1;
+      // residual fragments first: the window landed long ago (this wait only orders the TMA writes)
+      mbar_wait(&xfull[s], ph);
+      const uint32_t xs_a = x_a + static_cast<uint32_t>(s) * lay.stage;
+      uint32_t res[2][4];
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk) ldsm_x4_trans(xs_a + sw128(xrow, static_cast<uint32_t>((2 * q + blk) * 16)), res[blk]);
+      const uint32_t vm = __ballot_sync(0xffffffffu, row_valid(geo, p0 + r));
+      const long long ta = tr ? clock64() : 0;
+      mbar_wait(t2full, static_cast<uint32_t>(v) & 1u);
+      const long long t1 = tr ? clock64() : 0;
+      if (tr) t_full += t1 - ta;
+      tc_fence_after();
+      uint32_t a0[16], a1[16], xb = 0;
+      tmem_ld16x256b_x4(tq, a0);
+      tmem_ld16x256b_x4(tq + (16u << 16), a1);
+      if (H == 0) tmem_ld_x1(tq + 32, xb);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(t2empty);
+      const long long t2 = tr ? clock64() : 0;
+      uint32_t o[2][4];
+      combine_chunk<true, false>(a0, xb, 0, bias[0], res[0], vm, lane, o[0]);
+      combine_chunk<true, false>(a1, xb, 1, bias[1], res[1], vm, lane, o[1]);
+      long long t3 = 0;
+      if (tr) {
+        asm volatile("" ::"r"(o[0][0]), "r"(o[1][3]));
+        t3 = clock64();
+        e2_drain += t2 - t1;
+        e2_comb += t3 - t2;
+      }
+      // staging buffer sb is free once the TMA store of tile v - 2 has read it
+      mbar_wait(&sfree[sb], (static_cast<uint32_t>(v >> 1) & 1u) ^ 1u);
+      const uint32_t sba = stg_a + static_cast<uint32_t>(sb) * 64u * kRB;
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk) stsm_x4_trans(sba + sw128(srow, static_cast<uint32_t>((2 * q + blk) * 16)), o[blk]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfull[sb]);
+      if (lead) {
+        mbar_wait(&sfull[sb], static_cast<uint32_t>(v >> 1) & 1u);
+        tma_store_2d(&grp.out_map, smem + lay.stg_off + sb * 64 * kRB, 0, static_cast<int32_t>(p0));
+        bulk_commit();
+        mbar_arrive(&xempty[s]);  // every warp's residual reads precede its sfull arrival
+        if (v >= 1) {
+          bulk_wait_read1();      // the store of tile v - 1 has read its staging buffer
+          mbar_arrive(&sfree[sb ^ 1]);
+        }
+      }
+      if (tr) e2_store += clock64() - t3;
+    }
+    if (lead) bulk_wait0();
+    if (tr && lead) {
+      atomicAdd(&L.trace[kBlkTraceE2Full], static_cast<unsigned long long>(t_full));
+      atomicAdd(&L.trace[kBlkTraceE2Drain], static_cast<unsigned long long>(e2_drain));
+      atomicAdd(&L.trace[kBlkTraceE2Comb], static_cast<unsigned long long>(e2_comb));
+      atomicAdd(&L.trace[kBlkTraceE2Store], static_cast<unsigned long long>(e2_store));
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tbase, 512);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_blk() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void* p = nullptr;
+    CNRX_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr));
+    if (!p) throw Error(4, "cuTensorMapEncodeTiled not available");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+void make_map(const void* plane, int64_t nalloc, uint32_t box_rows, CUtensorMap* m) {
+  std::memset(m, 0, sizeof(CUtensorMap));
+  if (!plane) return;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(kC), static_cast<cuuint64_t>(nalloc)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(kRB)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kC), box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn_blk()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(plane), dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
+template <bool RELU_IN>
+void launch_t(const BlkLaunch& L, int grid, cudaStream_t stream) {
+  const BlkLayout lay = blk_layout(L.xstages, L.win_alloc, RELU_IN);
+  ensure_smem_attr(reinterpret_cast<const void*>(conv_blk64_kernel<RELU_IN>), static_cast<int>(lay.total));
+  launch_pdl(conv_blk64_kernel<RELU_IN>, dim3(grid), dim3(kThreads), lay.total, stream, L);
+}
+
+}  // namespace
+
+int64_t conv_blk64_tiles(int64_t nalloc) { return (nalloc + kTile - 1) / kTile; }
+
+int conv_blk64_win_alloc(int halo) { return (kN + 2 * halo + kBox - 1) / kBox * kBox; }
+
+// a window may take h rows from at most the neighbouring conv1 tile on either side
+bool conv_blk64_supported_halo(int halo) { return halo >= 1 && halo + 1 <= kTile; }
+
+void conv_blk64_make_maps(const void* in, const void* out, int64_t nalloc, BlkGroup* g) {
+  make_map(in, nalloc, kBox, &g->in_map);
+  make_map(out, nalloc, kTile, &g->out_map);
+}
+
+size_t conv_blk64_smem_bytes(int xstages, int win_alloc, int relu_in) {
+  return blk_layout(xstages, win_alloc, relu_in).total;
+}
+
+int conv_blk64_xstages(int win_alloc, int relu_in) {
+  for (int xs = kMaxXStages; xs >= 4; --xs)
+    if (blk_layout(xs, win_alloc, relu_in).total <= 227u * 1024u) return xs;
+  return 0;
+}
+
+const char* conv_blk64_launch(const BlkLaunch& L, int num_sms, cudaStream_t stream) {
+  const int64_t work = static_cast<int64_t>(L.ngroups) * L.n_tiles;
+  int grid = static_cast<int>(work < num_sms ? work : num_sms);
+  if (grid < L.ngroups) grid = L.ngroups;
+  if (L.relu_in)
+    launch_t<true>(L, grid, stream);
+  else
+    launch_t<false>(L, grid, stream);
+  return "conv_blk64_kernel";
+}
+
+}  // namespace cnrx

@@ -48,7 +48,6 @@ constexpr int kTileRows = 127;    // output rows per tile
 constexpr int kN = 128;           // UMMA N (plane rows per instruction)
 constexpr int kPairs = 6;
 constexpr int kKSteps = kC / 16;  // 4
-constexpr int kWCols = kPairs * kKSteps * 8;  // 192 TMEM columns of weights
 constexpr int kAcc0 = 256;        // accumulator columns [256,384) and [384,512)
 constexpr int kBox = 32;
 
@@ -85,6 +84,19 @@ __device__ __forceinline__ void epi_group_sync(int e) {
 // kWsDynamic reads them from the launch instead.
 enum : int { kWsRes = 1, kWsOut2 = 2, kWsOut2Bn = 4, kWsRelu = 8, kWsReluIn = 16, kWsDynamic = -1 };
 constexpr int kWsThreads = 640;  // 20 warps: producer, MMA (stage 0), 16 epilogue, input-ReLU, MMA (stage 1)
+
+// Poll back-off (ns) of the roles that are not on the tensor core's critical path.  The epilogue groups
+// spend most of their two-tile budget waiting for an accumulator: polled tightly, those waits were ~58 %
+// of the SM's issued instructions (ncu source view), taking issue slots from the ReLU and UMMA warps.
+#ifndef CNRX_WS_SLEEP_NS
+#define CNRX_WS_SLEEP_NS 128
+#endif
+__device__ __forceinline__ void ws_wait_relaxed(uint64_t* bar, uint32_t parity) {
+  if (CNRX_WS_SLEEP_NS > 0)
+    mbar_wait_backoff<CNRX_WS_SLEEP_NS>(bar, parity);
+  else
+    mbar_wait(bar, parity);
+}
 
 // In-place ReLU of 16-byte chunks [lo, hi) of a shared-memory window, one warp, batches of 16 chunks per
 // lane so all loads are in flight before the first store (shared-memory latency is long while the
@@ -193,7 +205,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
   const int relu_n = (kN + 1 + 2 * grp.halo) * (kRB / 16);  // only the rows the UMMAs read
   auto relu_stage = [&](int jr, int lo, int hi) {
     const int s = jr % L.stages;
-    mbar_wait(&full[s], static_cast<uint32_t>(jr / L.stages) & 1u);
+    ws_wait_relaxed(&full[s], static_cast<uint32_t>(jr / L.stages) & 1u);
     if (!(L.debug & 2)) relu_chunks(smem_u32(smem + lay.win_off + s * lay.win_stage), lo, hi, lane);
     fence_proxy_async_smem();
     __syncwarp();
@@ -213,7 +225,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
         const uint32_t k = static_cast<uint32_t>(j / L.stages);
         const int64_t p0 = tile * kTileRows;
         const long long tp0 = L.trace ? clock64() : 0;
-        mbar_wait(&empty[s], (k & 1u) ^ 1u);
+        ws_wait_relaxed(&empty[s], (k & 1u) ^ 1u);
         if (L.trace) tr_prod += clock64() - tp0;
         mbar_arrive_expect_tx(&full[s], stage_tx);
         uint8_t* win = smem + lay.win_off + s * lay.win_stage;
@@ -345,14 +357,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
     for (int64_t tile = local + static_cast<int64_t>(e) * nct; tile < n_tiles; tile += 2 * static_cast<int64_t>(nct), j += 2) {
       const int64_t p0 = tile * kTileRows;
       const long long te0 = clock64();
-      mbar_wait(&tfull[e], static_cast<uint32_t>(j >> 1) & 1u);
+      ws_wait_relaxed(&tfull[e], static_cast<uint32_t>(j >> 1) & 1u);
       const long long te1 = clock64();
       tr_ew += te1 - te0;
       // staging buffer free? (this group's previous TMA store has read it)
       if (lead) bulk_wait_read0();
       epi_group_sync(e);
       const int kb = (j >> 1) & 1;  // residual buffer of this group tile
-      if (has_res) mbar_wait(&rfull[2 * e + kb], static_cast<uint32_t>(j >> 2) & 1u);
+      if (has_res) ws_wait_relaxed(&rfull[2 * e + kb], static_cast<uint32_t>(j >> 2) & 1u);
       const uint32_t rbuf_a = smem_u32(rbuf0 + kb * 128 * kRB);
       const long long te2 = clock64();
       tr_sw += te2 - te1;

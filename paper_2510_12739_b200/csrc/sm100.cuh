@@ -90,6 +90,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Same, but polling with a nanosleep back-off: for kernels with many waiting warps, whose polls would
+// otherwise take issue slots from the working ones (a try_wait returns after a few tens of cycles).
+template <unsigned kSleepNs>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  const long long t0 = clock64();
+  for (;;) {
+    __nanosleep(kSleepNs);
+    if (mbar_try_wait(addr, parity)) return;
+    if (static_cast<unsigned long long>(clock64() - t0) > CNRX_WAIT_LIMIT_CYCLES) {
+      printf("cnrx: mbarrier wait timeout (block %d thread %d parity %u)\n", blockIdx.x, threadIdx.x, parity);
+      __trap();
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Async proxy fences and TMA
 // ---------------------------------------------------------------------------------------------

@@ -498,8 +498,8 @@ int main() {
     CUtensorMap tm = make_map(gs, 32768, 64, 32, 64, CU_TENSOR_MAP_SWIZZLE_128B);
     CK(cudaFuncSetAttribute(mma_ts_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
     const char* names[5] = {"none", "LDG.128 nc", "STG.128", "LDS+STS", "TMA 2D load"};
-    for (int N : {128, 256})
-      for (int mode = 0; mode < 5; ++mode) {
+    for (int N : {32, 64, 96, 128, 256})
+      for (int mode = 0; mode < (N < 128 ? 1 : 5); ++mode) {
         const int iters = 20000;
         CK(cudaMemset(dB, 0, 8));
         mma_ts_rate<<<nblk, 256, 80 * 1024>>>(N, iters, mode, dCyc, dB, gs, gd, tm);
