@@ -926,9 +926,29 @@ struct Bf16Compiler {
 // ------------------------------------------------------------------------------------------------
 // Execution
 // ------------------------------------------------------------------------------------------------
+void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F);
+
+// A failed (re)build (batch too large for one plane, out of device memory) leaves no half-built
+// workspace behind: the next call rebuilds from scratch.
 void ensure_workspace(cnrx_plan& p, int B, int T, int F) {
   Workspace& ws = p.ws;
   if (ws.B == B && ws.T == T && ws.F == F) return;
+  if (p.precision != CNRX_FP32) make_geom(B, T, F, p.npad);  // validate before touching any state
+  try {
+    ensure_workspace_impl(p, B, T, F);
+  } catch (...) {
+    for (void* b : ws.buffers) cudaFree(b);
+    ws.buffers.clear();
+    ws.sizes.clear();
+    ws.launches.clear();
+    ws.cap_B = 0;
+    ws.B = ws.T = ws.F = -1;
+    throw;
+  }
+}
+
+void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
+  Workspace& ws = p.ws;
   // A smaller batch of the same grid reuses the buffers (capacity cap_B): only the geometry and the
   // launch descriptors change.  Every producer writes all rows of [0, Nalloc) (zeros on padding rows)
   // and TMA zero-fills past the descriptor's Nalloc, so stale rows beyond it are never read.

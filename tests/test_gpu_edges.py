@@ -1,0 +1,75 @@
+"""Edge cases of the drop-in boundary on the GPU: empty / degenerate shapes rejected exactly as the
+reference rejects them (tensor.hpp checked_numel -> std::invalid_argument "tensor dimensions must be
+positive"), the one-plane row limit, recovery after a failed workspace build, the smallest grids, and
+the largest batch the bench sweeps (per-slot results identical to running the slot alone)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+import emulate_bf16 as E
+from paper_2510_12739_b200 import graph as G, plan as P, slots
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_empty_and_degenerate_shapes_are_rejected_like_the_reference(prec):
+    p = P.Plan(G.CONFIGS["cfg1"].graph(), prec)
+    for shape in [(0, 14, 72, 6), (2, 0, 72, 6), (2, 14, 0, 6)]:
+        with pytest.raises(P.CnrxInvalidArgument, match="dimensions must be positive"):
+            p.forward(np.zeros(shape, np.float32))
+    # the plan is still usable afterwards
+    x = np.random.default_rng(0).standard_normal((1, 14, 72, 6)).astype(np.float32)
+    y = p.forward(x)
+    assert y.shape == (1, 14, 72, 2) and np.isfinite(y).all()
+
+
+def test_batch_beyond_one_plane_is_an_error_and_the_plan_recovers():
+    import torch
+    g = G.CONFIGS["cfg2"].graph()
+    p = P.Plan(g, "bf16")
+    x = torch.zeros((1, 14, 612, 12), dtype=torch.float32, device="cuda")
+    out = torch.zeros((1, 14, 612, 4), dtype=torch.float32, device="cuda")
+    huge = 240_000  # 240000 slots x 9195 rows > 2^31 plane rows: rejected before any allocation or access
+    for _ in range(2):  # twice: a failed build must not leave a stale workspace for the same shape
+        rc = P.lib().cnrx_forward_device(p.h, C.c_void_p(x.data_ptr()), huge, 14, 612, 12, P.MODE_EVAL,
+                                         C.c_void_p(out.data_ptr()), None)
+        assert rc == P.ERR_INVALID_ARGUMENT
+        assert "too large" in P.lib().cnrx_last_error().decode()
+    xs = np.random.default_rng(1).standard_normal((2, 14, 612, 12)).astype(np.float32)
+    assert np.isfinite(p.forward(xs)).all()
+
+
+@pytest.mark.parametrize("F", [1, 2, 3])
+def test_smallest_grids_fp32_bit_exact_bf16_vs_emulation(F):
+    g = G.CONFIGS["cfg2"].graph(seed=5)
+    x = np.random.default_rng(F).standard_normal((2, 14, F, 12)).astype(np.float32)
+    ref = oracle.RefNet.from_graph(g).forward(x)
+    assert np.array_equal(P.Plan(g, "fp32").forward(x), ref)
+    got = P.Plan(g, "bf16").forward(x)
+    emu = E.emulate(g, x)
+    assert np.linalg.norm(got - emu) / np.linalg.norm(emu) <= 2e-2
+
+
+def test_largest_bench_batch_slots_match_single_slot_runs():
+    """B = 4096 cfg2 slots through the device receive path (30 GB of activation planes): sampled slots
+    are bit-identical to the same slot received alone."""
+    import torch
+    cfg = G.CONFIGS["cfg2"]
+    link = cfg.link
+    g = cfg.graph(seed=9)
+    p = P.Plan(g, "bf16")
+    pmask, pvals = slots.pilot_pattern(link.T, link.F, link.pilot_symbols, link.pilot_spacing)
+    p.set_pilots(pvals.astype(np.complex64), pmask)
+    B = 4096
+    y, _bits = P.generate_slots_device(link, B, 77, slot0=0)
+    out = torch.empty((B, link.T, link.F, link.bits), dtype=torch.float32, device="cuda")
+    p.receive_device(y, out, torch.cuda.current_stream().cuda_stream)
+    one = torch.empty((1, link.T, link.F, link.bits), dtype=torch.float32, device="cuda")
+    for i in (0, 1234, B - 1):
+        p.receive_device(y[i:i + 1].contiguous(), one, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(one[0], out[i]), i
+    assert torch.isfinite(out).all()
