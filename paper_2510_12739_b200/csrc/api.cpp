@@ -32,6 +32,7 @@
 #include "common.h"
 #include "conv_tc.h"
 #include "conv_blk.h"
+#include "conv_pair.h"
 #include "conv_ws.h"
 #include "slotgen.h"
 #include "kernels.h"
@@ -188,6 +189,7 @@ struct Workspace {
   struct GroupLaunch {
     bool ws = false;
     bool blk = false;
+    bool pair = false;  // conv_pair.cu (CTA-pair 96 -> 96 3x3)
     TcLaunch tc;
     WsLaunch wsl;
     BlkLaunch blkl;
@@ -1085,6 +1087,16 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           if (op.res_plane >= 0) L.flags |= 1;
           if (op.out2_plane >= 0) L.flags |= 2;
         }
+        // 96 -> 96 3x3 convs run on CTA pairs (CNRX_NO_PAIR=1: the single-CTA kernel)
+        const bool no_pair = getenv("CNRX_NO_PAIR") && atoi(getenv("CNRX_NO_PAIR")) != 0;
+        int max_halo = 0;
+        for (int k : grp) max_halo = std::max(max_halo, ws.geo.T1 * p.tc[static_cast<size_t>(k)].dil + 1);
+        if (!no_pair && conv_pair96_supported(op0.cin, op0.cout, op0.ks, max_halo)) {
+          GL.pair = true;
+          L.stages = conv_pair96_stages(win_alloc);
+          ws.launches.push_back(GL);
+          continue;
+        }
         int stages = 4;
         while (stages > 1 && conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc, L.flags) > 227 * 1024)
           --stages;
@@ -1262,6 +1274,10 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
         if (!dtrace) CNRX_CUDA(cudaMalloc(&dtrace, 32 * sizeof(unsigned long long)));
         CNRX_CUDA(cudaMemsetAsync(dtrace, 0, 32 * sizeof(unsigned long long), s));
         GL.tc.trace = dtrace;
+      }
+      if (GL.pair) {
+        p.note(conv_pair96_launch(GL.tc, p.num_sms, s), s, fl);
+        continue;
       }
       p.note(conv_tc_launch(op0.cin, op0.cout, op0.ks, GL.tc, p.num_sms, s), s, fl);
       if (trace) {

@@ -1,0 +1,17 @@
+// conv_pair.h — launch interface of the CTA-pair (tcgen05 cta_group::2) 96 -> 96 channel 3x3
+// convolution (conv_pair.cu).  Uses the same TcLaunch / TcGroup descriptors and weight image as
+// conv_tc.cu's <96,96,3> kernel.
+#pragma once
+#include "conv_tc.h"
+
+namespace cnrx {
+
+// True for a 3x3 96 -> 96 conv whose window (halo rows either side) fits the pair kernel's smem.
+bool conv_pair96_supported(int cin, int cout, int ks, int halo);
+// Window pipeline depth that fits in shared memory for `win_alloc`-row windows (0: none).
+int conv_pair96_stages(int win_alloc);
+size_t conv_pair96_smem_bytes(int stages, int win_alloc);
+// Grid: CTA pairs (cluster of 2), at most num_sms / 2 pairs.  Returns the kernel name.
+const char* conv_pair96_launch(const TcLaunch& L, int num_sms, cudaStream_t stream);
+
+}  // namespace cnrx
