@@ -286,7 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         if (leader)
-          mbar_arrive(&tempty[a]);
+          mbar_arrive_relaxed(&tempty[a]);
         else
           mbar_arrive_cluster_relaxed(a ? tempty_leader1 : tempty_leader0);
       }

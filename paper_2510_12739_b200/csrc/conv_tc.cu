@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
           if (cc == COUT / 32 - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[a]);
+            if (lane == 0) mbar_arrive_relaxed(&tempty[a]);
           }
 #pragma unroll
           for (int v8 = 0; v8 < 4; ++v8) {
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
           if (cc == COUT / 32 - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[a]);
+            if (lane == 0) mbar_arrive_relaxed(&tempty[a]);
           }
           // two 16-channel pieces per 32-column chunk, each stored with one 256-bit access
 #pragma unroll

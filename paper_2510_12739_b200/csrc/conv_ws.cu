@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
         if (h == 1) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[e]);
+          if (lane == 0) mbar_arrive_relaxed(&tempty[e]);
         }
 #pragma unroll
         for (int blk = 0; blk < 2; ++blk) {
