@@ -143,7 +143,6 @@ struct PlaneInfo {
   int level = 0;       // level of its producer
   int last_use = 0;    // last level reading it
   int buffer = -1;     // workspace buffer index
-  bool dead = false;   // conv1 output inside a fused block: never written, no buffer
 };
 struct TcOp {
   int node = -1;
@@ -155,8 +154,9 @@ struct TcOp {
   int in_plane = -1, res_plane = -1, out_plane = -1, out2_plane = -1;
   int relu = 0;
   int relu_in = 0;  // ws kernels: input is relu(in_plane), applied to the window on load
-  // fused residual block (conv_blk.cu): this op is conv2 and `blk_c1` its conv1, whose output plane is
-  // never materialised; the conv1 op is then `fused_away` (not launched)
+  // fused residual block (conv_blk.cu): this op is conv2 and `blk_c1` its conv1 (`fused_away`).  When
+  // the workspace runs blocks fused, conv1 is not launched and its output plane is not written; the
+  // two-kernel program over the same planes stays available (chosen per batch size).
   int blk_c1 = -1;
   bool fused_away = false;
   void* wimg = nullptr;
@@ -189,12 +189,14 @@ struct Workspace {
   struct GroupLaunch {
     bool ws = false;
     bool blk = false;
+    bool skip = false;  // conv1 group of fused blocks while the workspace runs them fused
     bool pair = false;  // conv_pair.cu (CTA-pair 96 -> 96 3x3)
     TcLaunch tc;
     WsLaunch wsl;
     BlkLaunch blkl;
   };
   std::vector<GroupLaunch> launches;  // prepared tensor maps per TC group (bf16)
+  bool blocks_fused = false;          // residual blocks run as conv_blk64 at this batch size
 };
 
 }  // namespace
@@ -679,13 +681,14 @@ struct Bf16Compiler {
     return st.out_plane;
   }
 
-  // Opt-in (CNRX_BLK=1): pre-activation residual blocks y = conv2(relu(bn(conv1(relu?(x))))) + x over
-  // 64-channel planes as one kernel (conv_blk.cu) when conv1's output feeds nothing but conv2.  Same
-  // values as the two-kernel path (conv1's output is rounded to bf16 either way); measured no faster at
-  // cfg2 sizes, so the two-kernel path stays the default.
+  // Pre-activation residual blocks y = conv2(relu(bn(conv1(relu?(x))))) + x over 64-channel planes, when
+  // conv1's output feeds nothing but conv2, can run as one kernel (conv_blk.cu): same values as the
+  // two-kernel path (conv1's output is rounded to bf16 either way).  Measured faster for small batches
+  // (half the launches: B = 1 latency -21 %) and not for large ones, so ensure_workspace picks the
+  // program per batch (blocks_fused); CNRX_BLK=0 disables the fused form, CNRX_BLK=1 forces it.
   void fuse_blocks() {
     const char* e = getenv("CNRX_BLK");
-    if (!e || atoi(e) == 0) return;
+    if (e && atoi(e) == 0) return;
     std::vector<int> readers(p.planes.size(), 0);
     for (const auto& op : p.tc) {
       if (op.in_plane >= 0) ++readers[static_cast<size_t>(op.in_plane)];
@@ -705,7 +708,6 @@ struct Bf16Compiler {
       if (readers[static_cast<size_t>(a.out_plane)] != 1) continue;
       b.blk_c1 = ai;
       a.fused_away = true;
-      p.planes[static_cast<size_t>(a.out_plane)].dead = true;
     }
   }
 
@@ -857,7 +859,6 @@ struct Bf16Compiler {
     static const bool no_stem = getenv("CNRX_STEM") == nullptr;
     for (int k = 0; k < static_cast<int>(p.tc.size()); ++k) {
       TcOp& op = p.tc[static_cast<size_t>(k)];
-      if (op.fused_away) continue;
       if (!no_stem && op.stem_w && static_cast<int>(p.stem_ops.size()) < kStemMaxOps &&
           (p.stem_ops.empty() || p.tc[static_cast<size_t>(p.stem_ops[0])].cin_real == op.cin_real)) {
         op.stem = true;
@@ -866,20 +867,20 @@ struct Bf16Compiler {
     }
     p.need_plane0 = false;
     for (const auto& op : p.tc)
-      if (!op.stem && !op.fused_away && (op.in_plane == 0 || op.res_plane == 0)) p.need_plane0 = true;
+      if (!op.stem && (op.in_plane == 0 || op.res_plane == 0)) p.need_plane0 = true;
     for (const auto& st2 : p.pw)
       for (int k = 0; k < st2.n_planes; ++k)
         if (st2.plane_ids[k] == 0) p.need_plane0 = true;
     for (int k = 0; k < static_cast<int>(p.tc.size()); ++k) {
       const TcOp& op = p.tc[static_cast<size_t>(k)];
-      if (op.stem || op.fused_away) continue;
+      if (op.stem) continue;
       auto& groups = p.tc_groups_by_level[static_cast<size_t>(op.level)];
       bool placed = false;
       for (auto& g : groups) {
         const TcOp& o0 = p.tc[static_cast<size_t>(g[0])];
         const bool blk0 = o0.blk_c1 >= 0, blk = op.blk_c1 >= 0;
         if (static_cast<int>(g.size()) < kTcMaxGroups && o0.cin == op.cin && o0.cout == op.cout && o0.ks == op.ks &&
-            o0.ws == op.ws && blk0 == blk &&
+            o0.ws == op.ws && blk0 == blk && o0.fused_away == op.fused_away &&
             (!blk || p.tc[static_cast<size_t>(o0.blk_c1)].relu_in == p.tc[static_cast<size_t>(op.blk_c1)].relu_in)) {
           g.push_back(k);
           placed = true;
@@ -906,7 +907,6 @@ struct Bf16Compiler {
     std::vector<int> buf_free_after;
     for (int pl : order) {
       auto& pi = p.planes[static_cast<size_t>(pl)];
-      if (pi.dead) continue;
       if (pi.last_use < pi.level) pi.last_use = pi.level;
       int chosen = -1;
       for (size_t b = 0; b < p.buf_channels.size(); ++b)
@@ -994,12 +994,27 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
     return pl < 0 ? nullptr
                   : static_cast<__nv_bfloat16*>(ws.buffers[static_cast<size_t>(p.planes[static_cast<size_t>(pl)].buffer)]);
   };
+  // fused residual blocks for small batches (or when forced), if every block's window fits
+  bool fused = false;
+  {
+    const char* e = getenv("CNRX_BLK");
+    const int force = e ? atoi(e) : -1;
+    fused = force == 1 || (force != 0 && B <= kBlkAutoMaxBatch);
+    for (const auto& op : p.tc)
+      if (op.blk_c1 >= 0 && !conv_blk64_supported_halo(ws.geo.T1 * op.dil + 1)) fused = false;
+  }
+  ws.blocks_fused = fused;
   for (int lv = 0; lv < p.n_levels; ++lv)
     for (auto& grp : p.tc_groups_by_level[static_cast<size_t>(lv)]) {
       Workspace::GroupLaunch GL;
       const TcOp& op0 = p.tc[static_cast<size_t>(grp[0])];
       GL.ws = op0.ws;
-      GL.blk = op0.blk_c1 >= 0;
+      GL.skip = fused && op0.fused_away;
+      GL.blk = fused && op0.blk_c1 >= 0;
+      if (GL.skip) {
+        ws.launches.push_back(GL);
+        continue;
+      }
       if (GL.blk) {
         BlkLaunch& L = GL.blkl;
         std::memset(&L, 0, sizeof(L));
@@ -1014,9 +1029,6 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           BlkGroup& g = L.g[gi];
           g.dil = c1.dil;
           g.halo = ws.geo.T1 * c1.dil + 1;
-          if (!conv_blk64_supported_halo(g.halo))
-            throw Error(CNRX_ERR_UNSUPPORTED, "fused residual block: T+1 = " + std::to_string(ws.geo.T1) + " with dilation " +
-                                                  std::to_string(c1.dil) + " exceeds its window (unset CNRX_BLK)");
           win_alloc = std::max(win_alloc, conv_blk64_win_alloc(g.halo));
           conv_blk64_make_maps(plane_ptr(c1.in_plane), plane_ptr(c2.out_plane), ws.geo.Nalloc, &g);
           g.wimg1 = static_cast<const uint32_t*>(c1.wimg);
@@ -1026,7 +1038,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
         }
         L.win_alloc = win_alloc;
         L.xstages = conv_blk64_xstages(win_alloc, L.relu_in);
-        if (L.xstages == 0) throw Error(CNRX_ERR_UNSUPPORTED, "fused residual block exceeds shared memory (unset CNRX_BLK)");
+        if (L.xstages == 0) throw Error(CNRX_ERR_UNSUPPORTED, "fused residual block exceeds shared memory (set CNRX_BLK=0)");
       } else if (op0.ws) {
         WsLaunch& L = GL.wsl;
         std::memset(&L, 0, sizeof(L));
@@ -1206,15 +1218,16 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
       if (grp.empty()) continue;
       const TcOp& op0 = p.tc[static_cast<size_t>(grp[0])];
       int64_t fl = 0;
+      Workspace::GroupLaunch& GL = ws.launches[li++];
+      if (GL.skip) continue;
       for (int k : grp) {
         const TcOp& o = p.tc[static_cast<size_t>(k)];
         fl += 2ll * o.ks * o.ks * o.cin_real * o.cout_real;
-        if (o.blk_c1 >= 0) {
+        if (GL.blk) {
           const TcOp& o1 = p.tc[static_cast<size_t>(o.blk_c1)];
           fl += 2ll * o1.ks * o1.ks * o1.cin_real * o1.cout_real;
         }
       }
-      Workspace::GroupLaunch& GL = ws.launches[li++];
       static const bool trace = getenv("CNRX_TRACE") != nullptr;
       static unsigned long long* dtrace = nullptr;
       if (GL.blk) {

@@ -8,6 +8,8 @@
 namespace cnrx {
 
 constexpr int kTcMaxGroups = 4;
+// batches up to this many slots run fused residual blocks (conv_blk.cu) when the plan has them
+constexpr int kBlkAutoMaxBatch = 48;
 
 // One convolution of a grouped launch (e.g. the same layer of the three CoNet subnetworks).
 struct TcGroup {
