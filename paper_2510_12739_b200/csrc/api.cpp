@@ -1105,7 +1105,19 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
         for (int k : grp) max_halo = std::max(max_halo, ws.geo.T1 * p.tc[static_cast<size_t>(k)].dil + 1);
         if (!no_pair && conv_pair96_supported(op0.cin, op0.cout, op0.ks, max_halo)) {
           GL.pair = true;
-          L.stages = conv_pair96_stages(win_alloc);
+          // TMA-staged epilogue for launches with a residual / second output when its two tile buffers fit
+          // (not for dilated windows: one buffer serialises the residual load behind the previous store
+          // and measured slower than direct stores); otherwise the direct-store epilogue
+          const bool staged = (L.flags & 3) != 0 && conv_pair96_stages(win_alloc, true) > 0;
+          if (staged) L.flags |= kPairStaged;
+          L.stages = conv_pair96_stages(win_alloc, staged);
+          for (size_t gi = 0; gi < grp.size(); ++gi) {
+            const TcOp& op = p.tc[static_cast<size_t>(grp[gi])];
+            TcGroup& g = L.g[gi];
+            conv_tc_make_maps(plane_ptr(op.res_plane), ws.geo.Nalloc, op.cout, 128, g.pres);
+            conv_tc_make_maps(plane_ptr(op.out_plane), ws.geo.Nalloc, op.cout, 128, g.pout);
+            conv_tc_make_maps(plane_ptr(op.out2_plane), ws.geo.Nalloc, op.cout, 128, g.pout2);
+          }
           ws.launches.push_back(GL);
           continue;
         }

@@ -40,23 +40,37 @@ constexpr int kTapBytes = kHalfN * (kRB0 + kRB1);  // 9216: one tap of this CTA'
 constexpr int kWBytes = 9 * kTapBytes;             // 82944
 constexpr int kTmemCols = 256;       // 2 accumulator stages x 96 columns
 constexpr int kBox = 32;
-constexpr int kThreads = 320;   // producer, UMMA, 8 epilogue warps
+constexpr int kThreads = 352;   // producer, UMMA, 8 epilogue warps, store warp
+constexpr int kStoreWarp = 10;
+constexpr uint32_t kTileBytes = 128u * (kRB0 + kRB1);  // one 128-row tile of a 96-ch plane (24 KB)
 
+// `staged` (launches with a residual and/or a second output): residual tiles arrive by TMA into rbuf,
+// the epilogue writes y over them in place (same swizzled positions) and the pre-activated copy into
+// o2buf, and the store warp writes both planes with TMA.  Those launches keep 2 window stages.
 struct PairLayout {
-  uint32_t w_off, win_off, win_stage, win_c1, par_off, bar_off, total;
+  uint32_t w_off, win_off, win_stage, win_c1, rbuf_off, o2_off, par_off, bar_off, total;
 };
-__host__ __device__ inline PairLayout pair_layout(int stages, int win_alloc) {
+__host__ __device__ inline PairLayout pair_layout(int stages, int win_alloc, bool staged) {
   PairLayout s{};
   s.w_off = 0;
   s.win_off = (kWBytes + 1023u) & ~1023u;
   s.win_c1 = (static_cast<uint32_t>(win_alloc * kRB0) + 1023u) & ~1023u;
   s.win_stage = (s.win_c1 + static_cast<uint32_t>(win_alloc * kRB1) + 1023u) & ~1023u;
   uint32_t off = s.win_off + static_cast<uint32_t>(stages) * s.win_stage;
+  s.rbuf_off = off;                  // staged: 2 x [128 rows: 64 ch SW128 | 32 ch SW64]
+  if (staged) off += 2u * kTileBytes;
+  s.o2_off = off;                    // staged: 1 x the same
+  if (staged) off += kTileBytes;
   s.par_off = off;                   // bias, s2, t2
   off += 3u * kC * 4u;
   s.bar_off = (off + 15u) & ~15u;
   s.total = s.bar_off + 256 + 1024;
   return s;
+}
+// byte offset of channels [ch, ch+8) of tile row r in a staged tile buffer
+__device__ __forceinline__ uint32_t tile_off(uint32_t r, uint32_t ch) {
+  return ch < 64 ? r * 128u + ((((ch >> 3) ^ (r & 7u))) << 4)
+                 : 128u * kRB0 + r * 64u + (((((ch - 64) >> 3) ^ ((r >> 1) & 3u))) << 4);
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -112,7 +126,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr uint32_t IDESC = idesc_bf16_f32(256, kC);
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
-  const PairLayout lay = pair_layout(L.stages, L.win_alloc);
+  const bool staged = (L.flags & kPairStaged) != 0;
+  const PairLayout lay = pair_layout(L.stages, L.win_alloc, staged);
+  // tile buffer (residual in / y out) of pair-tile j and the parity of its use
+  auto tbuf = [](int jj) { return jj & 1; };
+  auto tpar = [](int jj) { return static_cast<uint32_t>(jj >> 1) & 1u; };
   uint8_t* sW = smem + lay.w_off;
   float* s_bias = reinterpret_cast<float*>(smem + lay.par_off);
   float* s_s2 = s_bias + kC;
@@ -124,7 +142,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + L.stages;   // [stages] window stage consumed (multicast commit)
   uint64_t* tfull = empty + L.stages;  // [2] accumulator ready (multicast commit)
   uint64_t* tempty = tfull + 2;        // [2] (leader) accumulator drained by both CTAs
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;        // [2] staged: residual tile landed
+  uint64_t* rempty = rfull + 2;        // [2] staged: tile buffer's TMA store has read it
+  uint64_t* sfull = rempty + 2;        // [2] staged: all epilogue warps wrote the tile buffer
+  uint64_t* o2free = sfull + 2;        // staged: o2buf's TMA store has read it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o2free + 1);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -150,10 +172,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 16);  // 8 epilogue warps x 2 CTAs
+      mbar_init(&rfull[a], 1);
+      mbar_init(&rempty[a], 1);
+      mbar_init(&sfull[a], 8);
     }
+    mbar_init(o2free, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp >= 2) {
+  if (warp >= 2 && warp < kStoreWarp) {
     for (int c = threadIdx.x - 64; c < kC; c += 256) {
       s_bias[c] = grp.bias[c];
       s_s2[c] = grp.s2 ? grp.s2[c] : 1.f;
@@ -205,6 +231,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tma_load_2d_2sm(win + bx * kBox * kRB0, &grp.map[0], fb, 0, r0 + bx * kBox);
           tma_load_2d_2sm(win + lay.win_c1 + bx * kBox * kRB1, &grp.map[1], fb, 0, r0 + bx * kBox);
         }
+        const int64_t tile = 2 * k + rank;
+        if (staged && grp.res && tile < n_tiles) {
+          const int b = tbuf(j);
+          mbar_wait(&rempty[b], tpar(j) ^ 1u);
+          mbar_arrive_expect_tx(&rfull[b], kTileBytes);
+          uint8_t* rb = smem + lay.rbuf_off + b * kTileBytes;
+          tma_load_2d(rb, &grp.pres[0], &rfull[b], 0, static_cast<int32_t>(tile * 128));
+          tma_load_2d(rb + 128 * kRB0, &grp.pres[1], &rfull[b], 0, static_cast<int32_t>(tile * 128));
+        }
       }
     }
   } else if (warp == 1) {
@@ -251,25 +286,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
+  } else if (warp == kStoreWarp) {
+    // ------------------------------ TMA store warp (staged launches) ----------
+    if (staged && lane == 0) {
+      prefetch_tmap(&grp.pout[0]);
+      prefetch_tmap(&grp.pout[1]);
+      int j = 0;
+      for (int64_t k = local; k < n_ptiles; k += npc, ++j) {
+        const int64_t tile = 2 * k + rank;
+        if (tile >= n_tiles) continue;  // (only ever the last pair tile)
+        const int b = tbuf(j);
+        mbar_wait(&sfull[b], tpar(j));
+        const int32_t row0 = static_cast<int32_t>(tile * 128);
+        const uint8_t* rb = smem + lay.rbuf_off + b * kTileBytes;
+        tma_store_2d(&grp.pout[0], rb, 0, row0);
+        tma_store_2d(&grp.pout[1], rb + 128 * kRB0, 0, row0);
+        if (grp.out2) {
+          const uint8_t* ob = smem + lay.o2_off;
+          tma_store_2d(&grp.pout2[0], ob, 0, row0);
+          tma_store_2d(&grp.pout2[1], ob + 128 * kRB0, 0, row0);
+        }
+        bulk_commit();
+        bulk_wait_read0();  // the buffers may be rewritten once the stores have read them
+        mbar_arrive(&rempty[b]);
+        if (grp.out2) mbar_arrive(o2free);
+      }
+      bulk_wait0();
+    }
   } else {
     // ------------------------------ epilogue (warps 2..9, both CTAs) ----------
-    // As conv_tc.cu's unstaged epilogue, with two warps per TMEM lane quadrant (48 channels each): the
-    // residual row is fetched before the accumulator wait, the warp's 48 accumulator columns are read
-    // at once and the accumulator released before any arithmetic.
+    // Two warps per TMEM lane quadrant (48 channels each); the warp's 48 accumulator columns are read at
+    // once and the accumulator released before any arithmetic.  Unstaged (conv1: one output, no
+    // residual): 32-byte global stores per row.  Staged (residual and/or second output): the residual
+    // comes from the TMA-loaded tile buffer, y is written back in place and the pre-activated copy into
+    // o2buf (16-byte swizzled shared stores), and the store warp issues the TMA stores.
     asm volatile("bar.sync 1, 256;" ::: "memory");
     const int q = warp & 3;
     const int hh = (warp - 2) >> 2;  // channel half [48 hh, 48 hh + 48)
     const PlaneGeom geo = L.geo;
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
     const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
+    const uint32_t rbuf_a = smem_u32(smem + lay.rbuf_off);
+    const uint32_t o2_a = smem_u32(smem + lay.o2_off);
+    const uint32_t trow = static_cast<uint32_t>(q * 32 + lane);  // this thread's row in the tile
     int j = 0;
     for (int64_t k = local; k < n_ptiles; k += npc, ++j) {
-      const int a = j & 1;
+      const int a = j & 1, b = tbuf(j);
       const int64_t tile = 2 * k + rank;
       const bool live = tile < n_tiles;
-      const int64_t p = tile * 128 + q * 32 + lane;
-      u32x8 rres[3];
-      if (grp.res && live) {
+      const int64_t p = tile * 128 + trow;
+      u32x8 rres[3];  // unstaged: this row's residual, fetched before the accumulator wait
+      if (!staged && grp.res && live) {
         const __nv_bfloat16* rrow = grp.res + p * kC + 48 * hh;
 #pragma unroll
         for (int i = 0; i < 3; ++i) rres[i] = ldg256(rrow + 16 * i);
@@ -290,19 +357,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         else
           mbar_arrive_cluster_relaxed(a ? tempty_leader1 : tempty_leader0);
       }
-      __nv_bfloat16* orow = grp.out && live ? grp.out + p * kC : nullptr;
-      __nv_bfloat16* orow2 = grp.out2 && live ? grp.out2 + p * kC : nullptr;
+      if (!live) continue;  // (only ever the last pair tile)
+      if (staged) {
+        if (grp.res)
+          mbar_wait(&rfull[b], tpar(j));
+        else
+          mbar_wait(&rempty[b], tpar(j) ^ 1u);
+        if (grp.out2) mbar_wait(o2free, (static_cast<uint32_t>(j) & 1u) ^ 1u);
+      }
+      const uint32_t rb = rbuf_a + static_cast<uint32_t>(b) * kTileBytes;
+      __nv_bfloat16* orow = grp.out ? grp.out + p * kC : nullptr;
+      __nv_bfloat16* orow2 = grp.out2 ? grp.out2 + p * kC : nullptr;
 #pragma unroll
       for (int pc = 0; pc < 3; ++pc) {
         const int c0 = 48 * hh + 16 * pc;
+        const uint32_t off0 = tile_off(trow, static_cast<uint32_t>(c0));
+        const uint32_t off1 = tile_off(trow, static_cast<uint32_t>(c0 + 8));
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[16 * pc + i]) + s_bias[c0 + i];
-        if (grp.res) {
-          const u32x8& rv = rres[pc];
+        if (grp.res) {  // staged: the residual rows arrived by TMA in the tile buffer
+          uint4 rv[2];
+          if (staged) {
+            rv[0] = lds128(rb + off0);
+            rv[1] = lds128(rb + off1);
+          } else {
+            rv[0] = make_uint4(rres[pc].v[0], rres[pc].v[1], rres[pc].v[2], rres[pc].v[3]);
+            rv[1] = make_uint4(rres[pc].v[4], rres[pc].v[5], rres[pc].v[6], rres[pc].v[7]);
+          }
+          const __nv_bfloat162* rp = reinterpret_cast<const __nv_bfloat162*>(rv);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.v[i]));
+            const float2 f = __bfloat1622float2(rp[i]);
             v[2 * i] += f.x;
             v[2 * i + 1] += f.y;
           }
@@ -315,26 +401,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         }
-        if (orow) {
-          u32x8 o;
+        u32x8 o;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-            o.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
-          }
+        for (int i = 0; i < 8; ++i) {
+          const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+          o.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+        if (staged) {
+          sts128(rb + off0, make_uint4(o.v[0], o.v[1], o.v[2], o.v[3]));
+          sts128(rb + off1, make_uint4(o.v[4], o.v[5], o.v[6], o.v[7]));
+        } else if (orow) {
           stg256(orow + c0, o);
         }
         if (orow2) {
-          u32x8 o;
+          u32x8 o2;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float x0 = fmaxf(v[2 * i] * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
             const float x1 = fmaxf(v[2 * i + 1] * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
             const __nv_bfloat162 b2 = __floats2bfloat162_rn(valid ? x0 : 0.f, valid ? x1 : 0.f);
-            o.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
+            o2.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
           }
-          stg256(orow2 + c0, o);
+          if (staged) {
+            sts128(o2_a + off0, make_uint4(o2.v[0], o2.v[1], o2.v[2], o2.v[3]));
+            sts128(o2_a + off1, make_uint4(o2.v[4], o2.v[5], o2.v[6], o2.v[7]));
+          } else {
+            stg256(orow2 + c0, o2);
+          }
         }
+      }
+      if (staged) {
+        fence_proxy_async_smem();  // generic stores -> the TMA store's async-proxy reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfull[b]);
       }
     }
   }
@@ -350,19 +449,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }  // namespace
 
 bool conv_pair96_supported(int cin, int cout, int ks, int halo) {
-  return cin == kC && cout == kC && ks == 3 && conv_pair96_stages(((128 + 2 * halo) + 31) / 32 * 32) > 0;
+  return cin == kC && cout == kC && ks == 3 && conv_pair96_stages(((128 + 2 * halo) + 31) / 32 * 32, false) > 0;
 }
 
-int conv_pair96_stages(int win_alloc) {
-  for (int st = 4; st >= 2; --st)
-    if (pair_layout(st, win_alloc).total <= 227u * 1024u) return st;
+int conv_pair96_stages(int win_alloc, bool staged) {
+  for (int st = staged ? 2 : 4; st >= 2; --st)
+    if (pair_layout(st, win_alloc, staged).total <= 227u * 1024u) return st;
   return 0;
 }
 
-size_t conv_pair96_smem_bytes(int stages, int win_alloc) { return pair_layout(stages, win_alloc).total; }
+size_t conv_pair96_smem_bytes(int stages, int win_alloc, bool staged) { return pair_layout(stages, win_alloc, staged).total; }
 
 const char* conv_pair96_launch(const TcLaunch& L, int num_sms, cudaStream_t stream) {
-  const PairLayout lay = pair_layout(L.stages, L.win_alloc);
+  const PairLayout lay = pair_layout(L.stages, L.win_alloc, (L.flags & kPairStaged) != 0);
   ensure_smem_attr(reinterpret_cast<const void*>(conv_pair96_kernel), static_cast<int>(lay.total));
   const int64_t pair_work = static_cast<int64_t>(L.ngroups) * ((L.geo.n_tiles + 1) / 2);
   int pairs = static_cast<int>(pair_work < num_sms / 2 ? pair_work : num_sms / 2);

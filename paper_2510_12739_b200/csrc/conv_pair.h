@@ -6,11 +6,16 @@
 
 namespace cnrx {
 
+// TcLaunch::flags bit: this launch uses the TMA-staged epilogue (residual load + output stores by TMA;
+// set by the host when the staged shared-memory layout fits, i.e. not for dilated windows)
+constexpr int kPairStaged = 4;
+
 // True for a 3x3 96 -> 96 conv whose window (halo rows either side) fits the pair kernel's smem.
 bool conv_pair96_supported(int cin, int cout, int ks, int halo);
-// Window pipeline depth that fits in shared memory for `win_alloc`-row windows (0: none).
-int conv_pair96_stages(int win_alloc);
-size_t conv_pair96_smem_bytes(int stages, int win_alloc);
+// Window pipeline depth that fits in shared memory for `win_alloc`-row windows (0: none); `staged`:
+// a launch with a residual or a second output (TMA-staged epilogue).
+int conv_pair96_stages(int win_alloc, bool staged);
+size_t conv_pair96_smem_bytes(int stages, int win_alloc, bool staged);
 // Grid: CTA pairs (cluster of 2), at most num_sms / 2 pairs.  Returns the kernel name.
 const char* conv_pair96_launch(const TcLaunch& L, int num_sms, cudaStream_t stream);
 

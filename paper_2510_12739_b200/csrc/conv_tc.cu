@@ -568,10 +568,9 @@ void conv_tc_pack_weights(const float* w, int ks, int cin_real, int cout_real, c
 }
 
 void conv_tc_make_maps(const void* plane, int64_t nalloc, int cin, int box_rows, CUtensorMap* maps) {
-  (void)box_rows;
   const int chs[2] = {chunk0_ch(cin), chunk1_ch(cin)};
   for (int c = 0; c < 2; ++c) {
-    if (chs[c] == 0) {
+    if (chs[c] == 0 || !plane) {
       std::memset(&maps[c], 0, sizeof(CUtensorMap));
       continue;
     }
@@ -582,7 +581,7 @@ void conv_tc_make_maps(const void* plane, int64_t nalloc, int cin, int box_rows,
                                              : CU_TENSOR_MAP_SWIZZLE_NONE;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(chs[c]), static_cast<cuuint64_t>(nalloc)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(cin) * 2};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(chs[c]), static_cast<cuuint32_t>(kBoxRows)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(chs[c]), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t es[2] = {1, 1};
     void* base = const_cast<uint8_t*>(static_cast<const uint8_t*>(plane)) + (c == 0 ? 0 : chs[0] * 2);
     CUresult r = encode_fn()(&maps[c], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,

@@ -17,6 +17,9 @@ struct TcGroup {
   CUtensorMap res_map;              // staged epilogue (COUT <= 64): residual plane, 32-row boxes
   CUtensorMap out_map;              // staged epilogue: primary output plane, 32-row boxes
   CUtensorMap out2_map;             // staged epilogue: pre-activated copy
+  // conv_pair.cu staged epilogue (96-ch planes as 64 + 32 channel chunks, 128-row boxes): residual
+  // loads and output / pre-activated-copy stores by TMA
+  CUtensorMap pres[2], pout[2], pout2[2];
   const uint8_t* wimg;              // weights, pre-swizzled smem image: [tap][chunk][COUT rows]
   const float* bias;                // [COUT] (BN folded in)
   const __nv_bfloat16* res;         // residual plane [Nalloc][COUT] or nullptr
@@ -56,7 +59,8 @@ size_t conv_tc_wimg_bytes(int cin, int cout, int ks);
 // by `scale` (nullable, folded BN); written as bf16 into `img` (host buffer of conv_tc_wimg_bytes).
 void conv_tc_pack_weights(const float* w, int ks, int cin_real, int cout_real, const float* scale, int cin,
                           int cout, uint8_t* img);
-// Tensor maps for K-chunks of an input plane [nalloc][cin] bf16 with a window box of `box_rows` rows.
+// Tensor maps for the K-chunks (<= 64 + rest channels) of a plane [nalloc][cin] bf16, boxes of
+// `box_rows` rows; a null plane yields zeroed maps.
 void conv_tc_make_maps(const void* plane, int64_t nalloc, int cin, int box_rows, CUtensorMap* maps);
 // Single-chunk (<= 64 channels) plane map with 32-row boxes for the staged epilogue (residual load,
 // output stores); a null plane yields a zeroed map.
