@@ -197,6 +197,7 @@ struct Workspace {
   };
   std::vector<GroupLaunch> launches;  // prepared tensor maps per TC group (bf16)
   bool blocks_fused = false;          // residual blocks run as conv_blk64 at this batch size
+  bool head_fused = false;            // the head runs in the last convs' epilogue (two-kernel program)
 };
 
 }  // namespace
@@ -234,6 +235,10 @@ struct cnrx_plan {
   int n_levels = 0;
   int npad = 1;
   std::vector<int> stem_ops;   // TcOp indices run by the fused stem kernel
+  // fused interaction + LLR head (conv_ws.cu kWsHead): the tc group (level, index) whose convs produce
+  // every operand of the head's fold, in fold order, and the head's pointwise step it replaces
+  int hf_level = -1, hf_group = -1, hf_pw = -1;
+  WsHead hf{};
   bool need_plane0 = true;     // some kernel reads the input-feature plane
   std::vector<int> buf_channels;  // plane buffers
 
@@ -711,6 +716,69 @@ struct Bf16Compiler {
     }
   }
 
+  // The CoNet interaction + LLR head folded into the epilogue of the subnetworks' last convs
+  // (conv_ws.cu kWsHead) when the head is a fold over 64-channel planes each written by a 64->64
+  // weights-stationary conv (residual epilogue, no other reader), all in one launch group.  The
+  // two-kernel program then skips the head kernel; the fused-block program (small batches) keeps it.
+  // Both compute z the same way and run the same head UMMAs, so their LLRs are identical.
+  // Opt-in while it is slower than conv + head kernel (CNRX_HEADFUSE=1; CNRX_NO_HEADFUSE=1 wins; read per plan).
+  void fuse_head() {
+    if (!getenv("CNRX_HEADFUSE") || getenv("CNRX_NO_HEADFUSE") || getenv("CNRX_NO_TMA_HEAD")) return;
+    const int hk = static_cast<int>(p.pw.size()) - 1;
+    if (hk < 0) return;
+    const PwStep& hs = p.pw[static_cast<size_t>(hk)];
+    int ns = 0, ops[kPwMaxPlanes], affs[kPwMaxPlanes], relus[kPwMaxPlanes];
+    if (hs.out_plane >= 0 || hs.prog.C != 64 || hs.prog.head_bits > 8 || hs.prog.head_bits < 1) return;
+    const int nb = hs.prog.head_bits;
+    if (nb != 2 && nb != 4 && nb != 6 && nb != 8) return;  // head.cu's variants (identical results)
+    if (!pw_as_fold(hs.prog, &ns, ops, affs, relus) || hs.prog.n_planes_used != ns || ns < 1 || ns > 3) return;
+    std::vector<int> readers(p.planes.size(), 0);
+    for (const auto& op : p.tc) {
+      if (op.in_plane >= 0) ++readers[static_cast<size_t>(op.in_plane)];
+      if (op.res_plane >= 0) ++readers[static_cast<size_t>(op.res_plane)];
+    }
+    for (const auto& st : p.pw)
+      for (int k = 0; k < st.n_planes; ++k) ++readers[static_cast<size_t>(st.plane_ids[k])];
+    std::vector<int> prod(static_cast<size_t>(ns));
+    for (int k = 0; k < ns; ++k) {
+      const int pl = hs.plane_ids[k];
+      const int t = plane_producer_tc[static_cast<size_t>(pl)];
+      if (t < 0 || readers[static_cast<size_t>(pl)] != 1) return;
+      const TcOp& op = p.tc[static_cast<size_t>(t)];
+      if (!op.ws || op.stem || op.fused_away || op.out_plane != pl || op.out2_plane >= 0 || op.relu || op.relu_in ||
+          op.res_plane < 0)
+        return;
+      prod[static_cast<size_t>(k)] = t;
+    }
+    const int lv = p.tc[static_cast<size_t>(prod[0])].level;
+    auto& groups = p.tc_groups_by_level[static_cast<size_t>(lv)];
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      auto& grp = groups[gi];
+      if (static_cast<int>(grp.size()) != ns) continue;
+      bool all = true;
+      for (int t : prod)
+        if (std::find(grp.begin(), grp.end(), t) == grp.end()) all = false;
+      if (!all) continue;
+      grp = prod;  // launch member r = fold operand r (cluster rank r)
+      p.hf_level = lv;
+      p.hf_group = static_cast<int>(gi);
+      p.hf_pw = hk;
+      WsHead& h = p.hf;
+      std::memset(&h, 0, sizeof(h));
+      h.ns = ns;
+      h.nb = nb;
+      for (int k = 0; k < ns; ++k) {
+        h.op[k] = ops[k];
+        h.relu[k] = relus[k];
+        h.aff_s[k] = affs[k] >= 0 ? hs.prog.aff_s[affs[k]] : nullptr;
+        h.aff_t[k] = affs[k] >= 0 ? hs.prog.aff_t[affs[k]] : nullptr;
+      }
+      h.w = hs.prog.head_w;
+      h.b = hs.prog.head_b;
+      return;
+    }
+  }
+
   void compile() {
     const int n = static_cast<int>(p.nodes.size());
     node_plane.assign(static_cast<size_t>(n), -1);
@@ -891,6 +959,7 @@ struct Bf16Compiler {
     }
     for (int k = 0; k < static_cast<int>(p.pw.size()); ++k)
       p.pw_by_level[static_cast<size_t>(p.pw[static_cast<size_t>(k)].level)].push_back(k);
+    fuse_head();
     // out2 planes share their producer's level; every plane is live from its level to last use
     for (auto& op : p.tc) {
       if (op.out2_plane >= 0) p.planes[static_cast<size_t>(op.out2_plane)].level = op.level;
@@ -1004,8 +1073,10 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
       if (op.blk_c1 >= 0 && !conv_blk64_supported_halo(ws.geo.T1 * op.dil + 1)) fused = false;
   }
   ws.blocks_fused = fused;
+  ws.head_fused = false;
   for (int lv = 0; lv < p.n_levels; ++lv)
-    for (auto& grp : p.tc_groups_by_level[static_cast<size_t>(lv)]) {
+    for (size_t gidx = 0; gidx < p.tc_groups_by_level[static_cast<size_t>(lv)].size(); ++gidx) {
+      auto& grp = p.tc_groups_by_level[static_cast<size_t>(lv)][gidx];
       Workspace::GroupLaunch GL;
       const TcOp& op0 = p.tc[static_cast<size_t>(grp[0])];
       GL.ws = op0.ws;
@@ -1062,9 +1133,17 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           g.relu_in = op.relu_in;
         }
         L.win_alloc = win_alloc;
+        const bool head = !fused && lv == p.hf_level && static_cast<int>(gidx) == p.hf_group;
         int stages = 4;
-        while (stages > 1 && conv_ws64_smem_bytes(stages, win_alloc) > 227 * 1024) --stages;
+        while (stages > 1 && (head ? conv_ws64_head_smem_bytes(stages, win_alloc) : conv_ws64_smem_bytes(stages, win_alloc)) >
+                                 227 * 1024)
+          --stages;
         L.stages = stages;
+        if (head) {
+          L.head_on = 1;
+          L.head = p.hf;
+          ws.head_fused = true;
+        }
       } else {
         TcLaunch& L = GL.tc;
         std::memset(&L, 0, sizeof(L));
@@ -1277,6 +1356,11 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
         }
         static const int ws_debug = getenv("CNRX_WS_DEBUG") ? atoi(getenv("CNRX_WS_DEBUG")) : 0;
         GL.wsl.debug = ws_debug;
+        if (GL.wsl.head_on) {
+          GL.wsl.head.llr = out;
+          const PwProgram& hp = p.pw[static_cast<size_t>(p.hf_pw)].prog;
+          fl += 2ll * hp.C * hp.head_bits;
+        }
         p.note(conv_ws64_launch(GL.wsl, p.num_sms, s), s, fl);
         if (trace) {
           unsigned long long h[kWsTraceSlots];
@@ -1320,6 +1404,7 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
       }
     }
     for (int k : p.pw_by_level[static_cast<size_t>(lv)]) {
+      if (ws.head_fused && k == p.hf_pw) continue;  // ran in the last convs' epilogue
       PwStep& st = p.pw[static_cast<size_t>(k)];
       PwProgram prog = st.prog;
       for (int j = 0; j < st.n_planes; ++j) prog.planes[j] = plane_ptr(st.plane_ids[j]);

@@ -32,10 +32,14 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "conv_tc.h"
 #include "conv_ws.h"
+#include "kernels.h"
 #include "sm100.cuh"
 
 namespace cnrx {
@@ -52,9 +56,9 @@ constexpr int kAcc0 = 256;        // accumulator columns [256,384) and [384,512)
 constexpr int kBox = 32;
 
 struct WsLayout {
-  uint32_t win_off, win_stage, res_off, stg_off, par_off, bar_off, total;
+  uint32_t win_off, win_stage, res_off, stg_off, par_off, hw_off, fold_off, bar_off, total;
 };
-__host__ __device__ inline WsLayout ws_layout(int stages, int win_alloc) {
+__host__ __device__ inline WsLayout ws_layout(int stages, int win_alloc, bool head = false) {
   WsLayout s{};
   s.win_off = 0;
   s.win_stage = static_cast<uint32_t>(win_alloc * kRB);  // multiple of 4 KB (32-row boxes)
@@ -65,6 +69,13 @@ __host__ __device__ inline WsLayout ws_layout(int stages, int win_alloc) {
   off += 2u * 2u * 128u * kRB;
   s.par_off = off;                       // bias, s2, t2
   off += 3u * kC * 4u;
+  s.hw_off = off;                        // fused head: bf16 head weight image (1024-aligned)
+  s.fold_off = off;                      // fused head: fold scale / shift [3 steps][2][64] fp32
+  if (head) {
+    s.hw_off = (off + 1023u) & ~1023u;
+    s.fold_off = s.hw_off + kHeadTcWBytes;
+    off = s.fold_off + 3u * 2u * kC * 4u;
+  }
   s.bar_off = off;
   s.total = off + 256 + 1024;
   return s;
@@ -82,7 +93,8 @@ __device__ __forceinline__ void epi_group_sync(int e) {
 
 // Epilogue variant flags (compile-time so the unrolled epilogue carries no per-element branches);
 // kWsDynamic reads them from the launch instead.
-enum : int { kWsRes = 1, kWsOut2 = 2, kWsOut2Bn = 4, kWsRelu = 8, kWsReluIn = 16, kWsDynamic = -1 };
+enum : int { kWsRes = 1, kWsOut2 = 2, kWsOut2Bn = 4, kWsRelu = 8, kWsReluIn = 16, kWsHead = 32, kWsDynamic = -1 };
+constexpr uint32_t kHeadCol = 192;  // fused head: TMEM columns [192, 256) = [2 groups][2 tiles][16] (free between weights and accumulators)
 constexpr int kWsThreads = 640;  // 20 warps: producer, MMA (stage 0), 16 epilogue, input-ReLU, MMA (stage 1)
 
 // Poll back-off (ns) of the roles that are not on the tensor core's critical path.  The epilogue groups
@@ -124,9 +136,14 @@ __device__ __forceinline__ void relu_chunks(uint32_t win, int lo, int hi, int la
 template <int FL>
 __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_constant__ WsLaunch L) {
   constexpr uint32_t IDESC = idesc_bf16_f32(128, kN);
+  constexpr bool kHead = FL > 0 && (FL & kWsHead) != 0;
+  constexpr int kNS = kHead ? (FL >> 6) & 3 : 1;  // fused head: subnetworks (fold operands, cluster size)
+  // fused head with the fold shape compiled in (bit 16): bits 8-9 step 1/2 is a product, 10-12 step
+  // 0-2 has a ReLU, 13-15 step 0-2 has a BN; otherwise the fold is read from the launch (branch-free)
+  constexpr bool kFoldSpec = kHead && (FL & (1 << 16)) != 0;
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
-  const WsLayout lay = ws_layout(L.stages, L.win_alloc);
+  const WsLayout lay = ws_layout(L.stages, L.win_alloc, kHead);
   float* s_bias = reinterpret_cast<float*>(smem + lay.par_off);
   float* s_s2 = s_bias + kC;
   float* s_t2 = s_s2 + kC;
@@ -137,7 +154,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
   uint64_t* tempty = tfull + 2;           // [2]
   uint64_t* rfull = tempty + 2;           // [2 groups][2 buffers] residual tile landed
   uint64_t* ready = rfull + 4;            // [stages] window ReLU'd in place (relu_in only)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + L.stages);
+  uint64_t* zfull = ready + L.stages;     // [2] (head, rank 0) the other ranks' tiles of group tile landed
+  uint64_t* zfree = zfull + 2;            // [2 groups][2] (head, ranks >= 1) rank 0 has consumed the group's
+                                          // tile n (barrier n & 1)
+  uint64_t* hfull = zfree + 4;            // [2 groups][2] (head, rank 0) head UMMAs of group tile n (n & 1) done
+  uint64_t* zready = hfull + 4;           // [2] (head, rank 0) z tile of the group's current tile staged
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zready + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -163,8 +185,27 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
       mbar_init(&tempty[a], 8);
       mbar_init(&rfull[2 * a], 1);
       mbar_init(&rfull[2 * a + 1], 1);
+      if (kHead) {
+        mbar_init(&zfull[a], kNS > 1 ? static_cast<uint32_t>(kNS - 1) : 1u);
+        mbar_init(&zfree[2 * a], 1);
+        mbar_init(&zfree[2 * a + 1], 1);
+        mbar_init(&hfull[2 * a], 1);
+        mbar_init(&hfull[2 * a + 1], 1);
+        mbar_init(&zready[a], 8);
+      }
     }
     fence_barrier_init();
+  }
+  if (kHead && g == 0 && warp >= 2) {
+    head_tc_pack_weights(smem + lay.hw_off, L.head.w, L.head.nb, threadIdx.x - 64, kWsThreads - 64);
+    fence_proxy_async_smem();
+    float* s_fold = reinterpret_cast<float*>(smem + lay.fold_off);
+    for (int e = threadIdx.x - 64; e < 3 * kC; e += kWsThreads - 64) {
+      const int k = e / kC, c = e % kC;
+      const bool on = k < L.head.ns && L.head.aff_s[k] != nullptr;
+      s_fold[(2 * k) * kC + c] = on ? L.head.aff_s[k][c] : 1.f;
+      s_fold[(2 * k + 1) * kC + c] = on ? L.head.aff_t[k][c] : 0.f;
+    }
   }
   if (warp >= 2) {
     for (int c = threadIdx.x - 64; c < kC; c += 512) {
@@ -176,6 +217,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  if (kHead) cl_sync();  // every CTA's barriers initialised before any remote arrive / copy
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
@@ -300,6 +342,26 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
       atomicAdd(&L.trace[kWsTraceLoop], static_cast<unsigned long long>(tr_loop));
       atomicAdd(&L.trace[kWsTraceCommit], static_cast<unsigned long long>(tr_commit));
     }
+  } else if (warp == 18 && kHead) {
+    // ------------------------------ fused head: head UMMA issuer (rank 0) -----
+    // A warp of its own: a tcgen05.ld from a warp with UMMAs in flight waits for them, and the head
+    // UMMAs queue behind the conv UMMAs in the tensor pipe.
+    if (g == 0) {
+      const uint32_t hw_a = smem_u32(smem + lay.hw_off);
+      int j = 0;
+      for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
+        const int e = j & 1;
+        const uint32_t gn = static_cast<uint32_t>(j) >> 1;
+        ws_wait_relaxed(&zready[e], gn & 1u);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t hb = 2u * static_cast<uint32_t>(e) + (gn & 1u);
+          head_tc_umma(tbase + kHeadCol + 16u * hb, smem_u32(smem + lay.res_off + (2 * e + (gn & 1u)) * 128 * kRB), hw_a);
+          umma_commit(&hfull[hb]);
+        }
+        __syncwarp();
+      }
+    }
   } else if (warp == 18) {
     // ------------------------------ input ReLU (relu_in) ----------------------
     // The window is the B operand of the tensor core (async proxy): ReLU it in place with generic
@@ -331,6 +393,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
       s2v[blk] = s_s2[ch];
       t2v[blk] = s_t2[ch];
     }
+    // fused head (rank 0): per-channel fold tables of this thread's two channels
+    const float* s_fold = reinterpret_cast<const float*>(smem + lay.fold_off);
+    // fused head: per fold step, ReLU floor (-inf: none) and operation (branch-free in the epilogue)
+    float rfloor[3];
+    bool fmul[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      rfloor[k] = kHead && k < kNS && L.head.relu[k] ? 0.f : -INFINITY;
+      fmul[k] = kHead && k < kNS && L.head.op[k] == PW_MUL;
+    }
     const bool relu2_only = FL < 0 ? grp.s2 == nullptr : (FL & kWsOut2Bn) == 0;
     const bool lead = ((warp - 2) & 7) == 0 && lane == 0;
     // ldmatrix / stmatrix row addresses: thread a -> matrix a/8 (8-row group), row a%8
@@ -347,6 +419,38 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
         tma_load_2d(dst + bx * kBox * kRB, &grp.res_map, &rfull[2 * e + b], 0, static_cast<int32_t>(t * kTileRows + bx * kBox));
     };
     const int64_t gstride = 2 * static_cast<int64_t>(nct);
+    // Fused head (rank 0): z of group tile m replaces m's residual tile in shared memory; warp 18 issues
+    // the head UMMAs over it, and they are read back at the start of the group's next tile (they queue
+    // behind the conv UMMAs in the tensor pipe, so waiting for them at once would stall the epilogue).
+    // Then the residual buffer is refilled for group tile m + 2.
+    auto head_drain = [&](uint32_t m, int64_t mtile) {
+      const uint32_t hb = 2u * static_cast<uint32_t>(e) + (m & 1u);
+      if (H == 0) {
+        ws_wait_relaxed(&hfull[hb], (m >> 1) & 1u);
+        tc_fence_after();
+        uint32_t d[8];
+        tmem_ld8(tbase + kHeadCol + 16u * hb + (static_cast<uint32_t>(q * 32) << 16), d);
+        tmem_ld_wait();
+        tc_fence_before();
+        const int row = q * 32 + lane;
+        const int64_t pr = mtile * kTileRows + row;
+        if (row < kTileRows && geo.valid(pr)) {
+          int b, t, f;
+          geo.coords(pr, b, t, f);
+          const int nb = L.head.nb;
+          float* dst = L.head.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * nb;
+          if (nb == 4) {
+            *reinterpret_cast<float4*>(dst) =
+                make_float4(__uint_as_float(d[0]) + L.head.b[0], __uint_as_float(d[1]) + L.head.b[1],
+                            __uint_as_float(d[2]) + L.head.b[2], __uint_as_float(d[3]) + L.head.b[3]);
+          } else {
+            for (int k = 0; k < nb; ++k) dst[k] = __uint_as_float(d[k]) + L.head.b[k];
+          }
+        }
+      }
+      // z of group tile m sat in its residual buffer: now free for group tile m + 2's residual
+      if (lead && has_res && mtile + 2 * gstride < n_tiles) load_res(mtile + 2 * gstride, static_cast<int>(m & 1u));
+    };
     if (has_res && lead) {
       prefetch_tmap(&grp.res_map);
       const int64_t t0_ = local + static_cast<int64_t>(e) * nct;
@@ -354,113 +458,207 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
       if (t0_ + gstride < n_tiles) load_res(t0_ + gstride, 1);
     }
     int j = e;
-    for (int64_t tile = local + static_cast<int64_t>(e) * nct; tile < n_tiles; tile += 2 * static_cast<int64_t>(nct), j += 2) {
-      const int64_t p0 = tile * kTileRows;
-      const long long te0 = clock64();
-      ws_wait_relaxed(&tfull[e], static_cast<uint32_t>(j >> 1) & 1u);
-      const long long te1 = clock64();
-      tr_ew += te1 - te0;
-      // staging buffer free? (this group's previous TMA store has read it)
-      if (lead) bulk_wait_read0();
-      epi_group_sync(e);
-      const int kb = (j >> 1) & 1;  // residual buffer of this group tile
-      if (has_res) ws_wait_relaxed(&rfull[2 * e + kb], static_cast<uint32_t>(j >> 2) & 1u);
-      const uint32_t rbuf_a = smem_u32(rbuf0 + kb * 128 * kRB);
-      const long long te2 = clock64();
-      tr_sw += te2 - te1;
-      tc_fence_after();
-      // Chunk h = accumulator columns c = 64H + 32h + [0, 32).  Lanes 16k + i / 16k + 8 + i hold the
-      // A / B tap partial sums of channel 8k + i, so output row c = A[c] + B[c+1] needs one shuffle
-      // for odd c (B[c+1] sits with the neighbouring column pair) and none for even c.
-      // validity of this warp's 64 rows (padding rows are stored as zeros): one bit per row
-      uint32_t vmask[2];
-#pragma unroll
-      for (int w = 0; w < 2; ++w) vmask[w] = __ballot_sync(0xffffffffu, geo.valid(p0 + 64 * H + 32 * w + lane));
-      const uint32_t tq = tbase + kAcc0 + static_cast<uint32_t>(e * kN + 64 * H) + (static_cast<uint32_t>(q * 32) << 16);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t a0[16], a1[16], xb;
-        tmem_ld16x256b_x4(tq + 32 * h, a0);
-        tmem_ld16x256b_x4(tq + (16u << 16) + 32 * h, a1);
-        if (H == 0 || h == 0) {
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(xb) : "r"(tq + 32 * h + 32) : "memory");
-        } else {
-          xb = 0;  // column 128 would only feed row 127, which is never stored
-        }
-        tmem_ld_wait();
-        if (h == 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_relaxed(&tempty[e]);
-        }
-#pragma unroll
-        for (int blk = 0; blk < 2; ++blk) {
-          uint32_t (&a)[16] = blk == 0 ? a0 : a1;
-          uint32_t rres[4] = {0u, 0u, 0u, 0u};
-          if (has_res) {
-            // residual rows 64H + 32h + 8i + arow%8 (matrix i), channel chunk 2q + blk
-            const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
-            ldsm_x4_trans(rbuf_a + sw128(row, static_cast<uint32_t>((2 * q + blk) * 16)), rres);
+    // the tile loop, compiled separately for the CTA that folds the head (HF, rank 0) and the others
+    auto epi_loop = [&](auto hf_c) {
+      constexpr bool HF = decltype(hf_c)::value;  // fused head, rank 0: fold + head
+      constexpr bool HS = kHead && !HF;           // fused head, ranks >= 1: send the tile to rank 0
+      for (int64_t tile = local + static_cast<int64_t>(e) * nct; tile < n_tiles; tile += 2 * static_cast<int64_t>(nct), j += 2) {
+        const int64_t p0 = tile * kTileRows;
+        const long long te0 = clock64();
+        ws_wait_relaxed(&tfull[e], static_cast<uint32_t>(j >> 1) & 1u);
+        const long long te1 = clock64();
+        tr_ew += te1 - te0;
+        // staging buffer free? (this group's previous TMA store has read it)
+        // (fused head, ranks >= 1: rank 0 has consumed this group's previous tile, so the copy of it out
+        // of the staging buffer is complete)
+        // Ranks >= 1 alternate between the two halves of the group's staging buffer, so tile n's epilogue
+        // only needs tile n-2's copy to have landed (rank 0 has consumed it), not tile n-1's.
+        const uint32_t gn = static_cast<uint32_t>(j) >> 1;  // this group's tile count
+        if (lead) {
+          if (HS) {
+            if (gn >= 2) cl_wait(&zfree[2 * e + (gn & 1u)], ((gn >> 1) & 1u) ^ 1u);
+          } else {
+            bulk_wait_read0();
           }
-          const float bnd = __uint_as_float(__shfl_sync(0xffffffffu, xb, 16 * blk + 8 + ci));
-          uint32_t o[4], o2[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t snd = t0 == 0 ? (i < 3 ? a[4 * (i + 1) + 2] : 0u) : a[4 * i + 2];
-            float got = __uint_as_float(__shfl_sync(0xffffffffu, snd, t0 == 3 ? lane - 3 : lane + 1));
-            if (i == 3 && t0 == 3) got = bnd;
-            float y0 = __uint_as_float(a[4 * i + 0]) + __uint_as_float(a[4 * i + 3]) + bias[blk];
-            float y1 = __uint_as_float(a[4 * i + 1]) + got + bias[blk];
+        }
+        if (HF && gn >= 1) head_drain(gn - 1, tile - gstride);
+        epi_group_sync(e);
+        const int kb = (j >> 1) & 1;  // residual buffer of this group tile
+        if (has_res) ws_wait_relaxed(&rfull[2 * e + kb], static_cast<uint32_t>(j >> 2) & 1u);
+        if (HF && kNS > 1) cl_wait(&zfull[e], (static_cast<uint32_t>(j) >> 1) & 1u);
+        const uint32_t rbuf_a = smem_u32(rbuf0 + kb * 128 * kRB);
+        const long long te2 = clock64();
+        tr_sw += te2 - te1;
+        tc_fence_after();
+        // Chunk h = accumulator columns c = 64H + 32h + [0, 32).  Lanes 16k + i / 16k + 8 + i hold the
+        // A / B tap partial sums of channel 8k + i, so output row c = A[c] + B[c+1] needs one shuffle
+        // for odd c (B[c+1] sits with the neighbouring column pair) and none for even c.
+        // validity of this warp's 64 rows (padding rows are stored as zeros): one bit per row
+        uint32_t vmask[2];
+  #pragma unroll
+        for (int w = 0; w < 2; ++w) vmask[w] = __ballot_sync(0xffffffffu, geo.valid(p0 + 64 * H + 32 * w + lane));
+        const uint32_t tq = tbase + kAcc0 + static_cast<uint32_t>(e * kN + 64 * H) + (static_cast<uint32_t>(q * 32) << 16);
+  #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t a0[16], a1[16], xb;
+          tmem_ld16x256b_x4(tq + 32 * h, a0);
+          tmem_ld16x256b_x4(tq + (16u << 16) + 32 * h, a1);
+          if (H == 0 || h == 0) {
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(xb) : "r"(tq + 32 * h + 32) : "memory");
+          } else {
+            xb = 0;  // column 128 would only feed row 127, which is never stored
+          }
+          tmem_ld_wait();
+          if (h == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_relaxed(&tempty[e]);
+          }
+  #pragma unroll
+          for (int blk = 0; blk < 2; ++blk) {
+            uint32_t (&a)[16] = blk == 0 ? a0 : a1;
+            uint32_t rres[4] = {0u, 0u, 0u, 0u};
             if (has_res) {
-              const float2 rf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rres[i]));
-              y0 += rf.x;
-              y1 += rf.y;
+              // residual rows 64H + 32h + 8i + arow%8 (matrix i), channel chunk 2q + blk
+              const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
+              ldsm_x4_trans(rbuf_a + sw128(row, static_cast<uint32_t>((2 * q + blk) * 16)), rres);
             }
-            if (relu_main) {
-              y0 = fmaxf(y0, 0.f);
-              y1 = fmaxf(y1, 0.f);
-            }
-            const int rb = 8 * i + 2 * t0;  // row 64H + 32h + rb
-            const bool v0 = (vmask[h] >> rb) & 1u, v1 = (vmask[h] >> (rb + 1)) & 1u;
-            if (!v0) y0 = 0.f;
-            if (!v1) y1 = 0.f;
-            const __nv_bfloat162 ob = __floats2bfloat162_rn(y0, y1);
-            o[i] = *reinterpret_cast<const uint32_t*>(&ob);
-            if (has_out2) {
-              __nv_bfloat162 u;
-              if (relu2_only) {
-                u = __hmax2(ob, __float2bfloat162_rn(0.f));
-              } else {
-                const float2 f = __bfloat1622float2(ob);
-                const float x0 = fmaxf(f.x * s2v[blk] + t2v[blk], 0.f);
-                const float x1 = fmaxf(f.y * s2v[blk] + t2v[blk], 0.f);
-                u = __floats2bfloat162_rn(v0 ? x0 : 0.f, v1 ? x1 : 0.f);
-              }
-              o2[i] = *reinterpret_cast<const uint32_t*>(&u);
+            float fsv[3], ftv[3];  // fused head (rank 0): this blk's channel's fold tables
+          if (HF) {
+            const int ch = 16 * q + 8 * blk + ci;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              fsv[k] = k < kNS ? s_fold[(2 * k) * kC + ch] : 1.f;
+              ftv[k] = k < kNS ? s_fold[(2 * k + 1) * kC + ch] : 0.f;
             }
           }
-          const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
-          const uint32_t off = sw128(row, static_cast<uint32_t>((2 * q + blk) * 16));
-          if (!(L.debug & 1)) {
-            stsm_x4_trans(stg_a + off, o);
-            if (has_out2) stsm_x4_trans(stg_a + 128 * kRB + off, o2);
+          uint32_t zr[2][4];  // fused head (rank 0): the other subnetworks' values of the same elements
+            if (HF) {
+              const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
+  #pragma unroll
+              for (int k = 0; k < 2; ++k)
+                if (k + 1 < kNS) ldsm_x4_trans(stg_a + k * 128 * kRB + sw128(row, static_cast<uint32_t>((2 * q + blk) * 16)), zr[k]);
+            }
+            const float bnd = __uint_as_float(__shfl_sync(0xffffffffu, xb, 16 * blk + 8 + ci));
+            uint32_t o[4], o2[4];
+  #pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t snd = t0 == 0 ? (i < 3 ? a[4 * (i + 1) + 2] : 0u) : a[4 * i + 2];
+              float got = __uint_as_float(__shfl_sync(0xffffffffu, snd, t0 == 3 ? lane - 3 : lane + 1));
+              if (i == 3 && t0 == 3) got = bnd;
+              float y0 = __uint_as_float(a[4 * i + 0]) + __uint_as_float(a[4 * i + 3]) + bias[blk];
+              float y1 = __uint_as_float(a[4 * i + 1]) + got + bias[blk];
+              if (has_res) {
+                const float2 rf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rres[i]));
+                y0 += rf.x;
+                y1 += rf.y;
+              }
+              if (relu_main) {
+                y0 = fmaxf(y0, 0.f);
+                y1 = fmaxf(y1, 0.f);
+              }
+              const int rb = 8 * i + 2 * t0;  // row 64H + 32h + rb
+              const bool v0 = (vmask[h] >> rb) & 1u, v1 = (vmask[h] >> (rb + 1)) & 1u;
+              if (!v0) y0 = 0.f;
+              if (!v1) y1 = 0.f;
+              const __nv_bfloat162 ob = __floats2bfloat162_rn(y0, y1);
+              o[i] = *reinterpret_cast<const uint32_t*>(&ob);
+              if (HF) {
+                // head.cu's fold over this conv's stored value (bf16) and the received tiles: fp32,
+                // the two rows of a channel as one packed pair (FMUL2 / FADD2 / FFMA2, same rounding)
+                float2 z = __bfloat1622float2(ob);
+                auto post = [&](auto kc) {
+                  constexpr int k = decltype(kc)::value;
+                  if (kFoldSpec ? ((FL >> (13 + k)) & 1) != 0 : true)  // BN (generic: s = 1, t = 0 if none)
+                    z = __ffma2_rn(z, make_float2(fsv[k], fsv[k]), make_float2(ftv[k], ftv[k]));
+                  if (kFoldSpec ? ((FL >> (10 + k)) & 1) != 0 : true) {  // ReLU (generic: floor -inf if none)
+                    const float fl = kFoldSpec ? 0.f : rfloor[k];
+                    z.x = fmaxf(z.x, fl);
+                    z.y = fmaxf(z.y, fl);
+                  }
+                };
+                auto combine = [&](auto kc, uint32_t zw) {
+                  constexpr int k = decltype(kc)::value;
+                  const float2 zk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zw));
+                  if (kFoldSpec) {
+                    z = ((FL >> (7 + k)) & 1) ? __fmul2_rn(z, zk) : __fadd2_rn(z, zk);
+                  } else {
+                    const float2 m = __fmul2_rn(z, zk), a = __fadd2_rn(z, zk);
+                    z = fmul[k] ? m : a;
+                  }
+                  post(kc);
+                };
+                post(std::integral_constant<int, 0>{});
+                if constexpr (kNS > 1) combine(std::integral_constant<int, 1>{}, zr[0][i]);
+                if constexpr (kNS > 2) combine(std::integral_constant<int, 2>{}, zr[1][i]);
+                const float z0 = z.x, z1 = z.y;
+                const __nv_bfloat162 zb = __floats2bfloat162_rn(z0, z1);
+                o[i] = *reinterpret_cast<const uint32_t*>(&zb);
+              }
+              if (has_out2) {
+                __nv_bfloat162 u;
+                if (relu2_only) {
+                  u = __hmax2(ob, __float2bfloat162_rn(0.f));
+                } else {
+                  const float2 f = __bfloat1622float2(ob);
+                  const float x0 = fmaxf(f.x * s2v[blk] + t2v[blk], 0.f);
+                  const float x1 = fmaxf(f.y * s2v[blk] + t2v[blk], 0.f);
+                  u = __floats2bfloat162_rn(v0 ? x0 : 0.f, v1 ? x1 : 0.f);
+                }
+                o2[i] = *reinterpret_cast<const uint32_t*>(&u);
+              }
+            }
+            const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
+            const uint32_t off = sw128(row, static_cast<uint32_t>((2 * q + blk) * 16));
+            if (!(L.debug & 1)) {
+              // (fused head, ranks >= 1: staging half gn & 1)
+              // (fused head, rank 0: z overwrites the residual tile, same positions it was read from)
+              stsm_x4_trans((HF ? rbuf_a : stg_a + (HS ? (gn & 1u) * 128u * kRB : 0u)) + off, o);
+              if (has_out2) stsm_x4_trans(stg_a + 128 * kRB + off, o2);
+            }
           }
         }
+        const long long te3 = clock64();
+        tr_comb += te3 - te2;
+        fence_proxy_async_smem();
+        if (HF) {  // z tile staged: warp 18 issues the head UMMAs (read back at the group's next tile)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&zready[e]);
+        }
+        epi_group_sync(e);
+        if (kHead) {
+          if (g > 0 && lead) {
+            // this subnetwork's tile -> rank 0's receive buffer (distributed shared memory)
+            // (rank 0's receive buffer is free once it has consumed this group's previous tile)
+            if (gn >= 1) cl_wait(&zfree[2 * e + ((gn - 1) & 1u)], ((gn - 1) >> 1) & 1u);
+            {
+            const uint32_t zb = cl_map(&zfull[e], 0);
+            cl_arrive_expect_tx(zb, 128u * kRB);
+            const uint8_t* src = stg + (gn & 1u) * 128u * kRB;
+            bulk_copy_to_cta(cl_map(stg + (g - 1) * 128 * kRB, 0), src, 128u * kRB, zb);
+            }
+          }
+          // rank 0: the receive buffers are consumed; its residual buffer holds z until the head UMMAs
+          // have read it (reloaded in head_drain)
+          if (HF && lead)
+            for (int r = 1; r < kNS; ++r) cl_arrive(cl_map(&zfree[2 * e + (gn & 1u)], static_cast<uint32_t>(r)));
+          if (!HF && lead && has_res && tile + 2 * gstride < n_tiles) load_res(tile + 2 * gstride, kb);
+        } else if (lead && !(L.debug & 1)) {
+          tma_store_2d(&grp.out_map, stg, 0, static_cast<int32_t>(p0));
+          if (has_out2) tma_store_2d(&grp.out2_map, stg + 128 * kRB, 0, static_cast<int32_t>(p0));
+          bulk_commit();
+          if (has_res && tile + 2 * gstride < n_tiles) load_res(tile + 2 * gstride, kb);
+        }
+        tr_wr += clock64() - te3;
       }
-      const long long te3 = clock64();
-      tr_comb += te3 - te2;
-      fence_proxy_async_smem();
-      epi_group_sync(e);
-      if (lead && !(L.debug & 1)) {
-        tma_store_2d(&grp.out_map, stg, 0, static_cast<int32_t>(p0));
-        if (has_out2) tma_store_2d(&grp.out2_map, stg + 128 * kRB, 0, static_cast<int32_t>(p0));
-        bulk_commit();
-        if (has_res && tile + 2 * gstride < n_tiles) load_res(tile + 2 * gstride, kb);
-      }
-      tr_wr += clock64() - te3;
-    }
+        if (HF && j > e) head_drain((static_cast<uint32_t>(j) >> 1) - 1, local + static_cast<int64_t>(e) * nct + (static_cast<int64_t>(j >> 1) - 1) * gstride);
+    };
+    if (kHead && g == 0)
+      epi_loop(std::integral_constant<bool, kHead>{});
+    else
+      epi_loop(std::false_type{});
     if (lead) bulk_wait0();
-    if (L.trace && lead && e == 0) {
+    if (L.trace && lead && e == 0 && (!kHead || g == ((L.debug & 16) ? 1 : 0))) {  // (fused head: rank 0, or rank 1 with debug bit 4)
       atomicAdd(&L.trace[kTraceEpiWaitFull], static_cast<unsigned long long>(tr_ew));
       atomicAdd(&L.trace[kWsTraceCombine], static_cast<unsigned long long>(tr_comb));
       atomicAdd(&L.trace[kWsTraceStageWait], static_cast<unsigned long long>(tr_sw));
@@ -470,6 +668,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
 
   tc_fence_before();
   __syncthreads();
+  if (kHead) cl_sync();  // no CTA leaves while a peer may still signal its barriers or copy into it
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
@@ -569,9 +768,66 @@ void launch_fl(const WsLaunch& L, const WsLayout& lay, int grid, cudaStream_t st
   }
 }
 
+// Fused-head launches: clusters of ngroups CTAs (one per subnetwork), as many as can be co-resident.
+template <int FL>
+void launch_head(const WsLaunch& L, const WsLayout& lay, cudaStream_t stream) {
+  auto kern = conv_ws64_kernel<FL>;
+  ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(lay.total));
+  static const bool no_pdl = std::getenv("CNRX_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kWsThreads);
+  cfg.dynamicSmemBytes = lay.total;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(L.ngroups);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // co-resident clusters, per (device, cluster size)
+  static int cache[64][5] = {};
+  int dev = 0;
+  CNRX_CUDA(cudaGetDevice(&dev));
+  int& ncl = cache[dev & 63][L.ngroups];
+  if (ncl == 0) {
+    cfg.gridDim = dim3(static_cast<unsigned>(L.ngroups * 148));
+    CNRX_CUDA(cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg));
+    if (ncl <= 0) throw Error(4, "fused-head conv: no cluster of " + std::to_string(L.ngroups) + " CTAs fits an SM set");
+    if (std::getenv("CNRX_TRACE")) fprintf(stderr, "[trace] fused-head conv: %d co-resident clusters of %d\n", ncl, L.ngroups);
+  }
+  const int64_t nc = L.n_tiles < ncl ? L.n_tiles : ncl;
+  cfg.gridDim = dim3(static_cast<unsigned>(nc * L.ngroups));
+  cfg.numAttrs = 2;
+  CNRX_CUDA(cudaLaunchKernelEx(&cfg, kern, L));
+}
+
 }  // namespace
 
+size_t conv_ws64_head_smem_bytes(int stages, int win_alloc) { return ws_layout(stages, win_alloc, true).total; }
+
 const char* conv_ws64_launch(const WsLaunch& L, int num_sms, cudaStream_t stream) {
+  if (L.head_on) {
+    const WsLayout lay = ws_layout(L.stages, L.win_alloc, true);
+    for (int i = 0; i < L.ngroups; ++i)
+      if (group_flags(L.g[i]) != kWsRes) throw Error(4, "internal: fused-head conv needs residual-only epilogues");
+    if (L.ngroups != L.head.ns || L.head.ns > 3 || L.head.nb > 8) throw Error(4, "internal: fused-head shape");
+    const WsHead& h = L.head;
+    const bool cfg2_fold = h.ns == 3 && h.op[1] == PW_MUL && h.op[2] == PW_MUL && !h.aff_s[0] && h.aff_s[1] &&
+                           h.aff_s[2] && !h.relu[0] && !h.relu[1] && !h.relu[2];
+    if (cfg2_fold) {  // build_conet's mul -> BN -> mul -> BN tail (CoNet-ResNet)
+      launch_head<kWsRes | kWsHead | (3 << 6) | (3 << 8) | (6 << 13) | (1 << 16)>(L, lay, stream);
+      return "conv_ws64_kernel<head>";
+    }
+    switch (L.head.ns) {
+      case 1: launch_head<kWsRes | kWsHead | (1 << 6)>(L, lay, stream); break;
+      case 2: launch_head<kWsRes | kWsHead | (2 << 6)>(L, lay, stream); break;
+      default: launch_head<kWsRes | kWsHead | (3 << 6)>(L, lay, stream); break;
+    }
+    return "conv_ws64_kernel<head>";
+  }
   const WsLayout lay = ws_layout(L.stages, L.win_alloc);
   const int64_t work = static_cast<int64_t>(L.ngroups) * L.n_tiles;
   int grid = static_cast<int>(work < num_sms ? work : num_sms);

@@ -19,8 +19,26 @@ struct WsGroup {
   int32_t relu_in;       // apply ReLU to the input window in shared memory (consumer-side pre-activation)
 };
 
+// Fused CoNet interaction + LLR head (kWsHead launches: the last conv of every subnetwork in one
+// launch, clusters of ngroups CTAs, CTA rank r computing fold operand r of the same tile).  Ranks >= 1
+// copy their output tile into rank 0's shared memory (distributed shared memory); rank 0 folds
+//   z = [aff_0][relu_0](y_0) (op_1) y_1 [aff_1][relu_1] ...
+// (head.cu's fold, fp32), rounds z to bf16 and runs the 1x1 head on the tensor core.
+struct WsHead {
+  const float* aff_s[3];  // per fold step: eval BN scale / shift, or null
+  const float* aff_t[3];
+  int32_t op[3];          // PW_MUL / PW_ADD for steps >= 1
+  int32_t relu[3];
+  const float* w;         // [64][nb] head weights (reference 1x1 layout)
+  const float* b;         // [nb]
+  float* llr;             // [B,T,F,nb], set per call
+  int32_t ns, nb;
+};
+
 struct WsLaunch {
   WsGroup g[4];
+  WsHead head;
+  int32_t head_on;
   PlaneGeom geo;
   int64_t n_tiles;   // 127-row output tiles
   int32_t ngroups, stages, win_alloc;
@@ -37,6 +55,7 @@ void conv_ws64_pack_weights(const float* w, const float* scale, uint32_t* img);
 void conv_ws64_make_maps(const void* in, const void* res, const void* out, const void* out2, int64_t nalloc,
                          WsGroup* g);
 size_t conv_ws64_smem_bytes(int stages, int win_alloc);
+size_t conv_ws64_head_smem_bytes(int stages, int win_alloc);
 int conv_ws64_win_alloc(int halo);
 int64_t conv_ws64_tiles(int64_t nalloc);
 const char* conv_ws64_launch(const WsLaunch& L, int num_sms, cudaStream_t stream);

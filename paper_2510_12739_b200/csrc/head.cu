@@ -28,7 +28,7 @@ constexpr int kConsumers = 256;          // two threads per row, C/2 channels ea
 constexpr int kThreads = kConsumers + 32;
 
 struct HeadLayout {
-  uint32_t ring_off, stage_bytes, aff_off, w_off, b_off, part_off, bar_off, total;
+  uint32_t ring_off, stage_bytes, aff_off, w_off, b_off, part_off, hw_off, bar_off, total;
 };
 __host__ __device__ inline HeadLayout head_layout(int c, int ns, int nb, int stages) {
   HeadLayout l{};
@@ -43,10 +43,15 @@ __host__ __device__ inline HeadLayout head_layout(int c, int ns, int nb, int sta
   off += static_cast<uint32_t>(kHC * nb) * 4u;
   l.b_off = off;
   off += 64u;
-  l.part_off = off;  // [2][128 rows][nb] partial GEMV sums of the upper channel half
-  off += 2u * kHRows * static_cast<uint32_t>(nb) * 4u;
+  l.part_off = off;  // [2][128 rows][nb] partial GEMV sums of the upper channel half (CUDA-core GEMV)
+  if (c != 64) off += 2u * kHRows * static_cast<uint32_t>(nb) * 4u;
+  l.hw_off = off;
+  if (c == 64) {  // tensor-core GEMV: head weight image (1024-aligned); z overwrites the stage's plane 0
+    l.hw_off = (off + 1023u) & ~1023u;
+    off = l.hw_off + kHeadTcWBytes;
+  }
   l.bar_off = (off + 15u) & ~15u;
-  l.total = l.bar_off + 2u * 8u * static_cast<uint32_t>(stages) + 1024u;
+  l.total = l.bar_off + 2u * 8u * static_cast<uint32_t>(stages) + 16u + 1024u;
   return l;
 }
 
@@ -71,6 +76,11 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
   float* s_b = reinterpret_cast<float*>(smem + lay.b_off);      // [NB]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + lay.bar_off);
   uint64_t* empty = full + L.stages;
+  uint64_t* hdone = empty + L.stages;  // (kTC) head UMMAs of the tile complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hdone + 1);
+  // 64-channel planes: the head GEMV runs on the tensor core over the bf16-rounded z tile (the same
+  // UMMAs as conv_ws.cu's fused-head epilogue, so both programs give identical LLRs)
+  constexpr bool kTC = C == 64;
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -78,7 +88,13 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers / 32);
     }
+    mbar_init(hdone, 1);
     fence_barrier_init();
+  }
+  if constexpr (kTC) {
+    if (tid < 32) tmem_alloc(tmem_slot, 32);
+    head_tc_pack_weights(smem + lay.hw_off, L.head_w, NB, tid, kThreads);
+    fence_proxy_async_smem();
   }
   for (int e = tid; e < NS * kHC; e += kThreads) {
     const int i = e / kHC, c = e % kHC;
@@ -87,7 +103,10 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
   }
   for (int e = tid; e < kHC * NB; e += kThreads) s_w[e] = L.head_w[e];
   if (tid < NB) s_b[tid] = L.head_b[tid];
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = kTC ? *tmem_slot : 0u;
   pdl_trigger();
   pdl_wait();  // PDL: the prologue above overlapped the previous kernel's tail
 
@@ -149,10 +168,10 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
         for (int c = 0; c < CPT; c += 4) {
           const float4 sv = *reinterpret_cast<const float4*>(ps + c);
           const float4 tv = *reinterpret_cast<const float4*>(pt + c);
-          acc[c] = acc[c] * sv.x + tv.x;
-          acc[c + 1] = acc[c + 1] * sv.y + tv.y;
-          acc[c + 2] = acc[c + 2] * sv.z + tv.z;
-          acc[c + 3] = acc[c + 3] * sv.w + tv.w;
+          acc[c] = __fmaf_rn(acc[c], sv.x, tv.x);
+          acc[c + 1] = __fmaf_rn(acc[c + 1], sv.y, tv.y);
+          acc[c + 2] = __fmaf_rn(acc[c + 2], sv.z, tv.z);
+          acc[c + 3] = __fmaf_rn(acc[c + 3], sv.w, tv.w);
         }
       }
       if (L.relu[i]) {
@@ -161,6 +180,54 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
       }
     }
     __syncwarp();
+    if constexpr (kTC) {
+      // z (bf16) overwrites this thread's own chunks of the stage's plane-0 tile (same swizzled layout),
+      // one thread issues the head UMMAs, warps 0-3 read TMEM lane quadrants 0-3; the stage is released
+      // once the UMMAs have read it
+      const uint32_t za = smem_u32(st);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[8 * k + 2 * e], acc[8 * k + 2 * e + 1]);
+          pk[e] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+        sts128(za + hoff<64>(static_cast<uint32_t>(r), static_cast<uint32_t>(4 * hf + k)), make_uint4(pk[0], pk[1], pk[2], pk[3]));
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+      tc_fence_after();
+      if (tid == 0) {
+        head_tc_umma(tbase, za, smem_u32(smem + lay.hw_off));
+        umma_commit(hdone);
+      }
+      mbar_wait(hdone, static_cast<uint32_t>(j) & 1u);
+      tc_fence_after();
+      if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+      const int w = tid >> 5;
+      if (w < 4) {
+        uint32_t d[8];
+        tmem_ld8(tbase + (static_cast<uint32_t>(w * 32) << 16), d);
+        tmem_ld_wait();
+        const int64_t row = tile * kHRows + w * 32 + (tid & 31);
+        if (geo.valid(row)) {
+          int b, t, f;
+          geo.coords(row, b, t, f);
+          float* dst = L.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * NB;
+          if constexpr (NB == 4) {
+            *reinterpret_cast<float4*>(dst) = make_float4(__uint_as_float(d[0]) + s_b[0], __uint_as_float(d[1]) + s_b[1],
+                                                          __uint_as_float(d[2]) + s_b[2], __uint_as_float(d[3]) + s_b[3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) dst[q] = __uint_as_float(d[q]) + s_b[q];
+          }
+        }
+      }
+      tc_fence_before();
+      continue;
+    }
     if ((tid & 31) == 0) mbar_arrive(&empty[s]);
     float part[NB];
 #pragma unroll
@@ -195,6 +262,11 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
         for (int q = 0; q < NB; ++q) dst[q] = part[q] + s_b[q];
       }
     }
+  }
+  if constexpr (kTC) {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+    tc_fence_after();
+    if (tid < 32) tmem_dealloc(tbase, 32);
   }
 }
 

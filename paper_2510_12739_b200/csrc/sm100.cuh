@@ -312,6 +312,88 @@ __device__ __forceinline__ void stsm_x4_trans(uint32_t saddr, const uint32_t (&r
                : "memory");
 }
 
+// TMEM -> registers: 32 lanes x 32 bit, 8 consecutive columns.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------------------------
+// 1x1 LLR head on the tensor core (head.cu for 64-channel planes, conv_ws.cu's fused-head epilogue):
+// the folded interaction z of a 128-row tile, rounded to bf16 and stored K-major with the 128-byte
+// swizzle ([128 rows][64 ch], exactly the layout of a staged output tile), times the head weights
+// [16 outputs (nb real, rest zero)][64 ch] bf16 (same layout) -> D [128 lanes = rows][16 fp32 columns].
+// Both kernels issue the same four K=16 UMMAs per row, so a row's LLRs do not depend on which
+// kernel (or which TMEM lane) computed them.
+// ---------------------------------------------------------------------------------------------
+constexpr int kHeadTcN = 16;
+constexpr uint32_t kHeadTcWBytes = kHeadTcN * 128;
+__device__ __forceinline__ void head_tc_pack_weights(uint8_t* hw, const float* w, int nb, int tid, int nthreads) {
+  for (int e = tid; e < kHeadTcN * 64; e += nthreads) {
+    const int n = e >> 6, c = e & 63;
+    const float v = n < nb ? w[c * nb + n] : 0.f;
+    *reinterpret_cast<__nv_bfloat16*>(hw + n * 128 + ((((c >> 3) ^ (n & 7))) << 4) + (c & 7) * 2) =
+        __float2bfloat16(v);
+  }
+}
+__device__ __forceinline__ void head_tc_umma(uint32_t d_tmem, uint32_t z_addr, uint32_t hw_addr) {
+  constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((kHeadTcN >> 3) << 17) | ((128u >> 4) << 24);
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+    umma_bf16(d_tmem, make_sdesc(z_addr + kk * 32, 1024, kSwizzle128, 0), make_sdesc(hw_addr + kk * 32, 1024, kSwizzle128, 0),
+              idesc, kk > 0 ? 1u : 0u);
+}
+
+// ---------------------------------------------------------------------------------------------
+// clusters
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared-memory object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t cl_map(const void* p, uint32_t rank) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(smem_u32(p)), "r"(rank));
+  return d;
+}
+// Remote arrivals are relaxed: a release.cluster arrive first waits until every global store the warp
+// issued before it is visible cluster-wide (e.g. the fused head's LLR stores), while the only thing
+// these signals order is shared-memory reuse whose reads / async copies have already completed.
+__device__ __forceinline__ void cl_arrive(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void cl_arrive_expect_tx(uint32_t cluster_bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_bar), "r"(bytes)
+               : "memory");
+}
+// wait for a phase of a local barrier that remote CTAs arrive on (acquire at cluster scope)
+__device__ __forceinline__ void cl_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+}
+// bulk copy of this CTA's shared memory into another CTA's (cluster addresses from cl_map); completion
+// (bytes) is signalled on the destination CTA's barrier
+__device__ __forceinline__ void bulk_copy_to_cta(uint32_t dst_cluster, const void* src, uint32_t bytes,
+                                                 uint32_t bar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_cluster),
+               "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
+               : "memory");
+}
+
 // 1024-byte aligned base inside the dynamic shared-memory array.  Offsetting the __shared__ array itself
 // (instead of round-tripping through an integer) keeps the pointer in the shared state space, so
 // plain loads / stores through it compile to LDS / STS rather than generic LD / ST.

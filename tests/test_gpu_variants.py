@@ -3,7 +3,10 @@ when a plan is built):
   * the CTA-pair 96 -> 96 3x3 conv (csrc/conv_pair.cu, default) vs the single-CTA kernel
     (CNRX_NO_PAIR=1): same UMMA K order per output element, same epilogue -> identical LLRs;
   * the opt-in fused residual-block kernel (csrc/conv_blk.cu, CNRX_BLK=1) vs the default two-kernel
-    path: conv1's output is rounded to bf16 at the same point in both -> identical LLRs."""
+    path: conv1's output is rounded to bf16 at the same point in both -> identical LLRs;
+  * the CoNet interaction + LLR head fused into the last convs' epilogue (conv_ws.cu kWsHead: clusters
+    of one CTA per subnetwork exchanging tiles through distributed shared memory) vs the separate head
+    kernel (CNRX_NO_HEADFUSE=1): same fold arithmetic, same bf16 z, same head UMMAs -> identical LLRs."""
 import json
 import os
 import subprocess
@@ -81,3 +84,23 @@ def test_cta_pair_conv_is_bit_exact_with_single_cta(which, tmp_path):
     assert not any("conv_pair96" in n for n in ls), ls
     assert np.isfinite(yp).all()
     assert np.array_equal(yp, ys), (np.abs(yp - ys).max(), int((yp != ys).sum()))
+
+
+@pytest.mark.parametrize("which", ["cfg2", "dilated"])
+def test_fused_head_is_bit_exact_with_head_kernel(which, tmp_path):
+    # two-kernel program in both arms (CNRX_BLK=0 is set by _run's "fused=False"), head fused or not
+    out = {}
+    for nohf in (False, True):
+        o = str(tmp_path / f"{which}_hf{int(nohf)}.npy")
+        env = {**os.environ, "CNRX_BLK": "0", "CNRX_HEADFUSE": "1"}
+        if nohf:
+            env["CNRX_NO_HEADFUSE"] = "1"
+        r = subprocess.run([sys.executable, "-c", ARM, ROOT, which, o], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        out[nohf] = (np.load(o), json.loads(r.stdout.strip().splitlines()[-1])["launches"])
+    (yh, lh), (yk, lk) = out[False], out[True]
+    assert any("<head>" in n for n in lh) and not any("head_tma" in n for n in lh), lh
+    assert not any("<head>" in n for n in lk) and any("head_tma" in n for n in lk), lk
+    assert np.isfinite(yh).all()
+    assert np.array_equal(yh, yk), (np.abs(yh - yk).max(), int((yh != yk).sum()))
