@@ -28,6 +28,16 @@
 // With a residual the epilogue transposes the combined fp32 values (8x8 lane butterflies) so each
 // lane holds 8 channels of one row, adds the TMA-staged residual row chunk with one 16-byte shared
 // load, then rounds to bf16 (fp32 conv + bias + residual, a single rounding as the reference).
+//
+// Fused interaction + LLR head (kWsHead, opt-in CNRX_HEADFUSE=1): the subnetworks' last convs run as
+// clusters of kNS CTAs (rank r = fold operand r) over the same tiles.  Each rank stages its bf16 output
+// tile, copies the rows that rank d folds into d's receive slots (cp.async.bulk shared::cta ->
+// shared::cluster), then folds its own third of the rows over all kNS tiles (head.cu's fp32 fold ->
+// bf16 z), warp 18 runs the head as four UMMAs over the z rows (sm100.cuh head_tc_umma, the same
+// instructions as head.cu, so the LLRs are bit-identical), and the LLRs are read from TMEM at the
+// group's next tile.  The subnetworks' last activations never reach HBM.  Measured slower than conv +
+// head kernel (cfg2: 1.02 ms vs 0.84 ms): the c2 epilogue has ~25 % slack per tile, and the exchange
+// plus the fold pass and the LLR drain exceed it.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -154,11 +164,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
   uint64_t* tempty = tfull + 2;           // [2]
   uint64_t* rfull = tempty + 2;           // [2 groups][2 buffers] residual tile landed
   uint64_t* ready = rfull + 4;            // [stages] window ReLU'd in place (relu_in only)
-  uint64_t* zfull = ready + L.stages;     // [2] (head, rank 0) the other ranks' tiles of group tile landed
-  uint64_t* zfree = zfull + 2;            // [2 groups][2] (head, ranks >= 1) rank 0 has consumed the group's
-                                          // tile n (barrier n & 1)
-  uint64_t* hfull = zfree + 4;            // [2 groups][2] (head, rank 0) head UMMAs of group tile n (n & 1) done
-  uint64_t* zready = hfull + 4;           // [2] (head, rank 0) z tile of the group's current tile staged
+  uint64_t* land = ready + L.stages;      // [2] (head) the other ranks' rows of the group's tile landed
+  uint64_t* cons = land + 2;              // [2] (head) the other ranks have folded the group's tile
+  uint64_t* hfull = cons + 2;             // [2 groups][2] (head) head UMMAs of group tile n (n & 1) done
+  uint64_t* zready = hfull + 4;           // [2] (head) z rows of the group's current tile staged
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zready + 2);
 
   const int warp = threadIdx.x / 32;
@@ -186,9 +195,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
       mbar_init(&rfull[2 * a], 1);
       mbar_init(&rfull[2 * a + 1], 1);
       if (kHead) {
-        mbar_init(&zfull[a], kNS > 1 ? static_cast<uint32_t>(kNS - 1) : 1u);
-        mbar_init(&zfree[2 * a], 1);
-        mbar_init(&zfree[2 * a + 1], 1);
+        mbar_init(&land[a], kNS > 1 ? static_cast<uint32_t>(kNS - 1) : 1u);
+        mbar_init(&cons[a], kNS > 1 ? static_cast<uint32_t>(kNS - 1) : 1u);
         mbar_init(&hfull[2 * a], 1);
         mbar_init(&hfull[2 * a + 1], 1);
         mbar_init(&zready[a], 8);
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
     }
     fence_barrier_init();
   }
-  if (kHead && g == 0 && warp >= 2) {
+  if (kHead && warp >= 2) {
     head_tc_pack_weights(smem + lay.hw_off, L.head.w, L.head.nb, threadIdx.x - 64, kWsThreads - 64);
     fence_proxy_async_smem();
     float* s_fold = reinterpret_cast<float*>(smem + lay.fold_off);
@@ -343,10 +351,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
       atomicAdd(&L.trace[kWsTraceCommit], static_cast<unsigned long long>(tr_commit));
     }
   } else if (warp == 18 && kHead) {
-    // ------------------------------ fused head: head UMMA issuer (rank 0) -----
+    // ------------------------------ fused head: head UMMA issuer ---------------
     // A warp of its own: a tcgen05.ld from a warp with UMMAs in flight waits for them, and the head
     // UMMAs queue behind the conv UMMAs in the tensor pipe.
-    if (g == 0) {
+    {
       const uint32_t hw_a = smem_u32(smem + lay.hw_off);
       int j = 0;
       for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
@@ -356,7 +364,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
         tc_fence_after();
         if (elect_one()) {
           const uint32_t hb = 2u * static_cast<uint32_t>(e) + (gn & 1u);
-          head_tc_umma(tbase + kHeadCol + 16u * hb, smem_u32(smem + lay.res_off + (2 * e + (gn & 1u)) * 128 * kRB), hw_a);
+          if (!(L.debug & 32)) head_tc_umma(tbase + kHeadCol + 16u * hb, smem_u32(smem + lay.stg_off + e * 2 * 128 * kRB), hw_a);
           umma_commit(&hfull[hb]);
         }
         __syncwarp();
@@ -393,16 +401,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
       s2v[blk] = s_s2[ch];
       t2v[blk] = s_t2[ch];
     }
-    // fused head (rank 0): per-channel fold tables of this thread's two channels
+    // Fused head (kHead): every rank stages its output tile (as for a TMA store), copies the rows
+    // [hr0(d), hr1(d)) of it into rank d's receive slots (distributed shared memory), and folds its OWN
+    // row range of all kNS tiles: fold pass -> z (bf16, in place of its own rows) -> head UMMAs (warp
+    // 18) -> LLRs, read back at the group's next tile.  Symmetric, so every rank does a third of the fold.
     const float* s_fold = reinterpret_cast<const float*>(smem + lay.fold_off);
-    // fused head: per fold step, ReLU floor (-inf: none) and operation (branch-free in the epilogue)
-    float rfloor[3];
-    bool fmul[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      rfloor[k] = kHead && k < kNS && L.head.relu[k] ? 0.f : -INFINITY;
-      fmul[k] = kHead && k < kNS && L.head.op[k] == PW_MUL;
-    }
+    constexpr int kHRows = kNS == 3 ? 48 : kNS == 2 ? 64 : 128;  // fold rows per rank (multiple of 8)
+    const int hr0 = g * kHRows, hr1 = hr0 + kHRows < 128 ? hr0 + kHRows : 128;
+    const int gtid = ((warp - 2) & 7) * 32 + lane;  // thread in the epilogue group
     const bool relu2_only = FL < 0 ? grp.s2 == nullptr : (FL & kWsOut2Bn) == 0;
     const bool lead = ((warp - 2) & 7) == 0 && lane == 0;
     // ldmatrix / stmatrix row addresses: thread a -> matrix a/8 (8-row group), row a%8
@@ -419,10 +425,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
         tma_load_2d(dst + bx * kBox * kRB, &grp.res_map, &rfull[2 * e + b], 0, static_cast<int32_t>(t * kTileRows + bx * kBox));
     };
     const int64_t gstride = 2 * static_cast<int64_t>(nct);
-    // Fused head (rank 0): z of group tile m replaces m's residual tile in shared memory; warp 18 issues
-    // the head UMMAs over it, and they are read back at the start of the group's next tile (they queue
-    // behind the conv UMMAs in the tensor pipe, so waiting for them at once would stall the epilogue).
-    // Then the residual buffer is refilled for group tile m + 2.
+    // head results of group tile m (TMEM lane = tile row) -> LLRs of this rank's rows
     auto head_drain = [&](uint32_t m, int64_t mtile) {
       const uint32_t hb = 2u * static_cast<uint32_t>(e) + (m & 1u);
       if (H == 0) {
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
         tc_fence_before();
         const int row = q * 32 + lane;
         const int64_t pr = mtile * kTileRows + row;
-        if (row < kTileRows && geo.valid(pr)) {
+        if (row >= hr0 && row < hr1 && row < kTileRows && geo.valid(pr)) {
           int b, t, f;
           geo.coords(pr, b, t, f);
           const int nb = L.head.nb;
@@ -448,8 +451,57 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
           }
         }
       }
-      // z of group tile m sat in its residual buffer: now free for group tile m + 2's residual
-      if (lead && has_res && mtile + 2 * gstride < n_tiles) load_res(mtile + 2 * gstride, static_cast<int>(m & 1u));
+    };
+    // fold of this rank's rows: head.cu's fold (fp32, fold order = cluster rank) over 16-byte chunks
+    // (8 channels of a row, as 4 packed channel pairs), z written over the own tile's rows
+    auto fold_pass = [&]() {
+      const int nch = (hr1 - hr0) * 8;
+      for (int c = gtid; c < nch; c += 256) {
+        const int row = hr0 + (c >> 3), c8 = c & 7;
+        const uint32_t off = sw128(static_cast<uint32_t>(row), static_cast<uint32_t>(c8 * 16));
+        uint4 v[kNS];
+#pragma unroll
+        for (int k = 0; k < kNS; ++k) {
+          const int slot = k < g ? k : k - 1;  // receive slot of rank k's rows
+          v[k] = lds128(k == g ? stg_a + off
+                               : stg_a + sw128(static_cast<uint32_t>(128 + slot * kHRows + row - hr0), static_cast<uint32_t>(c8 * 16)));
+        }
+        uint32_t zo[4];
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+          const int ch = 8 * c8 + 2 * pp;
+          auto word = [&](int k) {
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[k]);
+            return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[pp]));
+          };
+          float2 z = word(0);
+          auto post = [&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            if (kFoldSpec ? ((FL >> (13 + k)) & 1) != 0 : L.head.aff_s[k] != nullptr) {
+              const float2 sv = *reinterpret_cast<const float2*>(s_fold + (2 * k) * kC + ch);
+              const float2 tv = *reinterpret_cast<const float2*>(s_fold + (2 * k + 1) * kC + ch);
+              z = __ffma2_rn(z, sv, tv);
+            }
+            if (kFoldSpec ? ((FL >> (10 + k)) & 1) != 0 : L.head.relu[k] != 0) {
+              z.x = fmaxf(z.x, 0.f);
+              z.y = fmaxf(z.y, 0.f);
+            }
+          };
+          auto step = [&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            const float2 zk = word(k);
+            const bool mul = kFoldSpec ? ((FL >> (7 + k)) & 1) != 0 : L.head.op[k] == PW_MUL;
+            z = mul ? __fmul2_rn(z, zk) : __fadd2_rn(z, zk);
+            post(kc);
+          };
+          post(std::integral_constant<int, 0>{});
+          if constexpr (kNS > 1) step(std::integral_constant<int, 1>{});
+          if constexpr (kNS > 2) step(std::integral_constant<int, 2>{});
+          const __nv_bfloat162 zb = __floats2bfloat162_rn(z.x, z.y);
+          zo[pp] = *reinterpret_cast<const uint32_t*>(&zb);
+        }
+        sts128(stg_a + off, make_uint4(zo[0], zo[1], zo[2], zo[3]));
+      }
     };
     if (has_res && lead) {
       prefetch_tmap(&grp.res_map);
@@ -458,205 +510,148 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
       if (t0_ + gstride < n_tiles) load_res(t0_ + gstride, 1);
     }
     int j = e;
-    // the tile loop, compiled separately for the CTA that folds the head (HF, rank 0) and the others
-    auto epi_loop = [&](auto hf_c) {
-      constexpr bool HF = decltype(hf_c)::value;  // fused head, rank 0: fold + head
-      constexpr bool HS = kHead && !HF;           // fused head, ranks >= 1: send the tile to rank 0
-      for (int64_t tile = local + static_cast<int64_t>(e) * nct; tile < n_tiles; tile += 2 * static_cast<int64_t>(nct), j += 2) {
-        const int64_t p0 = tile * kTileRows;
-        const long long te0 = clock64();
-        ws_wait_relaxed(&tfull[e], static_cast<uint32_t>(j >> 1) & 1u);
-        const long long te1 = clock64();
-        tr_ew += te1 - te0;
-        // staging buffer free? (this group's previous TMA store has read it)
-        // (fused head, ranks >= 1: rank 0 has consumed this group's previous tile, so the copy of it out
-        // of the staging buffer is complete)
-        // Ranks >= 1 alternate between the two halves of the group's staging buffer, so tile n's epilogue
-        // only needs tile n-2's copy to have landed (rank 0 has consumed it), not tile n-1's.
-        const uint32_t gn = static_cast<uint32_t>(j) >> 1;  // this group's tile count
-        if (lead) {
-          if (HS) {
-            if (gn >= 2) cl_wait(&zfree[2 * e + (gn & 1u)], ((gn >> 1) & 1u) ^ 1u);
-          } else {
-            bulk_wait_read0();
-          }
-        }
-        if (HF && gn >= 1) head_drain(gn - 1, tile - gstride);
-        epi_group_sync(e);
-        const int kb = (j >> 1) & 1;  // residual buffer of this group tile
-        if (has_res) ws_wait_relaxed(&rfull[2 * e + kb], static_cast<uint32_t>(j >> 2) & 1u);
-        if (HF && kNS > 1) cl_wait(&zfull[e], (static_cast<uint32_t>(j) >> 1) & 1u);
-        const uint32_t rbuf_a = smem_u32(rbuf0 + kb * 128 * kRB);
-        const long long te2 = clock64();
-        tr_sw += te2 - te1;
-        tc_fence_after();
-        // Chunk h = accumulator columns c = 64H + 32h + [0, 32).  Lanes 16k + i / 16k + 8 + i hold the
-        // A / B tap partial sums of channel 8k + i, so output row c = A[c] + B[c+1] needs one shuffle
-        // for odd c (B[c+1] sits with the neighbouring column pair) and none for even c.
-        // validity of this warp's 64 rows (padding rows are stored as zeros): one bit per row
-        uint32_t vmask[2];
-  #pragma unroll
-        for (int w = 0; w < 2; ++w) vmask[w] = __ballot_sync(0xffffffffu, geo.valid(p0 + 64 * H + 32 * w + lane));
-        const uint32_t tq = tbase + kAcc0 + static_cast<uint32_t>(e * kN + 64 * H) + (static_cast<uint32_t>(q * 32) << 16);
-  #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t a0[16], a1[16], xb;
-          tmem_ld16x256b_x4(tq + 32 * h, a0);
-          tmem_ld16x256b_x4(tq + (16u << 16) + 32 * h, a1);
-          if (H == 0 || h == 0) {
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(xb) : "r"(tq + 32 * h + 32) : "memory");
-          } else {
-            xb = 0;  // column 128 would only feed row 127, which is never stored
-          }
-          tmem_ld_wait();
-          if (h == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_relaxed(&tempty[e]);
-          }
-  #pragma unroll
-          for (int blk = 0; blk < 2; ++blk) {
-            uint32_t (&a)[16] = blk == 0 ? a0 : a1;
-            uint32_t rres[4] = {0u, 0u, 0u, 0u};
-            if (has_res) {
-              // residual rows 64H + 32h + 8i + arow%8 (matrix i), channel chunk 2q + blk
-              const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
-              ldsm_x4_trans(rbuf_a + sw128(row, static_cast<uint32_t>((2 * q + blk) * 16)), rres);
-            }
-            float fsv[3], ftv[3];  // fused head (rank 0): this blk's channel's fold tables
-          if (HF) {
-            const int ch = 16 * q + 8 * blk + ci;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              fsv[k] = k < kNS ? s_fold[(2 * k) * kC + ch] : 1.f;
-              ftv[k] = k < kNS ? s_fold[(2 * k + 1) * kC + ch] : 0.f;
-            }
-          }
-          uint32_t zr[2][4];  // fused head (rank 0): the other subnetworks' values of the same elements
-            if (HF) {
-              const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
-  #pragma unroll
-              for (int k = 0; k < 2; ++k)
-                if (k + 1 < kNS) ldsm_x4_trans(stg_a + k * 128 * kRB + sw128(row, static_cast<uint32_t>((2 * q + blk) * 16)), zr[k]);
-            }
-            const float bnd = __uint_as_float(__shfl_sync(0xffffffffu, xb, 16 * blk + 8 + ci));
-            uint32_t o[4], o2[4];
-  #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint32_t snd = t0 == 0 ? (i < 3 ? a[4 * (i + 1) + 2] : 0u) : a[4 * i + 2];
-              float got = __uint_as_float(__shfl_sync(0xffffffffu, snd, t0 == 3 ? lane - 3 : lane + 1));
-              if (i == 3 && t0 == 3) got = bnd;
-              float y0 = __uint_as_float(a[4 * i + 0]) + __uint_as_float(a[4 * i + 3]) + bias[blk];
-              float y1 = __uint_as_float(a[4 * i + 1]) + got + bias[blk];
-              if (has_res) {
-                const float2 rf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rres[i]));
-                y0 += rf.x;
-                y1 += rf.y;
-              }
-              if (relu_main) {
-                y0 = fmaxf(y0, 0.f);
-                y1 = fmaxf(y1, 0.f);
-              }
-              const int rb = 8 * i + 2 * t0;  // row 64H + 32h + rb
-              const bool v0 = (vmask[h] >> rb) & 1u, v1 = (vmask[h] >> (rb + 1)) & 1u;
-              if (!v0) y0 = 0.f;
-              if (!v1) y1 = 0.f;
-              const __nv_bfloat162 ob = __floats2bfloat162_rn(y0, y1);
-              o[i] = *reinterpret_cast<const uint32_t*>(&ob);
-              if (HF) {
-                // head.cu's fold over this conv's stored value (bf16) and the received tiles: fp32,
-                // the two rows of a channel as one packed pair (FMUL2 / FADD2 / FFMA2, same rounding)
-                float2 z = __bfloat1622float2(ob);
-                auto post = [&](auto kc) {
-                  constexpr int k = decltype(kc)::value;
-                  if (kFoldSpec ? ((FL >> (13 + k)) & 1) != 0 : true)  // BN (generic: s = 1, t = 0 if none)
-                    z = __ffma2_rn(z, make_float2(fsv[k], fsv[k]), make_float2(ftv[k], ftv[k]));
-                  if (kFoldSpec ? ((FL >> (10 + k)) & 1) != 0 : true) {  // ReLU (generic: floor -inf if none)
-                    const float fl = kFoldSpec ? 0.f : rfloor[k];
-                    z.x = fmaxf(z.x, fl);
-                    z.y = fmaxf(z.y, fl);
-                  }
-                };
-                auto combine = [&](auto kc, uint32_t zw) {
-                  constexpr int k = decltype(kc)::value;
-                  const float2 zk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zw));
-                  if (kFoldSpec) {
-                    z = ((FL >> (7 + k)) & 1) ? __fmul2_rn(z, zk) : __fadd2_rn(z, zk);
-                  } else {
-                    const float2 m = __fmul2_rn(z, zk), a = __fadd2_rn(z, zk);
-                    z = fmul[k] ? m : a;
-                  }
-                  post(kc);
-                };
-                post(std::integral_constant<int, 0>{});
-                if constexpr (kNS > 1) combine(std::integral_constant<int, 1>{}, zr[0][i]);
-                if constexpr (kNS > 2) combine(std::integral_constant<int, 2>{}, zr[1][i]);
-                const float z0 = z.x, z1 = z.y;
-                const __nv_bfloat162 zb = __floats2bfloat162_rn(z0, z1);
-                o[i] = *reinterpret_cast<const uint32_t*>(&zb);
-              }
-              if (has_out2) {
-                __nv_bfloat162 u;
-                if (relu2_only) {
-                  u = __hmax2(ob, __float2bfloat162_rn(0.f));
-                } else {
-                  const float2 f = __bfloat1622float2(ob);
-                  const float x0 = fmaxf(f.x * s2v[blk] + t2v[blk], 0.f);
-                  const float x1 = fmaxf(f.y * s2v[blk] + t2v[blk], 0.f);
-                  u = __floats2bfloat162_rn(v0 ? x0 : 0.f, v1 ? x1 : 0.f);
-                }
-                o2[i] = *reinterpret_cast<const uint32_t*>(&u);
-              }
-            }
-            const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
-            const uint32_t off = sw128(row, static_cast<uint32_t>((2 * q + blk) * 16));
-            if (!(L.debug & 1)) {
-              // (fused head, ranks >= 1: staging half gn & 1)
-              // (fused head, rank 0: z overwrites the residual tile, same positions it was read from)
-              stsm_x4_trans((HF ? rbuf_a : stg_a + (HS ? (gn & 1u) * 128u * kRB : 0u)) + off, o);
-              if (has_out2) stsm_x4_trans(stg_a + 128 * kRB + off, o2);
-            }
-          }
-        }
-        const long long te3 = clock64();
-        tr_comb += te3 - te2;
-        fence_proxy_async_smem();
-        if (HF) {  // z tile staged: warp 18 issues the head UMMAs (read back at the group's next tile)
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&zready[e]);
-        }
-        epi_group_sync(e);
+    for (int64_t tile = local + static_cast<int64_t>(e) * nct; tile < n_tiles; tile += 2 * static_cast<int64_t>(nct), j += 2) {
+      const int64_t p0 = tile * kTileRows;
+      const long long te0 = clock64();
+      ws_wait_relaxed(&tfull[e], static_cast<uint32_t>(j >> 1) & 1u);
+      const long long te1 = clock64();
+      tr_ew += te1 - te0;
+      const uint32_t gn = static_cast<uint32_t>(j) >> 1;  // this group's tile count
+      // staging buffer free?  TMA store: this group's previous store has read it.  Fused head: every
+      // other rank has folded the previous tile (so the copies out of it, and into their receive slots,
+      // are complete), and this rank's head UMMAs have read its z rows (head_drain).
+      if (lead) {
         if (kHead) {
-          if (g > 0 && lead) {
-            // this subnetwork's tile -> rank 0's receive buffer (distributed shared memory)
-            // (rank 0's receive buffer is free once it has consumed this group's previous tile)
-            if (gn >= 1) cl_wait(&zfree[2 * e + ((gn - 1) & 1u)], ((gn - 1) >> 1) & 1u);
-            {
-            const uint32_t zb = cl_map(&zfull[e], 0);
-            cl_arrive_expect_tx(zb, 128u * kRB);
-            const uint8_t* src = stg + (gn & 1u) * 128u * kRB;
-            bulk_copy_to_cta(cl_map(stg + (g - 1) * 128 * kRB, 0), src, 128u * kRB, zb);
+          if (kNS > 1 && gn >= 1 && !(L.debug & 128)) cl_wait(&cons[e], (gn - 1) & 1u);
+        } else {
+          bulk_wait_read0();
+        }
+      }
+      if (kHead && gn >= 1) head_drain(gn - 1, tile - gstride);
+      epi_group_sync(e);
+      const int kb = (j >> 1) & 1;  // residual buffer of this group tile
+      if (has_res) ws_wait_relaxed(&rfull[2 * e + kb], static_cast<uint32_t>(j >> 2) & 1u);
+      const uint32_t rbuf_a = smem_u32(rbuf0 + kb * 128 * kRB);
+      const long long te2 = clock64();
+      tr_sw += te2 - te1;
+      tc_fence_after();
+      // Chunk h = accumulator columns c = 64H + 32h + [0, 32).  Lanes 16k + i / 16k + 8 + i hold the
+      // A / B tap partial sums of channel 8k + i, so output row c = A[c] + B[c+1] needs one shuffle
+      // for odd c (B[c+1] sits with the neighbouring column pair) and none for even c.
+      // validity of this warp's 64 rows (padding rows are stored as zeros): one bit per row
+      uint32_t vmask[2];
+#pragma unroll
+      for (int w = 0; w < 2; ++w) vmask[w] = __ballot_sync(0xffffffffu, geo.valid(p0 + 64 * H + 32 * w + lane));
+      const uint32_t tq = tbase + kAcc0 + static_cast<uint32_t>(e * kN + 64 * H) + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t a0[16], a1[16], xb;
+        tmem_ld16x256b_x4(tq + 32 * h, a0);
+        tmem_ld16x256b_x4(tq + (16u << 16) + 32 * h, a1);
+        if (H == 0 || h == 0) {
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(xb) : "r"(tq + 32 * h + 32) : "memory");
+        } else {
+          xb = 0;  // column 128 would only feed row 127, which is never stored
+        }
+        tmem_ld_wait();
+        if (h == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_relaxed(&tempty[e]);
+        }
+#pragma unroll
+        for (int blk = 0; blk < 2; ++blk) {
+          uint32_t (&a)[16] = blk == 0 ? a0 : a1;
+          uint32_t rres[4] = {0u, 0u, 0u, 0u};
+          if (has_res) {
+            // residual rows 64H + 32h + 8i + arow%8 (matrix i), channel chunk 2q + blk
+            const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
+            ldsm_x4_trans(rbuf_a + sw128(row, static_cast<uint32_t>((2 * q + blk) * 16)), rres);
+          }
+          const float bnd = __uint_as_float(__shfl_sync(0xffffffffu, xb, 16 * blk + 8 + ci));
+          uint32_t o[4], o2[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t snd = t0 == 0 ? (i < 3 ? a[4 * (i + 1) + 2] : 0u) : a[4 * i + 2];
+            float got = __uint_as_float(__shfl_sync(0xffffffffu, snd, t0 == 3 ? lane - 3 : lane + 1));
+            if (i == 3 && t0 == 3) got = bnd;
+            float y0 = __uint_as_float(a[4 * i + 0]) + __uint_as_float(a[4 * i + 3]) + bias[blk];
+            float y1 = __uint_as_float(a[4 * i + 1]) + got + bias[blk];
+            if (has_res) {
+              const float2 rf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rres[i]));
+              y0 += rf.x;
+              y1 += rf.y;
+            }
+            if (relu_main) {
+              y0 = fmaxf(y0, 0.f);
+              y1 = fmaxf(y1, 0.f);
+            }
+            const int rb = 8 * i + 2 * t0;  // row 64H + 32h + rb
+            const bool v0 = (vmask[h] >> rb) & 1u, v1 = (vmask[h] >> (rb + 1)) & 1u;
+            if (!v0) y0 = 0.f;
+            if (!v1) y1 = 0.f;
+            const __nv_bfloat162 ob = __floats2bfloat162_rn(y0, y1);
+            o[i] = *reinterpret_cast<const uint32_t*>(&ob);
+            if (has_out2) {
+              __nv_bfloat162 u;
+              if (relu2_only) {
+                u = __hmax2(ob, __float2bfloat162_rn(0.f));
+              } else {
+                const float2 f = __bfloat1622float2(ob);
+                const float x0 = fmaxf(f.x * s2v[blk] + t2v[blk], 0.f);
+                const float x1 = fmaxf(f.y * s2v[blk] + t2v[blk], 0.f);
+                u = __floats2bfloat162_rn(v0 ? x0 : 0.f, v1 ? x1 : 0.f);
+              }
+              o2[i] = *reinterpret_cast<const uint32_t*>(&u);
             }
           }
-          // rank 0: the receive buffers are consumed; its residual buffer holds z until the head UMMAs
-          // have read it (reloaded in head_drain)
-          if (HF && lead)
-            for (int r = 1; r < kNS; ++r) cl_arrive(cl_map(&zfree[2 * e + (gn & 1u)], static_cast<uint32_t>(r)));
-          if (!HF && lead && has_res && tile + 2 * gstride < n_tiles) load_res(tile + 2 * gstride, kb);
-        } else if (lead && !(L.debug & 1)) {
-          tma_store_2d(&grp.out_map, stg, 0, static_cast<int32_t>(p0));
-          if (has_out2) tma_store_2d(&grp.out2_map, stg + 128 * kRB, 0, static_cast<int32_t>(p0));
-          bulk_commit();
+          const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
+          const uint32_t off = sw128(row, static_cast<uint32_t>((2 * q + blk) * 16));
+          if (!(L.debug & 1)) {
+            stsm_x4_trans(stg_a + off, o);
+            if (has_out2) stsm_x4_trans(stg_a + 128 * kRB + off, o2);
+          }
+        }
+      }
+      const long long te3 = clock64();
+      tr_comb += te3 - te2;
+      fence_proxy_async_smem();
+      epi_group_sync(e);
+      if (kHead) {
+        if (lead) {
+          // rows of rank d -> rank d's receive slot for this rank
+#pragma unroll
+          for (int d = 0; d < kNS; ++d) {
+            if (d == g || (L.debug & 128)) continue;
+            const int d0 = d * kHRows, dn = (d0 + kHRows < 128 ? d0 + kHRows : 128) - d0;
+            const int slot = g < d ? g : g - 1;
+            const uint32_t zb = cl_map(&land[e], static_cast<uint32_t>(d));
+            cl_arrive_expect_tx(zb, static_cast<uint32_t>(dn) * kRB);
+            bulk_copy_to_cta(cl_map(stg + (128 + slot * kHRows) * kRB, static_cast<uint32_t>(d)), stg + d0 * kRB,
+                             static_cast<uint32_t>(dn) * kRB, zb);
+          }
           if (has_res && tile + 2 * gstride < n_tiles) load_res(tile + 2 * gstride, kb);
         }
-        tr_wr += clock64() - te3;
+        if (kNS > 1 && !(L.debug & 128)) cl_wait(&land[e], gn & 1u);  // the other ranks' rows of this tile
+        if (!(L.debug & 64)) fold_pass();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&zready[e]);  // warp 18: head UMMAs over the z rows
+        epi_group_sync(e);
+        if (lead && !(L.debug & 128))  // receive slots read: the senders may reuse them (and their staging)
+          for (int r = 0; r < kNS; ++r)
+            if (r != g) cl_arrive(cl_map(&cons[e], static_cast<uint32_t>(r)));
+      } else if (lead && !(L.debug & 1)) {
+        tma_store_2d(&grp.out_map, stg, 0, static_cast<int32_t>(p0));
+        if (has_out2) tma_store_2d(&grp.out2_map, stg + 128 * kRB, 0, static_cast<int32_t>(p0));
+        bulk_commit();
+        if (has_res && tile + 2 * gstride < n_tiles) load_res(tile + 2 * gstride, kb);
       }
-        if (HF && j > e) head_drain((static_cast<uint32_t>(j) >> 1) - 1, local + static_cast<int64_t>(e) * nct + (static_cast<int64_t>(j >> 1) - 1) * gstride);
-    };
-    if (kHead && g == 0)
-      epi_loop(std::integral_constant<bool, kHead>{});
-    else
-      epi_loop(std::false_type{});
+      tr_wr += clock64() - te3;
+    }
+    if (kHead && j > e)
+      head_drain((static_cast<uint32_t>(j) >> 1) - 1,
+                 local + static_cast<int64_t>(e) * nct + (static_cast<int64_t>(j >> 1) - 1) * gstride);
     if (lead) bulk_wait0();
     if (L.trace && lead && e == 0 && (!kHead || g == ((L.debug & 16) ? 1 : 0))) {  // (fused head: rank 0, or rank 1 with debug bit 4)
       atomicAdd(&L.trace[kTraceEpiWaitFull], static_cast<unsigned long long>(tr_ew));

@@ -42,7 +42,9 @@ struct WsLaunch {
   PlaneGeom geo;
   int64_t n_tiles;   // 127-row output tiles
   int32_t ngroups, stages, win_alloc;
-  int32_t debug;     // experiments only (CNRX_WS_DEBUG): bit 0 skip staging writes + stores, bit 1 skip input ReLU pass
+  int32_t debug;     // experiments only (CNRX_WS_DEBUG): bit 0 skip staging writes + stores, bit 1 skip input ReLU pass;
+                     // fused head: bit 4 trace rank 1 instead of rank 0, bit 5 skip the head UMMAs, bit 6 skip
+                     // the fold pass, bit 7 skip the DSMEM exchange (results invalid with bits 5-7)
   unsigned long long* trace;  // debug: per-role clock64 totals (kTrace* in conv_tc.h + kWsTrace*)
 };
 enum : int { kWsTraceCombine = 8, kWsTraceStageWait, kWsTraceWrite, kWsTraceN };
