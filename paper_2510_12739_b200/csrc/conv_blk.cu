@@ -150,7 +150,7 @@ __device__ __forceinline__ void tmem_ld_x1(uint32_t taddr, uint32_t& r) {
 
 __device__ __forceinline__ bool row_valid(const PlaneGeom& geo, int64_t row) { return row >= 0 && geo.valid(row); }
 
-template <bool RELU_IN>
+template <bool RELU_IN, bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_constant__ BlkLaunch L) {
   constexpr uint32_t IDESC = idesc_bf16_f32(128, kN);
   extern __shared__ uint8_t smem_dyn[];
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
   const uint32_t x_a = smem_u32(smem + lay.x_off);
   const uint32_t xr_a = smem_u32(smem + lay.xr_off);
   const uint32_t w_a = smem_u32(smem + lay.w_off);
-  const bool tr = L.trace != nullptr;
+  constexpr bool tr = TRACE;  // per-role cycle counters (CNRX_TRACE): a separate instantiation
   // ring positions advance incrementally (the ring depth XS is a runtime value: no division in the loops)
   auto ring_next = [&](int& slot, uint32_t& phase) {
     if (++slot == XS) {
@@ -569,11 +569,18 @@ void make_map(const void* plane, int64_t nalloc, uint32_t box_rows, CUtensorMap*
   if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
+template <bool RELU_IN, bool TRACE>
+void launch_tt(const BlkLaunch& L, int grid, cudaStream_t stream) {
+  const BlkLayout lay = blk_layout(L.xstages, L.win_alloc, RELU_IN);
+  ensure_smem_attr(reinterpret_cast<const void*>(conv_blk64_kernel<RELU_IN, TRACE>), static_cast<int>(lay.total));
+  launch_pdl(conv_blk64_kernel<RELU_IN, TRACE>, dim3(grid), dim3(kThreads), lay.total, stream, L);
+}
 template <bool RELU_IN>
 void launch_t(const BlkLaunch& L, int grid, cudaStream_t stream) {
-  const BlkLayout lay = blk_layout(L.xstages, L.win_alloc, RELU_IN);
-  ensure_smem_attr(reinterpret_cast<const void*>(conv_blk64_kernel<RELU_IN>), static_cast<int>(lay.total));
-  launch_pdl(conv_blk64_kernel<RELU_IN>, dim3(grid), dim3(kThreads), lay.total, stream, L);
+  if (L.trace)
+    launch_tt<RELU_IN, true>(L, grid, stream);
+  else
+    launch_tt<RELU_IN, false>(L, grid, stream);
 }
 
 }  // namespace

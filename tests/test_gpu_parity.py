@@ -255,17 +255,20 @@ def test_device_api_graph_capture_and_sharded():
     assert np.array_equal(P.forward_sharded([p, q], feat), p.forward(feat))
 
 
-def test_tensor_core_kernels_are_used():
+def test_tensor_core_kernels_are_used(monkeypatch):
     g = G.CONFIGS["cfg2"].graph()
     p = P.Plan(g, "bf16")
-    p.forward(np.zeros((64, 14, 16, 12), np.float32))
-    names = p.launch_names()
-    assert sum("conv_ws64" in n for n in names) == 8, names  # large batch: two kernels per block
-    p.forward(np.zeros((1, 14, 16, 12), np.float32))
-    names = p.launch_names()
-    assert sum("conv_blk64" in n for n in names) == 4 and not any("conv_ws64" in n for n in names), names
+    for B in (1, 64):  # every batch runs the residual blocks fused (conv_blk.cu)
+        p.forward(np.zeros((B, 14, 16, 12), np.float32))
+        names = p.launch_names()
+        assert sum("conv_blk64" in n for n in names) == 4 and not any("conv_ws64" in n for n in names), names
     info = p.info()
     assert info["n_tc_convs"] == 27 and info["macs_per_re"] == 887296
+    monkeypatch.setenv("CNRX_BLK", "0")  # the two-kernel program: two weights-stationary convs per block
+    q = P.Plan(g, "bf16")
+    q.forward(np.zeros((64, 14, 16, 12), np.float32))
+    names = q.launch_names()
+    assert sum("conv_ws64" in n for n in names) == 8, names
 
 
 def test_cpp_drop_in_example():

@@ -14,7 +14,7 @@ for st in $STAGES; do
       B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-latency --no-e2e"
       timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
         -c 120 --csv --log-file gpurun_out/ncu_launches.csv $B > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv_ws64 -s 2 -c 1 \
-        -o gpurun_out/ncu_conv_ws64 -f $B > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?" ;;
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-conv_blk64} -s 2 -c 1 \
+        -o gpurun_out/ncu_${NCU_KERNEL:-conv_blk64} -f $B > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?" ;;
   esac
 done
