@@ -150,6 +150,17 @@ __device__ __forceinline__ void tmem_ld_x1(uint32_t taddr, uint32_t& r) {
 
 __device__ __forceinline__ bool row_valid(const PlaneGeom& geo, int64_t row) { return row >= 0 && geo.valid(row); }
 
+// Accumulator waits of the epilogue warps (16 warps polling): nanosleep back-off of this many ns (0: spin)
+#ifndef CNRX_BLK_EPI_SLEEP_NS
+#define CNRX_BLK_EPI_SLEEP_NS 0
+#endif
+__device__ __forceinline__ void epi_acc_wait(uint64_t* bar, uint32_t parity) {
+  if (CNRX_BLK_EPI_SLEEP_NS > 0)
+    mbar_wait_backoff<CNRX_BLK_EPI_SLEEP_NS>(bar, parity);
+  else
+    mbar_wait(bar, parity);
+}
+
 template <bool RELU_IN, bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_constant__ BlkLaunch L) {
   constexpr uint32_t IDESC = idesc_bf16_f32(128, kN);
@@ -392,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       const int64_t p0 = (t_begin + u - 1) * kTile;
       const uint32_t vm = __ballot_sync(0xffffffffu, row_valid(geo, p0 + r));
       const long long ta = tr ? clock64() : 0;
-      mbar_wait(t1full, static_cast<uint32_t>(u) & 1u);
+      epi_acc_wait(t1full, static_cast<uint32_t>(u) & 1u);
       const long long t1 = tr ? clock64() : 0;
       if (tr) t_full += t1 - ta;
       tc_fence_after();
@@ -486,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       for (int blk = 0; blk < 2; ++blk) ldsm_x4_trans(xs_a + sw128(xrow, static_cast<uint32_t>((2 * q + blk) * 16)), res[blk]);
       const uint32_t vm = __ballot_sync(0xffffffffu, row_valid(geo, p0 + r));
       const long long ta = tr ? clock64() : 0;
-      mbar_wait(t2full, static_cast<uint32_t>(v) & 1u);
+      epi_acc_wait(t2full, static_cast<uint32_t>(v) & 1u);
       const long long t1 = tr ? clock64() : 0;
       if (tr) t_full += t1 - ta;
       tc_fence_after();
