@@ -31,9 +31,15 @@ struct Cplx {
 __device__ __forceinline__ Cplx cmul(Cplx a, Cplx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
 
 // Computes the 6N features of (b, t, f) given per-pilot-symbol LS values hs[j][a] at column f.
-template <int OUT_PLANE>
-__global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, int N, PilotTablesDev pt,
+// NT / NS > 0: antenna and pilot-symbol counts known at compile time, so the per-column LS values and
+// the feature vector live in registers (the generic form indexes them at run time: an 816-byte stack
+// frame in local memory).
+template <int OUT_PLANE, int NT = 0, int NS = 0>
+__global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, int N_rt, PilotTablesDev pt,
                                  float* __restrict__ feat_ref, __nv_bfloat16* __restrict__ plane, int cpad) {
+  const int N = NT > 0 ? NT : N_rt;
+  constexpr int kN = NT > 0 ? NT : kMaxN;
+  constexpr int kS = NS > 0 ? NS : kMaxPilotSyms;
   const int64_t cols_per_slot = geo.F + geo.npad;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t n_cols = static_cast<int64_t>(geo.B) * cols_per_slot;
@@ -70,14 +76,19 @@ __global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, in
     return;
   }
   // LS estimate at every pilot symbol, interpolated along F to this column.
-  Cplx hs[kMaxPilotSyms][kMaxN];
-  for (int j = 0; j < pt.n_sym; ++j) {
+  Cplx hs[kS][kN];
+  const int n_sym = NS > 0 ? NS : pt.n_sym;
+#pragma unroll
+  for (int j = 0; j < kS; ++j) {
+    if (j >= n_sym) break;
     const int ts = pt.sym[j];
     const int flo = pt.flo[j * F + f], fhi = pt.fhi[j * F + f];
     const float w = pt.wf[j * F + f];
     const Cplx ilo = {pt.inv_x[2 * (ts * F + flo)], pt.inv_x[2 * (ts * F + flo) + 1]};
     const Cplx ihi = {pt.inv_x[2 * (ts * F + fhi)], pt.inv_x[2 * (ts * F + fhi) + 1]};
-    for (int a = 0; a < N; ++a) {
+#pragma unroll
+    for (int a = 0; a < kN; ++a) {
+      if (a >= N) break;
       const float2 ylo = y[((static_cast<int64_t>(b) * T + ts) * F + flo) * N + a];
       const float2 yhi = y[((static_cast<int64_t>(b) * T + ts) * F + fhi) * N + a];
       const Cplx llo = cmul({ylo.x, ylo.y}, ilo), lhi = cmul({yhi.x, yhi.y}, ihi);
@@ -85,23 +96,33 @@ __global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, in
     }
   }
   for (int t = 0; t < (OUT_PLANE ? geo.T1 : T); ++t) {
-    float v[6 * kMaxN];
+    float v[6 * kN];
     const int C = 6 * N;
     if (t < T) {
       const int j0 = pt.jlo[t], j1 = pt.jhi[t];
       const float wt = pt.wt[t];
       const float xr = pt.x[2 * (t * F + f)], xi = pt.x[2 * (t * F + f) + 1];
-      for (int a = 0; a < N; ++a) {
+#pragma unroll
+      for (int a = 0; a < kN; ++a) {
+        if (a >= N) break;
+        // hs[j0][a], hs[j1][a] by static indices (selects), so hs stays in registers
+        Cplx h0 = hs[0][a], h1 = hs[0][a];
+#pragma unroll
+        for (int j = 1; j < kS; ++j) {
+          if (j == j0) h0 = hs[j][a];
+          if (j == j1) h1 = hs[j][a];
+        }
         const float2 yv = y[((static_cast<int64_t>(b) * T + t) * F + f) * N + a];
         v[6 * a + 0] = yv.x;
         v[6 * a + 1] = yv.y;
         v[6 * a + 2] = xr;
         v[6 * a + 3] = xi;
-        v[6 * a + 4] = (1.f - wt) * hs[j0][a].re + wt * hs[j1][a].re;
-        v[6 * a + 5] = (1.f - wt) * hs[j0][a].im + wt * hs[j1][a].im;
+        v[6 * a + 4] = (1.f - wt) * h0.re + wt * h1.re;
+        v[6 * a + 5] = (1.f - wt) * h0.im + wt * h1.im;
       }
     } else {
-      for (int i = 0; i < C; ++i) v[i] = 0.f;
+#pragma unroll
+      for (int i = 0; i < 6 * kN; ++i) v[i] = 0.f;
     }
     if (OUT_PLANE && cpad == 16) {  // one 32-byte row: a single 256-bit store
       u32x8 o;
@@ -114,9 +135,12 @@ __global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, in
       stg256(plane + geo.row_of(b, t, f) * cpad, o);
     } else if (OUT_PLANE) {
       __nv_bfloat16* dst = plane + geo.row_of(b, t, f) * cpad;
-      for (int i0 = 0; i0 < cpad; i0 += 8) {
+#pragma unroll
+      for (int i0 = 0; i0 < (6 * kN + 15) / 16 * 16; i0 += 8) {
+        if (i0 >= cpad) break;
         uint4 o;
         __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int k = i0 + 2 * i;
           op[i] = __floats2bfloat162_rn(k < C ? v[k] : 0.f, k + 1 < C ? v[k + 1] : 0.f);
@@ -395,8 +419,16 @@ const char* launch_featurize_plane(const float* y, const PlaneGeom& geo, int N, 
     CNRX_CUDA(cudaGetLastError());
     return "featurize_row_kernel";
   }
-  featurize_kernel<1><<<static_cast<unsigned>((n + threads - 1) / threads), threads, 0, s>>>(
-      reinterpret_cast<const float2*>(y), geo, N, pt, nullptr, plane, cpad);
+  const unsigned blocks = static_cast<unsigned>((n + threads - 1) / threads);
+  const float2* y2 = reinterpret_cast<const float2*>(y);
+  if (pt.n_sym == 2 && N == 2)  // the BASELINE DM-RS layout (2 pilot symbols) with 2 / 1 / 4 antennas
+    featurize_kernel<1, 2, 2><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad);
+  else if (pt.n_sym == 2 && N == 1)
+    featurize_kernel<1, 1, 2><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad);
+  else if (pt.n_sym == 2 && N == 4)
+    featurize_kernel<1, 4, 2><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad);
+  else
+    featurize_kernel<1><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad);
   CNRX_CUDA(cudaGetLastError());
   return "featurize_kernel<plane>";
 }
