@@ -1340,8 +1340,8 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
                   GL.blkl.relu_in, h[kBlkTraceTiles], h[kBlkTraceProd] / nt, h[kBlkTraceM1In] / nt, h[kBlkTraceM1Acc] / nt,
                   h[kBlkTraceM2In] / nt, h[kBlkTraceM2Acc] / nt, h[kBlkTraceE1Full] / nt, h[kBlkTraceE1W] / nt,
                   h[kBlkTraceE2Full] / nt, h[kBlkTraceRelu] / nt, h[kBlkTraceTotal] / nt);
-          fprintf(stderr, "[trace]   epi1 drain %.0f combine %.0f store %.0f | epi2 drain %.0f combine %.0f store %.0f\n",
-                  h[kBlkTraceE1Drain] / nt, h[kBlkTraceE1Comb] / nt, h[kBlkTraceE1Store] / nt, h[kBlkTraceE2Drain] / nt,
+          fprintf(stderr, "[trace]   epi1 drain %.0f combine %.0f store %.0f (fence %.0f) | epi2 drain %.0f combine %.0f store %.0f\n",
+                  h[kBlkTraceE1Drain] / nt, h[kBlkTraceE1Comb] / nt, h[kBlkTraceE1Store] / nt, h[kBlkTraceE1Fence] / nt, h[kBlkTraceE2Drain] / nt,
                   h[kBlkTraceE2Comb] / nt, h[kBlkTraceE2Store] / nt);
           fprintf(stderr, "[trace]   CTAs %llu, span %.1f us, effective SM clock %.0f MHz\n", h[12], (h[14] - ~h[13]) * 1e-3,
                   h[15] ? static_cast<double>(h[kBlkTraceTotal]) / static_cast<double>(h[15]) * 1e3 : 0.0);

@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
     const uint32_t trash = smem_u32(smem + lay.trash_off);
     const int r = 32 * H + lane;  // this lane's stmatrix row within the tile
     const uint32_t tq = tbase + kAcc1 + static_cast<uint32_t>(32 * H) + (static_cast<uint32_t>(q * 32) << 16);
-    long long t_full = 0, t_w = 0, e1_drain = 0, e1_comb = 0, e1_store = 0;
+    long long t_full = 0, t_w = 0, e1_drain = 0, e1_comb = 0, e1_store = 0, e1_fence = 0;
     for (int u = 0; u < U; ++u) {
       const int64_t p0 = (t_begin + u - 1) * kTile;
       const uint32_t vm = __ballot_sync(0xffffffffu, row_valid(geo, p0 + r));
@@ -446,8 +446,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
           stsm_x4_trans(addr, o[blk]);
         }
       }
+      const long long tf = tr ? clock64() : 0;
       fence_proxy_async_smem();
       __syncwarp();
+      if (tr) e1_fence += clock64() - tf;
       if (lane == 0) {
 #pragma unroll
         for (int dv = -1; dv <= 1; ++dv) {
@@ -463,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       atomicAdd(&L.trace[kBlkTraceE1Drain], static_cast<unsigned long long>(e1_drain));
       atomicAdd(&L.trace[kBlkTraceE1Comb], static_cast<unsigned long long>(e1_comb));
       atomicAdd(&L.trace[kBlkTraceE1Store], static_cast<unsigned long long>(e1_store));
+      atomicAdd(&L.trace[kBlkTraceE1Fence], static_cast<unsigned long long>(e1_fence));
     }
   } else {
     // ------------------------------ conv2 epilogue (warps 10-17) --------------

@@ -27,7 +27,7 @@ struct BlkLaunch {
 };
 enum : int {
   kBlkTraceProd = 0, kBlkTraceM1In, kBlkTraceM1Acc, kBlkTraceM2In, kBlkTraceM2Acc, kBlkTraceE1Full, kBlkTraceE1W,
-  kBlkTraceE2Full, kBlkTraceTiles, kBlkTraceTotal, kBlkTraceRelu, kBlkTraceN
+  kBlkTraceE2Full, kBlkTraceTiles, kBlkTraceTotal, kBlkTraceRelu, kBlkTraceE1Fence, kBlkTraceN
 };
 // slots 12..15: CTA window (sm100.cuh trace_cta_window); 16..21: epilogue phases (TMEM drain, combine, store)
 enum : int { kBlkTraceE1Drain = 16, kBlkTraceE1Comb, kBlkTraceE1Store, kBlkTraceE2Drain, kBlkTraceE2Comb,
