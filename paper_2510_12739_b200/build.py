@@ -46,9 +46,14 @@ def flags(verbose_ptxas: bool = False):
     return f + extra.split()
 
 
+# per-source flags: the fp32 node kernels replay the reference's separately rounded products and sums;
+# ptxas must not contract packed mul/add pairs into FFMA2
+SOURCE_FLAGS = {"generic_f32.cu": ["-fmad=false"]}
+
+
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
-    cmd = [nvcc()] + flags(verbose) + ["-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [nvcc()] + flags(verbose) + SOURCE_FLAGS.get(src, []) + ["-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

@@ -10,6 +10,8 @@
 // single-consumer BN / ReLU / add|mul chain that follows it without changing any rounding.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace cnrx {
@@ -85,6 +87,141 @@ __global__ void __launch_bounds__(128) conv_f32_kernel(const ConvF32 p) {
     if (p.other_op == 6) v = __fadd_rn(v, orow[c]);
     if (p.other_op == 7) v = __fmul_rn(v, orow[c]);
     yr[c] = v;
+  }
+}
+
+// Packed fp32 pairs, each lane rounded separately (inline PTX: the __fmul2_rn / __fadd2_rn intrinsics
+// were contracted into FFMA2 by the compiler, which would change the reference's rounding).
+__device__ __forceinline__ float2 mul2_rn(float2 a, float2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+  return *reinterpret_cast<const float2*>(&r);
+}
+__device__ __forceinline__ float2 add2_rn(float2 a, float2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+  return *reinterpret_cast<const float2*>(&r);
+}
+
+// Same arithmetic (per output: bias, then taps in (dt, df) order, then input channels, separately
+// rounded products and sums, out-of-range taps skipped), PX horizontally adjacent output pixels per
+// thread, so every weight read from shared memory feeds PX x 16 products instead of 16.
+template <int PX>
+__global__ void __launch_bounds__(128) conv_f32_px_kernel(const ConvF32 p) {
+  extern __shared__ float sw[];  // [kh*kw][cin][kCot]
+  const int co0 = blockIdx.y * kCot;
+  const int ncot = min(kCot, p.cout - co0);
+  const int taps = p.kh * p.kw;
+  for (int i = threadIdx.x; i < taps * p.cin * kCot; i += blockDim.x) {
+    const int co = i % kCot;
+    const int tci = i / kCot;
+    sw[i] = co < ncot ? p.w[static_cast<int64_t>(tci) * p.cout + co0 + co] : 0.f;
+  }
+  __syncthreads();
+  const int64_t npix = static_cast<int64_t>(p.B) * p.T * p.F;
+  const int64_t pix0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * PX;
+  if (pix0 >= npix) return;
+  int fk[PX], tk[PX];
+  int64_t bk[PX];
+  bool live[PX];
+#pragma unroll
+  for (int k = 0; k < PX; ++k) {
+    const int64_t pix = pix0 + k;
+    live[k] = pix < npix;
+    fk[k] = static_cast<int>(pix % p.F);
+    tk[k] = static_cast<int>((pix / p.F) % p.T);
+    bk[k] = pix / (static_cast<int64_t>(p.F) * p.T);
+  }
+  float acc[PX][kCot];
+#pragma unroll
+  for (int k = 0; k < PX; ++k)
+#pragma unroll
+    for (int c = 0; c < kCot; ++c) acc[k][c] = (p.bias && c < ncot) ? p.bias[co0 + c] : 0.f;
+  const int oh = p.kh / 2, ow = p.kw / 2;
+  for (int dt = 0; dt < p.kh; ++dt) {
+    for (int df = 0; df < p.kw; ++df) {
+      const float* xr[PX];
+      bool ok[PX];
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < PX; ++k) {
+        const int ti = tk[k] + dt - oh, fi = fk[k] + (df - ow) * p.dil_f;
+        ok[k] = live[k] && ti >= 0 && ti < p.T && fi >= 0 && fi < p.F;
+        xr[k] = p.x + ((bk[k] * p.T + (ok[k] ? ti : 0)) * p.F + (ok[k] ? fi : 0)) * p.cin;
+        any |= ok[k];
+      }
+      if (!any) continue;
+      const float* wt = sw + (dt * p.kw + df) * p.cin * kCot;
+      int ci = 0;
+      if ((p.cin & 3) == 0) {
+        for (; ci < p.cin; ci += 4) {
+          float4 xv[PX];
+#pragma unroll
+          for (int k = 0; k < PX; ++k) xv[k] = ok[k] ? *reinterpret_cast<const float4*>(xr[k] + ci) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4* w4 = reinterpret_cast<const float4*>(wt + (ci + u) * kCot);
+            float4 wv[kCot / 4];
+#pragma unroll
+            for (int q = 0; q < kCot / 4; ++q) wv[q] = w4[q];
+            if (PX == 2 && ok[0] && ok[1]) {
+              // both pixels: packed pairs (FMUL2 / FADD2: two separately rounded fp32 ops per lane)
+              const float2 xs = u == 0 ? make_float2(xv[0].x, xv[1].x) : u == 1 ? make_float2(xv[0].y, xv[1].y)
+                              : u == 2 ? make_float2(xv[0].z, xv[1].z) : make_float2(xv[0].w, xv[1].w);
+#pragma unroll
+              for (int q = 0; q < kCot / 4; ++q) {
+                const float wq[4] = {wv[q].x, wv[q].y, wv[q].z, wv[q].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 m = mul2_rn(xs, make_float2(wq[e], wq[e]));
+                  acc[0][4 * q + e] = __fadd_rn(acc[0][4 * q + e], m.x);
+                  acc[PX - 1][4 * q + e] = __fadd_rn(acc[PX - 1][4 * q + e], m.y);
+                }
+              }
+              continue;
+            }
+#pragma unroll
+            for (int k = 0; k < PX; ++k) {
+              if (!ok[k]) continue;
+              const float xs = u == 0 ? xv[k].x : u == 1 ? xv[k].y : u == 2 ? xv[k].z : xv[k].w;
+#pragma unroll
+              for (int q = 0; q < kCot / 4; ++q) {
+                acc[k][4 * q + 0] = __fadd_rn(acc[k][4 * q + 0], __fmul_rn(xs, wv[q].x));
+                acc[k][4 * q + 1] = __fadd_rn(acc[k][4 * q + 1], __fmul_rn(xs, wv[q].y));
+                acc[k][4 * q + 2] = __fadd_rn(acc[k][4 * q + 2], __fmul_rn(xs, wv[q].z));
+                acc[k][4 * q + 3] = __fadd_rn(acc[k][4 * q + 3], __fmul_rn(xs, wv[q].w));
+              }
+            }
+          }
+        }
+      }
+      for (; ci < p.cin; ++ci) {
+#pragma unroll
+        for (int k = 0; k < PX; ++k) {
+          if (!ok[k]) continue;
+          const float xv = xr[k][ci];
+#pragma unroll
+          for (int c = 0; c < kCot; ++c) acc[k][c] = __fadd_rn(acc[k][c], __fmul_rn(xv, wt[ci * kCot + c]));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < PX; ++k) {
+    if (!live[k]) continue;
+    const int64_t pix = pix0 + k;
+    float* yr = p.y + pix * p.cout + co0;
+    const float* orow = p.other ? p.other + pix * p.cout + co0 : nullptr;
+#pragma unroll
+    for (int c = 0; c < kCot; ++c) {
+      if (c >= ncot) break;
+      float v = acc[k][c];
+      if (p.aff_s) v = __fadd_rn(__fmul_rn(v, p.aff_s[co0 + c]), p.aff_t[co0 + c]);
+      if (p.relu) v = v > 0.f ? v : 0.f;
+      if (p.other_op == 6) v = __fadd_rn(v, orow[c]);
+      if (p.other_op == 7) v = __fmul_rn(v, orow[c]);
+      yr[c] = v;
+    }
   }
 }
 
@@ -173,6 +310,14 @@ const char* launch_conv_f32(const ConvF32& p, cudaStream_t s) {
   const size_t smem = sizeof(float) * p.kh * p.kw * p.cin * kCot;
   if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(conv_f32_kernel), static_cast<int>(smem));
   require(smem <= 227 * 1024, "fp32 conv weights tile exceeds shared memory");
+  static const int px = std::getenv("CNRX_F32_PX") ? std::atoi(std::getenv("CNRX_F32_PX")) : 2;
+  if (px == 2 && npix >= 2 * 148 * 128) {
+    if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(conv_f32_px_kernel<2>), static_cast<int>(smem));
+    dim3 grid2(nblk((npix + 1) / 2, 128), static_cast<unsigned>((p.cout + kCot - 1) / kCot));
+    conv_f32_px_kernel<2><<<grid2, 128, smem, s>>>(p);
+    CNRX_CUDA(cudaGetLastError());
+    return "conv_f32_px_kernel<2>";
+  }
   dim3 grid(nblk(npix, 128), static_cast<unsigned>((p.cout + kCot - 1) / kCot));
   conv_f32_kernel<<<grid, 128, smem, s>>>(p);
   CNRX_CUDA(cudaGetLastError());

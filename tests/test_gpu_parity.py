@@ -105,8 +105,10 @@ def test_bf16_matches_reference_golden(name, wseed):
 # ------------------------------------------------------------------------------------------------
 # live oracle comparisons: configs, shapes, ragged edges
 # ------------------------------------------------------------------------------------------------
+# the last two cases are large enough (>= 2 x 148 x 128 pixels) for the two-pixels-per-thread fp32 conv
+# (packed products), one with an odd F so thread pixel pairs straddle frequency columns
 @pytest.mark.parametrize("name,B,F", [("cfg1", 3, 72), ("cfg2", 2, 37), ("cfg2", 1, 612), ("cfg4", 2, 29), ("cfg4m", 1, 33),
-                                      ("cfg3", 1, 40)])
+                                      ("cfg3", 1, 40), ("cfg2", 5, 612), ("cfg1", 39, 71)])
 def test_fp32_vs_oracle(name, B, F):
     g = G.CONFIGS[name].graph(seed=7)
     x = np.random.default_rng(B * F).standard_normal((B, 14, F, g.in_channels)).astype(np.float32)
