@@ -164,32 +164,36 @@ __global__ void __launch_bounds__(128) conv_f32_px_kernel(const ConvF32 p) {
             float4 wv[kCot / 4];
 #pragma unroll
             for (int q = 0; q < kCot / 4; ++q) wv[q] = w4[q];
-            if (PX == 2 && ok[0] && ok[1]) {
-              // both pixels: packed pairs (FMUL2 / FADD2: two separately rounded fp32 ops per lane)
-              const float2 xs = u == 0 ? make_float2(xv[0].x, xv[1].x) : u == 1 ? make_float2(xv[0].y, xv[1].y)
-                              : u == 2 ? make_float2(xv[0].z, xv[1].z) : make_float2(xv[0].w, xv[1].w);
+            // pixel pairs (k, k+1) with both taps in range: packed products (FMUL2), scalar sums
 #pragma unroll
-              for (int q = 0; q < kCot / 4; ++q) {
-                const float wq[4] = {wv[q].x, wv[q].y, wv[q].z, wv[q].w};
+            for (int k = 0; k < PX; k += 2) {
+              const float x0 = u == 0 ? xv[k].x : u == 1 ? xv[k].y : u == 2 ? xv[k].z : xv[k].w;
+              const float x1 = u == 0 ? xv[k + 1].x : u == 1 ? xv[k + 1].y : u == 2 ? xv[k + 1].z : xv[k + 1].w;
+              if (ok[k] && ok[k + 1]) {
+                const float2 xs = make_float2(x0, x1);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 m = mul2_rn(xs, make_float2(wq[e], wq[e]));
-                  acc[0][4 * q + e] = __fadd_rn(acc[0][4 * q + e], m.x);
-                  acc[PX - 1][4 * q + e] = __fadd_rn(acc[PX - 1][4 * q + e], m.y);
+                for (int q = 0; q < kCot / 4; ++q) {
+                  const float wq[4] = {wv[q].x, wv[q].y, wv[q].z, wv[q].w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 m = mul2_rn(xs, make_float2(wq[e], wq[e]));
+                    acc[k][4 * q + e] = __fadd_rn(acc[k][4 * q + e], m.x);
+                    acc[k + 1][4 * q + e] = __fadd_rn(acc[k + 1][4 * q + e], m.y);
+                  }
                 }
-              }
-              continue;
-            }
+              } else {
 #pragma unroll
-            for (int k = 0; k < PX; ++k) {
-              if (!ok[k]) continue;
-              const float xs = u == 0 ? xv[k].x : u == 1 ? xv[k].y : u == 2 ? xv[k].z : xv[k].w;
+                for (int kk = 0; kk < 2; ++kk) {
+                  if (!ok[k + kk]) continue;
+                  const float xs = kk == 0 ? x0 : x1;
 #pragma unroll
-              for (int q = 0; q < kCot / 4; ++q) {
-                acc[k][4 * q + 0] = __fadd_rn(acc[k][4 * q + 0], __fmul_rn(xs, wv[q].x));
-                acc[k][4 * q + 1] = __fadd_rn(acc[k][4 * q + 1], __fmul_rn(xs, wv[q].y));
-                acc[k][4 * q + 2] = __fadd_rn(acc[k][4 * q + 2], __fmul_rn(xs, wv[q].z));
-                acc[k][4 * q + 3] = __fadd_rn(acc[k][4 * q + 3], __fmul_rn(xs, wv[q].w));
+                  for (int q = 0; q < kCot / 4; ++q) {
+                    acc[k + kk][4 * q + 0] = __fadd_rn(acc[k + kk][4 * q + 0], __fmul_rn(xs, wv[q].x));
+                    acc[k + kk][4 * q + 1] = __fadd_rn(acc[k + kk][4 * q + 1], __fmul_rn(xs, wv[q].y));
+                    acc[k + kk][4 * q + 2] = __fadd_rn(acc[k + kk][4 * q + 2], __fmul_rn(xs, wv[q].z));
+                    acc[k + kk][4 * q + 3] = __fadd_rn(acc[k + kk][4 * q + 3], __fmul_rn(xs, wv[q].w));
+                  }
+                }
               }
             }
           }
@@ -311,7 +315,14 @@ const char* launch_conv_f32(const ConvF32& p, cudaStream_t s) {
   if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(conv_f32_kernel), static_cast<int>(smem));
   require(smem <= 227 * 1024, "fp32 conv weights tile exceeds shared memory");
   static const int px = std::getenv("CNRX_F32_PX") ? std::atoi(std::getenv("CNRX_F32_PX")) : 2;
-  if (px == 2 && npix >= 2 * 148 * 128) {
+  if (px == 4 && npix >= 4 * 148 * 128) {
+    if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(conv_f32_px_kernel<4>), static_cast<int>(smem));
+    dim3 grid4(nblk((npix + 3) / 4, 128), static_cast<unsigned>((p.cout + kCot - 1) / kCot));
+    conv_f32_px_kernel<4><<<grid4, 128, smem, s>>>(p);
+    CNRX_CUDA(cudaGetLastError());
+    return "conv_f32_px_kernel<4>";
+  }
+  if (px >= 2 && npix >= 2 * 148 * 128) {
     if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(conv_f32_px_kernel<2>), static_cast<int>(smem));
     dim3 grid2(nblk((npix + 1) / 2, 128), static_cast<unsigned>((p.cout + kCot - 1) / kCot));
     conv_f32_px_kernel<2><<<grid2, 128, smem, s>>>(p);
