@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "head.h"
@@ -350,8 +351,12 @@ const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const
   L.head_w = prog.head_w;
   L.head_b = prog.head_b;
   L.llr = prog.llr;
-  int stages = 3;
-  while (stages > 2 && head_layout(C, ns, nb, stages).total > 113u * 1024u) --stages;
+  // CNRX_HEAD_STAGES (experiments): ring depth; deeper rings fit one CTA per SM instead of two
+  static const int want = std::getenv("CNRX_HEAD_STAGES") ? std::atoi(std::getenv("CNRX_HEAD_STAGES")) : 0;
+  int stages = want >= 2 ? want : 3;
+  if (want < 2)
+    while (stages > 2 && head_layout(C, ns, nb, stages).total > 113u * 1024u) --stages;
+  while (stages > 2 && head_layout(C, ns, nb, stages).total > 227u * 1024u) --stages;
   L.stages = stages;
   const int total = static_cast<int>(head_layout(C, ns, nb, stages).total);
   if (total > 227 * 1024) return nullptr;
