@@ -136,9 +136,9 @@ __device__ __forceinline__ void combine_chunk(const uint32_t (&a)[16], uint32_t 
       y0 = fmaxf(y0, 0.f);
       y1 = fmaxf(y1, 0.f);
     }
-    const int rb = 8 * i + 2 * t0;
-    if (!((vm >> rb) & 1u)) y0 = 0.f;
-    if (!((vm >> (rb + 1)) & 1u)) y1 = 0.f;
+    // vm is pre-shifted by 2 * t0 (caller): this thread's rows 8i + 2t0 (+1) are bits 8i (+1)
+    if (!((vm >> (8 * i)) & 1u)) y0 = 0.f;
+    if (!((vm >> (8 * i + 1)) & 1u)) y1 = 0.f;
     const __nv_bfloat162 ob = __floats2bfloat162_rn(y0, y1);
     o[i] = *reinterpret_cast<const uint32_t*>(&ob);
   }
@@ -417,8 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       if (lane == 0) mbar_arrive(t1empty);
       const long long t2 = tr ? clock64() : 0;
       uint32_t o[2][4];
-      combine_chunk<false, true>(a0, xb, 0, bias[0], nullptr, vm, lane, o[0]);
-      combine_chunk<false, true>(a1, xb, 1, bias[1], nullptr, vm, lane, o[1]);
+      combine_chunk<false, true>(a0, xb, 0, bias[0], nullptr, vm >> (2 * (lane & 3)), lane, o[0]);
+      combine_chunk<false, true>(a1, xb, 1, bias[1], nullptr, vm >> (2 * (lane & 3)), lane, o[1]);
       if (tr) {
         asm volatile("" ::"r"(o[0][0]), "r"(o[1][3]));  // time the combine, not a sunk copy of it
         const long long t3 = clock64();
@@ -514,8 +514,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       if (lane == 0) mbar_arrive(t2empty);
       const long long t2 = tr ? clock64() : 0;
       uint32_t o[2][4];
-      combine_chunk<true, false>(a0, xb, 0, bias[0], res[0], vm, lane, o[0]);
-      combine_chunk<true, false>(a1, xb, 1, bias[1], res[1], vm, lane, o[1]);
+      combine_chunk<true, false>(a0, xb, 0, bias[0], res[0], vm >> (2 * (lane & 3)), lane, o[0]);
+      combine_chunk<true, false>(a1, xb, 1, bias[1], res[1], vm >> (2 * (lane & 3)), lane, o[1]);
       long long t3 = 0;
       if (tr) {
         asm volatile("" ::"r"(o[0][0]), "r"(o[1][3]));
