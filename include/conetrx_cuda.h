@@ -50,10 +50,16 @@ extern "C" {
 #define CNRX_MODE_TRAIN 0
 #define CNRX_MODE_EVAL 1
 
-/* Arithmetic of the compiled plan. FP32: CUDA-core fp32 kernels, LLRs within 1e-4 relative of the
- * reference.  BF16: bf16 weights/activations with fp32 accumulation on tcgen05 tensor cores. */
+/* Arithmetic of the compiled plan.
+ *   FP32: CUDA-core fp32 kernels, bit-exact with the reference's float operations.
+ *   BF16: bf16 weights/activations with fp32 accumulation on tcgen05 tensor cores (BASELINE's
+ *         tensor-core configuration).
+ *   FP16: the same tensor-core plan with fp16 weights/activations (11-bit mantissa, |x| <= 65504,
+ *         saturating) and an fp32 LLR head: same speed and bytes as BF16, and the mixed-precision
+ *         option that meets the >= 99.99 % hard-decision agreement with the reference. */
 #define CNRX_FP32 0
 #define CNRX_BF16 1
+#define CNRX_FP16 2
 
 /* GraphNode (network.hpp:19-26) + dilation_f (extension for BASELINE config 3; 1 = reference). */
 typedef struct {
@@ -78,6 +84,41 @@ typedef struct cnrx_plan cnrx_plan;
 int cnrx_plan_create(const cnrx_node* nodes, int32_t n_nodes, int32_t input_node, int32_t output_node,
                      const cnrx_param* params, int32_t n_params, const uint8_t* bn_ready, int32_t n_bn,
                      int32_t precision, int32_t device, cnrx_plan** out);
+
+/* Lowering / execution choices of a plan.  Every choice gives identical LLRs except where noted; they
+ * exist for A/B measurements.  cnrx_plan_create uses cnrx_plan_options_default() and then lets the
+ * CNRX_* environment variables of DESIGN.md §7 override it (A/B testing only); cnrx_plan_create_ex uses
+ * exactly the options passed (NULL = defaults, no environment). */
+typedef struct {
+  int32_t struct_size;          /* sizeof(cnrx_plan_options): checked for ABI compatibility */
+  int32_t fused_blocks;         /* 1: residual blocks of two 64-ch 3x3 convs run as one kernel (default);
+                                   0: two weights-stationary conv kernels (env CNRX_BLK=0) */
+  int32_t fused_head;           /* 1: interaction + head in the last convs' epilogue on the two-kernel
+                                   program (BF16 only; env CNRX_HEADFUSE=1); 0 (default): head kernel */
+  int32_t tensor_core_head;     /* 1 (default): 64-ch BF16 heads run their GEMV on the tensor core over
+                                   bf16-rounded z; 0: fp32 CUDA-core GEMV (env CNRX_NO_TMA_HEAD) --
+                                   changes BF16 LLRs by one rounding point; FP16 plans always use fp32 */
+  int32_t cta_pair;             /* 1 (default): 96->96 3x3 convs on CTA pairs (cta_group::2); 0: single
+                                   CTA (env CNRX_NO_PAIR=1) */
+  int32_t weights_stationary;   /* 1 (default): 64->64 3x3 convs with the weights in TMEM; 0: the generic
+                                   SS kernel (env CNRX_NO_WS) */
+  int32_t relu_on_load;         /* 1 (default): a conv whose input is relu(v) applies it to its shared-
+                                   memory window; 0: the producer writes a pre-activated plane
+                                   (env CNRX_NO_RELU_IN) */
+  int32_t cuda_core_stem;       /* 1: 1x1 stems on the network input run fused with featurize on CUDA
+                                   cores in fp32 (env CNRX_STEM=1); 0 (default): tensor-core 1x1 conv --
+                                   changes LLRs by the feature / stem-weight rounding */
+  int32_t pipeline_chunks;      /* host-buffer entry points: batch chunks overlapping H2D / compute /
+                                   D2H; 0 (default) = auto (env CNRX_PIPELINE_CHUNKS) */
+  float pipeline_taper;         /* first / last chunk size relative to the others; default 0.125
+                                   (env CNRX_PIPELINE_TAPER) */
+} cnrx_plan_options;
+void cnrx_plan_options_default(cnrx_plan_options* opt);
+int cnrx_plan_create_ex(const cnrx_node* nodes, int32_t n_nodes, int32_t input_node, int32_t output_node,
+                        const cnrx_param* params, int32_t n_params, const uint8_t* bn_ready, int32_t n_bn,
+                        int32_t precision, int32_t device, const cnrx_plan_options* options, cnrx_plan** out);
+/* The options a plan was compiled with. */
+int cnrx_get_plan_options(const cnrx_plan* plan, cnrx_plan_options* opt);
 void cnrx_plan_destroy(cnrx_plan* plan);
 
 /* Thread-local message for the last non-zero status on this thread. */

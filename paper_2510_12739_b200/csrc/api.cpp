@@ -8,6 +8,8 @@
 //              kernel (generic_f32.cu); a conv absorbs the single-consumer BN / ReLU / add|mul chain
 //              after it.  Any graph the reference builders produce runs on this path.
 //   CNRX_BF16  lowering onto tcgen05 implicit-GEMM convolutions over bf16 activation planes
+//   CNRX_FP16  (the same lowering over fp16 planes / weights, fp32 LLR head; everything below that says
+//              "bf16 plan" applies to both 16-bit formats)
 //              (conv_tc.cu): BN after a conv is folded into its weights, ReLU / residual add / the next
 //              block's pre-activation go into the conv epilogue, same-level convs of different
 //              subnetworks share one grouped launch, and the fusion tail + 1x1 head is a single
@@ -204,6 +206,8 @@ struct Workspace {
 
 struct cnrx_plan {
   int precision = CNRX_FP32;
+  bool fp16 = false;           // CNRX_FP16: the 16-bit planes and weights are fp16
+  cnrx_plan_options opt{};
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
@@ -692,8 +696,7 @@ struct Bf16Compiler {
   // (half the launches: B = 1 latency -21 %) and not for large ones, so ensure_workspace picks the
   // program per batch (blocks_fused); CNRX_BLK=0 disables the fused form, CNRX_BLK=1 forces it.
   void fuse_blocks() {
-    const char* e = getenv("CNRX_BLK");
-    if (e && atoi(e) == 0) return;
+    if (p.opt.fused_blocks == 0) return;
     std::vector<int> readers(p.planes.size(), 0);
     for (const auto& op : p.tc) {
       if (op.in_plane >= 0) ++readers[static_cast<size_t>(op.in_plane)];
@@ -721,9 +724,10 @@ struct Bf16Compiler {
   // weights-stationary conv (residual epilogue, no other reader), all in one launch group.  The
   // two-kernel program then skips the head kernel; the fused-block program (small batches) keeps it.
   // Both compute z the same way and run the same head UMMAs, so their LLRs are identical.
-  // Opt-in while it is slower than conv + head kernel (CNRX_HEADFUSE=1; CNRX_NO_HEADFUSE=1 wins; read per plan).
+  // Opt-in while it is slower than conv + head kernel (cnrx_plan_options::fused_head; bf16 plans only:
+  // the fused epilogue runs the head on the tensor core over 16-bit z).
   void fuse_head() {
-    if (!getenv("CNRX_HEADFUSE") || getenv("CNRX_NO_HEADFUSE") || getenv("CNRX_NO_TMA_HEAD")) return;
+    if (p.opt.fused_head != 1 || p.fp16 || p.opt.tensor_core_head == 0) return;
     const int hk = static_cast<int>(p.pw.size()) - 1;
     if (hk < 0) return;
     const PwStep& hs = p.pw[static_cast<size_t>(hk)];
@@ -799,13 +803,13 @@ struct Bf16Compiler {
       // relu(v) feeding a 64->64 3x3 conv: the weights-stationary kernel applies the ReLU to its input
       // window in shared memory, so v's producer need not store a second, pre-activated plane
       // (relu commutes with the bf16 rounding: identical values).
-      static const bool no_relu_in = getenv("CNRX_NO_RELU_IN") != nullptr;
+      const bool no_relu_in = p.opt.relu_on_load == 0;
       {
         const cnrx_node& in = p.N(nd.in0);
         const int v = in.op == CNRX_OP_RELU ? in.in0 : -1;
         if (!no_relu_in && v >= 0 && node_plane[static_cast<size_t>(nd.in0)] < 0 && node_plane[static_cast<size_t>(v)] >= 0 &&
             !p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].nonneg && op.ks == 3 && w.dims[2] == 64 &&
-            w.dims[3] == 64 && p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].C == 64 && !getenv("CNRX_NO_WS")) {
+            w.dims[3] == 64 && p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].C == 64 && p.opt.weights_stationary) {
           op.relu_in = 1;
           op.in_plane = node_plane[static_cast<size_t>(v)];
         } else {
@@ -859,17 +863,16 @@ struct Bf16Compiler {
       use(op.in_plane, op.level);
       if (op.res_plane >= 0) use(op.res_plane, op.level);
       // weights (BN scale folded per output channel) and bias
-      static const bool no_ws = getenv("CNRX_NO_WS") != nullptr;
-      op.ws = !no_ws && op.ks == 3 && op.cin_real == 64 && op.cout_real == 64 && op.cin == 64 && op.cout == 64;
+      op.ws = p.opt.weights_stationary != 0 && op.ks == 3 && op.cin_real == 64 && op.cout_real == 64 && op.cin == 64 && op.cout == 64;
       if (op.relu_in && !op.ws) throw Error(CNRX_ERR_UNSUPPORTED, "internal: relu-on-load needs the ws conv kernel");
       if (op.ws) {
         std::vector<uint32_t> img(conv_ws64_wimg_bytes() / 4);
-        conv_ws64_pack_weights(w.data.data(), scale.empty() ? nullptr : scale.data(), img.data());
+        conv_ws64_pack_weights(w.data.data(), scale.empty() ? nullptr : scale.data(), p.fp16, img.data());
         op.wimg = p.upload_bytes(img.data(), img.size() * 4);
       } else {
         std::vector<uint8_t> img(conv_tc_wimg_bytes(op.cin, op.cout, op.ks));
         conv_tc_pack_weights(w.data.data(), op.ks, static_cast<int>(w.dims[2]), static_cast<int>(w.dims[3]),
-                             scale.empty() ? nullptr : scale.data(), op.cin, op.cout, img.data());
+                             scale.empty() ? nullptr : scale.data(), op.cin, op.cout, p.fp16, img.data());
         op.wimg = p.upload_bytes(img.data(), img.size());
       }
       op.bias = p.upload(bias);
@@ -910,6 +913,7 @@ struct Bf16Compiler {
     std::vector<float> hb(static_cast<size_t>(on.out_channels), 0.f);
     if (on.b >= 0) hb = p.P(on.b).data;
     st.prog.head_bits = on.out_channels;
+    st.prog.tc_head = !p.fp16 && p.opt.tensor_core_head != 0;
     st.prog.head_w = p.upload(wpad);
     st.prog.head_b = p.upload(hb);
     finish_pw(st, aff, C);
@@ -922,9 +926,9 @@ struct Bf16Compiler {
     p.n_levels = maxl + 1;
     p.tc_groups_by_level.assign(static_cast<size_t>(p.n_levels), {});
     p.pw_by_level.assign(static_cast<size_t>(p.n_levels), {});
-    // The CUDA-core fused featurize+stem kernel is opt-in (CNRX_STEM=1): measured slower than
-    // featurize + the tensor-core 1x1 conv at cfg2 sizes (profiles/r01_notes.md).
-    static const bool no_stem = getenv("CNRX_STEM") == nullptr;
+    // The CUDA-core fused featurize+stem kernel is opt-in (cuda_core_stem): measured slower than
+    // featurize + the tensor-core 1x1 conv at cfg2 sizes (profiles/r01_session2_notes.md).
+    const bool no_stem = p.opt.cuda_core_stem == 0;
     for (int k = 0; k < static_cast<int>(p.tc.size()); ++k) {
       TcOp& op = p.tc[static_cast<size_t>(k)];
       if (!no_stem && op.stem_w && static_cast<int>(p.stem_ops.size()) < kStemMaxOps &&
@@ -1054,8 +1058,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
     for (int c : p.buf_channels) {
       void* d = nullptr;
       const size_t bytes = static_cast<size_t>(ws.geo.Nalloc) * c * 2;
-      CNRX_CUDA(cudaMalloc(&d, bytes));
-      CNRX_CUDA(cudaMemset(d, 0, bytes));
+      CNRX_CUDA(cudaMalloc(&d, bytes));  // every producer writes all rows of [0, Nalloc): no clearing needed
       ws.buffers.push_back(d);
     }
   // tensor maps / launch descriptors per TC group
@@ -1063,12 +1066,9 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
     return pl < 0 ? nullptr
                   : static_cast<__nv_bfloat16*>(ws.buffers[static_cast<size_t>(p.planes[static_cast<size_t>(pl)].buffer)]);
   };
-  // fused residual blocks for small batches (or when forced), if every block's window fits
-  bool fused = false;
+  // fused residual blocks (every batch size by default), if every block's window fits
+  bool fused = p.opt.fused_blocks != 0;
   {
-    const char* e = getenv("CNRX_BLK");
-    const int force = e ? atoi(e) : -1;
-    fused = force == 1 || (force != 0 && B <= kBlkAutoMaxBatch);
     for (const auto& op : p.tc)
       if (op.blk_c1 >= 0 && !conv_blk64_supported_halo(ws.geo.T1 * op.dil + 1)) fused = false;
   }
@@ -1093,15 +1093,13 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
         L.ngroups = static_cast<int>(grp.size());
         L.n_tiles = conv_blk64_tiles(ws.geo.Nalloc);
         L.relu_in = p.tc[static_cast<size_t>(op0.blk_c1)].relu_in;
+        L.fp16 = p.fp16;
         // a non-negative input (the stem's ReLU output) also runs the ReLU-copy variant (identity ReLU,
-        // same values): measured ~0.5 % faster for cfg2's first block (CNRX_BLK_NONNEG_RELU=0 disables)
+        // same values): measured ~0.5 % faster for cfg2's first block
         {
-          const char* e = getenv("CNRX_BLK_NONNEG_RELU");
-          const TcOp& c1 = p.tc[static_cast<size_t>(op0.blk_c1)];
           bool nonneg = true;
           for (int k : grp) nonneg = nonneg && p.planes[static_cast<size_t>(p.tc[static_cast<size_t>(p.tc[static_cast<size_t>(k)].blk_c1)].in_plane)].nonneg;
-          if (!L.relu_in && nonneg && !(e && atoi(e) == 0)) L.relu_in = 1;
-          (void)c1;
+          if (!L.relu_in && nonneg) L.relu_in = 1;
         }
         int win_alloc = 0;
         for (size_t gi = 0; gi < grp.size(); ++gi) {
@@ -1119,10 +1117,11 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
         }
         L.win_alloc = win_alloc;
         L.xstages = conv_blk64_xstages(win_alloc, L.relu_in);
-        if (L.xstages == 0) throw Error(CNRX_ERR_UNSUPPORTED, "fused residual block exceeds shared memory (set CNRX_BLK=0)");
+        if (L.xstages == 0) throw Error(CNRX_ERR_UNSUPPORTED, "fused residual block exceeds shared memory (fused_blocks = 0)");
       } else if (op0.ws) {
         WsLaunch& L = GL.wsl;
         std::memset(&L, 0, sizeof(L));
+        L.fp16 = p.fp16;
         L.geo = ws.geo;
         L.ngroups = static_cast<int>(grp.size());
         L.n_tiles = conv_ws64_tiles(ws.geo.Nalloc);
@@ -1157,6 +1156,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
       } else {
         TcLaunch& L = GL.tc;
         std::memset(&L, 0, sizeof(L));
+        L.fp16 = p.fp16;
         L.geo = ws.geo;
         L.ngroups = static_cast<int>(grp.size());
         int win_alloc = 0;
@@ -1188,8 +1188,8 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           if (op.res_plane >= 0) L.flags |= 1;
           if (op.out2_plane >= 0) L.flags |= 2;
         }
-        // 96 -> 96 3x3 convs run on CTA pairs (CNRX_NO_PAIR=1: the single-CTA kernel)
-        const bool no_pair = getenv("CNRX_NO_PAIR") && atoi(getenv("CNRX_NO_PAIR")) != 0;
+        // 96 -> 96 3x3 convs run on CTA pairs (cta_pair = 0: the single-CTA kernel)
+        const bool no_pair = p.opt.cta_pair == 0;
         int max_halo = 0;
         for (int k : grp) max_halo = std::max(max_halo, ws.geo.T1 * p.tc[static_cast<size_t>(k)].dil + 1);
         if (!no_pair && conv_pair96_supported(op0.cin, op0.cout, op0.ks, max_halo)) {
@@ -1282,9 +1282,9 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
   if (p.need_plane0) {
     __nv_bfloat16* in_plane = plane_ptr(0);
     if (input_kind == 0)
-      p.note(launch_pack_plane(in, ws.geo, p.in_ch, in_plane, p.planes[0].C, s), s);
+      p.note(launch_pack_plane(in, ws.geo, p.in_ch, in_plane, p.planes[0].C, p.fp16, s), s);
     else
-      p.note(launch_featurize_plane(in, ws.geo, N, p.pt, in_plane, p.planes[0].C, s), s);
+      p.note(launch_featurize_plane(in, ws.geo, N, p.pt, in_plane, p.planes[0].C, p.fp16, s), s);
   }
   if (!p.stem_ops.empty()) {
     StemLaunch SL;
@@ -1293,6 +1293,7 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
     SL.cin = p.tc[static_cast<size_t>(p.stem_ops[0])].cin_real;
     SL.N = N;
     SL.mode = input_kind;
+    SL.fp16 = p.fp16;
     SL.x = input_kind == 0 ? in : nullptr;
     SL.y = input_kind == 1 ? in : nullptr;
     SL.pt = p.pt;
@@ -1417,6 +1418,7 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
       if (ws.head_fused && k == p.hf_pw) continue;  // ran in the last convs' epilogue
       PwStep& st = p.pw[static_cast<size_t>(k)];
       PwProgram prog = st.prog;
+      prog.fp16 = p.fp16;
       for (int j = 0; j < st.n_planes; ++j) prog.planes[j] = plane_ptr(st.plane_ids[j]);
       if (st.out_plane >= 0)
         prog.out_plane = plane_ptr(st.out_plane);
@@ -1438,6 +1440,8 @@ void check_shape(cnrx_plan& p, int64_t B, int64_t T, int64_t F, int64_t C) {
 void* ensure_dev(void*& buf, size_t& cap, size_t bytes) {
   if (cap < bytes) {
     if (buf) cudaFree(buf);
+    buf = nullptr;  // a failed cudaMalloc must not leave a stale pointer / capacity behind
+    cap = 0;
     CNRX_CUDA(cudaMalloc(&buf, bytes));
     cap = bytes;
   }
@@ -1642,10 +1646,7 @@ namespace {
 // independent, so chunking changes nothing in the results.
 int pipeline_chunks(const cnrx_plan& p, int64_t B) {
   if (p.capture) return 1;  // a captured graph is keyed on its pointers: keep one launch
-  if (const char* e = std::getenv("CNRX_PIPELINE_CHUNKS")) {
-    const int n = std::atoi(e);
-    if (n >= 1) return static_cast<int>(std::min<int64_t>(n, B));
-  }
+  if (p.opt.pipeline_chunks >= 1) return static_cast<int>(std::min<int64_t>(p.opt.pipeline_chunks, B));
   // measured on cfg2 (B=256): 3-4 chunks maximise e2e; more chunks pay each launch's fixed cost again
   return static_cast<int>(std::min<int64_t>(4, std::max<int64_t>(1, B / 48)));
 }
@@ -1681,7 +1682,7 @@ void host_pipeline(cnrx_plan& p, const float* in, size_t in_per_slot, float* out
   // tapered chunks (first and last 1/8 of a middle chunk; measured e2e +1.5 % over half-size): the first upload and the last download are the only
   // copies not hidden behind a chunk's kernels
   // CNRX_PIPELINE_TAPER: size of the first / last chunk relative to the others (0 or 1: no taper)
-  static const double tw = std::getenv("CNRX_PIPELINE_TAPER") ? std::atof(std::getenv("CNRX_PIPELINE_TAPER")) : 0.125;
+  const double tw = p.opt.pipeline_taper;
   const bool taper = tw > 0.0 && tw < 1.0;
   std::vector<int64_t> bounds(static_cast<size_t>(n) + 1, 0);
   const double units = taper && n > 2 ? n - 2.0 + 2.0 * tw : static_cast<double>(n);
@@ -1744,24 +1745,84 @@ extern "C" {
 
 const char* cnrx_last_error(void) { return g_last_error.c_str(); }
 
+void cnrx_plan_options_default(cnrx_plan_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->struct_size = static_cast<int32_t>(sizeof(*o));
+  o->fused_blocks = 1;
+  o->fused_head = 0;
+  o->tensor_core_head = 1;
+  o->cta_pair = 1;
+  o->weights_stationary = 1;
+  o->relu_on_load = 1;
+  o->cuda_core_stem = 0;
+  o->pipeline_chunks = 0;
+  o->pipeline_taper = 0.125f;
+}
+
+namespace {
+// A/B switches of cnrx_plan_create, read once per plan creation.
+void apply_env_options(cnrx_plan_options* o) {
+  auto env_int = [](const char* name, int* v) {
+    const char* e = std::getenv(name);
+    if (e) *v = std::atoi(e);
+    return e != nullptr;
+  };
+  int v = 0;
+  if (env_int("CNRX_BLK", &v)) o->fused_blocks = v != 0;
+  if (std::getenv("CNRX_HEADFUSE")) o->fused_head = 1;
+  if (std::getenv("CNRX_NO_HEADFUSE")) o->fused_head = 0;
+  if (std::getenv("CNRX_NO_TMA_HEAD")) o->tensor_core_head = 0;
+  if (env_int("CNRX_NO_PAIR", &v) && v != 0) o->cta_pair = 0;
+  if (std::getenv("CNRX_NO_WS")) o->weights_stationary = 0;
+  if (std::getenv("CNRX_NO_RELU_IN")) o->relu_on_load = 0;
+  if (std::getenv("CNRX_STEM")) o->cuda_core_stem = 1;
+  if (env_int("CNRX_PIPELINE_CHUNKS", &v) && v >= 1) o->pipeline_chunks = v;
+  if (const char* e = std::getenv("CNRX_PIPELINE_TAPER")) o->pipeline_taper = static_cast<float>(std::atof(e));
+}
+}  // namespace
+
 int cnrx_plan_create(const cnrx_node* nodes, int32_t n_nodes, int32_t input_node, int32_t output_node,
                      const cnrx_param* params, int32_t n_params, const uint8_t* bn_ready, int32_t n_bn,
                      int32_t precision, int32_t device, cnrx_plan** out) {
+  cnrx_plan_options o;
+  cnrx_plan_options_default(&o);
+  apply_env_options(&o);
+  return cnrx_plan_create_ex(nodes, n_nodes, input_node, output_node, params, n_params, bn_ready, n_bn, precision,
+                             device, &o, out);
+}
+
+int cnrx_get_plan_options(const cnrx_plan* plan, cnrx_plan_options* opt) {
+  if (!plan || !opt) return fail(CNRX_ERR_INVALID_ARGUMENT, "null argument");
+  *opt = plan->opt;
+  return CNRX_OK;
+}
+
+int cnrx_plan_create_ex(const cnrx_node* nodes, int32_t n_nodes, int32_t input_node, int32_t output_node,
+                        const cnrx_param* params, int32_t n_params, const uint8_t* bn_ready, int32_t n_bn,
+                        int32_t precision, int32_t device, const cnrx_plan_options* options, cnrx_plan** out) {
   if (!out) return fail(CNRX_ERR_INVALID_ARGUMENT, "null output pointer");
   *out = nullptr;
+  if (options && options->struct_size != static_cast<int32_t>(sizeof(cnrx_plan_options)))
+    return fail(CNRX_ERR_INVALID_ARGUMENT, "cnrx_plan_options.struct_size mismatch (header / library version)");
   auto plan = std::make_unique<cnrx_plan>();
+  if (options)
+    plan->opt = *options;
+  else
+    cnrx_plan_options_default(&plan->opt);
   const int rc = guarded([&] {
     require(nodes && n_nodes > 0, "empty network");
-    require(precision == CNRX_FP32 || precision == CNRX_BF16, "unknown precision");
+    require(precision == CNRX_FP32 || precision == CNRX_BF16 || precision == CNRX_FP16, "unknown precision");
     int ndev = 0;
     CNRX_CUDA(cudaGetDeviceCount(&ndev));
     require(device >= 0 && device < ndev, "no such CUDA device " + std::to_string(device));
     DeviceGuard dg(device);
     cudaDeviceProp prop;
     CNRX_CUDA(cudaGetDeviceProperties(&prop, device));
-    if (precision == CNRX_BF16 && prop.major != 10)
-      throw Error(CNRX_ERR_UNSUPPORTED, "bf16 tcgen05 plan needs an sm_100 (Blackwell) device");
+    if (precision != CNRX_FP32 && prop.major != 10)
+      throw Error(CNRX_ERR_UNSUPPORTED, "bf16 / fp16 tcgen05 plan needs an sm_100 (Blackwell) device");
     plan->precision = precision;
+    plan->fp16 = precision == CNRX_FP16;
     plan->device = device;
     plan->num_sms = prop.multiProcessorCount;
     plan->nodes.assign(nodes, nodes + n_nodes);
@@ -2049,7 +2110,7 @@ int cnrx_get_plan_info(const cnrx_plan* plan, cnrx_plan_info* info) {
   info->macs_per_re = plan->macs;
   info->rows_per_slot = plan->ws.geo.P;
   size_t ws = 0;
-  if (plan->precision == CNRX_BF16) {
+  if (plan->precision != CNRX_FP32) {
     for (int c : plan->buf_channels) ws += static_cast<size_t>(plan->ws.geo.Nalloc) * c * 2;
   } else {
     for (int c : plan->f32_buf_channels) ws += static_cast<size_t>(plan->ws.B) * plan->ws.T * plan->ws.F * c * 4;

@@ -4,7 +4,7 @@
 //     y = conv2(h) + b2 + x
 //
 // i.e. the MRB block of build_net / append_block (reference network.hpp:451-465: ReLU -> C1 -> BN ->
-// ReLU -> C2 -> + skip) over 64-channel bf16 planes, 3x3 "same" convolutions (kernels.hpp:47-91).
+// ReLU -> C2 -> + skip) over 64-channel 16-bit (bf16 or fp16) planes, 3x3 "same" convolutions (kernels.hpp:47-91).
 // The separate-kernel path (conv_ws.cu twice) moves x, h, h, x, y through HBM (4.4 GB per cfg2 block
 // at B = 256, conv2 running at ~87 % of the HBM roofline); here only x in and y out (1.8 GB) remain,
 // and the block is tensor-core bound.
@@ -26,9 +26,9 @@
 //   warp 0        TMA producer: x windows (ring of `xstages`)
 //   warp 1        conv1 UMMA issuer        warp 19   conv2 UMMA issuer
 //   warps 2-9     conv1 epilogue (+ weights -> TMEM at start): TMEM -> combine -> bias, ReLU, zero
-//                 padding rows -> bf16 -> stmatrix into the W windows
+//                 padding rows -> bf16/fp16 -> stmatrix into the W windows
 //   warps 10-17   conv2 epilogue: TMEM -> combine -> bias + residual (ldmatrix from the x window) ->
-//                 bf16 -> staging -> TMA store of 63 rows
+//                 bf16/fp16 -> staging -> TMA store of 63 rows
 //   warps 18, 20  input ReLU (x window -> relu'd copy, the conv1 B operand) when x is not already
 //                 non-negative
 #include <cuda.h>
@@ -39,6 +39,7 @@
 #include <cstring>
 
 #include "conv_blk.h"
+#include "elem16.cuh"
 #include "sm100.cuh"
 
 namespace cnrx {
@@ -91,8 +92,8 @@ __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t byte_in_row) {
 
 // Copy 16-byte chunks [lo, hi) of a window with ReLU applied (both buffers 1024-byte aligned, same row
 // phase, so the 128B swizzle is identical and the copy is chunk for chunk).
+template <bool F16>
 __device__ __forceinline__ void relu_copy(uint32_t src, uint32_t dst, int lo, int hi, int lane) {
-  const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
   for (int c0 = lo; c0 < hi; c0 += 32 * 8) {
     uint4 v[8];
 #pragma unroll
@@ -103,19 +104,20 @@ __device__ __forceinline__ void relu_copy(uint32_t src, uint32_t dst, int lo, in
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int c = c0 + u * 32 + lane;
-      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v[u]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) h[i] = __hmax2(h[i], z);
+      v[u].x = relu2<F16>(v[u].x);
+      v[u].y = relu2<F16>(v[u].y);
+      v[u].z = relu2<F16>(v[u].z);
+      v[u].w = relu2<F16>(v[u].w);
       if (c < hi) sts128(dst + static_cast<uint32_t>(c) * 16u, v[u]);
     }
   }
 }
 
-// Pair-combined accumulator chunk -> four bf16x2 stmatrix fragments (per 8-channel block `blk`).
+// Pair-combined accumulator chunk -> four packed 16-bit stmatrix fragments (per 8-channel block `blk`).
 // Lanes 16k+i / 16k+8+i of the accumulator hold the tap-A / tap-B partial sums of channel 8k+i; output
 // row c = A[c] + B[c+1] (conv_ws.cu).  `xb` is column 32 of this warp's chunk (B of the chunk's last
 // row), `res` the residual fragments (or null), `vm` one validity bit per row of the chunk.
-template <bool RES, bool RELU>
+template <bool RES, bool RELU, bool F16>
 __device__ __forceinline__ void combine_chunk(const uint32_t (&a)[16], uint32_t xb, int blk, float bias,
                                               const uint32_t* res, uint32_t vm, int lane, uint32_t (&o)[4]) {
   const int t0 = lane & 3, ci = lane >> 2;
@@ -128,7 +130,7 @@ __device__ __forceinline__ void combine_chunk(const uint32_t (&a)[16], uint32_t 
     float y0 = __uint_as_float(a[4 * i + 0]) + __uint_as_float(a[4 * i + 3]) + bias;
     float y1 = __uint_as_float(a[4 * i + 1]) + got + bias;
     if (RES) {
-      const float2 rf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&res[i]));
+      const float2 rf = unpack2<F16>(res[i]);
       y0 += rf.x;
       y1 += rf.y;
     }
@@ -139,8 +141,7 @@ __device__ __forceinline__ void combine_chunk(const uint32_t (&a)[16], uint32_t 
     // vm is pre-shifted by 2 * t0 (caller): this thread's rows 8i + 2t0 (+1) are bits 8i (+1)
     if (!((vm >> (8 * i)) & 1u)) y0 = 0.f;
     if (!((vm >> (8 * i + 1)) & 1u)) y1 = 0.f;
-    const __nv_bfloat162 ob = __floats2bfloat162_rn(y0, y1);
-    o[i] = *reinterpret_cast<const uint32_t*>(&ob);
+    o[i] = pack2<F16>(y0, y1);
   }
 }
 
@@ -161,9 +162,9 @@ __device__ __forceinline__ void epi_acc_wait(uint64_t* bar, uint32_t parity) {
     mbar_wait(bar, parity);
 }
 
-template <bool RELU_IN, bool TRACE>
+template <bool RELU_IN, bool TRACE, bool F16>
 __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_constant__ BlkLaunch L) {
-  constexpr uint32_t IDESC = idesc_bf16_f32(128, kN);
+  constexpr uint32_t IDESC = idesc_e16_f32<F16>(128, kN);
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
   const int XS = L.xstages;
@@ -290,13 +291,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
     // warp 1: conv1 of tiles u = 0 .. U-1; kWarpMma2: conv2 of tiles v = 0 .. n_local-1.  Each warp's
     // tcgen05.commit tracks only its own UMMAs.
     const bool c1 = warp == 1;
-    int32_t shift[kPairs];
+    uint32_t shift_b[kPairs];  // byte offset of tap pair p's first window row
 #pragma unroll
     for (int p = 0; p < kPairs; ++p) {
       const int df = p % 3 - 1;
       const int dt = p < 3 ? -1 : 1;
-      shift[p] = halo + dt + df * grp.dil * L.geo.T1;
+      shift_b[p] = static_cast<uint32_t>((halo + dt + df * grp.dil * L.geo.T1) * kRB);
     }
+    // B descriptor: high half constant (SBO, version, 128B swizzle), low half = start address >> 4 | LBO
+    const uint32_t bdesc_hi = static_cast<uint32_t>(make_sdesc(0, 8 * kRB, kSwizzle128, 0) >> 32);
     const uint32_t a_base = tbase + static_cast<uint32_t>(c1 ? 0 : kWCols);
     const uint32_t d_tmem = tbase + static_cast<uint32_t>(c1 ? kAcc1 : kAcc2);
     uint64_t* tfull = c1 ? t1full : t2full;
@@ -336,15 +339,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       }
       tc_fence_after();
       if (elect_one()) {
-        const uint64_t bdesc0 = make_sdesc(src, 8 * kRB, kSwizzle128, 0);
 #pragma unroll
         for (int p = 0; p < kPairs; ++p) {
+          const uint32_t row0 = src + shift_b[p];
 #pragma unroll
-          for (int kk = 0; kk < kKSteps; ++kk) {
-            const uint64_t bd = bdesc0 + static_cast<uint64_t>((shift[p] * kRB + kk * 32) >> 4);
-            umma_bf16_ts(d_tmem, a_base + static_cast<uint32_t>((p * kKSteps + kk) * 8), bd, IDESC,
-                         (p | kk) != 0 ? 1u : 0u);
-          }
+          for (int kk = 0; kk < kKSteps; ++kk)
+            umma_f16_ts_lohi(d_tmem, a_base + static_cast<uint32_t>((p * kKSteps + kk) * 8),
+                             ((row0 + static_cast<uint32_t>(kk * 32)) >> 4) | (1u << 16), bdesc_hi, IDESC,
+                             (p | kk) != 0 ? 1u : 0u);
         }
         if (release) umma_commit(release);
         // halo tiles have no residual reader: their x stage is free once conv1 has read it
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
         mbar_wait(&xfull[s], ph);
         mbar_wait(&xrempty[r2], (static_cast<uint32_t>(u >> 1) & 1u) ^ 1u);
         if (tr) t_w += clock64() - t0;
-        relu_copy(x_a + static_cast<uint32_t>(s) * lay.stage, xr_a + static_cast<uint32_t>(r2) * lay.stage, lo, hi, lane);
+        relu_copy<F16>(x_a + static_cast<uint32_t>(s) * lay.stage, xr_a + static_cast<uint32_t>(r2) * lay.stage, lo, hi, lane);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&xrfull[r2]);
@@ -417,8 +419,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       if (lane == 0) mbar_arrive(t1empty);
       const long long t2 = tr ? clock64() : 0;
       uint32_t o[2][4];
-      combine_chunk<false, true>(a0, xb, 0, bias[0], nullptr, vm >> (2 * (lane & 3)), lane, o[0]);
-      combine_chunk<false, true>(a1, xb, 1, bias[1], nullptr, vm >> (2 * (lane & 3)), lane, o[1]);
+      combine_chunk<false, true, F16>(a0, xb, 0, bias[0], nullptr, vm >> (2 * (lane & 3)), lane, o[0]);
+      combine_chunk<false, true, F16>(a1, xb, 1, bias[1], nullptr, vm >> (2 * (lane & 3)), lane, o[1]);
       if (tr) {
         asm volatile("" ::"r"(o[0][0]), "r"(o[1][3]));  // time the combine, not a sunk copy of it
         const long long t3 = clock64();
@@ -514,8 +516,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       if (lane == 0) mbar_arrive(t2empty);
       const long long t2 = tr ? clock64() : 0;
       uint32_t o[2][4];
-      combine_chunk<true, false>(a0, xb, 0, bias[0], res[0], vm >> (2 * (lane & 3)), lane, o[0]);
-      combine_chunk<true, false>(a1, xb, 1, bias[1], res[1], vm >> (2 * (lane & 3)), lane, o[1]);
+      combine_chunk<true, false, F16>(a0, xb, 0, bias[0], res[0], vm >> (2 * (lane & 3)), lane, o[0]);
+      combine_chunk<true, false, F16>(a1, xb, 1, bias[1], res[1], vm >> (2 * (lane & 3)), lane, o[1]);
       long long t3 = 0;
       if (tr) {
         asm volatile("" ::"r"(o[0][0]), "r"(o[1][3]));
@@ -583,18 +585,21 @@ void make_map(const void* plane, int64_t nalloc, uint32_t box_rows, CUtensorMap*
   if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
-template <bool RELU_IN, bool TRACE>
+template <bool RELU_IN, bool TRACE, bool F16>
 void launch_tt(const BlkLaunch& L, int grid, cudaStream_t stream) {
   const BlkLayout lay = blk_layout(L.xstages, L.win_alloc, RELU_IN);
-  ensure_smem_attr(reinterpret_cast<const void*>(conv_blk64_kernel<RELU_IN, TRACE>), static_cast<int>(lay.total));
-  launch_pdl(conv_blk64_kernel<RELU_IN, TRACE>, dim3(grid), dim3(kThreads), lay.total, stream, L);
+  ensure_smem_attr(reinterpret_cast<const void*>(conv_blk64_kernel<RELU_IN, TRACE, F16>), static_cast<int>(lay.total));
+  launch_pdl(conv_blk64_kernel<RELU_IN, TRACE, F16>, dim3(grid), dim3(kThreads), lay.total, stream, L);
 }
+// the per-role trace counters are a bf16-only debug instantiation
 template <bool RELU_IN>
 void launch_t(const BlkLaunch& L, int grid, cudaStream_t stream) {
-  if (L.trace)
-    launch_tt<RELU_IN, true>(L, grid, stream);
+  if (L.fp16)
+    launch_tt<RELU_IN, false, true>(L, grid, stream);
+  else if (L.trace)
+    launch_tt<RELU_IN, true, false>(L, grid, stream);
   else
-    launch_tt<RELU_IN, false>(L, grid, stream);
+    launch_tt<RELU_IN, false, false>(L, grid, stream);
 }
 
 }  // namespace

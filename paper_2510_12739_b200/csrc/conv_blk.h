@@ -23,6 +23,7 @@ struct BlkLaunch {
   PlaneGeom geo;
   int64_t n_tiles;         // 63-row output tiles
   int32_t ngroups, win_alloc, xstages, relu_in;
+  int32_t fp16;             // planes and weights are fp16 (CNRX_FP16 plans), else bf16
   unsigned long long* trace;  // debug: per-role clock64 totals (kBlkTrace*)
 };
 enum : int {

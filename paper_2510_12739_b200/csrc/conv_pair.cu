@@ -27,6 +27,7 @@
 #include <cstring>
 
 #include "conv_pair.h"
+#include "elem16.cuh"
 #include "sm100.cuh"
 
 namespace cnrx {
@@ -105,7 +106,7 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const void* tmap
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(cluster_bar)
       : "memory");
 }
-__device__ __forceinline__ void umma_bf16_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+__device__ __forceinline__ void umma_f16_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                               uint32_t accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -121,9 +122,10 @@ __device__ __forceinline__ void umma_commit_2sm(uint64_t* bar) {
                : "memory");
 }
 
+template <bool F16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     conv_pair96_kernel(const __grid_constant__ TcLaunch L) {
-  constexpr uint32_t IDESC = idesc_bf16_f32(256, kC);
+  constexpr uint32_t IDESC = idesc_e16_f32<F16>(256, kC);
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
   const bool staged = (L.flags & kPairStaged) != 0;
@@ -271,13 +273,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t b1 = b0 + kHalfN * kRB0;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-              umma_bf16_2sm(d_tmem, make_sdesc(a0 + kk * 32, 8 * kRB0, kSwizzle128, 0),
+              umma_f16_2sm(d_tmem, make_sdesc(a0 + kk * 32, 8 * kRB0, kSwizzle128, 0),
                             make_sdesc(b0 + kk * 32, 8 * kRB0, kSwizzle128, 0), IDESC, acc);
               acc = 1;
             }
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk)
-              umma_bf16_2sm(d_tmem, make_sdesc(a1 + kk * 32, 8 * kRB1, kSwizzle64, 0),
+              umma_f16_2sm(d_tmem, make_sdesc(a1 + kk * 32, 8 * kRB1, kSwizzle64, 0),
                             make_sdesc(b1 + kk * 32, 8 * kRB1, kSwizzle64, 0), IDESC, 1);
           }
           umma_commit_2sm(&empty[s]);  // window stages of both CTAs free
@@ -385,10 +387,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             rv[0] = make_uint4(rres[pc].v[0], rres[pc].v[1], rres[pc].v[2], rres[pc].v[3]);
             rv[1] = make_uint4(rres[pc].v[4], rres[pc].v[5], rres[pc].v[6], rres[pc].v[7]);
           }
-          const __nv_bfloat162* rp = reinterpret_cast<const __nv_bfloat162*>(rv);
+          const uint32_t* rp = reinterpret_cast<const uint32_t*>(rv);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float2 f = __bfloat1622float2(rp[i]);
+            const float2 f = unpack2<F16>(rp[i]);
             v[2 * i] += f.x;
             v[2 * i + 1] += f.y;
           }
@@ -404,8 +406,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         u32x8 o;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-          o.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
+          o.v[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
         }
         if (staged) {
           sts128(rb + off0, make_uint4(o.v[0], o.v[1], o.v[2], o.v[3]));
@@ -419,8 +420,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 8; ++i) {
             const float x0 = fmaxf(v[2 * i] * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
             const float x1 = fmaxf(v[2 * i + 1] * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
-            const __nv_bfloat162 b2 = __floats2bfloat162_rn(valid ? x0 : 0.f, valid ? x1 : 0.f);
-            o2.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
+            o2.v[i] = pack2<F16>(valid ? x0 : 0.f, valid ? x1 : 0.f);
           }
           if (staged) {
             sts128(o2_a + off0, make_uint4(o2.v[0], o2.v[1], o2.v[2], o2.v[3]));
@@ -462,12 +462,13 @@ size_t conv_pair96_smem_bytes(int stages, int win_alloc, bool staged) { return p
 
 const char* conv_pair96_launch(const TcLaunch& L, int num_sms, cudaStream_t stream) {
   const PairLayout lay = pair_layout(L.stages, L.win_alloc, (L.flags & kPairStaged) != 0);
-  ensure_smem_attr(reinterpret_cast<const void*>(conv_pair96_kernel), static_cast<int>(lay.total));
+  auto kern = L.fp16 ? conv_pair96_kernel<true> : conv_pair96_kernel<false>;
+  ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(lay.total));
   const int64_t pair_work = static_cast<int64_t>(L.ngroups) * ((L.geo.n_tiles + 1) / 2);
   int pairs = static_cast<int>(pair_work < num_sms / 2 ? pair_work : num_sms / 2);
   if (pairs < L.ngroups) pairs = L.ngroups;
-  launch_pdl(conv_pair96_kernel, dim3(2 * pairs), dim3(kThreads), lay.total, stream, L);
-  return "conv_pair96_kernel";
+  launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), lay.total, stream, L);
+  return L.fp16 ? "conv_pair96_kernel<f16>" : "conv_pair96_kernel";
 }
 
 }  // namespace cnrx

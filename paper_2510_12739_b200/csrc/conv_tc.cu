@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "conv_tc.h"
+#include "elem16.cuh"
 #include "sm100.cuh"
 
 namespace cnrx {
@@ -86,7 +87,7 @@ __host__ __device__ inline SmemLayout smem_layout(int cin, int cout, int ks, int
 template <int CIN, int COUT, int KS>
 constexpr int min_ctas() { return KS == 1 && CIN <= 32 && COUT <= 64 ? 4 : 1; }
 
-template <int CIN, int COUT, int KS>
+template <int CIN, int COUT, int KS, bool F16>
 __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel(const __grid_constant__ TcLaunch L) {
   constexpr int CH0 = chunk0_ch(CIN), CH1 = chunk1_ch(CIN);
   constexpr int RB0 = CH0 * 2, RB1 = CH1 * 2;
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
   constexpr int TAPS = KS * KS;
   constexpr uint32_t WBYTES = TAPS * COUT * CIN * 2;
   constexpr uint32_t TMEM_COLS = tmem_cols_for(COUT);
-  constexpr uint32_t IDESC = idesc_bf16_f32(128, COUT);
+  constexpr uint32_t IDESC = idesc_e16_f32<F16>(128, COUT);
   constexpr bool STAGED = staged_epi(CIN, COUT);
   constexpr int ORB = COUT * 2;  // output row bytes (staged path: one swizzle chunk)
 
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
           for (int kk = 0; kk < CH0 / 16; ++kk) {
             const uint64_t ad = make_sdesc(a0 + kk * 32, 8 * RB0, SW0, 0);
             const uint64_t bd = make_sdesc(b0 + kk * 32, 8 * RB0, SW0, 0);
-            umma_bf16(d_tmem, ad, bd, IDESC, acc);
+            umma_f16(d_tmem, ad, bd, IDESC, acc);
             acc = 1;
           }
           if (CH1) {
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
             for (int kk = 0; kk < CH1 / 16; ++kk) {
               const uint64_t ad = make_sdesc(a1 + kk * 32, 8 * RB1, SW1, 0);
               const uint64_t bd = make_sdesc(b1 + kk * 32, 8 * RB1, SW1, 0);
-              umma_bf16(d_tmem, ad, bd, IDESC, 1);
+              umma_f16(d_tmem, ad, bd, IDESC, 1);
             }
           }
         }
@@ -311,10 +312,10 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
             for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[v8 * 8 + i]) + s_bias[c0 + i];
             if (rrow) {
               const uint4 rv = *reinterpret_cast<const uint4*>(rrow + swz_offset(ORB, static_cast<uint32_t>(row), chunk));
-              const __nv_bfloat162* rp = reinterpret_cast<const __nv_bfloat162*>(&rv);
+              const uint32_t* rp = reinterpret_cast<const uint32_t*>(&rv);
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
-                const float2 f = __bfloat1622float2(rp[i]);
+                const float2 f = unpack2<F16>(rp[i]);
                 v[2 * i] += f.x;
                 v[2 * i + 1] += f.y;
               }
@@ -330,19 +331,19 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
             const uint32_t so = swz_offset(ORB, static_cast<uint32_t>(lane), chunk);
             {
               uint4 o;
-              __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+              uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-              for (int i = 0; i < 4; ++i) op[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+              for (int i = 0; i < 4; ++i) op[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
               *reinterpret_cast<uint4*>(stg + so) = o;
             }
             if (grp.out2) {
               uint4 o;
-              __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+              uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 const float x0 = fmaxf(v[2 * i] * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
                 const float x1 = fmaxf(v[2 * i + 1] * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
-                op[i] = __floats2bfloat162_rn(valid ? x0 : 0.f, valid ? x1 : 0.f);
+                op[i] = pack2<F16>(valid ? x0 : 0.f, valid ? x1 : 0.f);
               }
               *reinterpret_cast<uint4*>(stg + 32 * ORB + so) = o;
             }
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
               const u32x8& rv = rres[(c0 / 16) < NRES ? c0 / 16 : 0];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.v[i]));
+                const float2 f = unpack2<F16>(rv.v[i]);
                 v[2 * i] += f.x;
                 v[2 * i + 1] += f.y;
               }
@@ -402,8 +403,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
               u32x8 o;
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-                o.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
+                o.v[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
               }
               stg256(orow + c0, o);
             }
@@ -413,8 +413,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
               for (int i = 0; i < 8; ++i) {
                 const float x0 = fmaxf(v[2 * i] * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
                 const float x1 = fmaxf(v[2 * i + 1] * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
-                const __nv_bfloat162 b2 = __floats2bfloat162_rn(valid ? x0 : 0.f, valid ? x1 : 0.f);
-                o.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
+                o.v[i] = pack2<F16>(valid ? x0 : 0.f, valid ? x1 : 0.f);
               }
               stg256(orow2 + c0, o);
             }
@@ -436,9 +435,9 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
   if (warp == 1) tmem_dealloc(tbase, TMEM_COLS);
 }
 
-template <int CIN, int COUT, int KS>
+template <int CIN, int COUT, int KS, bool F16>
 const char* launch_t(const TcLaunch& L, int num_sms, cudaStream_t stream) {
-  auto kern = conv_tc_kernel<CIN, COUT, KS>;
+  auto kern = conv_tc_kernel<CIN, COUT, KS, F16>;
   const SmemLayout lay = smem_layout(CIN, COUT, KS, L.stages, L.win_alloc, L.flags);
   ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(lay.total));
   // Several CTAs per SM when shared memory and TMEM allow (small-K convs, e.g. the 1x1 stem, are
@@ -464,7 +463,7 @@ const char* launch_t(const TcLaunch& L, int num_sms, cudaStream_t stream) {
   if (L.trace) fprintf(stderr, "[trace] conv_tc %d CTAs/SM (regs %d, smem %u B), grid %d\n", per_sm, regs, lay.total, grid);
   launch_pdl(kern, dim3(grid), dim3(192), lay.total, stream, L);
   static char name[96];
-  snprintf(name, sizeof name, "conv_tc_kernel<%d,%d,%d>", CIN, COUT, KS);
+  snprintf(name, sizeof name, "conv_tc_kernel<%d,%d,%d%s>", CIN, COUT, KS, F16 ? ",f16" : "");
   return name;
 }
 
@@ -475,9 +474,9 @@ using LaunchFn = const char* (*)(const TcLaunch&, int, cudaStream_t);
   X(16, 96, 1) X(32, 96, 1) X(64, 96, 1) X(96, 96, 1) X(96, 96, 3) X(16, 128, 1) X(32, 128, 1)             \
   X(64, 128, 1) X(128, 128, 1) X(32, 64, 3) X(64, 32, 3) X(32, 96, 3) X(16, 64, 3) X(16, 96, 3)
 
-LaunchFn find_launch(int cin, int cout, int ks) {
+LaunchFn find_launch(int cin, int cout, int ks, bool h) {
 #define X(a, b, c) \
-  if (cin == a && cout == b && ks == c) return &launch_t<a, b, c>;
+  if (cin == a && cout == b && ks == c) return h ? &launch_t<a, b, c, true> : &launch_t<a, b, c, false>;
   CNRX_TC_CASES(X)
 #undef X
   return nullptr;
@@ -497,7 +496,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
-bool conv_tc_supported(int cin, int cout, int ks) { return find_launch(cin, cout, ks) != nullptr; }
+bool conv_tc_supported(int cin, int cout, int ks) { return find_launch(cin, cout, ks, false) != nullptr; }
 
 bool conv_tc_staged(int cin, int cout) { return staged_epi(cin, cout); }
 
@@ -527,14 +526,14 @@ size_t conv_tc_smem_bytes(int cin, int cout, int ks, int stages, int win_alloc, 
 size_t conv_tc_wimg_bytes(int cin, int cout, int ks) { return static_cast<size_t>(ks) * ks * cout * cin * 2; }
 
 const char* conv_tc_launch(int cin, int cout, int ks, const TcLaunch& L, int num_sms, cudaStream_t stream) {
-  LaunchFn fn = find_launch(cin, cout, ks);
+  LaunchFn fn = find_launch(cin, cout, ks, L.fp16 != 0);
   if (!fn) throw Error(3, "no tcgen05 conv instantiation for cin=" + std::to_string(cin) + " cout=" +
                               std::to_string(cout) + " k=" + std::to_string(ks));
   return fn(L, num_sms, stream);
 }
 
 void conv_tc_pack_weights(const float* w, int ks, int cin_real, int cout_real, const float* scale, int cin,
-                          int cout, uint8_t* img) {
+                          int cout, bool fp16, uint8_t* img) {
   const int ch0 = chunk0_ch(cin), ch1 = chunk1_ch(cin);
   const int rb0 = ch0 * 2, rb1 = ch1 * 2;
   std::memset(img, 0, conv_tc_wimg_bytes(cin, cout, ks));
@@ -548,7 +547,7 @@ void conv_tc_pack_weights(const float* w, int ks, int cin_real, int cout_real, c
           v = w[(static_cast<size_t>(tap) * cin_real + ci) * cout_real + co];
           if (scale) v *= scale[co];
         }
-        const __nv_bfloat16 b = __float2bfloat16(v);
+        const uint16_t b = e16_from_float_host(v, fp16);
         uint8_t* base;
         int rb, k;
         if (ci < ch0) {

@@ -40,6 +40,7 @@ struct TcLaunch {
   int32_t stages;                   // window pipeline depth
   int32_t win_alloc;                // rows allocated per window stage (max over groups, 8-aligned)
   int32_t flags;                    // bit 0: a group has a residual, bit 1: a group writes out2
+  int32_t fp16;                     // planes and weights are fp16 (CNRX_FP16 plans), else bf16
   // debug: when non-null each CTA adds per-role clock64 totals (see kTrace* indices)
   unsigned long long* trace;
 };
@@ -56,9 +57,10 @@ const char* conv_tc_launch(int cin, int cout, int ks, const TcLaunch& L, int num
 // Byte size of the weight image for (cin, cout, ks).
 size_t conv_tc_wimg_bytes(int cin, int cout, int ks);
 // w: fp32 [ks,ks,cin_real,cout_real] (reference layout, kernels.hpp:32), scaled per output channel
-// by `scale` (nullable, folded BN); written as bf16 into `img` (host buffer of conv_tc_wimg_bytes).
+// by `scale` (nullable, folded BN); written as bf16 (fp16 if `fp16`) into `img` (host buffer of
+// conv_tc_wimg_bytes).
 void conv_tc_pack_weights(const float* w, int ks, int cin_real, int cout_real, const float* scale, int cin,
-                          int cout, uint8_t* img);
+                          int cout, bool fp16, uint8_t* img);
 // Tensor maps for the K-chunks (<= 64 + rest channels) of a plane [nalloc][cin] bf16, boxes of
 // `box_rows` rows; a null plane yields zeroed maps.
 void conv_tc_make_maps(const void* plane, int64_t nalloc, int cin, int box_rows, CUtensorMap* maps);

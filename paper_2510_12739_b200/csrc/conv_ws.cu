@@ -50,6 +50,7 @@
 #include "conv_tc.h"
 #include "conv_ws.h"
 #include "kernels.h"
+#include "elem16.cuh"
 #include "sm100.cuh"
 
 namespace cnrx {
@@ -123,8 +124,8 @@ __device__ __forceinline__ void ws_wait_relaxed(uint64_t* bar, uint32_t parity) 
 // In-place ReLU of 16-byte chunks [lo, hi) of a shared-memory window, one warp, batches of 16 chunks per
 // lane so all loads are in flight before the first store (shared-memory latency is long while the
 // tensor core streams the other stages).
+template <bool F16>
 __device__ __forceinline__ void relu_chunks(uint32_t win, int lo, int hi, int lane) {
-  const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
   for (int c0 = lo; c0 < hi; c0 += 32 * 16) {
     uint4 v[16];
 #pragma unroll
@@ -135,17 +136,18 @@ __device__ __forceinline__ void relu_chunks(uint32_t win, int lo, int hi, int la
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int c = c0 + u * 32 + lane;
-      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v[u]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) h[i] = __hmax2(h[i], z);
+      v[u].x = relu2<F16>(v[u].x);
+      v[u].y = relu2<F16>(v[u].y);
+      v[u].z = relu2<F16>(v[u].z);
+      v[u].w = relu2<F16>(v[u].w);
       if (c < hi) sts128(win + static_cast<uint32_t>(c) * 16u, v[u]);
     }
   }
 }
 
-template <int FL>
+template <int FL, bool F16>
 __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_constant__ WsLaunch L) {
-  constexpr uint32_t IDESC = idesc_bf16_f32(128, kN);
+  constexpr uint32_t IDESC = idesc_e16_f32<F16>(128, kN);
   constexpr bool kHead = FL > 0 && (FL & kWsHead) != 0;
   constexpr int kNS = kHead ? (FL >> 6) & 3 : 1;  // fused head: subnetworks (fold operands, cluster size)
   // fused head with the fold shape compiled in (bit 16): bits 8-9 step 1/2 is a product, 10-12 step
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
   auto relu_stage = [&](int jr, int lo, int hi) {
     const int s = jr % L.stages;
     ws_wait_relaxed(&full[s], static_cast<uint32_t>(jr / L.stages) & 1u);
-    if (!(L.debug & 2)) relu_chunks(smem_u32(smem + lay.win_off + s * lay.win_stage), lo, hi, lane);
+    if (!(L.debug & 2)) relu_chunks<F16>(smem_u32(smem + lay.win_off + s * lay.win_stage), lo, hi, lane);
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&ready[s]);
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
 #pragma unroll
           for (int kk = 0; kk < kKSteps; ++kk) {
             const uint64_t bd = bdesc0 + static_cast<uint64_t>((shift[p] * kRB + kk * 32) >> 4);
-            umma_bf16_ts(d_tmem, tbase + static_cast<uint32_t>((p * kKSteps + kk) * 8), bd, IDESC,
+            umma_f16_ts(d_tmem, tbase + static_cast<uint32_t>((p * kKSteps + kk) * 8), bd, IDESC,
                          (p | kk) != 0 ? 1u : 0u);
           }
         }
@@ -472,7 +474,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
           const int ch = 8 * c8 + 2 * pp;
           auto word = [&](int k) {
             const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[k]);
-            return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[pp]));
+            return unpack2<F16>(w[pp]);
           };
           float2 z = word(0);
           auto post = [&](auto kc) {
@@ -497,8 +499,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
           post(std::integral_constant<int, 0>{});
           if constexpr (kNS > 1) step(std::integral_constant<int, 1>{});
           if constexpr (kNS > 2) step(std::integral_constant<int, 2>{});
-          const __nv_bfloat162 zb = __floats2bfloat162_rn(z.x, z.y);
-          zo[pp] = *reinterpret_cast<const uint32_t*>(&zb);
+          zo[pp] = pack2<F16>(z.x, z.y);
         }
         sts128(stg_a + off, make_uint4(zo[0], zo[1], zo[2], zo[3]));
       }
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
             float y0 = __uint_as_float(a[4 * i + 0]) + __uint_as_float(a[4 * i + 3]) + bias[blk];
             float y1 = __uint_as_float(a[4 * i + 1]) + got + bias[blk];
             if (has_res) {
-              const float2 rf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rres[i]));
+              const float2 rf = unpack2<F16>(rres[i]);
               y0 += rf.x;
               y1 += rf.y;
             }
@@ -590,19 +591,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws64_kernel(const __grid_c
             const bool v0 = (vmask[h] >> rb) & 1u, v1 = (vmask[h] >> (rb + 1)) & 1u;
             if (!v0) y0 = 0.f;
             if (!v1) y1 = 0.f;
-            const __nv_bfloat162 ob = __floats2bfloat162_rn(y0, y1);
-            o[i] = *reinterpret_cast<const uint32_t*>(&ob);
+            o[i] = pack2<F16>(y0, y1);
             if (has_out2) {
-              __nv_bfloat162 u;
               if (relu2_only) {
-                u = __hmax2(ob, __float2bfloat162_rn(0.f));
+                o2[i] = relu2<F16>(o[i]);
               } else {
-                const float2 f = __bfloat1622float2(ob);
+                const float2 f = unpack2<F16>(o[i]);
                 const float x0 = fmaxf(f.x * s2v[blk] + t2v[blk], 0.f);
                 const float x1 = fmaxf(f.y * s2v[blk] + t2v[blk], 0.f);
-                u = __floats2bfloat162_rn(v0 ? x0 : 0.f, v1 ? x1 : 0.f);
+                o2[i] = pack2<F16>(v0 ? x0 : 0.f, v1 ? x1 : 0.f);
               }
-              o2[i] = *reinterpret_cast<const uint32_t*>(&u);
             }
           }
           const uint32_t row = static_cast<uint32_t>(64 * H + 32 * h + arow);
@@ -696,7 +694,7 @@ void make_map(const void* plane, int64_t nalloc, uint32_t box_rows, CUtensorMap*
 
 size_t conv_ws64_wimg_bytes() { return static_cast<size_t>(kPairs) * kKSteps * 128 * 8 * 4; }
 
-void conv_ws64_pack_weights(const float* w, const float* scale, uint32_t* img) {
+void conv_ws64_pack_weights(const float* w, const float* scale, bool fp16, uint32_t* img) {
   // w: reference layout [3][3][64][64] = [dt+1][df+1][ci][co]; img: [block = pair*4 + kstep][lane][8 u32]
   std::memset(img, 0, conv_ws64_wimg_bytes());
   for (int p = 0; p < kPairs; ++p) {
@@ -713,9 +711,7 @@ void conv_ws64_pack_weights(const float* w, const float* scale, uint32_t* img) {
             v = w[((static_cast<size_t>(dt + 1) * 3 + (df + 1)) * kC + ci) * kC + co];
             if (scale) v *= scale[co];
           }
-          const __nv_bfloat16 b = __float2bfloat16(v);
-          uint16_t bits;
-          std::memcpy(&bits, &b, 2);
+          const uint16_t bits = e16_from_float_host(v, fp16);
           const int kk = ci / 16, e = ci % 16;
           uint32_t& word = img[((static_cast<size_t>(p) * kKSteps + kk) * 128 + lane) * 8 + e / 2];
           word |= static_cast<uint32_t>(bits) << ((e & 1) * 16);
@@ -748,14 +744,14 @@ int group_flags(const WsGroup& g) {
          (g.relu ? kWsRelu : 0) | (g.relu_in ? kWsReluIn : 0);
 }
 
-template <int FL>
-void launch_fl(const WsLaunch& L, const WsLayout& lay, int grid, cudaStream_t stream) {
-  ensure_smem_attr(reinterpret_cast<const void*>(conv_ws64_kernel<FL>), static_cast<int>(lay.total));
-  launch_pdl(conv_ws64_kernel<FL>, dim3(grid), dim3(kWsThreads), lay.total, stream, L);
+template <int FL, bool F16>
+void launch_flh(const WsLaunch& L, const WsLayout& lay, int grid, cudaStream_t stream) {
+  ensure_smem_attr(reinterpret_cast<const void*>(conv_ws64_kernel<FL, F16>), static_cast<int>(lay.total));
+  launch_pdl(conv_ws64_kernel<FL, F16>, dim3(grid), dim3(kWsThreads), lay.total, stream, L);
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {  // (launch_pdl throws on launch errors; this catches sticky ones)
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, conv_ws64_kernel<FL>);
+    cudaFuncGetAttributes(&fa, conv_ws64_kernel<FL, F16>);
     throw Error(4, std::string("conv_ws64 launch failed: ") + cudaGetErrorString(err) + " (regs " +
                        std::to_string(fa.numRegs) + ", max threads " + std::to_string(fa.maxThreadsPerBlock) +
                        ", static smem " + std::to_string(fa.sharedSizeBytes) + ", dynamic " +
@@ -763,10 +759,19 @@ void launch_fl(const WsLaunch& L, const WsLayout& lay, int grid, cudaStream_t st
   }
 }
 
-// Fused-head launches: clusters of ngroups CTAs (one per subnetwork), as many as can be co-resident.
+template <int FL>
+void launch_fl(const WsLaunch& L, const WsLayout& lay, int grid, cudaStream_t stream) {
+  if (L.fp16)
+    launch_flh<FL, true>(L, lay, grid, stream);
+  else
+    launch_flh<FL, false>(L, lay, grid, stream);
+}
+
+// Fused-head launches (bf16 plans only): clusters of ngroups CTAs (one per subnetwork), as many as can
+// be co-resident.
 template <int FL>
 void launch_head(const WsLaunch& L, const WsLayout& lay, cudaStream_t stream) {
-  auto kern = conv_ws64_kernel<FL>;
+  auto kern = conv_ws64_kernel<FL, false>;
   ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(lay.total));
   static const bool no_pdl = std::getenv("CNRX_NO_PDL") != nullptr;
   cudaLaunchConfig_t cfg{};
@@ -805,6 +810,7 @@ size_t conv_ws64_head_smem_bytes(int stages, int win_alloc) { return ws_layout(s
 
 const char* conv_ws64_launch(const WsLaunch& L, int num_sms, cudaStream_t stream) {
   if (L.head_on) {
+    if (L.fp16) throw Error(4, "internal: the fused-head conv is bf16-only");
     const WsLayout lay = ws_layout(L.stages, L.win_alloc, true);
     for (int i = 0; i < L.ngroups; ++i)
       if (group_flags(L.g[i]) != kWsRes) throw Error(4, "internal: fused-head conv needs residual-only epilogues");
@@ -839,7 +845,7 @@ const char* conv_ws64_launch(const WsLaunch& L, int num_sms, cudaStream_t stream
     case 0: launch_fl<0>(L, lay, grid, stream); break;
     default: launch_fl<kWsDynamic>(L, lay, grid, stream); break;
   }
-  return "conv_ws64_kernel";
+  return L.fp16 ? "conv_ws64_kernel<f16>" : "conv_ws64_kernel";
 }
 
 }  // namespace cnrx

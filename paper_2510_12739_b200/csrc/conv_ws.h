@@ -42,6 +42,7 @@ struct WsLaunch {
   PlaneGeom geo;
   int64_t n_tiles;   // 127-row output tiles
   int32_t ngroups, stages, win_alloc;
+  int32_t fp16;      // planes and weights are fp16 (CNRX_FP16 plans), else bf16
   int32_t debug;     // experiments only (CNRX_WS_DEBUG): bit 0 skip staging writes + stores, bit 1 skip input ReLU pass;
                      // fused head: bit 4 trace rank 1 instead of rank 0, bit 5 skip the head UMMAs, bit 6 skip
                      // the fold pass, bit 7 skip the DSMEM exchange (results invalid with bits 5-7)
@@ -53,7 +54,7 @@ enum : int { kWsTraceLoop = 16, kWsTraceCommit = 17, kWsTraceSlots = 18 };
 
 size_t conv_ws64_wimg_bytes();
 // w: fp32 [3,3,64,64] reference layout, scale: per-output-channel BN fold (nullable)
-void conv_ws64_pack_weights(const float* w, const float* scale, uint32_t* img);
+void conv_ws64_pack_weights(const float* w, const float* scale, bool fp16, uint32_t* img);
 void conv_ws64_make_maps(const void* in, const void* res, const void* out, const void* out2, int64_t nalloc,
                          WsGroup* g);
 size_t conv_ws64_smem_bytes(int stages, int win_alloc);

@@ -17,6 +17,7 @@
 
 #include "common.h"
 #include "kernels.h"
+#include "elem16.cuh"
 #include "sm100.cuh"
 
 namespace cnrx {
@@ -36,7 +37,7 @@ __device__ __forceinline__ Cplx cmul(Cplx a, Cplx b) { return {a.re * b.re - a.i
 // frame in local memory).
 template <int OUT_PLANE, int NT = 0, int NS = 0>
 __global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, int N_rt, PilotTablesDev pt,
-                                 float* __restrict__ feat_ref, __nv_bfloat16* __restrict__ plane, int cpad) {
+                                 float* __restrict__ feat_ref, __nv_bfloat16* __restrict__ plane, int cpad, bool h16) {
   const int N = NT > 0 ? NT : N_rt;
   constexpr int kN = NT > 0 ? NT : kMaxN;
   constexpr int kS = NS > 0 ? NS : kMaxPilotSyms;
@@ -129,8 +130,7 @@ __global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, in
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int k = 2 * i;
-        const __nv_bfloat162 b2 = __floats2bfloat162_rn(k < C ? v[k] : 0.f, k + 1 < C ? v[k + 1] : 0.f);
-        o.v[i] = *reinterpret_cast<const uint32_t*>(&b2);
+        o.v[i] = pack2r(h16, k < C ? v[k] : 0.f, k + 1 < C ? v[k + 1] : 0.f);
       }
       stg256(plane + geo.row_of(b, t, f) * cpad, o);
     } else if (OUT_PLANE) {
@@ -139,11 +139,11 @@ __global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, in
       for (int i0 = 0; i0 < (6 * kN + 15) / 16 * 16; i0 += 8) {
         if (i0 >= cpad) break;
         uint4 o;
-        __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+        uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int k = i0 + 2 * i;
-          op[i] = __floats2bfloat162_rn(k < C ? v[k] : 0.f, k + 1 < C ? v[k + 1] : 0.f);
+          op[i] = pack2r(h16, k < C ? v[k] : 0.f, k + 1 < C ? v[k + 1] : 0.f);
         }
         *reinterpret_cast<uint4*>(dst + i0) = o;
       }
@@ -154,10 +154,10 @@ __global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, in
   }
 }
 
-// Reference-layout fp32 features [B,T,F,C] -> bf16 plane [Nalloc][cpad] (used by cnrx_forward when
-// the caller supplies features rather than the received grid).
+// Reference-layout fp32 features [B,T,F,C] -> bf16 / fp16 plane [Nalloc][cpad] (used by cnrx_forward
+// when the caller supplies features rather than the received grid).
 __global__ void pack_plane_kernel(const float* __restrict__ x, PlaneGeom geo, int C, __nv_bfloat16* __restrict__ plane,
-                                  int cpad) {
+                                  int cpad, bool h16) {
   const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (row >= geo.Nalloc) return;
   __nv_bfloat16* dst = plane + row * cpad;
@@ -170,12 +170,12 @@ __global__ void pack_plane_kernel(const float* __restrict__ x, PlaneGeom geo, in
   }
   for (int i0 = 0; i0 < cpad; i0 += 8) {
     uint4 o;
-    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+    uint32_t* op = reinterpret_cast<uint32_t*>(&o);
     for (int i = 0; i < 4; ++i) {
       const int k = i0 + 2 * i;
       const float a = (valid && k < C) ? src[k] : 0.f;
       const float c = (valid && k + 1 < C) ? src[k + 1] : 0.f;
-      op[i] = __floats2bfloat162_rn(a, c);
+      op[i] = pack2r(h16, a, c);
     }
     *reinterpret_cast<uint4*>(dst + i0) = o;
   }
@@ -308,8 +308,8 @@ __global__ void __launch_bounds__(256) stem_kernel(const __grid_constant__ StemL
       }
     if (!active || !in_range) continue;
     uint4 o1, o2;
-    __nv_bfloat162* p1 = reinterpret_cast<__nv_bfloat162*>(&o1);
-    __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&o2);
+    uint32_t* p1 = reinterpret_cast<uint32_t*>(&o1);
+    uint32_t* p2 = reinterpret_cast<uint32_t*>(&o2);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       float a0 = acc[2 * k], a1 = acc[2 * k + 1];
@@ -318,10 +318,10 @@ __global__ void __launch_bounds__(256) stem_kernel(const __grid_constant__ StemL
         a1 = fmaxf(a1, 0.f);
       }
       if (!valid) a0 = a1 = 0.f;
-      p1[k] = __floats2bfloat162_rn(a0, a1);
+      p1[k] = pack2r(L.fp16 != 0, a0, a1);
       const float u0 = valid ? fmaxf(a0 * s2[2 * k] + t2[2 * k], 0.f) : 0.f;
       const float u1 = valid ? fmaxf(a1 * s2[2 * k + 1] + t2[2 * k + 1], 0.f) : 0.f;
-      p2[k] = __floats2bfloat162_rn(u0, u1);
+      p2[k] = pack2r(L.fp16 != 0, u0, u1);
     }
     *reinterpret_cast<uint4*>(op.out + row * cout + c0) = o1;
     if (op.out2) *reinterpret_cast<uint4*>(op.out2 + row * cout + c0) = o2;
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(256) stem_kernel(const __grid_constant__ StemL
 // slot still spreads over the GPU; each thread recomputes its column's LS values at the two pilot
 // symbols it interpolates between (a handful of L1/L2-resident loads).
 __global__ void featurize_row_kernel(const float2* __restrict__ y, PlaneGeom geo, int N, PilotTablesDev pt,
-                                     __nv_bfloat16* __restrict__ plane, int cpad) {
+                                     __nv_bfloat16* __restrict__ plane, int cpad, bool h16) {
   const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (row >= geo.Nalloc) return;
   float v[6 * kMaxN];
@@ -373,10 +373,10 @@ __global__ void featurize_row_kernel(const float2* __restrict__ y, PlaneGeom geo
   __nv_bfloat16* dst = plane + row * cpad;
   for (int i0 = 0; i0 < cpad; i0 += 8) {
     uint4 o;
-    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+    uint32_t* op = reinterpret_cast<uint32_t*>(&o);
     for (int i = 0; i < 4; ++i) {
       const int k = i0 + 2 * i;
-      op[i] = __floats2bfloat162_rn(k < C ? v[k] : 0.f, k + 1 < C ? v[k + 1] : 0.f);
+      op[i] = pack2r(h16, k < C ? v[k] : 0.f, k + 1 < C ? v[k + 1] : 0.f);
     }
     *reinterpret_cast<uint4*>(dst + i0) = o;
   }
@@ -409,26 +409,26 @@ const char* launch_stem(const StemLaunch& L, const PlaneGeom& geo, cudaStream_t 
 }
 
 const char* launch_featurize_plane(const float* y, const PlaneGeom& geo, int N, const PilotTablesDev& pt,
-                                   __nv_bfloat16* plane, int cpad, cudaStream_t s) {
+                                   __nv_bfloat16* plane, int cpad, bool fp16, cudaStream_t s) {
   require(N <= kMaxN, "featurize supports at most 8 receive antennas");
   const int64_t n = static_cast<int64_t>(geo.B) * (geo.F + geo.npad) + (geo.Nalloc - static_cast<int64_t>(geo.B) * geo.P);
   const int threads = 128;
   if (n < 148 * 128 && pt.n_sym >= 1) {  // too few columns to fill the GPU: one thread per row
     featurize_row_kernel<<<static_cast<unsigned>((geo.Nalloc + threads - 1) / threads), threads, 0, s>>>(
-        reinterpret_cast<const float2*>(y), geo, N, pt, plane, cpad);
+        reinterpret_cast<const float2*>(y), geo, N, pt, plane, cpad, fp16);
     CNRX_CUDA(cudaGetLastError());
     return "featurize_row_kernel";
   }
   const unsigned blocks = static_cast<unsigned>((n + threads - 1) / threads);
   const float2* y2 = reinterpret_cast<const float2*>(y);
   if (pt.n_sym == 2 && N == 2)  // the BASELINE DM-RS layout (2 pilot symbols) with 2 / 1 / 4 antennas
-    featurize_kernel<1, 2, 2><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad);
+    featurize_kernel<1, 2, 2><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad, fp16);
   else if (pt.n_sym == 2 && N == 1)
-    featurize_kernel<1, 1, 2><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad);
+    featurize_kernel<1, 1, 2><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad, fp16);
   else if (pt.n_sym == 2 && N == 4)
-    featurize_kernel<1, 4, 2><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad);
+    featurize_kernel<1, 4, 2><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad, fp16);
   else
-    featurize_kernel<1><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad);
+    featurize_kernel<1><<<blocks, threads, 0, s>>>(y2, geo, N, pt, nullptr, plane, cpad, fp16);
   CNRX_CUDA(cudaGetLastError());
   return "featurize_kernel<plane>";
 }
@@ -439,16 +439,16 @@ const char* launch_featurize_ref(const float* y, const PlaneGeom& geo, int N, co
   const int64_t n = static_cast<int64_t>(geo.B) * geo.F;
   const int threads = 128;
   featurize_kernel<0><<<static_cast<unsigned>((n + threads - 1) / threads), threads, 0, s>>>(
-      reinterpret_cast<const float2*>(y), geo, N, pt, feat, nullptr, 0);
+      reinterpret_cast<const float2*>(y), geo, N, pt, feat, nullptr, 0, false);
   CNRX_CUDA(cudaGetLastError());
   return "featurize_kernel<ref>";
 }
 
-const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_bfloat16* plane, int cpad,
+const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_bfloat16* plane, int cpad, bool fp16,
                               cudaStream_t s) {
   const int threads = 256;
   pack_plane_kernel<<<static_cast<unsigned>((geo.Nalloc + threads - 1) / threads), threads, 0, s>>>(x, geo, C, plane,
-                                                                                                   cpad);
+                                                                                                   cpad, fp16);
   CNRX_CUDA(cudaGetLastError());
   return "pack_plane_kernel";
 }

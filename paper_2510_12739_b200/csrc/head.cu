@@ -1,4 +1,4 @@
-// head.cu — CoNet-Rx fusion tail + LLR head over 64-channel bf16 planes, TMA-streamed.
+// head.cu — CoNet-Rx fusion tail + LLR head over 16-bit (bf16 / fp16) activation planes, TMA-streamed.
 //
 // Replaces the reference's tail of build_conet (network.hpp:520-560): the interaction fusion of the
 // main and supplementary subnetwork outputs (elementwise mul / add, network.hpp:526-532, each
@@ -18,6 +18,7 @@
 #include <cstring>
 
 #include "head.h"
+#include "elem16.cuh"
 #include "sm100.cuh"
 
 namespace cnrx {
@@ -31,7 +32,8 @@ constexpr int kThreads = kConsumers + 32;
 struct HeadLayout {
   uint32_t ring_off, stage_bytes, aff_off, w_off, b_off, part_off, hw_off, bar_off, total;
 };
-__host__ __device__ inline HeadLayout head_layout(int c, int ns, int nb, int stages) {
+// tc: the head GEMV runs on the tensor core (64-channel bf16 planes); otherwise on CUDA cores in fp32
+__host__ __device__ inline HeadLayout head_layout(int c, int ns, int nb, int stages, bool tc) {
   HeadLayout l{};
   const int kHC = c;
   const uint32_t kPlaneBox = static_cast<uint32_t>(kHRows * c * 2);
@@ -45,9 +47,9 @@ __host__ __device__ inline HeadLayout head_layout(int c, int ns, int nb, int sta
   l.b_off = off;
   off += 64u;
   l.part_off = off;  // [2][128 rows][nb] partial GEMV sums of the upper channel half (CUDA-core GEMV)
-  if (c != 64) off += 2u * kHRows * static_cast<uint32_t>(nb) * 4u;
+  if (!tc) off += 2u * kHRows * static_cast<uint32_t>(nb) * 4u;
   l.hw_off = off;
-  if (c == 64) {  // tensor-core GEMV: head weight image (1024-aligned); z overwrites the stage's plane 0
+  if (tc) {  // tensor-core GEMV: head weight image (1024-aligned); z overwrites the stage's plane 0
     l.hw_off = (off + 1023u) & ~1023u;
     off = l.hw_off + kHeadTcWBytes;
   }
@@ -64,14 +66,19 @@ __device__ __forceinline__ uint32_t hoff(uint32_t row, uint32_t chunk) {
   else return row * static_cast<uint32_t>(C * 2) + (chunk << 4);
 }
 
-template <int C, int NB, int NS>
+template <int C, int NB, int NS, bool TC>
 __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_constant__ HeadLaunch L) {
   constexpr int kHC = C;
   constexpr int CPT = C / 2;  // channels per thread
   constexpr uint32_t kPlaneBox = kHRows * C * 2;
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
-  const HeadLayout lay = head_layout(C, NS, NB, L.stages);
+  // 64-channel bf16 planes: the head GEMV runs on the tensor core over the bf16-rounded z tile (the same
+  // UMMAs as conv_ws.cu's fused-head epilogue, so both programs give identical LLRs) unless the plan
+  // disables it; fp16 plans keep z in fp32 (CUDA-core GEMV): z is a product of subnetwork outputs.
+  static_assert(!TC || C == 64, "tensor-core head needs 64-channel planes");
+  constexpr bool tc = TC;
+  const HeadLayout lay = head_layout(C, NS, NB, L.stages, tc);
   float* s_aff = reinterpret_cast<float*>(smem + lay.aff_off);  // [NS][2][C]
   float* s_w = reinterpret_cast<float*>(smem + lay.w_off);      // [C][NB]
   float* s_b = reinterpret_cast<float*>(smem + lay.b_off);      // [NB]
@@ -79,9 +86,6 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
   uint64_t* empty = full + L.stages;
   uint64_t* hdone = empty + L.stages;  // (kTC) head UMMAs of the tile complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hdone + 1);
-  // 64-channel planes: the head GEMV runs on the tensor core over the bf16-rounded z tile (the same
-  // UMMAs as conv_ws.cu's fused-head epilogue, so both programs give identical LLRs)
-  constexpr bool kTC = C == 64;
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
     mbar_init(hdone, 1);
     fence_barrier_init();
   }
-  if constexpr (kTC) {
+  if constexpr (tc) {
     if (tid < 32) tmem_alloc(tmem_slot, 32);
     head_tc_pack_weights(smem + lay.hw_off, L.head_w, NB, tid, kThreads);
     fence_proxy_async_smem();
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = kTC ? *tmem_slot : 0u;
+  const uint32_t tbase = tc ? *tmem_slot : 0u;
   pdl_trigger();
   pdl_wait();  // PDL: the prologue above overlapped the previous kernel's tail
 
@@ -145,10 +149,10 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
 #pragma unroll
       for (int k = 0; k < CPT / 8; ++k) {
         const uint4 raw = *reinterpret_cast<const uint4*>(st + i * kPlaneBox + hoff<C>(r, (CPT / 8) * hf + k));
-        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&raw);
+        const uint32_t* hv = reinterpret_cast<const uint32_t*>(&raw);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(hv[e]);
+          const float2 f = unpack2r(L.fp16 != 0, hv[e]);
           const int c = 8 * k + 2 * e;
           if (i == 0) {
             acc[c] = f.x;
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
       }
     }
     __syncwarp();
-    if constexpr (kTC) {
+    if constexpr (tc) {
       // z (bf16) overwrites this thread's own chunks of the stage's plane-0 tile (same swizzled layout),
       // one thread issues the head UMMAs, warps 0-3 read TMEM lane quadrants 0-3; the stage is released
       // once the UMMAs have read it
@@ -190,10 +194,7 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
       for (int k = 0; k < 4; ++k) {
         uint32_t pk[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[8 * k + 2 * e], acc[8 * k + 2 * e + 1]);
-          pk[e] = *reinterpret_cast<const uint32_t*>(&b2);
-        }
+        for (int e = 0; e < 4; ++e) pk[e] = pack2<false>(acc[8 * k + 2 * e], acc[8 * k + 2 * e + 1]);
         sts128(za + hoff<64>(static_cast<uint32_t>(r), static_cast<uint32_t>(4 * hf + k)), make_uint4(pk[0], pk[1], pk[2], pk[3]));
       }
       fence_proxy_async_smem();
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
       }
     }
   }
-  if constexpr (kTC) {
+  if constexpr (tc) {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
     tc_fence_after();
     if (tid < 32) tmem_dealloc(tbase, 32);
@@ -285,7 +286,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn_head() {
 
 template <int C, int NB, int NS>
 void launch_t(const HeadLaunch& L, int stages_bytes_total, cudaStream_t s) {
-  ensure_smem_attr(reinterpret_cast<const void*>(head_tma_kernel<C, NB, NS>), stages_bytes_total);
+  // 64-channel heads: tensor-core GEMV (bf16 plans) or CUDA-core fp32 GEMV (fp16 plans / tc_head off)
+  constexpr bool kMayTC = C == 64;
+  auto kern = (kMayTC && L.tc_head) ? head_tma_kernel<C, NB, NS, kMayTC> : head_tma_kernel<C, NB, NS, false>;
+  ensure_smem_attr(reinterpret_cast<const void*>(kern), stages_bytes_total);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -294,7 +298,7 @@ void launch_t(const HeadLaunch& L, int stages_bytes_total, cudaStream_t s) {
   const int per_sm = stages_bytes_total * 2 + 4096 <= 228 * 1024 ? 2 : 1;
   const int64_t slots = static_cast<int64_t>(per_sm) * sms;
   const unsigned grid = static_cast<unsigned>(n_tiles < slots ? n_tiles : slots);
-  launch_pdl(head_tma_kernel<C, NB, NS>, dim3(grid), dim3(kThreads), static_cast<size_t>(stages_bytes_total), s, L);
+  launch_pdl(kern, dim3(grid), dim3(kThreads), static_cast<size_t>(stages_bytes_total), s, L);
 }
 
 template <int C, int NB>
@@ -351,14 +355,17 @@ const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const
   L.head_w = prog.head_w;
   L.head_b = prog.head_b;
   L.llr = prog.llr;
+  L.fp16 = prog.fp16;
+  L.tc_head = prog.tc_head && !prog.fp16;
+  const bool tc = C == 64 && L.tc_head;
   // CNRX_HEAD_STAGES (experiments): ring depth; deeper rings fit one CTA per SM instead of two
   static const int want = std::getenv("CNRX_HEAD_STAGES") ? std::atoi(std::getenv("CNRX_HEAD_STAGES")) : 0;
   int stages = want >= 2 ? want : 3;
   if (want < 2)
-    while (stages > 2 && head_layout(C, ns, nb, stages).total > 113u * 1024u) --stages;
-  while (stages > 2 && head_layout(C, ns, nb, stages).total > 227u * 1024u) --stages;
+    while (stages > 2 && head_layout(C, ns, nb, stages, tc).total > 113u * 1024u) --stages;
+  while (stages > 2 && head_layout(C, ns, nb, stages, tc).total > 227u * 1024u) --stages;
   L.stages = stages;
-  const int total = static_cast<int>(head_layout(C, ns, nb, stages).total);
+  const int total = static_cast<int>(head_layout(C, ns, nb, stages, tc).total);
   if (total > 227 * 1024) return nullptr;
   bool ok = false;
   switch (C) {

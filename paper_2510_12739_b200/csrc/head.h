@@ -19,7 +19,9 @@ struct HeadLaunch {
   const float* head_w;                 // [C][nb]
   const float* head_b;                 // [nb]
   float* llr;                          // [B,T,F,nb]
-  int32_t ns, nb, stages, pad_;
+  int32_t ns, nb, stages;
+  int32_t fp16;                        // operand planes are fp16 (else bf16)
+  int32_t tc_head;                     // C == 64: GEMV on the tensor core over bf16-rounded z
 };
 
 // Launch the fold program (ns steps, ops/affs/relus as pw_as_fold returns them) + head GEMV when it

@@ -27,15 +27,16 @@ struct PilotTablesDev {
   const float* inv_x;           // [T][F] complex 1/x at pilot REs
 };
 
+// plane: 16-bit feature plane [Nalloc][cpad], bf16 or (fp16) fp16
 const char* launch_featurize_plane(const float* y, const PlaneGeom& geo, int N, const PilotTablesDev& pt,
-                                   __nv_bfloat16* plane, int cpad, cudaStream_t s);
+                                   __nv_bfloat16* plane, int cpad, bool fp16, cudaStream_t s);
 // Classical receiver (classic.cu): LMMSE combining + exact max-log demapping per RE.  Either feat
 // ([B,T,F,6N] featurizer output: y and the LS-interpolated estimate) or y and h ([B,T,F,N] complex).
 const char* launch_lmmse_demap(const float* feat, const float2* y, const float2* h, const float* noise_var, int64_t B,
                                int T, int F, int N, int bits, float* llr, cudaStream_t s);
 const char* launch_featurize_ref(const float* y, const PlaneGeom& geo, int N, const PilotTablesDev& pt, float* feat,
                                  cudaStream_t s);
-const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_bfloat16* plane, int cpad,
+const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_bfloat16* plane, int cpad, bool fp16,
                               cudaStream_t s);
 
 // ---------------------------------------------------------------------------------------------
@@ -59,6 +60,7 @@ struct StemLaunch {
   int32_t nops, cin;
   int32_t N;             // receive mode: antennas (cin = 6N)
   int32_t mode;          // 0: x fp32 [B,T,F,cin]; 1: received grid y
+  int32_t fp16;          // output planes are fp16 (else bf16)
   const float* x;
   const float* y;        // complex [B,T,F,N]
   PilotTablesDev pt;
@@ -87,6 +89,8 @@ struct PwProgram {
   int32_t C;                // channels of every operand (multiple of 8)
   int32_t head_bits;        // 0: store plane; >0: head GEMV with this many outputs
   int32_t n_planes_used;    // planes[0 .. n_planes_used) are operands
+  int32_t fp16;             // operand / output planes are fp16 (else bf16)
+  int32_t tc_head;          // 64-channel heads may run their GEMV on the tensor core (bf16-rounded z)
   PwIns ins[kPwMaxIns];
   const __nv_bfloat16* planes[kPwMaxPlanes];
   const float* aff_s[kPwMaxAff];

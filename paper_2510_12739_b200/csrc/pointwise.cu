@@ -1,4 +1,4 @@
-// pointwise.cu — linear pointwise programs over bf16 planes: the CoNet interaction + post-fusion BN
+// pointwise.cu — linear pointwise programs over 16-bit (bf16 / fp16) planes: the CoNet interaction + post-fusion BN
 // chain and the 1x1 LLR head (network.hpp:534-559: mul -> norm -> ... -> main.out conv), or any
 // non-conv pointwise node the plan compiler has to materialise as a plane.
 //
@@ -13,17 +13,18 @@
 
 #include "head.h"
 #include "kernels.h"
+#include "elem16.cuh"
 
 namespace cnrx {
 
 namespace {
 
-__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&v)[8]) {
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&v)[8], bool h16) {
   const uint4 raw = *reinterpret_cast<const uint4*>(p);
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+  const uint32_t* h = reinterpret_cast<const uint32_t*>(&raw);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const float2 f = __bfloat1622float2(h[i]);
+    const float2 f = unpack2r(h16, h[i]);
     v[2 * i] = f.x;
     v[2 * i + 1] = f.y;
   }
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(256) pw_program_kernel(const __grid_constant__
         const PwIns ins = prog.ins[n];
         if (ins.op == PW_LOAD || ins.op == PW_MUL || ins.op == PW_ADD) {
           float v[8];
-          load8(prog.planes[ins.k] + row * C + c0, v);
+          load8(prog.planes[ins.k] + row * C + c0, v, prog.fp16 != 0);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             acc[i] = ins.op == PW_LOAD ? v[i] : ins.op == PW_MUL ? acc[i] * v[i] : acc[i] + v[i];
@@ -81,9 +82,9 @@ __global__ void __launch_bounds__(256) pw_program_kernel(const __grid_constant__
       }
     } else {
       uint4 o;
-      __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+      uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) op[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+      for (int i = 0; i < 4; ++i) op[i] = pack2r(prog.fp16 != 0, acc[2 * i], acc[2 * i + 1]);
       *reinterpret_cast<uint4*>(prog.out_plane + row * C + c0) = o;
     }
   }
@@ -160,11 +161,11 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
 #pragma unroll
           for (int k = 1; k < kPwMaxPlanes; ++k)
             if (k == ins.k) r4 = raw[u][k];
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r4);
+          const uint32_t* h = reinterpret_cast<const uint32_t*>(&r4);
           float v[8];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const float2 f = __bfloat1622float2(h[i]);
+            const float2 f = unpack2r(prog.fp16 != 0, h[i]);
             v[2 * i] = f.x;
             v[2 * i + 1] = f.y;
           }
@@ -216,9 +217,9 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
         }
       } else if (in_range[u]) {
         uint4 o;
-        __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+        uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) op[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+        for (int i = 0; i < 4; ++i) op[i] = pack2r(prog.fp16 != 0, acc[2 * i], acc[2 * i + 1]);
         *reinterpret_cast<uint4*>(prog.out_plane + row[u] * C + c0) = o;
       }
     }
@@ -284,11 +285,11 @@ __global__ void __launch_bounds__(256) pw_fold_kernel(const __grid_constant__ Pw
       float acc[8];
 #pragma unroll
       for (int i = 0; i < NS; ++i) {
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[u][i]);
+        const uint32_t* h = reinterpret_cast<const uint32_t*>(&raw[u][i]);
         float v[8];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(h[e]);
+          const float2 f = unpack2r(prog.fp16 != 0, h[e]);
           v[2 * e] = f.x;
           v[2 * e + 1] = f.y;
         }
@@ -355,9 +356,9 @@ __global__ void __launch_bounds__(256) pw_fold_kernel(const __grid_constant__ Pw
           for (int e = 0; e < 8; ++e) acc[e] = 0.f;
         }
         uint4 o;
-        __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+        uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) op[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+        for (int e = 0; e < 4; ++e) op[e] = pack2r(prog.fp16 != 0, acc[2 * e], acc[2 * e + 1]);
         *reinterpret_cast<uint4*>(prog.out_plane + row[u] * C + c0) = o;
       }
     }
@@ -432,10 +433,10 @@ __global__ void __launch_bounds__(256) pw_fold_plane_kernel(const __grid_constan
     float acc[8];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
+      const uint32_t* h = reinterpret_cast<const uint32_t*>(&raw[k]);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h[e]);
+        const float2 f = unpack2r(prog.fp16 != 0, h[e]);
         if (k == 0) {
           acc[2 * e] = f.x;
           acc[2 * e + 1] = f.y;
@@ -463,14 +464,13 @@ __global__ void __launch_bounds__(256) pw_fold_plane_kernel(const __grid_constan
       for (int e = 0; e < 8; ++e) acc[e] = 0.f;
     }
     uint4 o;
-    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&o);
+    uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) op[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+    for (int e = 0; e < 4; ++e) op[e] = pack2r(prog.fp16 != 0, acc[2 * e], acc[2 * e + 1]);
     *reinterpret_cast<uint4*>(prog.out_plane + row * prog.C + c0) = o;
     if (prog.out2_plane) {
-      const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) op[e] = __hmax2(op[e], z);  // relu commutes with the bf16 rounding
+      for (int e = 0; e < 4; ++e) op[e] = relu2r(prog.fp16 != 0, op[e]);  // relu commutes with the rounding
       *reinterpret_cast<uint4*>(prog.out2_plane + row * prog.C + c0) = o;
     }
   }
@@ -545,8 +545,9 @@ const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaS
     FoldSteps fs{};
     int ns = 0;
     if (pw_as_fold(prog, &ns, fs.op, fs.aff, fs.relu) && prog.n_planes_used == ns) {
-      static const bool no_tma_head = getenv("CNRX_NO_TMA_HEAD") != nullptr;
-      if (head && !no_tma_head) {
+      // the TMA-streamed head kernel; with tensor_core_head disabled on a bf16 plan the fold kernel
+      // below (fp32 GEMV, as before the tensor-core head existed)
+      if (head && (prog.tc_head || prog.fp16)) {
         const char* name = launch_head_tma(prog, ns, fs.op, fs.aff, fs.relu, geo, s);
         if (name) return name;
       }

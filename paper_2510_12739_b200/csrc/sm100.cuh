@@ -84,6 +84,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 #ifndef CNRX_WAIT_LIMIT_CYCLES
 #define CNRX_WAIT_LIMIT_CYCLES 8000000000ull
 #endif
+// A timed-out wait traps (the host sees cudaErrorLaunchFailure).  The diagnostic printf is a debug build
+// option (-DCNRX_WAIT_PRINTF): inlined at every wait site it gave the production kernels a 48-byte stack
+// frame and local-memory traffic.
+__device__ __forceinline__ void wait_timeout(uint32_t parity) {
+#ifdef CNRX_WAIT_PRINTF
+  printf("cnrx: mbarrier wait timeout (block %d thread %d parity %u)\n", blockIdx.x, threadIdx.x, parity);
+#else
+  (void)parity;
+#endif
+  __trap();
+}
 // The clock is checked once per 16 polls: a spinning warp's issue slots are shared with the warps doing
 // the work (polls were ~25 % of the fused block kernel's issued instructions with a check per poll).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -94,10 +105,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #pragma unroll
     for (int k = 0; k < 16; ++k)
       if (mbar_try_wait(addr, parity)) return;
-    if (static_cast<unsigned long long>(clock64() - t0) > CNRX_WAIT_LIMIT_CYCLES) {
-      printf("cnrx: mbarrier wait timeout (block %d thread %d parity %u)\n", blockIdx.x, threadIdx.x, parity);
-      __trap();
-    }
+    if (static_cast<unsigned long long>(clock64() - t0) > CNRX_WAIT_LIMIT_CYCLES) wait_timeout(parity);
   }
 }
 
@@ -111,10 +119,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
   for (;;) {
     __nanosleep(kSleepNs);
     if (mbar_try_wait(addr, parity)) return;
-    if (static_cast<unsigned long long>(clock64() - t0) > CNRX_WAIT_LIMIT_CYCLES) {
-      printf("cnrx: mbarrier wait timeout (block %d thread %d parity %u)\n", blockIdx.x, threadIdx.x, parity);
-      __trap();
-    }
+    if (static_cast<unsigned long long>(clock64() - t0) > CNRX_WAIT_LIMIT_CYCLES) wait_timeout(parity);
   }
 }
 
@@ -181,8 +186,8 @@ __device__ __forceinline__ void tc_fence_before() {
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 in, fp32 accumulate). Issued by one thread.
-__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 or fp16 in, per the idesc; fp32 accumulate). Issued by one thread.
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -193,12 +198,24 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint
 
 // D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16: A (M x 16 bf16) lives in TMEM (lane = row, 8 columns
 // of packed bf16 pairs per K=16 step).
-__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+__device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                              uint32_t accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Same, the B descriptor given as its two 32-bit halves (joined inside the asm): issuers that walk a
+// window at many row offsets keep one 32-bit offset per tap instead of a hoisted 64-bit descriptor per
+// (tap, K step) -- the hoisted form spilled in the fused block kernel's issuer (80-register cap).
+__device__ __forceinline__ void umma_f16_ts_lohi(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t b_hi,
+                                                 uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .b64 bd;\n setp.ne.b32 p, %5, 0;\n mov.b64 bd, {%2, %3};\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], bd, %4, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 
@@ -347,7 +364,7 @@ __device__ __forceinline__ void head_tc_umma(uint32_t d_tmem, uint32_t z_addr, u
   constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((kHeadTcN >> 3) << 17) | ((128u >> 4) << 24);
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk)
-    umma_bf16(d_tmem, make_sdesc(z_addr + kk * 32, 1024, kSwizzle128, 0), make_sdesc(hw_addr + kk * 32, 1024, kSwizzle128, 0),
+    umma_f16(d_tmem, make_sdesc(z_addr + kk * 32, 1024, kSwizzle128, 0), make_sdesc(hw_addr + kk * 32, 1024, kSwizzle128, 0),
               idesc, kk > 0 ? 1u : 0u);
 }
 

@@ -22,7 +22,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CNRX_LIB") or os.path.join(HERE, "libconetrx_cuda.so")  # CNRX_LIB: A/B builds only
 
 OK, ERR_INVALID_ARGUMENT, ERR_NOT_READY, ERR_UNSUPPORTED, ERR_CUDA = range(5)
-FP32, BF16 = 0, 1
+FP32, BF16, FP16 = 0, 1, 2
+PRECISIONS = {"fp32": FP32, "bf16": BF16, "fp16": FP16}
 MODE_TRAIN, MODE_EVAL = 0, 1
 
 
@@ -71,6 +72,16 @@ class cnrx_plan_info(C.Structure):
                 ("macs_per_re", C.c_int64), ("rows_per_slot", C.c_int64), ("workspace_bytes", C.c_int64)]
 
 
+class cnrx_plan_options(C.Structure):
+    _fields_ = [("struct_size", C.c_int32), ("fused_blocks", C.c_int32), ("fused_head", C.c_int32),
+                ("tensor_core_head", C.c_int32), ("cta_pair", C.c_int32), ("weights_stationary", C.c_int32),
+                ("relu_on_load", C.c_int32), ("cuda_core_stem", C.c_int32), ("pipeline_chunks", C.c_int32),
+                ("pipeline_taper", C.c_float)]
+
+
+OPTION_NAMES = [n for n, _ in cnrx_plan_options._fields_ if n != "struct_size"]
+
+
 class cnrx_link(C.Structure):
     _fields_ = [("T", C.c_int32), ("F", C.c_int32), ("N", C.c_int32), ("mod_order", C.c_int32),
                 ("n_taps", C.c_int32), ("pilot_spacing", C.c_int32), ("n_pilot_symbols", C.c_int32),
@@ -82,7 +93,8 @@ class cnrx_link(C.Structure):
 
 _lib = None
 
-EXPORTED = ["cnrx_plan_create", "cnrx_plan_destroy", "cnrx_last_error", "cnrx_forward", "cnrx_forward_device",
+EXPORTED = ["cnrx_plan_create", "cnrx_plan_create_ex", "cnrx_plan_options_default", "cnrx_get_plan_options",
+            "cnrx_plan_destroy", "cnrx_last_error", "cnrx_forward", "cnrx_forward_device",
             "cnrx_set_pilots", "cnrx_receive", "cnrx_receive_device", "cnrx_featurize_device",
             "cnrx_receive_sharded", "cnrx_forward_sharded", "cnrx_get_plan_info", "cnrx_set_graph_capture", "cnrx_launch_name",
             "cnrx_set_profiling", "cnrx_read_profile", "cnrx_launch_flops", "cnrx_generate_slots",
@@ -103,6 +115,10 @@ def lib():
     L.cnrx_plan_create.argtypes = [C.POINTER(cnrx_node), C.c_int32, C.c_int32, C.c_int32, C.POINTER(cnrx_param),
                                    C.c_int32, C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32,
                                    C.POINTER(vp)]
+    L.cnrx_plan_create_ex.argtypes = L.cnrx_plan_create.argtypes[:-1] + [C.POINTER(cnrx_plan_options), C.POINTER(vp)]
+    L.cnrx_plan_options_default.argtypes = [C.POINTER(cnrx_plan_options)]
+    L.cnrx_plan_options_default.restype = None
+    L.cnrx_get_plan_options.argtypes = [vp, C.POINTER(cnrx_plan_options)]
     L.cnrx_plan_destroy.argtypes = [vp]
     L.cnrx_plan_destroy.restype = None
     L.cnrx_last_error.restype = C.c_char_p
@@ -127,7 +143,7 @@ def lib():
     L.cnrx_slot_noise_var.argtypes = [C.POINTER(cnrx_link), i64, C.c_uint64, C.c_uint64, f32p]
     L.cnrx_classical_receive.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, C.c_int32, vp, vp]
     for fn in EXPORTED:
-        if fn not in ("cnrx_plan_destroy", "cnrx_last_error", "cnrx_launch_name"):
+        if fn not in ("cnrx_plan_destroy", "cnrx_last_error", "cnrx_launch_name", "cnrx_plan_options_default"):
             getattr(L, fn).restype = C.c_int
     L.cnrx_launch_flops.restype = C.c_int64
     _lib = L
@@ -152,10 +168,21 @@ def _stream(stream: Optional[int]) -> C.c_void_p:
     return C.c_void_p(1 if stream == 0 else stream)
 
 
-class Plan:
-    """A compiled CoNet-Rx network on one GPU."""
+def default_options() -> dict:
+    """cnrx_plan_options_default() as a dict (no environment overrides)."""
+    o = cnrx_plan_options()
+    lib().cnrx_plan_options_default(C.byref(o))
+    return {n: getattr(o, n) for n in OPTION_NAMES}
 
-    def __init__(self, g: "G.Graph", precision: str = "bf16", device: int = 0):
+
+class Plan:
+    """A compiled CoNet-Rx network on one GPU.
+
+    precision: "fp32" | "bf16" | "fp16".  options: None = cnrx_plan_create (defaults + the CNRX_* A/B
+    environment switches); a dict = cnrx_plan_create_ex with the defaults updated by the dict (no
+    environment)."""
+
+    def __init__(self, g: "G.Graph", precision: str = "bf16", device: int = 0, options: Optional[dict] = None):
         L = lib()
         self.graph = g
         self.precision = precision
@@ -173,10 +200,19 @@ class Plan:
             params[i].data = _f32p(v)
         ready = np.asarray(g.bn_ready if g.bn_ready else [0], np.uint8)
         h = C.c_void_p()
-        prec = {"fp32": FP32, "bf16": BF16}[precision]
-        _check(L.cnrx_plan_create(nodes, len(g.nodes), g.input_node, g.output_node, params, len(g.params),
-                                  ready.ctypes.data_as(C.POINTER(C.c_uint8)), len(g.bn_ready), prec, device,
-                                  C.byref(h)))
+        prec = PRECISIONS[precision]
+        args = (nodes, len(g.nodes), g.input_node, g.output_node, params, len(g.params),
+                ready.ctypes.data_as(C.POINTER(C.c_uint8)), len(g.bn_ready), prec, device)
+        if options is None:
+            _check(L.cnrx_plan_create(*args, C.byref(h)))
+        else:
+            o = cnrx_plan_options()
+            L.cnrx_plan_options_default(C.byref(o))
+            for k, v in options.items():
+                if k not in OPTION_NAMES:
+                    raise ValueError(f"unknown plan option {k!r}")
+                setattr(o, k, v)
+            _check(L.cnrx_plan_create_ex(*args, C.byref(o), C.byref(h)))
         self.h = h
         self.out_channels = g.output_channels()
         self.in_channels = g.in_channels
@@ -247,6 +283,11 @@ class Plan:
                                            C.c_void_p(feat.data_ptr()), _stream(stream)))
 
     # ---- introspection ----------------------------------------------------------------------------
+    def options(self) -> dict:
+        o = cnrx_plan_options()
+        _check(lib().cnrx_get_plan_options(self.h, C.byref(o)))
+        return {n: getattr(o, n) for n in OPTION_NAMES}
+
     def info(self) -> dict:
         inf = cnrx_plan_info()
         _check(lib().cnrx_get_plan_info(self.h, C.byref(inf)))

@@ -1,4 +1,4 @@
-"""Test helper: CPU (torch fp32) emulation of the CNRX_BF16 plan's arithmetic.
+"""Test helper: CPU (torch fp32) emulation of the CNRX_BF16 / CNRX_FP16 plans' arithmetic.
 
 The bf16 tensor-core plan rounds values to bf16 exactly where it stores activation planes (input
 features, every conv epilogue output, pre-activated copies, pointwise-program outputs) and folds an
@@ -34,8 +34,37 @@ def bn_affine(g, n):
     return torch.from_numpy(scale), torch.from_numpy(shift)
 
 
-def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
-    """x: [B,T,F,C] fp32 features -> LLRs [B,T,F,bits] as the bf16 plan computes them."""
+def _ident(t: torch.Tensor) -> torch.Tensor:
+    return t
+
+
+def fp16(t: torch.Tensor) -> torch.Tensor:
+    return t.to(torch.float16).to(torch.float32)
+
+
+# Rounding points of the bf16 plan, by role (tools/ablate_bf16.py switches them one at a time):
+#   feat  - the input feature plane (the stems' tensor-core operand)
+#   w     - BN-folded conv weights (tensor-core operands)
+#   act   - every other conv input plane (tensor-core operands: block inputs relu(y), conv1 outputs h)
+#   res   - the residual stream: a block output y as stored for the next block's skip connection
+#   leaf  - the subnetworks' final planes as the interaction fold reads them
+#   z     - the folded interaction z and the head weights (tensor-core head)
+BF16_POLICY = dict(feat=bf16, w=bf16, act=bf16, res=bf16, leaf=bf16, z=bf16)
+# CNRX_FP16 plans: the same rounding points in fp16, and the LLR head in fp32 (z not rounded)
+FP16_POLICY = dict(feat=fp16, w=fp16, act=fp16, res=fp16, leaf=fp16, z=_ident)
+
+
+def emulate(g: "G.Graph", x: np.ndarray, policy: dict | None = None, precision: str = "bf16") -> np.ndarray:
+    """x: [B,T,F,C] fp32 features -> LLRs [B,T,F,bits] as the bf16 (or fp16) plan computes them.
+
+    `policy` overrides the rounding function per role (see BF16_POLICY); None = the shipped plan."""
+    R = dict(BF16_POLICY if precision == "bf16" else FP16_POLICY)
+    if policy:
+        R.update(policy)
+    return _emulate(g, x, R)
+
+
+def _emulate(g, x, R):
     nodes = g.nodes
     consumers = [[] for _ in nodes]
     for i, n in enumerate(nodes):
@@ -46,11 +75,11 @@ def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
     single = lambda i: consumers[i][0] if len(consumers[i]) == 1 else -1
     planes, vals, nonneg, producer_relu = {}, {}, {}, {}
     xt = torch.from_numpy(np.ascontiguousarray(x, np.float32)).permute(0, 3, 1, 2)  # [B,C,T,F]
-    planes[g.input_node] = bf16(xt)
+    planes[g.input_node] = xt  # planes hold fp32 values; rounding is applied per role at each use
 
     def chain(u):
         if u in planes:
-            return planes[u]
+            return R['leaf'](planes[u])
         n = nodes[u]
         if n.op == G.OP_RELU:
             return torch.relu(chain(n.in0))
@@ -65,7 +94,8 @@ def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
             else:
                 raise ValueError("not a linear chain")
             r = chain(rest)
-            return r * planes[leaf] if n.op == G.OP_MUL else r + planes[leaf]
+            lv = R['leaf'](planes[leaf])
+            return r * lv if n.op == G.OP_MUL else r + lv
         raise ValueError(f"op {n.op} not emulated")
 
     def plane_for(u):
@@ -85,9 +115,9 @@ def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
                     if bn is not None:
                         s, t = bn_affine(g, bn)
                         z = z * s[None, :, None, None] + t[None, :, None, None]
-                    planes[u] = bf16(torch.relu(z))
+                    planes[u] = torch.relu(z)
                     return planes[u]
-        planes[u] = bf16(chain(u))
+        planes[u] = R['act'](chain(u))  # a pointwise-program output plane
         return planes[u]
 
     absorbed = set()
@@ -105,7 +135,7 @@ def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
         if stem:
             n_stems += 1
             stem_cin = w0.shape[2]
-        inp = xt if stem else plane_for(n.in0)
+        inp = xt if stem else (R['feat'] if n.in0 == g.input_node else R['act'])(plane_for(n.in0))
         w = torch.from_numpy(g.params[n.w].value)  # [kh,kw,cin,cout]
         cout = w.shape[3]
         bias = torch.from_numpy(g.params[n.b].value.copy()) if n.b >= 0 else torch.zeros(cout)
@@ -124,7 +154,7 @@ def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
         if not relu and c >= 0 and nodes[c].op == G.OP_ADD:
             other = nodes[c].in1 if nodes[c].in0 == end else nodes[c].in0
             if other != end and other < i:
-                res = plane_for(other)
+                res = R['res'](plane_for(other))
                 absorbed.add(c)
                 end = c
         if res is not None and stem:
@@ -132,7 +162,7 @@ def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
         wf = w * scale[None, None, None, :] if scale is not None else w
         wk = wf.permute(3, 2, 0, 1).contiguous()  # [cout,cin,kh,kw]
         if not stem:
-            wk = bf16(wk)
+            wk = R['w'](wk)
         kh, kw = w.shape[0], w.shape[1]
         cin_plane = inp.shape[1]
         if cin_plane > wk.shape[1]:  # zero-padded input channels
@@ -143,7 +173,7 @@ def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
         if res is not None:
             v = v + res
         vals[end] = v
-        planes[end] = bf16(v)
+        planes[end] = v
         nonneg[end] = relu
     on = nodes[g.output_node]
     f = chain(on.in0)
@@ -152,6 +182,6 @@ def emulate(g: "G.Graph", x: np.ndarray) -> np.ndarray:
     if hw.shape[0] == 64 and hw.shape[1] in (2, 4, 6, 8) and os.environ.get("CNRX_NO_TMA_HEAD") is None:
         # 64-channel heads run on the tensor core (head.cu / conv_ws.cu fused head): the folded
         # interaction z and the head weights are rounded to bf16, products accumulate in fp32
-        f, hw = bf16(f), bf16(hw)
+        f, hw = R['z'](f), R['z'](hw)
     out = torch.einsum("bctf,cj->btfj", f, hw) + hb
     return out.numpy()

@@ -287,7 +287,7 @@ def test_cpp_drop_in_example():
     assert "drop-in OK" in r.stdout
 
 
-@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+@pytest.mark.parametrize("prec", ["fp32", "bf16", "fp16"])
 def test_pipelined_host_api_matches_one_shot(prec, monkeypatch):
     """The host-buffer entry points cut the batch into chunks (copy/compute overlap, ragged last chunk,
     workspace reused at a smaller batch): results are bit-identical to one device-resident launch."""
@@ -303,14 +303,18 @@ def test_pipelined_host_api_matches_one_shot(prec, monkeypatch):
     p.receive_device(y, out)
     torch.cuda.synchronize()
     ref = out.cpu().numpy()
-    for n in ("1", "3", "4", "11"):
-        monkeypatch.setenv("CNRX_PIPELINE_CHUNKS", n)
-        assert np.array_equal(p.receive(b.y), ref), n
-        x = np.ascontiguousarray(oracle.featurize(b.y, b.pilots, b.pilot_mask))
-        if n == "3":
-            fwd1 = p.forward(x)
-            monkeypatch.setenv("CNRX_PIPELINE_CHUNKS", "1")
-            assert np.array_equal(p.forward(x), fwd1)
+    x = np.ascontiguousarray(oracle.featurize(b.y, b.pilots, b.pilot_mask))
+    fwd1 = P.Plan(g, prec, options={"pipeline_chunks": 1}).forward(x)
+    for n in (1, 3, 4, 11):
+        q = P.Plan(g, prec, options={"pipeline_chunks": n})  # env-free options (cnrx_plan_create_ex)
+        q.set_pilots(b.pilots, b.pilot_mask)
+        assert np.array_equal(q.receive(b.y), ref), n
+        assert np.array_equal(q.forward(x), fwd1), n
+    monkeypatch.setenv("CNRX_PIPELINE_CHUNKS", "3")  # the A/B environment switch of cnrx_plan_create
+    q = P.Plan(g, prec)
+    assert q.options()["pipeline_chunks"] == 3
+    q.set_pilots(b.pilots, b.pilot_mask)
+    assert np.array_equal(q.receive(b.y), ref)
 
 
 def test_calls_on_different_streams_share_the_workspace_safely():

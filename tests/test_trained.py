@@ -49,37 +49,62 @@ def test_trained_fp32_bit_exact_with_reference(ref):
     assert np.array_equal(p.forward(feat), oracle.RefNet.from_graph(g).forward(feat))
 
 
-@pytest.mark.gpu
-def test_trained_bf16_hard_decisions_and_ber():
+def _decision_run(precisions, n_batches=9, B=32, seed=12345):
+    """Hard decisions of plans of the given precisions against the fp32 plan (bit-exact with the
+    reference) on n_batches x B GPU-generated cfg2 slots; data bits only (pilots excluded)."""
     import torch
     from paper_2510_12739_b200 import plan as P
     g = _graph()
     link = G.CONFIGS["cfg2"].link
     pmask, pvals = slots.pilot_pattern(link.T, link.F, link.pilot_symbols, link.pilot_spacing)
-    p32, p16 = P.Plan(g, "fp32"), P.Plan(g, "bf16")
-    for p in (p32, p16):
+    plans = {pr: P.Plan(g, pr) for pr in ("fp32",) + tuple(precisions)}
+    for p in plans.values():
         p.set_pilots(pvals.astype(np.complex64), pmask)
     data = torch.from_numpy(pmask == 0).cuda()
-    B = 32
-    y, bits, h = P.generate_slots_device(link, B, 12345, slot0=0, with_h=True)
-    l32 = torch.empty((B, link.T, link.F, link.bits), dtype=torch.float32, device="cuda")
-    l16 = torch.empty_like(l32)
     st = torch.cuda.current_stream().cuda_stream
-    p32.receive_device(y, l32, st)
-    p16.receive_device(y, l16, st)
-    m = data[None, :, :, None].expand_as(l32)
-    a32, a16 = l32[m], l16[m]
-    agree = float(((a32 > 0) == (a16 > 0)).float().mean())
-    confident = a32.abs() >= 1.0  # |LLR| >= 1: P(bit) >= 0.73
-    agree_conf = float(((a32 > 0) == (a16 > 0))[confident].float().mean())
-    e32 = int(P.count_bit_errors(l32, bits, data).sum())
-    e16 = int(P.count_bit_errors(l16, bits, data).sum())
-    nbits = B * int(data.sum()) * link.bits
-    nv = P.slot_noise_var(link, B, 12345)
-    e_ls = int(P.count_bit_errors(P.classical_receive_device(p32, y, nv, link.mod_order), bits, data).sum())
-    print(f"agree {agree:.6f} confident {agree_conf:.6f} ({float(confident.float().mean()):.3f} of bits) "
-          f"BER fp32 {e32 / nbits:.5f} bf16 {e16 / nbits:.5f} LS-LMMSE {e_ls / nbits:.5f}")
-    assert agree_conf >= 0.9999
-    assert agree >= 0.999
-    assert abs(e16 - e32) / nbits <= 5e-4  # same BER
-    assert e32 < e_ls                       # the trained receiver beats LS-LMMSE on the same slots
+    res = {pr: dict(agree=0, conf_agree=0, conf=0, err=0) for pr in precisions}
+    err32 = err_ls = nbits = 0
+    for k in range(n_batches):
+        y, bits, _ = P.generate_slots_device(link, B, seed, slot0=k * B, with_h=True)
+        out = {}
+        for pr, p in plans.items():
+            out[pr] = torch.empty((B, link.T, link.F, link.bits), dtype=torch.float32, device="cuda")
+            p.receive_device(y, out[pr], st)
+        m = data[None, :, :, None].expand_as(out["fp32"])
+        a32 = out["fp32"][m]
+        confident = a32.abs() >= 1.0  # |LLR| >= 1: P(bit) >= 0.73
+        nbits += a32.numel()
+        err32 += int(P.count_bit_errors(out["fp32"], bits, data).sum())
+        nv = P.slot_noise_var(link, B, seed, slot0=k * B)
+        err_ls += int(P.count_bit_errors(P.classical_receive_device(plans["fp32"], y, nv, link.mod_order), bits,
+                                         data).sum())
+        for pr in precisions:
+            a = out[pr][m]
+            same = (a32 > 0) == (a > 0)
+            r = res[pr]
+            r["agree"] += int(same.sum())
+            r["conf_agree"] += int(same[confident].sum())
+            r["conf"] += int(confident.sum())
+            r["err"] += int(P.count_bit_errors(out[pr], bits, data).sum())
+    return res, err32, err_ls, nbits
+
+
+@pytest.mark.gpu
+def test_trained_fp16_meets_the_decision_bar():
+    """North star: hard-decision bits >= 99.99 % identical to the reference's (the fp32 plan is bit-exact
+    with it) over ALL data bits, on >= 8M bits, and the same BER within Monte-Carlo confidence.  The
+    CNRX_FP16 plan (fp16 tensor-core operands, fp32 head) is the mixed-precision option that meets it;
+    bf16 cannot (tools/ablate_bf16.py: bf16 conv operands alone cap agreement at ~99.97-99.99 %)."""
+    res, e32, e_ls, n = _decision_run(("fp16", "bf16"))
+    assert n >= 8_000_000
+    r16, rb = res["fp16"], res["bf16"]
+    a16, ab = r16["agree"] / n, rb["agree"] / n
+    ber32, ber16 = e32 / n, r16["err"] / n
+    sigma = np.sqrt(ber32 * (1 - ber32) / n)  # binomial std of the BER estimate
+    print(f"bits {n}: fp16 agree {a16:.6f} (confident {r16['conf_agree'] / r16['conf']:.6f}), bf16 agree {ab:.6f}; "
+          f"BER fp32 {ber32:.5f} fp16 {ber16:.5f} bf16 {rb['err'] / n:.5f} LS-LMMSE {e_ls / n:.5f}")
+    assert a16 >= 0.9999
+    assert abs(ber16 - ber32) <= 3 * sigma      # the same BER within Monte-Carlo confidence
+    assert e32 < e_ls                           # the trained receiver beats LS-LMMSE on the same slots
+    # bf16: recorded ceiling (DESIGN.md §4), not the north-star bar
+    assert ab >= 0.999 and abs(rb["err"] / n - ber32) <= 3 * sigma
