@@ -175,7 +175,16 @@ def cpu_baseline(cfg, g, batch, n_slots, reps=5, f_sample=None):
     """Median of `reps` reps over `n_slots` slots (featurize + Network<float>::forward, and
     forward_concurrent): slots/s.  f_sample: time a sub-grid of that many subcarriers and scale per RE
     (for cfg3, where one full slot takes seconds per core)."""
+    import copy
     import oracle
+    note = ""
+    if any(n.dilation_f != 1 for n in g.nodes):
+        # the reference conv2d has no dilation (kernels.hpp:70-75): time the same graph at dilation 1,
+        # which does the same work per RE (every tap computed, out-of-grid taps skipped either way)
+        g = copy.deepcopy(g)
+        for n in g.nodes:
+            n.dilation_f = 1
+        note = "; graph timed at dilation 1 (the reference conv has none; same work per RE)"
     kind, threads, fwd = ref_forward_fn(g)
     y = batch.y[:n_slots]
     pil, pm = batch.pilots, batch.pilot_mask
@@ -199,7 +208,7 @@ def cpu_baseline(cfg, g, batch, n_slots, reps=5, f_sample=None):
             "cpu": f"{cpu_model()}, {os.cpu_count()} logical CPUs",
             "per_call": {k: round(v, 4) for k, v in res.items()}, "best_call": best,
             "sample": f"median of {reps} reps of {samp}: restated featurize + reference Network<float>::"
-                      f"forward / forward_concurrent (eval), CONETRX_THREADS={os.environ.get('CONETRX_THREADS')}"}
+                      f"forward / forward_concurrent (eval), CONETRX_THREADS={os.environ.get('CONETRX_THREADS')}{note}"}
 
 
 def run_reference(args, cfg, g):
@@ -398,7 +407,7 @@ def extra_configs(torch, P, G, slots, local, pk, steps):
     out["cfg1_fp32_b64"] = measure_config(torch, P, G, slots, "cfg1", "fp32", 64, k, 3, local, pk, cpu_slots=64)
     for prec in ("bf16", "fp16"):
         out[f"cfg3_{prec}_b64"] = measure_config(torch, P, G, slots, "cfg3", prec, 64, k, 3, local, pk,
-                                                 want_cpu=prec == "bf16", cpu_slots=4, f_sample=273)
+                                                 want_cpu=prec == "bf16", cpu_slots=16, f_sample=137)
     out["cfg4_bf16_b256"] = measure_config(torch, P, G, slots, "cfg4", "bf16", 256, k, 3, local, pk, cpu_slots=8)
     out["cfg4m_bf16_b256"] = measure_config(torch, P, G, slots, "cfg4m", "bf16", 256, k, 3, local, pk, cpu_slots=8)
     # cfg5: the cfg2 batch sweep, bf16 / fp16 tensor-core plans and the fp32 CUDA-core plan
@@ -520,20 +529,20 @@ def main():
             h2d, d2h = batch.y.nbytes, out_host.numel() * 4
             how = "cnrx_receive (C ABI, pinned host buffers, batch pipelined in chunks over two copy streams)"
         else:
-            # every rank: H2D of its slots, receive on its GPU; NCCL gather of the LLRs to rank 0's GPU;
-            # rank 0: one D2H of the whole batch into its pinned host buffer
+            # every rank: H2D of its slots, receive on its GPU; NCCL gather of the LLRs to rank 0's GPU
+            # (shard.gather_llr_tensor, covered by the 2-rank gloo test); rank 0: one D2H of the whole
+            # batch into its pinned host buffer
+            from paper_2510_12739_b200 import shard
             y_dev = torch.empty((B, link.T, link.F, link.N), dtype=torch.complex64, device="cuda")
             out_dev = torch.empty((B, link.T, link.F, nb), dtype=torch.float32, device="cuda")
-            gath = [torch.empty_like(out_dev) for _ in range(world)] if rank == 0 else None
             out_host = torch.empty((world * B, link.T, link.F, nb), dtype=torch.float32).pin_memory() if rank == 0 else None
 
             def e2e_step():
                 y_dev.copy_(y_host, non_blocking=True)
                 plan.receive_device(y_dev, out_dev, torch.cuda.current_stream().cuda_stream)
-                dist.gather(out_dev, gath, dst=0)
+                full = shard.gather_llr_tensor(out_dev, world * B, world, rank)
                 if rank == 0:
-                    for r in range(world):
-                        out_host[r * B:(r + 1) * B].copy_(gath[r], non_blocking=True)
+                    out_host.copy_(full, non_blocking=True)
                 torch.cuda.synchronize()
             h2d, d2h = batch.y.nbytes * world, world * B * link.T * link.F * nb * 4
             how = "per rank: H2D + cnrx_receive_device; NCCL gather of the LLRs to rank 0; rank 0 D2H of the whole batch"

@@ -29,9 +29,10 @@ namespace conetrx {
 
 class GpuPlan {
  public:
-  enum class Precision { fp32 = CNRX_FP32, bf16 = CNRX_BF16 };
+  enum class Precision { fp32 = CNRX_FP32, bf16 = CNRX_BF16, fp16 = CNRX_FP16 };
 
-  GpuPlan(Network<float>& net, Precision precision, int device = 0) {
+  // output_node: the index the network's set_output() named; -1 = recover it (see below).
+  GpuPlan(Network<float>& net, Precision precision, int device = 0, int output_node = -1) {
     const auto& nodes = net.nodes();
     std::vector<cnrx_node> cn(nodes.size());
     int input = -1;
@@ -45,10 +46,19 @@ class GpuPlan {
       if (n.in1 >= 0) used[static_cast<size_t>(n.in1)] = 1;
     }
     // Network keeps output_node_ private; set_output() is always given the last unconsumed node by the
-    // reference builders (network.hpp:482, :560), so recover it that way.
-    int output = -1;
+    // reference builders (network.hpp:482, :560), so recover it that way unless the caller names it, and
+    // check the result against the output width the network reports (output_channels(), network.hpp:333):
+    // a raw-API graph whose set_output() names another node must pass output_node explicitly.
+    int output = output_node;
     for (int i = static_cast<int>(nodes.size()) - 1; i >= 0 && output < 0; --i)
       if (!used[static_cast<size_t>(i)]) output = i;
+    if (output < 0 || output >= static_cast<int>(nodes.size()))
+      throw std::invalid_argument("GpuPlan: bad output node index");
+    if (nodes[static_cast<size_t>(output)].out_channels != net.output_channels())
+      throw std::invalid_argument("GpuPlan: node " + std::to_string(output) + " has " +
+                                  std::to_string(nodes[static_cast<size_t>(output)].out_channels) +
+                                  " channels but the network's output has " + std::to_string(net.output_channels()) +
+                                  "; pass the set_output() node index explicitly");
     const auto& params = net.params();
     std::vector<cnrx_param> cp(params.size());
     for (size_t i = 0; i < params.size(); ++i) {

@@ -145,6 +145,12 @@ int cnrx_receive_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t 
 int cnrx_featurize_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t T, int64_t F, int64_t N,
                           float* feat_dev, void* stream);
 
+/* Test hook (synchronous): the network-input feature plane exactly as a BF16 / FP16 plan's first
+ * convolutions read it -- out_dev receives [B,T,F,cpad] 16-bit values (bf16 or fp16 bits, per the plan;
+ * padding channels zero) in the reference order; *cpad = the plan's padded input channel count. */
+int cnrx_feature_plane_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t T, int64_t F, int64_t N,
+                              uint16_t* out_dev, int32_t* cpad);
+
 /* Slot-sharded forward / receive across several plans (one per GPU, built from the same network): slots are
  * split into contiguous ranges, each GPU runs its range from host memory on its own thread, LLRs land
  * in the caller's buffer.  No collective on the data path. */

@@ -188,6 +188,8 @@ struct Workspace {
   size_t out_bytes = 0;
   void* feat_buf = nullptr; // fp32 features when an FP32 plan runs the receive path
   size_t feat_bytes = 0;
+  void* classic_buf = nullptr;  // fp32 features of the classical LS-LMMSE receiver
+  size_t classic_bytes = 0;
   struct GroupLaunch {
     bool ws = false;
     bool blk = false;
@@ -288,6 +290,9 @@ struct cnrx_plan {
   cudaEvent_t ws_done = nullptr;       // end of the last forward's work on the shared workspace
   cudaStream_t ws_stream = nullptr;    // stream that forward ran on
   bool ws_used = false;
+  cudaEvent_t classic_done = nullptr;  // end of the last classical receive on classic_buf
+  cudaStream_t classic_stream = nullptr;
+  bool classic_used = false;
   cudaGraphExec_t gexec = nullptr;
   std::string gkey;
 
@@ -359,7 +364,9 @@ void validate_graph(cnrx_plan& p) {
       case CNRX_OP_BN:
         require(param_ok(nd.gamma) && param_ok(nd.beta) && param_ok(nd.rmean) && param_ok(nd.rvar),
                 "batch norm parameters missing");
-        require(p.P(nd.gamma).numel() == cin, "batch norm gain must be [C]");
+        require(p.P(nd.gamma).numel() == cin && p.P(nd.beta).numel() == cin && p.P(nd.rmean).numel() == cin &&
+                    p.P(nd.rvar).numel() == cin,
+                "batch norm gain must be [C]");
         require(nd.bn_flag >= 0 && nd.bn_flag < static_cast<int>(p.bn_ready.size()), "bad bn flag");
         if (!p.bn_ready[static_cast<size_t>(nd.bn_flag)])
           throw Error(CNRX_ERR_NOT_READY,
@@ -367,7 +374,8 @@ void validate_graph(cnrx_plan& p) {
                       "running statistics");
         break;
       case CNRX_OP_LN:
-        require(param_ok(nd.gamma) && param_ok(nd.beta) && p.P(nd.gamma).numel() == cin, "layer norm gain must be [C]");
+        require(param_ok(nd.gamma) && param_ok(nd.beta) && p.P(nd.gamma).numel() == cin && p.P(nd.beta).numel() == cin,
+                "layer norm gain must be [C]");
         break;
       case CNRX_OP_ADD:
       case CNRX_OP_MUL:
@@ -376,12 +384,17 @@ void validate_graph(cnrx_plan& p) {
         break;
       case CNRX_OP_CONCAT:
         require(nd.in1 >= 0, "concat needs two inputs");
+        require(nd.out_channels == cin + p.N(nd.in1).out_channels, "concat output channel mismatch");
         break;
       case CNRX_OP_RELU:
         break;
       default:
         throw Error(CNRX_ERR_INVALID_ARGUMENT, "unknown op " + std::to_string(nd.op));
     }
+    // shape-preserving ops: every buffer is sized from out_channels, so it must equal the input's
+    if (nd.op == CNRX_OP_RELU || nd.op == CNRX_OP_BN || nd.op == CNRX_OP_LN || nd.op == CNRX_OP_ADD ||
+        nd.op == CNRX_OP_MUL || nd.op == CNRX_OP_DWCONV)
+      require(nd.out_channels == cin, "node " + std::to_string(i) + ": output channels must equal its input's");
   }
   p.in_ch = p.N(p.in_node).out_channels;
   p.out_ch = p.N(p.out_node).out_channels;
@@ -1868,6 +1881,8 @@ void cnrx_plan_destroy(cnrx_plan* plan) {
   if (plan->ws.in_buf) cudaFree(plan->ws.in_buf);
   if (plan->ws.out_buf) cudaFree(plan->ws.out_buf);
   if (plan->ws.feat_buf) cudaFree(plan->ws.feat_buf);
+  if (plan->ws.classic_buf) cudaFree(plan->ws.classic_buf);
+  if (plan->classic_done) cudaEventDestroy(plan->classic_done);
   for (void* d : plan->dev_allocs) cudaFree(d);
   for (auto& evs : plan->prof_events)
     for (auto e : evs) cudaEventDestroy(e);
@@ -1980,6 +1995,26 @@ int cnrx_featurize_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_
 }
 
 
+int cnrx_feature_plane_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t T, int64_t F, int64_t N,
+                              uint16_t* out_dev, int32_t* cpad) {
+  if (!plan || !cpad) return fail(CNRX_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    if (plan->precision == CNRX_FP32) throw Error(CNRX_ERR_UNSUPPORTED, "fp32 plans have no 16-bit feature plane");
+    check_receive(*plan, B, T, F, N);
+    DeviceGuard dg(plan->device);
+    CNRX_CUDA(cudaDeviceSynchronize());  // test hook: fully ordered against any earlier call
+    ensure_workspace(*plan, static_cast<int>(B), static_cast<int>(T), static_cast<int>(F));
+    const Workspace& ws = plan->ws;
+    auto* plane = static_cast<__nv_bfloat16*>(ws.buffers[static_cast<size_t>(plan->planes[0].buffer)]);
+    *cpad = plan->planes[0].C;
+    launch_featurize_plane(y_dev, ws.geo, static_cast<int>(N), plan->pt, plane, plan->planes[0].C, plan->fp16,
+                           plan->stream);
+    launch_plane_rows_to_ref(plane, ws.geo, plan->planes[0].C, out_dev, plan->stream);
+    CNRX_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
 int cnrx_forward_sharded(cnrx_plan* const* plans, int32_t n_plans, const float* x, int64_t B, int64_t T, int64_t F,
                          int64_t C, int32_t mode, float* out) {
   return run_sharded(plans, n_plans, B, [&](cnrx_plan* p, int64_t b0, int64_t nb) {
@@ -2086,8 +2121,12 @@ int cnrx_classical_receive(cnrx_plan* plan, const float* y_dev, const float* h_d
     if (!h_dev) {
       require(plan->has_pilots, "cnrx_set_pilots must be called before the LS-LMMSE receiver");
       require(T == plan->pT && F == plan->pF, "received grid does not match the pilot grid");
+      // its own scratch (not the receive path's feat_buf, which a captured fp32 forward graph may point
+      // at), ordered after the previous classical call when that ran on another stream
       const size_t bytes = static_cast<size_t>(B * T * F * 6 * N) * sizeof(float);
-      float* f = static_cast<float*>(ensure_dev(plan->ws.feat_buf, plan->ws.feat_bytes, bytes));
+      if (plan->ws.classic_bytes < bytes && plan->classic_used) CNRX_CUDA(cudaEventSynchronize(plan->classic_done));
+      float* f = static_cast<float*>(ensure_dev(plan->ws.classic_buf, plan->ws.classic_bytes, bytes));
+      if (plan->classic_used && plan->classic_stream != s) CNRX_CUDA(cudaStreamWaitEvent(s, plan->classic_done, 0));
       PlaneGeom g = make_geom(static_cast<int>(B), static_cast<int>(T), static_cast<int>(F), 1);
       launch_featurize_ref(y_dev, g, static_cast<int>(N), plan->pt, f, s);
       feat = f;
@@ -2095,6 +2134,12 @@ int cnrx_classical_receive(cnrx_plan* plan, const float* y_dev, const float* h_d
     launch_lmmse_demap(feat, reinterpret_cast<const float2*>(y_dev), reinterpret_cast<const float2*>(h_dev),
                        noise_var_dev, B, static_cast<int>(T), static_cast<int>(F), static_cast<int>(N), bits, llr_dev,
                        s);
+    if (!h_dev) {
+      if (!plan->classic_done) CNRX_CUDA(cudaEventCreateWithFlags(&plan->classic_done, cudaEventDisableTiming));
+      CNRX_CUDA(cudaEventRecord(plan->classic_done, s));
+      plan->classic_stream = s;
+      plan->classic_used = true;
+    }
   });
 }
 

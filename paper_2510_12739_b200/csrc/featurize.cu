@@ -444,6 +444,27 @@ const char* launch_featurize_ref(const float* y, const PlaneGeom& geo, int N, co
   return "featurize_kernel<ref>";
 }
 
+namespace {
+__global__ void plane_rows_to_ref_kernel(const uint16_t* __restrict__ plane, PlaneGeom geo, int cpad,
+                                         uint16_t* __restrict__ out) {
+  const int64_t n = static_cast<int64_t>(geo.B) * geo.T * geo.F * cpad;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = i % cpad, r = i / cpad;
+    const int f = static_cast<int>(r % geo.F), t = static_cast<int>((r / geo.F) % geo.T);
+    const int b = static_cast<int>(r / (static_cast<int64_t>(geo.F) * geo.T));
+    out[i] = plane[geo.row_of(b, t, f) * cpad + c];
+  }
+}
+}  // namespace
+
+const char* launch_plane_rows_to_ref(const __nv_bfloat16* plane, const PlaneGeom& geo, int cpad, uint16_t* out,
+                                     cudaStream_t s) {
+  plane_rows_to_ref_kernel<<<1024, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(plane), geo, cpad, out);
+  CNRX_CUDA(cudaGetLastError());
+  return "plane_rows_to_ref_kernel";
+}
+
 const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_bfloat16* plane, int cpad, bool fp16,
                               cudaStream_t s) {
   const int threads = 256;

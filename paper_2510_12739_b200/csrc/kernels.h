@@ -36,6 +36,9 @@ const char* launch_lmmse_demap(const float* feat, const float2* y, const float2*
                                int T, int F, int N, int bits, float* llr, cudaStream_t s);
 const char* launch_featurize_ref(const float* y, const PlaneGeom& geo, int N, const PilotTablesDev& pt, float* feat,
                                  cudaStream_t s);
+// Test hook: the valid rows of a 16-bit plane [Nalloc][cpad] in reference order [B,T,F,cpad].
+const char* launch_plane_rows_to_ref(const __nv_bfloat16* plane, const PlaneGeom& geo, int cpad, uint16_t* out,
+                                     cudaStream_t s);
 const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_bfloat16* plane, int cpad, bool fp16,
                               cudaStream_t s);
 

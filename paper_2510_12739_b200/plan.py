@@ -94,7 +94,7 @@ class cnrx_link(C.Structure):
 _lib = None
 
 EXPORTED = ["cnrx_plan_create", "cnrx_plan_create_ex", "cnrx_plan_options_default", "cnrx_get_plan_options",
-            "cnrx_plan_destroy", "cnrx_last_error", "cnrx_forward", "cnrx_forward_device",
+            "cnrx_plan_destroy", "cnrx_feature_plane_device", "cnrx_last_error", "cnrx_forward", "cnrx_forward_device",
             "cnrx_set_pilots", "cnrx_receive", "cnrx_receive_device", "cnrx_featurize_device",
             "cnrx_receive_sharded", "cnrx_forward_sharded", "cnrx_get_plan_info", "cnrx_set_graph_capture", "cnrx_launch_name",
             "cnrx_set_profiling", "cnrx_read_profile", "cnrx_launch_flops", "cnrx_generate_slots",
@@ -119,6 +119,7 @@ def lib():
     L.cnrx_plan_options_default.argtypes = [C.POINTER(cnrx_plan_options)]
     L.cnrx_plan_options_default.restype = None
     L.cnrx_get_plan_options.argtypes = [vp, C.POINTER(cnrx_plan_options)]
+    L.cnrx_feature_plane_device.argtypes = [vp, vp, i64, i64, i64, i64, vp, C.POINTER(C.c_int32)]
     L.cnrx_plan_destroy.argtypes = [vp]
     L.cnrx_plan_destroy.restype = None
     L.cnrx_last_error.restype = C.c_char_p
@@ -276,6 +277,19 @@ class Plan:
         B, T, F, N = y.shape[:4]
         _check(lib().cnrx_receive_device(self.h, C.c_void_p(y.data_ptr()), B, T, F, N,
                                          C.c_void_p(out.data_ptr()), _stream(stream)))
+
+    def feature_plane(self, y) -> np.ndarray:
+        """Test hook: the 16-bit input-feature plane of a bf16 / fp16 plan for y (torch complex64 CUDA
+        tensor [B,T,F,N]) as float32 [B,T,F,cpad] (the bf16 / fp16 values, exactly)."""
+        import torch
+        B, T, F, N = y.shape[:4]
+        cpad = C.c_int32()
+        buf = torch.empty((B, T, F, 128), dtype=torch.int16, device=y.device)
+        _check(lib().cnrx_feature_plane_device(self.h, C.c_void_p(y.data_ptr()), B, T, F, N,
+                                               C.c_void_p(buf.data_ptr()), C.byref(cpad)))
+        flat = buf.reshape(-1)[: B * T * F * cpad.value].reshape(B, T, F, cpad.value)
+        dt = torch.float16 if self.precision == "fp16" else torch.bfloat16
+        return flat.view(dt).float().cpu().numpy()
 
     def featurize_device(self, y, feat, stream: Optional[int] = None) -> None:
         B, T, F, N = y.shape[:4]

@@ -22,6 +22,26 @@ def slot_range(B: int, world: int, rank: int) -> Tuple[int, int]:
     return b0, min(B, b0 + per)
 
 
+def gather_llr_tensor(local, B: int, world: int, rank: int):
+    """Tensor form of the final LLR gather (bench.py's multi-GPU e2e leg): `local` is this rank's LLR
+    slice [b1-b0, T, F, bits] as a torch tensor on the backend's device (CUDA for NCCL, CPU for gloo),
+    padded here to the ceil-split slice size; rank 0 returns the full [B, T, F, bits] tensor on that
+    device, other ranks None.  One collective (gather), nothing else on the data path."""
+    import torch
+    import torch.distributed as dist
+
+    per = (B + world - 1) // world
+    if local.shape[0] != per:
+        pad = torch.zeros((per,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        pad[: local.shape[0]] = local
+        local = pad
+    parts = [torch.empty_like(local) for _ in range(world)] if rank == 0 else None
+    dist.gather(local.contiguous(), parts, dst=0)
+    if rank != 0:
+        return None
+    return torch.cat(parts, 0)[:B]
+
+
 def gather_llr(local: np.ndarray, B: int, world: int, rank: int):
     """All ranks pass their LLR slice [b1-b0, T, F, bits]; rank 0 returns the full [B, T, F, bits]."""
     import torch

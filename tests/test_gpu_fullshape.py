@@ -1,0 +1,87 @@
+"""Parity at the BASELINE configs' full shapes (parity was tested at reduced F only).
+
+  * fp32 plans, BIT-EXACT with the oracle (the C restatement pinned to the reference, which has no
+    dilation for cfg3): cfg1 at B = 64 x 72 subcarriers, cfg4 / cfg4m at the full 612-subcarrier grid,
+    and cfg3 at the full 3276-subcarrier, 4-antenna grid.  cfg3's oracle runs on subcarrier crops with a
+    margin of the network's receptive radius (12 3x3 layers x dilation 2 = 24 subcarriers), so the
+    cropped columns are computed from exactly the same inputs; crops at both grid edges and the middle.
+  * the receive path at cfg3's full grid (4 antennas, 24 features, interferer) against the oracle
+    featurizer + forward on the same crops, fp32 tolerance 1e-4 relative.
+  * bf16 / fp16 plans at the full grids against the CPU emulation of their rounding points
+    (relative L2 <= 2e-2 / 5e-3, the whole-network bars of test_gpu_parity / test_gpu_fp16).
+"""
+import numpy as np
+import pytest
+
+import emulate_bf16 as E
+import oracle
+from paper_2510_12739_b200 import graph as G, plan as P, slots
+from test_gpu_parity import assert_fp32
+
+pytestmark = pytest.mark.gpu
+R3 = 12 * 2 + 1  # cfg3 receptive radius along F (12 dilated 3x3 layers), +1 spare
+
+
+def _x(name, B, F, seed):
+    g = G.CONFIGS[name].graph(seed=seed)
+    x = np.random.default_rng(seed).standard_normal((B, 14, F, g.in_channels)).astype(np.float32)
+    return g, x
+
+
+@pytest.mark.parametrize("name,B,F", [("cfg1", 64, 72), ("cfg4", 2, 612), ("cfg4m", 2, 612), ("cfg2", 3, 612)])
+def test_fp32_full_grid_bit_exact(name, B, F):
+    g, x = _x(name, B, F, 31)
+    got, ref = P.Plan(g, "fp32").forward(x), oracle.forward(g, x)
+    assert np.array_equal(got, ref), np.abs(got - ref).max()
+
+
+def _crops(F, width=96):
+    return [(0, width), (F // 2 - width // 2, F // 2 + width // 2), (F - width, F)]
+
+
+def test_fp32_cfg3_full_grid_bit_exact_on_crops():
+    g, x = _x("cfg3", 1, 3276, 32)
+    got = P.Plan(g, "fp32").forward(x)
+    for a, b in _crops(3276):
+        lo, hi = max(0, a - R3), min(3276, b + R3)
+        ref = oracle.forward(g, np.ascontiguousarray(x[:, :, lo:hi]))
+        assert np.array_equal(got[:, :, a:b], ref[:, :, a - lo:b - lo]), (a, np.abs(got[:, :, a:b] - ref[:, :, a - lo:b - lo]).max())
+
+
+def test_fp32_cfg3_receive_full_grid():
+    cfg = G.CONFIGS["cfg3"]
+    b = slots.generate(cfg.link, 1, 33)
+    g = cfg.graph(seed=33)
+    p = P.Plan(g, "fp32")
+    p.set_pilots(b.pilots, b.pilot_mask)
+    got = p.receive(b.y)
+    feat = oracle.featurize(b.y, b.pilots, b.pilot_mask)
+    for a, bb in _crops(cfg.link.F):
+        lo, hi = max(0, a - R3), min(cfg.link.F, bb + R3)
+        ref = oracle.forward(g, np.ascontiguousarray(feat[:, :, lo:hi]))
+        assert_fp32(got[:, :, a:bb], ref[:, :, a - lo:bb - lo])
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp16"])
+@pytest.mark.parametrize("name,B,F", [("cfg3", 1, 3276), ("cfg4", 2, 612), ("cfg4m", 1, 612), ("cfg2", 4, 612)])
+def test_16bit_full_grid_vs_emulation(prec, name, B, F):
+    g, x = _x(name, B, F, 34)
+    got = P.Plan(g, prec).forward(x)
+    emu = E.emulate(g, x, precision=prec)
+    l2 = np.linalg.norm(got - emu) / np.linalg.norm(emu)
+    assert l2 <= (2e-2 if prec == "bf16" else 5e-3), l2
+
+
+def test_malformed_graphs_are_rejected():
+    """validate_graph (api.cpp): shapes the fp32 plan sizes its buffers from must be consistent, as the
+    reference derives them from the tensors themselves."""
+    def bad(mutate):
+        g = G.CONFIGS["cfg2"].graph(seed=1)
+        mutate(g)
+        with pytest.raises(P.CnrxInvalidArgument):
+            P.Plan(g, "fp32")
+    relu = next(i for i, n in enumerate(G.CONFIGS["cfg2"].graph(seed=1).nodes) if n.op == G.OP_RELU)
+    bn = next(i for i, n in enumerate(G.CONFIGS["cfg2"].graph(seed=1).nodes) if n.op == G.OP_BN)
+    bad(lambda g: setattr(g.nodes[relu], "out_channels", g.nodes[relu].out_channels + 8))
+    bad(lambda g: setattr(g.params[g.nodes[bn].beta], "value", np.zeros(3, np.float32)))
+    bad(lambda g: setattr(g.params[g.nodes[bn].rvar], "value", np.ones(5, np.float32)))

@@ -37,6 +37,42 @@ def _worker(rank, world, port, B, q):
     dist.destroy_process_group()
 
 
+def _gather_worker(rank, world, port, B, q):
+    """bench.py's multi-GPU e2e gather at the cfg2 LLR shape [B, 14, 612, 4] (ragged split)."""
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_2510_12739_b200 import shard
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    full_ref = torch.arange(B * 14 * 612 * 4, dtype=torch.float32).reshape(B, 14, 612, 4)
+    b0, b1 = shard.slot_range(B, world, rank)
+    got = shard.gather_llr_tensor(full_ref[b0:b1].clone(), B, world, rank)
+    if rank == 0:
+        q.put(bool(torch.equal(got, full_ref)) and tuple(got.shape) == (B, 14, 612, 4))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _spawn(target, world, *args):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port) + args + (q,)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=5)
+
+
+@pytest.mark.parametrize("B", [3, 8])
+def test_two_rank_llr_gather_cfg2_shape(B):
+    _spawn(_gather_worker, 2, B)
+
+
 @pytest.mark.parametrize("B", [5, 6])
 def test_two_rank_sharded_forward_equals_full(B):
     import torch.multiprocessing as mp
