@@ -5,8 +5,9 @@
     and cfg3 at the full 3276-subcarrier, 4-antenna grid.  cfg3's oracle runs on subcarrier crops with a
     margin of the network's receptive radius (12 3x3 layers x dilation 2 = 24 subcarriers), so the
     cropped columns are computed from exactly the same inputs; crops at both grid edges and the middle.
-  * the receive path at cfg3's full grid (4 antennas, 24 features, interferer) against the oracle
-    featurizer + forward on the same crops, fp32 tolerance 1e-4 relative.
+  * the receive path at cfg3's full grid (4 antennas, 24 features, interferer): the GPU featurizer
+    against the oracle featurizer (rtol 1e-5) and receive == featurize + oracle forward bit for bit on
+    the same crops.
   * bf16 / fp16 plans at the full grids against the CPU emulation of their rounding points
     (relative L2 <= 2e-2 / 5e-3, the whole-network bars of test_gpu_parity / test_gpu_fp16).
 """
@@ -16,7 +17,6 @@ import pytest
 import emulate_bf16 as E
 import oracle
 from paper_2510_12739_b200 import graph as G, plan as P, slots
-from test_gpu_parity import assert_fp32
 
 pytestmark = pytest.mark.gpu
 R3 = 12 * 2 + 1  # cfg3 receptive radius along F (12 dilated 3x3 layers), +1 spare
@@ -49,17 +49,26 @@ def test_fp32_cfg3_full_grid_bit_exact_on_crops():
 
 
 def test_fp32_cfg3_receive_full_grid():
+    """receive == GPU featurize + forward, bit for bit, at cfg3's full grid (the featurizer itself is
+    checked against the oracle featurizer at rtol 1e-5 in test_gpu_featurize; a deep random-weight
+    network amplifies those 1e-7 input differences to ~1e-4, so the forward is compared on the GPU's
+    own features)."""
+    import torch
     cfg = G.CONFIGS["cfg3"]
     b = slots.generate(cfg.link, 1, 33)
     g = cfg.graph(seed=33)
     p = P.Plan(g, "fp32")
     p.set_pilots(b.pilots, b.pilot_mask)
     got = p.receive(b.y)
-    feat = oracle.featurize(b.y, b.pilots, b.pilot_mask)
+    feat_t = torch.empty((1, 14, cfg.link.F, 6 * cfg.link.N), dtype=torch.float32, device="cuda")
+    p.featurize_device(torch.from_numpy(b.y).cuda(), feat_t)
+    torch.cuda.synchronize()
+    feat = feat_t.cpu().numpy()
+    np.testing.assert_allclose(feat, oracle.featurize(b.y, b.pilots, b.pilot_mask), rtol=1e-5, atol=1e-5)
     for a, bb in _crops(cfg.link.F):
         lo, hi = max(0, a - R3), min(cfg.link.F, bb + R3)
         ref = oracle.forward(g, np.ascontiguousarray(feat[:, :, lo:hi]))
-        assert_fp32(got[:, :, a:bb], ref[:, :, a - lo:bb - lo])
+        assert np.array_equal(got[:, :, a:bb], ref[:, :, a - lo:bb - lo]), a
 
 
 @pytest.mark.parametrize("prec", ["bf16", "fp16"])
