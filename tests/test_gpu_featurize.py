@@ -92,5 +92,7 @@ def test_feature_plane_equals_rounded_oracle(prec, case):
     assert plane.shape[-1] >= C and not plane[..., C:].any()  # padding channels are zero
     want = _round16(ref, prec)
     diff = np.abs(plane[..., :C] - want)
-    assert (diff <= _ulp16(want, prec) + 1e-30).all(), (diff.max(), (diff > 0).mean())
+    # one 16-bit ulp, or 1e-6 absolute where the exact value is ~0 (e.g. Im h_hat of a real channel: the
+    # kernel's fp32 complex products leave ~1e-8 residues where the oracle's are exactly zero)
+    assert (diff <= np.maximum(_ulp16(want, prec), 1e-6)).all(), (diff.max(), (diff > 0).mean())
     assert (diff == 0).mean() > 0.999
