@@ -113,19 +113,22 @@ os.makedirs(os.path.dirname(out_path) or ".", exist_ok=True)
 Fi.save_checkpoint(g, out_path)
 
 # held-out evaluation on the B200 plans
-p32, p16 = P.Plan(g, "fp32"), P.Plan(g, "bf16")
-for p in (p32, p16):
+p32, p16, ph = P.Plan(g, "fp32"), P.Plan(g, "bf16"), P.Plan(g, "fp16")
+for p in (p32, p16, ph):
     p.set_pilots(pvals.astype(np.complex64), pmask)
-n_eval, agree, tot = 8, 0, 0
-err = {"net_bf16": 0, "net_fp32": 0, "ls_lmmse": 0, "perfect_csi_lmmse": 0}
+n_eval, agree, agree_h, tot = max(8, 64 // batch), 0, 0, 0
+err = {"net_bf16": 0, "net_fp16": 0, "net_fp32": 0, "ls_lmmse": 0, "perfect_csi_lmmse": 0}
 nbits = 0
 for k in range(n_eval):
     y, bits, h = P.generate_slots_device(link, batch, seed=99, slot0=k * batch, with_h=True)
     l32 = torch.empty((batch, link.T, link.F, link.bits), dtype=torch.float32, device=dev)
     l16 = torch.empty_like(l32)
+    lh = torch.empty_like(l32)
     st = torch.cuda.current_stream().cuda_stream
     p32.receive_device(y, l32, st)
     p16.receive_device(y, l16, st)
+    ph.receive_device(y, lh, st)
+    err["net_fp16"] += int(P.count_bit_errors(lh, bits, data).sum())
     nv = P.slot_noise_var(link, batch, 99, k * batch)
     err["net_fp32"] += int(P.count_bit_errors(l32, bits, data).sum())
     err["net_bf16"] += int(P.count_bit_errors(l16, bits, data).sum())
@@ -134,9 +137,11 @@ for k in range(n_eval):
                                                        bits, data).sum())
     m = data[None, :, :, None].expand_as(l32)
     agree += int(((l32 > 0) == (l16 > 0))[m].sum())
+    agree_h += int(((l32 > 0) == (lh > 0))[m].sum())
     tot += int(m.sum())
     nbits += batch * int(data.sum()) * link.bits
 print(json.dumps({"config": name, "steps": steps, "batch": batch, "train_s": round(train_s, 1),
                   "loss": losses[::max(1, len(losses) // 8)] + [losses[-1]], "checkpoint": out_path,
                   "ber": {k: v / nbits for k, v in err.items()}, "eval_bits": nbits,
-                  "hard_decision_agreement_bf16_vs_fp32": agree / tot}))
+                  "hard_decision_agreement_bf16_vs_fp32": agree / tot,
+                  "hard_decision_agreement_fp16_vs_fp32": agree_h / tot}))
