@@ -59,8 +59,15 @@ constexpr int kBox = 32;
 constexpr int kWSlots = 5;        // conv2 windows in flight
 // warp roles: 0 TMA producer, 1 conv1 UMMA, 2-9 conv1 epilogue, 10-17 conv2 epilogue, 18 and 20 input
 // ReLU, 19 conv2 UMMA
-constexpr int kWarpE2 = 10, kWarpRelu0 = 18, kWarpMma2 = 19, kWarpRelu1 = 20;
-constexpr int kThreads = 21 * 32;
+// input-ReLU warps: 18 and 20 .. (they copy the window with ReLU applied while the tensor core streams;
+// 24 warps keep the same 80-register cap as 21: 6 warps per SM sub-partition either way)
+#ifndef CNRX_BLK_RELU_WARPS
+#define CNRX_BLK_RELU_WARPS 2
+#endif
+constexpr int kReluWarps = CNRX_BLK_RELU_WARPS;
+constexpr int kWarpE2 = 10, kWarpRelu0 = 18, kWarpMma2 = 19;
+constexpr int kThreads = (19 + kReluWarps) * 32;
+__device__ __forceinline__ int relu_index(int warp) { return warp == kWarpRelu0 ? 0 : warp - 19; }
 constexpr int kMaxXStages = 6;
 
 struct BlkLayout {
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       mbar_init(&xempty[s], 1);  // conv2's store thread (residual read) or, for halo tiles, conv1's commit
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&xrfull[s], 2);  // both ReLU warps
+      mbar_init(&xrfull[s], kReluWarps);  // every ReLU warp
       mbar_init(&xrempty[s], 1);
       mbar_init(&sfull[s], 8);
       mbar_init(&sfree[s], 1);
@@ -365,12 +372,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
         trace_cta_window(L.trace, g_start);
       }
     }
-  } else if (warp == kWarpRelu0 || warp == kWarpRelu1) {
+  } else if (warp == kWarpRelu0 || warp > kWarpMma2) {
     // ------------------------------ input ReLU --------------------------------
     if (RELU_IN) {
       const int nchunks = win_rows * (kRB / 16);
-      const int half = (nchunks / 2 + 31) / 32 * 32;
-      const int lo = warp == kWarpRelu0 ? 0 : half, hi = warp == kWarpRelu0 ? half : nchunks;
+      const int per = (nchunks / kReluWarps + 31) / 32 * 32;
+      const int ri = relu_index(warp);
+      const int lo = ri * per < nchunks ? ri * per : nchunks;
+      const int hi = ri == kReluWarps - 1 ? nchunks : (lo + per < nchunks ? lo + per : nchunks);
       long long t_w = 0;
       int s = 0;
       uint32_t ph = 0;

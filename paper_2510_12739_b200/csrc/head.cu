@@ -9,7 +9,7 @@
 // per RE), so the operand rows are streamed by TMA (128-row boxes; 128-byte swizzle for 64 channels)
 // into a shared-memory ring instead of per-thread global loads, which saturated the L1 path at ~3 TB/s.
 // Two threads per plane row (C/2 channels each) do the fold and the GEMV in fp32 and combine with one
-// shuffle.  C in {64, 96, 128}.
+// shuffle.  C in {64, 96}.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -328,7 +328,8 @@ bool launch_nb(const HeadLaunch& L, int total, cudaStream_t s) {
 const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const int* affs, const int* relus,
                             const PlaneGeom& geo, cudaStream_t s) {
   const int C = prog.C;
-  if ((C != 64 && C != 96 && C != 128) || ns < 1 || ns > kHeadMaxPlanes || geo.Nalloc % kHRows != 0) return nullptr;
+  // C in {64, 96} (every BASELINE head); other widths use pointwise.cu's fold kernel
+  if ((C != 64 && C != 96) || ns < 1 || ns > kHeadMaxPlanes || geo.Nalloc % kHRows != 0) return nullptr;
   const int nb = prog.head_bits;
   if (nb != 2 && nb != 4 && nb != 6 && nb != 8) return nullptr;
   HeadLaunch L;
@@ -371,7 +372,6 @@ const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const
   switch (C) {
     case 64: ok = launch_nb<64>(L, total, s); break;
     case 96: ok = launch_nb<96>(L, total, s); break;
-    case 128: ok = launch_nb<128>(L, total, s); break;
     default: break;
   }
   return ok ? "head_tma_kernel" : nullptr;

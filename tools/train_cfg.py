@@ -47,7 +47,9 @@ for i, p in enumerate(g.params):
     if owner is not None and owner.op == G.OP_CONV:
         v = v.permute(3, 2, 0, 1).contiguous()  # [kh,kw,cin,cout] -> [cout,cin,kh,kw]
     tp[i] = torch.nn.Parameter(v, requires_grad=p.learnable)
-opt = torch.optim.Adam([v for v in tp.values() if v.requires_grad], lr=2e-3)
+lr = float(os.environ.get("LR", "2e-3"))
+clip = float(os.environ.get("CLIP", "0"))  # global grad-norm clip (0: off); cfg3's 4-way product needs it
+opt = torch.optim.Adam([v for v in tp.values() if v.requires_grad], lr=lr)
 sched = torch.optim.lr_scheduler.CosineAnnealingLR(opt, steps)
 
 
@@ -95,6 +97,8 @@ for step in range(steps):
     loss = Fn.binary_cross_entropy_with_logits(llr[:, data], bits[:, data].float())
     opt.zero_grad(set_to_none=True)
     loss.backward()
+    if clip > 0:
+        torch.nn.utils.clip_grad_norm_([v for v in tp.values() if v.requires_grad], clip)
     opt.step()
     sched.step()
     if step % 50 == 0 or step == steps - 1:
