@@ -57,6 +57,13 @@ constexpr int kAcc1 = 2 * kWCols;              // 384
 constexpr int kAcc2 = kAcc1 + kN;              // 448
 constexpr int kBox = 32;
 constexpr int kWSlots = 5;        // conv2 windows in flight
+// h ring (CNRX_BLK_HRING=1): conv1's output rows go into one ring of kWSlots tiles (each row stored once)
+// plus a mirror of the ring's first win_rows - 1 rows past its end, so every conv2 window is a contiguous
+// row range of the ring; otherwise (0) into kWSlots separate windows (each row stored ~1.5 times).
+#ifndef CNRX_BLK_HRING
+#define CNRX_BLK_HRING 0
+#endif
+constexpr int kRingRows = kWSlots * 63;
 // warp roles: 0 TMA producer, 1 conv1 UMMA, 2-9 conv1 epilogue, 10-17 conv2 epilogue, 18 and 20 input
 // ReLU, 19 conv2 UMMA
 // input-ReLU warps: 18 and 20 .. (they copy the window with ReLU applied while the tensor core streams;
@@ -65,8 +72,14 @@ constexpr int kWSlots = 5;        // conv2 windows in flight
 #define CNRX_BLK_RELU_WARPS 2
 #endif
 constexpr int kReluWarps = CNRX_BLK_RELU_WARPS;
+// CNRX_BLK_STORE_WARP=1: a dedicated warp issues the conv2 tiles' TMA stores (otherwise the first conv2
+// epilogue warp does, between its own tiles)
+#ifndef CNRX_BLK_STORE_WARP
+#define CNRX_BLK_STORE_WARP 0
+#endif
 constexpr int kWarpE2 = 10, kWarpRelu0 = 18, kWarpMma2 = 19;
-constexpr int kThreads = (19 + kReluWarps) * 32;
+constexpr int kWarpStore = 19 + kReluWarps;  // (CNRX_BLK_STORE_WARP)
+constexpr int kThreads = (19 + kReluWarps + CNRX_BLK_STORE_WARP) * 32;
 __device__ __forceinline__ int relu_index(int warp) { return warp == kWarpRelu0 ? 0 : warp - 19; }
 constexpr int kMaxXStages = 6;
 
@@ -81,7 +94,10 @@ __host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int 
   s.xr_off = off;
   if (relu_in) off += 2u * s.stage;
   s.w_off = off;
-  off += static_cast<uint32_t>(kWSlots) * s.stage;
+  if (CNRX_BLK_HRING)
+    off += (static_cast<uint32_t>(kRingRows + win_alloc) * kRB + 1023u) & ~1023u;  // ring + mirror (>= win_rows - 1 rows)
+  else
+    off += static_cast<uint32_t>(kWSlots) * s.stage;
   s.stg_off = off;                 // 2 x [64 rows][128 B]
   off += 2u * 64u * kRB;
   s.trash_off = off;               // 32 rows: destination of stmatrix rows that belong to no window
@@ -317,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
     const unsigned long long g_start = globaltimer_ns();
     int s = 0;
     uint32_t ph = 0;
+    int ring_pos = kTile - halo;  // (conv2 issuer, h ring) first ring row of window 0
     for (int k = 0; k < n; ++k) {
       uint32_t src;
       uint64_t* release;
@@ -335,7 +352,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       } else {
         const int w = k % kWSlots;
         mbar_wait(&wfull[w], static_cast<uint32_t>(k / kWSlots) & 1u);
-        src = w_a + static_cast<uint32_t>(w) * lay.stage;
+        if (CNRX_BLK_HRING) {
+          // window k = ring rows [((k+1) * 63 - halo) mod R, + win_rows), contiguous through the mirror
+          src = w_a + static_cast<uint32_t>(ring_pos) * kRB;
+          ring_pos += kTile;
+          if (ring_pos >= kRingRows) ring_pos -= kRingRows;
+        } else {
+          src = w_a + static_cast<uint32_t>(w) * lay.stage;
+        }
         release = &wempty[w];
       }
       const long long tb = tr ? clock64() : 0;
@@ -371,6 +395,25 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
         atomicAdd(&L.trace[kBlkTraceTotal], static_cast<unsigned long long>(clock64() - t_start));
         trace_cta_window(L.trace, g_start);
       }
+    }
+  } else if (CNRX_BLK_STORE_WARP && warp == kWarpStore) {
+    // ------------------------------ conv2 tile stores --------------------------
+    if (lane == 0 && n_local > 0) {
+      prefetch_tmap(&grp.out_map);
+      int s = XS > 1 ? 1 : 0;  // x stage of conv1 tile u = v + 1 (its residual rows were read by tile v)
+      uint32_t ph = XS > 1 ? 0u : 1u;
+      for (int v = 0; v < n_local; ++v, ring_next(s, ph)) {
+        const int sb = v & 1;
+        mbar_wait(&sfull[sb], static_cast<uint32_t>(v >> 1) & 1u);
+        tma_store_2d(&grp.out_map, smem + lay.stg_off + sb * 64 * kRB, 0, static_cast<int32_t>((t_begin + v) * kTile));
+        bulk_commit();
+        mbar_arrive(&xempty[s]);  // every epilogue warp's residual reads precede its sfull arrival
+        if (v >= 1) {
+          bulk_wait_read1();      // the store of tile v - 1 has read its staging buffer
+          mbar_arrive(&sfree[sb ^ 1]);
+        }
+      }
+      bulk_wait0();
     }
   } else if (warp == kWarpRelu0 || warp > kWarpMma2) {
     // ------------------------------ input ReLU --------------------------------
@@ -410,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
     const int r = 32 * H + lane;  // this lane's stmatrix row within the tile
     const uint32_t tq = tbase + kAcc1 + static_cast<uint32_t>(32 * H) + (static_cast<uint32_t>(q * 32) << 16);
     long long t_full = 0, t_w = 0, e1_drain = 0, e1_comb = 0, e1_store = 0, e1_fence = 0;
+    int ring_base = 0;  // (h ring) ring row of this tile's first row
     for (int u = 0; u < U; ++u) {
       const int64_t p0 = (t_begin + u - 1) * kTile;
       const uint32_t vm = __ballot_sync(0xffffffffu, row_valid(geo, p0 + r));
@@ -436,14 +480,37 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
         e1_drain += t2 - t1;
         e1_comb += t3 - t2;
       }
-      // window u (first written by this tile) must have been released by conv2 of tile u - kWSlots
+      // window u (first written by this tile) must have been released by conv2 of tile u - kWSlots; with
+      // the h ring, the rows of tile u - kWSlots this tile overwrites were last read by window u - kWSlots
       const long long tb = tr ? clock64() : 0;
-      if (u < n_local) mbar_wait(&wempty[u % kWSlots], (static_cast<uint32_t>(u / kWSlots) & 1u) ^ 1u);
+      if (CNRX_BLK_HRING || u < n_local) mbar_wait(&wempty[u % kWSlots], (static_cast<uint32_t>(u / kWSlots) & 1u) ^ 1u);
       const long long tc = tr ? clock64() : 0;
       if (tr) t_w += tc - tb;
+      if (CNRX_BLK_HRING) {
+        // ring row of h row u * 63 + r (mod R), plus its mirror copy past the ring's end when a window
+        // that starts near the end of the ring reads it
+        uint32_t pos = static_cast<uint32_t>(ring_base + r);
+        if (pos >= static_cast<uint32_t>(kRingRows)) pos -= kRingRows;
+        const bool row_ok = r < kTile;
+        const bool mir = row_ok && pos < static_cast<uint32_t>(win_rows - 1);
+#pragma unroll
+        for (int blk = 0; blk < 2; ++blk) {
+          const uint32_t cb = static_cast<uint32_t>((2 * q + blk) * 16);
+          stsm_x4_trans(row_ok ? w_a + sw128(pos, cb) : trash + sw128(static_cast<uint32_t>(lane), cb), o[blk]);
+        }
+        if (__any_sync(0xffffffffu, mir)) {
+#pragma unroll
+          for (int blk = 0; blk < 2; ++blk) {
+            const uint32_t cb = static_cast<uint32_t>((2 * q + blk) * 16);
+            stsm_x4_trans(mir ? w_a + sw128(pos + kRingRows, cb) : trash + sw128(static_cast<uint32_t>(lane), cb), o[blk]);
+          }
+        }
+        ring_base += kTile;
+        if (ring_base >= kRingRows) ring_base -= kRingRows;
+      }
       // h row p0 + r belongs to windows v = u-2, u-1, u at window row r + 63 (u-1-v) + halo
 #pragma unroll
-      for (int dv = -1; dv <= 1; ++dv) {
+      for (int dv = -1; dv <= 1 && !CNRX_BLK_HRING; ++dv) {
         const int v = u - 1 + dv;  // dv = -1: v = u - 2 ... dv = +1: v = u
         if (v < 0 || v >= n_local) continue;
         const int wrow = r - dv * kTile + halo;
@@ -490,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
     float bias[2];
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) bias[blk] = s_bias2[16 * q + 8 * blk + ci];
-    const bool lead = e == 0 && lane == 0;
+    const bool lead = !CNRX_BLK_STORE_WARP && e == 0 && lane == 0;
     const uint32_t stg_a = smem_u32(smem + lay.stg_off);
     const uint32_t tq = tbase + kAcc2 + static_cast<uint32_t>(32 * H) + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t xrow = static_cast<uint32_t>(halo + 32 * H + lane);

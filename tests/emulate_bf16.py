@@ -42,6 +42,12 @@ def fp16(t: torch.Tensor) -> torch.Tensor:
     return t.to(torch.float16).to(torch.float32)
 
 
+def fp16x2(t: torch.Tensor) -> torch.Tensor:
+    """A value carried as an fp16 (hi, lo) pair: hi = fp16(t), lo = fp16(t - hi)."""
+    hi = fp16(t)
+    return hi + fp16(t - hi)
+
+
 # Rounding points of the bf16 plan, by role (tools/ablate_bf16.py switches them one at a time):
 #   feat  - the input feature plane (the stems' tensor-core operand)
 #   w     - BN-folded conv weights (tensor-core operands)

@@ -13,12 +13,13 @@ from paper_2510_12739_b200 import graph as G
 from paper_2510_12739_b200 import slots
 
 CKPT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cfg2_trained.cnck")
+CKPT3 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cfg3_trained.cnck")
 pytestmark = pytest.mark.skipif(not os.path.exists(CKPT), reason="trained checkpoint not generated")
 
 
-def _graph():
-    g = G.CONFIGS["cfg2"].graph_fn()
-    Fi.load_checkpoint(g, CKPT)
+def _graph(name="cfg2"):
+    g = G.CONFIGS[name].graph_fn()
+    Fi.load_checkpoint(g, CKPT if name == "cfg2" else CKPT3)
     return g
 
 
@@ -49,13 +50,13 @@ def test_trained_fp32_bit_exact_with_reference(ref):
     assert np.array_equal(p.forward(feat), oracle.RefNet.from_graph(g).forward(feat))
 
 
-def _decision_run(precisions, n_batches=9, B=32, seed=12345):
+def _decision_run(precisions, n_batches=9, B=32, seed=12345, name="cfg2"):
     """Hard decisions of plans of the given precisions against the fp32 plan (bit-exact with the
-    reference) on n_batches x B GPU-generated cfg2 slots; data bits only (pilots excluded)."""
+    reference) on n_batches x B GPU-generated slots; data bits only (pilots excluded)."""
     import torch
     from paper_2510_12739_b200 import plan as P
-    g = _graph()
-    link = G.CONFIGS["cfg2"].link
+    g = _graph(name)
+    link = G.CONFIGS[name].link
     pmask, pvals = slots.pilot_pattern(link.T, link.F, link.pilot_symbols, link.pilot_spacing)
     plans = {pr: P.Plan(g, pr) for pr in ("fp32",) + tuple(precisions)}
     for p in plans.values():
@@ -108,3 +109,49 @@ def test_trained_fp16_meets_the_decision_bar():
     assert e32 < e_ls                           # the trained receiver beats LS-LMMSE on the same slots
     # bf16: recorded ceiling, not the north-star bar
     assert ab >= 0.999 and abs(rb["err"] / n - ber32) <= 3 * sigma
+
+
+@pytest.mark.skipif(not os.path.exists(CKPT3), reason="cfg3 checkpoint not generated")
+def test_cfg3_checkpoint_loads():
+    g = _graph("cfg3")
+    assert all(g.bn_ready) and g.learnable_count() == G.CONFIGS["cfg3"].graph_fn().learnable_count()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(CKPT3), reason="cfg3 checkpoint not generated")
+def test_trained_cfg3_fp32_bit_exact_and_16bit_decisions():
+    """cfg3 (4 subnets x 6 MRB @ 96, dilation 2, 64-QAM + interferer) with TRAINED weights
+    (tools/train_cfg.py, 8000 steps; profiles/r02_train_cfg3.json: BER 0.170 vs LS-LMMSE 0.202):
+      * the fp32 plan is bit-exact with the oracle (the reference restated with dilation) on crops
+        with the receptive-radius margin, at the full 3276-subcarrier grid;
+      * fp16 / bf16 hard decisions vs fp32 over >= 8 M data bits, same BER within 3 sigma.  The recorded
+        agreement is below the 99.99 % bar that fp16 meets on cfg2: this network sits at BER 0.17, so
+        many more bits are near the decision boundary, and the ablation (tools/ablate_bf16.py CFG=cfg3)
+        shows no single fp32 rounding point closes the gap (fp16 operands alone cap it at ~99.99 %);
+        the fp32 plan is the exact mode."""
+    import oracle
+    import torch
+    from paper_2510_12739_b200 import plan as P
+    g = _graph("cfg3")
+    cfg = G.CONFIGS["cfg3"]
+    b = slots.generate(cfg.link, 1, 5)
+    feat = oracle.featurize(b.y, b.pilots, b.pilot_mask)
+    got = P.Plan(g, "fp32").forward(feat)
+    R = 25
+    for a, e in ((0, 96), (1600, 1696), (3180, 3276)):
+        lo, hi = max(0, a - R), min(3276, e + R)
+        ref = oracle.forward(g, np.ascontiguousarray(feat[:, :, lo:hi]))
+        assert np.array_equal(got[:, :, a:e], ref[:, :, a - lo:e - lo]), a
+    res, e32, e_ls, n = _decision_run(("fp16", "bf16"), n_batches=16, B=4, name="cfg3")
+    assert n >= 8_000_000
+    ber32 = e32 / n
+    sigma = np.sqrt(ber32 * (1 - ber32) / n)
+    r16, rb = res["fp16"], res["bf16"]
+    print(f"cfg3 bits {n}: fp16 agree {r16['agree'] / n:.6f} (confident {r16['conf_agree'] / r16['conf']:.6f}), "
+          f"bf16 agree {rb['agree'] / n:.6f}; BER fp32 {ber32:.5f} fp16 {r16['err'] / n:.5f} bf16 {rb['err'] / n:.5f} "
+          f"LS-LMMSE {e_ls / n:.5f}")
+    assert r16["agree"] / n >= 0.9998 and rb["agree"] / n >= 0.998
+    assert r16["conf_agree"] == r16["conf"]          # every |LLR| >= 1 decision identical
+    for r in (r16, rb):
+        assert abs(r["err"] / n - ber32) <= 3 * sigma
+    assert e32 < e_ls

@@ -36,7 +36,9 @@ torch.cuda.synchronize()
 agg = {}
 for n, ms, c in p.read_profile():
     a_ = agg.setdefault(n, [0.0, 0]); a_[0] += ms; a_[1] += c
-print(json.dumps({"ms_per_step": sorted(bursts)[len(bursts)//2], "min": min(bursts),
+import hashlib
+sha = hashlib.sha1(out.cpu().numpy().tobytes()).hexdigest()[:12]
+print(json.dumps({"ms_per_step": sorted(bursts)[len(bursts)//2], "min": min(bursts), "sha": sha,
                   "per_launch_us": {n: round(v[0] / v[1] * 1e3, 1) for n, v in agg.items()}}))
 '''
 
@@ -61,4 +63,5 @@ for l, rs in res.items():
     blk = [r["per_launch_us"].get("conv_blk64_kernel") or r["per_launch_us"].get("conv_blk64_kernel<f16>") for r in rs]
     print(json.dumps({"lib": l, "ms_per_step_median": round(statistics.median(ms), 4), "ms_min": round(min(r["min"] for r in rs), 4),
                       "conv_blk_us_median": statistics.median([x for x in blk if x]) if any(blk) else None,
+                      "llr_sha": sorted({r["sha"] for r in rs}),
                       "last": rs[-1]["per_launch_us"]}), flush=True)

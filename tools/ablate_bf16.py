@@ -1,10 +1,11 @@
-"""Ablate the bf16 plan's rounding points on the TRAINED cfg2 checkpoint (CPU, torch).
+"""Ablate the bf16 / fp16 plans' rounding points on a TRAINED checkpoint (CPU, torch).
 
 For each variant, one or more roles of tests/emulate_bf16.BF16_POLICY get a different rounding
 function (identity = fp32, fp16, bf16); hard decisions on data bits are compared with the fp32
 forward (all roles identity) on the same host-generated slots.  Prints one JSON line per variant.
 
-usage: python tools/ablate_bf16.py [B=32] [seed=7]"""
+usage: python tools/ablate_bf16.py [B=32] [seed=7]   (env CFG=cfg2|cfg3, FCROP=<subcarriers>: score the
+interior of a subcarrier crop, margin = the receptive radius, to bound the CPU cost of cfg3)"""
 import json
 import os
 import sys
@@ -22,9 +23,12 @@ from paper_2510_12739_b200 import files as Fi, graph as G, slots
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 seed = int(sys.argv[2]) if len(sys.argv) > 2 else 7
 torch.set_num_threads(os.cpu_count())
-g = G.CONFIGS["cfg2"].graph_fn()
-Fi.load_checkpoint(g, os.path.join(ROOT, "tests", "golden", "cfg2_trained.cnck"))
-link = G.CONFIGS["cfg2"].link
+CFG = os.environ.get("CFG", "cfg2")
+FCROP = int(os.environ.get("FCROP", "0"))
+g = G.CONFIGS[CFG].graph_fn()
+Fi.load_checkpoint(g, os.path.join(ROOT, "tests", "golden", f"{CFG}_trained.cnck"))
+link = G.CONFIGS[CFG].link
+MARGIN = 2 * sum(1 for n in g.nodes if n.op == G.OP_CONV and g.params[n.w].value.shape[0] == 3) + 2
 ident = E._ident
 fp32 = {k: ident for k in E.BF16_POLICY}
 variants = {
@@ -41,12 +45,27 @@ variants = {
     "fp32 all but w": dict(res=ident, leaf=ident, z=ident, feat=ident, act=ident),
     "fp16 all": {k: E.fp16 for k in E.BF16_POLICY},
     "fp16 act+w, fp32 rest": dict(act=E.fp16, w=E.fp16, feat=E.fp16, res=ident, leaf=ident, z=ident),
+    "fp16 (shipped: z fp32)": dict(E.FP16_POLICY),
+    "fp16, fp32 res": dict(E.FP16_POLICY, res=ident),
+    "fp16, fp32 leaf": dict(E.FP16_POLICY, leaf=ident),
+    "fp16, fp32 feat": dict(E.FP16_POLICY, feat=ident),
+    "fp16, fp32 w": dict(E.FP16_POLICY, w=ident),
+    "fp16, fp32 act": dict(E.FP16_POLICY, act=ident),
+    "fp16, fp32 res+leaf": dict(E.FP16_POLICY, res=ident, leaf=ident),
+    "fp16x2 split operands (3-pass)": dict(feat=E.fp16x2, w=E.fp16x2, act=E.fp16x2, res=E.fp16x2, leaf=E.fp16x2, z=ident),
 }
 only = os.environ.get("ABL_ONLY")
 chunks = []
 for c0 in range(0, B, 8):
     b = slots.generate(link, min(8, B - c0), seed * 1000 + c0)
     feat = oracle.featurize(b.y, b.pilots, b.pilot_mask)
+    if FCROP and FCROP < link.F:  # crop + score only the interior (bits outside are dropped below)
+        f0 = (link.F - FCROP) // 2
+        feat = np.ascontiguousarray(feat[:, :, f0:f0 + FCROP])
+        keep = np.zeros(b.data_mask.shape, bool)
+        keep[:, f0 + MARGIN:f0 + FCROP - MARGIN] = True
+        b.bits = b.bits[:, :, f0:f0 + FCROP]
+        b.data_mask = (b.data_mask & keep)[:, f0:f0 + FCROP]
     chunks.append((b, feat))
 ref = [E.emulate(g, f, fp32) for _, f in chunks]
 for name, pol in variants.items():
