@@ -57,11 +57,13 @@ constexpr int kAcc1 = 2 * kWCols;              // 384
 constexpr int kAcc2 = kAcc1 + kN;              // 448
 constexpr int kBox = 32;
 constexpr int kWSlots = 5;        // conv2 windows in flight
-// h ring (CNRX_BLK_HRING=1): conv1's output rows go into one ring of kWSlots tiles (each row stored once)
-// plus a mirror of the ring's first win_rows - 1 rows past its end, so every conv2 window is a contiguous
-// row range of the ring; otherwise (0) into kWSlots separate windows (each row stored ~1.5 times).
+// h ring (CNRX_BLK_HRING=1, default): conv1's output rows go into one ring of kWSlots tiles (each row
+// stored once) plus a mirror of the ring's first win_rows - 1 rows past its end, so every conv2 window is
+// a contiguous row range of the ring; otherwise (0) into kWSlots separate windows (each row stored ~1.5
+// times, a third of them through a trash row).  A/B on cfg2 B=256: -3.2 % per block launch
+// (profiles/r02_ab_blk_ring.log), bit-identical LLRs.
 #ifndef CNRX_BLK_HRING
-#define CNRX_BLK_HRING 0
+#define CNRX_BLK_HRING 1
 #endif
 constexpr int kRingRows = kWSlots * 63;
 // warp roles: 0 TMA producer, 1 conv1 UMMA, 2-9 conv1 epilogue, 10-17 conv2 epilogue, 18 and 20 input
@@ -174,9 +176,10 @@ __device__ __forceinline__ void tmem_ld_x1(uint32_t taddr, uint32_t& r) {
 
 __device__ __forceinline__ bool row_valid(const PlaneGeom& geo, int64_t row) { return row >= 0 && geo.valid(row); }
 
-// Accumulator waits of the epilogue warps (16 warps polling): nanosleep back-off of this many ns (0: spin)
+// Accumulator waits of the epilogue warps (16 warps polling): nanosleep back-off of this many ns (0: spin;
+// 64 measured -1 % per launch: fewer polls competing for issue slots)
 #ifndef CNRX_BLK_EPI_SLEEP_NS
-#define CNRX_BLK_EPI_SLEEP_NS 0
+#define CNRX_BLK_EPI_SLEEP_NS 64
 #endif
 __device__ __forceinline__ void epi_acc_wait(uint64_t* bar, uint32_t parity) {
   if (CNRX_BLK_EPI_SLEEP_NS > 0)
