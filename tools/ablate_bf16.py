@@ -52,6 +52,9 @@ variants = {
     "fp16, fp32 w": dict(E.FP16_POLICY, w=ident),
     "fp16, fp32 act": dict(E.FP16_POLICY, act=ident),
     "fp16, fp32 res+leaf": dict(E.FP16_POLICY, res=ident, leaf=ident),
+    "fp16, fp32 feat+leaf": dict(E.FP16_POLICY, feat=ident, leaf=ident),
+    "fp16, fp32 feat+res": dict(E.FP16_POLICY, feat=ident, res=ident),
+    "fp16, fp32 feat+res+leaf": dict(E.FP16_POLICY, feat=ident, res=ident, leaf=ident),
     "fp16x2 split operands (3-pass)": dict(feat=E.fp16x2, w=E.fp16x2, act=E.fp16x2, res=E.fp16x2, leaf=E.fp16x2, z=ident),
 }
 only = os.environ.get("ABL_ONLY")

@@ -51,6 +51,7 @@ def measure(g, B, reps, graph):
         b.record()
         b.synchronize()
         ts.append(a.elapsed_time(b))
+    measure.kernels = sorted(set(p.launch_names()))
     p.close()
     return np.array(ts)
 
@@ -83,7 +84,8 @@ for name, spec in SPECS.items():
         thr = measure(g, 64, 20, False)
         row.update({"latency_b1_ms": {"median": float(np.median(lat)), "p25": float(np.percentile(lat, 25)),
                                       "p75": float(np.percentile(lat, 75)), "runs": runs},
-                    "throughput_b64_slots_per_s": float(64 / (np.median(thr) * 1e-3))})
+                    "throughput_b64_slots_per_s": float(64 / (np.median(thr) * 1e-3)),
+                    "kernels_b64": measure.kernels})
     except Exception as e:  # no GPU / unsupported lowering: graph properties only
         row["measure_error"] = str(e)
     rows[name] = row
