@@ -93,11 +93,15 @@ typedef struct {
   int32_t struct_size;          /* sizeof(cnrx_plan_options): checked for ABI compatibility */
   int32_t fused_blocks;         /* 1: residual blocks of two 64-ch 3x3 convs run as one kernel (default);
                                    0: two weights-stationary conv kernels (env CNRX_BLK=0) */
-  int32_t fused_head;           /* 1: interaction + head in the last convs' epilogue on the two-kernel
-                                   program (BF16 only; env CNRX_HEADFUSE=1); 0 (default): head kernel */
-  int32_t tensor_core_head;     /* 1 (default): 64-ch BF16 heads run their GEMV on the tensor core over
-                                   bf16-rounded z; 0: fp32 CUDA-core GEMV (env CNRX_NO_TMA_HEAD) --
-                                   changes BF16 LLRs by one rounding point; FP16 plans always use fp32 */
+  int32_t fused_head;           /* 1: the CoNet interaction + LLR head run in the epilogues of the
+                                   subnetworks' last convs instead of a separate head kernel (env
+                                   CNRX_HEADFUSE=1): on the fused-block program the last blocks run one
+                                   launch per subnetwork folding into an fp32 partial plane (LLRs
+                                   bit-identical to the head kernel's fp32 GEMV); on the two-kernel
+                                   program (BF16 with tensor_core_head) 3-CTA clusters; 0: head kernel */
+  int32_t tensor_core_head;     /* 1: 64-ch BF16 heads run their GEMV on the tensor core over bf16-rounded
+                                   z (env CNRX_TC_HEAD=1); 0 (default): fp32 CUDA-core GEMV -- one rounding
+                                   point fewer; FP16 plans always use fp32 */
   int32_t cta_pair;             /* 1 (default): 96->96 3x3 convs on CTA pairs (cta_group::2); 0: single
                                    CTA (env CNRX_NO_PAIR=1) */
   int32_t weights_stationary;   /* 1 (default): 64->64 3x3 convs with the weights in TMEM; 0: the generic

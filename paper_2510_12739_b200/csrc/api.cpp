@@ -198,10 +198,14 @@ struct Workspace {
     TcLaunch tc;
     WsLaunch wsl;
     BlkLaunch blkl;
+    std::vector<BlkLaunch> chain;  // fused-block head: one block launch per subnetwork, in fold order
   };
   std::vector<GroupLaunch> launches;  // prepared tensor maps per TC group (bf16)
   bool blocks_fused = false;          // residual blocks run as conv_blk64 at this batch size
   bool head_fused = false;            // the head runs in the last convs' epilogue (two-kernel program)
+  bool head_blk_fused = false;        // ... in the last fused blocks' conv2 epilogues (fused-block program)
+  void* fold_bufs[2] = {nullptr, nullptr};  // fp32 partial-fold planes [Nalloc][64] of the fused-block head
+  size_t fold_bytes = 0;
 };
 
 }  // namespace
@@ -244,6 +248,10 @@ struct cnrx_plan {
   // fused interaction + LLR head (conv_ws.cu kWsHead): the tc group (level, index) whose convs produce
   // every operand of the head's fold, in fold order, and the head's pointwise step it replaces
   int hf_level = -1, hf_group = -1, hf_pw = -1;
+  // interaction + head folded into the last fused blocks (conv_blk.cu BlkFold): the tc group (level, index)
+  // of those blocks, its ops in fold order, the head's pointwise step, and the fold steps
+  int hb_level = -1, hb_group = -1, hb_pw = -1, hb_ns = 0;
+  int hb_ops[kPwMaxPlanes] = {}, hb_affs[kPwMaxPlanes] = {}, hb_relus[kPwMaxPlanes] = {}, hb_tc[kPwMaxPlanes] = {};
   WsHead hf{};
   bool need_plane0 = true;     // some kernel reads the input-feature plane
   std::vector<int> buf_channels;  // plane buffers
@@ -796,6 +804,59 @@ struct Bf16Compiler {
     }
   }
 
+  // The CoNet interaction + LLR head folded into the subnetworks' last fused residual blocks (conv_blk.cu
+  // BlkFold, fused-block program): the head is a fold over 64-channel planes each written by the conv2 of
+  // a fused block (ReLU'd block input, residual, no other reader) of one launch group.  The group then
+  // runs as one launch per subnetwork in fold order (ensure_workspace builds the chain); LLRs equal the
+  // separate head kernel's fp32 GEMV path bit for bit.  cnrx_plan_options::fused_head.
+  void fuse_head_blk() {
+    if (p.opt.fused_head != 1 || p.opt.fused_blocks == 0) return;
+    const int hk = static_cast<int>(p.pw.size()) - 1;
+    if (hk < 0) return;
+    const PwStep& hs = p.pw[static_cast<size_t>(hk)];
+    int ns = 0, ops[kPwMaxPlanes], affs[kPwMaxPlanes], relus[kPwMaxPlanes];
+    if (hs.out_plane >= 0 || hs.prog.C != 64 || hs.prog.head_bits < 1 || hs.prog.head_bits > 8) return;
+    if (!pw_as_fold(hs.prog, &ns, ops, affs, relus) || hs.prog.n_planes_used != ns || ns < 2 || ns > 4) return;
+    std::vector<int> readers(p.planes.size(), 0);
+    for (const auto& op : p.tc) {
+      if (op.in_plane >= 0) ++readers[static_cast<size_t>(op.in_plane)];
+      if (op.res_plane >= 0) ++readers[static_cast<size_t>(op.res_plane)];
+    }
+    for (const auto& st : p.pw)
+      for (int k = 0; k < st.n_planes; ++k) ++readers[static_cast<size_t>(st.plane_ids[k])];
+    std::vector<int> prod(static_cast<size_t>(ns));
+    for (int k = 0; k < ns; ++k) {
+      const int pl = hs.plane_ids[k];
+      const int t = plane_producer_tc[static_cast<size_t>(pl)];
+      if (t < 0 || readers[static_cast<size_t>(pl)] != 1) return;
+      const TcOp& op = p.tc[static_cast<size_t>(t)];
+      if (op.blk_c1 < 0 || op.out_plane != pl || op.out2_plane >= 0 || op.relu || op.res_plane < 0) return;
+      if (!p.tc[static_cast<size_t>(op.blk_c1)].relu_in) return;  // fold epilogues exist for ReLU'd inputs
+      prod[static_cast<size_t>(k)] = t;
+    }
+    const int lv = p.tc[static_cast<size_t>(prod[0])].level;
+    auto& groups = p.tc_groups_by_level[static_cast<size_t>(lv)];
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      auto& grp = groups[gi];
+      if (static_cast<int>(grp.size()) != ns) continue;
+      bool all = true;
+      for (int t : prod)
+        if (std::find(grp.begin(), grp.end(), t) == grp.end()) all = false;
+      if (!all) continue;
+      p.hb_level = lv;
+      p.hb_group = static_cast<int>(gi);
+      p.hb_pw = hk;
+      p.hb_ns = ns;
+      for (int k = 0; k < ns; ++k) {
+        p.hb_ops[k] = ops[k];
+        p.hb_affs[k] = affs[k];
+        p.hb_relus[k] = relus[k];
+        p.hb_tc[k] = prod[static_cast<size_t>(k)];
+      }
+      return;
+    }
+  }
+
   void compile() {
     const int n = static_cast<int>(p.nodes.size());
     node_plane.assign(static_cast<size_t>(n), -1);
@@ -977,6 +1038,7 @@ struct Bf16Compiler {
     for (int k = 0; k < static_cast<int>(p.pw.size()); ++k)
       p.pw_by_level[static_cast<size_t>(p.pw[static_cast<size_t>(k)].level)].push_back(k);
     fuse_head();
+    fuse_head_blk();
     // out2 planes share their producer's level; every plane is live from its level to last use
     for (auto& op : p.tc) {
       if (op.out2_plane >= 0) p.planes[static_cast<size_t>(op.out2_plane)].level = op.level;
@@ -1087,6 +1149,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
   }
   ws.blocks_fused = fused;
   ws.head_fused = false;
+  ws.head_blk_fused = false;
   for (int lv = 0; lv < p.n_levels; ++lv)
     for (size_t gidx = 0; gidx < p.tc_groups_by_level[static_cast<size_t>(lv)].size(); ++gidx) {
       auto& grp = p.tc_groups_by_level[static_cast<size_t>(lv)][gidx];
@@ -1131,6 +1194,51 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
         L.win_alloc = win_alloc;
         L.xstages = conv_blk64_xstages(win_alloc, L.relu_in);
         if (L.xstages == 0) throw Error(CNRX_ERR_UNSUPPORTED, "fused residual block exceeds shared memory (fused_blocks = 0)");
+        if (lv == p.hb_level && static_cast<int>(gidx) == p.hb_group) {
+          // interaction + head folded into these blocks: one launch per subnetwork, in fold order
+          const PwProgram& hp = p.pw[static_cast<size_t>(p.hb_pw)].prog;
+          const size_t fbytes = static_cast<size_t>(ws.geo.Nalloc) * 64 * sizeof(float);
+          const int nbuf = p.hb_ns > 3 ? 2 : (p.hb_ns > 2 ? 1 : 0);
+          if (ws.fold_bytes < fbytes) {
+            for (void*& b : ws.fold_bufs) {
+              if (b) cudaFree(b);
+              b = nullptr;
+            }
+            ws.fold_bytes = 0;
+            for (int i = 0; i < nbuf; ++i) CNRX_CUDA(cudaMalloc(&ws.fold_bufs[i], fbytes));
+            ws.fold_bytes = fbytes;
+          }
+          for (int k = 0; k < p.hb_ns; ++k) {
+            size_t gi = 0;
+            while (grp[gi] != p.hb_tc[k]) ++gi;
+            BlkLaunch C = L;
+            C.ngroups = 1;
+            C.g[0] = L.g[gi];
+            C.epi = k == 0 ? 0 : (k == p.hb_ns - 1 ? 2 : 1);
+            if (C.epi) {
+              BlkFold& f = C.fold;
+              std::memset(&f, 0, sizeof(f));
+              const bool f32 = k >= 2;
+              const void* opnd = f32 ? ws.fold_bufs[(k - 1) & 1]
+                                     : plane_ptr(p.tc[static_cast<size_t>(p.hb_tc[0])].out_plane);
+              conv_blk64_make_fold_maps(opnd, f32, C.epi == 1 ? ws.fold_bufs[k & 1] : nullptr, ws.geo.Nalloc, &f);
+              f.s_prev = p.hb_affs[0] >= 0 ? hp.aff_s[p.hb_affs[0]] : nullptr;
+              f.t_prev = p.hb_affs[0] >= 0 ? hp.aff_t[p.hb_affs[0]] : nullptr;
+              f.relu_prev = p.hb_relus[0];
+              f.op = p.hb_ops[k];
+              f.s = p.hb_affs[k] >= 0 ? hp.aff_s[p.hb_affs[k]] : nullptr;
+              f.t = p.hb_affs[k] >= 0 ? hp.aff_t[p.hb_affs[k]] : nullptr;
+              f.relu = p.hb_relus[k];
+              f.head_w = hp.head_w;
+              f.head_b = hp.head_b;
+              f.nb = hp.head_bits;
+              C.xstages = conv_blk64_xstages(win_alloc, C.relu_in, C.epi);
+              if (C.xstages == 0) throw Error(CNRX_ERR_UNSUPPORTED, "fused-block head exceeds shared memory");
+            }
+            GL.chain.push_back(C);
+          }
+          ws.head_blk_fused = true;
+        }
       } else if (op0.ws) {
         WsLaunch& L = GL.wsl;
         std::memset(&L, 0, sizeof(L));
@@ -1351,6 +1459,17 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
           CNRX_CUDA(cudaMemsetAsync(dtrace, 0, 32 * sizeof(unsigned long long), s));
           GL.blkl.trace = dtrace;
         }
+        if (!GL.chain.empty()) {
+          const PwProgram& hp = p.pw[static_cast<size_t>(p.hb_pw)].prog;
+          for (size_t k = 0; k < GL.chain.size(); ++k) {
+            BlkLaunch& C = GL.chain[k];
+            C.fold.llr = out;
+            const int64_t flc = fl / static_cast<int64_t>(GL.chain.size()) +
+                                (C.epi == 2 ? 2ll * hp.C * hp.head_bits : 0);
+            p.note(conv_blk64_launch(C, p.num_sms, s), s, flc);
+          }
+          continue;
+        }
         p.note(conv_blk64_launch(GL.blkl, p.num_sms, s), s, fl);
         if (trace) {
           unsigned long long h[kBlkTraceSlots];
@@ -1428,7 +1547,8 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
       }
     }
     for (int k : p.pw_by_level[static_cast<size_t>(lv)]) {
-      if (ws.head_fused && k == p.hf_pw) continue;  // ran in the last convs' epilogue
+      if (ws.head_fused && k == p.hf_pw) continue;      // ran in the last convs' epilogue
+      if (ws.head_blk_fused && k == p.hb_pw) continue;  // ran in the last fused blocks' epilogues
       PwStep& st = p.pw[static_cast<size_t>(k)];
       PwProgram prog = st.prog;
       prog.fp16 = p.fp16;
@@ -1764,7 +1884,7 @@ void cnrx_plan_options_default(cnrx_plan_options* o) {
   o->struct_size = static_cast<int32_t>(sizeof(*o));
   o->fused_blocks = 1;
   o->fused_head = 0;
-  o->tensor_core_head = 1;
+  o->tensor_core_head = 0;
   o->cta_pair = 1;
   o->weights_stationary = 1;
   o->relu_on_load = 1;
@@ -1785,6 +1905,7 @@ void apply_env_options(cnrx_plan_options* o) {
   if (env_int("CNRX_BLK", &v)) o->fused_blocks = v != 0;
   if (std::getenv("CNRX_HEADFUSE")) o->fused_head = 1;
   if (std::getenv("CNRX_NO_HEADFUSE")) o->fused_head = 0;
+  if (std::getenv("CNRX_TC_HEAD")) o->tensor_core_head = 1;
   if (std::getenv("CNRX_NO_TMA_HEAD")) o->tensor_core_head = 0;
   if (env_int("CNRX_NO_PAIR", &v) && v != 0) o->cta_pair = 0;
   if (std::getenv("CNRX_NO_WS")) o->weights_stationary = 0;
@@ -1882,6 +2003,8 @@ void cnrx_plan_destroy(cnrx_plan* plan) {
   if (plan->ws.out_buf) cudaFree(plan->ws.out_buf);
   if (plan->ws.feat_buf) cudaFree(plan->ws.feat_buf);
   if (plan->ws.classic_buf) cudaFree(plan->ws.classic_buf);
+  for (void* b : plan->ws.fold_bufs)
+    if (b) cudaFree(b);
   if (plan->classic_done) cudaEventDestroy(plan->classic_done);
   for (void* d : plan->dev_allocs) cudaFree(d);
   for (auto& evs : plan->prof_events)

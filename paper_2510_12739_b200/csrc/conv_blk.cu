@@ -39,6 +39,7 @@
 #include <cstring>
 
 #include "conv_blk.h"
+#include "kernels.h"
 #include "elem16.cuh"
 #include "sm100.cuh"
 
@@ -56,7 +57,10 @@ constexpr int kWCols = kPairs * kKSteps * 8;  // 192 TMEM columns per weight set
 constexpr int kAcc1 = 2 * kWCols;              // 384
 constexpr int kAcc2 = kAcc1 + kN;              // 448
 constexpr int kBox = 32;
-constexpr int kWSlots = 5;        // conv2 windows in flight
+#ifndef CNRX_BLK_WSLOTS
+#define CNRX_BLK_WSLOTS 5
+#endif
+constexpr int kWSlots = CNRX_BLK_WSLOTS;  // conv2 windows in flight
 // h ring (CNRX_BLK_HRING=1, default): conv1's output rows go into one ring of kWSlots tiles (each row
 // stored once) plus a mirror of the ring's first win_rows - 1 rows past its end, so every conv2 window is
 // a contiguous row range of the ring; otherwise (0) into kWSlots separate windows (each row stored ~1.5
@@ -86,9 +90,10 @@ __device__ __forceinline__ int relu_index(int warp) { return warp == kWarpRelu0 
 constexpr int kMaxXStages = 6;
 
 struct BlkLayout {
-  uint32_t x_off, stage, xr_off, w_off, stg_off, trash_off, par_off, bar_off, total;
+  uint32_t x_off, stage, xr_off, w_off, stg_off, trash_off, f_off, par_off, bar_off, total;
 };
-__host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int relu_in) {
+constexpr uint32_t kF32Tile = 64u * 256u;  // one 64-row tile of fp32 channels (fold operand / partial / z)
+__host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int relu_in, int epi = 0) {
   BlkLayout s{};
   s.stage = static_cast<uint32_t>(win_alloc * kRB);  // multiple of 4 KB
   s.x_off = 0;
@@ -100,12 +105,15 @@ __host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int 
     off += (static_cast<uint32_t>(kRingRows + win_alloc) * kRB + 1023u) & ~1023u;  // ring + mirror (>= win_rows - 1 rows)
   else
     off += static_cast<uint32_t>(kWSlots) * s.stage;
-  s.stg_off = off;                 // 2 x [64 rows][128 B]
-  off += 2u * 64u * kRB;
+  s.stg_off = off;                 // 2 x [64 rows][128 B]; fold epilogues: 2 x [64 rows][64 fp32]
+  off += epi ? 2u * kF32Tile : 2u * 64u * kRB;
   s.trash_off = off;               // 32 rows: destination of stmatrix rows that belong to no window
   off += 32u * kRB;
-  s.par_off = off;                 // bias1, bias2
+  s.f_off = off;                   // fold epilogues: 2 operand tiles (16-bit or fp32 rows)
+  if (epi) off += 2u * kF32Tile;
+  s.par_off = off;                 // bias1, bias2; fold: s_prev, t_prev, s, t [64] + head w [64][8], b [8]
   off += 2u * kC * 4u;
+  if (epi) off += (4u * kC + kC * 8u + 8u) * 4u;
   s.bar_off = off;                 // 34 mbarriers + the TMEM address slot
   s.total = off + 512 + 1024;
   return s;
@@ -188,13 +196,13 @@ __device__ __forceinline__ void epi_acc_wait(uint64_t* bar, uint32_t parity) {
     mbar_wait(bar, parity);
 }
 
-template <bool RELU_IN, bool TRACE, bool F16>
+template <bool RELU_IN, bool TRACE, bool F16, int EPI>
 __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_constant__ BlkLaunch L) {
   constexpr uint32_t IDESC = idesc_e16_f32<F16>(128, kN);
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
   const int XS = L.xstages;
-  const BlkLayout lay = blk_layout(XS, L.win_alloc, RELU_IN);
+  const BlkLayout lay = blk_layout(XS, L.win_alloc, RELU_IN, EPI);
   float* s_bias1 = reinterpret_cast<float*>(smem + lay.par_off);
   float* s_bias2 = s_bias1 + kC;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.bar_off);
@@ -210,7 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
   uint64_t* t2empty = t2full + 1;
   uint64_t* sfull = t2empty + 1;            // [2] staging buffer written by all conv2-epilogue warps
   uint64_t* sfree = sfull + 2;              // [2] staging buffer read by its TMA store
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
+  uint64_t* ffull = sfree + 2;              // [2] fold operand tile landed
+  uint64_t* fempty = ffull + 2;             // [2] fold operand tile consumed by all conv2-epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fempty + 2);
+  float* s_fold = s_bias2 + kC;             // (EPI) s_prev, t_prev, s, t [64] each, head w [64][8], b [8]
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -237,6 +248,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       mbar_init(&xrempty[s], 1);
       mbar_init(&sfull[s], 8);
       mbar_init(&sfree[s], 1);
+      mbar_init(&ffull[s], 1);
+      mbar_init(&fempty[s], 8);
     }
     for (int s = 0; s < kWSlots; ++s) {
       mbar_init(&wfull[s], 8 * 3);  // 8 conv1-epilogue warps x the 3 conv1 tiles a window spans
@@ -249,8 +262,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
     fence_barrier_init();
   }
   if (threadIdx.x >= 64 && threadIdx.x < 64 + kC) {
-    s_bias1[threadIdx.x - 64] = grp.bias1[threadIdx.x - 64];
-    s_bias2[threadIdx.x - 64] = grp.bias2[threadIdx.x - 64];
+    const int c = threadIdx.x - 64;
+    s_bias1[c] = grp.bias1[c];
+    s_bias2[c] = grp.bias2[c];
+    if (EPI) {
+      const BlkFold& fd = L.fold;
+      s_fold[c] = fd.s_prev ? fd.s_prev[c] : 1.f;
+      s_fold[kC + c] = fd.t_prev ? fd.t_prev[c] : 0.f;
+      s_fold[2 * kC + c] = fd.s ? fd.s[c] : 1.f;
+      s_fold[3 * kC + c] = fd.t ? fd.t[c] : 0.f;
+      if (EPI == 2) {
+        for (int q = 0; q < 8; ++q) s_fold[4 * kC + c * 8 + q] = q < fd.nb ? fd.head_w[c * fd.nb + q] : 0.f;
+        if (c < 8) s_fold[4 * kC + kC * 8 + c] = c < fd.nb ? fd.head_b[c] : 0.f;
+      }
+    }
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -311,6 +336,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
         for (int bx = 0; bx < nboxes; ++bx) tma_load_2d(win + bx * kBox * kRB, &grp.in_map, &xfull[s], 0, r0 + bx * kBox);
       }
       if (tr) atomicAdd(&L.trace[kBlkTraceProd], static_cast<unsigned long long>(t_wait));
+    }
+    if (EPI && lane == 1 && n_local > 0) {
+      // fold operand tiles (one per conv2 tile), double-buffered, consumed by the conv2 epilogue
+      prefetch_tmap(&L.fold.opnd_map);
+      const uint32_t bytes = static_cast<uint32_t>(kTile) * (L.fold.opnd_f32 ? 256u : static_cast<uint32_t>(kRB));
+      for (int v = 0; v < n_local; ++v) {
+        const int fb = v & 1;
+        mbar_wait(&fempty[fb], (static_cast<uint32_t>(v >> 1) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&ffull[fb], bytes);
+        tma_load_2d(smem + lay.f_off + fb * kF32Tile, &L.fold.opnd_map, &ffull[fb], 0,
+                    static_cast<int32_t>((t_begin + v) * kTile));
+      }
     }
   } else if (warp == 1 || warp == kWarpMma2) {
     // ------------------------------ UMMA issuers ------------------------------
@@ -550,6 +587,149 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
     }
   } else {
     // ------------------------------ conv2 epilogue (warps 10-17) --------------
+   if constexpr (EPI != 0) {
+    // interaction fold (BlkFold): y (16-bit rounded, as the separate head kernel would read it) is combined
+    // with the fold so far; mid launches store the fp32 partial (staged, TMA store), the last launch
+    // writes z to shared memory and runs the head GEMV, two threads per row as head.cu does.
+    const int e = warp - kWarpE2;
+    const int q = warp & 3;
+    const int H = (e >> 2) & 1;
+    const int ci = lane >> 2;
+    const int t0 = lane & 3;
+    const PlaneGeom geo = L.geo;
+    const BlkFold& fd = L.fold;
+    float bias[2];
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) bias[blk] = s_bias2[16 * q + 8 * blk + ci];
+    const bool lead = e == 0 && lane == 0;
+    const uint32_t tq = tbase + kAcc2 + static_cast<uint32_t>(32 * H) + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t xrow = static_cast<uint32_t>(halo + 32 * H + lane);
+    const uint32_t srow = static_cast<uint32_t>(32 * H + lane);
+    const int r = 32 * H + lane;
+    const int etid = e * 32 + lane;  // 0..255 over the conv2-epilogue warps
+    if (lead && EPI == 1) prefetch_tmap(&fd.pout_map);
+    int s = XS > 1 ? 1 : 0;  // x stage of conv1 tile u = v + 1
+    uint32_t ph = XS > 1 ? 0u : 1u;
+    for (int v = 0; v < n_local; ++v, ring_next(s, ph)) {
+      const int64_t p0 = (t_begin + v) * kTile;
+      const int sb = v & 1;
+      mbar_wait(&xfull[s], ph);
+      const uint32_t xs_a = x_a + static_cast<uint32_t>(s) * lay.stage;
+      uint32_t res[2][4];
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk) ldsm_x4_trans(xs_a + sw128(xrow, static_cast<uint32_t>((2 * q + blk) * 16)), res[blk]);
+      const uint32_t vm = __ballot_sync(0xffffffffu, row_valid(geo, p0 + r));
+      epi_acc_wait(t2full, static_cast<uint32_t>(v) & 1u);
+      tc_fence_after();
+      uint32_t a0[16], a1[16], xb = 0;
+      tmem_ld16x256b_x4(tq, a0);
+      tmem_ld16x256b_x4(tq + (16u << 16), a1);
+      if (H == 0) tmem_ld_x1(tq + 32, xb);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(t2empty);
+      uint32_t o[2][4];
+      combine_chunk<true, false, F16>(a0, xb, 0, bias[0], res[0], vm >> (2 * t0), lane, o[0]);
+      combine_chunk<true, false, F16>(a1, xb, 1, bias[1], res[1], vm >> (2 * t0), lane, o[1]);
+      // the fold operand of this tile
+      mbar_wait(&ffull[sb], static_cast<uint32_t>(v >> 1) & 1u);
+      const uint32_t fb_a = smem_u32(smem + lay.f_off + sb * kF32Tile);
+      const float* fb_f = reinterpret_cast<const float*>(smem + lay.f_off + sb * kF32Tile);
+      uint32_t op16[2][4];
+      if (!fd.opnd_f32) {
+#pragma unroll
+        for (int blk = 0; blk < 2; ++blk) ldsm_x4_trans(fb_a + sw128(srow, static_cast<uint32_t>((2 * q + blk) * 16)), op16[blk]);
+      }
+      // this thread: channel c = 16q + 8 blk + ci, tile rows 32H + 8i + 2 t0 + j
+      float z[2][4][2];
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk) {
+        const int c = 16 * q + 8 * blk + ci;
+        const float sp = s_fold[c], tp = s_fold[kC + c], sk = s_fold[2 * kC + c], tk = s_fold[3 * kC + c];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 yv = unpack2<F16>(o[blk][i]);
+          const float2 pv16 = fd.opnd_f32 ? make_float2(0.f, 0.f) : unpack2<F16>(op16[blk][i]);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int row = 32 * H + 8 * i + 2 * t0 + j;
+            float prev;
+            if (fd.opnd_f32) {
+              prev = fb_f[row * 64 + c];
+            } else {
+              prev = j ? pv16.y : pv16.x;  // fold step 0 = subnetwork 0's 16-bit output, its BN / ReLU
+              if (fd.s_prev) prev = __fmaf_rn(prev, sp, tp);
+              if (fd.relu_prev) prev = fmaxf(prev, 0.f);
+            }
+            const float y = j ? yv.y : yv.x;
+            float acc = fd.op == PW_MUL ? prev * y : prev + y;
+            if (fd.s) acc = __fmaf_rn(acc, sk, tk);
+            if (fd.relu) acc = fmaxf(acc, 0.f);
+            z[blk][i][j] = acc;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fempty[sb]);
+      float* zb = reinterpret_cast<float*>(smem + lay.stg_off + sb * kF32Tile);  // [64 rows][64] fp32
+      if (EPI == 1) {
+        // staging buffer sb free once the TMA store of tile v - 2 has read it
+        mbar_wait(&sfree[sb], (static_cast<uint32_t>(v >> 1) & 1u) ^ 1u);
+      }
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) zb[(32 * H + 8 * i + 2 * t0 + j) * 64 + 16 * q + 8 * blk + ci] = z[blk][i][j];
+      if (EPI == 1) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfull[sb]);
+        if (lead) {
+          mbar_wait(&sfull[sb], static_cast<uint32_t>(v >> 1) & 1u);
+          tma_store_2d(&fd.pout_map, smem + lay.stg_off + sb * kF32Tile, 0, static_cast<int32_t>(p0));
+          bulk_commit();
+          mbar_arrive(&xempty[s]);  // every warp's residual reads precede its sfull arrival
+          if (v >= 1) {
+            bulk_wait_read1();      // the store of tile v - 1 has read its staging buffer
+            mbar_arrive(&sfree[sb ^ 1]);
+          }
+        }
+      } else {
+        asm volatile("bar.sync 3, 256;" ::: "memory");  // z of the tile complete (all residual reads done)
+        if (lead) mbar_arrive(&xempty[s]);
+        // head GEMV: threads (row, channel half hf, output half qh); per output the summation order of
+        // head.cu's CUDA-core path: fma over the half's 32 channels in order, then half 0 + half 1, + b
+        const int row = etid >> 2, hf = etid & 1, qh = (etid >> 1) & 1;
+        const int nb = fd.nb, q0 = qh * ((nb + 1) / 2), q1 = qh ? nb : (nb + 1) / 2;
+        float part[4] = {0.f, 0.f, 0.f, 0.f};
+        const float* zr = zb + row * 64 + 32 * hf;
+        const float* wf = s_fold + 4 * kC + 32 * hf * 8;
+#pragma unroll 4
+        for (int c = 0; c < 32; ++c) {
+          const float zc = zr[c];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (q0 + k < q1) part[k] = fmaf(zc, wf[c * 8 + q0 + k], part[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) part[k] += __shfl_xor_sync(0xffffffffu, part[k], 1);  // half 0 + half 1
+        const int64_t prow = p0 + row;
+        if (hf == 0 && row < kTile && row_valid(geo, prow)) {
+          int b, t, f;
+          geo.coords(prow, b, t, f);
+          float* dst = fd.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * nb;
+          const float* bb = s_fold + 4 * kC + kC * 8;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (q0 + k < q1) dst[q0 + k] = part[k] + bb[q0 + k];
+        }
+      }
+    }
+    if (lead && EPI == 1) bulk_wait0();
+   } else {
     // Staging buffers are handed over by mbarriers (no group-wide bar.sync): each warp waits for its
     // buffer to be free, writes its 32 rows x 16 channels, arrives; one thread issues the TMA store.
     const int e = warp - kWarpE2;
@@ -631,6 +811,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       atomicAdd(&L.trace[kBlkTraceE2Comb], static_cast<unsigned long long>(e2_comb));
       atomicAdd(&L.trace[kBlkTraceE2Store], static_cast<unsigned long long>(e2_store));
     }
+   }
   }
 
   tc_fence_before();
@@ -664,21 +845,44 @@ void make_map(const void* plane, int64_t nalloc, uint32_t box_rows, CUtensorMap*
   if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
-template <bool RELU_IN, bool TRACE, bool F16>
-void launch_tt(const BlkLaunch& L, int grid, cudaStream_t stream) {
-  const BlkLayout lay = blk_layout(L.xstages, L.win_alloc, RELU_IN);
-  ensure_smem_attr(reinterpret_cast<const void*>(conv_blk64_kernel<RELU_IN, TRACE, F16>), static_cast<int>(lay.total));
-  launch_pdl(conv_blk64_kernel<RELU_IN, TRACE, F16>, dim3(grid), dim3(kThreads), lay.total, stream, L);
+void make_map_f32(const void* plane, int64_t nalloc, uint32_t box_rows, CUtensorMap* m) {
+  std::memset(m, 0, sizeof(CUtensorMap));
+  if (!plane) return;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(kC), static_cast<cuuint64_t>(nalloc)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(kC * 4)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kC), box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn_blk()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(plane), dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
-// the per-role trace counters are a bf16-only debug instantiation
+
+template <bool RELU_IN, bool TRACE, bool F16, int EPI>
+void launch_tt(const BlkLaunch& L, int grid, cudaStream_t stream) {
+  const BlkLayout lay = blk_layout(L.xstages, L.win_alloc, RELU_IN, EPI);
+  ensure_smem_attr(reinterpret_cast<const void*>(conv_blk64_kernel<RELU_IN, TRACE, F16, EPI>), static_cast<int>(lay.total));
+  launch_pdl(conv_blk64_kernel<RELU_IN, TRACE, F16, EPI>, dim3(grid), dim3(kThreads), lay.total, stream, L);
+}
+// the per-role trace counters are a bf16-only debug instantiation; the fold epilogues take a ReLU'd input
+// (the last blocks of MRB subnetworks)
 template <bool RELU_IN>
 void launch_t(const BlkLaunch& L, int grid, cudaStream_t stream) {
-  if (L.fp16)
-    launch_tt<RELU_IN, false, true>(L, grid, stream);
-  else if (L.trace)
-    launch_tt<RELU_IN, true, false>(L, grid, stream);
-  else
-    launch_tt<RELU_IN, false, false>(L, grid, stream);
+  if (RELU_IN && L.epi == 1) {
+    if (L.fp16) launch_tt<true, false, true, 1>(L, grid, stream);
+    else launch_tt<true, false, false, 1>(L, grid, stream);
+  } else if (RELU_IN && L.epi == 2) {
+    if (L.fp16) launch_tt<true, false, true, 2>(L, grid, stream);
+    else launch_tt<true, false, false, 2>(L, grid, stream);
+  } else if (L.epi) {
+    throw Error(4, "internal: fused-block fold epilogue needs a ReLU'd block input");
+  } else if (L.fp16) {
+    launch_tt<RELU_IN, false, true, 0>(L, grid, stream);
+  } else if (L.trace) {
+    launch_tt<RELU_IN, true, false, 0>(L, grid, stream);
+  } else {
+    launch_tt<RELU_IN, false, false, 0>(L, grid, stream);
+  }
 }
 
 }  // namespace
@@ -695,13 +899,22 @@ void conv_blk64_make_maps(const void* in, const void* out, int64_t nalloc, BlkGr
   make_map(out, nalloc, kTile, &g->out_map);
 }
 
-size_t conv_blk64_smem_bytes(int xstages, int win_alloc, int relu_in) {
-  return blk_layout(xstages, win_alloc, relu_in).total;
+void conv_blk64_make_fold_maps(const void* opnd, bool opnd_f32, const void* pout, int64_t nalloc, BlkFold* f) {
+  if (opnd_f32)
+    make_map_f32(opnd, nalloc, kTile, &f->opnd_map);
+  else
+    make_map(opnd, nalloc, kTile, &f->opnd_map);
+  make_map_f32(pout, nalloc, kTile, &f->pout_map);
+  f->opnd_f32 = opnd_f32 ? 1 : 0;
 }
 
-int conv_blk64_xstages(int win_alloc, int relu_in) {
+size_t conv_blk64_smem_bytes(int xstages, int win_alloc, int relu_in, int epi) {
+  return blk_layout(xstages, win_alloc, relu_in, epi).total;
+}
+
+int conv_blk64_xstages(int win_alloc, int relu_in, int epi) {
   for (int xs = kMaxXStages; xs >= 4; --xs)
-    if (blk_layout(xs, win_alloc, relu_in).total <= 227u * 1024u) return xs;
+    if (blk_layout(xs, win_alloc, relu_in, epi).total <= 227u * 1024u) return xs;
   return 0;
 }
 
@@ -713,7 +926,7 @@ const char* conv_blk64_launch(const BlkLaunch& L, int num_sms, cudaStream_t stre
     launch_t<true>(L, grid, stream);
   else
     launch_t<false>(L, grid, stream);
-  return "conv_blk64_kernel";
+  return L.epi == 2 ? "conv_blk64_kernel<fold+head>" : L.epi == 1 ? "conv_blk64_kernel<fold>" : "conv_blk64_kernel";
 }
 
 }  // namespace cnrx

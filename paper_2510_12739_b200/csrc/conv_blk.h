@@ -18,11 +18,34 @@ struct BlkGroup {
   int32_t dil, halo;
 };
 
+// The CoNet interaction + LLR head folded into the last residual blocks' conv2 epilogues (fused_head on
+// the fused-block program): the last blocks of the subnetworks run as one launch per subnetwork, in fold
+// order.  Launch k >= 1 reads the fold so far -- the 16-bit output plane of subnetwork 0 (k = 1, its
+// step-0 BN / ReLU applied on load) or the fp32 partial-fold plane of launch k - 1 -- and combines it with
+// its own output exactly as head.cu's fold does (fp32, the 16-bit-rounded subnetwork output):
+//   acc = prev (op) y; [acc = fma(acc, s, t)]; [relu]
+// Mid launches (EPI 1) store acc as an fp32 plane; the last (EPI 2) runs the 1x1 head on it (fp32, the
+// summation order of head.cu's CUDA-core GEMV) and writes the LLRs.  network.hpp:534-559.
+struct BlkFold {
+  CUtensorMap opnd_map;      // operand tiles (63-row boxes): 16-bit plane (128B swizzle) or fp32 plane
+  CUtensorMap pout_map;      // (EPI 1) fp32 partial-fold plane, 63-row boxes
+  const float* s_prev;       // (16-bit operand) fold step 0's BN scale / shift, nullable
+  const float* t_prev;
+  const float* s;            // this step's BN, nullable
+  const float* t;
+  const float* head_w;       // (EPI 2) [64][nb] fp32, reference 1x1 layout
+  const float* head_b;       // [nb]
+  float* llr;                // [B,T,F,nb]
+  int32_t relu_prev, op, relu, opnd_f32, nb;
+};
+
 struct BlkLaunch {
   BlkGroup g[4];
   PlaneGeom geo;
   int64_t n_tiles;         // 63-row output tiles
   int32_t ngroups, win_alloc, xstages, relu_in;
+  int32_t epi;             // 0: store y; 1 / 2: interaction fold (mid / last + head), ngroups == 1
+  BlkFold fold;
   int32_t fp16;             // planes and weights are fp16 (CNRX_FP16 plans), else bf16
   unsigned long long* trace;  // debug: per-role clock64 totals (kBlkTrace*)
 };
@@ -38,9 +61,11 @@ int64_t conv_blk64_tiles(int64_t nalloc);
 int conv_blk64_win_alloc(int halo);
 bool conv_blk64_supported_halo(int halo);
 void conv_blk64_make_maps(const void* in, const void* out, int64_t nalloc, BlkGroup* g);
+// fold operand / output maps: `opnd` a 16-bit plane (opnd_f32 = 0) or an fp32 partial plane; `pout` (EPI 1)
+void conv_blk64_make_fold_maps(const void* opnd, bool opnd_f32, const void* pout, int64_t nalloc, BlkFold* f);
 // largest x-window ring depth (<= 6) that fits in shared memory, 0 if none
-int conv_blk64_xstages(int win_alloc, int relu_in);
-size_t conv_blk64_smem_bytes(int xstages, int win_alloc, int relu_in);
+int conv_blk64_xstages(int win_alloc, int relu_in, int epi = 0);
+size_t conv_blk64_smem_bytes(int xstages, int win_alloc, int relu_in, int epi = 0);
 const char* conv_blk64_launch(const BlkLaunch& L, int num_sms, cudaStream_t stream);
 
 }  // namespace cnrx

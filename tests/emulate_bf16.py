@@ -185,8 +185,8 @@ def _emulate(g, x, R):
     f = chain(on.in0)
     hw = torch.from_numpy(g.params[on.w].value[0, 0])  # [C,bits]
     hb = torch.from_numpy(g.params[on.b].value) if on.b >= 0 else torch.zeros(hw.shape[1])
-    if hw.shape[0] == 64 and hw.shape[1] in (2, 4, 6, 8) and os.environ.get("CNRX_NO_TMA_HEAD") is None:
-        # 64-channel heads run on the tensor core (head.cu / conv_ws.cu fused head): the folded
+    if hw.shape[0] == 64 and hw.shape[1] in (2, 4, 6, 8) and os.environ.get("CNRX_TC_HEAD") is not None:
+        # opt-in tensor-core head (cnrx_plan_options::tensor_core_head, bf16 plans): the folded
         # interaction z and the head weights are rounded to bf16, products accumulate in fp32
         f, hw = R['z'](f), R['z'](hw)
     out = torch.einsum("bctf,cj->btfj", f, hw) + hb

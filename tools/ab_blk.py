@@ -16,7 +16,8 @@ import torch
 from paper_2510_12739_b200 import graph as G, plan as P, slots
 B = int(os.environ.get("B", "256")); prec = os.environ.get("PREC", "bf16")
 cfg = G.CONFIGS["cfg2"]; b = slots.generate(cfg.link, B, 1)
-p = P.Plan(cfg.graph(seed=1), prec, options={}); p.set_pilots(b.pilots, b.pilot_mask)
+opts = json.loads(os.environ.get("OPTS", "{}"))
+p = P.Plan(cfg.graph(seed=1), prec, options=opts); p.set_pilots(b.pilots, b.pilot_mask)
 y = torch.from_numpy(b.y).cuda(); out = torch.empty((B, 14, cfg.link.F, 4), device="cuda")
 s = torch.cuda.Stream()
 for _ in range(5): p.receive_device(y, out, s.cuda_stream)
@@ -49,8 +50,10 @@ res = {l: [] for l in libs}
 for _ in range(reps):
     for l in libs:
         env = dict(os.environ, ROOT=root)
-        if l != "default":
-            env["CNRX_LIB"] = os.path.abspath(l)
+        lib, _, opt = l.partition("+")  # "lib+opt=1,opt2=0": plan options for this arm
+        if lib != "default":
+            env["CNRX_LIB"] = os.path.abspath(lib)
+        env["OPTS"] = json.dumps({k: float(v) if "." in v else int(v) for k, v in (kv.split("=") for kv in opt.split(",") if kv)})
         r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
         try:
             res[l].append(json.loads(r.stdout.strip().splitlines()[-1]))
@@ -60,7 +63,7 @@ for l, rs in res.items():
     if not rs:
         continue
     ms = [r["ms_per_step"] for r in rs]
-    blk = [r["per_launch_us"].get("conv_blk64_kernel") or r["per_launch_us"].get("conv_blk64_kernel<f16>") for r in rs]
+    blk = [r["per_launch_us"].get("conv_blk64_kernel") for r in rs]
     print(json.dumps({"lib": l, "ms_per_step_median": round(statistics.median(ms), 4), "ms_min": round(min(r["min"] for r in rs), 4),
                       "conv_blk_us_median": statistics.median([x for x in blk if x]) if any(blk) else None,
                       "llr_sha": sorted({r["sha"] for r in rs}),

@@ -20,7 +20,7 @@ prec = sys.argv[2] if len(sys.argv) > 2 else "fp32"
 runs = int(sys.argv[3]) if len(sys.argv) > 3 else 200
 # io_kernel 3: the spec-file templates (3x3 stem/head); 1: 1x1 stem/head as in the BASELINE configs
 # (NetSpec.kernel = 1, BlockSpec.kernel = 3), which the bf16 lowering needs for its pointwise head
-io_kernel = int(sys.argv[4]) if len(sys.argv) > 4 else (1 if prec == "bf16" else 3)
+io_kernel = int(sys.argv[4]) if len(sys.argv) > 4 else (1 if prec in ("bf16", "fp16") else 3)
 T, F, C_IN, BITS = 14, 612, 12, 4  # cfg2 grid and features
 
 SPECS = {
