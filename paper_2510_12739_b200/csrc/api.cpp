@@ -1219,9 +1219,12 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
               BlkFold& f = C.fold;
               std::memset(&f, 0, sizeof(f));
               const bool f32 = k >= 2;
-              const void* opnd = f32 ? ws.fold_bufs[(k - 1) & 1]
+              // mid launch k writes partial buffer (k - 1) & 1; launch k >= 2 reads (k - 2) & 1
+              const void* opnd = f32 ? ws.fold_bufs[(k - 2) & 1]
                                      : plane_ptr(p.tc[static_cast<size_t>(p.hb_tc[0])].out_plane);
-              conv_blk64_make_fold_maps(opnd, f32, C.epi == 1 ? ws.fold_bufs[k & 1] : nullptr, ws.geo.Nalloc, &f);
+              const void* pout = C.epi == 1 ? ws.fold_bufs[(k - 1) & 1] : nullptr;
+              if (!opnd || (C.epi == 1 && !pout)) throw Error(CNRX_ERR_CUDA, "internal: fused-block head buffers");
+              conv_blk64_make_fold_maps(opnd, f32, pout, ws.geo.Nalloc, &f);
               f.s_prev = p.hb_affs[0] >= 0 ? hp.aff_s[p.hb_affs[0]] : nullptr;
               f.t_prev = p.hb_affs[0] >= 0 ? hp.aff_t[p.hb_affs[0]] : nullptr;
               f.relu_prev = p.hb_relus[0];
@@ -1232,6 +1235,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
               f.head_w = hp.head_w;
               f.head_b = hp.head_b;
               f.nb = hp.head_bits;
+              f.dbg = std::getenv("CNRX_FOLD_DEBUG") ? std::atoi(std::getenv("CNRX_FOLD_DEBUG")) : 0;
               C.xstages = conv_blk64_xstages(win_alloc, C.relu_in, C.epi);
               if (C.xstages == 0) throw Error(CNRX_ERR_UNSUPPORTED, "fused-block head exceeds shared memory");
             }

@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       }
       if (tr) atomicAdd(&L.trace[kBlkTraceProd], static_cast<unsigned long long>(t_wait));
     }
-    if (EPI && lane == 1 && n_local > 0) {
+    if (EPI && lane == 1 && n_local > 0 && !(L.fold.dbg & 1)) {
       // fold operand tiles (one per conv2 tile), double-buffered, consumed by the conv2 epilogue
       prefetch_tmap(&L.fold.opnd_map);
       const uint32_t bytes = static_cast<uint32_t>(kTile) * (L.fold.opnd_f32 ? 256u : static_cast<uint32_t>(kRB));
@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       combine_chunk<true, false, F16>(a0, xb, 0, bias[0], res[0], vm >> (2 * t0), lane, o[0]);
       combine_chunk<true, false, F16>(a1, xb, 1, bias[1], res[1], vm >> (2 * t0), lane, o[1]);
       // the fold operand of this tile
-      mbar_wait(&ffull[sb], static_cast<uint32_t>(v >> 1) & 1u);
+      if (!(fd.dbg & 1)) mbar_wait(&ffull[sb], static_cast<uint32_t>(v >> 1) & 1u);
       const uint32_t fb_a = smem_u32(smem + lay.f_off + sb * kF32Tile);
       const float* fb_f = reinterpret_cast<const float*>(smem + lay.f_off + sb * kF32Tile);
       uint32_t op16[2][4];
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
         if (lane == 0) mbar_arrive(&sfull[sb]);
         if (lead) {
           mbar_wait(&sfull[sb], static_cast<uint32_t>(v >> 1) & 1u);
-          tma_store_2d(&fd.pout_map, smem + lay.stg_off + sb * kF32Tile, 0, static_cast<int32_t>(p0));
+          if (!(fd.dbg & 4)) tma_store_2d(&fd.pout_map, smem + lay.stg_off + sb * kF32Tile, 0, static_cast<int32_t>(p0));
           bulk_commit();
           mbar_arrive(&xempty[s]);  // every warp's residual reads precede its sfull arrival
           if (v >= 1) {
@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
 #pragma unroll
         for (int k = 0; k < 4; ++k) part[k] += __shfl_xor_sync(0xffffffffu, part[k], 1);  // half 0 + half 1
         const int64_t prow = p0 + row;
-        if (hf == 0 && row < kTile && row_valid(geo, prow)) {
+        if (hf == 0 && row < kTile && row_valid(geo, prow) && !(fd.dbg & 2)) {
           int b, t, f;
           geo.coords(prow, b, t, f);
           float* dst = fd.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * nb;

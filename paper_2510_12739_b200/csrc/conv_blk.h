@@ -37,6 +37,7 @@ struct BlkFold {
   const float* head_b;       // [nb]
   float* llr;                // [B,T,F,nb]
   int32_t relu_prev, op, relu, opnd_f32, nb;
+  int32_t dbg;               // experiments (CNRX_FOLD_DEBUG): bit 0 no operand loads, 1 no head, 2 no partial store
 };
 
 struct BlkLaunch {
