@@ -92,7 +92,12 @@ constexpr int kMaxXStages = 6;
 struct BlkLayout {
   uint32_t x_off, stage, xr_off, w_off, stg_off, trash_off, f_off, par_off, bar_off, total;
 };
-constexpr uint32_t kF32Tile = 64u * 256u;  // one 64-row tile of fp32 channels (fold operand / partial / z)
+constexpr uint32_t kF32Tile = 64u * 256u;  // one 64-row tile of fp32 channels (fold operand / partial)
+// z tile of the fold + head epilogue: rows of 68 floats, channels 32..63 at +33, so the head GEMV's reads
+// (8 rows x 2 channel halves per warp, same channel) fall in 16 distinct banks
+constexpr int kZStride = 68;
+constexpr uint32_t kZTile = 64u * kZStride * 4u;
+__host__ __device__ constexpr int zidx(int row, int c) { return row * kZStride + (c >= 32 ? c + 1 : c); }
 __host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int relu_in, int epi = 0) {
   BlkLayout s{};
   s.stage = static_cast<uint32_t>(win_alloc * kRB);  // multiple of 4 KB
@@ -105,8 +110,8 @@ __host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int 
     off += (static_cast<uint32_t>(kRingRows + win_alloc) * kRB + 1023u) & ~1023u;  // ring + mirror (>= win_rows - 1 rows)
   else
     off += static_cast<uint32_t>(kWSlots) * s.stage;
-  s.stg_off = off;                 // 2 x [64 rows][128 B]; fold epilogues: 2 x [64 rows][64 fp32]
-  off += epi ? 2u * kF32Tile : 2u * 64u * kRB;
+  s.stg_off = off;                 // 2 x [64 rows][128 B]; fold: 2 x [64 rows][64 fp32] (mid) / 2 z tiles (head)
+  off += epi == 2 ? (2u * kZTile + 1023u) & ~1023u : epi ? 2u * kF32Tile : 2u * 64u * kRB;
   s.trash_off = off;               // 32 rows: destination of stmatrix rows that belong to no window
   off += 32u * kRB;
   s.f_off = off;                   // fold epilogues: 2 operand tiles (16-bit or fp32 rows)
@@ -672,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&fempty[sb]);
-      float* zb = reinterpret_cast<float*>(smem + lay.stg_off + sb * kF32Tile);  // [64 rows][64] fp32
+      float* zb = reinterpret_cast<float*>(smem + lay.stg_off + sb * (EPI == 2 ? kZTile : kF32Tile));
       if (EPI == 1) {
         // staging buffer sb free once the TMA store of tile v - 2 has read it
         mbar_wait(&sfree[sb], (static_cast<uint32_t>(v >> 1) & 1u) ^ 1u);
@@ -682,7 +687,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 2; ++j) zb[(32 * H + 8 * i + 2 * t0 + j) * 64 + 16 * q + 8 * blk + ci] = z[blk][i][j];
+          for (int j = 0; j < 2; ++j) {
+            const int row = 32 * H + 8 * i + 2 * t0 + j, c = 16 * q + 8 * blk + ci;
+            zb[EPI == 2 ? zidx(row, c) : row * 64 + c] = z[blk][i][j];
+          }
       if (EPI == 1) {
         fence_proxy_async_smem();
         __syncwarp();
@@ -705,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
         const int row = etid >> 2, hf = etid & 1, qh = (etid >> 1) & 1;
         const int nb = fd.nb, q0 = qh * ((nb + 1) / 2), q1 = qh ? nb : (nb + 1) / 2;
         float part[4] = {0.f, 0.f, 0.f, 0.f};
-        const float* zr = zb + row * 64 + 32 * hf;
+        const float* zr = zb + zidx(row, 32 * hf);
         const float* wf = s_fold + 4 * kC + 32 * hf * 8;
 #pragma unroll 4
         for (int c = 0; c < 32; ++c) {

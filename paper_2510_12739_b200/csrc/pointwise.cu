@@ -545,9 +545,8 @@ const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaS
     FoldSteps fs{};
     int ns = 0;
     if (pw_as_fold(prog, &ns, fs.op, fs.aff, fs.relu) && prog.n_planes_used == ns) {
-      // the TMA-streamed head kernel; with tensor_core_head disabled on a bf16 plan the fold kernel
-      // below (fp32 GEMV, as before the tensor-core head existed)
-      if (head && (prog.tc_head || prog.fp16)) {
+      // the TMA-streamed head kernel (tensor-core GEMV over bf16 z when the plan asks for it, else fp32)
+      if (head) {
         const char* name = launch_head_tma(prog, ns, fs.op, fs.aff, fs.relu, geo, s);
         if (name) return name;
       }
