@@ -296,10 +296,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
 #pragma unroll 1
     for (int b = 0; b < kPairs * kKSteps; ++b) {
       uint32_t r[8];
-      const uint4* p4 = reinterpret_cast<const uint4*>(src + static_cast<size_t>(b) * 128 * 8);
-      const uint4 v0 = p4[0], v1 = p4[1];
-      r[0] = v0.x; r[1] = v0.y; r[2] = v0.z; r[3] = v0.w;
-      r[4] = v1.x; r[5] = v1.y; r[6] = v1.z; r[7] = v1.w;
+      // one 32-byte load per lane (a warp reads 1 KB contiguous): full sectors, where two 16-byte loads
+      // at a 32-byte lane stride used half of every sector each (ncu: "excessive global sectors")
+      const u32x8 w8 = ldg256(src + static_cast<size_t>(b) * 128 * 8);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = w8.v[k];
       tmem_st8(tbase + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(set * kWCols + b * 8), r);
     }
     tmem_st_wait();

@@ -1,65 +1,44 @@
-"""Summarise an ncu launch list (--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
---csv) per kernel: launches, mean duration, share of the listed time, mean DRAM bytes per launch.
-Writes the per-kernel DRAM traffic that bench.py reports as roofline.traffic (profiles/ncu_traffic.json).
-
-usage: python tools/ncu_summary.py gpurun_out/ncu_launches.csv [out_prefix]"""
-import collections
+"""Summarise an `ncu --set full` report (one or more kernel launches) into the metrics DESIGN.md cites.
+usage: python tools/ncu_summary.py report.ncu-rep > profiles/<name>_summary.txt"""
 import csv
-import json
-import os
-import re
+import io
+import subprocess
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("sm__cycles_elapsed.avg", "SM cycles elapsed (avg)"),
+    ("smsp__cycles_active.avg", "SMSP cycles active (avg)"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active, % of peak sustained (active cycles)"),
+    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe active, % of elapsed (realtime)"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy, %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy, %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "LSU shared-memory wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "shared-load bank conflicts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "shared-store bank conflicts"),
+    ("derived__memory_l1_wavefronts_shared_excessive", "excessive shared wavefronts"),
+    ("derived__memory_l2_theoretical_sectors_global_excessive", "excessive global sectors"),
+    ("dram__bytes_read.sum", "DRAM bytes read"),
+    ("dram__bytes_write.sum", "DRAM bytes written"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput, % of peak"),
+    ("sass__inst_executed_local_loads", "local loads (SASS)"),
+    ("sass__inst_executed_local_stores", "local stores (SASS)"),
+    ("launch__registers_per_thread", "registers per thread"),
+    ("launch__shared_mem_per_block_dynamic", "dynamic shared memory per CTA"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("smsp__inst_executed.sum", "instructions executed"),
+]
 
-# library launch names (cnrx_launch_name) <- demangled ncu kernel names
-ALIASES = [(r"conv_ws64_kernel", "conv_ws64_kernel"), (r"conv_tc_kernel<(\d+), ?(\d+), ?(\d+)>", r"conv_tc_kernel<\1,\2,\3>"),
-           (r"head_tma_kernel", "head_tma_kernel"), (r"featurize_kernel<1", "featurize_kernel<plane>"),
-           (r"pw_fold_kernel", "pw_fold_kernel<head>")]
-
-
-def short(name):
-    for pat, rep in ALIASES:
-        m = re.search(pat, name)
-        if m:
-            return m.expand(rep)
-    return name.split("(")[0][:60]
-
-
-def main():
-    path = sys.argv[1]
-    prefix = sys.argv[2] if len(sys.argv) > 2 else None
-    rows = [r for r in csv.reader(open(path)) if r]
-    hdr = next(i for i, r in enumerate(rows) if r[0] == "ID")
-    H = rows[hdr]
-    per = collections.defaultdict(dict)
-    names = {}
-    for r in rows[hdr + 1:]:
-        if len(r) != len(H):
-            continue
-        d = dict(zip(H, r))
-        per[d["ID"]][d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
-        names[d["ID"]] = short(d["Kernel Name"])
-    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
-    for i, m in per.items():
-        a = agg[names[i]]
-        a[0] += 1
-        a[1] += m.get("gpu__time_duration.sum", 0.0)
-        a[2] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
-    total = sum(a[1] for a in agg.values())
-    lines = [f"{'kernel':32s} {'launches':>8s} {'mean us':>9s} {'share':>7s} {'DRAM MB/launch':>15s} {'GB/s':>8s}"]
-    traffic = {}
-    for k, (n, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        lines.append(f"{k:32s} {n:8d} {t / n / 1e3:9.1f} {t / total:7.1%} {b / n / 1e6:15.1f} {b / t:8.0f}")
-        traffic[k] = b / n
-    print("\n".join(lines))
-    with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
-        json.dump({"source": os.path.basename(path), "unit": "bytes per launch (dram read + write)", **traffic}, f,
-                  indent=1)
-    if prefix:
-        with open(prefix + "_summary.txt", "w") as f:
-            f.write("\n".join(lines) + "\n")
-
-
-if __name__ == "__main__":
-    main()
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units = rows[0], rows[1]
+print(f"# {rep}")
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    u = dict(zip(hdr, units))
+    print(f"\n## {d.get('Kernel Name', '?')[:110]}  (ID {d.get('ID')})")
+    for k, label in KEYS:
+        if k in d:
+            print(f"  {label:58s} {d[k]:>18s} {u.get(k, '')}")
