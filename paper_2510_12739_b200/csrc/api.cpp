@@ -1197,7 +1197,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
         if (lv == p.hb_level && static_cast<int>(gidx) == p.hb_group) {
           // interaction + head folded into these blocks: one launch per subnetwork, in fold order
           const PwProgram& hp = p.pw[static_cast<size_t>(p.hb_pw)].prog;
-          const size_t fbytes = static_cast<size_t>(ws.geo.Nalloc) * 64 * sizeof(float);
+          const size_t fbytes = conv_blk64_part_bytes(ws.geo.Nalloc);
           const int nbuf = p.hb_ns > 3 ? 2 : (p.hb_ns > 2 ? 1 : 0);
           if (ws.fold_bytes < fbytes) {
             for (void*& b : ws.fold_bufs) {
@@ -1222,7 +1222,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
               // mid launch k writes partial buffer (k - 1) & 1; launch k >= 2 reads (k - 2) & 1
               const void* opnd = f32 ? ws.fold_bufs[(k - 2) & 1]
                                      : plane_ptr(p.tc[static_cast<size_t>(p.hb_tc[0])].out_plane);
-              const void* pout = C.epi == 1 ? ws.fold_bufs[(k - 1) & 1] : nullptr;
+              void* pout = C.epi == 1 ? ws.fold_bufs[(k - 1) & 1] : nullptr;
               if (!opnd || (C.epi == 1 && !pout)) throw Error(CNRX_ERR_CUDA, "internal: fused-block head buffers");
               conv_blk64_make_fold_maps(opnd, f32, pout, ws.geo.Nalloc, &f);
               f.s_prev = p.hb_affs[0] >= 0 ? hp.aff_s[p.hb_affs[0]] : nullptr;

@@ -93,11 +93,15 @@ struct BlkLayout {
   uint32_t x_off, stage, xr_off, w_off, stg_off, trash_off, f_off, par_off, bar_off, total;
 };
 constexpr uint32_t kF32Tile = 64u * 256u;  // one 64-row tile of fp32 channels (fold operand / partial)
-// z tile of the fold + head epilogue: rows of 68 floats, channels 32..63 at +33, so the head GEMV's reads
-// (8 rows x 2 channel halves per warp, same channel) fall in 16 distinct banks
-constexpr int kZStride = 68;
+// z tile of the fold + head epilogue: rows of 72 floats, channels 32..63 at +36, so the head GEMV's 16-byte
+// reads of 16 rows x 2 channel halves per warp spread over all banks
+constexpr int kZStride = 72;
 constexpr uint32_t kZTile = 64u * kZStride * 4u;
-__host__ __device__ constexpr int zidx(int row, int c) { return row * kZStride + (c >= 32 ? c + 1 : c); }
+__host__ __device__ constexpr int zidx(int row, int c) { return row * kZStride + (c >= 32 ? c + 4 : c); }
+// partial-fold tile (fp32, 16 KB per 63-row tile): row pair pr, channel c, row parity j at
+// pr * 128 + 2 * (c ^ 4 (pr & 3)) + j floats -- a thread's (channel, rows 2t0 / 2t0 + 1) fragment is one
+// 8-byte access, and the four t0 of a warp land in different banks
+__host__ __device__ constexpr int pidx(int pr, int c) { return pr * 128 + 2 * (c ^ ((pr & 3) << 2)); }
 __host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int relu_in, int epi = 0) {
   BlkLayout s{};
   s.stage = static_cast<uint32_t>(win_alloc * kRB);  // multiple of 4 KB
@@ -344,15 +348,21 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       if (tr) atomicAdd(&L.trace[kBlkTraceProd], static_cast<unsigned long long>(t_wait));
     }
     if (EPI && lane == 1 && n_local > 0 && !(L.fold.dbg & 1)) {
-      // fold operand tiles (one per conv2 tile), double-buffered, consumed by the conv2 epilogue
-      prefetch_tmap(&L.fold.opnd_map);
-      const uint32_t bytes = static_cast<uint32_t>(kTile) * (L.fold.opnd_f32 ? 256u : static_cast<uint32_t>(kRB));
+      // fold operand tiles (one per conv2 tile), double-buffered, consumed by the conv2 epilogue: subnetwork
+      // 0's 16-bit rows by TMA, or this tile's 16 KB block of the partial-fold buffer by a plain bulk copy
+      const bool f32 = L.fold.opnd_f32 != 0;
+      if (!f32) prefetch_tmap(&L.fold.opnd_map);
       for (int v = 0; v < n_local; ++v) {
         const int fb = v & 1;
         mbar_wait(&fempty[fb], (static_cast<uint32_t>(v >> 1) & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&ffull[fb], bytes);
-        tma_load_2d(smem + lay.f_off + fb * kF32Tile, &L.fold.opnd_map, &ffull[fb], 0,
-                    static_cast<int32_t>((t_begin + v) * kTile));
+        uint8_t* dst = smem + lay.f_off + fb * kF32Tile;
+        if (f32) {
+          mbar_arrive_expect_tx(&ffull[fb], kF32Tile);
+          bulk_load(dst, L.fold.opnd_part + static_cast<size_t>(t_begin + v) * (kF32Tile / 4), kF32Tile, &ffull[fb]);
+        } else {
+          mbar_arrive_expect_tx(&ffull[fb], static_cast<uint32_t>(kTile) * kRB);
+          tma_load_2d(dst, &L.fold.opnd_map, &ffull[fb], 0, static_cast<int32_t>((t_begin + v) * kTile));
+        }
       }
     }
   } else if (warp == 1 || warp == kWarpMma2) {
@@ -613,7 +623,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
     const uint32_t srow = static_cast<uint32_t>(32 * H + lane);
     const int r = 32 * H + lane;
     const int etid = e * 32 + lane;  // 0..255 over the conv2-epilogue warps
-    if (lead && EPI == 1) prefetch_tmap(&fd.pout_map);
     int s = XS > 1 ? 1 : 0;  // x stage of conv1 tile u = v + 1
     uint32_t ph = XS > 1 ? 0u : 1u;
     for (int v = 0; v < n_local; ++v, ring_next(s, ph)) {
@@ -656,15 +665,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float2 yv = unpack2<F16>(o[blk][i]);
-          const float2 pv16 = fd.opnd_f32 ? make_float2(0.f, 0.f) : unpack2<F16>(op16[blk][i]);
+          const float2 pv = fd.opnd_f32 ? *reinterpret_cast<const float2*>(fb_f + pidx(16 * H + 4 * i + t0, c))
+                                        : unpack2<F16>(op16[blk][i]);
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
-            const int row = 32 * H + 8 * i + 2 * t0 + j;
             float prev;
             if (fd.opnd_f32) {
-              prev = fb_f[row * 64 + c];
+              prev = j ? pv.y : pv.x;
             } else {
-              prev = j ? pv16.y : pv16.x;  // fold step 0 = subnetwork 0's 16-bit output, its BN / ReLU
+              prev = j ? pv.y : pv.x;  // fold step 0 = subnetwork 0's 16-bit output, its BN / ReLU
               if (fd.s_prev) prev = __fmaf_rn(prev, sp, tp);
               if (fd.relu_prev) prev = fmaxf(prev, 0.f);
             }
@@ -686,19 +695,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
 #pragma unroll
       for (int blk = 0; blk < 2; ++blk)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i) {
+          const int c = 16 * q + 8 * blk + ci;
+          if (EPI == 1) {
+            *reinterpret_cast<float2*>(zb + pidx(16 * H + 4 * i + t0, c)) = make_float2(z[blk][i][0], z[blk][i][1]);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int row = 32 * H + 8 * i + 2 * t0 + j, c = 16 * q + 8 * blk + ci;
-            zb[EPI == 2 ? zidx(row, c) : row * 64 + c] = z[blk][i][j];
+            for (int j = 0; j < 2; ++j) zb[zidx(32 * H + 8 * i + 2 * t0 + j, c)] = z[blk][i][j];
           }
+        }
       if (EPI == 1) {
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sfull[sb]);
         if (lead) {
           mbar_wait(&sfull[sb], static_cast<uint32_t>(v >> 1) & 1u);
-          if (!(fd.dbg & 4)) tma_store_2d(&fd.pout_map, smem + lay.stg_off + sb * kF32Tile, 0, static_cast<int32_t>(p0));
+          if (!(fd.dbg & 4))
+            bulk_store(fd.pout_part + static_cast<size_t>(t_begin + v) * (kF32Tile / 4), smem + lay.stg_off + sb * kF32Tile,
+                       kF32Tile);
           bulk_commit();
           mbar_arrive(&xempty[s]);  // every warp's residual reads precede its sfull arrival
           if (v >= 1) {
@@ -709,31 +723,50 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       } else {
         asm volatile("bar.sync 3, 256;" ::: "memory");  // z of the tile complete (all residual reads done)
         if (lead) mbar_arrive(&xempty[s]);
-        // head GEMV: threads (row, channel half hf, output half qh); per output the summation order of
-        // head.cu's CUDA-core path: fma over the half's 32 channels in order, then half 0 + half 1, + b
-        const int row = etid >> 2, hf = etid & 1, qh = (etid >> 1) & 1;
-        const int nb = fd.nb, q0 = qh * ((nb + 1) / 2), q1 = qh ? nb : (nb + 1) / 2;
-        float part[4] = {0.f, 0.f, 0.f, 0.f};
-        const float* zr = zb + zidx(row, 32 * hf);
-        const float* wf = s_fold + 4 * kC + 32 * hf * 8;
-#pragma unroll 4
-        for (int c = 0; c < 32; ++c) {
-          const float zc = zr[c];
+        // head GEMV on 4 warps: thread (row, channel half hf) computes every output of its half with
+        // head.cu's CUDA-core summation order (fma over the half's 32 channels in order, then half 0 +
+        // half 1, + bias); z and the weights are read 16 bytes at a time
+        if (etid < 128) {
+          const int row = etid >> 1, hf = etid & 1, nb = fd.nb;
+          float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          const float* zr = zb + zidx(row, 32 * hf);
+          const float* wf = s_fold + 4 * kC + 32 * hf * 8;
+#pragma unroll 2
+          for (int c4 = 0; c4 < 32; c4 += 4) {
+            const float4 zq = *reinterpret_cast<const float4*>(zr + c4);
+            const float zc[4] = {zq.x, zq.y, zq.z, zq.w};
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (q0 + k < q1) part[k] = fmaf(zc, wf[c * 8 + q0 + k], part[k]);
-        }
+            for (int u = 0; u < 4; ++u) {
+              const float4 w0 = *reinterpret_cast<const float4*>(wf + (c4 + u) * 8);
+              part[0] = fmaf(zc[u], w0.x, part[0]);
+              part[1] = fmaf(zc[u], w0.y, part[1]);
+              part[2] = fmaf(zc[u], w0.z, part[2]);
+              part[3] = fmaf(zc[u], w0.w, part[3]);
+              if (nb > 4) {
+                const float4 w1 = *reinterpret_cast<const float4*>(wf + (c4 + u) * 8 + 4);
+                part[4] = fmaf(zc[u], w1.x, part[4]);
+                part[5] = fmaf(zc[u], w1.y, part[5]);
+                part[6] = fmaf(zc[u], w1.z, part[6]);
+                part[7] = fmaf(zc[u], w1.w, part[7]);
+              }
+            }
+          }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) part[k] += __shfl_xor_sync(0xffffffffu, part[k], 1);  // half 0 + half 1
-        const int64_t prow = p0 + row;
-        if (hf == 0 && row < kTile && row_valid(geo, prow) && !(fd.dbg & 2)) {
-          int b, t, f;
-          geo.coords(prow, b, t, f);
-          float* dst = fd.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * nb;
-          const float* bb = s_fold + 4 * kC + kC * 8;
+          for (int k = 0; k < 8; ++k) part[k] += __shfl_xor_sync(0xffffffffu, part[k], 1);  // half 0 + half 1
+          const int64_t prow = p0 + row;
+          if (hf == 0 && row < kTile && row_valid(geo, prow) && !(fd.dbg & 2)) {
+            int b, t, f;
+            geo.coords(prow, b, t, f);
+            float* dst = fd.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * nb;
+            const float* bb = s_fold + 4 * kC + kC * 8;
+            if (nb == 4) {
+              *reinterpret_cast<float4*>(dst) = make_float4(part[0] + bb[0], part[1] + bb[1], part[2] + bb[2], part[3] + bb[3]);
+            } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (q0 + k < q1) dst[q0 + k] = part[k] + bb[q0 + k];
+              for (int k = 0; k < 8; ++k)
+                if (k < nb) dst[k] = part[k] + bb[k];
+            }
+          }
         }
       }
     }
@@ -854,18 +887,6 @@ void make_map(const void* plane, int64_t nalloc, uint32_t box_rows, CUtensorMap*
   if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
-void make_map_f32(const void* plane, int64_t nalloc, uint32_t box_rows, CUtensorMap* m) {
-  std::memset(m, 0, sizeof(CUtensorMap));
-  if (!plane) return;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(kC), static_cast<cuuint64_t>(nalloc)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(kC * 4)};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kC), box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_fn_blk()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(plane), dims, strides, box, es,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
-}
 
 template <bool RELU_IN, bool TRACE, bool F16, int EPI>
 void launch_tt(const BlkLaunch& L, int grid, cudaStream_t stream) {
@@ -908,12 +929,16 @@ void conv_blk64_make_maps(const void* in, const void* out, int64_t nalloc, BlkGr
   make_map(out, nalloc, kTile, &g->out_map);
 }
 
-void conv_blk64_make_fold_maps(const void* opnd, bool opnd_f32, const void* pout, int64_t nalloc, BlkFold* f) {
+size_t conv_blk64_part_bytes(int64_t nalloc) { return static_cast<size_t>(conv_blk64_tiles(nalloc)) * kF32Tile; }
+
+void conv_blk64_make_fold_maps(const void* opnd, bool opnd_f32, void* pout, int64_t nalloc, BlkFold* f) {
+  std::memset(&f->opnd_map, 0, sizeof(f->opnd_map));
+  f->opnd_part = nullptr;
   if (opnd_f32)
-    make_map_f32(opnd, nalloc, kTile, &f->opnd_map);
+    f->opnd_part = static_cast<const float*>(opnd);
   else
     make_map(opnd, nalloc, kTile, &f->opnd_map);
-  make_map_f32(pout, nalloc, kTile, &f->pout_map);
+  f->pout_part = static_cast<float*>(pout);
   f->opnd_f32 = opnd_f32 ? 1 : 0;
 }
 

@@ -27,8 +27,9 @@ struct BlkGroup {
 // Mid launches (EPI 1) store acc as an fp32 plane; the last (EPI 2) runs the 1x1 head on it (fp32, the
 // summation order of head.cu's CUDA-core GEMV) and writes the LLRs.  network.hpp:534-559.
 struct BlkFold {
-  CUtensorMap opnd_map;      // operand tiles (63-row boxes): 16-bit plane (128B swizzle) or fp32 plane
-  CUtensorMap pout_map;      // (EPI 1) fp32 partial-fold plane, 63-row boxes
+  CUtensorMap opnd_map;      // (k = 1) subnetwork 0's 16-bit output plane, 63-row boxes (128B swizzle)
+  const float* opnd_part;    // (k >= 2) fp32 partial-fold buffer of launch k - 1 (conv_blk64_part_bytes)
+  float* pout_part;          // (EPI 1) this launch's fp32 partial-fold buffer
   const float* s_prev;       // (16-bit operand) fold step 0's BN scale / shift, nullable
   const float* t_prev;
   const float* s;            // this step's BN, nullable
@@ -62,8 +63,12 @@ int64_t conv_blk64_tiles(int64_t nalloc);
 int conv_blk64_win_alloc(int halo);
 bool conv_blk64_supported_halo(int halo);
 void conv_blk64_make_maps(const void* in, const void* out, int64_t nalloc, BlkGroup* g);
-// fold operand / output maps: `opnd` a 16-bit plane (opnd_f32 = 0) or an fp32 partial plane; `pout` (EPI 1)
-void conv_blk64_make_fold_maps(const void* opnd, bool opnd_f32, const void* pout, int64_t nalloc, BlkFold* f);
+// fold operand / output: `opnd` subnetwork 0's 16-bit plane (opnd_f32 = 0) or a partial-fold buffer;
+// `pout` (EPI 1) a partial-fold buffer.  Partial-fold buffers are tile-major: per 63-row output tile one
+// 16 KB block of fp32 [32 row pairs][64 channels][2 rows] (channel index swizzled per row pair), moved
+// with plain bulk copies.
+size_t conv_blk64_part_bytes(int64_t nalloc);
+void conv_blk64_make_fold_maps(const void* opnd, bool opnd_f32, void* pout, int64_t nalloc, BlkFold* f);
 // largest x-window ring depth (<= 6) that fits in shared memory, 0 if none
 int conv_blk64_xstages(int win_alloc, int relu_in, int epi = 0);
 size_t conv_blk64_smem_bytes(int xstages, int win_alloc, int relu_in, int epi = 0);
