@@ -47,3 +47,26 @@ def test_no_oracle_import_in_product():
             if f.endswith((".py", ".cpp", ".cu", ".h", ".cuh")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "liboracle" not in txt and "_ref/" not in txt, f
+
+
+def test_plan_options_defaults_and_abi_check():
+    """cnrx_plan_options_default (no GPU needed) and the struct_size guard of cnrx_plan_create_ex, which
+    rejects a caller compiled against another header version before touching the device."""
+    if not os.path.exists(P.LIB_PATH):
+        pytest.skip("libconetrx_cuda.so not built")
+    import ctypes as C
+    d = P.default_options()
+    assert d == {"fused_blocks": 1, "fused_head": 0, "tensor_core_head": 0, "cta_pair": 1, "weights_stationary": 1,
+                 "relu_on_load": 1, "cuda_core_stem": 0, "pipeline_chunks": 0, "pipeline_taper": pytest.approx(0.125)}
+    o = P.cnrx_plan_options()
+    P.lib().cnrx_plan_options_default(C.byref(o))
+    assert o.struct_size == C.sizeof(P.cnrx_plan_options)
+    o.struct_size -= 4
+    g = G.CONFIGS["cfg1"].graph()
+    node = (P.cnrx_node * len(g.nodes))(*[P.cnrx_node(*n.as_row()) for n in g.nodes])
+    h = C.c_void_p()
+    rc = P.lib().cnrx_plan_create_ex(node, len(g.nodes), g.input_node, g.output_node, None, 0, None, 0, P.BF16, 0,
+                                     C.byref(o), C.byref(h))
+    assert rc == P.ERR_INVALID_ARGUMENT and "struct_size" in P.lib().cnrx_last_error().decode()
+    with pytest.raises(ValueError, match="unknown plan option"):
+        P.Plan(g, "fp32", options={"no_such_option": 1})

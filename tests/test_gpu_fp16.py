@@ -97,3 +97,25 @@ def test_plan_options_round_trip_and_env_free():
     p = P.Plan(g, "bf16", options={"fused_blocks": 0, "pipeline_chunks": 3})
     o = p.options()
     assert o["fused_blocks"] == 0 and o["pipeline_chunks"] == 3 and o["cta_pair"] == 1
+
+
+def test_fp16_packs_saturate_instead_of_overflowing():
+    """fp16 planes hold |x| <= 65504: out-of-range values saturate (cvt.rn.satfinite) rather than
+    becoming inf and poisoning the network with NaNs downstream."""
+    import torch
+    link = dataclasses.replace(G.CONFIGS["cfg2"].link, F=48)
+    b = slots.generate(link, 2, 3)
+    spec = G.conet_template(64, 2, [2], "mul", "bn", False, 12, 4, "standard", 3, [1])
+    for ns in [spec.main] + spec.supports:
+        ns.kernel = 1
+    g = G.build_conet(spec)
+    g.init_he_normal(1, randomize_aux=True)
+    p = P.Plan(g, "fp16")
+    p.set_pilots(b.pilots, b.pilot_mask)
+    y = torch.from_numpy(b.y * np.float32(3e5)).cuda()   # |Re y| up to ~1e6 > 65504
+    plane = p.feature_plane(y)
+    assert np.isfinite(plane).all() and np.abs(plane).max() == 65504.0
+    out = torch.empty((2, link.T, link.F, 4), dtype=torch.float32, device="cuda")
+    p.receive_device(y, out)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
