@@ -874,16 +874,20 @@ struct Bf16Compiler {
       if (op.ks != 1 && op.ks != 3)
         throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan supports 1x1 and 3x3 convolutions");
       op.dil = nd.dilation_f;
-      // relu(v) feeding a 64->64 3x3 conv: the weights-stationary kernel applies the ReLU to its input
-      // window in shared memory, so v's producer need not store a second, pre-activated plane
-      // (relu commutes with the bf16 rounding: identical values).
+      // relu(v) feeding a 64->64 3x3 conv (weights-stationary kernel) or a 96->96 one (CTA-pair kernel):
+      // the conv applies the ReLU to its input window in shared memory, so v's producer need not store a
+      // second, pre-activated plane (relu commutes with the 16-bit rounding: identical values).
       const bool no_relu_in = p.opt.relu_on_load == 0;
       {
         const cnrx_node& in = p.N(nd.in0);
         const int v = in.op == CNRX_OP_RELU ? in.in0 : -1;
+        const int vC = v >= 0 && node_plane[static_cast<size_t>(v)] >= 0
+                           ? p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].C : 0;
+        const bool ws64 = w.dims[2] == 64 && w.dims[3] == 64 && vC == 64 && p.opt.weights_stationary;
+        const bool pair96 = round_cin(static_cast<int>(w.dims[2])) == 96 && round_cout(static_cast<int>(w.dims[3])) == 96 &&
+                            vC == 96 && p.opt.cta_pair;
         if (!no_relu_in && v >= 0 && node_plane[static_cast<size_t>(nd.in0)] < 0 && node_plane[static_cast<size_t>(v)] >= 0 &&
-            !p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].nonneg && op.ks == 3 && w.dims[2] == 64 &&
-            w.dims[3] == 64 && p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].C == 64 && p.opt.weights_stationary) {
+            !p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].nonneg && op.ks == 3 && (ws64 || pair96)) {
           op.relu_in = 1;
           op.in_plane = node_plane[static_cast<size_t>(v)];
         } else {
@@ -938,7 +942,8 @@ struct Bf16Compiler {
       if (op.res_plane >= 0) use(op.res_plane, op.level);
       // weights (BN scale folded per output channel) and bias
       op.ws = p.opt.weights_stationary != 0 && op.ks == 3 && op.cin_real == 64 && op.cout_real == 64 && op.cin == 64 && op.cout == 64;
-      if (op.relu_in && !op.ws) throw Error(CNRX_ERR_UNSUPPORTED, "internal: relu-on-load needs the ws conv kernel");
+      if (op.relu_in && !op.ws && !(op.cin == 96 && op.cout == 96 && op.ks == 3))
+        throw Error(CNRX_ERR_UNSUPPORTED, "internal: relu-on-load needs the ws or the CTA-pair conv kernel");
       if (op.ws) {
         std::vector<uint32_t> img(conv_ws64_wimg_bytes() / 4);
         conv_ws64_pack_weights(w.data.data(), scale.empty() ? nullptr : scale.data(), p.fp16, img.data());
@@ -1026,7 +1031,7 @@ struct Bf16Compiler {
         const TcOp& o0 = p.tc[static_cast<size_t>(g[0])];
         const bool blk0 = o0.blk_c1 >= 0, blk = op.blk_c1 >= 0;
         if (static_cast<int>(g.size()) < kTcMaxGroups && o0.cin == op.cin && o0.cout == op.cout && o0.ks == op.ks &&
-            o0.ws == op.ws && blk0 == blk && o0.fused_away == op.fused_away &&
+            o0.ws == op.ws && blk0 == blk && o0.fused_away == op.fused_away && (op.ws || o0.relu_in == op.relu_in) &&
             (!blk || p.tc[static_cast<size_t>(o0.blk_c1)].relu_in == p.tc[static_cast<size_t>(op.blk_c1)].relu_in)) {
           g.push_back(k);
           placed = true;
@@ -1308,10 +1313,12 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           g.relu = op.relu;
         }
         L.win_alloc = win_alloc;
+        bool relu_in = false;
         for (size_t gi = 0; gi < grp.size(); ++gi) {
           const TcOp& op = p.tc[static_cast<size_t>(grp[gi])];
           if (op.res_plane >= 0) L.flags |= 1;
           if (op.out2_plane >= 0) L.flags |= 2;
+          relu_in = relu_in || op.relu_in;
         }
         // 96 -> 96 3x3 convs run on CTA pairs (cta_pair = 0: the single-CTA kernel)
         const bool no_pair = p.opt.cta_pair == 0;
@@ -1324,6 +1331,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           // and measured slower than direct stores); otherwise the direct-store epilogue
           const bool staged = (L.flags & 3) != 0 && conv_pair96_stages(win_alloc, true) > 0;
           if (staged) L.flags |= kPairStaged;
+          if (relu_in) L.flags |= kPairReluIn;
           L.stages = conv_pair96_stages(win_alloc, staged);
           for (size_t gi = 0; gi < grp.size(); ++gi) {
             const TcOp& op = p.tc[static_cast<size_t>(grp[gi])];
@@ -1335,6 +1343,9 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           ws.launches.push_back(GL);
           continue;
         }
+        if (relu_in)
+          throw Error(CNRX_ERR_UNSUPPORTED, "96-channel ReLU-on-load conv does not fit the CTA-pair kernel at this grid "
+                                            "(plan option relu_on_load = 0 selects pre-activated planes)");
         int stages = 4;
         while (stages > 1 && conv_tc_smem_bytes(op0.cin, op0.cout, op0.ks, stages, win_alloc, L.flags) > 227 * 1024)
           --stages;

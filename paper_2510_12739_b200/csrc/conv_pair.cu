@@ -41,8 +41,9 @@ constexpr int kTapBytes = kHalfN * (kRB0 + kRB1);  // 9216: one tap of this CTA'
 constexpr int kWBytes = 9 * kTapBytes;             // 82944
 constexpr int kTmemCols = 256;       // 2 accumulator stages x 96 columns
 constexpr int kBox = 32;
-constexpr int kThreads = 352;   // producer, UMMA, 8 epilogue warps, store warp
+constexpr int kThreads = 416;   // producer, UMMA, 8 epilogue warps, store warp, 2 input-ReLU warps
 constexpr int kStoreWarp = 10;
+constexpr int kReluWarp0 = 11, kReluWarps = 2;
 constexpr uint32_t kTileBytes = 128u * (kRB0 + kRB1);  // one 128-row tile of a 96-ch plane (24 KB)
 
 // `staged` (launches with a residual and/or a second output): residual tiles arrive by TMA into rbuf,
@@ -148,7 +149,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* rempty = rfull + 2;        // [2] staged: tile buffer's TMA store has read it
   uint64_t* sfull = rempty + 2;        // [2] staged: all epilogue warps wrote the tile buffer
   uint64_t* o2free = sfull + 2;        // staged: o2buf's TMA store has read it
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o2free + 1);
+  uint64_t* lfull = o2free + 1;        // [stages] (ReLU-on-load) this CTA's window stage landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lfull + L.stages);
+  const bool relu_in = (L.flags & kPairReluIn) != 0;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -168,8 +171,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mbar_init(w_full, 1);
     mbar_init(wpeer, 1);
     for (int s = 0; s < L.stages; ++s) {
-      mbar_init(&full[s], 1);
+      // ReLU-on-load: the leader's full[s] completes when both CTAs' ReLU warps have processed their
+      // window halves (2 x kReluWarps arrivals); otherwise on both CTAs' TMA bytes
+      mbar_init(&full[s], relu_in ? 2 * kReluWarps : 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&lfull[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -225,13 +231,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int64_t k = local; k < n_ptiles; k += npc, ++j) {
         const int s = j % L.stages;
         mbar_wait(&empty[s], (static_cast<uint32_t>(j / L.stages) & 1u) ^ 1u);
-        const uint32_t fb = map_to_rank(&full[s], 0);
-        if (leader) mbar_arrive_expect_tx(&full[s], 2u * stage_tx);
         uint8_t* win = smem + lay.win_off + s * lay.win_stage;
         const int32_t r0 = static_cast<int32_t>((2 * k + rank) * 128 - grp.halo);
-        for (int bx = 0; bx < nboxes; ++bx) {
-          tma_load_2d_2sm(win + bx * kBox * kRB0, &grp.map[0], fb, 0, r0 + bx * kBox);
-          tma_load_2d_2sm(win + lay.win_c1 + bx * kBox * kRB1, &grp.map[1], fb, 0, r0 + bx * kBox);
+        if (relu_in) {  // own window on the own barrier; the ReLU warps report to the leader
+          mbar_arrive_expect_tx(&lfull[s], stage_tx);
+          for (int bx = 0; bx < nboxes; ++bx) {
+            tma_load_2d(win + bx * kBox * kRB0, &grp.map[0], &lfull[s], 0, r0 + bx * kBox);
+            tma_load_2d(win + lay.win_c1 + bx * kBox * kRB1, &grp.map[1], &lfull[s], 0, r0 + bx * kBox);
+          }
+        } else {
+          const uint32_t fb = map_to_rank(&full[s], 0);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2u * stage_tx);
+          for (int bx = 0; bx < nboxes; ++bx) {
+            tma_load_2d_2sm(win + bx * kBox * kRB0, &grp.map[0], fb, 0, r0 + bx * kBox);
+            tma_load_2d_2sm(win + lay.win_c1 + bx * kBox * kRB1, &grp.map[1], fb, 0, r0 + bx * kBox);
+          }
         }
         const int64_t tile = 2 * k + rank;
         if (staged && grp.res && tile < n_tiles) {
@@ -256,7 +270,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int64_t k = local; k < n_ptiles; k += npc, ++j) {
         const int s = j % L.stages;
         const int a = j & 1;
-        mbar_wait(&full[s], static_cast<uint32_t>(j / L.stages) & 1u);
+        if (relu_in)
+          mbar_wait_cluster(&full[s], static_cast<uint32_t>(j / L.stages) & 1u);  // both CTAs' ReLU passes
+        else
+          mbar_wait(&full[s], static_cast<uint32_t>(j / L.stages) & 1u);
         mbar_wait(&tempty[a], (static_cast<uint32_t>(j >> 1) & 1u) ^ 1u);
         tc_fence_after();
         if (elect_one()) {
@@ -286,6 +303,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           umma_commit_2sm(&tfull[a]);  // both CTAs' accumulators ready
         }
         __syncwarp();
+      }
+    }
+  } else if (warp >= kReluWarp0) {
+    // ------------------------------ input ReLU (ReLU-on-load launches) ---------
+    // in place over this CTA's window stage (16-byte chunks of both K-chunk blocks; ReLU commutes with the
+    // 16-bit rounding, so the values equal a pre-activated plane's), then a release arrive on the
+    // leader's full[s]: its UMMAs read both CTAs' windows
+    if (relu_in) {
+      const int rw = warp - kReluWarp0;
+      const int nch = L.win_alloc * (kRB0 + kRB1) / 16;  // chunks per stage (chunk0 rows, then chunk1 rows)
+      const int per = (nch / kReluWarps + 31) / 32 * 32;
+      const int lo = rw * per < nch ? rw * per : nch, hi = rw == kReluWarps - 1 ? nch : (lo + per < nch ? lo + per : nch);
+      const int c1_first = L.win_alloc * kRB0 / 16;   // chunk index where the 64-byte-row block starts
+      int j = 0;
+      for (int64_t k = local; k < n_ptiles; k += npc, ++j) {
+        const int s = j % L.stages;
+        mbar_wait(&lfull[s], static_cast<uint32_t>(j / L.stages) & 1u);
+        const uint32_t wa = smem_u32(smem + lay.win_off + s * lay.win_stage);
+        for (int c0 = lo; c0 < hi; c0 += 32 * 8) {
+          uint4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int c = c0 + u * 32 + lane;
+            const uint32_t off = c < c1_first ? static_cast<uint32_t>(c) * 16u
+                                              : lay.win_c1 + static_cast<uint32_t>(c - c1_first) * 16u;
+            if (c < hi) v[u] = lds128(wa + off);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int c = c0 + u * 32 + lane;
+            const uint32_t off = c < c1_first ? static_cast<uint32_t>(c) * 16u
+                                              : lay.win_c1 + static_cast<uint32_t>(c - c1_first) * 16u;
+            v[u].x = relu2<F16>(v[u].x);
+            v[u].y = relu2<F16>(v[u].y);
+            v[u].z = relu2<F16>(v[u].z);
+            v[u].w = relu2<F16>(v[u].w);
+            if (c < hi) sts128(wa + off, v[u]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(map_to_rank(&full[s], 0));
       }
     }
   } else if (warp == kStoreWarp) {
@@ -468,6 +527,7 @@ const char* conv_pair96_launch(const TcLaunch& L, int num_sms, cudaStream_t stre
   int pairs = static_cast<int>(pair_work < num_sms / 2 ? pair_work : num_sms / 2);
   if (pairs < L.ngroups) pairs = L.ngroups;
   launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), lay.total, stream, L);
+  if (L.flags & kPairReluIn) return L.fp16 ? "conv_pair96_kernel<f16,relu_in>" : "conv_pair96_kernel<relu_in>";
   return L.fp16 ? "conv_pair96_kernel<f16>" : "conv_pair96_kernel";
 }
 

@@ -9,6 +9,10 @@ namespace cnrx {
 // TcLaunch::flags bit: this launch uses the TMA-staged epilogue (residual load + output stores by TMA;
 // set by the host when the staged shared-memory layout fits, i.e. not for dilated windows)
 constexpr int kPairStaged = 4;
+// TcLaunch::flags bit: the launch's input is relu(plane) -- two ReLU warps per CTA apply it to each
+// window stage in shared memory before the UMMAs read it (MRB blocks' conv1: the previous conv2 then
+// writes one plane instead of a second, pre-activated copy).  Every group of the launch has it.
+constexpr int kPairReluIn = 8;
 
 // True for a 3x3 96 -> 96 conv whose window (halo rows either side) fits the pair kernel's smem.
 bool conv_pair96_supported(int cin, int cout, int ks, int halo);

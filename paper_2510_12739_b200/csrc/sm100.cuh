@@ -109,6 +109,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Bounded wait with cluster-scope acquire: for barriers other CTAs of the cluster arrive on with
+// release.cluster semantics (their shared-memory writes must be visible to this CTA's UMMAs).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  auto try_once = [&]() {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+  };
+  if (try_once()) return;
+  const long long t0 = clock64();
+  for (;;) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (try_once()) return;
+    if (static_cast<unsigned long long>(clock64() - t0) > CNRX_WAIT_LIMIT_CYCLES) wait_timeout(parity);
+  }
+}
+
 // Same, but polling with a nanosleep back-off: for kernels with many waiting warps, whose polls would
 // otherwise take issue slots from the working ones (a try_wait returns after a few tens of cycles).
 template <unsigned kSleepNs>

@@ -86,6 +86,28 @@ def test_cta_pair_conv_is_bit_exact_with_single_cta(which):
 
 
 @pytest.mark.parametrize("prec", ["bf16", "fp16"])
+@pytest.mark.parametrize("which", ["dilated96", "cfg3"])
+def test_pair_relu_on_load_is_bit_exact(which, prec):
+    """96-channel MRB blocks: conv1 applies the input ReLU to its window in shared memory (two ReLU warps
+    per CTA of the pair) instead of reading a pre-activated plane the previous conv2 wrote."""
+    if which == "cfg3":
+        g = G.CONFIGS["cfg3"].graph(seed=5)
+        x = np.random.default_rng(5).standard_normal((1, 14, 70, g.in_channels)).astype(np.float32)
+        q = P.Plan(g, prec, options={"relu_on_load": 1})
+        yo = q.forward(x)
+        lo = q.launch_names()
+        r = P.Plan(g, prec, options={"relu_on_load": 0})
+        yp, lp = r.forward(x), r.launch_names()
+    else:
+        yo, lo = _run(which, prec, relu_on_load=1)
+        yp, lp = _run(which, prec, relu_on_load=0)
+    assert any("relu_in" in n for n in lo), lo
+    assert not any("relu_in" in n for n in lp), lp
+    assert len(lo) <= len(lp)
+    _same(yo, yp)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp16"])
 @pytest.mark.parametrize("which", ["cfg2", "conet2", "conet4"])
 def test_fused_block_head_is_bit_exact_with_head_kernel(which, prec):
     yh, lh = _run(which, prec, fused_head=1)
