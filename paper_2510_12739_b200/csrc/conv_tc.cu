@@ -291,7 +291,16 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
           mbar_wait(&rfull[a], static_cast<uint32_t>(j >> 1) & 1u);
           rrow = smem + lay.res_off + a * 128 * ORB;
         }
-        if (lane == 0) bulk_wait_read0();  // staging buffer free (previous tile's stores read it)
+        // staging buffer free?  Launches without a second output use the out2 half as a second buffer
+        // (alternate tiles), so the wait covers the store issued two tiles ago, not the one just issued
+        const bool dbl = (L.flags & 2) == 0;
+        uint8_t* sb = dbl && (j & 1) ? stg + 32 * ORB : stg;
+        if (lane == 0) {
+          if (dbl)
+            bulk_wait_read1();
+          else
+            bulk_wait_read0();
+        }
         __syncwarp();
 #pragma unroll 1
         for (int cc = 0; cc < COUT / 32; ++cc) {
@@ -334,7 +343,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
               uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
               for (int i = 0; i < 4; ++i) op[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
-              *reinterpret_cast<uint4*>(stg + so) = o;
+              *reinterpret_cast<uint4*>(sb + so) = o;
             }
             if (grp.out2) {
               uint4 o;
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
         __syncwarp();
         if (lane == 0) {
           const int32_t r0 = static_cast<int32_t>(tile * 128 + q * 32);
-          tma_store_2d(&grp.out_map, stg, 0, r0);
+          tma_store_2d(&grp.out_map, sb, 0, r0);
           if (grp.out2) tma_store_2d(&grp.out2_map, stg + 32 * ORB, 0, r0);
           bulk_commit();
         }
