@@ -78,19 +78,17 @@ constexpr int kRingRows = kWSlots * 63;
 #define CNRX_BLK_RELU_WARPS 2
 #endif
 constexpr int kReluWarps = CNRX_BLK_RELU_WARPS;
-// CNRX_BLK_STORE_WARP=1: a dedicated warp issues the conv2 tiles' TMA stores (otherwise the first conv2
-// epilogue warp does, between its own tiles)
-#ifndef CNRX_BLK_STORE_WARP
-#define CNRX_BLK_STORE_WARP 0
-#endif
 constexpr int kWarpE2 = 10, kWarpRelu0 = 18, kWarpMma2 = 19;
-constexpr int kWarpStore = 19 + kReluWarps;  // (CNRX_BLK_STORE_WARP)
-constexpr int kThreads = (19 + kReluWarps + CNRX_BLK_STORE_WARP) * 32;
+constexpr int kThreads = (19 + kReluWarps) * 32;
+// fold epilogues (EPI 1 / 2): three more warps combine the staged conv2 tile with the fold operand (and run
+// the head GEMV), so the conv2-epilogue warps keep their plain per-tile work; 24 warps keep 80 registers
+constexpr int kFoldWarps = 3, kWarpFold0 = 19 + kReluWarps;
+constexpr int kThreadsFold = kThreads + kFoldWarps * 32;
 __device__ __forceinline__ int relu_index(int warp) { return warp == kWarpRelu0 ? 0 : warp - 19; }
 constexpr int kMaxXStages = 6;
 
 struct BlkLayout {
-  uint32_t x_off, stage, xr_off, w_off, stg_off, trash_off, f_off, par_off, bar_off, total;
+  uint32_t x_off, stage, xr_off, w_off, stg_off, trash_off, f_off, stg2_off, par_off, bar_off, total;
 };
 constexpr uint32_t kF32Tile = 64u * 256u;  // one 64-row tile of fp32 channels (fold operand / partial)
 // z tile of the fold + head epilogue: rows of 72 floats, channels 32..63 at +36, so the head GEMV's 16-byte
@@ -98,10 +96,7 @@ constexpr uint32_t kF32Tile = 64u * 256u;  // one 64-row tile of fp32 channels (
 constexpr int kZStride = 72;
 constexpr uint32_t kZTile = 64u * kZStride * 4u;
 __host__ __device__ constexpr int zidx(int row, int c) { return row * kZStride + (c >= 32 ? c + 4 : c); }
-// partial-fold tile (fp32, 16 KB per 63-row tile): row pair pr, channel c, row parity j at
-// pr * 128 + 2 * (c ^ 4 (pr & 3)) + j floats -- a thread's (channel, rows 2t0 / 2t0 + 1) fragment is one
-// 8-byte access, and the four t0 of a warp land in different banks
-__host__ __device__ constexpr int pidx(int pr, int c) { return pr * 128 + 2 * (c ^ ((pr & 3) << 2)); }
+// partial-fold tiles are row-major fp32 [64 rows][64 channels], 16 KB per 63-row output tile
 __host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int relu_in, int epi = 0) {
   BlkLayout s{};
   s.stage = static_cast<uint32_t>(win_alloc * kRB);  // multiple of 4 KB
@@ -114,12 +109,14 @@ __host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int 
     off += (static_cast<uint32_t>(kRingRows + win_alloc) * kRB + 1023u) & ~1023u;  // ring + mirror (>= win_rows - 1 rows)
   else
     off += static_cast<uint32_t>(kWSlots) * s.stage;
-  s.stg_off = off;                 // 2 x [64 rows][128 B]; fold: 2 x [64 rows][64 fp32] (mid) / 2 z tiles (head)
-  off += epi == 2 ? (2u * kZTile + 1023u) & ~1023u : epi ? 2u * kF32Tile : 2u * 64u * kRB;
+  s.stg_off = off;                 // 2 x [64 rows][128 B]: the conv2 tile staged for its TMA store / the fold
+  off += 2u * 64u * kRB;
   s.trash_off = off;               // 32 rows: destination of stmatrix rows that belong to no window
   off += 32u * kRB;
   s.f_off = off;                   // fold epilogues: 2 operand tiles (16-bit or fp32 rows)
   if (epi) off += 2u * kF32Tile;
+  s.stg2_off = off;                // fold epilogues: 2 fp32 partial tiles (EPI 1) / 2 padded z tiles (EPI 2)
+  if (epi) off += (2u * (epi == 2 ? kZTile : kF32Tile) + 1023u) & ~1023u;
   s.par_off = off;                 // bias1, bias2; fold: s_prev, t_prev, s, t [64] + head w [64][8], b [8]
   off += 2u * kC * 4u;
   if (epi) off += (4u * kC + kC * 8u + 8u) * 4u;
@@ -206,7 +203,7 @@ __device__ __forceinline__ void epi_acc_wait(uint64_t* bar, uint32_t parity) {
 }
 
 template <bool RELU_IN, bool TRACE, bool F16, int EPI>
-__global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_constant__ BlkLaunch L) {
+__global__ void __launch_bounds__(EPI ? kThreadsFold : kThreads, 1) conv_blk64_kernel(const __grid_constant__ BlkLaunch L) {
   constexpr uint32_t IDESC = idesc_e16_f32<F16>(128, kN);
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
@@ -258,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       mbar_init(&sfull[s], 8);
       mbar_init(&sfree[s], 1);
       mbar_init(&ffull[s], 1);
-      mbar_init(&fempty[s], 8);
+      mbar_init(&fempty[s], kFoldWarps);
     }
     for (int s = 0; s < kWSlots; ++s) {
       mbar_init(&wfull[s], 8 * 3);  // 8 conv1-epilogue warps x the 3 conv1 tiles a window spans
@@ -452,26 +449,138 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
         trace_cta_window(L.trace, g_start);
       }
     }
-  } else if (CNRX_BLK_STORE_WARP && warp == kWarpStore) {
-    // ------------------------------ conv2 tile stores --------------------------
-    if (lane == 0 && n_local > 0) {
-      prefetch_tmap(&grp.out_map);
-      int s = XS > 1 ? 1 : 0;  // x stage of conv1 tile u = v + 1 (its residual rows were read by tile v)
-      uint32_t ph = XS > 1 ? 0u : 1u;
-      for (int v = 0; v < n_local; ++v, ring_next(s, ph)) {
-        const int sb = v & 1;
-        mbar_wait(&sfull[sb], static_cast<uint32_t>(v >> 1) & 1u);
-        tma_store_2d(&grp.out_map, smem + lay.stg_off + sb * 64 * kRB, 0, static_cast<int32_t>((t_begin + v) * kTile));
-        bulk_commit();
-        mbar_arrive(&xempty[s]);  // every epilogue warp's residual reads precede its sfull arrival
-        if (v >= 1) {
-          bulk_wait_read1();      // the store of tile v - 1 has read its staging buffer
-          mbar_arrive(&sfree[sb ^ 1]);
+  } else if (EPI != 0 && warp >= kWarpFold0) {
+    // ------------------------------ interaction fold (EPI 1 / 2) ---------------
+    // Per conv2 tile v: the 16-bit y tile the conv2-epilogue warps staged (y rounded exactly as the head
+    // kernel would read it from its plane) is combined with the fold operand -- subnetwork 0's 16-bit
+    // tile (launch 1, its step-0 BN / ReLU applied) or the previous launch's fp32 partial -- exactly as
+    // head.cu folds:  acc = prev (op) y; [fma(acc, s, t)]; [relu].  EPI 1 stores acc (fp32 tile, bulk
+    // copy); EPI 2 writes z and runs the 1x1 head, one thread per row, in head.cu's CUDA-core order
+    // (fma over channels 0..31 and 32..63 separately, then half 0 + half 1, + bias).
+    const int ft = (warp - kWarpFold0) * 32 + lane;  // 0 .. 95
+    const BlkFold& fd = L.fold;
+    const PlaneGeom geo = L.geo;
+    const uint32_t stg_a = smem_u32(smem + lay.stg_off);
+    const uint32_t f_a = smem_u32(smem + lay.f_off);
+    const float* wf = s_fold + 4 * kC;               // head weights [64][8]
+    const float* hb = s_fold + 4 * kC + kC * 8;      // head bias [8]
+    int s = XS > 1 ? 1 : 0;  // x stage of conv1 tile u = v + 1 (the residual rows of conv2 tile v)
+    uint32_t ph = XS > 1 ? 0u : 1u;
+    for (int v = 0; v < n_local; ++v, ring_next(s, ph)) {
+      const int sb = v & 1;
+      const int64_t p0 = (t_begin + v) * kTile;
+      mbar_wait(&sfull[sb], static_cast<uint32_t>(v >> 1) & 1u);
+      if (ft == 0) mbar_arrive(&xempty[s]);  // every conv2-epilogue warp read its residual before sfull
+      if (!(fd.dbg & 1)) mbar_wait(&ffull[sb], static_cast<uint32_t>(v >> 1) & 1u);
+      if (EPI == 1 && ft == 0 && v >= 2) bulk_wait_read1();  // partial tile sb's store (tile v - 2) has read it
+      asm volatile("bar.sync 4, %0;" ::"n"(kFoldWarps * 32) : "memory");
+      float* out_t = reinterpret_cast<float*>(smem + lay.stg2_off + sb * (EPI == 2 ? kZTile : kF32Tile));
+      const uint32_t ys = stg_a + static_cast<uint32_t>(sb) * 64u * kRB;
+      const uint32_t fs = f_a + static_cast<uint32_t>(sb) * kF32Tile;
+      for (int uu = ft; uu < kTile * 8; uu += kFoldWarps * 32) {
+        const int row = uu >> 3, c8 = uu & 7;
+        const uint32_t sw = static_cast<uint32_t>(row) * 128u + ((static_cast<uint32_t>(c8) ^ (static_cast<uint32_t>(row) & 7u)) << 4);
+        const uint4 yw = lds128(ys + sw);
+        const uint32_t yv[4] = {yw.x, yw.y, yw.z, yw.w};
+        float prev[8];
+        if (fd.opnd_f32) {
+          const uint4 a = lds128(fs + static_cast<uint32_t>(row * 256 + c8 * 32));
+          const uint4 b = lds128(fs + static_cast<uint32_t>(row * 256 + c8 * 32 + 16));
+          prev[0] = __uint_as_float(a.x); prev[1] = __uint_as_float(a.y); prev[2] = __uint_as_float(a.z); prev[3] = __uint_as_float(a.w);
+          prev[4] = __uint_as_float(b.x); prev[5] = __uint_as_float(b.y); prev[6] = __uint_as_float(b.z); prev[7] = __uint_as_float(b.w);
+        } else {
+          const uint4 ow = lds128(fs + sw);  // subnetwork 0's tile, TMA-loaded with the same 128B swizzle
+          const uint32_t ov[4] = {ow.x, ow.y, ow.z, ow.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = unpack2<F16>(ov[e]);
+            prev[2 * e] = f.x;
+            prev[2 * e + 1] = f.y;
+          }
+          if (fd.s_prev) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) prev[e] = __fmaf_rn(prev[e], s_fold[8 * c8 + e], s_fold[kC + 8 * c8 + e]);
+          }
+          if (fd.relu_prev) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) prev[e] = fmaxf(prev[e], 0.f);
+          }
+        }
+        float acc[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 y = unpack2<F16>(yv[e]);
+          acc[2 * e] = fd.op == PW_MUL ? prev[2 * e] * y.x : prev[2 * e] + y.x;
+          acc[2 * e + 1] = fd.op == PW_MUL ? prev[2 * e + 1] * y.y : prev[2 * e + 1] + y.y;
+        }
+        if (fd.s) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = __fmaf_rn(acc[e], s_fold[2 * kC + 8 * c8 + e], s_fold[3 * kC + 8 * c8 + e]);
+        }
+        if (fd.relu) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = fmaxf(acc[e], 0.f);
+        }
+        float* dst = EPI == 2 ? out_t + zidx(row, 8 * c8) : out_t + row * 64 + 8 * c8;
+        *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      }
+      if (EPI == 1) fence_proxy_async_smem();  // generic stores -> the bulk store's reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fempty[sb]);
+      asm volatile("bar.sync 4, %0;" ::"n"(kFoldWarps * 32) : "memory");
+      if (ft == 0) mbar_arrive(&sfree[sb]);  // the staged y tile is consumed
+      if (EPI == 1) {
+        if (ft == 0 && !(fd.dbg & 4))
+          bulk_store(fd.pout_part + static_cast<size_t>(t_begin + v) * (kF32Tile / 4), out_t, kF32Tile);
+        if (ft == 0) bulk_commit();
+      } else if (ft < kTile) {
+        const int64_t prow = p0 + ft;
+        if (row_valid(geo, prow) && !(fd.dbg & 2)) {
+          const int nb = fd.nb;
+          float part[2][8];
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) part[hf][k] = 0.f;
+            const float* zr = out_t + zidx(ft, 32 * hf);
+#pragma unroll 2
+            for (int c4 = 0; c4 < 32; c4 += 4) {
+              const float4 zq = *reinterpret_cast<const float4*>(zr + c4);
+              const float zc[4] = {zq.x, zq.y, zq.z, zq.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float4 w0 = *reinterpret_cast<const float4*>(wf + (32 * hf + c4 + u) * 8);
+                part[hf][0] = fmaf(zc[u], w0.x, part[hf][0]);
+                part[hf][1] = fmaf(zc[u], w0.y, part[hf][1]);
+                part[hf][2] = fmaf(zc[u], w0.z, part[hf][2]);
+                part[hf][3] = fmaf(zc[u], w0.w, part[hf][3]);
+                if (nb > 4) {
+                  const float4 w1 = *reinterpret_cast<const float4*>(wf + (32 * hf + c4 + u) * 8 + 4);
+                  part[hf][4] = fmaf(zc[u], w1.x, part[hf][4]);
+                  part[hf][5] = fmaf(zc[u], w1.y, part[hf][5]);
+                  part[hf][6] = fmaf(zc[u], w1.z, part[hf][6]);
+                  part[hf][7] = fmaf(zc[u], w1.w, part[hf][7]);
+                }
+              }
+            }
+          }
+          int b, t, f;
+          geo.coords(prow, b, t, f);
+          float* dst = fd.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * nb;
+          if (nb == 4) {
+            *reinterpret_cast<float4*>(dst) = make_float4((part[0][0] + part[1][0]) + hb[0], (part[0][1] + part[1][1]) + hb[1],
+                                                          (part[0][2] + part[1][2]) + hb[2], (part[0][3] + part[1][3]) + hb[3]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k < nb) dst[k] = (part[0][k] + part[1][k]) + hb[k];
+          }
         }
       }
-      bulk_wait0();
     }
-  } else if (warp == kWarpRelu0 || warp > kWarpMma2) {
+    if (EPI == 1 && ft == 0) bulk_wait0();
+  } else if (warp == kWarpRelu0 || (warp > kWarpMma2 && warp < 19 + kReluWarps)) {
     // ------------------------------ input ReLU --------------------------------
     if (RELU_IN) {
       const int nchunks = win_rows * (kRB / 16);
@@ -603,175 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
     }
   } else {
     // ------------------------------ conv2 epilogue (warps 10-17) --------------
-   if constexpr (EPI != 0) {
-    // interaction fold (BlkFold): y (16-bit rounded, as the separate head kernel would read it) is combined
-    // with the fold so far; mid launches store the fp32 partial (staged, TMA store), the last launch
-    // writes z to shared memory and runs the head GEMV, two threads per row as head.cu does.
-    const int e = warp - kWarpE2;
-    const int q = warp & 3;
-    const int H = (e >> 2) & 1;
-    const int ci = lane >> 2;
-    const int t0 = lane & 3;
-    const PlaneGeom geo = L.geo;
-    const BlkFold& fd = L.fold;
-    float bias[2];
-#pragma unroll
-    for (int blk = 0; blk < 2; ++blk) bias[blk] = s_bias2[16 * q + 8 * blk + ci];
-    const bool lead = e == 0 && lane == 0;
-    const uint32_t tq = tbase + kAcc2 + static_cast<uint32_t>(32 * H) + (static_cast<uint32_t>(q * 32) << 16);
-    const uint32_t xrow = static_cast<uint32_t>(halo + 32 * H + lane);
-    const uint32_t srow = static_cast<uint32_t>(32 * H + lane);
-    const int r = 32 * H + lane;
-    const int etid = e * 32 + lane;  // 0..255 over the conv2-epilogue warps
-    int s = XS > 1 ? 1 : 0;  // x stage of conv1 tile u = v + 1
-    uint32_t ph = XS > 1 ? 0u : 1u;
-    for (int v = 0; v < n_local; ++v, ring_next(s, ph)) {
-      const int64_t p0 = (t_begin + v) * kTile;
-      const int sb = v & 1;
-      mbar_wait(&xfull[s], ph);
-      const uint32_t xs_a = x_a + static_cast<uint32_t>(s) * lay.stage;
-      uint32_t res[2][4];
-#pragma unroll
-      for (int blk = 0; blk < 2; ++blk) ldsm_x4_trans(xs_a + sw128(xrow, static_cast<uint32_t>((2 * q + blk) * 16)), res[blk]);
-      const uint32_t vm = __ballot_sync(0xffffffffu, row_valid(geo, p0 + r));
-      epi_acc_wait(t2full, static_cast<uint32_t>(v) & 1u);
-      tc_fence_after();
-      uint32_t a0[16], a1[16], xb = 0;
-      tmem_ld16x256b_x4(tq, a0);
-      tmem_ld16x256b_x4(tq + (16u << 16), a1);
-      if (H == 0) tmem_ld_x1(tq + 32, xb);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(t2empty);
-      uint32_t o[2][4];
-      combine_chunk<true, false, F16>(a0, xb, 0, bias[0], res[0], vm >> (2 * t0), lane, o[0]);
-      combine_chunk<true, false, F16>(a1, xb, 1, bias[1], res[1], vm >> (2 * t0), lane, o[1]);
-      // the fold operand of this tile
-      if (!(fd.dbg & 1)) mbar_wait(&ffull[sb], static_cast<uint32_t>(v >> 1) & 1u);
-      const uint32_t fb_a = smem_u32(smem + lay.f_off + sb * kF32Tile);
-      const float* fb_f = reinterpret_cast<const float*>(smem + lay.f_off + sb * kF32Tile);
-      uint32_t op16[2][4];
-      if (!fd.opnd_f32) {
-#pragma unroll
-        for (int blk = 0; blk < 2; ++blk) ldsm_x4_trans(fb_a + sw128(srow, static_cast<uint32_t>((2 * q + blk) * 16)), op16[blk]);
-      }
-      // this thread: channel c = 16q + 8 blk + ci, tile rows 32H + 8i + 2 t0 + j
-      float z[2][4][2];
-#pragma unroll
-      for (int blk = 0; blk < 2; ++blk) {
-        const int c = 16 * q + 8 * blk + ci;
-        const float sp = s_fold[c], tp = s_fold[kC + c], sk = s_fold[2 * kC + c], tk = s_fold[3 * kC + c];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 yv = unpack2<F16>(o[blk][i]);
-          const float2 pv = fd.opnd_f32 ? *reinterpret_cast<const float2*>(fb_f + pidx(16 * H + 4 * i + t0, c))
-                                        : unpack2<F16>(op16[blk][i]);
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            float prev;
-            if (fd.opnd_f32) {
-              prev = j ? pv.y : pv.x;
-            } else {
-              prev = j ? pv.y : pv.x;  // fold step 0 = subnetwork 0's 16-bit output, its BN / ReLU
-              if (fd.s_prev) prev = __fmaf_rn(prev, sp, tp);
-              if (fd.relu_prev) prev = fmaxf(prev, 0.f);
-            }
-            const float y = j ? yv.y : yv.x;
-            float acc = fd.op == PW_MUL ? prev * y : prev + y;
-            if (fd.s) acc = __fmaf_rn(acc, sk, tk);
-            if (fd.relu) acc = fmaxf(acc, 0.f);
-            z[blk][i][j] = acc;
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&fempty[sb]);
-      float* zb = reinterpret_cast<float*>(smem + lay.stg_off + sb * (EPI == 2 ? kZTile : kF32Tile));
-      if (EPI == 1) {
-        // staging buffer sb free once the TMA store of tile v - 2 has read it
-        mbar_wait(&sfree[sb], (static_cast<uint32_t>(v >> 1) & 1u) ^ 1u);
-      }
-#pragma unroll
-      for (int blk = 0; blk < 2; ++blk)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int c = 16 * q + 8 * blk + ci;
-          if (EPI == 1) {
-            *reinterpret_cast<float2*>(zb + pidx(16 * H + 4 * i + t0, c)) = make_float2(z[blk][i][0], z[blk][i][1]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 2; ++j) zb[zidx(32 * H + 8 * i + 2 * t0 + j, c)] = z[blk][i][j];
-          }
-        }
-      if (EPI == 1) {
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sfull[sb]);
-        if (lead) {
-          mbar_wait(&sfull[sb], static_cast<uint32_t>(v >> 1) & 1u);
-          if (!(fd.dbg & 4))
-            bulk_store(fd.pout_part + static_cast<size_t>(t_begin + v) * (kF32Tile / 4), smem + lay.stg_off + sb * kF32Tile,
-                       kF32Tile);
-          bulk_commit();
-          mbar_arrive(&xempty[s]);  // every warp's residual reads precede its sfull arrival
-          if (v >= 1) {
-            bulk_wait_read1();      // the store of tile v - 1 has read its staging buffer
-            mbar_arrive(&sfree[sb ^ 1]);
-          }
-        }
-      } else {
-        asm volatile("bar.sync 3, 256;" ::: "memory");  // z of the tile complete (all residual reads done)
-        if (lead) mbar_arrive(&xempty[s]);
-        // head GEMV on 4 warps: thread (row, channel half hf) computes every output of its half with
-        // head.cu's CUDA-core summation order (fma over the half's 32 channels in order, then half 0 +
-        // half 1, + bias); z and the weights are read 16 bytes at a time
-        if (etid < 128) {
-          const int row = etid >> 1, hf = etid & 1, nb = fd.nb;
-          float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          const float* zr = zb + zidx(row, 32 * hf);
-          const float* wf = s_fold + 4 * kC + 32 * hf * 8;
-#pragma unroll 2
-          for (int c4 = 0; c4 < 32; c4 += 4) {
-            const float4 zq = *reinterpret_cast<const float4*>(zr + c4);
-            const float zc[4] = {zq.x, zq.y, zq.z, zq.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float4 w0 = *reinterpret_cast<const float4*>(wf + (c4 + u) * 8);
-              part[0] = fmaf(zc[u], w0.x, part[0]);
-              part[1] = fmaf(zc[u], w0.y, part[1]);
-              part[2] = fmaf(zc[u], w0.z, part[2]);
-              part[3] = fmaf(zc[u], w0.w, part[3]);
-              if (nb > 4) {
-                const float4 w1 = *reinterpret_cast<const float4*>(wf + (c4 + u) * 8 + 4);
-                part[4] = fmaf(zc[u], w1.x, part[4]);
-                part[5] = fmaf(zc[u], w1.y, part[5]);
-                part[6] = fmaf(zc[u], w1.z, part[6]);
-                part[7] = fmaf(zc[u], w1.w, part[7]);
-              }
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) part[k] += __shfl_xor_sync(0xffffffffu, part[k], 1);  // half 0 + half 1
-          const int64_t prow = p0 + row;
-          if (hf == 0 && row < kTile && row_valid(geo, prow) && !(fd.dbg & 2)) {
-            int b, t, f;
-            geo.coords(prow, b, t, f);
-            float* dst = fd.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * nb;
-            const float* bb = s_fold + 4 * kC + kC * 8;
-            if (nb == 4) {
-              *reinterpret_cast<float4*>(dst) = make_float4(part[0] + bb[0], part[1] + bb[1], part[2] + bb[2], part[3] + bb[3]);
-            } else {
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                if (k < nb) dst[k] = part[k] + bb[k];
-            }
-          }
-        }
-      }
-    }
-    if (lead && EPI == 1) bulk_wait0();
-   } else {
+   {
     // Staging buffers are handed over by mbarriers (no group-wide bar.sync): each warp waits for its
     // buffer to be free, writes its 32 rows x 16 channels, arrives; one thread issues the TMA store.
     const int e = warp - kWarpE2;
@@ -782,7 +723,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
     float bias[2];
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) bias[blk] = s_bias2[16 * q + 8 * blk + ci];
-    const bool lead = !CNRX_BLK_STORE_WARP && e == 0 && lane == 0;
+    const bool lead = e == 0 && lane == 0;
     const uint32_t stg_a = smem_u32(smem + lay.stg_off);
     const uint32_t tq = tbase + kAcc2 + static_cast<uint32_t>(32 * H) + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t xrow = static_cast<uint32_t>(halo + 32 * H + lane);
@@ -834,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk64_kernel(const __grid_co
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sfull[sb]);
-      if (lead) {
+      if (EPI == 0 && lead) {  // (fold launches: the fold warps consume the staged tile instead)
         mbar_wait(&sfull[sb], static_cast<uint32_t>(v >> 1) & 1u);
         tma_store_2d(&grp.out_map, smem + lay.stg_off + sb * 64 * kRB, 0, static_cast<int32_t>(p0));
         bulk_commit();
@@ -892,7 +833,8 @@ template <bool RELU_IN, bool TRACE, bool F16, int EPI>
 void launch_tt(const BlkLaunch& L, int grid, cudaStream_t stream) {
   const BlkLayout lay = blk_layout(L.xstages, L.win_alloc, RELU_IN, EPI);
   ensure_smem_attr(reinterpret_cast<const void*>(conv_blk64_kernel<RELU_IN, TRACE, F16, EPI>), static_cast<int>(lay.total));
-  launch_pdl(conv_blk64_kernel<RELU_IN, TRACE, F16, EPI>, dim3(grid), dim3(kThreads), lay.total, stream, L);
+  launch_pdl(conv_blk64_kernel<RELU_IN, TRACE, F16, EPI>, dim3(grid), dim3(EPI ? kThreadsFold : kThreads), lay.total,
+             stream, L);
 }
 // the per-role trace counters are a bf16-only debug instantiation; the fold epilogues take a ReLU'd input
 // (the last blocks of MRB subnetworks)

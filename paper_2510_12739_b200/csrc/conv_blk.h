@@ -24,8 +24,10 @@ struct BlkGroup {
 // step-0 BN / ReLU applied on load) or the fp32 partial-fold plane of launch k - 1 -- and combines it with
 // its own output exactly as head.cu's fold does (fp32, the 16-bit-rounded subnetwork output):
 //   acc = prev (op) y; [acc = fma(acc, s, t)]; [relu]
-// Mid launches (EPI 1) store acc as an fp32 plane; the last (EPI 2) runs the 1x1 head on it (fp32, the
-// summation order of head.cu's CUDA-core GEMV) and writes the LLRs.  network.hpp:534-559.
+// Mid launches (EPI 1) store acc as an fp32 partial; the last (EPI 2) runs the 1x1 head on it (fp32, the
+// summation order of head.cu's CUDA-core GEMV) and writes the LLRs.  The fold runs on three extra warps
+// that consume the conv2 tile the epilogue warps staged, so those keep their plain per-tile work.
+// network.hpp:534-559.
 struct BlkFold {
   CUtensorMap opnd_map;      // (k = 1) subnetwork 0's 16-bit output plane, 63-row boxes (128B swizzle)
   const float* opnd_part;    // (k >= 2) fp32 partial-fold buffer of launch k - 1 (conv_blk64_part_bytes)
@@ -65,8 +67,7 @@ bool conv_blk64_supported_halo(int halo);
 void conv_blk64_make_maps(const void* in, const void* out, int64_t nalloc, BlkGroup* g);
 // fold operand / output: `opnd` subnetwork 0's 16-bit plane (opnd_f32 = 0) or a partial-fold buffer;
 // `pout` (EPI 1) a partial-fold buffer.  Partial-fold buffers are tile-major: per 63-row output tile one
-// 16 KB block of fp32 [32 row pairs][64 channels][2 rows] (channel index swizzled per row pair), moved
-// with plain bulk copies.
+// 16 KB block of fp32 [64 rows][64 channels], moved with plain bulk copies.
 size_t conv_blk64_part_bytes(int64_t nalloc);
 void conv_blk64_make_fold_maps(const void* opnd, bool opnd_f32, void* pout, int64_t nalloc, BlkFold* f);
 // largest x-window ring depth (<= 6) that fits in shared memory, 0 if none
