@@ -80,9 +80,13 @@ constexpr int kRingRows = kWSlots * 63;
 constexpr int kReluWarps = CNRX_BLK_RELU_WARPS;
 constexpr int kWarpE2 = 10, kWarpRelu0 = 18, kWarpMma2 = 19;
 constexpr int kThreads = (19 + kReluWarps) * 32;
-// fold epilogues (EPI 1 / 2): three more warps combine the staged conv2 tile with the fold operand (and run
-// the head GEMV), so the conv2-epilogue warps keep their plain per-tile work; 24 warps keep 80 registers
-constexpr int kFoldWarps = 3, kWarpFold0 = 19 + kReluWarps;
+// fold epilogues (EPI 1 / 2): more warps combine the staged conv2 tile with the fold operand (and run the
+// head GEMV), so the conv2-epilogue warps keep their plain per-tile work (7 fold warps: 28 warps, which
+// compile to 72 registers without spills)
+#ifndef CNRX_BLK_FOLD_WARPS
+#define CNRX_BLK_FOLD_WARPS 7
+#endif
+constexpr int kFoldWarps = CNRX_BLK_FOLD_WARPS, kWarpFold0 = 19 + kReluWarps;
 constexpr int kThreadsFold = kThreads + kFoldWarps * 32;
 __device__ __forceinline__ int relu_index(int warp) { return warp == kWarpRelu0 ? 0 : warp - 19; }
 constexpr int kMaxXStages = 6;
@@ -457,7 +461,7 @@ __global__ void __launch_bounds__(EPI ? kThreadsFold : kThreads, 1) conv_blk64_k
     // head.cu folds:  acc = prev (op) y; [fma(acc, s, t)]; [relu].  EPI 1 stores acc (fp32 tile, bulk
     // copy); EPI 2 writes z and runs the 1x1 head, one thread per row, in head.cu's CUDA-core order
     // (fma over channels 0..31 and 32..63 separately, then half 0 + half 1, + bias).
-    const int ft = (warp - kWarpFold0) * 32 + lane;  // 0 .. 95
+    const int ft = (warp - kWarpFold0) * 32 + lane;  // 0 .. 32 * kFoldWarps - 1
     const BlkFold& fd = L.fold;
     const PlaneGeom geo = L.geo;
     const uint32_t stg_a = smem_u32(smem + lay.stg_off);
@@ -534,47 +538,47 @@ __global__ void __launch_bounds__(EPI ? kThreadsFold : kThreads, 1) conv_blk64_k
         if (ft == 0 && !(fd.dbg & 4))
           bulk_store(fd.pout_part + static_cast<size_t>(t_begin + v) * (kF32Tile / 4), out_t, kF32Tile);
         if (ft == 0) bulk_commit();
-      } else if (ft < kTile) {
-        const int64_t prow = p0 + ft;
-        if (row_valid(geo, prow) && !(fd.dbg & 2)) {
-          const int nb = fd.nb;
-          float part[2][8];
+      } else if (ft < 128) {
+        // two threads per row (channel halves), combined with one shuffle: half 0 + half 1, + bias
+        const int row = ft >> 1, hf = ft & 1;
+        const int64_t prow = p0 + row;
+        const int nb = fd.nb;
+        float part[8];
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) part[hf][k] = 0.f;
-            const float* zr = out_t + zidx(ft, 32 * hf);
+        for (int k = 0; k < 8; ++k) part[k] = 0.f;
+        const float* zr = out_t + zidx(row, 32 * hf);
 #pragma unroll 2
-            for (int c4 = 0; c4 < 32; c4 += 4) {
-              const float4 zq = *reinterpret_cast<const float4*>(zr + c4);
-              const float zc[4] = {zq.x, zq.y, zq.z, zq.w};
+        for (int c4 = 0; c4 < 32; c4 += 4) {
+          const float4 zq = *reinterpret_cast<const float4*>(zr + c4);
+          const float zc[4] = {zq.x, zq.y, zq.z, zq.w};
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const float4 w0 = *reinterpret_cast<const float4*>(wf + (32 * hf + c4 + u) * 8);
-                part[hf][0] = fmaf(zc[u], w0.x, part[hf][0]);
-                part[hf][1] = fmaf(zc[u], w0.y, part[hf][1]);
-                part[hf][2] = fmaf(zc[u], w0.z, part[hf][2]);
-                part[hf][3] = fmaf(zc[u], w0.w, part[hf][3]);
-                if (nb > 4) {
-                  const float4 w1 = *reinterpret_cast<const float4*>(wf + (32 * hf + c4 + u) * 8 + 4);
-                  part[hf][4] = fmaf(zc[u], w1.x, part[hf][4]);
-                  part[hf][5] = fmaf(zc[u], w1.y, part[hf][5]);
-                  part[hf][6] = fmaf(zc[u], w1.z, part[hf][6]);
-                  part[hf][7] = fmaf(zc[u], w1.w, part[hf][7]);
-                }
-              }
+          for (int u = 0; u < 4; ++u) {
+            const float4 w0 = *reinterpret_cast<const float4*>(wf + (32 * hf + c4 + u) * 8);
+            part[0] = fmaf(zc[u], w0.x, part[0]);
+            part[1] = fmaf(zc[u], w0.y, part[1]);
+            part[2] = fmaf(zc[u], w0.z, part[2]);
+            part[3] = fmaf(zc[u], w0.w, part[3]);
+            if (nb > 4) {
+              const float4 w1 = *reinterpret_cast<const float4*>(wf + (32 * hf + c4 + u) * 8 + 4);
+              part[4] = fmaf(zc[u], w1.x, part[4]);
+              part[5] = fmaf(zc[u], w1.y, part[5]);
+              part[6] = fmaf(zc[u], w1.z, part[6]);
+              part[7] = fmaf(zc[u], w1.w, part[7]);
             }
           }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) part[k] += __shfl_xor_sync(0xffffffffu, part[k], 1);
+        if (hf == 0 && row < kTile && row_valid(geo, prow) && !(fd.dbg & 2)) {
           int b, t, f;
           geo.coords(prow, b, t, f);
           float* dst = fd.llr + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * nb;
           if (nb == 4) {
-            *reinterpret_cast<float4*>(dst) = make_float4((part[0][0] + part[1][0]) + hb[0], (part[0][1] + part[1][1]) + hb[1],
-                                                          (part[0][2] + part[1][2]) + hb[2], (part[0][3] + part[1][3]) + hb[3]);
+            *reinterpret_cast<float4*>(dst) = make_float4(part[0] + hb[0], part[1] + hb[1], part[2] + hb[2], part[3] + hb[3]);
           } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-              if (k < nb) dst[k] = (part[0][k] + part[1][k]) + hb[k];
+              if (k < nb) dst[k] = part[k] + hb[k];
           }
         }
       }
