@@ -322,7 +322,11 @@ class Leg:
             peak = SM_COUNT * 128 * 2 * mhz * 1e6 / 1e12
             out.update({"bound": "ffma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                         "frac": achieved / peak if achieved else None,
-                        "peak_kind": f"nominal FP32 (148 SMs x 128 FMA/clk) at the sampled {mhz:.0f} MHz"})
+                        "peak_kind": f"nominal FP32 (148 SMs x 128 FMA/clk) at the sampled {mhz:.0f} MHz",
+                        # the reference's arithmetic is a separately rounded multiply then add (no FMA):
+                        # two FP32 lane-ops per MAC, measured 62 MAC/clk/SM (tools/probes/ffma2_probe.cu)
+                        "bit_exact_peak": peak / 2,
+                        "frac_of_bit_exact_peak": 2 * achieved / peak if achieved else None})
         else:
             peak, kind = pick_peak(pk, clocks or {})
             out.update({"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

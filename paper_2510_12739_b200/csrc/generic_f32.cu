@@ -10,6 +10,8 @@
 // single-consumer BN / ReLU / add|mul chain that follows it without changing any rounding.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <string>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -95,6 +97,14 @@ __global__ void __launch_bounds__(128) conv_f32_kernel(const ConvF32 p) {
 __device__ __forceinline__ float2 mul2_rn(float2 a, float2 b) {
   uint64_t r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+  return *reinterpret_cast<const float2*>(&r);
+}
+// acc + m as fma.rn.f32x2(m, one, acc) with `one` a runtime 1.0 (a kernel argument): m * 1 is exact, so
+// this is the separately rounded add; ptxas contracts a mul.rn.f32x2 feeding an add.rn.f32x2 into FFMA2
+// (single rounding) even under -fmad=false, but cannot fold a product into an fma it cannot see through.
+__device__ __forceinline__ float2 acc2_rn(float2 acc, float2 m, float2 one) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(*reinterpret_cast<const uint64_t*>(&m)), "l"(*reinterpret_cast<const uint64_t*>(&one)), "l"(*reinterpret_cast<const uint64_t*>(&acc)));
   return *reinterpret_cast<const float2*>(&r);
 }
 __device__ __forceinline__ float2 add2_rn(float2 a, float2 b) {
@@ -229,6 +239,155 @@ __global__ void __launch_bounds__(128) conv_f32_px_kernel(const ConvF32 p) {
   }
 }
 
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+
+// Shared-memory tiled form of the same conv (same per-output operation order: bias, taps in (dt, df)
+// order, input channels in order, separately rounded products and sums, out-of-range taps skipped).
+// A block owns one slot's T x FT output window for NG x COT output channels: the T x (FT + 2*halo) x cin
+// input window is staged in shared memory once (cp.async; row stride cin|1 words, so lanes walking f hit
+// distinct banks) and shared by NG groups of 128 threads, group g computing output channels
+// [co0 + g*COT, +COT) from its own weight slab [tap][cin][COT].  A thread computes PX adjacent pixels
+// of one row as COT/2 channel pairs: one packed multiply (mul.rn.f32x2) and one packed add per two MACs,
+// each lane rounded on its own — the reference's scalar x*w then y+=, two at a time.  (Packing saves
+// issue slots only: the FP32 pipe does 128 lane-ops/clk/SM either way, tools/probes/ffma2_probe.cu.)
+template <int PX, int COT, int NG>
+__global__ void __launch_bounds__(128 * NG) conv_f32_tile_kernel(const ConvF32 p, int FT, int ntf, float one_) {
+  const float2 one = make_float2(one_, one_);
+  extern __shared__ __align__(16) float smem_f[];
+  const int taps = p.kh * p.kw;
+  const int oh = p.kh / 2, ow = p.kw / 2;
+  const int hf = ow * p.dil_f;
+  const int W = FT + 2 * hf;
+  const int cs = p.cin | 1;
+  const int wslab = taps * p.cin * COT;
+  float* sx = smem_f + NG * wslab;  // [T][W][cs] after NG weight slabs [taps][cin][COT]
+  const int b = blockIdx.x / ntf;
+  const int f0 = (blockIdx.x % ntf) * FT;
+  const int cob = blockIdx.y * NG * COT;
+  // staging by cp.async (4-byte copies, zero-filled when out of range): every load in flight at once
+  for (int i = threadIdx.x; i < NG * wslab; i += blockDim.x) {
+    const int co = cob + (i / wslab) * COT + i % COT;
+    const int tci = (i % wslab) / COT;
+    cp_async4(smem_f + i, p.w + static_cast<int64_t>(tci) * p.cout + (co < p.cout ? co : 0), co < p.cout);
+  }
+  {
+    const float* xb = p.x + static_cast<int64_t>(b) * p.T * p.F * p.cin;
+    // one warp per window pixel, lanes over its channels (coalesced: a pixel's cin floats are contiguous)
+    const int lane = threadIdx.x & 31;
+    for (int pc = threadIdx.x >> 5; pc < p.T * W; pc += blockDim.x >> 5) {
+      const int t = pc / W, fc = pc - t * W;
+      const int fi = f0 - hf + fc;
+      const bool in = fi >= 0 && fi < p.F;
+      const float* src = xb + (static_cast<int64_t>(t) * p.F + (in ? fi : 0)) * p.cin;
+      for (int ci = lane; ci < p.cin; ci += 32) cp_async4(sx + pc * cs + ci, src + ci, in);
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const int g = threadIdx.x / 128;
+  const int co0 = cob + g * COT;
+  const int ncot = min(COT, p.cout - co0);
+  const int tid = threadIdx.x % 128;
+  const int tpr = FT / PX;
+  const int t = tid / tpr;
+  const int fl = (tid - t * tpr) * PX;  // first local column of this thread
+  if (ncot <= 0 || t >= p.T || f0 + fl >= p.F) return;
+  const float* sw = smem_f + g * wslab;
+  bool live[PX];
+#pragma unroll
+  for (int k = 0; k < PX; ++k) live[k] = f0 + fl + k < p.F;
+  float2 acc[PX][COT / 2];
+#pragma unroll
+  for (int k = 0; k < PX; ++k)
+#pragma unroll
+    for (int q = 0; q < COT / 2; ++q)
+      acc[k][q] = make_float2((p.bias && 2 * q < ncot) ? p.bias[co0 + 2 * q] : 0.f,
+                              (p.bias && 2 * q + 1 < ncot) ? p.bias[co0 + 2 * q + 1] : 0.f);
+  for (int dt = 0; dt < p.kh; ++dt) {
+    const int ti = t + dt - oh;
+    if (ti < 0 || ti >= p.T) continue;
+    for (int df = 0; df < p.kw; ++df) {
+      bool ok[PX];
+      bool all = true, any = false;
+#pragma unroll
+      for (int k = 0; k < PX; ++k) {
+        const int fi = f0 + fl + k + (df - ow) * p.dil_f;
+        ok[k] = live[k] && fi >= 0 && fi < p.F;
+        all &= ok[k];
+        any |= ok[k];
+      }
+      if (!any) continue;
+      const float* xr = sx + (ti * W + fl + df * p.dil_f) * cs;  // pixel k at xr + k*cs
+      const float* wt = sw + (dt * p.kw + df) * p.cin * COT;
+      if (all) {
+#pragma unroll 4
+        for (int ci = 0; ci < p.cin; ++ci) {
+          const float4* w4 = reinterpret_cast<const float4*>(wt + ci * COT);
+          float2 wp[COT / 2];
+#pragma unroll
+          for (int q = 0; q < COT / 4; ++q) {
+            const float4 v = w4[q];
+            wp[2 * q] = make_float2(v.x, v.y);
+            wp[2 * q + 1] = make_float2(v.z, v.w);
+          }
+#pragma unroll
+          for (int k = 0; k < PX; ++k) {
+            const float xv = xr[k * cs + ci];
+            const float2 xx = make_float2(xv, xv);
+#pragma unroll
+            for (int q = 0; q < COT / 2; ++q) acc[k][q] = acc2_rn(acc[k][q], mul2_rn(xx, wp[q]), one);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < PX; ++k) {
+          if (!ok[k]) continue;
+          for (int ci = 0; ci < p.cin; ++ci) {
+            const float4* w4 = reinterpret_cast<const float4*>(wt + ci * COT);
+            const float xv = xr[k * cs + ci];
+            const float2 xx = make_float2(xv, xv);
+#pragma unroll
+            for (int q = 0; q < COT / 4; ++q) {
+              const float4 v = w4[q];
+              acc[k][2 * q] = acc2_rn(acc[k][2 * q], mul2_rn(xx, make_float2(v.x, v.y)), one);
+              acc[k][2 * q + 1] = acc2_rn(acc[k][2 * q + 1], mul2_rn(xx, make_float2(v.z, v.w)), one);
+            }
+          }
+        }
+      }
+    }
+  }
+  const int64_t pixrow = (static_cast<int64_t>(b) * p.T + t) * p.F + f0 + fl;
+#pragma unroll
+  for (int k = 0; k < PX; ++k) {
+    if (!live[k]) continue;
+    const int64_t pix = pixrow + k;
+    float* yr = p.y + pix * p.cout + co0;
+    const float* orow = p.other ? p.other + pix * p.cout + co0 : nullptr;
+    float v[COT];
+#pragma unroll
+    for (int c = 0; c < COT; ++c) {
+      v[c] = (c & 1) ? acc[k][c / 2].y : acc[k][c / 2].x;
+      if (c >= ncot) continue;
+      if (p.aff_s) v[c] = __fadd_rn(__fmul_rn(v[c], p.aff_s[co0 + c]), p.aff_t[co0 + c]);
+      if (p.relu) v[c] = v[c] > 0.f ? v[c] : 0.f;
+      if (p.other_op == 6) v[c] = __fadd_rn(v[c], orow[c]);
+      if (p.other_op == 7) v[c] = __fmul_rn(v[c], orow[c]);
+    }
+    if (ncot == COT && (p.cout & 3) == 0) {
+#pragma unroll
+      for (int c = 0; c < COT; c += 4) *reinterpret_cast<float4*>(yr + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < COT; ++c)
+        if (c < ncot) yr[c] = v[c];
+    }
+  }
+}
+
 __global__ void dwconv_f32_kernel(const float* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
                                   float* __restrict__ y, int B, int T, int F, int C, int kh, int kw) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -309,12 +468,49 @@ inline unsigned nblk(int64_t n, int t) { return static_cast<unsigned>((n + t - 1
 
 }  // namespace
 
+// T rows x FT columns per block, PX pixels per thread; NG groups x COT output channels share the staged
+// input window.  Returns null when the window does not fit (the caller falls back to conv_f32_px).
+template <int PX, int COT, int NG>
+const char* launch_conv_f32_tile(const ConvF32& p, cudaStream_t s) {
+  int FT = (128 / p.T) * PX;
+  FT = std::min(FT, (p.F + PX - 1) / PX * PX);
+  const int hf = (p.kw / 2) * p.dil_f;
+  const size_t tsmem = sizeof(float) * (static_cast<size_t>(NG) * p.kh * p.kw * p.cin * COT +
+                                        static_cast<size_t>(p.T) * (FT + 2 * hf) * (p.cin | 1));
+  if (tsmem > 120 * 1024) return nullptr;
+  const int ntf = (p.F + FT - 1) / FT;
+  auto kern = conv_f32_tile_kernel<PX, COT, NG>;
+  if (tsmem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(tsmem));
+  dim3 grid(static_cast<unsigned>(p.B * ntf), static_cast<unsigned>((p.cout + NG * COT - 1) / (NG * COT)));
+  kern<<<grid, 128 * NG, tsmem, s>>>(p, FT, ntf, 1.0f);
+  CNRX_CUDA(cudaGetLastError());
+  static const std::string name = "conv_f32_tile_kernel<" + std::to_string(PX) + "," + std::to_string(COT) + "," +
+                                  std::to_string(NG) + ">";
+  return name.c_str();
+}
+
 const char* launch_conv_f32(const ConvF32& p, cudaStream_t s) {
   const int64_t npix = static_cast<int64_t>(p.B) * p.T * p.F;
   const size_t smem = sizeof(float) * p.kh * p.kw * p.cin * kCot;
   if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(conv_f32_kernel), static_cast<int>(smem));
   require(smem <= 227 * 1024, "fp32 conv weights tile exceeds shared memory");
   static const int px = std::getenv("CNRX_F32_PX") ? std::atoi(std::getenv("CNRX_F32_PX")) : 2;
+  static const int tile = std::getenv("CNRX_F32_TILE") ? std::atoi(std::getenv("CNRX_F32_TILE")) : 1;
+  if (tile && p.T <= 64) {
+    switch (tile) {  // 1: measured choice (tools/f32_ab.py, profiles/r02_f32_tile_ab.log); 2..5 A/B variants
+      case 2: if (const char* n = launch_conv_f32_tile<1, 8, 2>(p, s)) return n; break;
+      case 3: if (const char* n = launch_conv_f32_tile<2, 8, 4>(p, s)) return n; break;
+      case 4: if (const char* n = launch_conv_f32_tile<2, 4, 4>(p, s)) return n; break;
+      case 5: if (const char* n = launch_conv_f32_tile<1, 8, 4>(p, s)) return n; break;
+      default:
+        // narrow inputs (cfg1's 32 channels): one pixel per thread, twice the warps; wide inputs: two
+        // pixels per thread (half the weight reads), one pixel when that window does not fit
+        if (p.cin > 32)
+          if (const char* n = launch_conv_f32_tile<2, 8, 2>(p, s)) return n;
+        if (const char* n = launch_conv_f32_tile<1, 8, 2>(p, s)) return n;
+        break;
+    }
+  }
   if (px == 4 && npix >= 4 * 148 * 128) {
     if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(conv_f32_px_kernel<4>), static_cast<int>(smem));
     dim3 grid4(nblk((npix + 3) / 4, 128), static_cast<unsigned>((p.cout + kCot - 1) / kCot));

@@ -73,3 +73,31 @@ def test_largest_bench_batch_slots_match_single_slot_runs():
         torch.cuda.synchronize()
         assert torch.equal(one[0], out[i]), i
     assert torch.isfinite(out).all()
+
+
+@pytest.mark.parametrize("k,dil,cin,cout,T,F", [
+    (3, 1, 6, 32, 14, 72),     # cfg1's first conv: narrow input, tile kernel <1,8,2>
+    (1, 1, 1, 1, 1, 1),        # smallest everything
+    (5, 3, 33, 17, 7, 40),     # 5x5 dilated, odd channel counts, partial output-channel group
+    (3, 2, 64, 24, 12, 37),    # wide input: two pixels per thread <2,8,2>, ragged F tiles
+    (3, 1, 96, 16, 14, 20),    # 96 channels: only the one-pixel window fits
+    (3, 1, 128, 8, 14, 19),    # window too large for shared memory: direct-conv fallback
+    (3, 1, 8, 8, 64, 5),       # T = 64: two columns per tile
+    (3, 1, 8, 8, 65, 5),       # T > 64: direct-conv fallback
+])
+def test_fp32_conv_tiles_bit_exact(k, dil, cin, cout, T, F):
+    """The fp32 direct conv over its tiling corners (conv_f32_tile_kernel variants and the conv_f32_px
+    fallback) inside a conv -> BN -> ReLU -> conv -> add block: bit-exact with the reference arithmetic."""
+    g = G.Graph()
+    xi = g.add_input(cin)
+    s = g.add_conv(xi, "s", k, cin, cout, True, dilation_f=dil)
+    h = g.add_relu(g.add_norm(g.add_conv(s, "a", k, cout, cout, False, dilation_f=dil), "bn", "n", cout))
+    g.set_output(g.add_binary(G.OP_ADD, g.add_conv(h, "b", k, cout, cout, True, dilation_f=dil), s))
+    g.init_he_normal(k * 100 + cin, randomize_aux=True)
+    x = np.random.default_rng(cin + T).standard_normal((3, T, F, cin)).astype(np.float32)
+    p = P.Plan(g, "fp32")
+    got = p.forward(x)
+    assert np.array_equal(got, oracle.forward(g, x)), "fp32 conv differs from the reference arithmetic"
+    names = p.launch_names()
+    fallback = cin == 128 or T > 64  # conv_f32_px_kernel, or conv_f32_kernel on small grids
+    assert any(("conv_f32_px" in n or n == "conv_f32_kernel") if fallback else "conv_f32_tile" in n for n in names), names
