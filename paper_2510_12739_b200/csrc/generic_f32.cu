@@ -244,16 +244,22 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool val
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(valid ? 4 : 0) : "memory");
 }
 
+// Row stride (words) of a staged input pixel: cin rounded up to 4 (16-byte reads of four channels), with
+// an odd number of 16-byte units so the 8 lanes of each LDS.128 phase, walking f, hit distinct banks.
+__host__ __device__ inline int f32_tile_row_stride(int cin) {
+  const int u = (cin + 3) / 4;
+  return 4 * (u | 1);
+}
+
 // Shared-memory tiled form of the same conv (same per-output operation order: bias, taps in (dt, df)
 // order, input channels in order, separately rounded products and sums, out-of-range taps skipped).
 // A block owns one slot's T x FT output window for NG x COT output channels: the T x (FT + 2*halo) x cin
-// input window is staged in shared memory once (cp.async; row stride cin|1 words, so lanes walking f hit
-// distinct banks) and shared by NG groups of 128 threads, group g computing output channels
+// input window is staged in shared memory once (cp.async; row stride f32_tile_row_stride) and shared by NG groups of 128 threads, group g computing output channels
 // [co0 + g*COT, +COT) from its own weight slab [tap][cin][COT].  A thread computes PX adjacent pixels
 // of one row as COT/2 channel pairs: one packed multiply (mul.rn.f32x2) and one packed add per two MACs,
 // each lane rounded on its own — the reference's scalar x*w then y+=, two at a time.  (Packing saves
 // issue slots only: the FP32 pipe does 128 lane-ops/clk/SM either way, tools/probes/ffma2_probe.cu.)
-template <int PX, int COT, int NG>
+template <int PX, int COT, int NG, bool WS>
 __global__ void __launch_bounds__(128 * NG) conv_f32_tile_kernel(const ConvF32 p, int FT, int ntf, float one_) {
   const float2 one = make_float2(one_, one_);
   extern __shared__ __align__(16) float smem_f[];
@@ -261,18 +267,23 @@ __global__ void __launch_bounds__(128 * NG) conv_f32_tile_kernel(const ConvF32 p
   const int oh = p.kh / 2, ow = p.kw / 2;
   const int hf = ow * p.dil_f;
   const int W = FT + 2 * hf;
-  const int cs = p.cin | 1;
-  const int wslab = taps * p.cin * COT;
-  float* sx = smem_f + NG * wslab;  // [T][W][cs] after NG weight slabs [taps][cin][COT]
+  const int cs = f32_tile_row_stride(p.cin);
+  const int wtap = p.cin * COT;                 // one group's weights of one tap: [cin][COT]
+  const int wslab = (WS ? 1 : taps) * wtap;     // one group's share of a weight buffer
+  float* sx = smem_f + (WS ? 2 : 1) * NG * wslab;  // [T][W][cs] after the weight buffer(s) [NG][taps|1][cin][COT]
   const int b = blockIdx.x / ntf;
   const int f0 = (blockIdx.x % ntf) * FT;
   const int cob = blockIdx.y * NG * COT;
   // staging by cp.async (4-byte copies, zero-filled when out of range): every load in flight at once
-  for (int i = threadIdx.x; i < NG * wslab; i += blockDim.x) {
-    const int co = cob + (i / wslab) * COT + i % COT;
-    const int tci = (i % wslab) / COT;
-    cp_async4(smem_f + i, p.w + static_cast<int64_t>(tci) * p.cout + (co < p.cout ? co : 0), co < p.cout);
-  }
+  auto stage_w = [&](int tap0, int ntap, float* dst) {
+    for (int i = threadIdx.x; i < NG * ntap * wtap; i += blockDim.x) {
+      const int gi = i / (ntap * wtap), r = i - gi * ntap * wtap;
+      const int co = cob + gi * COT + r % COT;
+      const int tci = tap0 * p.cin + r / COT;  // tap * cin + ci
+      cp_async4(dst + i, p.w + static_cast<int64_t>(tci) * p.cout + (co < p.cout ? co : 0), co < p.cout);
+    }
+  };
+  stage_w(0, WS ? 1 : taps, smem_f);
   {
     const float* xb = p.x + static_cast<int64_t>(b) * p.T * p.F * p.cin;
     // one warp per window pixel, lanes over its channels (coalesced: a pixel's cin floats are contiguous)
@@ -294,8 +305,8 @@ __global__ void __launch_bounds__(128 * NG) conv_f32_tile_kernel(const ConvF32 p
   const int tpr = FT / PX;
   const int t = tid / tpr;
   const int fl = (tid - t * tpr) * PX;  // first local column of this thread
-  if (ncot <= 0 || t >= p.T || f0 + fl >= p.F) return;
-  const float* sw = smem_f + g * wslab;
+  const bool active = ncot > 0 && t < p.T && f0 + fl < p.F;
+  if (!WS && !active) return;  // (streamed weights: every thread stays for the per-tap barriers)
   bool live[PX];
 #pragma unroll
   for (int k = 0; k < PX; ++k) live[k] = f0 + fl + k < p.F;
@@ -304,27 +315,52 @@ __global__ void __launch_bounds__(128 * NG) conv_f32_tile_kernel(const ConvF32 p
   for (int k = 0; k < PX; ++k)
 #pragma unroll
     for (int q = 0; q < COT / 2; ++q)
-      acc[k][q] = make_float2((p.bias && 2 * q < ncot) ? p.bias[co0 + 2 * q] : 0.f,
-                              (p.bias && 2 * q + 1 < ncot) ? p.bias[co0 + 2 * q + 1] : 0.f);
-  for (int dt = 0; dt < p.kh; ++dt) {
+      acc[k][q] = make_float2((active && p.bias && 2 * q < ncot) ? p.bias[co0 + 2 * q] : 0.f,
+                              (active && p.bias && 2 * q + 1 < ncot) ? p.bias[co0 + 2 * q + 1] : 0.f);
+  for (int tap = 0; tap < taps; ++tap) {
+    if (WS && tap + 1 < taps) stage_w(tap + 1, 1, smem_f + ((tap + 1) & 1) * NG * wslab);
+    const int dt = tap / p.kw, df = tap - dt * p.kw;
     const int ti = t + dt - oh;
-    if (ti < 0 || ti >= p.T) continue;
-    for (int df = 0; df < p.kw; ++df) {
-      bool ok[PX];
-      bool all = true, any = false;
+    bool ok[PX];
+    bool all = true, any = false;
 #pragma unroll
-      for (int k = 0; k < PX; ++k) {
-        const int fi = f0 + fl + k + (df - ow) * p.dil_f;
-        ok[k] = live[k] && fi >= 0 && fi < p.F;
-        all &= ok[k];
-        any |= ok[k];
-      }
-      if (!any) continue;
+    for (int k = 0; k < PX; ++k) {
+      const int fi = f0 + fl + k + (df - ow) * p.dil_f;
+      ok[k] = active && live[k] && ti >= 0 && ti < p.T && fi >= 0 && fi < p.F;
+      all &= ok[k];
+      any |= ok[k];
+    }
+    if (any) {
       const float* xr = sx + (ti * W + fl + df * p.dil_f) * cs;  // pixel k at xr + k*cs
-      const float* wt = sw + (dt * p.kw + df) * p.cin * COT;
+      const float* wt = WS ? smem_f + (tap & 1) * NG * wslab + g * wslab : smem_f + g * wslab + tap * wtap;
       if (all) {
-#pragma unroll 4
-        for (int ci = 0; ci < p.cin; ++ci) {
+        // four input channels per step: one 16-byte read of each pixel's x, 4 x COT/4 of weights
+        const int cin4 = p.cin >> 2;
+#pragma unroll 2
+        for (int c4 = 0; c4 < cin4; ++c4) {
+          float4 xq[PX];
+#pragma unroll
+          for (int k = 0; k < PX; ++k) xq[k] = *reinterpret_cast<const float4*>(xr + k * cs + 4 * c4);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4* w4 = reinterpret_cast<const float4*>(wt + (4 * c4 + u) * COT);
+            float2 wp[COT / 2];
+#pragma unroll
+            for (int q = 0; q < COT / 4; ++q) {
+              const float4 v = w4[q];
+              wp[2 * q] = make_float2(v.x, v.y);
+              wp[2 * q + 1] = make_float2(v.z, v.w);
+            }
+#pragma unroll
+            for (int k = 0; k < PX; ++k) {
+              const float xv = u == 0 ? xq[k].x : u == 1 ? xq[k].y : u == 2 ? xq[k].z : xq[k].w;
+              const float2 xx = make_float2(xv, xv);
+#pragma unroll
+              for (int q = 0; q < COT / 2; ++q) acc[k][q] = acc2_rn(acc[k][q], mul2_rn(xx, wp[q]), one);
+            }
+          }
+        }
+        for (int ci = 4 * cin4; ci < p.cin; ++ci) {
           const float4* w4 = reinterpret_cast<const float4*>(wt + ci * COT);
           float2 wp[COT / 2];
 #pragma unroll
@@ -359,7 +395,12 @@ __global__ void __launch_bounds__(128 * NG) conv_f32_tile_kernel(const ConvF32 p
         }
       }
     }
+    if (WS) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+    }
   }
+  if (!active) return;
   const int64_t pixrow = (static_cast<int64_t>(b) * p.T + t) * p.F + f0 + fl;
 #pragma unroll
   for (int k = 0; k < PX; ++k) {
@@ -470,43 +511,58 @@ inline unsigned nblk(int64_t n, int t) { return static_cast<unsigned>((n + t - 1
 
 // T rows x FT columns per block, PX pixels per thread; NG groups x COT output channels share the staged
 // input window.  Returns null when the window does not fit (the caller falls back to conv_f32_px).
+// T rows x FT columns per block, PX pixels per thread; NG groups x COT output channels share the staged
+// input window.  Weights: all taps resident, or (WS) one tap at a time, double-buffered, when the
+// resident form would leave fewer than two blocks per SM (force_ws: -1 choose, 0 resident only, 1 WS).
+// Returns null when that does not fit (the caller falls back to conv_f32_px).
 template <int PX, int COT, int NG>
-const char* launch_conv_f32_tile(const ConvF32& p, cudaStream_t s) {
+const char* launch_conv_f32_tile(const ConvF32& p, cudaStream_t s, int force_ws = -1) {
   int FT = (128 / p.T) * PX;
   FT = std::min(FT, (p.F + PX - 1) / PX * PX);
   const int hf = (p.kw / 2) * p.dil_f;
-  const size_t tsmem = sizeof(float) * (static_cast<size_t>(NG) * p.kh * p.kw * p.cin * COT +
-                                        static_cast<size_t>(p.T) * (FT + 2 * hf) * (p.cin | 1));
-  if (tsmem > 120 * 1024) return nullptr;
+  const size_t xwin = static_cast<size_t>(p.T) * (FT + 2 * hf) * f32_tile_row_stride(p.cin);
+  const size_t wres = static_cast<size_t>(NG) * p.kh * p.kw * p.cin * COT;
+  const size_t wstr = 2 * static_cast<size_t>(NG) * p.cin * COT;
+  // resident weights while two blocks still fit on an SM (2 x (112 + 1 reserved) KB of 228)
+  const bool fits2 = sizeof(float) * (wres + xwin) <= 112 * 1024;
+  if (force_ws == 0 && !fits2) return nullptr;
+  const bool ws = force_ws >= 0 ? force_ws == 1 : !fits2;
+  const size_t tsmem = sizeof(float) * ((ws ? wstr : wres) + xwin);
+  if (tsmem > 200 * 1024) return nullptr;
   const int ntf = (p.F + FT - 1) / FT;
-  auto kern = conv_f32_tile_kernel<PX, COT, NG>;
+  auto kern = ws ? conv_f32_tile_kernel<PX, COT, NG, true> : conv_f32_tile_kernel<PX, COT, NG, false>;
   if (tsmem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(tsmem));
   dim3 grid(static_cast<unsigned>(p.B * ntf), static_cast<unsigned>((p.cout + NG * COT - 1) / (NG * COT)));
   kern<<<grid, 128 * NG, tsmem, s>>>(p, FT, ntf, 1.0f);
   CNRX_CUDA(cudaGetLastError());
-  static const std::string name = "conv_f32_tile_kernel<" + std::to_string(PX) + "," + std::to_string(COT) + "," +
-                                  std::to_string(NG) + ">";
-  return name.c_str();
+  static const std::string name[2] = {
+      "conv_f32_tile_kernel<" + std::to_string(PX) + "," + std::to_string(COT) + "," + std::to_string(NG) + ">",
+      "conv_f32_tile_kernel<" + std::to_string(PX) + "," + std::to_string(COT) + "," + std::to_string(NG) + ",ws>"};
+  return name[ws].c_str();
 }
 
 const char* launch_conv_f32(const ConvF32& p, cudaStream_t s) {
   const int64_t npix = static_cast<int64_t>(p.B) * p.T * p.F;
   const size_t smem = sizeof(float) * p.kh * p.kw * p.cin * kCot;
-  if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(conv_f32_kernel), static_cast<int>(smem));
   require(smem <= 227 * 1024, "fp32 conv weights tile exceeds shared memory");
+  if (smem > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(conv_f32_kernel), static_cast<int>(smem));
   static const int px = std::getenv("CNRX_F32_PX") ? std::atoi(std::getenv("CNRX_F32_PX")) : 2;
   static const int tile = std::getenv("CNRX_F32_TILE") ? std::atoi(std::getenv("CNRX_F32_TILE")) : 1;
   if (tile && p.T <= 64) {
-    switch (tile) {  // 1: measured choice (tools/f32_ab.py, profiles/r02_f32_tile_ab.log); 2..5 A/B variants
+    switch (tile) {  // 1: measured choice (tools/f32_ab.py, profiles/r02_f32_tile_ab.log); 2..8 A/B variants
       case 2: if (const char* n = launch_conv_f32_tile<1, 8, 2>(p, s)) return n; break;
       case 3: if (const char* n = launch_conv_f32_tile<2, 8, 4>(p, s)) return n; break;
-      case 4: if (const char* n = launch_conv_f32_tile<2, 4, 4>(p, s)) return n; break;
+      case 4: if (const char* n = launch_conv_f32_tile<2, 8, 2>(p, s, 1)) return n; break;
       case 5: if (const char* n = launch_conv_f32_tile<1, 8, 4>(p, s)) return n; break;
+      case 6: if (const char* n = launch_conv_f32_tile<1, 16, 2>(p, s)) return n; break;
+      case 7: if (const char* n = launch_conv_f32_tile<1, 8, 2>(p, s, 1)) return n; break;
+      case 8: if (const char* n = launch_conv_f32_tile<2, 8, 4>(p, s, 1)) return n; break;
       default:
         // narrow inputs (cfg1's 32 channels): one pixel per thread, twice the warps; wide inputs: two
-        // pixels per thread (half the weight reads), one pixel when that window does not fit
+        // pixels per thread (half the weight reads) while the weights stay resident, else one pixel per
+        // thread with per-tap weights (96 channels: 13.1 -> 9.6 ms for cfg4 B = 8)
         if (p.cin > 32)
-          if (const char* n = launch_conv_f32_tile<2, 8, 2>(p, s)) return n;
+          if (const char* n = launch_conv_f32_tile<2, 8, 2>(p, s, 0)) return n;
         if (const char* n = launch_conv_f32_tile<1, 8, 2>(p, s)) return n;
         break;
     }

@@ -80,8 +80,9 @@ def test_largest_bench_batch_slots_match_single_slot_runs():
     (1, 1, 1, 1, 1, 1),        # smallest everything
     (5, 3, 33, 17, 7, 40),     # 5x5 dilated, odd channel counts, partial output-channel group
     (3, 2, 64, 24, 12, 37),    # wide input: two pixels per thread <2,8,2>, ragged F tiles
-    (3, 1, 96, 16, 14, 20),    # 96 channels: only the one-pixel window fits
-    (3, 1, 128, 8, 14, 19),    # window too large for shared memory: direct-conv fallback
+    (3, 1, 96, 16, 14, 20),    # 96 channels: one pixel per thread, weights streamed per tap (ws)
+    (3, 2, 128, 8, 14, 19),    # 128 channels, dilated: ws
+    (3, 1, 320, 8, 14, 9),     # window too large for shared memory: direct-conv fallback
     (3, 1, 8, 8, 64, 5),       # T = 64: two columns per tile
     (3, 1, 8, 8, 65, 5),       # T > 64: direct-conv fallback
 ])
@@ -99,5 +100,7 @@ def test_fp32_conv_tiles_bit_exact(k, dil, cin, cout, T, F):
     got = p.forward(x)
     assert np.array_equal(got, oracle.forward(g, x)), "fp32 conv differs from the reference arithmetic"
     names = p.launch_names()
-    fallback = cin == 128 or T > 64  # conv_f32_px_kernel, or conv_f32_kernel on small grids
+    fallback = cin == 320 or T > 64  # conv_f32_px_kernel, or conv_f32_kernel on small grids
     assert any(("conv_f32_px" in n or n == "conv_f32_kernel") if fallback else "conv_f32_tile" in n for n in names), names
+    if cin in (96, 128):
+        assert any(n.endswith(",ws>") for n in names), names
