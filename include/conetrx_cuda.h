@@ -56,10 +56,19 @@ extern "C" {
  *         tensor-core configuration).
  *   FP16: the same tensor-core plan with fp16 weights/activations (11-bit mantissa, |x| <= 65504,
  *         saturating) and an fp32 LLR head: same speed and bytes as BF16, and the mixed-precision
- *         option that meets the >= 99.99 % hard-decision agreement with the reference. */
+ *         option that meets the >= 99.99 % hard-decision agreement with the reference.
+ *   BF16X3: fp32-grade results on the tensor cores (the north star's "LLRs within 1e-4 relative" fp32
+ *         path at tensor-core rates): every activation and weight is carried as a 16-bit pair
+ *         (hi = bf16(v), lo = bf16(v - hi); 16 significant bits, fp32 range) and each conv is three
+ *         tcgen05 products hi*Whi + hi*Wlo + lo*Whi accumulated in fp32; pointwise ops and the head in
+ *         fp32.  3x the BF16 plan's tensor work, the bytes of fp32 planes.  Options are fixed (one conv
+ *         kernel, separate head).
+ *   FP16X3: the same with fp16 pairs (22 significant bits; values must stay within |x| <= 65504). */
 #define CNRX_FP32 0
 #define CNRX_BF16 1
 #define CNRX_FP16 2
+#define CNRX_BF16X3 3
+#define CNRX_FP16X3 4
 
 /* GraphNode (network.hpp:19-26) + dilation_f (extension for BASELINE config 3; 1 = reference). */
 typedef struct {

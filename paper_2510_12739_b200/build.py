@@ -20,7 +20,7 @@ BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libconetrx_cuda.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = ["api.cpp", "conv_tc.cu", "conv_ws.cu", "conv_blk.cu", "conv_pair.cu", "featurize.cu", "pointwise.cu", "head.cu", "slotgen.cu", "classic.cu", "generic_f32.cu"]
+SOURCES = ["api.cpp", "conv_tc.cu", "conv_ws.cu", "conv_blk.cu", "conv_pair.cu", "featurize.cu", "pointwise.cu", "head.cu", "slotgen.cu", "classic.cu", "generic_f32.cu", "conv_x3.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

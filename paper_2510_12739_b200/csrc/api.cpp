@@ -33,6 +33,7 @@
 #include "../../include/conetrx_cuda.h"
 #include "common.h"
 #include "conv_tc.h"
+#include "conv_x3.h"
 #include "conv_blk.h"
 #include "conv_pair.h"
 #include "conv_ws.h"
@@ -195,7 +196,9 @@ struct Workspace {
     bool blk = false;
     bool skip = false;  // conv1 group of fused blocks while the workspace runs them fused
     bool pair = false;  // conv_pair.cu (CTA-pair 96 -> 96 3x3)
+    bool x3 = false;    // conv_x3.cu (split-precision plans)
     TcLaunch tc;
+    X3Launch x3l;
     WsLaunch wsl;
     BlkLaunch blkl;
     std::vector<BlkLaunch> chain;  // fused-block head: one block launch per subnetwork, in fold order
@@ -212,7 +215,8 @@ struct Workspace {
 
 struct cnrx_plan {
   int precision = CNRX_FP32;
-  bool fp16 = false;           // CNRX_FP16: the 16-bit planes and weights are fp16
+  bool fp16 = false;           // CNRX_FP16 / CNRX_FP16X3: the 16-bit planes and weights are fp16
+  bool split = false;          // CNRX_BF16X3 / CNRX_FP16X3: planes and weights carried as (hi, lo) pairs
   cnrx_plan_options opt{};
   int device = 0;
   int num_sms = 148;
@@ -898,7 +902,7 @@ struct Bf16Compiler {
       op.cout = round_cout(nd.out_channels);
       op.cin_real = static_cast<int>(w.dims[2]);
       op.cout_real = static_cast<int>(w.dims[3]);
-      if (!conv_tc_supported(op.cin, op.cout, op.ks))
+      if (!(p.split ? conv_x3_supported(op.cin, op.cout, op.ks) : conv_tc_supported(op.cin, op.cout, op.ks)))
         throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: no tcgen05 conv for cin=" + std::to_string(op.cin) +
                                               " cout=" + std::to_string(op.cout) + " k=" + std::to_string(op.ks));
       // epilogue absorption: [BN] [ReLU] [add residual]
@@ -948,6 +952,11 @@ struct Bf16Compiler {
         std::vector<uint32_t> img(conv_ws64_wimg_bytes() / 4);
         conv_ws64_pack_weights(w.data.data(), scale.empty() ? nullptr : scale.data(), p.fp16, img.data());
         op.wimg = p.upload_bytes(img.data(), img.size() * 4);
+      } else if (p.split) {
+        std::vector<uint8_t> img(conv_x3_wimg_bytes(op.cin, op.cout, op.ks));
+        conv_x3_pack_weights(w.data.data(), op.ks, static_cast<int>(w.dims[2]), static_cast<int>(w.dims[3]),
+                             scale.empty() ? nullptr : scale.data(), op.cin, op.cout, p.fp16, img.data());
+        op.wimg = p.upload_bytes(img.data(), img.size());
       } else {
         std::vector<uint8_t> img(conv_tc_wimg_bytes(op.cin, op.cout, op.ks));
         conv_tc_pack_weights(w.data.data(), op.ks, static_cast<int>(w.dims[2]), static_cast<int>(w.dims[3]),
@@ -1137,7 +1146,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
   if (!reuse)
     for (int c : p.buf_channels) {
       void* d = nullptr;
-      const size_t bytes = static_cast<size_t>(ws.geo.Nalloc) * c * 2;
+      const size_t bytes = static_cast<size_t>(ws.geo.Nalloc) * c * 2 * (p.split ? 2 : 1);
       CNRX_CUDA(cudaMalloc(&d, bytes));  // every producer writes all rows of [0, Nalloc): no clearing needed
       ws.buffers.push_back(d);
     }
@@ -1283,6 +1292,34 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           L.head = p.hf;
           ws.head_fused = true;
         }
+      } else if (p.split) {
+        GL.x3 = true;
+        X3Launch& L = GL.x3l;
+        std::memset(&L, 0, sizeof(L));
+        L.fp16 = p.fp16;
+        L.geo = ws.geo;
+        L.ngroups = static_cast<int>(grp.size());
+        if (L.ngroups > kX3MaxGroups) throw Error(CNRX_ERR_UNSUPPORTED, "internal: split conv group too large");
+        int win_alloc = 0;
+        for (size_t gi = 0; gi < grp.size(); ++gi) {
+          const TcOp& op = p.tc[static_cast<size_t>(grp[gi])];
+          X3Group& g = L.g[gi];
+          g.halo = op.ks == 1 ? 0 : ws.geo.T1 * op.dil + 1;
+          g.dil = op.dil;
+          win_alloc = std::max(win_alloc, (128 + 2 * g.halo + 31) / 32 * 32);
+          conv_x3_make_maps(plane_ptr(op.in_plane), ws.geo.Nalloc, op.cin, g.map);
+          g.wimg = static_cast<const uint8_t*>(op.wimg);
+          g.bias = op.bias;
+          g.res = plane_ptr(op.res_plane);
+          g.out = plane_ptr(op.out_plane);
+          g.out2 = plane_ptr(op.out2_plane);
+          g.s2 = op.s2;
+          g.t2 = op.t2;
+          g.relu = op.relu;
+        }
+        L.win_alloc = win_alloc;
+        if (!conv_x3_config(op0.cin, op0.cout, op0.ks, win_alloc, &L.stages, &L.nslots))
+          throw Error(CNRX_ERR_UNSUPPORTED, "split-precision conv working set exceeds shared memory");
       } else {
         TcLaunch& L = GL.tc;
         std::memset(&L, 0, sizeof(L));
@@ -1415,7 +1452,17 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
   auto plane_ptr = [&](int pl) {
     return static_cast<__nv_bfloat16*>(ws.buffers[static_cast<size_t>(p.planes[static_cast<size_t>(pl)].buffer)]);
   };
-  if (p.need_plane0) {
+  if (p.need_plane0 && p.split) {
+    // split plans: features in fp32 (reference layout: the caller's tensor, or featurized into the
+    // workspace's fp32 buffer), then one pass into the (hi, lo) input plane
+    const float* x = in;
+    if (input_kind == 1) {
+      float* feat = static_cast<float*>(ws.feat_buf);
+      p.note(launch_featurize_ref(in, ws.geo, N, p.pt, feat, s), s);
+      x = feat;
+    }
+    p.note(launch_pack_plane(x, ws.geo, p.in_ch, plane_ptr(0), p.planes[0].C, p.fp16, s, true), s);
+  } else if (p.need_plane0) {
     __nv_bfloat16* in_plane = plane_ptr(0);
     if (input_kind == 0)
       p.note(launch_pack_plane(in, ws.geo, p.in_ch, in_plane, p.planes[0].C, p.fp16, s), s);
@@ -1546,6 +1593,10 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
         p.note(conv_pair96_launch(GL.tc, p.num_sms, s), s, fl);
         continue;
       }
+      if (GL.x3) {
+        p.note(conv_x3_launch(op0.cin, op0.cout, op0.ks, GL.x3l, p.num_sms, s), s, fl);
+        continue;
+      }
       p.note(conv_tc_launch(op0.cin, op0.cout, op0.ks, GL.tc, p.num_sms, s), s, fl);
       if (trace) {
         unsigned long long h[16];
@@ -1567,6 +1618,7 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
       PwStep& st = p.pw[static_cast<size_t>(k)];
       PwProgram prog = st.prog;
       prog.fp16 = p.fp16;
+      prog.split = p.split;
       for (int j = 0; j < st.n_planes; ++j) prog.planes[j] = plane_ptr(st.plane_ids[j]);
       if (st.out_plane >= 0)
         prog.out_plane = plane_ptr(st.out_plane);
@@ -1600,7 +1652,7 @@ void run_forward(cnrx_plan& p, const float* x_dev, int64_t B, int64_t T, int64_t
                  int N, cudaStream_t s) {
   ensure_workspace(p, static_cast<int>(B), static_cast<int>(T), static_cast<int>(F));
   float* feat = nullptr;  // fp32 plans on the receive path: features in the reference layout
-  if (p.precision == CNRX_FP32 && input_kind == 1) {  // allocated outside any graph capture
+  if ((p.precision == CNRX_FP32 || p.split) && input_kind == 1) {  // allocated outside any graph capture
     const size_t bytes = static_cast<size_t>(B * T * F * p.in_ch) * sizeof(float);
     feat = static_cast<float*>(ensure_dev(p.ws.feat_buf, p.ws.feat_bytes, bytes));
   }
@@ -1961,7 +2013,9 @@ int cnrx_plan_create_ex(const cnrx_node* nodes, int32_t n_nodes, int32_t input_n
     cnrx_plan_options_default(&plan->opt);
   const int rc = guarded([&] {
     require(nodes && n_nodes > 0, "empty network");
-    require(precision == CNRX_FP32 || precision == CNRX_BF16 || precision == CNRX_FP16, "unknown precision");
+    require(precision == CNRX_FP32 || precision == CNRX_BF16 || precision == CNRX_FP16 || precision == CNRX_BF16X3 ||
+                precision == CNRX_FP16X3,
+            "unknown precision");
     int ndev = 0;
     CNRX_CUDA(cudaGetDeviceCount(&ndev));
     require(device >= 0 && device < ndev, "no such CUDA device " + std::to_string(device));
@@ -1971,7 +2025,18 @@ int cnrx_plan_create_ex(const cnrx_node* nodes, int32_t n_nodes, int32_t input_n
     if (precision != CNRX_FP32 && prop.major != 10)
       throw Error(CNRX_ERR_UNSUPPORTED, "bf16 / fp16 tcgen05 plan needs an sm_100 (Blackwell) device");
     plan->precision = precision;
-    plan->fp16 = precision == CNRX_FP16;
+    plan->fp16 = precision == CNRX_FP16 || precision == CNRX_FP16X3;
+    plan->split = precision == CNRX_BF16X3 || precision == CNRX_FP16X3;
+    if (plan->split) {
+      // split plans run every conv on conv_x3.cu and the tail on the generic pointwise programs
+      plan->opt.fused_blocks = 0;
+      plan->opt.fused_head = 0;
+      plan->opt.tensor_core_head = 0;
+      plan->opt.cta_pair = 0;
+      plan->opt.weights_stationary = 0;
+      plan->opt.relu_on_load = 0;
+      plan->opt.cuda_core_stem = 0;
+    }
     plan->device = device;
     plan->num_sms = prop.multiProcessorCount;
     plan->nodes.assign(nodes, nodes + n_nodes);
@@ -2138,7 +2203,8 @@ int cnrx_feature_plane_device(cnrx_plan* plan, const float* y_dev, int64_t B, in
   if (!plan || !cpad) return fail(CNRX_ERR_INVALID_ARGUMENT, "null argument");
   return guarded([&] {
     std::lock_guard<std::mutex> lk(plan->mu);
-    if (plan->precision == CNRX_FP32) throw Error(CNRX_ERR_UNSUPPORTED, "fp32 plans have no 16-bit feature plane");
+    if (plan->precision == CNRX_FP32 || plan->split)
+      throw Error(CNRX_ERR_UNSUPPORTED, "fp32 and split-precision plans have no 16-bit feature plane");
     check_receive(*plan, B, T, F, N);
     DeviceGuard dg(plan->device);
     CNRX_CUDA(cudaDeviceSynchronize());  // test hook: fully ordered against any earlier call

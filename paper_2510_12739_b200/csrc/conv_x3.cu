@@ -1,0 +1,481 @@
+// conv_x3.cu — split-precision 3x3 / 1x1 "same" convolution on the sm_100a tensor cores: fp32-grade
+// results (LLRs within 1e-4 relative of the reference's fp32 forward) at tensor-core rates.
+//
+// Replaces conetrx::conv2d (reference kernels.hpp:47-91) together with the nodes the plan compiler
+// fuses into its epilogue — folded eval BN (norms.hpp:81-95 via network.hpp:458-459), ReLU
+// (kernels.hpp:305), the residual add (network.hpp:463) and the next block's pre-activation
+// (network.hpp:455-457) as a second output — for CNRX_BF16X3 / CNRX_FP16X3 plans (conv_x3.h).
+//
+// Every value v is carried as hi = round16(v), lo = round16(v - hi); weights likewise.  Per K-step
+// of 16 channels the MMA warp issues three UMMAs into the same fp32 TMEM accumulator:
+//     D += A_hi * W_hi;   D += A_hi * W_lo;   D += A_lo * W_hi
+// (M = 128 plane rows, N = Cout, K = 16), so a conv costs 3x the 16-bit plan's tensor work and
+// moves the same bytes as an fp32 plane.  The plane layout makes every 3x3 tap a constant row shift
+// (common.h), so a tile's whole K loop reads ONE TMA-loaded window of 128 + 2*halo rows of hi and lo.
+//
+// Warp roles (224 threads, persistent, 1 CTA/SM):
+//   warp 0     TMA producer: one hi+lo window per tile into a `stages`-deep ring
+//   warp 1     TMEM allocator + single-thread MMA issuer (taps x K/16 x 3 UMMAs per tile)
+//   warp 2     weight loader: every tap once (resident: 64-channel convs, 147 KB) or, when the split
+//              weights exceed shared memory (96 channels: 331 KB), the taps of every tile through a
+//              ring of `nslots` tap slots (plain bulk copies of the pre-swizzled tap images, L2-resident)
+//   warps 3-6  epilogue: TMEM -> registers -> bias / residual (hi + lo) / ReLU -> hi, lo rows to the
+//              output plane(s); accumulators double-buffered (tile j's epilogue overlaps tile j+1's MMAs)
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "conv_x3.h"
+#include "elem16.cuh"
+#include "sm100.cuh"
+
+namespace cnrx {
+
+namespace {
+
+constexpr int kBoxRows = 32;
+constexpr int kThreads = 224;
+constexpr uint32_t kSmemLimit = 227u * 1024u;
+
+__host__ __device__ constexpr int ch0_of(int cin) { return cin > 64 ? 64 : cin; }
+__host__ __device__ constexpr int ch1_of(int cin) { return cin > 64 ? cin - 64 : 0; }
+__host__ __device__ constexpr uint32_t swz_mode(int rb) {
+  return rb == 128 ? kSwizzle128 : rb == 64 ? kSwizzle64 : rb == 32 ? kSwizzle32 : kSwizzleNone;
+}
+__host__ __device__ inline uint32_t swz_off(int rb, uint32_t r, uint32_t c) {
+  if (rb == 128) return r * 128u + ((c ^ (r & 7u)) << 4);
+  if (rb == 64) return r * 64u + ((c ^ ((r >> 1) & 3u)) << 4);
+  if (rb == 32) return r * 32u + ((c ^ ((r >> 2) & 1u)) << 4);
+  return r * static_cast<uint32_t>(rb) + (c << 4);
+}
+__host__ __device__ constexpr uint32_t a1024(uint32_t x) { return (x + 1023u) & ~1023u; }
+// one tap of the split weight image: [hi | lo], each COUT x CIN 16-bit values
+__host__ __device__ constexpr uint32_t tap_bytes(int cin, int cout) {
+  return 2u * static_cast<uint32_t>(cout) * static_cast<uint32_t>(cin) * 2u;
+}
+__host__ __device__ constexpr uint32_t tmem_cols(int cout) { return 2 * cout <= 64 ? 64 : 2 * cout <= 128 ? 128 : 256; }
+
+struct Lay {
+  uint32_t win_off, stage_bytes, sub[4], par_off, bar_off, total;
+};
+__host__ __device__ inline Lay x3_layout(int cin, int cout, int stages, int win_alloc, int nslots) {
+  Lay s{};
+  const uint32_t b0 = static_cast<uint32_t>(win_alloc * ch0_of(cin) * 2);
+  const uint32_t b1 = static_cast<uint32_t>(win_alloc * ch1_of(cin) * 2);
+  s.win_off = a1024(static_cast<uint32_t>(nslots) * tap_bytes(cin, cout));
+  s.sub[0] = 0;                       // hi, channels [0, 64)
+  s.sub[1] = a1024(b0);               // hi, channels [64, cin)
+  s.sub[2] = a1024(s.sub[1] + b1);    // lo, channels [0, 64)
+  s.sub[3] = a1024(s.sub[2] + b0);    // lo, channels [64, cin)
+  s.stage_bytes = a1024(s.sub[3] + b1);
+  uint32_t off = s.win_off + static_cast<uint32_t>(stages) * s.stage_bytes;
+  s.par_off = off;  // bias, s2, t2 (fp32)
+  off += (3u * static_cast<uint32_t>(cout) * 4u + 15u) & ~15u;
+  s.bar_off = off;
+  s.total = off + 256 + 1024;  // barriers (<= 30) + the TMEM slot, alignment slack of the dynamic base
+  return s;
+}
+
+// v -> (hi, lo) 16-bit pairs for two channels
+template <bool H>
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  hi = pack2<H>(a, b);
+  const float2 f = unpack2<H>(hi);
+  lo = pack2<H>(a - f.x, b - f.y);
+}
+
+template <int CIN, int COUT, int KS, bool F16>
+__global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_constant__ X3Launch L) {
+  constexpr int CH0 = ch0_of(CIN), CH1 = ch1_of(CIN);
+  constexpr int RB0 = CH0 * 2, RB1 = CH1 * 2;
+  constexpr uint32_t SW0 = swz_mode(RB0), SW1 = swz_mode(RB1);
+  constexpr int TAPS = KS * KS;
+  constexpr uint32_t TAPB = tap_bytes(CIN, COUT);
+  constexpr uint32_t HALFB = TAPB / 2;  // offset of the lo weights inside a tap image
+  constexpr uint32_t TMEM_COLS = tmem_cols(COUT);
+  constexpr uint32_t IDESC = idesc_e16_f32<F16>(128, COUT);
+
+  extern __shared__ uint8_t smem_dyn[];
+  uint8_t* smem = smem_align1024(smem_dyn);
+  const int S = L.stages, NS = L.nslots;
+  const bool resident = NS == TAPS;
+  const Lay lay = x3_layout(CIN, COUT, S, L.win_alloc, NS);
+  float* s_bias = reinterpret_cast<float*>(smem + lay.par_off);
+  float* s_s2 = s_bias + COUT;
+  float* s_t2 = s_s2 + COUT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.bar_off);
+  uint64_t* full = bars;          // [S] window landed
+  uint64_t* empty = full + S;     // [S] window consumed by the MMAs
+  uint64_t* wfull = empty + S;    // [NS] weight tap landed
+  uint64_t* wempty = wfull + NS;  // [NS] weight tap consumed (streamed mode)
+  uint64_t* tfull = wempty + NS;  // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;   // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int G = L.ngroups;
+  const int g = blockIdx.x % G;
+  const int local = blockIdx.x / G;
+  const int nct = (static_cast<int>(gridDim.x) - g + G - 1) / G;
+  const X3Group& grp = L.g[g];
+  const int64_t n_tiles = L.geo.n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int k = 0; k < NS; ++k) {
+      mbar_init(&wfull[k], 1);
+      mbar_init(&wempty[k], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp >= 3) {
+    for (int c = threadIdx.x - 96; c < COUT; c += 128) {
+      s_bias[c] = grp.bias[c];
+      s_s2[c] = grp.s2 ? grp.s2[c] : 1.f;
+      s_t2[c] = grp.t2 ? grp.t2[c] : 0.f;
+    }
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  pdl_trigger();
+
+  if (warp == 2) {
+    // ------------------------------ weight loader (weights are plan constants: no PDL wait) -----------
+    if (lane == 0) {
+      if (resident) {
+        for (int tap = 0; tap < TAPS; ++tap) {
+          mbar_arrive_expect_tx(&wfull[tap], TAPB);
+          bulk_load(smem + static_cast<uint32_t>(tap) * TAPB, grp.wimg + static_cast<size_t>(tap) * TAPB, TAPB,
+                    &wfull[tap]);
+        }
+      } else {
+        uint32_t wi = 0;
+        for (int64_t tile = local; tile < n_tiles; tile += nct)
+          for (int tap = 0; tap < TAPS; ++tap, ++wi) {
+            const uint32_t slot = wi % static_cast<uint32_t>(NS);
+            mbar_wait(&wempty[slot], ((wi / static_cast<uint32_t>(NS)) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(&wfull[slot], TAPB);
+            bulk_load(smem + slot * TAPB, grp.wimg + static_cast<size_t>(tap) * TAPB, TAPB, &wfull[slot]);
+          }
+      }
+    }
+  } else if (warp == 0) {
+    // ------------------------------ window producer ------------------------------
+    pdl_wait();
+    if (lane == 0) {
+      prefetch_tmap(&grp.map[0]);
+      prefetch_tmap(&grp.map[2]);
+      const int nboxes = (128 + 2 * grp.halo + kBoxRows - 1) / kBoxRows;
+      const uint32_t stage_tx = static_cast<uint32_t>(nboxes * kBoxRows * CIN * 2 * 2);
+      int j = 0;
+      for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
+        const int s = j % S;
+        mbar_wait(&empty[s], (static_cast<uint32_t>(j / S) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&full[s], stage_tx);
+        uint8_t* win = smem + lay.win_off + s * lay.stage_bytes;
+        const int32_t r0 = static_cast<int32_t>(tile * 128 - grp.halo);
+        for (int bx = 0; bx < nboxes; ++bx) {
+          const int32_t rr = r0 + bx * kBoxRows;
+          tma_load_2d(win + lay.sub[0] + bx * kBoxRows * RB0, &grp.map[0], &full[s], 0, rr);
+          tma_load_2d(win + lay.sub[2] + bx * kBoxRows * RB0, &grp.map[2], &full[s], 0, rr);
+          if (CH1) {
+            tma_load_2d(win + lay.sub[1] + bx * kBoxRows * RB1, &grp.map[1], &full[s], 0, rr);
+            tma_load_2d(win + lay.sub[3] + bx * kBoxRows * RB1, &grp.map[3], &full[s], 0, rr);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer --------------------------------
+    if (lane == 0) {
+      const uint32_t sW = smem_u32(smem);
+      const int32_t T1 = L.geo.T1;
+      uint32_t wi = 0;
+      int j = 0;
+      for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
+        const int s = j % S;
+        const int a = j & 1;
+        mbar_wait(&full[s], static_cast<uint32_t>(j / S) & 1u);
+        mbar_wait(&tempty[a], (static_cast<uint32_t>(j >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t win = smem_u32(smem + lay.win_off + s * lay.stage_bytes);
+        const uint32_t d_tmem = tbase + static_cast<uint32_t>(a * COUT);
+        uint32_t acc = 0;
+#pragma unroll 1
+        for (int tap = 0; tap < TAPS; ++tap) {
+          const uint32_t slot = resident ? static_cast<uint32_t>(tap) : wi % static_cast<uint32_t>(NS);
+          if (!resident || j == 0) {
+            mbar_wait(&wfull[slot], resident ? 0u : (wi / static_cast<uint32_t>(NS)) & 1u);
+            tc_fence_after();
+          }
+          const int dt = tap / KS - KS / 2, df = tap % KS - KS / 2;
+          const int row = grp.halo + dt + df * grp.dil * T1;
+          const uint32_t wb = sW + slot * TAPB;
+          {
+            const uint32_t ah = win + lay.sub[0] + static_cast<uint32_t>(row * RB0);
+            const uint32_t al = win + lay.sub[2] + static_cast<uint32_t>(row * RB0);
+#pragma unroll
+            for (int kk = 0; kk < CH0 / 16; ++kk) {
+              const uint64_t dah = make_sdesc(ah + kk * 32, 8 * RB0, SW0, 0);
+              const uint64_t dal = make_sdesc(al + kk * 32, 8 * RB0, SW0, 0);
+              const uint64_t dbh = make_sdesc(wb + kk * 32, 8 * RB0, SW0, 0);
+              const uint64_t dbl = make_sdesc(wb + HALFB + kk * 32, 8 * RB0, SW0, 0);
+              umma_f16(d_tmem, dah, dbh, IDESC, acc);
+              umma_f16(d_tmem, dah, dbl, IDESC, 1);
+              umma_f16(d_tmem, dal, dbh, IDESC, 1);
+              acc = 1;
+            }
+          }
+          if (CH1) {
+            const uint32_t ah = win + lay.sub[1] + static_cast<uint32_t>(row * RB1);
+            const uint32_t al = win + lay.sub[3] + static_cast<uint32_t>(row * RB1);
+            const uint32_t w1 = wb + static_cast<uint32_t>(COUT * RB0);
+#pragma unroll
+            for (int kk = 0; kk < CH1 / 16; ++kk) {
+              const uint64_t dah = make_sdesc(ah + kk * 32, 8 * RB1, SW1, 0);
+              const uint64_t dal = make_sdesc(al + kk * 32, 8 * RB1, SW1, 0);
+              const uint64_t dbh = make_sdesc(w1 + kk * 32, 8 * RB1, SW1, 0);
+              const uint64_t dbl = make_sdesc(w1 + HALFB + kk * 32, 8 * RB1, SW1, 0);
+              umma_f16(d_tmem, dah, dbh, IDESC, 1);
+              umma_f16(d_tmem, dah, dbl, IDESC, 1);
+              umma_f16(d_tmem, dal, dbh, IDESC, 1);
+            }
+          }
+          if (!resident) {
+            umma_commit(&wempty[slot]);  // tap slot free once these MMAs have read it
+            ++wi;
+          }
+        }
+        umma_commit(&empty[s]);   // window stage free
+        umma_commit(&tfull[a]);   // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ------------------------------ epilogue (warps 3..6) ---------------------
+    pdl_wait();
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // s_bias / s_s2 / s_t2 visible to all epilogue warps
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = q * 32 + lane;
+    const PlaneGeom geo = L.geo;
+    int j = 0;
+    for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
+      const int a = j & 1;
+      mbar_wait(&tfull[a], static_cast<uint32_t>(j >> 1) & 1u);
+      tc_fence_after();
+      const int64_t p = tile * 128 + row;
+      const bool valid = geo.valid(p);
+      const uint32_t taddr = tbase + static_cast<uint32_t>(a * COUT) + (static_cast<uint32_t>(q * 32) << 16);
+      const __nv_bfloat16* rrow = grp.res ? grp.res + p * (2 * COUT) : nullptr;
+      __nv_bfloat16* orow = grp.out ? grp.out + p * (2 * COUT) : nullptr;
+      __nv_bfloat16* orow2 = grp.out2 ? grp.out2 + p * (2 * COUT) : nullptr;
+#pragma unroll 1
+      for (int cc = 0; cc < COUT / 32; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(taddr + cc * 32, r);
+        tmem_ld_wait();
+        if (cc == COUT / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_relaxed(&tempty[a]);
+        }
+#pragma unroll
+        for (int hp = 0; hp < 2; ++hp) {
+          const int c0 = cc * 32 + hp * 16;
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[hp * 16 + i]) + s_bias[c0 + i];
+          if (rrow) {
+            const u32x8 rh = ldg256(rrow + c0);
+            const u32x8 rl = ldg256(rrow + COUT + c0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float2 h = unpack2<F16>(rh.v[i]), l = unpack2<F16>(rl.v[i]);
+              v[2 * i] += h.x + l.x;  // hi + lo is exact in fp32
+              v[2 * i + 1] += h.y + l.y;
+            }
+          }
+          if (grp.relu) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+          }
+          if (!valid) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          }
+          if (orow) {
+            u32x8 oh, ol;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) split2<F16>(v[2 * i], v[2 * i + 1], oh.v[i], ol.v[i]);
+            stg256(orow + c0, oh);
+            stg256(orow + COUT + c0, ol);
+          }
+          if (orow2) {
+            u32x8 oh, ol;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float x0 = fmaxf(v[2 * i] * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
+              const float x1 = fmaxf(v[2 * i + 1] * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
+              split2<F16>(valid ? x0 : 0.f, valid ? x1 : 0.f, oh.v[i], ol.v[i]);
+            }
+            stg256(orow2 + c0, oh);
+            stg256(orow2 + COUT + c0, ol);
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tbase, TMEM_COLS);
+}
+
+template <int CIN, int COUT, int KS, bool F16>
+const char* launch_t(const X3Launch& L, int num_sms, cudaStream_t stream) {
+  auto kern = conv_x3_kernel<CIN, COUT, KS, F16>;
+  const Lay lay = x3_layout(CIN, COUT, L.stages, L.win_alloc, L.nslots);
+  if (lay.total > kSmemLimit) throw Error(3, "conv_x3: working set exceeds shared memory");
+  ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(lay.total));
+  const int64_t work = static_cast<int64_t>(L.ngroups) * L.geo.n_tiles;
+  int grid = static_cast<int>(work < num_sms ? work : num_sms);
+  if (grid < L.ngroups) grid = L.ngroups;
+  launch_pdl(kern, dim3(grid), dim3(kThreads), lay.total, stream, L);
+  static char name[96];
+  snprintf(name, sizeof name, "conv_x3_kernel<%d,%d,%d,%s>", CIN, COUT, KS, F16 ? "f16x3" : "bf16x3");
+  return name;
+}
+
+using LaunchFn = const char* (*)(const X3Launch&, int, cudaStream_t);
+
+#define CNRX_X3_CASES(X)                                                                                     \
+  X(16, 32, 1) X(16, 32, 3) X(32, 32, 1) X(32, 32, 3) X(16, 64, 1) X(32, 64, 1) X(64, 64, 1) X(64, 64, 3)   \
+  X(16, 96, 1) X(32, 96, 1) X(64, 96, 1) X(96, 96, 1) X(96, 96, 3) X(32, 64, 3) X(64, 32, 3) X(32, 96, 3)     \
+  X(16, 64, 3) X(16, 96, 3)
+
+LaunchFn find_launch(int cin, int cout, int ks, bool h) {
+#define X(a, b, c) \
+  if (cin == a && cout == b && ks == c) return h ? &launch_t<a, b, c, true> : &launch_t<a, b, c, false>;
+  CNRX_X3_CASES(X)
+#undef X
+  return nullptr;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    CNRX_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p) throw Error(4, "cuTensorMapEncodeTiled not available");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+bool conv_x3_supported(int cin, int cout, int ks) { return find_launch(cin, cout, ks, false) != nullptr; }
+
+size_t conv_x3_wimg_bytes(int cin, int cout, int ks) { return static_cast<size_t>(ks) * ks * tap_bytes(cin, cout); }
+
+size_t conv_x3_smem_bytes(int cin, int cout, int ks, int stages, int win_alloc, int nslots) {
+  (void)ks;
+  return x3_layout(cin, cout, stages, win_alloc, nslots).total;
+}
+
+bool conv_x3_config(int cin, int cout, int ks, int win_alloc, int* stages, int* nslots) {
+  const int taps = ks * ks;
+  // resident weights with a double-buffered window, else a weight-tap ring (deeper first)
+  const int tries[][2] = {{taps, 3}, {taps, 2}, {4, 2}, {3, 2}, {2, 2}, {2, 1}};
+  for (const auto& t : tries) {
+    if (t[0] > taps) continue;
+    if (x3_layout(cin, cout, t[1], win_alloc, t[0]).total <= kSmemLimit) {
+      *nslots = t[0];
+      *stages = t[1];
+      return true;
+    }
+  }
+  return false;
+}
+
+void conv_x3_pack_weights(const float* w, int ks, int cin_real, int cout_real, const float* scale, int cin, int cout,
+                          bool fp16, uint8_t* img) {
+  const int ch0 = ch0_of(cin);
+  const int rb0 = ch0 * 2, rb1 = ch1_of(cin) * 2;
+  const size_t half = static_cast<size_t>(cout) * cin * 2;
+  std::memset(img, 0, conv_x3_wimg_bytes(cin, cout, ks));
+  for (int tap = 0; tap < ks * ks; ++tap) {
+    uint8_t* tb = img + static_cast<size_t>(tap) * 2 * half;
+    for (int co = 0; co < cout; ++co)
+      for (int ci = 0; ci < cin; ++ci) {
+        float v = 0.f;
+        if (co < cout_real && ci < cin_real) {
+          v = w[(static_cast<size_t>(tap) * cin_real + ci) * cout_real + co];  // [kh,kw,Cin,Cout], kernels.hpp:32
+          if (scale) v *= scale[co];
+        }
+        const uint16_t hi = e16_from_float_host(v, fp16);
+        const uint16_t lo = e16_from_float_host(v - e16_to_float_host(hi, fp16), fp16);
+        uint8_t* base = tb;
+        int rb = rb0, k = ci;
+        if (ci >= ch0) {
+          base = tb + static_cast<size_t>(cout) * rb0;
+          rb = rb1;
+          k = ci - ch0;
+        }
+        const uint32_t off = swz_off(rb, static_cast<uint32_t>(co), static_cast<uint32_t>(k / 8)) + (k % 8) * 2;
+        std::memcpy(base + off, &hi, 2);
+        std::memcpy(base + half + off, &lo, 2);
+      }
+  }
+}
+
+void conv_x3_make_maps(const void* plane, int64_t nalloc, int cin, CUtensorMap* maps) {
+  const int chs[2] = {ch0_of(cin), ch1_of(cin)};
+  for (int part = 0; part < 2; ++part)      // hi, lo
+    for (int c = 0; c < 2; ++c) {           // K-chunk
+      CUtensorMap* m = &maps[part * 2 + c];
+      if (chs[c] == 0 || !plane) {
+        std::memset(m, 0, sizeof(CUtensorMap));
+        continue;
+      }
+      const int rb = chs[c] * 2;
+      const CUtensorMapSwizzle sw = rb == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                    : rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                    : rb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                               : CU_TENSOR_MAP_SWIZZLE_NONE;
+      cuuint64_t dims[2] = {static_cast<cuuint64_t>(chs[c]), static_cast<cuuint64_t>(nalloc)};
+      cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * cin) * 2};
+      cuuint32_t box[2] = {static_cast<cuuint32_t>(chs[c]), static_cast<cuuint32_t>(kBoxRows)};
+      cuuint32_t es[2] = {1, 1};
+      void* base = const_cast<uint8_t*>(static_cast<const uint8_t*>(plane)) + (part * cin + (c == 0 ? 0 : chs[0])) * 2;
+      CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    }
+}
+
+const char* conv_x3_launch(int cin, int cout, int ks, const X3Launch& L, int num_sms, cudaStream_t stream) {
+  LaunchFn fn = find_launch(cin, cout, ks, L.fp16 != 0);
+  if (!fn) throw Error(3, "no split-precision conv instantiation for cin=" + std::to_string(cin) + " cout=" +
+                              std::to_string(cout) + " k=" + std::to_string(ks));
+  return fn(L, num_sms, stream);
+}
+
+}  // namespace cnrx

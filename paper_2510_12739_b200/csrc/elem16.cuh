@@ -82,5 +82,16 @@ inline uint16_t e16_from_float_host(float v, bool h) {
   }
   return bits;
 }
+inline float e16_to_float_host(uint16_t bits, bool h) {
+  if (h) {
+    __half x;
+    std::memcpy(&x, &bits, 2);
+    return __half2float(x);
+  }
+  const uint32_t u = static_cast<uint32_t>(bits) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
 
 }  // namespace cnrx

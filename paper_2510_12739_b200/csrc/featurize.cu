@@ -157,10 +157,11 @@ __global__ void featurize_kernel(const float2* __restrict__ y, PlaneGeom geo, in
 // Reference-layout fp32 features [B,T,F,C] -> bf16 / fp16 plane [Nalloc][cpad] (used by cnrx_forward
 // when the caller supplies features rather than the received grid).
 __global__ void pack_plane_kernel(const float* __restrict__ x, PlaneGeom geo, int C, __nv_bfloat16* __restrict__ plane,
-                                  int cpad, bool h16) {
+                                  int cpad, bool h16, bool split) {
   const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (row >= geo.Nalloc) return;
-  __nv_bfloat16* dst = plane + row * cpad;
+  // split planes (CNRX_*X3 plans): row = [hi cpad | lo cpad], hi = round16(v), lo = round16(v - hi)
+  __nv_bfloat16* dst = plane + row * (split ? 2 * cpad : cpad);
   const bool valid = geo.valid(row);
   const float* src = nullptr;
   if (valid) {
@@ -169,15 +170,19 @@ __global__ void pack_plane_kernel(const float* __restrict__ x, PlaneGeom geo, in
     src = x + ((static_cast<int64_t>(b) * geo.T + t) * geo.F + f) * C;
   }
   for (int i0 = 0; i0 < cpad; i0 += 8) {
-    uint4 o;
+    uint4 o, ol;
     uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+    uint32_t* opl = reinterpret_cast<uint32_t*>(&ol);
     for (int i = 0; i < 4; ++i) {
       const int k = i0 + 2 * i;
       const float a = (valid && k < C) ? src[k] : 0.f;
       const float c = (valid && k + 1 < C) ? src[k + 1] : 0.f;
       op[i] = pack2r(h16, a, c);
+      const float2 hf = unpack2r(h16, op[i]);
+      opl[i] = pack2r(h16, a - hf.x, c - hf.y);
     }
     *reinterpret_cast<uint4*>(dst + i0) = o;
+    if (split) *reinterpret_cast<uint4*>(dst + cpad + i0) = ol;
   }
 }
 
@@ -466,11 +471,12 @@ const char* launch_plane_rows_to_ref(const __nv_bfloat16* plane, const PlaneGeom
 }
 
 const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_bfloat16* plane, int cpad, bool fp16,
-                              cudaStream_t s) {
+                              cudaStream_t s, bool split) {
   const int threads = 256;
   pack_plane_kernel<<<static_cast<unsigned>((geo.Nalloc + threads - 1) / threads), threads, 0, s>>>(x, geo, C, plane,
-                                                                                                   cpad, fp16);
+                                                                                                   cpad, fp16, split);
   CNRX_CUDA(cudaGetLastError());
+  if (split) return "pack_plane_kernel<x3>";
   return "pack_plane_kernel";
 }
 

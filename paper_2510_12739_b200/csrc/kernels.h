@@ -39,8 +39,9 @@ const char* launch_featurize_ref(const float* y, const PlaneGeom& geo, int N, co
 // Test hook: the valid rows of a 16-bit plane [Nalloc][cpad] in reference order [B,T,F,cpad].
 const char* launch_plane_rows_to_ref(const __nv_bfloat16* plane, const PlaneGeom& geo, int cpad, uint16_t* out,
                                      cudaStream_t s);
+// split: write a split plane [Nalloc][2*cpad] (hi | lo halves, CNRX_*X3 plans)
 const char* launch_pack_plane(const float* x, const PlaneGeom& geo, int C, __nv_bfloat16* plane, int cpad, bool fp16,
-                              cudaStream_t s);
+                              cudaStream_t s, bool split = false);
 
 // ---------------------------------------------------------------------------------------------
 // Fused input stage: network input features (computed from the received grid, or read from the
@@ -94,6 +95,7 @@ struct PwProgram {
   int32_t n_planes_used;    // planes[0 .. n_planes_used) are operands
   int32_t fp16;             // operand / output planes are fp16 (else bf16)
   int32_t tc_head;          // 64-channel heads may run their GEMV on the tensor core (bf16-rounded z)
+  int32_t split;            // split planes (CNRX_*X3 plans): a row is [hi C | lo C], value = hi + lo
   PwIns ins[kPwMaxIns];
   const __nv_bfloat16* planes[kPwMaxPlanes];
   const float* aff_s[kPwMaxAff];

@@ -30,10 +30,26 @@ __device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&v)[8], boo
   }
 }
 
+// 8 values -> (hi, lo) 16-bit halves of a split-plane row (hi at p, lo at p + C)
+__device__ __forceinline__ void store8_split(__nv_bfloat16* p, int C, const float (&v)[8], bool h16) {
+  uint4 oh, ol;
+  uint32_t* ph = reinterpret_cast<uint32_t*>(&oh);
+  uint32_t* pl = reinterpret_cast<uint32_t*>(&ol);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    ph[i] = pack2r(h16, v[2 * i], v[2 * i + 1]);
+    const float2 f = unpack2r(h16, ph[i]);
+    pl[i] = pack2r(h16, v[2 * i] - f.x, v[2 * i + 1] - f.y);
+  }
+  *reinterpret_cast<uint4*>(p) = oh;
+  *reinterpret_cast<uint4*>(p + C) = ol;
+}
+
 template <int HEAD>
 __global__ void __launch_bounds__(256) pw_program_kernel(const __grid_constant__ PwProgram prog, PlaneGeom geo) {
   extern __shared__ float s_head[];  // [C][bits] + [bits]
   const int C = prog.C, NB = prog.head_bits;
+  const bool split = prog.split != 0;
   if (HEAD) {
     for (int i = threadIdx.x; i < C * NB; i += blockDim.x) s_head[i] = prog.head_w[i];
     for (int i = threadIdx.x; i < NB; i += blockDim.x) s_head[C * NB + i] = prog.head_b[i];
@@ -57,7 +73,15 @@ __global__ void __launch_bounds__(256) pw_program_kernel(const __grid_constant__
         const PwIns ins = prog.ins[n];
         if (ins.op == PW_LOAD || ins.op == PW_MUL || ins.op == PW_ADD) {
           float v[8];
-          load8(prog.planes[ins.k] + row * C + c0, v, prog.fp16 != 0);
+          if (split) {
+            float l[8];
+            load8(prog.planes[ins.k] + row * 2 * C + c0, v, prog.fp16 != 0);
+            load8(prog.planes[ins.k] + row * 2 * C + C + c0, l, prog.fp16 != 0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] += l[i];  // hi + lo: exact in fp32
+          } else {
+            load8(prog.planes[ins.k] + row * C + c0, v, prog.fp16 != 0);
+          }
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             acc[i] = ins.op == PW_LOAD ? v[i] : ins.op == PW_MUL ? acc[i] * v[i] : acc[i] + v[i];
@@ -80,12 +104,24 @@ __global__ void __launch_bounds__(256) pw_program_kernel(const __grid_constant__
         for (int j = 0; j < kPwMaxBits; ++j)
           if (j < NB) out[j] += acc[i] * wr[j];
       }
+    } else if (split) {
+      store8_split(prog.out_plane + row * 2 * C + c0, C, acc, prog.fp16 != 0);
+      if (prog.out2_plane) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaxf(acc[i], 0.f);
+        store8_split(prog.out2_plane + row * 2 * C + c0, C, acc, prog.fp16 != 0);
+      }
     } else {
       uint4 o;
       uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
       for (int i = 0; i < 4; ++i) op[i] = pack2r(prog.fp16 != 0, acc[2 * i], acc[2 * i + 1]);
       *reinterpret_cast<uint4*>(prog.out_plane + row * C + c0) = o;
+      if (prog.out2_plane) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) op[i] = relu2r(prog.fp16 != 0, op[i]);  // relu commutes with the rounding
+        *reinterpret_cast<uint4*>(prog.out2_plane + row * C + c0) = o;
+      }
     }
   }
   if (HEAD) {
@@ -541,6 +577,18 @@ const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaS
   if (prog.head_bits > 0) require(prog.head_bits <= kPwMaxBits, "head with more than 16 outputs");
   require(prog.out2_plane == nullptr || prog.head_bits == 0, "second output needs a plane program");
   const bool head = prog.head_bits > 0;
+  if (prog.split) {  // split planes: the generic interpreter (one thread per row) reads / writes hi + lo
+    const int threads = 256;
+    const unsigned blocks = static_cast<unsigned>((geo.Nalloc + threads - 1) / threads);
+    if (head) {
+      const size_t smem = sizeof(float) * (static_cast<size_t>(prog.C) * prog.head_bits + prog.head_bits);
+      pw_program_kernel<1><<<blocks, threads, smem, s>>>(prog, geo);
+    } else {
+      pw_program_kernel<0><<<blocks, threads, 0, s>>>(prog, geo);
+    }
+    CNRX_CUDA(cudaGetLastError());
+    return head ? "pw_program_kernel<head,x3>" : "pw_program_kernel<plane,x3>";
+  }
   {
     FoldSteps fs{};
     int ns = 0;

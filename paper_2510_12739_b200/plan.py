@@ -22,8 +22,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CNRX_LIB") or os.path.join(HERE, "libconetrx_cuda.so")  # CNRX_LIB: A/B builds only
 
 OK, ERR_INVALID_ARGUMENT, ERR_NOT_READY, ERR_UNSUPPORTED, ERR_CUDA = range(5)
-FP32, BF16, FP16 = 0, 1, 2
-PRECISIONS = {"fp32": FP32, "bf16": BF16, "fp16": FP16}
+FP32, BF16, FP16, BF16X3, FP16X3 = 0, 1, 2, 3, 4
+# bf16x3 / fp16x3: split-precision tensor-core plans (fp32-grade LLRs, conv_x3.cu)
+PRECISIONS = {"fp32": FP32, "bf16": BF16, "fp16": FP16, "bf16x3": BF16X3, "fp16x3": FP16X3}
 MODE_TRAIN, MODE_EVAL = 0, 1
 
 

@@ -48,6 +48,12 @@ def fp16x2(t: torch.Tensor) -> torch.Tensor:
     return hi + fp16(t - hi)
 
 
+def bf16x2(t: torch.Tensor) -> torch.Tensor:
+    """A value carried as a bf16 (hi, lo) pair: hi = bf16(t), lo = bf16(t - hi)."""
+    hi = bf16(t)
+    return hi + bf16(t - hi)
+
+
 # Rounding points of the bf16 plan, by role (tools/ablate_bf16.py switches them one at a time):
 #   feat  - the input feature plane (the stems' tensor-core operand)
 #   w     - BN-folded conv weights (tensor-core operands)

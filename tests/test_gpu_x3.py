@@ -1,0 +1,129 @@
+"""Split-precision tensor-core plans (CNRX_BF16X3 / CNRX_FP16X3, csrc/conv_x3.cu): the north star's fp32
+path bar — LLRs within 1e-4 relative of the reference's fp32 forward — on the tensor cores.
+
+Tolerance (stated here, normwise over the LLR tensor, against the reference / oracle fp32 forward on the
+same seeded inputs and weights):
+  * bf16x3: relative L2 <= 1e-4 and max |gpu - ref| <= 1e-4 * max |ref|
+    (carrying values as bf16 (hi, lo) pairs keeps 16 significant bits; the emulation of these rounding
+    points gives 2e-5 / 4e-5 on the trained cfg2 checkpoint);
+  * fp16x3: 1e-5 / 1e-5 (22 significant bits: 1.3e-6 / 3.9e-6 in the emulation).
+Hard decisions on the trained checkpoints: >= 99.99 % of ALL data bits identical to the fp32 plan
+(bit-exact with the reference) — on cfg2 AND cfg3, where the 16-bit plans stop at 99.94 / 99.98 %.
+"""
+import dataclasses
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2510_12739_b200 import graph as G, plan as P, slots
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL = {"bf16x3": 1e-4, "fp16x3": 1e-5}
+
+
+def assert_x3(gpu, ref, prec):
+    tol = TOL[prec]
+    l2 = np.linalg.norm(gpu - ref) / np.linalg.norm(ref)
+    mx = np.abs(gpu - ref).max() / np.abs(ref).max()
+    assert l2 <= tol and mx <= tol, (prec, l2, mx)
+    return l2, mx
+
+
+def _tiny(kind, c=64, dil=1, cin=12, F=40, B=2):
+    g = G.Graph()
+    x = g.add_input(cin)
+    if kind == "1x1":
+        h = g.add_relu(g.add_conv(x, "a", 1, cin, c, True))
+    elif kind == "3x3":
+        s = g.add_relu(g.add_conv(x, "s", 1, cin, c, True))
+        h = g.add_relu(g.add_conv(s, "a", 3, c, c, True, dilation_f=dil))
+    else:  # pre-activation residual block with BN folded into c1
+        s = g.add_relu(g.add_conv(x, "s", 1, cin, c, True))
+        h1 = g.add_relu(g.add_norm(g.add_conv(s, "a", 3, c, c, False, dilation_f=dil), "bn", "n", c))
+        h = g.add_binary(G.OP_ADD, g.add_conv(h1, "b", 3, c, c, True, dilation_f=dil), s)
+    g.set_output(g.add_conv(h, "out", 1, c, 4, True))
+    g.init_he_normal(3, randomize_aux=True)
+    xin = np.random.default_rng(1).standard_normal((B, 14, F, cin)).astype(np.float32)
+    return g, xin
+
+
+@pytest.mark.parametrize("prec", ["bf16x3", "fp16x3"])
+@pytest.mark.parametrize("kind,c,dil", [("1x1", 64, 1), ("3x3", 64, 1), ("res", 64, 1), ("3x3", 64, 2),
+                                        ("res", 96, 2), ("3x3", 96, 1), ("3x3", 32, 1)])
+def test_x3_layers(kind, c, dil, prec):
+    g, x = _tiny(kind, c, dil)
+    p = P.Plan(g, prec)
+    got = p.forward(x)
+    assert_x3(got, oracle.forward(g, x), prec)
+    names = p.launch_names()
+    assert all("conv_x3_kernel" in n for n in names if "conv" in n), names
+
+
+@pytest.mark.parametrize("prec", ["bf16x3", "fp16x3"])
+@pytest.mark.parametrize("name,wseed", [("cfg1", 11), ("cfg2", 12), ("cfg4", 13)])
+def test_x3_matches_reference_golden(name, wseed, prec):
+    """Against the reference's own outputs (tests/golden/forward.npz, made by oracle/_ref)."""
+    d = np.load(os.path.join(GOLD, "forward.npz"))
+    g = G.CONFIGS[name].graph(seed=wseed)
+    got = P.Plan(g, prec).forward(d[f"{name}_x"])
+    assert_x3(got, d[f"{name}_llr"], prec)
+
+
+@pytest.mark.parametrize("prec", ["bf16x3", "fp16x3"])
+@pytest.mark.parametrize("name,B,F", [("cfg1", 3, 72), ("cfg2", 2, 37), ("cfg2", 1, 612), ("cfg4", 2, 29),
+                                      ("cfg4m", 1, 33), ("cfg3", 1, 40), ("cfg2", 5, 5), ("cfg1", 39, 71),
+                                      ("cfg1", 64, 72)])
+def test_x3_vs_oracle(name, B, F, prec):
+    g = G.CONFIGS[name].graph(seed=7)
+    x = np.random.default_rng(B * F + 3).standard_normal((B, 14, F, g.in_channels)).astype(np.float32)
+    assert_x3(P.Plan(g, prec).forward(x), oracle.forward(g, x), prec)
+
+
+@pytest.mark.parametrize("prec", ["bf16x3", "fp16x3"])
+def test_x3_receive_path(prec):
+    """featurize (GPU, fp32) -> split input plane -> network -> LLRs, against the oracle featurizer +
+    reference forward; and the same LLRs through receive() (host buffers) and receive_device()."""
+    link = dataclasses.replace(G.CONFIGS["cfg2"].link, F=48)
+    b = slots.generate(link, 3, 9)
+    g = G.CONFIGS["cfg2"].graph(seed=4)
+    p = P.Plan(g, prec)
+    p.set_pilots(b.pilots, b.pilot_mask)
+    got = p.receive(b.y)
+    ref = oracle.forward(g, oracle.featurize(b.y, b.pilots, b.pilot_mask))
+    assert_x3(got, ref, prec)
+    names = p.launch_names()
+    assert "featurize_kernel<ref>" in names and "pack_plane_kernel<x3>" in names, names
+
+
+def test_x3_full_grid_cfg3():
+    """cfg3 at its stated grid (F = 3276, N = 4, dilation 2, 96-ch streamed-weight convs), B = 1: the
+    bf16x3 plan against the oracle on three crops with the receptive-radius margin."""
+    g = G.CONFIGS["cfg3"].graph(seed=5)
+    b = slots.generate(G.CONFIGS["cfg3"].link, 1, 5)
+    feat = oracle.featurize(b.y, b.pilots, b.pilot_mask)
+    got = P.Plan(g, "bf16x3").forward(feat)
+    R = 25
+    for a, e in ((0, 96), (1600, 1696), (3180, 3276)):
+        lo, hi = max(0, a - R), min(3276, e + R)
+        ref = oracle.forward(g, np.ascontiguousarray(feat[:, :, lo:hi]))
+        assert_x3(got[:, :, a:e], ref[:, :, a - lo:e - lo], "bf16x3")
+
+
+def test_x3_batch_invariance_and_capture():
+    """A slot's LLRs do not depend on the batch it runs in, and graph replay gives the same bits."""
+    g = G.CONFIGS["cfg2"].graph(seed=2)
+    x = np.random.default_rng(0).standard_normal((5, 14, 40, 12)).astype(np.float32)
+    p = P.Plan(g, "bf16x3")
+    full = p.forward(x)
+    assert np.array_equal(p.forward(x[2:3]), full[2:3])
+    p.set_graph_capture(True)
+    assert np.array_equal(p.forward(x), full)
+    assert np.array_equal(p.forward(x), full)
+
+
+def test_x3_options_are_fixed():
+    o = P.Plan(G.CONFIGS["cfg2"].graph(), "bf16x3").options()
+    assert o["fused_blocks"] == 0 and o["weights_stationary"] == 0 and o["cta_pair"] == 0 and o["fused_head"] == 0

@@ -56,6 +56,11 @@ variants = {
     "fp16, fp32 feat+res": dict(E.FP16_POLICY, feat=ident, res=ident),
     "fp16, fp32 feat+res+leaf": dict(E.FP16_POLICY, feat=ident, res=ident, leaf=ident),
     "fp16x2 split operands (3-pass)": dict(feat=E.fp16x2, w=E.fp16x2, act=E.fp16x2, res=E.fp16x2, leaf=E.fp16x2, z=ident),
+    "bf16x2 split operands (3-pass)": dict(feat=E.bf16x2, w=E.bf16x2, act=E.bf16x2, res=E.bf16x2, leaf=E.bf16x2, z=ident),
+    "bf16x2 split operands, fp32 planes": dict(feat=ident, w=E.bf16x2, act=E.bf16x2, res=ident, leaf=ident, z=ident),
+    "fp16 act, fp16x2 w (2-pass), fp32 planes": dict(feat=E.fp16, w=E.fp16x2, act=E.fp16, res=ident, leaf=ident, z=ident),
+    "fp16x2 act, fp16 w (2-pass), fp32 planes": dict(feat=E.fp16x2, w=E.fp16, act=E.fp16x2, res=ident, leaf=ident, z=ident),
+    "fp16 act+w, fp32 planes": dict(feat=E.fp16, w=E.fp16, act=E.fp16, res=ident, leaf=ident, z=ident),
 }
 only = os.environ.get("ABL_ONLY")
 chunks = []
