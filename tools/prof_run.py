@@ -6,7 +6,8 @@ from paper_2510_12739_b200 import graph as G, plan as P, slots
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 cfg = G.CONFIGS[name]; g = cfg.graph(); B = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.batch
 b = slots.generate(cfg.link, B, 1)
-p = P.Plan(g, cfg.precision if hasattr(cfg, "precision") else "bf16"); p.set_pilots(b.pilots, b.pilot_mask)
+prec = os.environ.get("PREC") or (cfg.precision if hasattr(cfg, "precision") else "bf16")
+p = P.Plan(g, prec); p.set_pilots(b.pilots, b.pilot_mask)
 y = torch.from_numpy(b.y).cuda(); out = torch.empty((B, cfg.link.T, cfg.link.F, p.out_channels), device="cuda")
 for _ in range(3):
     p.receive_device(y, out, 0)
