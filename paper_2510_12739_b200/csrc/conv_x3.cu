@@ -7,15 +7,19 @@
 // (network.hpp:455-457) as a second output — for CNRX_BF16X3 / CNRX_FP16X3 plans (conv_x3.h).
 //
 // Every value v is carried as hi = round16(v), lo = round16(v - hi); weights likewise.  Per K-step
-// of 16 channels the MMA warp issues three UMMAs into the same fp32 TMEM accumulator:
-//     D += A_hi * W_hi;   D += A_hi * W_lo;   D += A_lo * W_hi
-// (M = 128 plane rows, N = Cout, K = 16), so a conv costs 3x the 16-bit plan's tensor work and
-// moves the same bytes as an fp32 plane.  The plane layout makes every 3x3 tap a constant row shift
-// (common.h), so a tile's whole K loop reads ONE TMA-loaded window of 128 + 2*halo rows of hi and lo.
+// of 16 channels the MMA warp issues two UMMAs (M = 128 plane rows, K = 16):
+//     [D | E] += A_hi * [W_hi | W_lo]      (N = 2*Cout: the tap image stacks W_hi and W_lo rows)
+//      D      += A_lo * W_hi               (N = Cout)
+// and the epilogue adds D + E: the three products hi*Whi + lo*Whi + hi*Wlo, 3x the 16-bit plan's
+// tensor work, with the fp32 plane's bytes.  SS UMMAs at N = Cout read more shared memory per cycle
+// than the SM delivers (A 4 KB + B 2 KB per 32-cycle 128x64x16), so stacking the hi / lo weights along
+// N (one A read for two products) cuts the operand traffic per K-step from 18 KB to 14 KB (64 ch).
+// The plane layout makes every 3x3 tap a constant row shift (common.h), so a tile's whole K loop reads
+// ONE TMA-loaded window of 128 + 2*halo rows of hi and lo.
 //
 // Warp roles (224 threads, persistent, 1 CTA/SM):
 //   warp 0     TMA producer: one hi+lo window per tile into a `stages`-deep ring
-//   warp 1     TMEM allocator + single-thread MMA issuer (taps x K/16 x 3 UMMAs per tile)
+//   warp 1     TMEM allocator + single-thread MMA issuer (taps x K/16 x 2 UMMAs per tile)
 //   warp 2     weight loader: every tap once (resident: 64-channel convs, 147 KB) or, when the split
 //              weights exceed shared memory (96 channels: 331 KB), the taps of every tile through a
 //              ring of `nslots` tap slots (plain bulk copies of the pre-swizzled tap images, L2-resident)
@@ -53,11 +57,14 @@ __host__ __device__ inline uint32_t swz_off(int rb, uint32_t r, uint32_t c) {
   return r * static_cast<uint32_t>(rb) + (c << 4);
 }
 __host__ __device__ constexpr uint32_t a1024(uint32_t x) { return (x + 1023u) & ~1023u; }
-// one tap of the split weight image: [hi | lo], each COUT x CIN 16-bit values
+// one tap of the split weight image: per K-chunk [W_hi rows | W_lo rows], COUT x chunk 16-bit values each
 __host__ __device__ constexpr uint32_t tap_bytes(int cin, int cout) {
   return 2u * static_cast<uint32_t>(cout) * static_cast<uint32_t>(cin) * 2u;
 }
-__host__ __device__ constexpr uint32_t tmem_cols(int cout) { return 2 * cout <= 64 ? 64 : 2 * cout <= 128 ? 128 : 256; }
+// two accumulator stages of [D | E] = 2 * Cout columns each
+__host__ __device__ constexpr uint32_t tmem_cols(int cout) {
+  return 4 * cout <= 128 ? 128 : 4 * cout <= 256 ? 256 : 512;
+}
 
 struct Lay {
   uint32_t win_off, stage_bytes, sub[4], par_off, bar_off, total;
@@ -95,9 +102,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
   constexpr uint32_t SW0 = swz_mode(RB0), SW1 = swz_mode(RB1);
   constexpr int TAPS = KS * KS;
   constexpr uint32_t TAPB = tap_bytes(CIN, COUT);
-  constexpr uint32_t HALFB = TAPB / 2;  // offset of the lo weights inside a tap image
   constexpr uint32_t TMEM_COLS = tmem_cols(COUT);
-  constexpr uint32_t IDESC = idesc_e16_f32<F16>(128, COUT);
+  constexpr uint32_t IDESC1 = idesc_e16_f32<F16>(128, COUT);      // A_lo * W_hi
+  constexpr uint32_t IDESC2 = idesc_e16_f32<F16>(128, 2 * COUT);  // A_hi * [W_hi | W_lo]
 
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
@@ -214,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
         mbar_wait(&tempty[a], (static_cast<uint32_t>(j >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t win = smem_u32(smem + lay.win_off + s * lay.stage_bytes);
-        const uint32_t d_tmem = tbase + static_cast<uint32_t>(a * COUT);
+        const uint32_t d_tmem = tbase + static_cast<uint32_t>(a * 2 * COUT);
         uint32_t acc = 0;
 #pragma unroll 1
         for (int tap = 0; tap < TAPS; ++tap) {
@@ -233,27 +240,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
             for (int kk = 0; kk < CH0 / 16; ++kk) {
               const uint64_t dah = make_sdesc(ah + kk * 32, 8 * RB0, SW0, 0);
               const uint64_t dal = make_sdesc(al + kk * 32, 8 * RB0, SW0, 0);
-              const uint64_t dbh = make_sdesc(wb + kk * 32, 8 * RB0, SW0, 0);
-              const uint64_t dbl = make_sdesc(wb + HALFB + kk * 32, 8 * RB0, SW0, 0);
-              umma_f16(d_tmem, dah, dbh, IDESC, acc);
-              umma_f16(d_tmem, dah, dbl, IDESC, 1);
-              umma_f16(d_tmem, dal, dbh, IDESC, 1);
+              const uint64_t db = make_sdesc(wb + kk * 32, 8 * RB0, SW0, 0);
+              umma_f16(d_tmem, dah, db, IDESC2, acc);
+              umma_f16(d_tmem, dal, db, IDESC1, 1);
               acc = 1;
             }
           }
           if (CH1) {
             const uint32_t ah = win + lay.sub[1] + static_cast<uint32_t>(row * RB1);
             const uint32_t al = win + lay.sub[3] + static_cast<uint32_t>(row * RB1);
-            const uint32_t w1 = wb + static_cast<uint32_t>(COUT * RB0);
+            const uint32_t w1 = wb + static_cast<uint32_t>(2 * COUT * RB0);
 #pragma unroll
             for (int kk = 0; kk < CH1 / 16; ++kk) {
               const uint64_t dah = make_sdesc(ah + kk * 32, 8 * RB1, SW1, 0);
               const uint64_t dal = make_sdesc(al + kk * 32, 8 * RB1, SW1, 0);
-              const uint64_t dbh = make_sdesc(w1 + kk * 32, 8 * RB1, SW1, 0);
-              const uint64_t dbl = make_sdesc(w1 + HALFB + kk * 32, 8 * RB1, SW1, 0);
-              umma_f16(d_tmem, dah, dbh, IDESC, 1);
-              umma_f16(d_tmem, dah, dbl, IDESC, 1);
-              umma_f16(d_tmem, dal, dbh, IDESC, 1);
+              const uint64_t db = make_sdesc(w1 + kk * 32, 8 * RB1, SW1, 0);
+              umma_f16(d_tmem, dah, db, IDESC2, 1);
+              umma_f16(d_tmem, dal, db, IDESC1, 1);
             }
           }
           if (!resident) {
@@ -279,14 +282,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
       tc_fence_after();
       const int64_t p = tile * 128 + row;
       const bool valid = geo.valid(p);
-      const uint32_t taddr = tbase + static_cast<uint32_t>(a * COUT) + (static_cast<uint32_t>(q * 32) << 16);
+      const uint32_t taddr = tbase + static_cast<uint32_t>(a * 2 * COUT) + (static_cast<uint32_t>(q * 32) << 16);
       const __nv_bfloat16* rrow = grp.res ? grp.res + p * (2 * COUT) : nullptr;
       __nv_bfloat16* orow = grp.out ? grp.out + p * (2 * COUT) : nullptr;
       __nv_bfloat16* orow2 = grp.out2 ? grp.out2 + p * (2 * COUT) : nullptr;
 #pragma unroll 1
       for (int cc = 0; cc < COUT / 32; ++cc) {
-        uint32_t r[32];
-        tmem_ld32(taddr + cc * 32, r);
+        uint32_t r[32], e[32];
+        tmem_ld32(taddr + cc * 32, r);          // D: hi*Whi + lo*Whi
+        tmem_ld32(taddr + COUT + cc * 32, e);   // E: hi*Wlo
         tmem_ld_wait();
         if (cc == COUT / 32 - 1) {
           tc_fence_before();
@@ -298,7 +302,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
           const int c0 = cc * 32 + hp * 16;
           float v[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[hp * 16 + i]) + s_bias[c0 + i];
+          for (int i = 0; i < 16; ++i)
+            v[i] = (__uint_as_float(r[hp * 16 + i]) + __uint_as_float(e[hp * 16 + i])) + s_bias[c0 + i];
           if (rrow) {
             const u32x8 rh = ldg256(rrow + c0);
             const u32x8 rl = ldg256(rrow + COUT + c0);
@@ -418,10 +423,9 @@ void conv_x3_pack_weights(const float* w, int ks, int cin_real, int cout_real, c
                           bool fp16, uint8_t* img) {
   const int ch0 = ch0_of(cin);
   const int rb0 = ch0 * 2, rb1 = ch1_of(cin) * 2;
-  const size_t half = static_cast<size_t>(cout) * cin * 2;
   std::memset(img, 0, conv_x3_wimg_bytes(cin, cout, ks));
   for (int tap = 0; tap < ks * ks; ++tap) {
-    uint8_t* tb = img + static_cast<size_t>(tap) * 2 * half;
+    uint8_t* tb = img + static_cast<size_t>(tap) * tap_bytes(cin, cout);
     for (int co = 0; co < cout; ++co)
       for (int ci = 0; ci < cin; ++ci) {
         float v = 0.f;
@@ -431,16 +435,17 @@ void conv_x3_pack_weights(const float* w, int ks, int cin_real, int cout_real, c
         }
         const uint16_t hi = e16_from_float_host(v, fp16);
         const uint16_t lo = e16_from_float_host(v - e16_to_float_host(hi, fp16), fp16);
+        // chunk c: 2*COUT rows, W_hi for output channel co in row co, W_lo in row COUT + co
         uint8_t* base = tb;
         int rb = rb0, k = ci;
         if (ci >= ch0) {
-          base = tb + static_cast<size_t>(cout) * rb0;
+          base = tb + static_cast<size_t>(2 * cout) * rb0;
           rb = rb1;
           k = ci - ch0;
         }
-        const uint32_t off = swz_off(rb, static_cast<uint32_t>(co), static_cast<uint32_t>(k / 8)) + (k % 8) * 2;
-        std::memcpy(base + off, &hi, 2);
-        std::memcpy(base + half + off, &lo, 2);
+        const uint32_t c16 = static_cast<uint32_t>(k / 8), e2 = static_cast<uint32_t>(k % 8) * 2;
+        std::memcpy(base + swz_off(rb, static_cast<uint32_t>(co), c16) + e2, &hi, 2);
+        std::memcpy(base + swz_off(rb, static_cast<uint32_t>(cout + co), c16) + e2, &lo, 2);
       }
   }
 }
