@@ -23,9 +23,11 @@ cfg5's total batch split across the ranks).
           without them); peak = MEASURED_PEAKS.json burst bf16 when the SM clock sampled during the
           timed region stays within 5 % of max, the sustained figure otherwise (`peak_kind`)
   clocks  NVML SM clock + clock-event reasons sampled every 5 ms inside the timed region
-  precision_variants  the same step on the FP16 plan (the option that meets the hard-decision bar)
-  extra_configs (N = 1)  cfg1 (fp32), cfg3, cfg4 / cfg4m at their BASELINE batch, the cfg5 batch sweep
-          (bf16 / fp16 / fp32) with p50 latency at B = 1, each with its roofline and a CPU baseline
+  precision_variants  the same step on the FP16 plan (the option that meets the hard-decision bar) and on
+          the BF16X3 split-precision plan (fp32-grade LLRs on the tensor cores)
+  extra_configs (N = 1)  cfg1 (fp32 and bf16x3), cfg3 (bf16 / fp16 / bf16x3), cfg4 / cfg4m at their BASELINE
+          batch, the cfg5 batch sweep (bf16 / fp16 / bf16x3 / fp32) with p50 latency at B = 1, each with its
+          roofline and a CPU baseline
   cpu_baseline  the reference's own Network<float>::forward and forward_concurrent (oracle/_ref,
           compiled in place from /root/reference) + the restated featurizer, all host threads,
           median of 5 reps of a bounded sample
@@ -256,6 +258,7 @@ class Leg:
 
     def __init__(self, torch, P, g, prec, batch, link, device, options=None):
         self.torch = torch
+        self.prec = prec
         self.plan = P.Plan(g, prec, device=device, options=options)
         self.plan.set_pilots(batch.pilots, batch.pilot_mask)
         self.B = batch.y.shape[0]
@@ -332,6 +335,10 @@ class Leg:
             out.update({"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                         "frac": achieved / peak if achieved else None,
                         "peak_kind": f"{kind} bf16 ({pk['source']}); the fp16 kind::f16 rate is the same"})
+            if self.prec.endswith("x3"):
+                # split-precision plans: every MAC is three 16-bit tensor-core products (hi*Whi + lo*Whi +
+                # hi*Wlo); `achieved` counts the algorithmic (fp32) FLOPs, `issued_frac` the tensor pipe's
+                out.update({"tensor_products_per_mac": 3, "issued_frac": 3 * achieved / peak if achieved else None})
         return out
 
     def close(self):
@@ -409,19 +416,23 @@ def extra_configs(torch, P, G, slots, local, pk, steps):
     out = {}
     k = max(3, min(steps, 10))
     out["cfg1_fp32_b64"] = measure_config(torch, P, G, slots, "cfg1", "fp32", 64, k, 3, local, pk, cpu_slots=64)
+    # the fp32-grade tensor-core plan (LLRs within 1e-4 of the reference) on the fp32 config
+    out["cfg1_bf16x3_b64"] = measure_config(torch, P, G, slots, "cfg1", "bf16x3", 64, k, 3, local, pk, want_cpu=False)
+    out["cfg3_bf16x3_b64"] = measure_config(torch, P, G, slots, "cfg3", "bf16x3", 64, 3, 2, local, pk, want_cpu=False)
     for prec in ("bf16", "fp16"):
         out[f"cfg3_{prec}_b64"] = measure_config(torch, P, G, slots, "cfg3", prec, 64, k, 3, local, pk,
                                                  want_cpu=prec == "bf16", cpu_slots=16, f_sample=137)
     out["cfg4_bf16_b256"] = measure_config(torch, P, G, slots, "cfg4", "bf16", 256, k, 3, local, pk, cpu_slots=8)
     out["cfg4m_bf16_b256"] = measure_config(torch, P, G, slots, "cfg4m", "bf16", 256, k, 3, local, pk, cpu_slots=8)
-    # cfg5: the cfg2 batch sweep, bf16 / fp16 tensor-core plans and the fp32 CUDA-core plan
+    # cfg5: the cfg2 batch sweep, bf16 / fp16 tensor-core plans, the fp32-grade split-precision tensor-core
+    # plan (bf16x3) and the bit-exact fp32 CUDA-core plan
     sweep = []
     cfg = G.CONFIGS["cfg2"]
     g = cfg.graph(seed=1)
     for prec, Bs in (("bf16", (1, 4, 16, 64, 256, 1024, 4096, 8192)), ("fp16", (1, 64, 256, 1024, 8192)),
-                     ("fp32", (1, 16, 256, 1024))):
+                     ("bf16x3", (1, 16, 256, 1024, 8192)), ("fp32", (1, 16, 256, 1024))):
         for B in Bs:
-            kk = 3 if (prec == "fp32" and B >= 256) or B >= 4096 else k
+            kk = 3 if (prec in ("fp32", "bf16x3") and B >= 256) or B >= 4096 else k
             r = measure_config(torch, P, G, slots, "cfg2", prec, B, kk, 2, local, pk, want_cpu=False)
             sweep.append({kk2: r[kk2] for kk2 in ("precision", "batch", "ms_per_step_median", "slots_per_s",
                                                    "res_per_s", "whole_step_tflops")} |
@@ -580,6 +591,17 @@ def main():
         variants = {"fp16": {"value": B * args.steps / (sum(vms) * 1e-3), "ms_per_step": sum(vms) / args.steps,
                              "roofline": v.roofline(vprof, args.steps, pk, vclk), "clocks": vclk,
                              "decision_agreement": "tests/test_trained.py (>= 99.99 % of all data bits vs fp32)"}}
+        v.close()
+        torch.cuda.empty_cache()
+        # the split-precision plan: fp32-grade LLRs (<= 1e-4 relative of the reference) on the tensor cores
+        v = Leg(torch, P, g, "bf16x3", batch, link, local, options={})
+        v.warm(args.warmup)
+        vms, _, vclk = v.timed(args.steps, clock_index=local)
+        _, vprof, _ = v.timed(args.steps, profile=True)
+        variants["bf16x3"] = {"value": B * args.steps / (sum(vms) * 1e-3), "ms_per_step": sum(vms) / args.steps,
+                              "roofline": v.roofline(vprof, args.steps, pk, vclk), "clocks": vclk,
+                              "parity": "tests/test_gpu_x3.py (<= 1e-4 relative of the reference); decisions "
+                                        ">= 99.99 % on trained cfg2 and cfg3 (tests/test_trained.py)"}
         v.close()
         torch.cuda.empty_cache()
 
