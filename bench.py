@@ -415,15 +415,21 @@ def extra_configs(torch, P, G, slots, local, pk, steps):
     """Driver-visible numbers for the other BASELINE configs, N = 1."""
     out = {}
     k = max(3, min(steps, 10))
-    out["cfg1_fp32_b64"] = measure_config(torch, P, G, slots, "cfg1", "fp32", 64, k, 3, local, pk, cpu_slots=64)
+    def one(key, *a, **kw):  # a failing config is recorded, the others still run
+        try:
+            out[key] = measure_config(torch, P, G, slots, *a, **kw)
+        except Exception as e:
+            out[key] = {"error": repr(e)}
+            torch.cuda.empty_cache()
+
+    one("cfg1_fp32_b64", "cfg1", "fp32", 64, k, 3, local, pk, cpu_slots=64)
     # the fp32-grade tensor-core plan (LLRs within 1e-4 of the reference) on the fp32 config
-    out["cfg1_bf16x3_b64"] = measure_config(torch, P, G, slots, "cfg1", "bf16x3", 64, k, 3, local, pk, want_cpu=False)
-    out["cfg3_bf16x3_b64"] = measure_config(torch, P, G, slots, "cfg3", "bf16x3", 64, 3, 2, local, pk, want_cpu=False)
+    one("cfg1_bf16x3_b64", "cfg1", "bf16x3", 64, k, 3, local, pk, want_cpu=False)
+    one("cfg3_bf16x3_b64", "cfg3", "bf16x3", 64, 3, 2, local, pk, want_cpu=False)
     for prec in ("bf16", "fp16"):
-        out[f"cfg3_{prec}_b64"] = measure_config(torch, P, G, slots, "cfg3", prec, 64, k, 3, local, pk,
-                                                 want_cpu=prec == "bf16", cpu_slots=16, f_sample=137)
-    out["cfg4_bf16_b256"] = measure_config(torch, P, G, slots, "cfg4", "bf16", 256, k, 3, local, pk, cpu_slots=8)
-    out["cfg4m_bf16_b256"] = measure_config(torch, P, G, slots, "cfg4m", "bf16", 256, k, 3, local, pk, cpu_slots=8)
+        one(f"cfg3_{prec}_b64", "cfg3", prec, 64, k, 3, local, pk, want_cpu=prec == "bf16", cpu_slots=16, f_sample=137)
+    one("cfg4_bf16_b256", "cfg4", "bf16", 256, k, 3, local, pk, cpu_slots=8)
+    one("cfg4m_bf16_b256", "cfg4m", "bf16", 256, k, 3, local, pk, cpu_slots=8)
     # cfg5: the cfg2 batch sweep, bf16 / fp16 tensor-core plans, the fp32-grade split-precision tensor-core
     # plan (bf16x3) and the bit-exact fp32 CUDA-core plan
     sweep = []
@@ -433,7 +439,12 @@ def extra_configs(torch, P, G, slots, local, pk, steps):
                      ("bf16x3", (1, 16, 256, 1024, 8192)), ("fp32", (1, 16, 256, 1024))):
         for B in Bs:
             kk = 3 if (prec in ("fp32", "bf16x3") and B >= 256) or B >= 4096 else k
-            r = measure_config(torch, P, G, slots, "cfg2", prec, B, kk, 2, local, pk, want_cpu=False)
+            try:
+                r = measure_config(torch, P, G, slots, "cfg2", prec, B, kk, 2, local, pk, want_cpu=False)
+            except Exception as e:  # recorded per point, never fatal for the rest of the sweep
+                sweep.append({"precision": prec, "batch": B, "error": repr(e)})
+                torch.cuda.empty_cache()
+                continue
             sweep.append({kk2: r[kk2] for kk2 in ("precision", "batch", "ms_per_step_median", "slots_per_s",
                                                    "res_per_s", "whole_step_tflops")} |
                          {"roofline_frac": r["roofline"]["frac"], "roofline_kernel": r["roofline"]["kernel"],

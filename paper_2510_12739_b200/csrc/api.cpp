@@ -220,6 +220,7 @@ struct cnrx_plan {
   cnrx_plan_options opt{};
   int device = 0;
   int num_sms = 148;
+  size_t mem_budget = 0;       // workspace bytes one forward may use; larger batches run in slot chunks
   cudaStream_t stream = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host APIs
   std::vector<cudaEvent_t> pipe_ev;            // [2 * chunks]: input landed / chunk computed
@@ -1648,8 +1649,30 @@ void* ensure_dev(void*& buf, size_t& cap, size_t bytes) {
   return buf;
 }
 
+// Slots per forward whose workspace (activation planes, or fp32 node buffers, plus the fp32 feature
+// buffer) fits the plan's memory budget (55 % of the device's HBM): bigger batches run as consecutive
+// slot chunks through the same workspace (every op is per slot, so the LLRs are the same).
+int64_t max_batch(const cnrx_plan& p, int64_t T, int64_t F) {
+  if (p.mem_budget == 0) return int64_t{1} << 40;
+  double per_slot = static_cast<double>(T * F * p.in_ch) * sizeof(float);  // fp32 features (receive path)
+  if (p.precision == CNRX_FP32) {
+    for (int c : p.f32_buf_channels) per_slot += static_cast<double>(T * F * c) * sizeof(float);
+  } else {
+    const double rows = static_cast<double>(F + p.npad) * static_cast<double>(T + 1);
+    for (int c : p.buf_channels) per_slot += rows * c * 2.0 * (p.split ? 2 : 1);
+  }
+  return std::max<int64_t>(1, static_cast<int64_t>(static_cast<double>(p.mem_budget) / per_slot));
+}
+
 void run_forward(cnrx_plan& p, const float* x_dev, int64_t B, int64_t T, int64_t F, float* out_dev, int input_kind,
                  int N, cudaStream_t s) {
+  const int64_t cap = max_batch(p, T, F);
+  if (B > cap) {
+    const int64_t in_slot = T * F * (input_kind == 1 ? 2 * N : p.in_ch), out_slot = T * F * p.out_ch;
+    for (int64_t b0 = 0; b0 < B; b0 += cap)
+      run_forward(p, x_dev + b0 * in_slot, std::min(cap, B - b0), T, F, out_dev + b0 * out_slot, input_kind, N, s);
+    return;
+  }
   ensure_workspace(p, static_cast<int>(B), static_cast<int>(T), static_cast<int>(F));
   float* feat = nullptr;  // fp32 plans on the receive path: features in the reference layout
   if ((p.precision == CNRX_FP32 || p.split) && input_kind == 1) {  // allocated outside any graph capture
@@ -2039,6 +2062,9 @@ int cnrx_plan_create_ex(const cnrx_node* nodes, int32_t n_nodes, int32_t input_n
     }
     plan->device = device;
     plan->num_sms = prop.multiProcessorCount;
+    plan->mem_budget = static_cast<size_t>(0.55 * static_cast<double>(prop.totalGlobalMem));
+    if (const char* mb = std::getenv("CNRX_MEM_BUDGET_MB"))  // tests of the slot-chunked forward only
+      plan->mem_budget = static_cast<size_t>(std::atof(mb) * 1048576.0);
     plan->nodes.assign(nodes, nodes + n_nodes);
     plan->in_node = input_node;
     plan->out_node = output_node;

@@ -137,7 +137,9 @@ __global__ void __launch_bounds__(256) pw_program_kernel(const __grid_constant__
 // Coalesced variant for C in {16, 32, 64, 128}: LPR = C/8 lanes share a row (each lane owns one
 // 16-byte, 8-channel slice), so a warp instruction reads 32 consecutive 16-byte slices of 32/LPR rows.
 // The head GEMV partial sums are reduced across the row's lanes with shuffles.
-template <int HEAD, int LPR>
+// SPLIT (CNRX_*X3 plans): rows are [hi C | lo C]; a lane loads its 8-channel slice of both halves (each
+// warp instruction still covers whole 128-byte lines) and stores the result split the same way.
+template <int HEAD, int LPR, bool SPLIT = false>
 __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ PwProgram prog, PlaneGeom geo) {
   extern __shared__ float smem_f[];
   const int C = prog.C, NB = prog.head_bits;
@@ -164,7 +166,8 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
   }
   __syncthreads();
   constexpr int RPW = 32 / LPR;  // rows per warp pass
-  constexpr int U = 2;           // row groups per iteration (loads of both issued before compute)
+  constexpr int U = SPLIT ? 1 : 2;  // row groups per iteration (loads of both issued before compute)
+  const int64_t RS = SPLIT ? 2 * C : C;  // row stride (16-bit values)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cg = lane % LPR;
   const int c0 = cg * 8;
@@ -175,6 +178,7 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
     int64_t row[U];
     bool in_range[U], valid[U];
     uint4 raw[U][kPwMaxPlanes];
+    uint4 rawl[U][SPLIT ? kPwMaxPlanes : 1];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       row[u] = (grp0 + u) * RPW + lane / LPR;
@@ -182,8 +186,13 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
       valid[u] = in_range[u] && geo.valid(row[u]);
 #pragma unroll
       for (int k = 0; k < kPwMaxPlanes; ++k)
-        if (k < np) raw[u][k] = valid[u] ? *reinterpret_cast<const uint4*>(prog.planes[k] + row[u] * C + c0)
-                                          : make_uint4(0, 0, 0, 0);
+        if (k < np) {
+          raw[u][k] = valid[u] ? *reinterpret_cast<const uint4*>(prog.planes[k] + row[u] * RS + c0)
+                               : make_uint4(0, 0, 0, 0);
+          if constexpr (SPLIT)
+            rawl[u][k] = valid[u] ? *reinterpret_cast<const uint4*>(prog.planes[k] + row[u] * RS + C + c0)
+                                  : make_uint4(0, 0, 0, 0);
+        }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -204,6 +213,19 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
             const float2 f = unpack2r(prog.fp16 != 0, h[i]);
             v[2 * i] = f.x;
             v[2 * i + 1] = f.y;
+          }
+          if constexpr (SPLIT) {
+            uint4 l4 = rawl[u][0];
+#pragma unroll
+            for (int k = 1; k < kPwMaxPlanes; ++k)
+              if (k == ins.k) l4 = rawl[u][k];
+            const uint32_t* hl = reinterpret_cast<const uint32_t*>(&l4);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = unpack2r(prog.fp16 != 0, hl[i]);
+              v[2 * i] += f.x;  // hi + lo: exact in fp32
+              v[2 * i + 1] += f.y;
+            }
           }
 #pragma unroll
           for (int i = 0; i < 8; ++i)
@@ -252,11 +274,15 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
           }
         }
       } else if (in_range[u]) {
-        uint4 o;
-        uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+        if constexpr (SPLIT) {
+          store8_split(prog.out_plane + row[u] * RS + c0, C, acc, prog.fp16 != 0);
+        } else {
+          uint4 o;
+          uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) op[i] = pack2r(prog.fp16 != 0, acc[2 * i], acc[2 * i + 1]);
-        *reinterpret_cast<uint4*>(prog.out_plane + row[u] * C + c0) = o;
+          for (int i = 0; i < 4; ++i) op[i] = pack2r(prog.fp16 != 0, acc[2 * i], acc[2 * i + 1]);
+          *reinterpret_cast<uint4*>(prog.out_plane + row[u] * C + c0) = o;
+        }
       }
     }
   }
@@ -556,7 +582,7 @@ bool pw_as_fold(const PwProgram& prog, int* nsteps, int* ops, int* affs, int* re
   return ns > 0;
 }
 
-template <int HEAD, int LPR>
+template <int HEAD, int LPR, bool SPLIT = false>
 static void launch_rows(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s) {
   int n_aff = 0;
   for (int n = 0; n < prog.n_ins; ++n)
@@ -569,7 +595,7 @@ static void launch_rows(const PwProgram& prog, const PlaneGeom& geo, cudaStream_
   const int64_t groups = (geo.Nalloc + (32 / LPR) - 1) / (32 / LPR);
   const int64_t want = (groups + 15) / 16;
   const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(sms) * 8));
-  pw_rows_kernel<HEAD, LPR><<<blocks, 256, smem, s>>>(prog, geo);
+  pw_rows_kernel<HEAD, LPR, SPLIT><<<blocks, 256, smem, s>>>(prog, geo);
   CNRX_CUDA(cudaGetLastError());
 }
 
@@ -577,7 +603,16 @@ const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaS
   if (prog.head_bits > 0) require(prog.head_bits <= kPwMaxBits, "head with more than 16 outputs");
   require(prog.out2_plane == nullptr || prog.head_bits == 0, "second output needs a plane program");
   const bool head = prog.head_bits > 0;
-  if (prog.split) {  // split planes: the generic interpreter (one thread per row) reads / writes hi + lo
+  if (prog.split && !prog.out2_plane && (prog.C == 16 || prog.C == 32 || prog.C == 64)) {
+    // split planes, coalesced: a row's lanes read their slices of both halves
+    switch (prog.C) {
+      case 16: head ? launch_rows<1, 2, true>(prog, geo, s) : launch_rows<0, 2, true>(prog, geo, s); break;
+      case 32: head ? launch_rows<1, 4, true>(prog, geo, s) : launch_rows<0, 4, true>(prog, geo, s); break;
+      default: head ? launch_rows<1, 8, true>(prog, geo, s) : launch_rows<0, 8, true>(prog, geo, s); break;
+    }
+    return head ? "pw_rows_kernel<head,x3>" : "pw_rows_kernel<plane,x3>";
+  }
+  if (prog.split) {  // other widths / a second output: the generic interpreter (one thread per row)
     const int threads = 256;
     const unsigned blocks = static_cast<unsigned>((geo.Nalloc + threads - 1) / threads);
     if (head) {

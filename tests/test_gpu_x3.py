@@ -130,3 +130,23 @@ def test_x3_batch_invariance_and_capture():
 def test_x3_options_are_fixed():
     o = P.Plan(G.CONFIGS["cfg2"].graph(), "bf16x3").options()
     assert o["fused_blocks"] == 0 and o["weights_stationary"] == 0 and o["cta_pair"] == 0 and o["fused_head"] == 0
+
+
+@pytest.mark.parametrize("prec", ["bf16", "bf16x3", "fp32"])
+def test_batches_beyond_the_memory_budget_run_in_slot_chunks(prec, monkeypatch):
+    """A batch whose workspace exceeds the plan's budget (55 % of HBM; here forced to ~2 slots' worth)
+    runs as consecutive slot chunks through one workspace: same LLRs as the one-shot forward, through
+    forward(), receive() and the device entry points."""
+    g = G.CONFIGS["cfg2"].graph(seed=3)
+    link = dataclasses.replace(G.CONFIGS["cfg2"].link, F=40)
+    b = slots.generate(link, 7, 11)
+    ref = P.Plan(g, prec)
+    ref.set_pilots(b.pilots, b.pilot_mask)
+    want = ref.receive(b.y)
+    # ~2.5 slots of cfg2 planes at F = 40 (bf16: 12 planes x 41 x 15 rows x 64 ch x 2 B = 0.9 MB per slot)
+    monkeypatch.setenv("CNRX_MEM_BUDGET_MB", "3" if prec != "bf16" else "2")
+    p = P.Plan(g, prec)
+    p.set_pilots(b.pilots, b.pilot_mask)
+    assert np.array_equal(p.receive(b.y), want)
+    x = oracle.featurize(b.y, b.pilots, b.pilot_mask)
+    assert np.array_equal(p.forward(x), ref.forward(x))
