@@ -891,8 +891,10 @@ struct Bf16Compiler {
         const bool ws64 = w.dims[2] == 64 && w.dims[3] == 64 && vC == 64 && p.opt.weights_stationary;
         const bool pair96 = round_cin(static_cast<int>(w.dims[2])) == 96 && round_cout(static_cast<int>(w.dims[3])) == 96 &&
                             vC == 96 && p.opt.cta_pair;
+        // split plans: every 3x3 conv (conv_x3.cu has a ReLU warp for its (hi, lo) windows)
+        const bool x3 = p.split && vC > 0;
         if (!no_relu_in && v >= 0 && node_plane[static_cast<size_t>(nd.in0)] < 0 && node_plane[static_cast<size_t>(v)] >= 0 &&
-            !p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].nonneg && op.ks == 3 && (ws64 || pair96)) {
+            !p.planes[static_cast<size_t>(node_plane[static_cast<size_t>(v)])].nonneg && op.ks == 3 && (ws64 || pair96 || x3)) {
           op.relu_in = 1;
           op.in_plane = node_plane[static_cast<size_t>(v)];
         } else {
@@ -947,7 +949,7 @@ struct Bf16Compiler {
       if (op.res_plane >= 0) use(op.res_plane, op.level);
       // weights (BN scale folded per output channel) and bias
       op.ws = p.opt.weights_stationary != 0 && op.ks == 3 && op.cin_real == 64 && op.cout_real == 64 && op.cin == 64 && op.cout == 64;
-      if (op.relu_in && !op.ws && !(op.cin == 96 && op.cout == 96 && op.ks == 3))
+      if (op.relu_in && !op.ws && !p.split && !(op.cin == 96 && op.cout == 96 && op.ks == 3))
         throw Error(CNRX_ERR_UNSUPPORTED, "internal: relu-on-load needs the ws or the CTA-pair conv kernel");
       if (op.ws) {
         std::vector<uint32_t> img(conv_ws64_wimg_bytes() / 4);
@@ -1317,10 +1319,12 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           g.s2 = op.s2;
           g.t2 = op.t2;
           g.relu = op.relu;
+          if (op.relu_in) L.relu_in = 1;  // a launch group shares relu_in (grouping rule)
         }
         L.win_alloc = win_alloc;
         if (!conv_x3_config(op0.cin, op0.cout, op0.ks, win_alloc, &L.stages, &L.nslots))
           throw Error(CNRX_ERR_UNSUPPORTED, "split-precision conv working set exceeds shared memory");
+        if (const char* d = std::getenv("CNRX_X3_DBG")) L.dbg = std::atoi(d);  // A/B experiments only
       } else {
         TcLaunch& L = GL.tc;
         std::memset(&L, 0, sizeof(L));
@@ -1595,7 +1599,21 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
         continue;
       }
       if (GL.x3) {
+        GL.x3l.trace = trace ? dtrace : nullptr;
         p.note(conv_x3_launch(op0.cin, op0.cout, op0.ks, GL.x3l, p.num_sms, s), s, fl);
+        if (trace) {
+          unsigned long long h[16];
+          CNRX_CUDA(cudaMemcpyAsync(h, dtrace, sizeof h, cudaMemcpyDeviceToHost, s));
+          CNRX_CUDA(cudaStreamSynchronize(s));
+          const double nct = static_cast<double>(h[kTraceTiles] ? h[kTraceTiles] : 1);
+          fprintf(stderr,
+                  "[trace] %s tiles=%llu per-tile cycles: prod_wait_empty %.0f mma_wait_full %.0f mma_wait_tmem %.0f "
+                  "mma_issue %.0f | epi(warp 3) wait %.0f work %.0f | mma-thread total/tile %.0f\n",
+                  p.launch_names.back().c_str(), h[kTraceTiles], h[kTraceProdWaitEmpty] / nct, h[kTraceMmaWaitFull] / nct,
+                  h[kTraceMmaWaitTmem] / nct, h[kTraceMmaIssue] / nct, h[kTraceEpiWaitFull] / nct, h[kTraceEpiWork] / nct,
+                  h[kTraceTotal] / nct);
+          trace_window(h);
+        }
         continue;
       }
       p.note(conv_tc_launch(op0.cin, op0.cout, op0.ks, GL.tc, p.num_sms, s), s, fl);
@@ -2057,7 +2075,6 @@ int cnrx_plan_create_ex(const cnrx_node* nodes, int32_t n_nodes, int32_t input_n
       plan->opt.tensor_core_head = 0;
       plan->opt.cta_pair = 0;
       plan->opt.weights_stationary = 0;
-      plan->opt.relu_on_load = 0;
       plan->opt.cuda_core_stem = 0;
     }
     plan->device = device;

@@ -17,14 +17,17 @@
 // The plane layout makes every 3x3 tap a constant row shift (common.h), so a tile's whole K loop reads
 // ONE TMA-loaded window of 128 + 2*halo rows of hi and lo.
 //
-// Warp roles (224 threads, persistent, 1 CTA/SM):
+// Warp roles (persistent, 1 CTA/SM):
 //   warp 0     TMA producer: one hi+lo window per tile into a `stages`-deep ring
 //   warp 1     TMEM allocator + single-thread MMA issuer (taps x K/16 x 2 UMMAs per tile)
 //   warp 2     weight loader: every tap once (resident: 64-channel convs, 147 KB) or, when the split
 //              weights exceed shared memory (96 channels: 331 KB), the taps of every tile through a
 //              ring of `nslots` tap slots (plain bulk copies of the pre-swizzled tap images, L2-resident)
-//   warps 3-6  epilogue: TMEM -> registers -> bias / residual (hi + lo) / ReLU -> hi, lo rows to the
-//              output plane(s); accumulators double-buffered (tile j's epilogue overlaps tile j+1's MMAs)
+//   last 1-2   input ReLU of each window pair in place when the conv's input is relu(plane) (relu_in):
+//              the producing conv then writes one plane instead of y and relu(y)
+//   warps 3..  epilogue, 2 (3 for 96 channels) warps per TMEM lane quadrant, each owning a 32-channel
+//              slice of its 32 rows: TMEM -> registers -> bias / residual (hi + lo) / ReLU -> hi, lo to
+//              the output plane(s); accumulators double-buffered (tile j's epilogue overlaps tile j+1's MMAs)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -42,7 +45,13 @@ namespace cnrx {
 namespace {
 
 constexpr int kBoxRows = 32;
-constexpr int kThreads = 224;
+// epilogue warps per TMEM lane quadrant and channels per epilogue warp
+__host__ __device__ constexpr int epi_per_quadrant(int cout) { return cout == 96 ? 3 : 2; }
+// input-ReLU warps (96 channels: one, to stay within 128 registers at 16 warps)
+__host__ __device__ constexpr int relu_warps(int cout) { return cout == 96 ? 1 : 2; }
+// warps: producer, MMA, weight loader, 4 * EH epilogue, input ReLU
+__host__ __device__ constexpr int threads_of(int cout) { return 32 * (3 + 4 * epi_per_quadrant(cout) + relu_warps(cout)); }
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 constexpr uint32_t kSmemLimit = 227u * 1024u;
 
 __host__ __device__ constexpr int ch0_of(int cin) { return cin > 64 ? 64 : cin; }
@@ -83,8 +92,44 @@ __host__ __device__ inline Lay x3_layout(int cin, int cout, int stages, int win_
   s.par_off = off;  // bias, s2, t2 (fp32)
   off += (3u * static_cast<uint32_t>(cout) * 4u + 15u) & ~15u;
   s.bar_off = off;
-  s.total = off + 256 + 1024;  // barriers (<= 30) + the TMEM slot, alignment slack of the dynamic base
+  s.total = off + 256 + 1024;  // barriers (<= 31) + the TMEM slot, alignment slack of the dynamic base
   return s;
+}
+
+// In-place ReLU of n 16-byte chunk pairs of a split window (hi chunk i at hi + 16 i, its lo chunk at the
+// same offset of the lo buffer: same row, same swizzle position).  relu(hi + lo) = (hi, lo) where hi > 0
+// and (0, 0) elsewhere: hi = round16(v) has the sign of v, so a 16-bit lane compare on hi (signed integer
+// compare of a sign-magnitude format: positive non-zero <=> > 0) masks both halves.  Batches of 8 chunk
+// pairs per lane keep the loads in flight before the first store.
+template <int RB>
+__device__ __forceinline__ void relu_pairs(uint32_t hi, uint32_t lo, int n, int lane) {
+  for (int c0 = 0; c0 < n; c0 += 32 * RB) {
+    uint4 h[RB], l[RB];
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int c = c0 + u * 32 + lane;
+      if (c < n) {
+        h[u] = lds128(hi + static_cast<uint32_t>(c) * 16u);
+        l[u] = lds128(lo + static_cast<uint32_t>(c) * 16u);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int c = c0 + u * 32 + lane;
+      if (c < n) {
+        uint32_t* hp = reinterpret_cast<uint32_t*>(&h[u]);
+        uint32_t* lp = reinterpret_cast<uint32_t*>(&l[u]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t m = __vcmpgts2(hp[k], 0u);
+          hp[k] &= m;
+          lp[k] &= m;
+        }
+        sts128(hi + static_cast<uint32_t>(c) * 16u, h[u]);
+        sts128(lo + static_cast<uint32_t>(c) * 16u, l[u]);
+      }
+    }
+  }
 }
 
 // v -> (hi, lo) 16-bit pairs for two channels
@@ -96,7 +141,7 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
 }
 
 template <int CIN, int COUT, int KS, bool F16>
-__global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_constant__ X3Launch L) {
+__global__ void __launch_bounds__(threads_of(COUT), 1) conv_x3_kernel(const __grid_constant__ X3Launch L) {
   constexpr int CH0 = ch0_of(CIN), CH1 = ch1_of(CIN);
   constexpr int RB0 = CH0 * 2, RB1 = CH1 * 2;
   constexpr uint32_t SW0 = swz_mode(RB0), SW1 = swz_mode(RB1);
@@ -105,6 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
   constexpr uint32_t TMEM_COLS = tmem_cols(COUT);
   constexpr uint32_t IDESC1 = idesc_e16_f32<F16>(128, COUT);      // A_lo * W_hi
   constexpr uint32_t IDESC2 = idesc_e16_f32<F16>(128, 2 * COUT);  // A_hi * [W_hi | W_lo]
+  constexpr int EH = epi_per_quadrant(COUT), NEPI = 4 * EH, ECH = COUT / EH;
+  static_assert(ECH % 16 == 0, "epilogue warps own whole 16-column TMEM slices");
 
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
@@ -121,7 +168,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
   uint64_t* wempty = wfull + NS;  // [NS] weight tap consumed (streamed mode)
   uint64_t* tfull = wempty + NS;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;   // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ready = tempty + 2;   // [S] window ReLU'd in place (relu_in)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + S);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -143,12 +191,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], NEPI);
     }
+    for (int s = 0; s < S; ++s) mbar_init(&ready[s], relu_warps(COUT));
     fence_barrier_init();
   }
   if (warp >= 3) {
-    for (int c = threadIdx.x - 96; c < COUT; c += 128) {
+    for (int c = threadIdx.x - 96; c < COUT; c += 32 * NEPI) {
       s_bias[c] = grp.bias[c];
       s_s2[c] = grp.s2 ? grp.s2[c] : 1.f;
       s_t2[c] = grp.t2 ? grp.t2[c] : 0.f;
@@ -175,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
         for (int64_t tile = local; tile < n_tiles; tile += nct)
           for (int tap = 0; tap < TAPS; ++tap, ++wi) {
             const uint32_t slot = wi % static_cast<uint32_t>(NS);
-            mbar_wait(&wempty[slot], ((wi / static_cast<uint32_t>(NS)) & 1u) ^ 1u);
+            mbar_wait_backoff<64>(&wempty[slot], ((wi / static_cast<uint32_t>(NS)) & 1u) ^ 1u);
             mbar_arrive_expect_tx(&wfull[slot], TAPB);
             bulk_load(smem + slot * TAPB, grp.wimg + static_cast<size_t>(tap) * TAPB, TAPB, &wfull[slot]);
           }
@@ -190,9 +239,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
       const int nboxes = (128 + 2 * grp.halo + kBoxRows - 1) / kBoxRows;
       const uint32_t stage_tx = static_cast<uint32_t>(nboxes * kBoxRows * CIN * 2 * 2);
       int j = 0;
+      long long tr_prod = 0;
       for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
         const int s = j % S;
-        mbar_wait(&empty[s], (static_cast<uint32_t>(j / S) & 1u) ^ 1u);
+        const long long tw0 = L.trace ? clock64() : 0;
+        if (L.dbg & 1)
+          mbar_wait(&empty[s], (static_cast<uint32_t>(j / S) & 1u) ^ 1u);
+        else
+          mbar_wait_backoff<64>(&empty[s], (static_cast<uint32_t>(j / S) & 1u) ^ 1u);
+        if (L.trace) tr_prod += clock64() - tw0;
+        if (L.dbg & 16) {  // A/B: no window loads
+          mbar_arrive(&full[s]);
+          continue;
+        }
         mbar_arrive_expect_tx(&full[s], stage_tx);
         uint8_t* win = smem + lay.win_off + s * lay.stage_bytes;
         const int32_t r0 = static_cast<int32_t>(tile * 128 - grp.halo);
@@ -206,142 +265,206 @@ __global__ void __launch_bounds__(kThreads, 1) conv_x3_kernel(const __grid_const
           }
         }
       }
+      if (L.trace) atomicAdd(&L.trace[kTraceProdWaitEmpty], static_cast<unsigned long long>(tr_prod));
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer --------------------------------
-    if (lane == 0) {
-      const uint32_t sW = smem_u32(smem);
-      const int32_t T1 = L.geo.T1;
-      uint32_t wi = 0;
-      int j = 0;
-      for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
-        const int s = j % S;
-        const int a = j & 1;
-        mbar_wait(&full[s], static_cast<uint32_t>(j / S) & 1u);
-        mbar_wait(&tempty[a], (static_cast<uint32_t>(j >> 1) & 1u) ^ 1u);
-        tc_fence_after();
-        const uint32_t win = smem_u32(smem + lay.win_off + s * lay.stage_bytes);
-        const uint32_t d_tmem = tbase + static_cast<uint32_t>(a * 2 * COUT);
-        uint32_t acc = 0;
-#pragma unroll 1
-        for (int tap = 0; tap < TAPS; ++tap) {
-          const uint32_t slot = resident ? static_cast<uint32_t>(tap) : wi % static_cast<uint32_t>(NS);
-          if (!resident || j == 0) {
-            mbar_wait(&wfull[slot], resident ? 0u : (wi / static_cast<uint32_t>(NS)) & 1u);
-            tc_fence_after();
-          }
-          const int dt = tap / KS - KS / 2, df = tap % KS - KS / 2;
-          const int row = grp.halo + dt + df * grp.dil * T1;
-          const uint32_t wb = sW + slot * TAPB;
-          {
-            const uint32_t ah = win + lay.sub[0] + static_cast<uint32_t>(row * RB0);
-            const uint32_t al = win + lay.sub[2] + static_cast<uint32_t>(row * RB0);
+    // The whole warp runs the loop (waits, bookkeeping and descriptor bases stay warp-uniform) and one
+    // elected lane issues each tap's UMMAs: issued from a lane-0-only branch every UMMA was wrapped in
+    // an ELECT / BRA.U.ANY loop and the issue alone took ~6400 cycles per tile (trace), twice the
+    // tensor time.  Descriptors: 32-bit low words advanced by one add per UMMA (sm100.cuh umma_ss_lohi).
+    const uint32_t dh0 = sdesc_hi(8 * RB0, SW0), dh1 = sdesc_hi(8 * RB1, SW1);
+    const uint32_t w_lo = sdesc_lo(smem_u32(smem));
+    const int32_t T1 = L.geo.T1;
+    int32_t trow[TAPS];  // window row of each tap's A operand
 #pragma unroll
-            for (int kk = 0; kk < CH0 / 16; ++kk) {
-              const uint64_t dah = make_sdesc(ah + kk * 32, 8 * RB0, SW0, 0);
-              const uint64_t dal = make_sdesc(al + kk * 32, 8 * RB0, SW0, 0);
-              const uint64_t db = make_sdesc(wb + kk * 32, 8 * RB0, SW0, 0);
-              umma_f16(d_tmem, dah, db, IDESC2, acc);
-              umma_f16(d_tmem, dal, db, IDESC1, 1);
-              acc = 1;
-            }
+    for (int tap = 0; tap < TAPS; ++tap)
+      trow[tap] = grp.halo + (tap / KS - KS / 2) + (tap % KS - KS / 2) * grp.dil * T1;
+    if (resident)
+      for (int tap = 0; tap < TAPS; ++tap) mbar_wait(&wfull[tap], 0);
+    uint32_t wi = 0;
+    int j = 0;
+    long long tr_full = 0, tr_tmem = 0, tr_issue = 0;
+    const long long t_start = clock64();
+    const unsigned long long g_start = L.trace ? globaltimer_ns() : 0;
+    for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
+      const int s = j % S;
+      const int a = j & 1;
+      const long long tm0 = L.trace ? clock64() : 0;
+      mbar_wait(L.relu_in ? &ready[s] : &full[s], static_cast<uint32_t>(j / S) & 1u);
+      const long long tm1 = L.trace ? clock64() : 0;
+      mbar_wait(&tempty[a], (static_cast<uint32_t>(j >> 1) & 1u) ^ 1u);
+      const long long tm2 = L.trace ? clock64() : 0;
+      if (L.trace) {
+        tr_full += tm1 - tm0;
+        tr_tmem += tm2 - tm1;
+      }
+      tc_fence_after();
+      const uint32_t wlo = sdesc_lo(smem_u32(smem + lay.win_off + s * lay.stage_bytes));
+      const uint32_t ah0 = wlo + (lay.sub[0] >> 4), al0 = wlo + (lay.sub[2] >> 4);
+      const uint32_t ah1 = wlo + (lay.sub[1] >> 4), al1 = wlo + (lay.sub[3] >> 4);
+      const uint32_t d_tmem = tbase + static_cast<uint32_t>(a * 2 * COUT);
+#pragma unroll
+      for (int tap = 0; tap < TAPS; ++tap) {
+        const uint32_t slot = resident ? static_cast<uint32_t>(tap) : wi % static_cast<uint32_t>(NS);
+        if (!resident) {
+          mbar_wait(&wfull[slot], (wi / static_cast<uint32_t>(NS)) & 1u);
+          tc_fence_after();
+        }
+        if (elect_one()) {
+          const uint32_t wb = w_lo + slot * (TAPB >> 4);
+          const uint32_t r0 = static_cast<uint32_t>(trow[tap] * (RB0 >> 4));
+#pragma unroll
+          for (int kk = 0; kk < CH0 / 16; ++kk) {
+            umma_ss_lohi(d_tmem, ah0 + r0 + 2 * kk, dh0, wb + 2 * kk, dh0, IDESC2, (tap | kk) != 0 ? 1u : 0u);
+            umma_ss_lohi(d_tmem, al0 + r0 + 2 * kk, dh0, wb + 2 * kk, dh0, IDESC1, 1u);
           }
           if (CH1) {
-            const uint32_t ah = win + lay.sub[1] + static_cast<uint32_t>(row * RB1);
-            const uint32_t al = win + lay.sub[3] + static_cast<uint32_t>(row * RB1);
-            const uint32_t w1 = wb + static_cast<uint32_t>(2 * COUT * RB0);
+            const uint32_t r1 = static_cast<uint32_t>(trow[tap] * (RB1 >> 4));
+            const uint32_t w1 = wb + ((2 * COUT * RB0) >> 4);
 #pragma unroll
             for (int kk = 0; kk < CH1 / 16; ++kk) {
-              const uint64_t dah = make_sdesc(ah + kk * 32, 8 * RB1, SW1, 0);
-              const uint64_t dal = make_sdesc(al + kk * 32, 8 * RB1, SW1, 0);
-              const uint64_t db = make_sdesc(w1 + kk * 32, 8 * RB1, SW1, 0);
-              umma_f16(d_tmem, dah, db, IDESC2, 1);
-              umma_f16(d_tmem, dal, db, IDESC1, 1);
+              umma_ss_lohi(d_tmem, ah1 + r1 + 2 * kk, dh1, w1 + 2 * kk, dh1, IDESC2, 1u);
+              umma_ss_lohi(d_tmem, al1 + r1 + 2 * kk, dh1, w1 + 2 * kk, dh1, IDESC1, 1u);
             }
           }
-          if (!resident) {
-            umma_commit(&wempty[slot]);  // tap slot free once these MMAs have read it
-            ++wi;
-          }
+          if (!resident) umma_commit(&wempty[slot]);  // tap slot free once these MMAs have read it
         }
+        __syncwarp();
+        if (!resident) ++wi;
+      }
+      if (elect_one()) {
         umma_commit(&empty[s]);   // window stage free
         umma_commit(&tfull[a]);   // accumulator ready for the epilogue
       }
+      __syncwarp();
+      if (L.trace) tr_issue += clock64() - tm2;
+    }
+    if (L.trace && lane == 0) {
+      atomicAdd(&L.trace[kTraceTotal], static_cast<unsigned long long>(clock64() - t_start));
+      trace_cta_window(L.trace, g_start);
+      atomicAdd(&L.trace[kTraceMmaWaitFull], static_cast<unsigned long long>(tr_full));
+      atomicAdd(&L.trace[kTraceMmaWaitTmem], static_cast<unsigned long long>(tr_tmem));
+      atomicAdd(&L.trace[kTraceMmaIssue], static_cast<unsigned long long>(tr_issue));
+      atomicAdd(&L.trace[kTraceTiles], static_cast<unsigned long long>(j));
+    }
+  } else if (warp >= 3 + NEPI) {
+    // ------------------------------ input ReLU (relu_in) ----------------------
+    // The window is the tensor core's A operand (async proxy): ReLU it in place with generic 16-byte
+    // shared accesses, then fence them to the async proxy before releasing the stage to the MMA warp.
+    if (L.relu_in) {
+      const int nrows = (128 + 2 * grp.halo + kBoxRows - 1) / kBoxRows * kBoxRows;
+      constexpr int RW = relu_warps(COUT);
+      const int rw = warp - 3 - NEPI;  // this warp's share: rows [rw * nrows / RW, (rw + 1) * nrows / RW)
+      const int r0 = rw * nrows / RW, r1 = (rw + 1) * nrows / RW;
+      int j = 0;
+      for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
+        const int s = j % S;
+        mbar_wait(&full[s], static_cast<uint32_t>(j / S) & 1u);
+        const uint32_t win = smem_u32(smem + lay.win_off + s * lay.stage_bytes);
+        relu_pairs<COUT == 96 ? 4 : 8>(win + lay.sub[0] + r0 * RB0, win + lay.sub[2] + r0 * RB0, (r1 - r0) * (CH0 / 8), lane);
+        if (CH1)
+          relu_pairs<COUT == 96 ? 4 : 8>(win + lay.sub[1] + r0 * RB1, win + lay.sub[3] + r0 * RB1, (r1 - r0) * (CH1 / 8), lane);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ready[s]);
+      }
     }
   } else {
-    // ------------------------------ epilogue (warps 3..6) ---------------------
+    // ------------------------------ epilogue (warps 3..) ---------------------
+    // EH warps per TMEM lane quadrant (warp % 4), each owning ECH of the Cout channels of its 32 rows:
+    // one warp per quadrant left the epilogue latency-bound (a single dependent instruction stream per
+    // SM sub-partition: ~5000 cycles per tile with the MMAs switched off)
     pdl_wait();
-    asm volatile("bar.sync 1, 128;" ::: "memory");  // s_bias / s_s2 / s_t2 visible to all epilogue warps
+    named_bar_sync(1, 32 * NEPI);  // s_bias / s_s2 / s_t2 visible to all epilogue warps
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int cb = ((warp - 3) / 4) * ECH;  // first channel of this warp
     const int row = q * 32 + lane;
     const PlaneGeom geo = L.geo;
     int j = 0;
+    long long tr_ew = 0, tr_ework = 0;
     for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
       const int a = j & 1;
-      mbar_wait(&tfull[a], static_cast<uint32_t>(j >> 1) & 1u);
-      tc_fence_after();
+      const long long te0 = L.trace ? clock64() : 0;
       const int64_t p = tile * 128 + row;
-      const bool valid = geo.valid(p);
-      const uint32_t taddr = tbase + static_cast<uint32_t>(a * 2 * COUT) + (static_cast<uint32_t>(q * 32) << 16);
       const __nv_bfloat16* rrow = grp.res ? grp.res + p * (2 * COUT) : nullptr;
-      __nv_bfloat16* orow = grp.out ? grp.out + p * (2 * COUT) : nullptr;
-      __nv_bfloat16* orow2 = grp.out2 ? grp.out2 + p * (2 * COUT) : nullptr;
-#pragma unroll 1
-      for (int cc = 0; cc < COUT / 32; ++cc) {
-        uint32_t r[32], e[32];
-        tmem_ld32(taddr + cc * 32, r);          // D: hi*Whi + lo*Whi
-        tmem_ld32(taddr + COUT + cc * 32, e);   // E: hi*Wlo
-        tmem_ld_wait();
-        if (cc == COUT / 32 - 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_relaxed(&tempty[a]);
-        }
+      __nv_bfloat16* orow = grp.out && !(L.dbg & 8) ? grp.out + p * (2 * COUT) : nullptr;
+      __nv_bfloat16* orow2 = grp.out2 && !(L.dbg & 8) ? grp.out2 + p * (2 * COUT) : nullptr;
+      // the residual slices are fetched before the accumulator wait: their latency hides behind the MMAs
+      u32x8 rh[ECH / 16], rl[ECH / 16];
+      if (rrow) {
 #pragma unroll
-        for (int hp = 0; hp < 2; ++hp) {
-          const int c0 = cc * 32 + hp * 16;
-          float v[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            v[i] = (__uint_as_float(r[hp * 16 + i]) + __uint_as_float(e[hp * 16 + i])) + s_bias[c0 + i];
-          if (rrow) {
-            const u32x8 rh = ldg256(rrow + c0);
-            const u32x8 rl = ldg256(rrow + COUT + c0);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float2 h = unpack2<F16>(rh.v[i]), l = unpack2<F16>(rl.v[i]);
-              v[2 * i] += h.x + l.x;  // hi + lo is exact in fp32
-              v[2 * i + 1] += h.y + l.y;
-            }
-          }
-          if (grp.relu) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
-          }
-          if (!valid) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0.f;
-          }
-          if (orow) {
-            u32x8 oh, ol;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) split2<F16>(v[2 * i], v[2 * i + 1], oh.v[i], ol.v[i]);
-            stg256(orow + c0, oh);
-            stg256(orow + COUT + c0, ol);
-          }
-          if (orow2) {
-            u32x8 oh, ol;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float x0 = fmaxf(v[2 * i] * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
-              const float x1 = fmaxf(v[2 * i + 1] * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
-              split2<F16>(valid ? x0 : 0.f, valid ? x1 : 0.f, oh.v[i], ol.v[i]);
-            }
-            stg256(orow2 + c0, oh);
-            stg256(orow2 + COUT + c0, ol);
-          }
+        for (int i = 0; i < ECH / 16; ++i) {
+          rh[i] = ldg256(rrow + cb + 16 * i);
+          rl[i] = ldg256(rrow + COUT + cb + 16 * i);
         }
       }
+      const bool valid = geo.valid(p);
+      if (L.dbg & 1)
+        mbar_wait(&tfull[a], static_cast<uint32_t>(j >> 1) & 1u);
+      else
+        mbar_wait_backoff<128>(&tfull[a], static_cast<uint32_t>(j >> 1) & 1u);  // polls cost smem issue
+      tc_fence_after();
+      const long long te1 = L.trace ? clock64() : 0;
+      if (L.trace) tr_ew += te1 - te0;
+      const uint32_t taddr = tbase + static_cast<uint32_t>(a * 2 * COUT + cb) + (static_cast<uint32_t>(q * 32) << 16);
+      uint32_t r[ECH], e[ECH];
+#pragma unroll
+      for (int i = 0; i < ECH / 16; ++i) {
+        tmem_ld16(taddr + 16 * i, *reinterpret_cast<uint32_t(*)[16]>(&r[16 * i]));         // D: hi*Whi + lo*Whi
+        tmem_ld16(taddr + COUT + 16 * i, *reinterpret_cast<uint32_t(*)[16]>(&e[16 * i]));  // E: hi*Wlo
+      }
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_relaxed(&tempty[a]);
+#pragma unroll
+      for (int hp = 0; hp < ECH / 16; ++hp) {
+        const int c0 = cb + hp * 16;
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          v[i] = (__uint_as_float(r[hp * 16 + i]) + __uint_as_float(e[hp * 16 + i])) + s_bias[c0 + i];
+        if (rrow) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float2 h = unpack2<F16>(rh[hp].v[i]), l = unpack2<F16>(rl[hp].v[i]);
+            v[2 * i] += h.x + l.x;  // hi + lo is exact in fp32
+            v[2 * i + 1] += h.y + l.y;
+          }
+        }
+        if (grp.relu) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        if (!valid) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (orow) {
+          u32x8 oh, ol;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) split2<F16>(v[2 * i], v[2 * i + 1], oh.v[i], ol.v[i]);
+          stg256(orow + c0, oh);
+          stg256(orow + COUT + c0, ol);
+        }
+        if (orow2) {
+          u32x8 oh, ol;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float x0 = fmaxf(v[2 * i] * s_s2[c0 + 2 * i] + s_t2[c0 + 2 * i], 0.f);
+            const float x1 = fmaxf(v[2 * i + 1] * s_s2[c0 + 2 * i + 1] + s_t2[c0 + 2 * i + 1], 0.f);
+            split2<F16>(valid ? x0 : 0.f, valid ? x1 : 0.f, oh.v[i], ol.v[i]);
+          }
+          stg256(orow2 + c0, oh);
+          stg256(orow2 + COUT + c0, ol);
+        }
+      }
+      if (L.trace) tr_ework += clock64() - te1;
+    }
+    if (L.trace && warp == 3 && lane == 0) {
+      atomicAdd(&L.trace[kTraceEpiWaitFull], static_cast<unsigned long long>(tr_ew));
+      atomicAdd(&L.trace[kTraceEpiWork], static_cast<unsigned long long>(tr_ework));
     }
   }
 
@@ -360,7 +483,7 @@ const char* launch_t(const X3Launch& L, int num_sms, cudaStream_t stream) {
   const int64_t work = static_cast<int64_t>(L.ngroups) * L.geo.n_tiles;
   int grid = static_cast<int>(work < num_sms ? work : num_sms);
   if (grid < L.ngroups) grid = L.ngroups;
-  launch_pdl(kern, dim3(grid), dim3(kThreads), lay.total, stream, L);
+  launch_pdl(kern, dim3(grid), dim3(threads_of(COUT)), lay.total, stream, L);
   static char name[96];
   snprintf(name, sizeof name, "conv_x3_kernel<%d,%d,%d,%s>", CIN, COUT, KS, F16 ? "f16x3" : "bf16x3");
   return name;

@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
   // disables it; fp16 plans keep z in fp32 (CUDA-core GEMV): z is a product of subnetwork outputs.
   static_assert(!TC || C == 64, "tensor-core head needs 64-channel planes");
   constexpr bool tc = TC;
-  const HeadLayout lay = head_layout(C, NS, NB, L.stages, tc);
+  const bool spl = L.split != 0;  // split planes: each operand tile is a (hi, lo) pair of boxes
+  const HeadLayout lay = head_layout(C, spl ? 2 * NS : NS, NB, L.stages, tc);
   float* s_aff = reinterpret_cast<float*>(smem + lay.aff_off);  // [NS][2][C]
   float* s_w = reinterpret_cast<float*>(smem + lay.w_off);      // [C][NB]
   float* s_b = reinterpret_cast<float*>(smem + lay.b_off);      // [NB]
@@ -120,14 +121,18 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
     // ------------------------------ TMA producer ------------------------------
     if (tid == kConsumers) {
       for (int i = 0; i < NS; ++i) prefetch_tmap(&L.maps[i]);
+      const uint32_t tx = static_cast<uint32_t>(spl ? 2 * NS : NS) * kPlaneBox;
       int j = 0;
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
         const int s = j % L.stages;
         mbar_wait(&empty[s], (static_cast<uint32_t>(j / L.stages) & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(NS) * kPlaneBox);
+        mbar_arrive_expect_tx(&full[s], tx);
         uint8_t* dst = smem + lay.ring_off + s * lay.stage_bytes;
-        for (int i = 0; i < NS; ++i)
+        for (int i = 0; i < NS; ++i) {
           tma_load_2d(dst + i * kPlaneBox, &L.maps[i], &full[s], 0, static_cast<int32_t>(tile * kHRows));
+          if (spl)
+            tma_load_2d(dst + (NS + i) * kPlaneBox, &L.lo_maps[i], &full[s], 0, static_cast<int32_t>(tile * kHRows));
+        }
       }
     }
     return;
@@ -150,9 +155,17 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
       for (int k = 0; k < CPT / 8; ++k) {
         const uint4 raw = *reinterpret_cast<const uint4*>(st + i * kPlaneBox + hoff<C>(r, (CPT / 8) * hf + k));
         const uint32_t* hv = reinterpret_cast<const uint32_t*>(&raw);
+        uint4 rawl = make_uint4(0, 0, 0, 0);
+        if (spl) rawl = *reinterpret_cast<const uint4*>(st + (NS + i) * kPlaneBox + hoff<C>(r, (CPT / 8) * hf + k));
+        const uint32_t* lv = reinterpret_cast<const uint32_t*>(&rawl);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float2 f = unpack2r(L.fp16 != 0, hv[e]);
+          float2 f = unpack2r(L.fp16 != 0, hv[e]);
+          if (spl) {  // hi + lo: exact in fp32
+            const float2 g = unpack2r(L.fp16 != 0, lv[e]);
+            f.x += g.x;
+            f.y += g.y;
+          }
           const int c = 8 * k + 2 * e;
           if (i == 0) {
             acc[c] = f.x;
@@ -337,36 +350,41 @@ const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const
   L.geo = geo;
   L.ns = ns;
   L.nb = nb;
+  L.split = prog.split;
+  const int rs = prog.split ? 2 : 1;  // row stride in C-channel units (split rows: [hi C | lo C])
   for (int i = 0; i < ns; ++i) {
     L.op[i] = ops[i];
     L.relu[i] = relus[i];
     L.aff_s[i] = affs[i] >= 0 ? prog.aff_s[affs[i]] : nullptr;
     L.aff_t[i] = affs[i] >= 0 ? prog.aff_t[affs[i]] : nullptr;
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(geo.Nalloc)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(C * 2)};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(C), static_cast<cuuint32_t>(kHRows)};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = encode_fn_head()(&L.maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                                  const_cast<__nv_bfloat16*>(prog.planes[i]), dims, strides, box, es,
-                                  CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                  C == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    for (int part = 0; part < rs; ++part) {
+      cuuint64_t dims[2] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(geo.Nalloc)};
+      cuuint64_t strides[1] = {static_cast<cuuint64_t>(rs * C * 2)};
+      cuuint32_t box[2] = {static_cast<cuuint32_t>(C), static_cast<cuuint32_t>(kHRows)};
+      cuuint32_t es[2] = {1, 1};
+      CUresult r = encode_fn_head()(part == 0 ? &L.maps[i] : &L.lo_maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                    const_cast<__nv_bfloat16*>(prog.planes[i]) + part * C, dims, strides, box, es,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    C == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    }
   }
   L.head_w = prog.head_w;
   L.head_b = prog.head_b;
   L.llr = prog.llr;
   L.fp16 = prog.fp16;
-  L.tc_head = prog.tc_head && !prog.fp16;
+  L.tc_head = prog.tc_head && !prog.fp16 && !prog.split;
   const bool tc = C == 64 && L.tc_head;
+  const int nsb = rs * ns;  // operand boxes per tile
   // CNRX_HEAD_STAGES (experiments): ring depth; deeper rings fit one CTA per SM instead of two
   static const int want = std::getenv("CNRX_HEAD_STAGES") ? std::atoi(std::getenv("CNRX_HEAD_STAGES")) : 0;
   int stages = want >= 2 ? want : 3;
   if (want < 2)
-    while (stages > 2 && head_layout(C, ns, nb, stages, tc).total > 113u * 1024u) --stages;
-  while (stages > 2 && head_layout(C, ns, nb, stages, tc).total > 227u * 1024u) --stages;
+    while (stages > 2 && head_layout(C, nsb, nb, stages, tc).total > 113u * 1024u) --stages;
+  while (stages > 2 && head_layout(C, nsb, nb, stages, tc).total > 227u * 1024u) --stages;
   L.stages = stages;
-  const int total = static_cast<int>(head_layout(C, ns, nb, stages, tc).total);
+  const int total = static_cast<int>(head_layout(C, nsb, nb, stages, tc).total);
   if (total > 227 * 1024) return nullptr;
   bool ok = false;
   switch (C) {

@@ -22,6 +22,8 @@ struct HeadLaunch {
   int32_t ns, nb, stages;
   int32_t fp16;                        // operand planes are fp16 (else bf16)
   int32_t tc_head;                     // C == 64: GEMV on the tensor core over bf16-rounded z
+  int32_t split;                       // split planes (CNRX_*X3 plans): operand i = hi (maps[i]) + lo (lo_maps[i])
+  CUtensorMap lo_maps[kHeadMaxPlanes];
 };
 
 // Launch the fold program (ns steps, ops/affs/relus as pw_as_fold returns them) + head GEMV when it

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) pw_program_kernel(const __grid_constant__
 // The head GEMV partial sums are reduced across the row's lanes with shuffles.
 // SPLIT (CNRX_*X3 plans): rows are [hi C | lo C]; a lane loads its 8-channel slice of both halves (each
 // warp instruction still covers whole 128-byte lines) and stores the result split the same way.
-template <int HEAD, int LPR, bool SPLIT = false>
+template <int HEAD, int LPR, bool SPLIT = false, int NPMAX = kPwMaxPlanes>
 __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ PwProgram prog, PlaneGeom geo) {
   extern __shared__ float smem_f[];
   const int C = prog.C, NB = prog.head_bits;
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
   }
   __syncthreads();
   constexpr int RPW = 32 / LPR;  // rows per warp pass
-  constexpr int U = SPLIT ? 1 : 2;  // row groups per iteration (loads of both issued before compute)
+  constexpr int U = 2;  // row groups per iteration (loads of both issued before compute)
   const int64_t RS = SPLIT ? 2 * C : C;  // row stride (16-bit values)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cg = lane % LPR;
@@ -177,15 +177,15 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
   for (int64_t grp0 = (static_cast<int64_t>(blockIdx.x) * 8 + warp) * U; grp0 < groups; grp0 += wstride * U) {
     int64_t row[U];
     bool in_range[U], valid[U];
-    uint4 raw[U][kPwMaxPlanes];
-    uint4 rawl[U][SPLIT ? kPwMaxPlanes : 1];
+    uint4 raw[U][NPMAX];
+    uint4 rawl[U][SPLIT ? NPMAX : 1];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       row[u] = (grp0 + u) * RPW + lane / LPR;
       in_range[u] = row[u] < geo.Nalloc;
       valid[u] = in_range[u] && geo.valid(row[u]);
 #pragma unroll
-      for (int k = 0; k < kPwMaxPlanes; ++k)
+      for (int k = 0; k < NPMAX; ++k)
         if (k < np) {
           raw[u][k] = valid[u] ? *reinterpret_cast<const uint4*>(prog.planes[k] + row[u] * RS + c0)
                                : make_uint4(0, 0, 0, 0);
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
         if (ins.op == PW_LOAD || ins.op == PW_MUL || ins.op == PW_ADD) {
           uint4 r4 = raw[u][0];
 #pragma unroll
-          for (int k = 1; k < kPwMaxPlanes; ++k)
+          for (int k = 1; k < NPMAX; ++k)
             if (k == ins.k) r4 = raw[u][k];
           const uint32_t* h = reinterpret_cast<const uint32_t*>(&r4);
           float v[8];
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) pw_rows_kernel(const __grid_constant__ Pw
           if constexpr (SPLIT) {
             uint4 l4 = rawl[u][0];
 #pragma unroll
-            for (int k = 1; k < kPwMaxPlanes; ++k)
+            for (int k = 1; k < NPMAX; ++k)
               if (k == ins.k) l4 = rawl[u][k];
             const uint32_t* hl = reinterpret_cast<const uint32_t*>(&l4);
 #pragma unroll
@@ -582,7 +582,7 @@ bool pw_as_fold(const PwProgram& prog, int* nsteps, int* ops, int* affs, int* re
   return ns > 0;
 }
 
-template <int HEAD, int LPR, bool SPLIT = false>
+template <int HEAD, int LPR, bool SPLIT = false, int NPMAX = kPwMaxPlanes>
 static void launch_rows(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s) {
   int n_aff = 0;
   for (int n = 0; n < prog.n_ins; ++n)
@@ -595,7 +595,7 @@ static void launch_rows(const PwProgram& prog, const PlaneGeom& geo, cudaStream_
   const int64_t groups = (geo.Nalloc + (32 / LPR) - 1) / (32 / LPR);
   const int64_t want = (groups + 15) / 16;
   const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(sms) * 8));
-  pw_rows_kernel<HEAD, LPR, SPLIT><<<blocks, 256, smem, s>>>(prog, geo);
+  pw_rows_kernel<HEAD, LPR, SPLIT, NPMAX><<<blocks, 256, smem, s>>>(prog, geo);
   CNRX_CUDA(cudaGetLastError());
 }
 
@@ -603,12 +603,22 @@ const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaS
   if (prog.head_bits > 0) require(prog.head_bits <= kPwMaxBits, "head with more than 16 outputs");
   require(prog.out2_plane == nullptr || prog.head_bits == 0, "second output needs a plane program");
   const bool head = prog.head_bits > 0;
-  if (prog.split && !prog.out2_plane && (prog.C == 16 || prog.C == 32 || prog.C == 64)) {
-    // split planes, coalesced: a row's lanes read their slices of both halves
+  if (prog.split && head) {  // split planes: the TMA-streamed head kernel reads hi + lo tiles when it fits
+    FoldSteps fs{};
+    int ns = 0;
+    if (pw_as_fold(prog, &ns, fs.op, fs.aff, fs.relu) && prog.n_planes_used == ns) {
+      const char* name = launch_head_tma(prog, ns, fs.op, fs.aff, fs.relu, geo, s);
+      if (name) return "head_tma_kernel<x3>";
+    }
+  }
+  if (prog.split && !prog.out2_plane && prog.n_planes_used <= 4 && (prog.C == 16 || prog.C == 32 || prog.C == 64) &&
+      !head) {
+    // split planes, coalesced: a row's lanes read their slices of both halves (<= 4 operand planes: the
+    // register arrays are sized for them)
     switch (prog.C) {
-      case 16: head ? launch_rows<1, 2, true>(prog, geo, s) : launch_rows<0, 2, true>(prog, geo, s); break;
-      case 32: head ? launch_rows<1, 4, true>(prog, geo, s) : launch_rows<0, 4, true>(prog, geo, s); break;
-      default: head ? launch_rows<1, 8, true>(prog, geo, s) : launch_rows<0, 8, true>(prog, geo, s); break;
+      case 16: head ? launch_rows<1, 2, true, 4>(prog, geo, s) : launch_rows<0, 2, true, 4>(prog, geo, s); break;
+      case 32: head ? launch_rows<1, 4, true, 4>(prog, geo, s) : launch_rows<0, 4, true, 4>(prog, geo, s); break;
+      default: head ? launch_rows<1, 8, true, 4>(prog, geo, s) : launch_rows<0, 8, true, 4>(prog, geo, s); break;
     }
     return head ? "pw_rows_kernel<head,x3>" : "pw_rows_kernel<plane,x3>";
   }

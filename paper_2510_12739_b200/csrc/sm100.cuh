@@ -249,6 +249,22 @@ __device__ __forceinline__ void umma_f16_ts_lohi(uint32_t d_tmem, uint32_t a_tme
       : "memory");
 }
 
+// SS form with both descriptors given as 32-bit halves: the low word of a K-major smem descriptor is
+// (address >> 4) | (1 << 16), so an issuer walking a window keeps one 32-bit base per operand and adds
+// (row * row_bytes + k_bytes) / 16 per UMMA -- one IADD instead of rebuilding a 64-bit descriptor.
+__device__ __forceinline__ uint32_t sdesc_hi(uint32_t sbo, uint32_t swizzle) {
+  return ((sbo >> 4) & 0x3FFFu) | (1u << 14) | ((swizzle & 7u) << 29);
+}
+__device__ __forceinline__ uint32_t sdesc_lo(uint32_t addr) { return ((addr >> 4) & 0x3FFFu) | (1u << 16); }
+__device__ __forceinline__ void umma_ss_lohi(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .b64 ad, bd;\n setp.ne.b32 p, %6, 0;\n mov.b64 ad, {%1, %2};\n mov.b64 bd, {%3, %4};\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %5, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // registers -> TMEM: 32 lanes x 32 bit, 8 consecutive columns (lane quadrant fixed by warp % 4).
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
