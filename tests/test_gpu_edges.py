@@ -26,8 +26,11 @@ def test_empty_and_degenerate_shapes_are_rejected_like_the_reference(prec):
     assert y.shape == (1, 14, 72, 2) and np.isfinite(y).all()
 
 
-def test_batch_beyond_one_plane_is_an_error_and_the_plan_recovers():
+def test_batch_beyond_one_plane_is_an_error_and_the_plan_recovers(monkeypatch):
+    """Batches whose workspace exceeds the plan's memory budget run in slot chunks (test_gpu_x3.py); with the
+    budget lifted, a chunk beyond 2^31 plane rows is rejected before any allocation or access."""
     import torch
+    monkeypatch.setenv("CNRX_MEM_BUDGET_MB", "1e12")
     g = G.CONFIGS["cfg2"].graph()
     p = P.Plan(g, "bf16")
     x = torch.zeros((1, 14, 612, 12), dtype=torch.float32, device="cuda")
