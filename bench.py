@@ -316,10 +316,15 @@ class Leg:
         top_flops = [f for n, f in zip(names, fl) if n == top_name]
         res = self.B * self.link.T * self.link.F
         avg_ms = top_ms / top_cnt
-        achieved = float(np.mean(top_flops)) * res / (avg_ms * 1e-3) / 1e12 if top_flops and np.mean(top_flops) > 0 else None
+        # algorithmic work of the kernel per step / its device time per step.  `top_flops` lists the
+        # kernel's launches in one pass of the program; batches beyond the plan's memory budget run the
+        # program once per slot chunk (launches_per_step > len(top_flops)) over the same REs in total.
+        work = float(np.sum(top_flops)) * res if top_flops else 0.0
+        achieved = work / (top_ms / steps * 1e-3) / 1e12 if work > 0 else None
         out = {"kernel": top_name, "avg_launch_ms": avg_ms, "launches_per_step": top_cnt // steps,
                "share_of_step": top_ms / sum(v[0] for v in agg.values()),
-               "algorithmic_tflop_per_launch": float(np.mean(top_flops)) * res / 1e12 if top_flops else None}
+               "algorithmic_tflop_per_launch": work / (top_cnt // steps) / 1e12 if top_flops else None,
+               "slot_chunks": max(1, (top_cnt // steps) // max(1, len(top_flops)))}
         if bound == "ffma":  # fp32 CUDA-core plans: nominal FP32 FMA peak at the sampled SM clock
             mhz = (clocks or {}).get("sm_mhz") or pk["sm_max_mhz"]
             peak = SM_COUNT * 128 * 2 * mhz * 1e6 / 1e12
