@@ -298,15 +298,19 @@ __global__ void __launch_bounds__(EPI ? kThreadsFold : kThreads, 1) conv_blk64_k
     const int q = warp & 3;
     const int set = (warp - 2) >> 2;
     const uint32_t* src = (set == 0 ? grp.wimg1 : grp.wimg2) + static_cast<size_t>(q * 32 + lane) * 8;
+    // one 32-byte load per lane (a warp reads 1 KB contiguous: full sectors); kWB blocks' loads in flight
+    // before their TMEM stores -- one dependent load -> store round trip per block was ~3.5 us of
+    // prologue per launch, most of a small batch's block kernel (B = 1: 19 us per launch, 6 us of MMAs)
+    constexpr int kWB = 6;
+    static_assert((kPairs * kKSteps) % kWB == 0, "weight blocks per batch");
 #pragma unroll 1
-    for (int b = 0; b < kPairs * kKSteps; ++b) {
-      uint32_t r[8];
-      // one 32-byte load per lane (a warp reads 1 KB contiguous): full sectors, where two 16-byte loads
-      // at a 32-byte lane stride used half of every sector each (ncu: "excessive global sectors")
-      const u32x8 w8 = ldg256(src + static_cast<size_t>(b) * 128 * 8);
+    for (int b0 = 0; b0 < kPairs * kKSteps; b0 += kWB) {
+      u32x8 w8[kWB];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) r[k] = w8.v[k];
-      tmem_st8(tbase + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(set * kWCols + b * 8), r);
+      for (int i = 0; i < kWB; ++i) w8[i] = ldg256(src + static_cast<size_t>(b0 + i) * 128 * 8);
+#pragma unroll
+      for (int i = 0; i < kWB; ++i)
+        tmem_st8(tbase + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(set * kWCols + (b0 + i) * 8), w8[i].v);
     }
     tmem_st_wait();
   }
