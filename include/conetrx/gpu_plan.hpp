@@ -29,7 +29,8 @@ namespace conetrx {
 
 class GpuPlan {
  public:
-  enum class Precision { fp32 = CNRX_FP32, bf16 = CNRX_BF16, fp16 = CNRX_FP16 };
+  // bf16x3 / fp16x3: split-precision tensor-core plans, LLRs within 1e-4 relative of the fp32 forward
+  enum class Precision { fp32 = CNRX_FP32, bf16 = CNRX_BF16, fp16 = CNRX_FP16, bf16x3 = CNRX_BF16X3, fp16x3 = CNRX_FP16X3 };
 
   // output_node: the index the network's set_output() named; -1 = recover it (see below).
   GpuPlan(Network<float>& net, Precision precision, int device = 0, int output_node = -1) {
