@@ -490,9 +490,18 @@ def main():
     from paper_2510_12739_b200 import plan as P, slots
 
     rank, local, world = dist_env()
+    # flow test of the multi-rank path on a one-GPU box only (never a measurement): every rank on cuda:0,
+    # gloo plumbing (NCCL refuses two ranks on one GPU)
+    share = os.environ.get("CNRX_BENCH_SHARE_GPU") == "1"
+    backend = "gloo" if share else "nccl"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -501,7 +510,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -571,7 +580,10 @@ def main():
             def e2e_step():
                 y_dev.copy_(y_host, non_blocking=True)
                 plan.receive_device(y_dev, out_dev, torch.cuda.current_stream().cuda_stream)
-                full = shard.gather_llr_tensor(out_dev, world * B, world, rank)
+                if backend == "nccl":
+                    full = shard.gather_llr_tensor(out_dev, world * B, world, rank)
+                else:  # flow test (CNRX_BENCH_SHARE_GPU): gloo gathers host tensors
+                    full = shard.gather_llr_tensor(out_dev.cpu(), world * B, world, rank)
                 if rank == 0:
                     out_host.copy_(full, non_blocking=True)
                 torch.cuda.synchronize()
@@ -590,7 +602,7 @@ def main():
         e2e = {"value": global_batch * e2e_steps / e2e_s, "unit": "slots/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "api": how, "steps": e2e_steps}
         if world > 1:
-            e2e["nccl_ranks"] = dist.get_world_size()
+            e2e["nccl_ranks" if backend == "nccl" else "gloo_ranks_flow_test"] = dist.get_world_size()
         plan.close()
 
     lat = None
