@@ -475,6 +475,9 @@ def main():
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling runs only)")
     ap.add_argument("--no-extra", action="store_true", help="skip extra_configs / precision variants")
+    ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
+                    help="N > 1 e2e: LLRs stored into rank 0's buffer by each rank's head kernel over NVLink "
+                         "(peer, default) or an NCCL gather after the forward")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -568,6 +571,27 @@ def main():
                 plan.receive_host_ptr(y_host.data_ptr(), batch.y.shape, out_host.data_ptr())
             h2d, d2h = batch.y.nbytes, out_host.numel() * 4
             how = "cnrx_receive (C ABI, pinned host buffers, batch pipelined in chunks over two copy streams)"
+        elif args.gather == "peer":
+            # the final gather fused into the LLR head: rank 0's batch buffer is mapped into every rank (CUDA
+            # IPC) and each rank's head kernel stores its slots straight into it over NVLink; completion =
+            # stream sync + host barrier; rank 0 then reads the whole batch (one D2H)
+            from paper_2510_12739_b200 import shard
+            y_dev = torch.empty((B, link.T, link.F, link.N), dtype=torch.complex64, device="cuda")
+            peer = shard.PeerLLR(world * B, (link.T, link.F, nb), rank, local)
+            dst = peer.dst(rank * B)
+            out_host = torch.empty((world * B, link.T, link.F, nb), dtype=torch.float32).pin_memory() if rank == 0 else None
+
+            def e2e_step():
+                y_dev.copy_(y_host, non_blocking=True)
+                plan.receive_device_ptr(y_dev, dst, torch.cuda.current_stream().cuda_stream)
+                torch.cuda.synchronize()
+                barrier()
+                if rank == 0:
+                    peer.to_host(out_host)
+            h2d, d2h = batch.y.nbytes * world, world * B * link.T * link.F * nb * 4
+            how = ("per rank: H2D + cnrx_receive_device whose LLR head stores its slots into rank 0's buffer over "
+                   "NVLink (CUDA IPC peer memory: the gather fused into the last kernel, no collective); stream "
+                   "sync + barrier; rank 0 D2H of the whole batch")
         else:
             # every rank: H2D of its slots, receive on its GPU; NCCL gather of the LLRs to rank 0's GPU
             # (shard.gather_llr_tensor, covered by the 2-rank gloo test); rank 0: one D2H of the whole
@@ -603,6 +627,18 @@ def main():
                "d2h_bytes_per_step": int(d2h), "api": how, "steps": e2e_steps}
         if world > 1:
             e2e["nccl_ranks" if backend == "nccl" else "gloo_ranks_flow_test"] = dist.get_world_size()
+            e2e["gather"] = args.gather
+            if args.gather == "peer":
+                # the peer-written batch equals the ranks' own LLRs gathered by the process group
+                mine = torch.empty((B, link.T, link.F, nb), dtype=torch.float32, device="cuda")
+                plan.receive_device(y_dev, mine, torch.cuda.current_stream().cuda_stream)
+                torch.cuda.synchronize()
+                from paper_2510_12739_b200 import shard as _sh
+                ref = _sh.gather_llr_tensor(mine if backend == "nccl" else mine.cpu(), world * B, world, rank)
+                if rank == 0:
+                    e2e["peer_gather_bit_exact"] = bool(torch.equal(ref.cpu(), out_host))
+                barrier()
+                peer.close()
         plan.close()
 
     lat = None

@@ -248,6 +248,22 @@ int cnrx_classical_receive(cnrx_plan* plan, const float* y_dev, const float* h_d
                            int64_t B, int64_t T, int64_t F, int64_t N, int32_t mod_order, float* llr_dev,
                            void* stream);
 
+/* Peer-memory LLR gather (one process per GPU, the final LLR gather fused into the last
+ * kernel).  Rank 0 allocates the whole batch's LLR buffer with cnrx_ipc_alloc and shares the 64-byte
+ * CUDA IPC handle; every rank opens it (cnrx_ipc_open) and passes base + (its first slot) * T*F*bits as
+ * the llr_dev of cnrx_receive_device / cnrx_forward_device: the LLR head's stores then land directly in
+ * rank 0's HBM over NVLink -- no gather collective, no staging copy.  Completion: each rank synchronizes
+ * its stream, then a host barrier; rank 0 then owns the full batch. */
+typedef struct {
+  uint8_t bytes[64];
+} cnrx_ipc_handle;
+int cnrx_ipc_alloc(int32_t device, int64_t bytes, void** ptr_out, cnrx_ipc_handle* handle_out);
+int cnrx_ipc_open(int32_t device, const cnrx_ipc_handle* handle, void** ptr_out);
+int cnrx_ipc_close(int32_t device, void* opened_ptr);
+int cnrx_ipc_free(int32_t device, void* allocated_ptr);
+/* Synchronous copy of `bytes` from a (local or opened) device buffer to host memory. */
+int cnrx_ipc_read(int32_t device, const void* src, void* host_dst, int64_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

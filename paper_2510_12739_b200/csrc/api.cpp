@@ -2472,4 +2472,56 @@ const char* cnrx_launch_name(const cnrx_plan* plan, int32_t i) {
   return plan->launch_names[static_cast<size_t>(i)].c_str();
 }
 
+int cnrx_ipc_alloc(int32_t device, int64_t bytes, void** ptr_out, cnrx_ipc_handle* handle_out) {
+  if (!ptr_out || !handle_out || bytes <= 0) return fail(CNRX_ERR_INVALID_ARGUMENT, "bad argument");
+  return guarded([&] {
+    static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(cnrx_ipc_handle), "CUDA IPC handle size");
+    DeviceGuard dg(device);
+    void* p = nullptr;
+    CNRX_CUDA(cudaMalloc(&p, static_cast<size_t>(bytes)));  // its own allocation: the handle maps it from offset 0
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      throw Error(CNRX_ERR_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+    }
+    std::memcpy(handle_out->bytes, &h, sizeof h);
+    *ptr_out = p;
+  });
+}
+
+int cnrx_ipc_open(int32_t device, const cnrx_ipc_handle* handle, void** ptr_out) {
+  if (!handle || !ptr_out) return fail(CNRX_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle->bytes, sizeof h);
+    void* p = nullptr;
+    CNRX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    *ptr_out = p;
+  });
+}
+
+int cnrx_ipc_close(int32_t device, void* opened_ptr) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    CNRX_CUDA(cudaIpcCloseMemHandle(opened_ptr));
+  });
+}
+
+int cnrx_ipc_read(int32_t device, const void* src, void* host_dst, int64_t bytes) {
+  if (!src || !host_dst || bytes < 0) return fail(CNRX_ERR_INVALID_ARGUMENT, "bad argument");
+  return guarded([&] {
+    DeviceGuard dg(device);
+    CNRX_CUDA(cudaMemcpy(host_dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost));
+  });
+}
+
+int cnrx_ipc_free(int32_t device, void* allocated_ptr) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    CNRX_CUDA(cudaFree(allocated_ptr));
+  });
+}
+
 }  // extern "C"

@@ -99,7 +99,8 @@ EXPORTED = ["cnrx_plan_create", "cnrx_plan_create_ex", "cnrx_plan_options_defaul
             "cnrx_set_pilots", "cnrx_receive", "cnrx_receive_device", "cnrx_featurize_device",
             "cnrx_receive_sharded", "cnrx_forward_sharded", "cnrx_get_plan_info", "cnrx_set_graph_capture", "cnrx_launch_name",
             "cnrx_set_profiling", "cnrx_read_profile", "cnrx_launch_flops", "cnrx_generate_slots",
-            "cnrx_count_bit_errors", "cnrx_slot_noise_var", "cnrx_classical_receive"]
+            "cnrx_count_bit_errors", "cnrx_slot_noise_var", "cnrx_classical_receive", "cnrx_ipc_alloc", "cnrx_ipc_open",
+            "cnrx_ipc_close", "cnrx_ipc_free", "cnrx_ipc_read"]
 
 
 def lib():
@@ -129,6 +130,11 @@ def lib():
     L.cnrx_set_pilots.argtypes = [vp, i64, i64, f32p, C.POINTER(C.c_uint8)]
     L.cnrx_receive.argtypes = [vp, f32p, i64, i64, i64, i64, f32p]
     L.cnrx_receive_device.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp]
+    L.cnrx_ipc_alloc.argtypes = [C.c_int32, i64, C.POINTER(vp), C.c_void_p]
+    L.cnrx_ipc_open.argtypes = [C.c_int32, C.c_void_p, C.POINTER(vp)]
+    L.cnrx_ipc_close.argtypes = [C.c_int32, vp]
+    L.cnrx_ipc_free.argtypes = [C.c_int32, vp]
+    L.cnrx_ipc_read.argtypes = [C.c_int32, vp, vp, i64]
     L.cnrx_featurize_device.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp]
     L.cnrx_receive_sharded.argtypes = [C.POINTER(vp), C.c_int32, f32p, i64, i64, i64, i64, f32p]
     L.cnrx_forward_sharded.argtypes = [C.POINTER(vp), C.c_int32, f32p, i64, i64, i64, i64, C.c_int32, f32p]
@@ -278,6 +284,13 @@ class Plan:
         B, T, F, N = y.shape[:4]
         _check(lib().cnrx_receive_device(self.h, C.c_void_p(y.data_ptr()), B, T, F, N,
                                          C.c_void_p(out.data_ptr()), _stream(stream)))
+
+    def receive_device_ptr(self, y, out_ptr: int, stream: Optional[int] = None) -> None:
+        """receive_device with a raw LLR destination (e.g. a slice of a peer GPU's buffer opened with
+        ipc_open: the head kernel's stores then go over NVLink)."""
+        B, T, F, N = y.shape[:4]
+        _check(lib().cnrx_receive_device(self.h, C.c_void_p(y.data_ptr()), B, T, F, N, C.c_void_p(out_ptr),
+                                         _stream(stream)))
 
     def feature_plane(self, y) -> np.ndarray:
         """Test hook: the 16-bit input-feature plane of a bf16 / fp16 plan for y (torch complex64 CUDA
@@ -434,3 +447,32 @@ def classical_receive_device(plan: "Plan", y, noise_var, mod_order: int, h=None,
                                         h.contiguous().data_ptr() if h is not None else None, nv.data_ptr(), B, T, F, N,
                                         mod_order, out.data_ptr(), _stream(st)))
     return out
+
+
+# ---- peer-memory LLR gather (include/conetrx_cuda.h cnrx_ipc_*) -------------------------------------------
+def ipc_alloc(device: int, nbytes: int):
+    """Allocate `nbytes` on `device` and export it: returns (device pointer, 64-byte handle)."""
+    ptr = C.c_void_p()
+    h = (C.c_uint8 * 64)()
+    _check(lib().cnrx_ipc_alloc(device, nbytes, C.byref(ptr), C.cast(h, C.c_void_p)))
+    return ptr.value, bytes(h)
+
+
+def ipc_open(device: int, handle: bytes) -> int:
+    """Map another process's exported allocation into this process (peer access enabled lazily)."""
+    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    ptr = C.c_void_p()
+    _check(lib().cnrx_ipc_open(device, C.cast(h, C.c_void_p), C.byref(ptr)))
+    return ptr.value
+
+
+def ipc_close(device: int, ptr: int) -> None:
+    _check(lib().cnrx_ipc_close(device, C.c_void_p(ptr)))
+
+
+def ipc_read(device: int, ptr: int, host_ptr: int, nbytes: int) -> None:
+    _check(lib().cnrx_ipc_read(device, C.c_void_p(ptr), C.c_void_p(host_ptr), nbytes))
+
+
+def ipc_free(device: int, ptr: int) -> None:
+    _check(lib().cnrx_ipc_free(device, C.c_void_p(ptr)))

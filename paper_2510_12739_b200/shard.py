@@ -4,7 +4,9 @@ data-path collective.  The only exchange is the final LLR gather.
 
 `slot_range` is the partition both bench.py (one process per GPU under torchrun) and
 cnrx_receive_sharded (one process, several GPUs; api.cpp) use.  `gather_llr` collects per-rank LLR
-slices on rank 0 over torch.distributed (NCCL on the GPU box, gloo in the CPU tests).
+slices on rank 0 over torch.distributed (NCCL on the GPU box, gloo in the CPU tests).  `PeerLLR` fuses
+the gather into the last kernel instead: rank 0's LLR buffer is mapped into every rank (CUDA IPC), and
+each rank's LLR head stores its slots straight into it over NVLink.
 """
 from __future__ import annotations
 
@@ -60,3 +62,41 @@ def gather_llr(local: np.ndarray, B: int, world: int, rank: int):
         return None
     full = np.concatenate([p.cpu().numpy() for p in parts], 0)
     return full[:B]
+
+
+class PeerLLR:
+    """The whole batch's LLR buffer on rank 0's GPU, mapped into every rank (cnrx_ipc_alloc / _open):
+    rank r passes `dst(b0)` (its first slot) as the LLR destination of receive_device_ptr, so the head
+    kernel's stores land in rank 0's HBM over NVLink -- the final gather fused into the last kernel, no
+    collective on the data path.  Completion protocol: every rank synchronizes its stream, then a
+    host barrier (torch.distributed); rank 0 then reads the full batch (`to_host`).  The 64-byte handle
+    travels once, at setup, with broadcast_object_list."""
+
+    def __init__(self, B: int, row_shape, rank: int, device: int):
+        import torch.distributed as dist
+        from paper_2510_12739_b200 import plan as P
+        self.rank, self.device = rank, device
+        self.slot_bytes = 4 * int(np.prod(row_shape))
+        self.B = B
+        obj = [None]
+        if rank == 0:
+            self.ptr, handle = P.ipc_alloc(device, B * self.slot_bytes)
+            obj = [handle]
+        dist.broadcast_object_list(obj, src=0)
+        if rank != 0:
+            self.ptr = P.ipc_open(device, obj[0])
+
+    def dst(self, b0: int) -> int:
+        return self.ptr + b0 * self.slot_bytes
+
+    def to_host(self, out) -> None:
+        """rank 0: copy the full batch into `out` (a pinned torch tensor of B * slot_bytes bytes)."""
+        from paper_2510_12739_b200 import plan as P
+        P.ipc_read(self.device, self.ptr, out.data_ptr(), self.B * self.slot_bytes)
+
+    def close(self) -> None:
+        from paper_2510_12739_b200 import plan as P
+        if self.rank == 0:
+            P.ipc_free(self.device, self.ptr)
+        else:
+            P.ipc_close(self.device, self.ptr)
