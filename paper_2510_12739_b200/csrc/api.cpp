@@ -1324,7 +1324,6 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
         L.win_alloc = win_alloc;
         if (!conv_x3_config(op0.cin, op0.cout, op0.ks, win_alloc, &L.stages, &L.nslots))
           throw Error(CNRX_ERR_UNSUPPORTED, "split-precision conv working set exceeds shared memory");
-        if (const char* d = std::getenv("CNRX_X3_DBG")) L.dbg = std::atoi(d);  // A/B experiments only
       } else {
         TcLaunch& L = GL.tc;
         std::memset(&L, 0, sizeof(L));

@@ -243,15 +243,8 @@ __global__ void __launch_bounds__(threads_of(COUT), 1) conv_x3_kernel(const __gr
       for (int64_t tile = local; tile < n_tiles; tile += nct, ++j) {
         const int s = j % S;
         const long long tw0 = L.trace ? clock64() : 0;
-        if (L.dbg & 1)
-          mbar_wait(&empty[s], (static_cast<uint32_t>(j / S) & 1u) ^ 1u);
-        else
-          mbar_wait_backoff<64>(&empty[s], (static_cast<uint32_t>(j / S) & 1u) ^ 1u);
+        mbar_wait_backoff<64>(&empty[s], (static_cast<uint32_t>(j / S) & 1u) ^ 1u);
         if (L.trace) tr_prod += clock64() - tw0;
-        if (L.dbg & 16) {  // A/B: no window loads
-          mbar_arrive(&full[s]);
-          continue;
-        }
         mbar_arrive_expect_tx(&full[s], stage_tx);
         uint8_t* win = smem + lay.win_off + s * lay.stage_bytes;
         const int32_t r0 = static_cast<int32_t>(tile * 128 - grp.halo);
@@ -388,8 +381,8 @@ __global__ void __launch_bounds__(threads_of(COUT), 1) conv_x3_kernel(const __gr
       const long long te0 = L.trace ? clock64() : 0;
       const int64_t p = tile * 128 + row;
       const __nv_bfloat16* rrow = grp.res ? grp.res + p * (2 * COUT) : nullptr;
-      __nv_bfloat16* orow = grp.out && !(L.dbg & 8) ? grp.out + p * (2 * COUT) : nullptr;
-      __nv_bfloat16* orow2 = grp.out2 && !(L.dbg & 8) ? grp.out2 + p * (2 * COUT) : nullptr;
+      __nv_bfloat16* orow = grp.out ? grp.out + p * (2 * COUT) : nullptr;
+      __nv_bfloat16* orow2 = grp.out2 ? grp.out2 + p * (2 * COUT) : nullptr;
       // the residual slices are fetched before the accumulator wait: their latency hides behind the MMAs
       u32x8 rh[ECH / 16], rl[ECH / 16];
       if (rrow) {
@@ -400,10 +393,7 @@ __global__ void __launch_bounds__(threads_of(COUT), 1) conv_x3_kernel(const __gr
         }
       }
       const bool valid = geo.valid(p);
-      if (L.dbg & 1)
-        mbar_wait(&tfull[a], static_cast<uint32_t>(j >> 1) & 1u);
-      else
-        mbar_wait_backoff<128>(&tfull[a], static_cast<uint32_t>(j >> 1) & 1u);  // polls cost smem issue
+      mbar_wait_backoff<128>(&tfull[a], static_cast<uint32_t>(j >> 1) & 1u);  // polls cost smem issue
       tc_fence_after();
       const long long te1 = L.trace ? clock64() : 0;
       if (L.trace) tr_ew += te1 - te0;

@@ -39,9 +39,7 @@ struct X3Launch {
   int32_t win_alloc;   // rows per window stage (multiple of 32)
   int32_t nslots;      // weight-tap slots in shared memory; == taps: weights resident for the CTA's life
   int32_t fp16;        // 16-bit format: fp16 (else bf16)
-  int32_t dbg;         // A/B experiments only (env CNRX_X3_DBG): bit 0 poll back-off off, 8 no stores, 16 no loads
-  int32_t relu_in;     // the input is relu(plane): applied to each window pair in shared memory (ReLU warp)
-  int32_t pad_;
+  int32_t relu_in;     // the input is relu(plane): applied to each window pair in shared memory (ReLU warps)
   unsigned long long* trace;  // debug (CNRX_TRACE): per-role clock64 totals, conv_tc.h kTrace* indices
 };
 
