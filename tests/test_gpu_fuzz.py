@@ -1,0 +1,69 @@
+"""Randomised builder graphs (the reference's conet_template / deeprx_template, netspec.cpp:53-81, with
+random widths, depths, fusion ops and points, stem/head kernels, input channels and bit counts) through
+every plan precision, against the oracle on random inputs (seeded, so a failure reproduces):
+  * fp32: bit-exact;
+  * bf16x3 / fp16x3: rel L2 and max |d| / max |ref| <= 1e-4 (tests/test_gpu_x3.py's bar), and the split
+    plans lower every graph the bf16 plan lowers;
+  * bf16 / fp16: within the emulation bound of tests/test_gpu_parity.py (rel L2 <= 2e-2 / 5e-3).
+Graphs a 16-bit plan cannot express must be rejected loudly (CnrxUnsupported), never computed wrong."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+import emulate_bf16 as E
+from paper_2510_12739_b200 import graph as G, plan as P
+
+pytestmark = pytest.mark.gpu
+
+
+def _random_graph(seed):
+    r = np.random.default_rng(seed)
+    in_ch = int(r.choice([6, 12, 24]))
+    bits = int(r.choice([2, 4, 6]))
+    width = int(r.choice([32, 64, 96]))
+    kernel = int(r.choice([1, 1, 1, 3]))  # stem / head kernel (the 16-bit plans lower 1x1 heads only)
+    if r.random() < 0.25:
+        spec = dataclasses.replace(G.deeprx_template(width, int(r.integers(1, 4)), in_ch, bits), kernel=kernel)
+        g = G.build_net(spec)
+    else:
+        main = int(r.integers(1, 4))
+        sups = [int(x) for x in r.integers(1, 4, size=int(r.integers(1, 4)))]
+        op = str(r.choice(["mul", "add"]))
+        pts = sorted(set(int(x) for x in r.integers(0, main, size=int(r.integers(1, main + 1)))))
+        spec = G.conet_template(width, main, sups, op, "bn", False, in_ch, bits, kernel=kernel, fusion_points=pts)
+        g = G.build_conet(spec)
+    g.init_he_normal(seed, randomize_aux=True)
+    B, F = int(r.integers(1, 4)), int(r.integers(3, 40))
+    x = r.standard_normal((B, 14, F, in_ch)).astype(np.float32)
+    return g, x
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_random_builder_graphs_all_precisions(seed):
+    g, x = _random_graph(1000 + seed)
+    ref = oracle.forward(g, x)
+    assert np.array_equal(P.Plan(g, "fp32").forward(x), ref)
+    lowered = {}
+    for prec in ("bf16", "fp16", "bf16x3", "fp16x3"):
+        try:
+            lowered[prec] = P.Plan(g, prec).forward(x)
+        except P.CnrxUnsupported:
+            lowered[prec] = None
+    if lowered["bf16"] is not None:  # the split plans lower whatever the 16-bit plans lower
+        assert lowered["bf16x3"] is not None and lowered["fp16x3"] is not None
+    scale = np.abs(ref).max()
+    for prec in ("bf16x3", "fp16x3"):
+        got = lowered[prec]
+        if got is None:
+            continue
+        l2 = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        mx = np.abs(got - ref).max() / scale
+        assert l2 <= 1e-4 and mx <= 1e-4, (prec, l2, mx)
+    for prec, bound in (("bf16", 2e-2), ("fp16", 5e-3)):
+        got = lowered[prec]
+        if got is None:
+            continue
+        emu = E.emulate(g, x, precision=prec)
+        assert np.linalg.norm(got - emu) / np.linalg.norm(emu) <= bound, prec
