@@ -70,9 +70,19 @@ __host__ __device__ constexpr uint32_t a1024(uint32_t x) { return (x + 1023u) & 
 __host__ __device__ constexpr uint32_t tap_bytes(int cin, int cout) {
   return 2u * static_cast<uint32_t>(cout) * static_cast<uint32_t>(cin) * 2u;
 }
-// two accumulator stages of [D | E] = 2 * Cout columns each
+// UMMA issue order (A/B builds: -DCNRX_X3_ORDER=n): 0 interleaved per K-step into [D | E]; 1 (default) the lo
+// product into its own accumulator F (Cout <= 64: [D | E | F]; 96 channels have no TMEM for it and use 0);
+// 2 per tap all A_hi UMMAs, then all A_lo UMMAs; 3 the lo product accumulated into E.  Measured
+// (profiles/r02_x3_order_ab.log, cfg2 64-ch convs): 1 is 3-4 % faster than 0; 2 and 3 equal 0 -- UMMAs of
+// different N into the same accumulator columns do not overlap in the tensor pipe.
+#ifndef CNRX_X3_ORDER
+#define CNRX_X3_ORDER 1
+#endif
+__host__ __device__ constexpr int x3_order(int cout) { return CNRX_X3_ORDER == 1 && cout > 64 ? 0 : CNRX_X3_ORDER; }
+// accumulator stage width: [D | E] (+ F) = 2 (3) * Cout columns; two stages
+__host__ __device__ constexpr int acc_cols(int cout) { return (x3_order(cout) == 1 ? 3 : 2) * cout; }
 __host__ __device__ constexpr uint32_t tmem_cols(int cout) {
-  return 4 * cout <= 128 ? 128 : 4 * cout <= 256 ? 256 : 512;
+  return 2 * acc_cols(cout) <= 128 ? 128 : 2 * acc_cols(cout) <= 256 ? 256 : 512;
 }
 
 struct Lay {
@@ -296,7 +306,9 @@ __global__ void __launch_bounds__(threads_of(COUT), 1) conv_x3_kernel(const __gr
       const uint32_t wlo = sdesc_lo(smem_u32(smem + lay.win_off + s * lay.stage_bytes));
       const uint32_t ah0 = wlo + (lay.sub[0] >> 4), al0 = wlo + (lay.sub[2] >> 4);
       const uint32_t ah1 = wlo + (lay.sub[1] >> 4), al1 = wlo + (lay.sub[3] >> 4);
-      const uint32_t d_tmem = tbase + static_cast<uint32_t>(a * 2 * COUT);
+      const uint32_t d_tmem = tbase + static_cast<uint32_t>(a * acc_cols(COUT));
+      constexpr int ORD = x3_order(COUT);
+      const uint32_t f_tmem = ORD == 1 ? d_tmem + 2 * COUT : ORD == 3 ? d_tmem + COUT : d_tmem;  // A_lo * W_hi
 #pragma unroll
       for (int tap = 0; tap < TAPS; ++tap) {
         const uint32_t slot = resident ? static_cast<uint32_t>(tap) : wi % static_cast<uint32_t>(NS);
@@ -307,10 +319,20 @@ __global__ void __launch_bounds__(threads_of(COUT), 1) conv_x3_kernel(const __gr
         if (elect_one()) {
           const uint32_t wb = w_lo + slot * (TAPB >> 4);
           const uint32_t r0 = static_cast<uint32_t>(trow[tap] * (RB0 >> 4));
+          if (ORD == 2) {
 #pragma unroll
-          for (int kk = 0; kk < CH0 / 16; ++kk) {
-            umma_ss_lohi(d_tmem, ah0 + r0 + 2 * kk, dh0, wb + 2 * kk, dh0, IDESC2, (tap | kk) != 0 ? 1u : 0u);
-            umma_ss_lohi(d_tmem, al0 + r0 + 2 * kk, dh0, wb + 2 * kk, dh0, IDESC1, 1u);
+            for (int kk = 0; kk < CH0 / 16; ++kk)
+              umma_ss_lohi(d_tmem, ah0 + r0 + 2 * kk, dh0, wb + 2 * kk, dh0, IDESC2, (tap | kk) != 0 ? 1u : 0u);
+#pragma unroll
+            for (int kk = 0; kk < CH0 / 16; ++kk)
+              umma_ss_lohi(d_tmem, al0 + r0 + 2 * kk, dh0, wb + 2 * kk, dh0, IDESC1, 1u);
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < CH0 / 16; ++kk) {
+              umma_ss_lohi(d_tmem, ah0 + r0 + 2 * kk, dh0, wb + 2 * kk, dh0, IDESC2, (tap | kk) != 0 ? 1u : 0u);
+              umma_ss_lohi(f_tmem, al0 + r0 + 2 * kk, dh0, wb + 2 * kk, dh0, IDESC1,
+                           ORD == 1 && (tap | kk) == 0 ? 0u : 1u);
+            }
           }
           if (CH1) {
             const uint32_t r1 = static_cast<uint32_t>(trow[tap] * (RB1 >> 4));
@@ -318,7 +340,7 @@ __global__ void __launch_bounds__(threads_of(COUT), 1) conv_x3_kernel(const __gr
 #pragma unroll
             for (int kk = 0; kk < CH1 / 16; ++kk) {
               umma_ss_lohi(d_tmem, ah1 + r1 + 2 * kk, dh1, w1 + 2 * kk, dh1, IDESC2, 1u);
-              umma_ss_lohi(d_tmem, al1 + r1 + 2 * kk, dh1, w1 + 2 * kk, dh1, IDESC1, 1u);
+              umma_ss_lohi(f_tmem, al1 + r1 + 2 * kk, dh1, w1 + 2 * kk, dh1, IDESC1, 1u);
             }
           }
           if (!resident) umma_commit(&wempty[slot]);  // tap slot free once these MMAs have read it
@@ -397,12 +419,24 @@ __global__ void __launch_bounds__(threads_of(COUT), 1) conv_x3_kernel(const __gr
       tc_fence_after();
       const long long te1 = L.trace ? clock64() : 0;
       if (L.trace) tr_ew += te1 - te0;
-      const uint32_t taddr = tbase + static_cast<uint32_t>(a * 2 * COUT + cb) + (static_cast<uint32_t>(q * 32) << 16);
+      const uint32_t taddr = tbase + static_cast<uint32_t>(a * acc_cols(COUT) + cb) + (static_cast<uint32_t>(q * 32) << 16);
       uint32_t r[ECH], e[ECH];
 #pragma unroll
       for (int i = 0; i < ECH / 16; ++i) {
-        tmem_ld16(taddr + 16 * i, *reinterpret_cast<uint32_t(*)[16]>(&r[16 * i]));         // D: hi*Whi + lo*Whi
+        tmem_ld16(taddr + 16 * i, *reinterpret_cast<uint32_t(*)[16]>(&r[16 * i]));         // D: hi*Whi (+ lo*Whi)
         tmem_ld16(taddr + COUT + 16 * i, *reinterpret_cast<uint32_t(*)[16]>(&e[16 * i]));  // E: hi*Wlo
+      }
+      if constexpr (x3_order(COUT) == 1) {  // F: lo*Whi, folded into E
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < ECH / 16; ++i) {
+          uint32_t f[16];
+          tmem_ld16(taddr + 2 * COUT + 16 * i, f);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            e[16 * i + k] = __float_as_uint(__uint_as_float(e[16 * i + k]) + __uint_as_float(f[k]));
+        }
       }
       tmem_ld_wait();
       tc_fence_before();
