@@ -162,6 +162,7 @@ struct TcOp {
   // two-kernel program over the same planes stays available (chosen per batch size).
   int blk_c1 = -1;
   bool fused_away = false;
+  bool llr_head = false;  // the network's output conv (3x3 head): its epilogue writes the fp32 LLRs
   void* wimg = nullptr;
   float* bias = nullptr;
   float* s2 = nullptr;
@@ -981,12 +982,46 @@ struct Bf16Compiler {
       plane_producer_tc[static_cast<size_t>(op.out_plane)] = static_cast<int>(p.tc.size()) - 1;
       node_plane[static_cast<size_t>(end)] = op.out_plane;
     }
-    // output: 1x1 conv head over a linear pointwise chain
+    // output: 1x1 conv head over a linear pointwise chain (pointwise program / TMA head kernel), or a 3x3
+    // head (NetSpec.kernel = 3, network.hpp:559) as a tensor-core conv over the chain's plane whose epilogue
+    // writes the fp32 LLRs
     const cnrx_node& on = p.N(p.out_node);
     if (on.op != CNRX_OP_CONV) throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: output node must be a conv");
     const auto& hw = p.P(on.w);
+    if (hw.dims[0] == 3 && hw.dims[1] == 3 && on.out_channels <= 32) {
+      TcOp op;
+      op.node = p.out_node;
+      op.ks = 3;
+      op.dil = on.dilation_f;
+      op.llr_head = true;
+      op.in_plane = plane_for(on.in0);
+      op.cin = p.planes[static_cast<size_t>(op.in_plane)].C;
+      op.cout = round_cout(on.out_channels);
+      op.cin_real = static_cast<int>(hw.dims[2]);
+      op.cout_real = static_cast<int>(hw.dims[3]);
+      if (!(p.split ? conv_x3_supported(op.cin, op.cout, 3) : conv_tc_supported(op.cin, op.cout, 3)))
+        throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: no tcgen05 conv for the 3x3 head (cin=" + std::to_string(op.cin) + ")");
+      if (p.split) {
+        std::vector<uint8_t> img(conv_x3_wimg_bytes(op.cin, op.cout, 3));
+        conv_x3_pack_weights(hw.data.data(), 3, op.cin_real, op.cout_real, nullptr, op.cin, op.cout, p.fp16, img.data());
+        op.wimg = p.upload_bytes(img.data(), img.size());
+      } else {
+        std::vector<uint8_t> img(conv_tc_wimg_bytes(op.cin, op.cout, 3));
+        conv_tc_pack_weights(hw.data.data(), 3, op.cin_real, op.cout_real, nullptr, op.cin, op.cout, p.fp16, img.data());
+        op.wimg = p.upload_bytes(img.data(), img.size());
+      }
+      std::vector<float> hbias(static_cast<size_t>(op.cout), 0.f);
+      if (on.b >= 0)
+        for (int c = 0; c < on.out_channels; ++c) hbias[static_cast<size_t>(c)] = p.P(on.b).data[static_cast<size_t>(c)];
+      op.bias = p.upload(hbias);
+      op.level = p.planes[static_cast<size_t>(op.in_plane)].level + 1;
+      use(op.in_plane, op.level);
+      p.tc.push_back(op);
+      finish_schedule();
+      return;
+    }
     if (hw.dims[0] != 1 || hw.dims[1] != 1 || on.out_channels > kPwMaxBits)
-      throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: output conv must be 1x1 with <= 16 outputs");
+      throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: output conv must be 1x1 (or 3x3) with <= 16 outputs");
     PwStep st;
     std::vector<std::vector<float>> aff;
     int level = 0;
@@ -1009,6 +1044,11 @@ struct Bf16Compiler {
     st.prog.head_b = p.upload(hb);
     finish_pw(st, aff, C);
     p.pw.push_back(st);
+    finish_schedule();
+  }
+
+  // residual-block fusion, level schedule, launch groups, fused heads, buffer assignment
+  void finish_schedule() {
     fuse_blocks();
     // level schedule
     int maxl = 0;
@@ -1043,6 +1083,7 @@ struct Bf16Compiler {
         const TcOp& o0 = p.tc[static_cast<size_t>(g[0])];
         const bool blk0 = o0.blk_c1 >= 0, blk = op.blk_c1 >= 0;
         if (static_cast<int>(g.size()) < kTcMaxGroups && o0.cin == op.cin && o0.cout == op.cout && o0.ks == op.ks &&
+            !o0.llr_head && !op.llr_head &&
             o0.ws == op.ws && blk0 == blk && o0.fused_away == op.fused_away && (op.ws || o0.relu_in == op.relu_in) &&
             (!blk || p.tc[static_cast<size_t>(o0.blk_c1)].relu_in == p.tc[static_cast<size_t>(op.blk_c1)].relu_in)) {
           g.push_back(k);
@@ -1319,6 +1360,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           g.s2 = op.s2;
           g.t2 = op.t2;
           g.relu = op.relu;
+          g.nb = op.llr_head ? op.cout_real : 0;  // (the LLR pointer is the forward's output, set per call)
           if (op.relu_in) L.relu_in = 1;  // a launch group shares relu_in (grouping rule)
         }
         L.win_alloc = win_alloc;
@@ -1352,6 +1394,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           g.s2 = op.s2;
           g.t2 = op.t2;
           g.relu = op.relu;
+          g.nb = op.llr_head ? op.cout_real : 0;  // (the LLR pointer is the forward's output, set per call)
         }
         L.win_alloc = win_alloc;
         bool relu_in = false;
@@ -1596,6 +1639,10 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
       if (GL.pair) {
         p.note(conv_pair96_launch(GL.tc, p.num_sms, s), s, fl);
         continue;
+      }
+      if (op0.llr_head) {  // 3x3 LLR head: the epilogue writes this forward's output
+        GL.tc.g[0].llr = out;
+        GL.x3l.g[0].llr = out;
       }
       if (GL.x3) {
         GL.x3l.trace = trace ? dtrace : nullptr;

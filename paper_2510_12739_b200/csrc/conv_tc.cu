@@ -285,7 +285,32 @@ __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel
       const int64_t p = tile * 128 + row;
       const bool valid = geo.valid(p);
       const uint32_t taddr = tbase + static_cast<uint32_t>(a * COUT) + (static_cast<uint32_t>(q * 32) << 16);
-      if constexpr (STAGED) {
+      if (grp.llr) {
+        // LLR head (a 3x3 output conv, NetSpec.kernel = 3): fp32 LLRs of valid rows in the reference layout
+        // [B,T,F,nb], straight from the accumulator (no plane, no rounding)
+        float* dst = nullptr;
+        if (valid) {
+          int32_t bb, tt, ff;
+          geo.coords(p, bb, tt, ff);
+          dst = grp.llr + ((static_cast<int64_t>(bb) * geo.T + tt) * geo.F + ff) * grp.nb;
+        }
+#pragma unroll 1
+        for (int cc = 0; cc < COUT / 32; ++cc) {
+          uint32_t r[32];
+          tmem_ld32(taddr + cc * 32, r);
+          tmem_ld_wait();
+          if (cc == COUT / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_relaxed(&tempty[a]);
+          }
+          if (dst) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (cc * 32 + i < grp.nb) dst[cc * 32 + i] = __uint_as_float(r[i]) + s_bias[cc * 32 + i];
+          }
+        }
+      } else if constexpr (STAGED) {
         const uint8_t* rrow = nullptr;
         if (has_res) {
           mbar_wait(&rfull[a], static_cast<uint32_t>(j >> 1) & 1u);
@@ -481,7 +506,7 @@ using LaunchFn = const char* (*)(const TcLaunch&, int, cudaStream_t);
 #define CNRX_TC_CASES(X)                                                                                     \
   X(16, 32, 1) X(16, 32, 3) X(32, 32, 1) X(32, 32, 3) X(16, 64, 1) X(32, 64, 1) X(64, 64, 1) X(64, 64, 3)   \
   X(16, 96, 1) X(32, 96, 1) X(64, 96, 1) X(96, 96, 1) X(96, 96, 3) X(32, 64, 3) X(64, 32, 3) X(32, 96, 3)     \
-  X(16, 64, 3) X(16, 96, 3)
+  X(16, 64, 3) X(16, 96, 3) X(96, 32, 3)
 
 LaunchFn find_launch(int cin, int cout, int ks, bool h) {
 #define X(a, b, c) \

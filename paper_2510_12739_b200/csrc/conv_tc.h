@@ -30,7 +30,8 @@ struct TcGroup {
   int32_t relu;                     // relu on the primary output (after bias / residual)
   int32_t dil;                      // dilation along F
   int32_t halo;                     // window halo rows = (T+1)*dil + 1 (0 for 1x1)
-  int32_t pad_;
+  int32_t nb;                       // LLR head launches: bits per RE
+  float* llr;                       // LLR head (3x3 output conv): fp32 [B,T,F,nb], valid rows only, instead of a plane
 };
 
 struct TcLaunch {

@@ -442,6 +442,12 @@ __global__ void __launch_bounds__(threads_of(COUT), 1) conv_x3_kernel(const __gr
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_relaxed(&tempty[a]);
+      float* lrow = nullptr;  // LLR head (3x3 output conv): fp32 [B,T,F,nb] rows of valid positions
+      if (grp.llr && valid) {
+        int32_t bb, tt, ff;
+        geo.coords(p, bb, tt, ff);
+        lrow = grp.llr + ((static_cast<int64_t>(bb) * geo.T + tt) * geo.F + ff) * grp.nb;
+      }
 #pragma unroll
       for (int hp = 0; hp < ECH / 16; ++hp) {
         const int c0 = cb + hp * 16;
@@ -449,6 +455,14 @@ __global__ void __launch_bounds__(threads_of(COUT), 1) conv_x3_kernel(const __gr
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           v[i] = (__uint_as_float(r[hp * 16 + i]) + __uint_as_float(e[hp * 16 + i])) + s_bias[c0 + i];
+        if (grp.llr) {
+          if (lrow) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < grp.nb) lrow[c0 + i] = v[i];
+          }
+          continue;
+        }
         if (rrow) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -520,7 +534,7 @@ using LaunchFn = const char* (*)(const X3Launch&, int, cudaStream_t);
 #define CNRX_X3_CASES(X)                                                                                     \
   X(16, 32, 1) X(16, 32, 3) X(32, 32, 1) X(32, 32, 3) X(16, 64, 1) X(32, 64, 1) X(64, 64, 1) X(64, 64, 3)   \
   X(16, 96, 1) X(32, 96, 1) X(64, 96, 1) X(96, 96, 1) X(96, 96, 3) X(32, 64, 3) X(64, 32, 3) X(32, 96, 3)     \
-  X(16, 64, 3) X(16, 96, 3)
+  X(16, 64, 3) X(16, 96, 3) X(96, 32, 3)
 
 LaunchFn find_launch(int cin, int cout, int ks, bool h) {
 #define X(a, b, c) \

@@ -28,7 +28,8 @@ struct X3Group {
   int32_t relu;
   int32_t dil;
   int32_t halo;                     // (T+1)*dil + 1, 0 for 1x1
-  int32_t pad_;
+  int32_t nb;                       // LLR head launches: bits per RE
+  float* llr;                       // LLR head (3x3 output conv): fp32 [B,T,F,nb], valid rows only, instead of a plane
 };
 
 struct X3Launch {

@@ -188,6 +188,17 @@ def _emulate(g, x, R):
         planes[end] = v
         nonneg[end] = relu
     on = nodes[g.output_node]
+    w_out = g.params[on.w].value
+    if w_out.shape[0] == 3:
+        # 3x3 LLR head (NetSpec.kernel = 3): the fold chain materialised as a 16-bit plane, a tensor-core conv
+        # with rounded weights, fp32 LLRs (Bf16Compiler's llr_head op)
+        z = R['act'](plane_for(on.in0))
+        wk = R['w'](torch.from_numpy(w_out).permute(3, 2, 0, 1).contiguous())
+        if z.shape[1] > wk.shape[1]:
+            wk = torch.cat([wk, torch.zeros(wk.shape[0], z.shape[1] - wk.shape[1], 3, 3)], 1)
+        hb = torch.from_numpy(g.params[on.b].value) if on.b >= 0 else torch.zeros(w_out.shape[3])
+        v = Fn.conv2d(z, wk, bias=hb, padding=(1, on.dilation_f), dilation=(1, on.dilation_f))
+        return v.permute(0, 2, 3, 1).contiguous().numpy()
     f = chain(on.in0)
     hw = torch.from_numpy(g.params[on.w].value[0, 0])  # [C,bits]
     hb = torch.from_numpy(g.params[on.b].value) if on.b >= 0 else torch.zeros(hw.shape[1])
