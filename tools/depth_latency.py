@@ -5,7 +5,7 @@ GPU plan.
 Reports param counts, sequential conv depths (network.hpp:320-330), the depth ratio, and the measured
 single-slot (B=1, one TTI) forward latency — median and interquartile range over >= 100 runs, device
 time of a CUDA-graph replay, subnets of a stage executed concurrently (grouped launches) — plus batch
-throughput.  usage: python tools/depth_latency.py [P=1900000] [precision=fp32|bf16] [runs=200]"""
+throughput.  usage: python tools/depth_latency.py [P=1900000] [precision=fp32|bf16|fp16|bf16x3] [runs=200] [io_kernel=3]"""
 import json
 import os
 import sys
@@ -18,9 +18,9 @@ from paper_2510_12739_b200 import files as Fi
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 1_900_000
 prec = sys.argv[2] if len(sys.argv) > 2 else "fp32"
 runs = int(sys.argv[3]) if len(sys.argv) > 3 else 200
-# io_kernel 3: the spec-file templates (3x3 stem/head); 1: 1x1 stem/head as in the BASELINE configs
-# (NetSpec.kernel = 1, BlockSpec.kernel = 3), which the bf16 lowering needs for its pointwise head
-io_kernel = int(sys.argv[4]) if len(sys.argv) > 4 else (1 if prec in ("bf16", "fp16") else 3)
+# io_kernel 3 (default): the spec-file templates (3x3 stem/head, as the paper's networks); 1: 1x1 stem/head as
+# in the BASELINE configs (NetSpec.kernel = 1, BlockSpec.kernel = 3).  Every plan precision lowers both.
+io_kernel = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 T, F, C_IN, BITS = 14, 612, 12, 4  # cfg2 grid and features
 
 SPECS = {
