@@ -1597,6 +1597,12 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
                   h[kBlkTraceE2Comb] / nt, h[kBlkTraceE2Store] / nt);
           fprintf(stderr, "[trace]   CTAs %llu, span %.1f us, effective SM clock %.0f MHz\n", h[12], (h[14] - ~h[13]) * 1e-3,
                   h[15] ? static_cast<double>(h[kBlkTraceTotal]) / static_cast<double>(h[15]) * 1e3 : 0.0);
+          unsigned long long hx[32];
+          CNRX_CUDA(cudaMemcpy(hx, dtrace, sizeof hx, cudaMemcpyDeviceToHost));
+          const double e0 = static_cast<double>(~hx[24]);
+          fprintf(stderr, "[trace]   phases from the first CTA entry: prologues done %.2f us | MMA loops %.2f .. %.2f us | "
+                  "last exit %.2f us\n", (hx[25] - e0) * 1e-3, (~hx[13] - e0) * 1e-3, (hx[14] - e0) * 1e-3,
+                  (hx[26] - e0) * 1e-3);
         }
         continue;
       }

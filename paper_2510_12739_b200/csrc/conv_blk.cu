@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(EPI ? kThreadsFold : kThreads, 1) conv_blk64_k
   constexpr uint32_t IDESC = idesc_e16_f32<F16>(128, kN);
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_align1024(smem_dyn);
+  const unsigned long long t_entry = TRACE ? globaltimer_ns() : 0;  // trace: kernel phases (slots 24..27)
   const int XS = L.xstages;
   const BlkLayout lay = blk_layout(XS, L.win_alloc, RELU_IN, EPI);
   float* s_bias1 = reinterpret_cast<float*>(smem + lay.par_off);
@@ -317,6 +318,10 @@ __global__ void __launch_bounds__(EPI ? kThreadsFold : kThreads, 1) conv_blk64_k
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (TRACE && threadIdx.x == 0) {
+    atomicMax(&L.trace[24], ~t_entry);            // earliest CTA entry
+    atomicMax(&L.trace[25], globaltimer_ns());    // latest end of a CTA prologue (barriers, TMEM, weights)
+  }
   pdl_trigger();
   pdl_wait();
 
@@ -809,6 +814,7 @@ __global__ void __launch_bounds__(EPI ? kThreadsFold : kThreads, 1) conv_blk64_k
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tbase, 512);
+  if (TRACE && threadIdx.x == 0) atomicMax(&L.trace[26], globaltimer_ns());  // latest CTA exit
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn_blk() {
