@@ -58,11 +58,16 @@ __host__ __device__ inline HeadLayout head_layout(int c, int ns, int nb, int sta
   return l;
 }
 
-// byte offset of 16-byte chunk `chunk` of row `row` in a TMA tile: 128-byte swizzle for 64-channel
-// rows, plain row-major otherwise (96 / 128 channels: rows wider than the swizzle span)
+// byte offset of 16-byte chunk `chunk` of row `row` in a TMA tile: 128-byte swizzle for 64-channel rows;
+// 96-channel rows are two boxes, channels [0, 64) with the 128-byte swizzle and [64, 96) with the 64-byte
+// one (rows wider than a swizzle span; unswizzled 192-byte rows put 16 of a warp's 32 rows on the same
+// banks: ncu, cfg3 head at 2 TB/s)
 template <int C>
 __device__ __forceinline__ uint32_t hoff(uint32_t row, uint32_t chunk) {
   if constexpr (C == 64) return row * 128u + ((chunk ^ (row & 7u)) << 4);
+  else if constexpr (C == 96)
+    return chunk < 8u ? row * 128u + ((chunk ^ (row & 7u)) << 4)
+                      : kHRows * 128u + row * 64u + (((chunk - 8u) ^ ((row >> 1) & 3u)) << 4);
   else return row * static_cast<uint32_t>(C * 2) + (chunk << 4);
 }
 
@@ -128,10 +133,14 @@ __global__ void __launch_bounds__(kThreads, 2) head_tma_kernel(const __grid_cons
         mbar_wait(&empty[s], (static_cast<uint32_t>(j / L.stages) & 1u) ^ 1u);
         mbar_arrive_expect_tx(&full[s], tx);
         uint8_t* dst = smem + lay.ring_off + s * lay.stage_bytes;
+        const int32_t r0 = static_cast<int32_t>(tile * kHRows);
         for (int i = 0; i < NS; ++i) {
-          tma_load_2d(dst + i * kPlaneBox, &L.maps[i], &full[s], 0, static_cast<int32_t>(tile * kHRows));
-          if (spl)
-            tma_load_2d(dst + (NS + i) * kPlaneBox, &L.lo_maps[i], &full[s], 0, static_cast<int32_t>(tile * kHRows));
+          tma_load_2d(dst + i * kPlaneBox, &L.maps[i], &full[s], 0, r0);
+          if (C == 96) tma_load_2d(dst + i * kPlaneBox + kHRows * 128, &L.maps_c1[i], &full[s], 0, r0);
+          if (spl) {
+            tma_load_2d(dst + (NS + i) * kPlaneBox, &L.lo_maps[i], &full[s], 0, r0);
+            if (C == 96) tma_load_2d(dst + (NS + i) * kPlaneBox + kHRows * 128, &L.lo_maps_c1[i], &full[s], 0, r0);
+          }
         }
       }
     }
@@ -357,18 +366,21 @@ const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const
     L.relu[i] = relus[i];
     L.aff_s[i] = affs[i] >= 0 ? prog.aff_s[affs[i]] : nullptr;
     L.aff_t[i] = affs[i] >= 0 ? prog.aff_t[affs[i]] : nullptr;
-    for (int part = 0; part < rs; ++part) {
-      cuuint64_t dims[2] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(geo.Nalloc)};
-      cuuint64_t strides[1] = {static_cast<cuuint64_t>(rs * C * 2)};
-      cuuint32_t box[2] = {static_cast<cuuint32_t>(C), static_cast<cuuint32_t>(kHRows)};
-      cuuint32_t es[2] = {1, 1};
-      CUresult r = encode_fn_head()(part == 0 ? &L.maps[i] : &L.lo_maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                                    const_cast<__nv_bfloat16*>(prog.planes[i]) + part * C, dims, strides, box, es,
-                                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                    C == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
-    }
+    for (int part = 0; part < rs; ++part)
+      for (int cb = 0; cb < (C == 96 ? 2 : 1); ++cb) {  // 96 channels: [0, 64) and [64, 96) boxes
+        const int bc = C == 96 ? (cb == 0 ? 64 : 32) : C;
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(bc), static_cast<cuuint64_t>(geo.Nalloc)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(rs * C * 2)};
+        cuuint32_t box[2] = {static_cast<cuuint32_t>(bc), static_cast<cuuint32_t>(kHRows)};
+        cuuint32_t es[2] = {1, 1};
+        CUtensorMap* m = part == 0 ? (cb == 0 ? &L.maps[i] : &L.maps_c1[i]) : (cb == 0 ? &L.lo_maps[i] : &L.lo_maps_c1[i]);
+        const CUtensorMapSwizzle sw = bc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+        CUresult r = encode_fn_head()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                      const_cast<__nv_bfloat16*>(prog.planes[i]) + part * C + cb * 64, dims, strides,
+                                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(4, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+      }
   }
   L.head_w = prog.head_w;
   L.head_b = prog.head_b;
@@ -377,12 +389,14 @@ const char* launch_head_tma(const PwProgram& prog, int ns, const int* ops, const
   L.tc_head = prog.tc_head && !prog.fp16 && !prog.split;
   const bool tc = C == 64 && L.tc_head;
   const int nsb = rs * ns;  // operand boxes per tile
-  // CNRX_HEAD_STAGES (experiments): ring depth; deeper rings fit one CTA per SM instead of two
+  // ring depth: the deepest (<= 3) that still lets two CTAs share an SM (16 consumer warps hide the per-row
+  // chains; with one CTA and 96-channel tiles the kernel was latency-bound at 2.5 TB/s), else whatever fits
+  // one CTA.  CNRX_HEAD_STAGES (experiments) forces a depth.
   static const int want = std::getenv("CNRX_HEAD_STAGES") ? std::atoi(std::getenv("CNRX_HEAD_STAGES")) : 0;
-  int stages = want >= 2 ? want : 3;
-  if (want < 2)
-    while (stages > 2 && head_layout(C, nsb, nb, stages, tc).total > 113u * 1024u) --stages;
-  while (stages > 2 && head_layout(C, nsb, nb, stages, tc).total > 227u * 1024u) --stages;
+  int stages = want >= 1 ? want : 3;
+  if (want < 1)
+    while (stages > 1 && head_layout(C, nsb, nb, stages, tc).total > 113u * 1024u) --stages;
+  while (stages > 1 && head_layout(C, nsb, nb, stages, tc).total > 227u * 1024u) --stages;
   L.stages = stages;
   const int total = static_cast<int>(head_layout(C, nsb, nb, stages, tc).total);
   if (total > 227 * 1024) return nullptr;

@@ -24,6 +24,10 @@ struct HeadLaunch {
   int32_t tc_head;                     // C == 64: GEMV on the tensor core over bf16-rounded z
   int32_t split;                       // split planes (CNRX_*X3 plans): operand i = hi (maps[i]) + lo (lo_maps[i])
   CUtensorMap lo_maps[kHeadMaxPlanes];
+  // C = 96: each tile row is two swizzled boxes, channels [0, 64) (maps / lo_maps, 128B swizzle) and
+  // [64, 96) (these, 64B swizzle), so the consumers' 16-byte reads of 32 rows spread over all banks
+  CUtensorMap maps_c1[kHeadMaxPlanes];
+  CUtensorMap lo_maps_c1[kHeadMaxPlanes];
 };
 
 // Launch the fold program (ns steps, ops/affs/relus as pw_as_fold returns them) + head GEMV when it
