@@ -84,8 +84,11 @@ __host__ __device__ inline SmemLayout smem_layout(int cin, int cout, int ks, int
 }
 
 // 1x1 convs with few input channels (the stem) are epilogue-latency bound: let three CTAs share an SM.
+#ifndef CNRX_STEM_CTAS
+#define CNRX_STEM_CTAS 4
+#endif
 template <int CIN, int COUT, int KS>
-constexpr int min_ctas() { return KS == 1 && CIN <= 32 && COUT <= 64 ? 4 : 1; }
+constexpr int min_ctas() { return KS == 1 && CIN <= 32 && COUT <= 64 ? CNRX_STEM_CTAS : 1; }
 
 template <int CIN, int COUT, int KS, bool F16>
 __global__ void __launch_bounds__(192, min_ctas<CIN, COUT, KS>()) conv_tc_kernel(const __grid_constant__ TcLaunch L) {
