@@ -571,13 +571,21 @@ def main():
                 plan.receive_host_ptr(y_host.data_ptr(), batch.y.shape, out_host.data_ptr())
             h2d, d2h = batch.y.nbytes, out_host.numel() * 4
             how = "cnrx_receive (C ABI, pinned host buffers, batch pipelined in chunks over two copy streams)"
-        elif args.gather == "peer":
+        gather = args.gather
+        if world > 1 and gather == "peer":
+            try:  # collective: every rank agrees on the outcome
+                from paper_2510_12739_b200 import shard as _shp
+                peer = _shp.PeerLLR(world * B, (link.T, link.F, nb), rank, local)
+            except RuntimeError as e:
+                gather, peer_err = "nccl", repr(e)  # no peer access: the NCCL gather instead
+        if world == 1:
+            pass
+        elif gather == "peer":
             # the final gather fused into the LLR head: rank 0's batch buffer is mapped into every rank (CUDA
             # IPC) and each rank's head kernel stores its slots straight into it over NVLink; completion =
             # stream sync + host barrier; rank 0 then reads the whole batch (one D2H)
             from paper_2510_12739_b200 import shard
             y_dev = torch.empty((B, link.T, link.F, link.N), dtype=torch.complex64, device="cuda")
-            peer = shard.PeerLLR(world * B, (link.T, link.F, nb), rank, local)
             dst = peer.dst(rank * B)
             out_host = torch.empty((world * B, link.T, link.F, nb), dtype=torch.float32).pin_memory() if rank == 0 else None
 
@@ -627,8 +635,10 @@ def main():
                "d2h_bytes_per_step": int(d2h), "api": how, "steps": e2e_steps}
         if world > 1:
             e2e["nccl_ranks" if backend == "nccl" else "gloo_ranks_flow_test"] = dist.get_world_size()
-            e2e["gather"] = args.gather
-            if args.gather == "peer":
+            e2e["gather"] = gather
+            if gather != args.gather:
+                e2e["gather_fallback"] = peer_err
+            if gather == "peer":
                 # the peer-written batch equals the ranks' own LLRs gathered by the process group
                 mine = torch.empty((B, link.T, link.F, nb), dtype=torch.float32, device="cuda")
                 plan.receive_device(y_dev, mine, torch.cuda.current_stream().cuda_stream)

@@ -83,8 +83,22 @@ class PeerLLR:
             self.ptr, handle = P.ipc_alloc(device, B * self.slot_bytes)
             obj = [handle]
         dist.broadcast_object_list(obj, src=0)
+        err = None
         if rank != 0:
-            self.ptr = P.ipc_open(device, obj[0])
+            try:
+                self.ptr = P.ipc_open(device, obj[0])
+            except Exception as e:  # e.g. no peer access between these GPUs
+                self.ptr, err = None, e
+        # every rank learns whether all mappings succeeded (so a failure cannot leave ranks in different code paths)
+        ok = [err is None]
+        allok = [None] * dist.get_world_size()
+        dist.all_gather_object(allok, ok[0])
+        if not all(allok):
+            if rank == 0:
+                P.ipc_free(device, self.ptr)
+            elif self.ptr is not None:
+                P.ipc_close(device, self.ptr)
+            raise RuntimeError(f"peer mapping of rank 0's LLR buffer failed on some rank ({err!r})")
 
     def dst(self, b0: int) -> int:
         return self.ptr + b0 * self.slot_bytes
