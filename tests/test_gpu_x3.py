@@ -150,3 +150,16 @@ def test_batches_beyond_the_memory_budget_run_in_slot_chunks(prec, monkeypatch):
     assert np.array_equal(p.receive(b.y), want)
     x = oracle.featurize(b.y, b.pilots, b.pilot_mask)
     assert np.array_equal(p.forward(x), ref.forward(x))
+
+
+def test_chunked_forward_under_graph_capture(monkeypatch):
+    """Slot chunks (memory budget) with CUDA-graph capture on: each chunk is its own captured forward;
+    the LLRs equal the uncaptured one-shot run."""
+    g = G.CONFIGS["cfg2"].graph(seed=8)
+    x = np.random.default_rng(4).standard_normal((6, 14, 40, 12)).astype(np.float32)
+    want = P.Plan(g, "bf16").forward(x)
+    monkeypatch.setenv("CNRX_MEM_BUDGET_MB", "2")
+    p = P.Plan(g, "bf16")
+    p.set_graph_capture(True)
+    assert np.array_equal(p.forward(x), want)
+    assert np.array_equal(p.forward(x), want)
