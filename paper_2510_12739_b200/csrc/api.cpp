@@ -595,6 +595,10 @@ struct Bf16Compiler {
     }
     const cnrx_node& nd = p.N(u);
     if (st.prog.n_ins >= kPwMaxIns - 1) return false;
+    if (nd.op == CNRX_OP_LN) {  // a layer norm is a row-wise program of its own: its plane is a leaf here
+      plane_for(u);
+      return build_chain(u, st, aff_tables, level);
+    }
     switch (nd.op) {
       case CNRX_OP_RELU:
         if (!build_chain(nd.in0, st, aff_tables, level)) return false;
@@ -613,7 +617,9 @@ struct Bf16Compiler {
       }
       case CNRX_OP_ADD:
       case CNRX_OP_MUL: {
-        // one operand must be a plane leaf
+        // one operand must be a plane leaf (a layer norm operand becomes one)
+        for (int o : {nd.in0, nd.in1})
+          if (node_plane[static_cast<size_t>(o)] < 0 && p.N(o).op == CNRX_OP_LN) plane_for(o);
         int leaf = -1, rest = -1;
         if (node_plane[static_cast<size_t>(nd.in1)] >= 0) {
           leaf = nd.in1;
@@ -671,7 +677,7 @@ struct Bf16Compiler {
           return vp;
         }
         const int pprod = plane_producer_pw[static_cast<size_t>(vp)];
-        if (!bn && pprod >= 0 && p.pw[static_cast<size_t>(pprod)].out2_plane < 0) {
+        if (!bn && pprod >= 0 && p.pw[static_cast<size_t>(pprod)].out2_plane < 0 && p.pw[static_cast<size_t>(pprod)].prog.ln == 0) {
           PwStep& ps = p.pw[static_cast<size_t>(pprod)];
           int ns = 0, ops[kPwMaxPlanes], affs[kPwMaxPlanes], relus[kPwMaxPlanes];
           if (pw_as_fold(ps.prog, &ns, ops, affs, relus) && ps.prog.n_planes_used == ns) {
@@ -699,6 +705,30 @@ struct Bf16Compiler {
           return np;
         }
       }
+    }
+    if (nd.op == CNRX_OP_LN) {
+      // layer norm over the channels of each row: the chain feeding it, then the row statistics (generic
+      // pointwise kernel, double accumulation like norms.hpp:171-184), output rounded to the plane format
+      PwStep st;
+      std::vector<std::vector<float>> aff;
+      int level = 0;
+      if (!build_chain(nd.in0, st, aff, level))
+        throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: layer norm input " + std::to_string(nd.in0) +
+                                              " is not a linear pointwise chain over planes");
+      const int k = static_cast<int>(aff.size()) / 2;
+      if (k >= kPwMaxAff) throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: too many affine steps before a layer norm");
+      aff.push_back(p.P(nd.gamma).data);
+      aff.push_back(p.P(nd.beta).data);
+      st.prog.ln = k + 1;
+      st.prog.ln_c = nd.out_channels;
+      const int C = round_cin(nd.out_channels);
+      st.level = level + 1;
+      st.out_plane = new_plane(C, st.level, false);
+      finish_pw(st, aff, C);
+      p.pw.push_back(st);
+      plane_producer_pw[static_cast<size_t>(st.out_plane)] = static_cast<int>(p.pw.size()) - 1;
+      node_plane[static_cast<size_t>(u)] = st.out_plane;
+      return st.out_plane;
     }
     // general linear pointwise chain -> pointwise program kernel
     PwStep st;

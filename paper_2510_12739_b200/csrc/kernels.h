@@ -96,6 +96,9 @@ struct PwProgram {
   int32_t fp16;             // operand / output planes are fp16 (else bf16)
   int32_t tc_head;          // 64-channel heads may run their GEMV on the tensor core (bf16-rounded z)
   int32_t split;            // split planes (CNRX_*X3 plans): a row is [hi C | lo C], value = hi + lo
+  int32_t ln;               // k + 1: the program's result per row is layer-normalised over its channels
+                            // (norms.hpp:155-191, double statistics), gain / shift aff_s[k] / aff_t[k]; 0: none
+  int32_t ln_c;             // real channel count the statistics run over (<= C)
   PwIns ins[kPwMaxIns];
   const __nv_bfloat16* planes[kPwMaxPlanes];
   const float* aff_s[kPwMaxAff];

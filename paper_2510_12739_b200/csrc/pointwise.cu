@@ -45,6 +45,81 @@ __device__ __forceinline__ void store8_split(__nv_bfloat16* p, int C, const floa
   *reinterpret_cast<uint4*>(p + C) = ol;
 }
 
+// Layer-norm programs (prog.ln = k + 1, plane output): the chain for all C channels of the row into local
+// memory, then norms.hpp:171-184's statistics in double (sum and sum of squares, v = sq / c - m^2 clamped at
+// 0, istd = 1 / sqrt(v + eps)) over the real channels, y = (x - m) * istd * g + b in double, then the
+// 16-bit (or split) store; padding channels and invalid rows stay 0.
+constexpr int kLnMaxC = 128;
+constexpr double kPwLnEps = 1e-5;  // network.hpp:431
+__global__ void __launch_bounds__(128) pw_ln_kernel(const __grid_constant__ PwProgram prog, PlaneGeom geo) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= geo.Nalloc) return;
+  const int C = prog.C;
+  const bool split = prog.split != 0, h16 = prog.fp16 != 0;
+  const int64_t rs = split ? 2 * C : C;
+  float acc[kLnMaxC];
+  const bool valid = geo.valid(row);
+  for (int c0 = 0; c0 < C; c0 += 8) {
+    float a8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a8[i] = 0.f;
+    if (valid) {
+      for (int n = 0; n < prog.n_ins; ++n) {
+        const PwIns ins = prog.ins[n];
+        if (ins.op == PW_LOAD || ins.op == PW_MUL || ins.op == PW_ADD) {
+          float v[8];
+          load8(prog.planes[ins.k] + row * rs + c0, v, h16);
+          if (split) {
+            float l[8];
+            load8(prog.planes[ins.k] + row * rs + C + c0, l, h16);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] += l[i];
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            a8[i] = ins.op == PW_LOAD ? v[i] : ins.op == PW_MUL ? a8[i] * v[i] : a8[i] + v[i];
+        } else if (ins.op == PW_AFF) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a8[i] = a8[i] * __ldg(&prog.aff_s[ins.k][c0 + i]) + __ldg(&prog.aff_t[ins.k][c0 + i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a8[i] = fmaxf(a8[i], 0.f);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[c0 + i] = a8[i];
+  }
+  const int k = prog.ln - 1, n = prog.ln_c;
+  double sum = 0.0, sq = 0.0;
+  for (int i = 0; i < n; ++i) {
+    sum += acc[i];
+    sq += static_cast<double>(acc[i]) * acc[i];
+  }
+  const double m = sum / n;
+  double var = sq / n - m * m;
+  if (var < 0) var = 0;
+  const double istd = 1.0 / sqrt(var + kPwLnEps);
+  for (int c0 = 0; c0 < C; c0 += 8) {
+    float y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int c = c0 + i;
+      y[i] = valid && c < n ? static_cast<float>((static_cast<double>(acc[c]) - m) * istd * prog.aff_s[k][c] + prog.aff_t[k][c])
+                            : 0.f;
+    }
+    if (split) {
+      store8_split(prog.out_plane + row * rs + c0, C, y, h16);
+    } else {
+      uint4 o;
+      uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) op[i] = pack2r(h16, y[2 * i], y[2 * i + 1]);
+      *reinterpret_cast<uint4*>(prog.out_plane + row * C + c0) = o;
+    }
+  }
+}
+
 template <int HEAD>
 __global__ void __launch_bounds__(256) pw_program_kernel(const __grid_constant__ PwProgram prog, PlaneGeom geo) {
   extern __shared__ float s_head[];  // [C][bits] + [bits]
@@ -603,6 +678,12 @@ const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaS
   if (prog.head_bits > 0) require(prog.head_bits <= kPwMaxBits, "head with more than 16 outputs");
   require(prog.out2_plane == nullptr || prog.head_bits == 0, "second output needs a plane program");
   const bool head = prog.head_bits > 0;
+  if (prog.ln) {  // layer-norm program (plane output)
+    require(!head && prog.C <= kLnMaxC && !prog.out2_plane, "internal: layer-norm program shape");
+    pw_ln_kernel<<<static_cast<unsigned>((geo.Nalloc + 127) / 128), 128, 0, s>>>(prog, geo);
+    CNRX_CUDA(cudaGetLastError());
+    return prog.split ? "pw_ln_kernel<x3>" : "pw_ln_kernel";
+  }
   if (prog.split && head) {  // split planes: the TMA-streamed head kernel reads hi + lo tiles when it fits
     FoldSteps fs{};
     int ns = 0;

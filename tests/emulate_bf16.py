@@ -89,16 +89,32 @@ def _emulate(g, x, R):
     xt = torch.from_numpy(np.ascontiguousarray(x, np.float32)).permute(0, 3, 1, 2)  # [B,C,T,F]
     planes[g.input_node] = xt  # planes hold fp32 values; rounding is applied per role at each use
 
+    def layer_norm(xv, n):  # norms.hpp:171-184 in double over the channel dim, as the GPU's pw_ln_kernel
+        xd = xv.double()
+        c = xd.shape[1]
+        m = xd.sum(1, keepdim=True) / c
+        v = torch.clamp((xd * xd).sum(1, keepdim=True) / c - m * m, min=0.0)
+        istd = 1.0 / torch.sqrt(v + 1e-5)
+        gm = torch.from_numpy(g.params[n.gamma].value).double()[None, :, None, None]
+        bt = torch.from_numpy(g.params[n.beta].value).double()[None, :, None, None]
+        return ((xd - m) * istd * gm + bt).float()
+
     def chain(u):
         if u in planes:
             return R['leaf'](planes[u])
         n = nodes[u]
+        if n.op == G.OP_LN:  # its own row-wise program: a materialised plane, then a leaf
+            planes[u] = R['act'](layer_norm(chain(n.in0), n))
+            return R['leaf'](planes[u])
         if n.op == G.OP_RELU:
             return torch.relu(chain(n.in0))
         if n.op == G.OP_BN:
             s, t = bn_affine(g, n)
             return chain(n.in0) * s[None, :, None, None] + t[None, :, None, None]
         if n.op in (G.OP_ADD, G.OP_MUL):
+            for o in (n.in0, n.in1):  # a layer-norm operand is materialised as a plane first
+                if o not in planes and nodes[o].op == G.OP_LN:
+                    chain(o)
             if n.in1 in planes:
                 leaf, rest = n.in1, n.in0
             elif n.in0 in planes:

@@ -7,7 +7,8 @@ every plan precision, against the oracle on random inputs (seeded, so a failure 
   * bf16 / fp16: within the emulation bound of tests/test_gpu_parity.py (rel L2 <= 2e-2 / 5e-3).
 Graphs a 16-bit plan cannot express must be rejected loudly (CnrxUnsupported), never computed wrong.
 Since round 2 the tensor-core plans also lower 3x3 LLR heads (NetSpec.kernel = 3: a conv whose epilogue
-writes the fp32 LLRs); LN fusion norms, concat fusion and depthwise convs stay fp32-only."""
+writes the fp32 LLRs) and LN fusion norms (a row-wise program with double statistics); concat fusion and
+depthwise convs stay fp32-only."""
 import dataclasses
 
 import numpy as np
@@ -35,7 +36,8 @@ def _random_graph(seed):
         op = str(r.choice(["mul", "add"]))
         pts = sorted(set(int(x) for x in r.integers(0, main, size=int(r.integers(1, main + 1)))))
         bidir = bool(r.random() < 0.3)  # feedback fusion (network.hpp:518-522)
-        spec = G.conet_template(width, main, sups, op, "bn", bidir, in_ch, bits, kernel=kernel, fusion_points=pts)
+        norm = str(r.choice(["bn", "bn", "ln"]))  # fusion norm (network.hpp:550)
+        spec = G.conet_template(width, main, sups, op, norm, bidir, in_ch, bits, kernel=kernel, fusion_points=pts)
         g = G.build_conet(spec)
     g.init_he_normal(seed, randomize_aux=True)
     B, F = int(r.integers(1, 4)), int(r.integers(3, 40))
@@ -43,7 +45,7 @@ def _random_graph(seed):
     return g, x
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(48))
 def test_random_builder_graphs_all_precisions(seed):
     g, x = _random_graph(1000 + seed)
     ref = oracle.forward(g, x)

@@ -145,9 +145,11 @@ def test_generic_ops_fp32():
 
 
 def test_bf16_unsupported_graph_is_rejected_not_fallback():
-    g = G.build_conet(G.conet_template(16, 2, [2], "mul", "ln", False, 6, 2)).init_he_normal(1, True)
-    with pytest.raises(P.CnrxUnsupported):
-        P.Plan(g, "bf16")
+    # depthwise-separable convs stay fp32-only (LN fusion norms lower since round 2: test_gpu_fuzz.py)
+    g = G.build_conet(G.conet_template(32, 2, [2], "mul", "bn", False, 6, 2, conv="depthwise")).init_he_normal(1, True)
+    for prec in ("bf16", "fp16", "bf16x3"):
+        with pytest.raises(P.CnrxUnsupported):
+            P.Plan(g, prec)
 
 
 # ------------------------------------------------------------------------------------------------
