@@ -171,6 +171,7 @@ struct TcOp {
 };
 struct PwStep {
   PwProgram prog{};
+  bool concat = false;  // channel concatenation of plane_ids[0], plane_ids[1] (launch_concat_planes)
   int plane_ids[kPwMaxPlanes];
   int n_planes = 0;
   int out_plane = -1;  // -1: head
@@ -677,7 +678,8 @@ struct Bf16Compiler {
           return vp;
         }
         const int pprod = plane_producer_pw[static_cast<size_t>(vp)];
-        if (!bn && pprod >= 0 && p.pw[static_cast<size_t>(pprod)].out2_plane < 0 && p.pw[static_cast<size_t>(pprod)].prog.ln == 0) {
+        if (!bn && pprod >= 0 && p.pw[static_cast<size_t>(pprod)].out2_plane < 0 && p.pw[static_cast<size_t>(pprod)].prog.ln == 0 &&
+            !p.pw[static_cast<size_t>(pprod)].concat) {
           PwStep& ps = p.pw[static_cast<size_t>(pprod)];
           int ns = 0, ops[kPwMaxPlanes], affs[kPwMaxPlanes], relus[kPwMaxPlanes];
           if (pw_as_fold(ps.prog, &ns, ops, affs, relus) && ps.prog.n_planes_used == ns) {
@@ -705,6 +707,28 @@ struct Bf16Compiler {
           return np;
         }
       }
+    }
+    if (nd.op == CNRX_OP_CONCAT) {
+      // concat fusion (network.hpp:541-544): the two planes side by side, consumed by the 1x1 restore conv
+      const int a = plane_for(nd.in0), b = plane_for(nd.in1);
+      const int ca = p.planes[static_cast<size_t>(a)].C, cb = p.planes[static_cast<size_t>(b)].C;
+      if (ca != p.N(nd.in0).out_channels || cb != p.N(nd.in1).out_channels || round_cin(ca + cb) != ca + cb)
+        throw Error(CNRX_ERR_UNSUPPORTED, "bf16 plan: concat of " + std::to_string(p.N(nd.in0).out_channels) + " + " +
+                                              std::to_string(p.N(nd.in1).out_channels) + " channels");
+      PwStep st;
+      st.concat = true;
+      st.plane_ids[0] = a;
+      st.plane_ids[1] = b;
+      st.n_planes = 2;
+      st.prog.C = ca + cb;
+      st.level = std::max(p.planes[static_cast<size_t>(a)].level, p.planes[static_cast<size_t>(b)].level) + 1;
+      st.out_plane = new_plane(ca + cb, st.level, false);
+      use(a, st.level);
+      use(b, st.level);
+      p.pw.push_back(st);
+      plane_producer_pw[static_cast<size_t>(st.out_plane)] = static_cast<int>(p.pw.size()) - 1;
+      node_plane[static_cast<size_t>(u)] = st.out_plane;
+      return st.out_plane;
     }
     if (nd.op == CNRX_OP_LN) {
       // layer norm over the channels of each row: the chain feeding it, then the row statistics (generic
@@ -1717,6 +1741,13 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
       if (ws.head_fused && k == p.hf_pw) continue;      // ran in the last convs' epilogue
       if (ws.head_blk_fused && k == p.hb_pw) continue;  // ran in the last fused blocks' epilogues
       PwStep& st = p.pw[static_cast<size_t>(k)];
+      if (st.concat) {
+        const int ca = p.planes[static_cast<size_t>(st.plane_ids[0])].C;
+        p.note(launch_concat_planes(plane_ptr(st.plane_ids[0]), ca, plane_ptr(st.plane_ids[1]), st.prog.C - ca,
+                                    plane_ptr(st.out_plane), p.split, ws.geo, s),
+               s);
+        continue;
+      }
       PwProgram prog = st.prog;
       prog.fp16 = p.fp16;
       prog.split = p.split;

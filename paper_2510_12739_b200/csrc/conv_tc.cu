@@ -509,7 +509,7 @@ using LaunchFn = const char* (*)(const TcLaunch&, int, cudaStream_t);
 #define CNRX_TC_CASES(X)                                                                                     \
   X(16, 32, 1) X(16, 32, 3) X(32, 32, 1) X(32, 32, 3) X(16, 64, 1) X(32, 64, 1) X(64, 64, 1) X(64, 64, 3)   \
   X(16, 96, 1) X(32, 96, 1) X(64, 96, 1) X(96, 96, 1) X(96, 96, 3) X(32, 64, 3) X(64, 32, 3) X(32, 96, 3)     \
-  X(16, 64, 3) X(16, 96, 3) X(96, 32, 3)
+  X(16, 64, 3) X(16, 96, 3) X(96, 32, 3) X(64, 32, 1) X(128, 64, 1)
 
 LaunchFn find_launch(int cin, int cout, int ks, bool h) {
 #define X(a, b, c) \

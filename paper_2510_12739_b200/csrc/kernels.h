@@ -111,6 +111,10 @@ struct PwProgram {
 };
 
 const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s);
+// Channel concatenation of two planes (CoNet concat fusion, network.hpp:541-544): out row = [a (ca) | b (cb)]
+// (split planes: [a_hi | b_hi | a_lo | b_lo]); ca, cb multiples of 8.
+const char* launch_concat_planes(const __nv_bfloat16* a, int ca, const __nv_bfloat16* b, int cb, __nv_bfloat16* out,
+                                 bool split, const PlaneGeom& geo, cudaStream_t s);
 
 // Specialised form of the common program shape, a left fold over operand planes:
 //   acc = P[0]; [aff_0]; [relu_0];  for i >= 1: acc = acc (mul|add) P[i]; [aff_i]; [relu_i]

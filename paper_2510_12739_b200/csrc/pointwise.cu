@@ -674,6 +674,33 @@ static void launch_rows(const PwProgram& prog, const PlaneGeom& geo, cudaStream_
   CNRX_CUDA(cudaGetLastError());
 }
 
+namespace {
+// one thread per 16-byte (8-channel) chunk of an output row half
+__global__ void __launch_bounds__(256) concat_planes_kernel(const uint4* __restrict__ a, int ca8, const uint4* __restrict__ b,
+                                                            int cb8, uint4* __restrict__ out, int halves, int64_t n) {
+  const int c8 = ca8 + cb8;  // output chunks per half row
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / (halves * c8);
+    const int r = static_cast<int>(i - row * halves * c8);
+    const int h = r / c8, k = r - h * c8;  // half (hi / lo), chunk within the half
+    out[i] = k < ca8 ? a[(row * halves + h) * ca8 + k] : b[(row * halves + h) * cb8 + (k - ca8)];
+  }
+}
+}  // namespace
+
+const char* launch_concat_planes(const __nv_bfloat16* a, int ca, const __nv_bfloat16* b, int cb, __nv_bfloat16* out,
+                                 bool split, const PlaneGeom& geo, cudaStream_t s) {
+  require(ca % 8 == 0 && cb % 8 == 0, "internal: concat channel counts must be multiples of 8");
+  const int halves = split ? 2 : 1;
+  const int64_t n = geo.Nalloc * halves * ((ca + cb) / 8);
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  concat_planes_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(a), ca / 8, reinterpret_cast<const uint4*>(b),
+                                              cb / 8, reinterpret_cast<uint4*>(out), halves, n);
+  CNRX_CUDA(cudaGetLastError());
+  return split ? "concat_planes_kernel<x3>" : "concat_planes_kernel";
+}
+
 const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s) {
   if (prog.head_bits > 0) require(prog.head_bits <= kPwMaxBits, "head with more than 16 outputs");
   require(prog.out2_plane == nullptr || prog.head_bits == 0, "second output needs a plane program");

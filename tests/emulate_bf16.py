@@ -130,6 +130,9 @@ def _emulate(g, x, R):
         if u in planes:
             return planes[u]
         n = nodes[u]
+        if n.op == G.OP_CONCAT:  # the two planes side by side (launch_concat_planes): a copy, no rounding
+            planes[u] = torch.cat([plane_for(n.in0), plane_for(n.in1)], 1)
+            return planes[u]
         if n.op == G.OP_RELU:
             v, bn = n.in0, None
             if v not in planes and nodes[v].op == G.OP_BN and nodes[v].in0 in planes:

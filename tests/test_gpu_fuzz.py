@@ -7,8 +7,8 @@ every plan precision, against the oracle on random inputs (seeded, so a failure 
   * bf16 / fp16: within the emulation bound of tests/test_gpu_parity.py (rel L2 <= 2e-2 / 5e-3).
 Graphs a 16-bit plan cannot express must be rejected loudly (CnrxUnsupported), never computed wrong.
 Since round 2 the tensor-core plans also lower 3x3 LLR heads (NetSpec.kernel = 3: a conv whose epilogue
-writes the fp32 LLRs) and LN fusion norms (a row-wise program with double statistics); concat fusion and
-depthwise convs stay fp32-only."""
+writes the fp32 LLRs), LN fusion norms (a row-wise program with double statistics) and concat fusion at
+widths <= 64 (the planes side by side, then the 1x1 restore conv); depthwise convs stay fp32-only."""
 import dataclasses
 
 import numpy as np
@@ -33,7 +33,7 @@ def _random_graph(seed):
     else:
         main = int(r.integers(1, 4))
         sups = [int(x) for x in r.integers(1, 4, size=int(r.integers(1, 4)))]
-        op = str(r.choice(["mul", "add"]))
+        op = str(r.choice(["mul", "add", "concat"] if width <= 64 else ["mul", "add"]))
         pts = sorted(set(int(x) for x in r.integers(0, main, size=int(r.integers(1, main + 1)))))
         bidir = bool(r.random() < 0.3)  # feedback fusion (network.hpp:518-522)
         norm = str(r.choice(["bn", "bn", "ln"]))  # fusion norm (network.hpp:550)
