@@ -172,6 +172,10 @@ struct TcOp {
 struct PwStep {
   PwProgram prog{};
   bool concat = false;  // channel concatenation of plane_ids[0], plane_ids[1] (launch_concat_planes)
+  bool dw = false;      // depthwise conv of plane_ids[0] (launch_dwconv_plane)
+  const float* dw_w = nullptr;
+  const float* dw_b = nullptr;
+  int dw_kh = 0, dw_kw = 0, dw_dil = 1;
   int plane_ids[kPwMaxPlanes];
   int n_planes = 0;
   int out_plane = -1;  // -1: head
@@ -413,7 +417,8 @@ void validate_graph(cnrx_plan& p) {
   }
   p.in_ch = p.N(p.in_node).out_channels;
   p.out_ch = p.N(p.out_node).out_channels;
-  for (auto& nd : p.nodes) p.npad = std::max(p.npad, nd.op == CNRX_OP_CONV ? nd.dilation_f : 1);
+  for (auto& nd : p.nodes)
+    p.npad = std::max(p.npad, nd.op == CNRX_OP_CONV || nd.op == CNRX_OP_DWCONV ? nd.dilation_f : 1);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -679,7 +684,7 @@ struct Bf16Compiler {
         }
         const int pprod = plane_producer_pw[static_cast<size_t>(vp)];
         if (!bn && pprod >= 0 && p.pw[static_cast<size_t>(pprod)].out2_plane < 0 && p.pw[static_cast<size_t>(pprod)].prog.ln == 0 &&
-            !p.pw[static_cast<size_t>(pprod)].concat) {
+            !p.pw[static_cast<size_t>(pprod)].concat && !p.pw[static_cast<size_t>(pprod)].dw) {
           PwStep& ps = p.pw[static_cast<size_t>(pprod)];
           int ns = 0, ops[kPwMaxPlanes], affs[kPwMaxPlanes], relus[kPwMaxPlanes];
           if (pw_as_fold(ps.prog, &ns, ops, affs, relus) && ps.prog.n_planes_used == ns) {
@@ -707,6 +712,38 @@ struct Bf16Compiler {
           return np;
         }
       }
+    }
+    if (nd.op == CNRX_OP_DWCONV) {
+      // depthwise conv (network.hpp:443-449 conv_stage "depthwise"): CUDA cores, fp32 weights, plane in / out
+      const int a = plane_for(nd.in0);
+      const int C = p.planes[static_cast<size_t>(a)].C;
+      const auto& w = p.P(nd.w);
+      PwStep st;
+      st.dw = true;
+      st.plane_ids[0] = a;
+      st.n_planes = 1;
+      st.prog.C = C;
+      st.dw_kh = static_cast<int>(w.dims[0]);
+      st.dw_kw = static_cast<int>(w.dims[1]);
+      st.dw_dil = nd.dilation_f;
+      const int creal = static_cast<int>(w.dims[2]);
+      std::vector<float> wp(static_cast<size_t>(st.dw_kh * st.dw_kw * C), 0.f);
+      for (int t = 0; t < st.dw_kh * st.dw_kw; ++t)
+        for (int c = 0; c < creal; ++c)
+          wp[static_cast<size_t>(t * C + c)] = w.data[static_cast<size_t>(t * creal + c)];  // [kh,kw,C,1]
+      st.dw_w = p.upload(wp);
+      if (nd.b >= 0) {
+        std::vector<float> bp(static_cast<size_t>(C), 0.f);
+        for (int c = 0; c < creal; ++c) bp[static_cast<size_t>(c)] = p.P(nd.b).data[static_cast<size_t>(c)];
+        st.dw_b = p.upload(bp);
+      }
+      st.level = p.planes[static_cast<size_t>(a)].level + 1;
+      st.out_plane = new_plane(C, st.level, false);
+      use(a, st.level);
+      p.pw.push_back(st);
+      plane_producer_pw[static_cast<size_t>(st.out_plane)] = static_cast<int>(p.pw.size()) - 1;
+      node_plane[static_cast<size_t>(u)] = st.out_plane;
+      return st.out_plane;
     }
     if (nd.op == CNRX_OP_CONCAT) {
       // concat fusion (network.hpp:541-544): the two planes side by side, consumed by the 1x1 restore conv
@@ -1741,6 +1778,12 @@ void run_bf16(cnrx_plan& p, const float* in, int input_kind, int N, float* out, 
       if (ws.head_fused && k == p.hf_pw) continue;      // ran in the last convs' epilogue
       if (ws.head_blk_fused && k == p.hb_pw) continue;  // ran in the last fused blocks' epilogues
       PwStep& st = p.pw[static_cast<size_t>(k)];
+      if (st.dw) {
+        p.note(launch_dwconv_plane(plane_ptr(st.plane_ids[0]), plane_ptr(st.out_plane), st.dw_w, st.dw_b, st.prog.C,
+                                   st.dw_kh, st.dw_kw, st.dw_dil, p.fp16, p.split, ws.geo, s),
+               s, 2ll * st.dw_kh * st.dw_kw * st.prog.C);
+        continue;
+      }
       if (st.concat) {
         const int ca = p.planes[static_cast<size_t>(st.plane_ids[0])].C;
         p.note(launch_concat_planes(plane_ptr(st.plane_ids[0]), ca, plane_ptr(st.plane_ids[1]), st.prog.C - ca,

@@ -111,6 +111,11 @@ struct PwProgram {
 };
 
 const char* launch_pw_program(const PwProgram& prog, const PlaneGeom& geo, cudaStream_t s);
+// Depthwise conv (kernels.hpp:197-236) over a plane: per channel, bias then the taps in (dt, df) order in fp32
+// (fp32 weights [kh*kw][C]), taps as row offsets of the plane layout (padding rows are zero), the result
+// rounded to the plane format (split: hi / lo); padding rows written zero.
+const char* launch_dwconv_plane(const __nv_bfloat16* in, __nv_bfloat16* out, const float* w, const float* bias, int C,
+                                int kh, int kw, int dil, bool h16, bool split, const PlaneGeom& geo, cudaStream_t s);
 // Channel concatenation of two planes (CoNet concat fusion, network.hpp:541-544): out row = [a (ca) | b (cb)]
 // (split planes: [a_hi | b_hi | a_lo | b_lo]); ca, cb multiples of 8.
 const char* launch_concat_planes(const __nv_bfloat16* a, int ca, const __nv_bfloat16* b, int cb, __nv_bfloat16* out,

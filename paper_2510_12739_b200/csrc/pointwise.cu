@@ -689,6 +689,62 @@ __global__ void __launch_bounds__(256) concat_planes_kernel(const uint4* __restr
 }
 }  // namespace
 
+namespace {
+// one thread per (row, 8-channel chunk)
+__global__ void __launch_bounds__(256) dwconv_plane_kernel(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                                           const float* __restrict__ w, const float* __restrict__ bias, int C,
+                                                           int kh, int kw, int dil, bool h16, bool split, PlaneGeom geo) {
+  const int c8 = C / 8;
+  const int64_t n = geo.Nalloc * c8;
+  const int64_t rs = split ? 2 * C : C;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / c8;
+    const int c0 = static_cast<int>(i - row * c8) * 8;
+    float acc[8];
+    const bool valid = geo.valid(row);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = valid && bias ? bias[c0 + e] : 0.f;
+    if (valid) {
+      for (int dt = 0; dt < kh; ++dt)
+        for (int df = 0; df < kw; ++df) {
+          const int64_t r2 = row + (dt - kh / 2) + static_cast<int64_t>(df - kw / 2) * dil * geo.T1;
+          if (r2 < 0 || r2 >= geo.Nalloc) continue;  // zero rows (out-of-grid taps) contribute nothing
+          float v[8];
+          load8(in + r2 * rs + c0, v, h16);
+          if (split) {
+            float l[8];
+            load8(in + r2 * rs + C + c0, l, h16);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] += l[e];
+          }
+          const float* wt = w + (dt * kw + df) * C + c0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], __fmul_rn(v[e], wt[e]));
+        }
+    }
+    if (split) {
+      store8_split(out + row * rs + c0, C, acc, h16);
+    } else {
+      uint4 o;
+      uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) op[e] = pack2r(h16, acc[2 * e], acc[2 * e + 1]);
+      *reinterpret_cast<uint4*>(out + row * C + c0) = o;
+    }
+  }
+}
+}  // namespace
+
+const char* launch_dwconv_plane(const __nv_bfloat16* in, __nv_bfloat16* out, const float* w, const float* bias, int C,
+                                int kh, int kw, int dil, bool h16, bool split, const PlaneGeom& geo, cudaStream_t s) {
+  const int64_t n = geo.Nalloc * (C / 8);
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  dwconv_plane_kernel<<<blocks, 256, 0, s>>>(in, out, w, bias, C, kh, kw, dil, h16, split, geo);
+  CNRX_CUDA(cudaGetLastError());
+  return split ? "dwconv_plane_kernel<x3>" : "dwconv_plane_kernel";
+}
+
 const char* launch_concat_planes(const __nv_bfloat16* a, int ca, const __nv_bfloat16* b, int cb, __nv_bfloat16* out,
                                  bool split, const PlaneGeom& geo, cudaStream_t s) {
   require(ca % 8 == 0 && cb % 8 == 0, "internal: concat channel counts must be multiples of 8");

@@ -130,6 +130,15 @@ def _emulate(g, x, R):
         if u in planes:
             return planes[u]
         n = nodes[u]
+        if n.op == G.OP_DWCONV:  # depthwise conv on CUDA cores (launch_dwconv_plane): fp32 weights
+            xin = R['act'](plane_for(n.in0))
+            wv = g.params[n.w].value  # [kh,kw,C,1]
+            kh, kw = wv.shape[0], wv.shape[1]
+            wk = torch.from_numpy(np.ascontiguousarray(wv[..., 0].transpose(2, 0, 1)))[:, None]  # [C,1,kh,kw]
+            bias = torch.from_numpy(g.params[n.b].value) if n.b >= 0 else None
+            planes[u] = Fn.conv2d(xin, wk, bias=bias, padding=(kh // 2, (kw // 2) * n.dilation_f),
+                                  dilation=(1, n.dilation_f), groups=wk.shape[0])
+            return planes[u]
         if n.op == G.OP_CONCAT:  # the two planes side by side (launch_concat_planes): a copy, no rounding
             planes[u] = torch.cat([plane_for(n.in0), plane_for(n.in1)], 1)
             return planes[u]

@@ -7,8 +7,9 @@ every plan precision, against the oracle on random inputs (seeded, so a failure 
   * bf16 / fp16: within the emulation bound of tests/test_gpu_parity.py (rel L2 <= 2e-2 / 5e-3).
 Graphs a 16-bit plan cannot express must be rejected loudly (CnrxUnsupported), never computed wrong.
 Since round 2 the tensor-core plans also lower 3x3 LLR heads (NetSpec.kernel = 3: a conv whose epilogue
-writes the fp32 LLRs), LN fusion norms (a row-wise program with double statistics) and concat fusion at
-widths <= 64 (the planes side by side, then the 1x1 restore conv); depthwise convs stay fp32-only."""
+writes the fp32 LLRs), LN fusion norms (a row-wise program with double statistics), concat fusion at
+widths <= 64 (the planes side by side, then the 1x1 restore conv) and depthwise-separable convs (the
+depthwise stage on CUDA cores over the plane, the pointwise stage on the tensor cores)."""
 import dataclasses
 
 import numpy as np
@@ -37,7 +38,9 @@ def _random_graph(seed):
         pts = sorted(set(int(x) for x in r.integers(0, main, size=int(r.integers(1, main + 1)))))
         bidir = bool(r.random() < 0.3)  # feedback fusion (network.hpp:518-522)
         norm = str(r.choice(["bn", "bn", "ln"]))  # fusion norm (network.hpp:550)
-        spec = G.conet_template(width, main, sups, op, norm, bidir, in_ch, bits, kernel=kernel, fusion_points=pts)
+        conv = str(r.choice(["standard", "standard", "depthwise"]))  # conv_stage kinds (network.hpp:443-449)
+        spec = G.conet_template(width, main, sups, op, norm, bidir, in_ch, bits, conv=conv, kernel=kernel,
+                                fusion_points=pts)
         g = G.build_conet(spec)
     g.init_he_normal(seed, randomize_aux=True)
     B, F = int(r.integers(1, 4)), int(r.integers(3, 40))

@@ -144,9 +144,29 @@ def test_generic_ops_fp32():
         assert np.array_equal(got, ref), np.abs(got - ref).max()
 
 
+@pytest.mark.parametrize("prec,bound", [("bf16", 2e-2), ("fp16", 5e-3)])
+def test_16bit_depthwise_separable_vs_emulation(prec, bound):
+    """Depthwise stage: dwconv_plane_kernel (CUDA cores, fp32 weights, one 16-bit rounding of the
+    output); the emulation rounds at the same points."""
+    g = G.build_conet(G.conet_template(64, 2, [2, 1], "add", "bn", True, 12, 4, conv="depthwise",
+                                       kernel=3)).init_he_normal(9, randomize_aux=True)
+    x = np.random.default_rng(2).standard_normal((3, 14, 33, 12)).astype(np.float32)
+    p = P.Plan(g, prec)
+    got = p.forward(x)
+    emu = E.emulate(g, x, precision=prec)
+    assert np.isfinite(emu).all() and np.linalg.norm(got - emu) / np.linalg.norm(emu) <= bound
+    assert any("dwconv_plane_kernel" in n for n in p.launch_names())
+
+
 def test_bf16_unsupported_graph_is_rejected_not_fallback():
-    # depthwise-separable convs stay fp32-only (LN fusion norms lower since round 2: test_gpu_fuzz.py)
-    g = G.build_conet(G.conet_template(32, 2, [2], "mul", "bn", False, 6, 2, conv="depthwise")).init_he_normal(1, True)
+    # a 5x5 conv has no tensor-core lowering (every reference builder graph lowers since round 2:
+    # test_gpu_fuzz.py); it must be rejected, not computed another way
+    g = G.Graph()
+    x = g.add_input(12)
+    s = g.add_relu(g.add_conv(x, "s", 1, 12, 32, True))
+    h = g.add_relu(g.add_conv(s, "a", 5, 32, 32, True))
+    g.set_output(g.add_conv(h, "out", 1, 32, 4, True))
+    g.init_he_normal(1, randomize_aux=True)
     for prec in ("bf16", "fp16", "bf16x3"):
         with pytest.raises(P.CnrxUnsupported):
             P.Plan(g, prec)

@@ -86,6 +86,19 @@ def test_x3_vs_oracle(name, B, F, prec):
 
 
 @pytest.mark.parametrize("prec", ["bf16x3", "fp16x3"])
+@pytest.mark.parametrize("width,kernel,norm", [(64, 3, "bn"), (32, 1, "ln"), (96, 3, "bn")])
+def test_x3_depthwise_separable(width, kernel, norm, prec):
+    """Depthwise-separable blocks (network.hpp:443-449): the depthwise stage on CUDA cores over the split
+    plane (dwconv_plane_kernel, fp32 weights), the pointwise stage on the tensor cores."""
+    g = G.build_conet(G.conet_template(width, 2, [2], "add", norm, False, 12, 4, conv="depthwise",
+                                       kernel=kernel)).init_he_normal(5, randomize_aux=True)
+    x = np.random.default_rng(width).standard_normal((2, 14, 40, 12)).astype(np.float32)
+    p = P.Plan(g, prec)
+    assert_x3(p.forward(x), oracle.forward(g, x), prec)
+    assert any("dwconv_plane_kernel" in n for n in p.launch_names()), p.launch_names()
+
+
+@pytest.mark.parametrize("prec", ["bf16x3", "fp16x3"])
 def test_x3_receive_path(prec):
     """featurize (GPU, fp32) -> split input plane -> network -> LLRs, against the oracle featurizer +
     reference forward; and the same LLRs through receive() (host buffers) and receive_device()."""
