@@ -164,6 +164,19 @@ int cnrx_featurize_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_
 int cnrx_feature_plane_device(cnrx_plan* plan, const float* y_dev, int64_t B, int64_t T, int64_t F, int64_t N,
                               uint16_t* out_dev, int32_t* cpad);
 
+/* Debug hook: the plan's own bounds check (compute-sanitizer memcheck's stand-in for out-of-range writes).
+ * With guard bands on, every workspace allocation of the plan (activation planes, fp32 node buffers,
+ * staging, feature and fold buffers) sits between two 256 KB canary bands; cnrx_plan_check_guard_bands
+ * synchronises the device and counts canary bytes that no longer hold their pattern (0 = no kernel wrote
+ * outside its buffers since they were allocated).  Switching the mode frees the workspace (the next call
+ * reallocates it).  No reference counterpart: the reference allocates one Tensor per node
+ * (network.hpp:170-178) and relies on the host sanitizers. */
+int cnrx_plan_set_guard_bands(cnrx_plan* plan, int32_t enable);
+int cnrx_plan_check_guard_bands(cnrx_plan* plan, int64_t* n_buffers, int64_t* bad_bytes);
+/* Device address of guard band `side` (0 below, 1 above) of guarded buffer `index` (256 KB each): lets a
+ * test of the check itself overwrite a canary. */
+int cnrx_plan_guard_band_ptr(cnrx_plan* plan, int64_t index, int32_t side, void** band_dev);
+
 /* Slot-sharded forward / receive across several plans (one per GPU, built from the same network): slots are
  * split into contiguous ranges, each GPU runs its range from host memory on its own thread, LLRs land
  * in the caller's buffer.  No collective on the data path. */

@@ -215,7 +215,49 @@ struct Workspace {
   bool head_blk_fused = false;        // ... in the last fused blocks' conv2 epilogues (fused-block program)
   void* fold_bufs[2] = {nullptr, nullptr};  // fp32 partial-fold planes [Nalloc][64] of the fused-block head
   size_t fold_bytes = 0;
+  // guard bands (cnrx_plan_set_guard_bands): every workspace allocation sits between two canary bands
+  bool guard = false;
+  struct Guarded {
+    char* base;
+    size_t bytes;
+  };
+  std::vector<Guarded> guarded;
 };
+
+constexpr size_t kGuardBytes = 256u << 10;  // > one TMA window / staged tile either side; keeps 1 KB alignment
+constexpr int kGuardByte = 0xA5;
+
+// Workspace allocations go through these two, so a plan in guard-band mode can check that no kernel
+// wrote outside its buffers (the pool's compute-sanitizer is closed; this is the plan's own bounds check).
+void* ws_malloc(Workspace& ws, size_t bytes) {
+  void* d = nullptr;
+  if (!ws.guard) {
+    CNRX_CUDA(cudaMalloc(&d, bytes));
+    return d;
+  }
+  CNRX_CUDA(cudaMalloc(&d, bytes + 2 * kGuardBytes));
+  char* base = static_cast<char*>(d);
+  cudaError_t e = cudaMemset(base, kGuardByte, kGuardBytes);
+  if (e == cudaSuccess) e = cudaMemset(base + kGuardBytes + bytes, kGuardByte, kGuardBytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();  // the memsets run on the legacy stream, forwards do not
+  if (e != cudaSuccess) {
+    cudaFree(base);
+    CNRX_CUDA(e);
+  }
+  ws.guarded.push_back({base, bytes});
+  return base + kGuardBytes;
+}
+
+void ws_free(Workspace& ws, void* ptr) {
+  if (!ptr) return;
+  for (size_t i = 0; i < ws.guarded.size(); ++i)
+    if (ws.guarded[i].base + kGuardBytes == ptr) {
+      cudaFree(ws.guarded[i].base);
+      ws.guarded.erase(ws.guarded.begin() + static_cast<std::ptrdiff_t>(i));
+      return;
+    }
+  cudaFree(ptr);
+}
 
 }  // namespace
 
@@ -1236,7 +1278,7 @@ void ensure_workspace(cnrx_plan& p, int B, int T, int F) {
   try {
     ensure_workspace_impl(p, B, T, F);
   } catch (...) {
-    for (void* b : ws.buffers) cudaFree(b);
+    for (void* b : ws.buffers) ws_free(ws, b);
     ws.buffers.clear();
     ws.sizes.clear();
     ws.launches.clear();
@@ -1259,7 +1301,7 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
     p.gkey.clear();
   }
   if (!reuse) {
-    for (void* b : ws.buffers) cudaFree(b);
+    for (void* b : ws.buffers) ws_free(ws, b);
     ws.buffers.clear();
     ws.sizes.clear();
     ws.cap_B = B;
@@ -1271,19 +1313,15 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
     if (reuse) return;
     const int64_t rows = static_cast<int64_t>(B) * T * F;
     for (int c : p.f32_buf_channels) {
-      void* d = nullptr;
-      CNRX_CUDA(cudaMalloc(&d, static_cast<size_t>(rows) * c * sizeof(float)));
-      ws.buffers.push_back(d);
+      ws.buffers.push_back(ws_malloc(ws, static_cast<size_t>(rows) * c * sizeof(float)));
     }
     return;
   }
   ws.geo = make_geom(B, T, F, p.npad);
   if (!reuse)
     for (int c : p.buf_channels) {
-      void* d = nullptr;
       const size_t bytes = static_cast<size_t>(ws.geo.Nalloc) * c * 2 * (p.split ? 2 : 1);
-      CNRX_CUDA(cudaMalloc(&d, bytes));  // every producer writes all rows of [0, Nalloc): no clearing needed
-      ws.buffers.push_back(d);
+      ws.buffers.push_back(ws_malloc(ws, bytes));  // every producer writes all rows of [0, Nalloc): no clearing needed
     }
   // tensor maps / launch descriptors per TC group
   auto plane_ptr = [&](int pl) -> __nv_bfloat16* {
@@ -1350,11 +1388,11 @@ void ensure_workspace_impl(cnrx_plan& p, int B, int T, int F) {
           const int nbuf = p.hb_ns > 3 ? 2 : (p.hb_ns > 2 ? 1 : 0);
           if (ws.fold_bytes < fbytes) {
             for (void*& b : ws.fold_bufs) {
-              if (b) cudaFree(b);
+              ws_free(ws, b);
               b = nullptr;
             }
             ws.fold_bytes = 0;
-            for (int i = 0; i < nbuf; ++i) CNRX_CUDA(cudaMalloc(&ws.fold_bufs[i], fbytes));
+            for (int i = 0; i < nbuf; ++i) ws.fold_bufs[i] = ws_malloc(ws, fbytes);
             ws.fold_bytes = fbytes;
           }
           for (int k = 0; k < p.hb_ns; ++k) {
@@ -1812,12 +1850,12 @@ void check_shape(cnrx_plan& p, int64_t B, int64_t T, int64_t F, int64_t C) {
   require(B < (1ll << 31) && T < 4096 && F < (1 << 20), "tensor dimensions too large");
 }
 
-void* ensure_dev(void*& buf, size_t& cap, size_t bytes) {
+void* ensure_dev(Workspace& ws, void*& buf, size_t& cap, size_t bytes) {
   if (cap < bytes) {
-    if (buf) cudaFree(buf);
+    ws_free(ws, buf);
     buf = nullptr;  // a failed cudaMalloc must not leave a stale pointer / capacity behind
     cap = 0;
-    CNRX_CUDA(cudaMalloc(&buf, bytes));
+    buf = ws_malloc(ws, bytes);
     cap = bytes;
   }
   return buf;
@@ -1851,7 +1889,7 @@ void run_forward(cnrx_plan& p, const float* x_dev, int64_t B, int64_t T, int64_t
   float* feat = nullptr;  // fp32 plans on the receive path: features in the reference layout
   if ((p.precision == CNRX_FP32 || p.split) && input_kind == 1) {  // allocated outside any graph capture
     const size_t bytes = static_cast<size_t>(B * T * F * p.in_ch) * sizeof(float);
-    feat = static_cast<float*>(ensure_dev(p.ws.feat_buf, p.ws.feat_bytes, bytes));
+    feat = static_cast<float*>(ensure_dev(p.ws, p.ws.feat_buf, p.ws.feat_bytes, bytes));
   }
   auto enqueue = [&]() {
     p.launch_names.clear();
@@ -2053,8 +2091,8 @@ void host_pipeline(cnrx_plan& p, const float* in, size_t in_per_slot, float* out
                    Run&& run) {
   const size_t in_bytes = static_cast<size_t>(B) * in_per_slot;
   const size_t out_bytes = static_cast<size_t>(B) * out_per_slot;
-  char* din = static_cast<char*>(ensure_dev(p.ws.in_buf, p.ws.in_bytes, in_bytes));
-  char* dout = static_cast<char*>(ensure_dev(p.ws.out_buf, p.ws.out_bytes, out_bytes));
+  char* din = static_cast<char*>(ensure_dev(p.ws, p.ws.in_buf, p.ws.in_bytes, in_bytes));
+  char* dout = static_cast<char*>(ensure_dev(p.ws, p.ws.out_buf, p.ws.out_bytes, out_bytes));
   const int n = pipeline_chunks(p, B);
   if (n == 1) {
     CNRX_CUDA(cudaMemcpyAsync(din, in, in_bytes, cudaMemcpyHostToDevice, p.stream));
@@ -2277,13 +2315,12 @@ void cnrx_plan_destroy(cnrx_plan* plan) {
   if (plan->gexec) cudaGraphExecDestroy(plan->gexec);
   if (plan->fence_in) cudaEventDestroy(plan->fence_in);
   if (plan->fence_out) cudaEventDestroy(plan->fence_out);
-  for (void* b : plan->ws.buffers) cudaFree(b);
-  if (plan->ws.in_buf) cudaFree(plan->ws.in_buf);
-  if (plan->ws.out_buf) cudaFree(plan->ws.out_buf);
-  if (plan->ws.feat_buf) cudaFree(plan->ws.feat_buf);
-  if (plan->ws.classic_buf) cudaFree(plan->ws.classic_buf);
-  for (void* b : plan->ws.fold_bufs)
-    if (b) cudaFree(b);
+  for (void* b : plan->ws.buffers) ws_free(plan->ws, b);
+  ws_free(plan->ws, plan->ws.in_buf);
+  ws_free(plan->ws, plan->ws.out_buf);
+  ws_free(plan->ws, plan->ws.feat_buf);
+  ws_free(plan->ws, plan->ws.classic_buf);
+  for (void* b : plan->ws.fold_bufs) ws_free(plan->ws, b);
   if (plan->classic_done) cudaEventDestroy(plan->classic_done);
   for (void* d : plan->dev_allocs) cudaFree(d);
   for (auto& evs : plan->prof_events)
@@ -2296,6 +2333,78 @@ void cnrx_plan_destroy(cnrx_plan* plan) {
   if (plan->stream) cudaStreamDestroy(plan->stream);
   if (prev >= 0) cudaSetDevice(prev);
   delete plan;
+}
+
+// Drops every workspace buffer (plane / node buffers, staging, feature and fold buffers) so the next call
+// reallocates them; a captured graph refers to the old addresses and goes with them.
+static void release_workspace(cnrx_plan& p) {
+  Workspace& ws = p.ws;
+  if (p.gexec) {
+    cudaGraphExecDestroy(p.gexec);
+    p.gexec = nullptr;
+    p.gkey.clear();
+  }
+  for (void* b : ws.buffers) ws_free(ws, b);
+  ws.buffers.clear();
+  ws.sizes.clear();
+  ws.launches.clear();
+  ws.cap_B = 0;
+  ws.B = ws.T = ws.F = -1;
+  for (void*& b : ws.fold_bufs) {
+    ws_free(ws, b);
+    b = nullptr;
+  }
+  ws.fold_bytes = 0;
+  void** bufs[] = {&ws.in_buf, &ws.out_buf, &ws.feat_buf, &ws.classic_buf};
+  size_t* caps[] = {&ws.in_bytes, &ws.out_bytes, &ws.feat_bytes, &ws.classic_bytes};
+  for (int i = 0; i < 4; ++i) {
+    ws_free(ws, *bufs[i]);
+    *bufs[i] = nullptr;
+    *caps[i] = 0;
+  }
+}
+
+int cnrx_plan_set_guard_bands(cnrx_plan* plan, int32_t enable) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    DeviceGuard dg(plan->device);
+    CNRX_CUDA(cudaDeviceSynchronize());
+    release_workspace(*plan);
+    plan->ws.guard = enable != 0;
+  });
+}
+
+int cnrx_plan_check_guard_bands(cnrx_plan* plan, int64_t* n_buffers, int64_t* bad_bytes) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    require(n_buffers && bad_bytes, "null result pointer");
+    require(plan->ws.guard, "guard bands are off (cnrx_plan_set_guard_bands)");
+    DeviceGuard dg(plan->device);
+    CNRX_CUDA(cudaDeviceSynchronize());
+    std::vector<unsigned char> h(kGuardBytes);
+    int64_t bad = 0;
+    for (const auto& gb : plan->ws.guarded)
+      for (int side = 0; side < 2; ++side) {
+        CNRX_CUDA(cudaMemcpy(h.data(), gb.base + (side ? kGuardBytes + gb.bytes : 0), kGuardBytes, cudaMemcpyDeviceToHost));
+        for (unsigned char v : h) bad += v != kGuardByte;
+      }
+    *n_buffers = static_cast<int64_t>(plan->ws.guarded.size());
+    *bad_bytes = bad;
+  });
+}
+
+int cnrx_plan_guard_band_ptr(cnrx_plan* plan, int64_t index, int32_t side, void** band_dev) {
+  if (!plan) return fail(CNRX_ERR_INVALID_ARGUMENT, "null plan");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    require(band_dev != nullptr, "null result pointer");
+    require(index >= 0 && index < static_cast<int64_t>(plan->ws.guarded.size()) && (side == 0 || side == 1),
+            "no such guard band");
+    const auto& gb = plan->ws.guarded[static_cast<size_t>(index)];
+    *band_dev = gb.base + (side ? kGuardBytes + gb.bytes : 0);
+  });
 }
 
 int cnrx_forward_device(cnrx_plan* plan, const float* x_dev, int64_t B, int64_t T, int64_t F, int64_t C,
@@ -2528,7 +2637,7 @@ int cnrx_classical_receive(cnrx_plan* plan, const float* y_dev, const float* h_d
       // at), ordered after the previous classical call when that ran on another stream
       const size_t bytes = static_cast<size_t>(B * T * F * 6 * N) * sizeof(float);
       if (plan->ws.classic_bytes < bytes && plan->classic_used) CNRX_CUDA(cudaEventSynchronize(plan->classic_done));
-      float* f = static_cast<float*>(ensure_dev(plan->ws.classic_buf, plan->ws.classic_bytes, bytes));
+      float* f = static_cast<float*>(ensure_dev(plan->ws, plan->ws.classic_buf, plan->ws.classic_bytes, bytes));
       if (plan->classic_used && plan->classic_stream != s) CNRX_CUDA(cudaStreamWaitEvent(s, plan->classic_done, 0));
       PlaneGeom g = make_geom(static_cast<int>(B), static_cast<int>(T), static_cast<int>(F), 1);
       launch_featurize_ref(y_dev, g, static_cast<int>(N), plan->pt, f, s);

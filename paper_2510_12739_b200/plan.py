@@ -100,7 +100,8 @@ EXPORTED = ["cnrx_plan_create", "cnrx_plan_create_ex", "cnrx_plan_options_defaul
             "cnrx_receive_sharded", "cnrx_forward_sharded", "cnrx_get_plan_info", "cnrx_set_graph_capture", "cnrx_launch_name",
             "cnrx_set_profiling", "cnrx_read_profile", "cnrx_launch_flops", "cnrx_generate_slots",
             "cnrx_count_bit_errors", "cnrx_slot_noise_var", "cnrx_classical_receive", "cnrx_ipc_alloc", "cnrx_ipc_open",
-            "cnrx_ipc_close", "cnrx_ipc_free", "cnrx_ipc_read"]
+            "cnrx_ipc_close", "cnrx_ipc_free", "cnrx_ipc_read", "cnrx_plan_set_guard_bands",
+            "cnrx_plan_check_guard_bands", "cnrx_plan_guard_band_ptr"]
 
 
 def lib():
@@ -123,6 +124,9 @@ def lib():
     L.cnrx_get_plan_options.argtypes = [vp, C.POINTER(cnrx_plan_options)]
     L.cnrx_feature_plane_device.argtypes = [vp, vp, i64, i64, i64, i64, vp, C.POINTER(C.c_int32)]
     L.cnrx_plan_destroy.argtypes = [vp]
+    L.cnrx_plan_set_guard_bands.argtypes = [vp, C.c_int32]
+    L.cnrx_plan_check_guard_bands.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.cnrx_plan_guard_band_ptr.argtypes = [vp, i64, C.c_int32, C.POINTER(vp)]
     L.cnrx_plan_destroy.restype = None
     L.cnrx_last_error.restype = C.c_char_p
     L.cnrx_forward.argtypes = [vp, f32p, i64, i64, i64, i64, C.c_int32, f32p]
@@ -309,6 +313,21 @@ class Plan:
         B, T, F, N = y.shape[:4]
         _check(lib().cnrx_featurize_device(self.h, C.c_void_p(y.data_ptr()), B, T, F, N,
                                            C.c_void_p(feat.data_ptr()), _stream(stream)))
+
+    # ---- debug: guard bands around every workspace buffer (include/conetrx_cuda.h) -------------------
+    def set_guard_bands(self, enable: bool = True) -> None:
+        _check(lib().cnrx_plan_set_guard_bands(self.h, 1 if enable else 0))
+
+    def check_guard_bands(self):
+        """(guarded buffers, canary bytes overwritten) -- the second must be 0."""
+        n, bad = C.c_int64(), C.c_int64()
+        _check(lib().cnrx_plan_check_guard_bands(self.h, C.byref(n), C.byref(bad)))
+        return n.value, bad.value
+
+    def guard_band_ptr(self, index: int, side: int) -> int:
+        ptr = C.c_void_p()
+        _check(lib().cnrx_plan_guard_band_ptr(self.h, index, side, C.byref(ptr)))
+        return ptr.value
 
     # ---- introspection ----------------------------------------------------------------------------
     def options(self) -> dict:
