@@ -575,7 +575,10 @@ def main():
         if world > 1 and gather == "peer":
             try:  # collective: every rank agrees on the outcome
                 from paper_2510_12739_b200 import shard as _shp
-                peer = _shp.PeerLLR(world * B, (link.T, link.F, nb), rank, local)
+                # two buffers, alternating by step: rank 0 reads step k's batch while the other ranks' step
+                # k + 1 stores go to the other buffer; the barrier of step k + 1 orders rank 0's read of
+                # buffer k % 2 before anybody's step k + 2 stores into it
+                peers = [_shp.PeerLLR(world * B, (link.T, link.F, nb), rank, local) for _ in range(2)]
             except RuntimeError as e:
                 gather, peer_err = "nccl", repr(e)  # no peer access: the NCCL gather instead
         if world == 1:
@@ -586,20 +589,39 @@ def main():
             # stream sync + host barrier; rank 0 then reads the whole batch (one D2H)
             from paper_2510_12739_b200 import shard
             y_dev = torch.empty((B, link.T, link.F, link.N), dtype=torch.complex64, device="cuda")
-            dst = peer.dst(rank * B)
-            out_host = torch.empty((world * B, link.T, link.F, nb), dtype=torch.float32).pin_memory() if rank == 0 else None
+            out_hosts = ([torch.empty((world * B, link.T, link.F, nb), dtype=torch.float32).pin_memory()
+                          for _ in range(2)] if rank == 0 else None)
+            out_host = out_hosts[0] if rank == 0 else None
+            rd_stream = torch.cuda.Stream() if rank == 0 else None  # rank 0's D2H of step k overlaps step k + 1
+            rd_done = [None, None]
+            peer_step = [0]
 
             def e2e_step():
+                k = peer_step[0] & 1
+                peer = peers[k]
+                peer_step[0] += 1
                 y_dev.copy_(y_host, non_blocking=True)
-                plan.receive_device_ptr(y_dev, dst, torch.cuda.current_stream().cuda_stream)
-                torch.cuda.synchronize()
+                plan.receive_device_ptr(y_dev, peer.dst(rank * B), torch.cuda.current_stream().cuda_stream)
+                torch.cuda.current_stream().synchronize()
+                if rank == 0 and rd_done[k ^ 1] is not None:
+                    # the previous step's read (of the other peer buffer) is complete before this barrier releases
+                    # the ranks into the step that stores into that buffer again
+                    rd_done[k ^ 1].synchronize()
                 barrier()
                 if rank == 0:
-                    peer.to_host(out_host)
+                    peer.to_host_async(out_hosts[k], rd_stream.cuda_stream)
+                    rd_done[k] = torch.cuda.Event()
+                    rd_done[k].record(rd_stream)
+
+            def e2e_finish():  # inside the timed region: the last steps' reads have landed
+                if rank == 0:
+                    rd_stream.synchronize()
             h2d, d2h = batch.y.nbytes * world, world * B * link.T * link.F * nb * 4
             how = ("per rank: H2D + cnrx_receive_device whose LLR head stores its slots into rank 0's buffer over "
                    "NVLink (CUDA IPC peer memory: the gather fused into the last kernel, no collective); stream "
-                   "sync + barrier; rank 0 D2H of the whole batch")
+                   "sync + barrier; rank 0 D2H of the whole batch on a side stream (two peer buffers alternate by "
+                   "step, so rank 0's read of step k overlaps step k + 1 without its stores landing in the buffer "
+                   "being read; the last reads complete inside the timed region)")
         else:
             # every rank: H2D of its slots, receive on its GPU; NCCL gather of the LLRs to rank 0's GPU
             # (shard.gather_llr_tensor, covered by the 2-rank gloo test); rank 0: one D2H of the whole
@@ -621,14 +643,19 @@ def main():
                 torch.cuda.synchronize()
             h2d, d2h = batch.y.nbytes * world, world * B * link.T * link.F * nb * 4
             how = "per rank: H2D + cnrx_receive_device; NCCL gather of the LLRs to rank 0; rank 0 D2H of the whole batch"
+        if not (world > 1 and gather == "peer"):
+            def e2e_finish():
+                pass
         for _ in range(max(2, args.warmup // 2)):
             e2e_step()
+        e2e_finish()
         e2e_steps = max(5, args.steps // 4)
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             e2e_step()
+        e2e_finish()
         e2e_s = max_over_ranks(time.perf_counter() - t0)
         barrier()
         e2e = {"value": global_batch * e2e_steps / e2e_s, "unit": "slots/s", "h2d_bytes_per_step": int(h2d),
@@ -646,9 +673,11 @@ def main():
                 from paper_2510_12739_b200 import shard as _sh
                 ref = _sh.gather_llr_tensor(mine if backend == "nccl" else mine.cpu(), world * B, world, rank)
                 if rank == 0:
-                    e2e["peer_gather_bit_exact"] = bool(torch.equal(ref.cpu(), out_host))
+                    e2e["peer_gather_bit_exact"] = bool(torch.equal(ref.cpu(), out_hosts[0]) and
+                                                        torch.equal(ref.cpu(), out_hosts[1]))
                 barrier()
-                peer.close()
+                for peer in peers:
+                    peer.close()
         plan.close()
 
     lat = None

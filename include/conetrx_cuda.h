@@ -276,6 +276,9 @@ int cnrx_ipc_close(int32_t device, void* opened_ptr);
 int cnrx_ipc_free(int32_t device, void* allocated_ptr);
 /* Synchronous copy of `bytes` from a (local or opened) device buffer to host memory. */
 int cnrx_ipc_read(int32_t device, const void* src, void* host_dst, int64_t bytes);
+/* The same copy enqueued on `stream` (a cudaStream_t of `device`; host_dst pinned), not waited for: rank 0
+ * reads step k's batch on a side stream while step k + 1 computes into the other buffer of a pair. */
+int cnrx_ipc_read_async(int32_t device, const void* src, void* host_dst, int64_t bytes, void* stream);
 
 #ifdef __cplusplus
 }

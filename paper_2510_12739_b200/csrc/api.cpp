@@ -2782,6 +2782,15 @@ int cnrx_ipc_read(int32_t device, const void* src, void* host_dst, int64_t bytes
   });
 }
 
+int cnrx_ipc_read_async(int32_t device, const void* src, void* host_dst, int64_t bytes, void* stream) {
+  if (!src || !host_dst || bytes < 0) return fail(CNRX_ERR_INVALID_ARGUMENT, "bad argument");
+  return guarded([&] {
+    DeviceGuard dg(device);
+    CNRX_CUDA(cudaMemcpyAsync(host_dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost,
+                              static_cast<cudaStream_t>(stream)));
+  });
+}
+
 int cnrx_ipc_free(int32_t device, void* allocated_ptr) {
   return guarded([&] {
     DeviceGuard dg(device);

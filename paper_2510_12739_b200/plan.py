@@ -100,7 +100,7 @@ EXPORTED = ["cnrx_plan_create", "cnrx_plan_create_ex", "cnrx_plan_options_defaul
             "cnrx_receive_sharded", "cnrx_forward_sharded", "cnrx_get_plan_info", "cnrx_set_graph_capture", "cnrx_launch_name",
             "cnrx_set_profiling", "cnrx_read_profile", "cnrx_launch_flops", "cnrx_generate_slots",
             "cnrx_count_bit_errors", "cnrx_slot_noise_var", "cnrx_classical_receive", "cnrx_ipc_alloc", "cnrx_ipc_open",
-            "cnrx_ipc_close", "cnrx_ipc_free", "cnrx_ipc_read", "cnrx_plan_set_guard_bands",
+            "cnrx_ipc_close", "cnrx_ipc_free", "cnrx_ipc_read", "cnrx_ipc_read_async", "cnrx_plan_set_guard_bands",
             "cnrx_plan_check_guard_bands", "cnrx_plan_guard_band_ptr"]
 
 
@@ -139,6 +139,7 @@ def lib():
     L.cnrx_ipc_close.argtypes = [C.c_int32, vp]
     L.cnrx_ipc_free.argtypes = [C.c_int32, vp]
     L.cnrx_ipc_read.argtypes = [C.c_int32, vp, vp, i64]
+    L.cnrx_ipc_read_async.argtypes = [C.c_int32, vp, vp, i64, vp]
     L.cnrx_featurize_device.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp]
     L.cnrx_receive_sharded.argtypes = [C.POINTER(vp), C.c_int32, f32p, i64, i64, i64, i64, f32p]
     L.cnrx_forward_sharded.argtypes = [C.POINTER(vp), C.c_int32, f32p, i64, i64, i64, i64, C.c_int32, f32p]
@@ -491,6 +492,10 @@ def ipc_close(device: int, ptr: int) -> None:
 
 def ipc_read(device: int, ptr: int, host_ptr: int, nbytes: int) -> None:
     _check(lib().cnrx_ipc_read(device, C.c_void_p(ptr), C.c_void_p(host_ptr), nbytes))
+
+
+def ipc_read_async(device: int, ptr: int, host_ptr: int, nbytes: int, stream: int) -> None:
+    _check(lib().cnrx_ipc_read_async(device, C.c_void_p(ptr), C.c_void_p(host_ptr), nbytes, C.c_void_p(stream)))
 
 
 def ipc_free(device: int, ptr: int) -> None:

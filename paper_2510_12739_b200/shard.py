@@ -108,6 +108,11 @@ class PeerLLR:
         from paper_2510_12739_b200 import plan as P
         P.ipc_read(self.device, self.ptr, out.data_ptr(), self.B * self.slot_bytes)
 
+    def to_host_async(self, out, stream: int) -> None:
+        """rank 0: the same copy enqueued on `stream` (a cudaStream_t handle), not waited for."""
+        from paper_2510_12739_b200 import plan as P
+        P.ipc_read_async(self.device, self.ptr, out.data_ptr(), self.B * self.slot_bytes, stream)
+
     def close(self) -> None:
         from paper_2510_12739_b200 import plan as P
         if self.rank == 0:

@@ -58,4 +58,10 @@ def test_peer_llr_stores_land_in_the_owner_buffer():
     P.ipc_read(0, ptr, out.data_ptr(), B * slot_bytes)
     assert np.array_equal(out.numpy()[b0:], res)            # the writer's head stores, bit for bit
     assert np.array_equal(out.numpy()[:b0], p.receive(own.y))  # the owner's slots untouched
+    # the stream-ordered read (bench.py's rank 0 reads step k on a side stream while step k + 1 computes)
+    out2 = torch.zeros((B, link.T, link.F, 4), dtype=torch.float32).pin_memory()
+    side = torch.cuda.Stream()
+    P.ipc_read_async(0, ptr, out2.data_ptr(), B * slot_bytes, side.cuda_stream)
+    side.synchronize()
+    assert torch.equal(out2, out)
     P.ipc_free(0, ptr)
