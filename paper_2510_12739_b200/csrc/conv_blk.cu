@@ -89,7 +89,10 @@ constexpr int kThreads = (19 + kReluWarps) * 32;
 constexpr int kFoldWarps = CNRX_BLK_FOLD_WARPS, kWarpFold0 = 19 + kReluWarps;
 constexpr int kThreadsFold = kThreads + kFoldWarps * 32;
 __device__ __forceinline__ int relu_index(int warp) { return warp == kWarpRelu0 ? 0 : warp - 19; }
-constexpr int kMaxXStages = 6;
+#ifndef CNRX_BLK_MAXX
+#define CNRX_BLK_MAXX 10  // x ring cap; the chooser takes what fits 227 KB (cfg2: 10 stages). 6 -> 10: -1.5 % per launch (profiles/r02m_ab_xring.log)
+#endif
+constexpr int kMaxXStages = CNRX_BLK_MAXX;
 
 struct BlkLayout {
   uint32_t x_off, stage, xr_off, w_off, stg_off, trash_off, f_off, stg2_off, par_off, bar_off, total;
@@ -124,7 +127,7 @@ __host__ __device__ inline BlkLayout blk_layout(int xstages, int win_alloc, int 
   s.par_off = off;                 // bias1, bias2; fold: s_prev, t_prev, s, t [64] + head w [64][8], b [8]
   off += 2u * kC * 4u;
   if (epi) off += (4u * kC + kC * 8u + 8u) * 4u;
-  s.bar_off = off;                 // 34 mbarriers + the TMEM address slot
+  s.bar_off = off;                 // 2 * kMaxXStages + 26 mbarriers (46 at 10 stages) + the TMEM address slot: < 512 B
   s.total = off + 512 + 1024;
   return s;
 }
