@@ -393,13 +393,17 @@ def latency_b1(torch, P, g, prec, batch, link, local):
             p1.receive_device(y1, o1, st)
     torch.cuda.synchronize()
     dev_lat = []
-    for _ in range(200):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        p1.receive_device(y1, o1, st)
-        b.record(stream)
-        b.synchronize()
-        dev_lat.append(a.elapsed_time(b))
+    # one synchronous replay at a time leaves the GPU mostly idle: the SM clock during these runs is what the
+    # driver's idle governor gives (it scales the latency ~1/clock), so it is sampled and reported with them
+    with ClockSampler(local) as cs:
+        for _ in range(200):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            p1.receive_device(y1, o1, st)
+            b.record(stream)
+            b.synchronize()
+            dev_lat.append(a.elapsed_time(b))
+    lat_clocks = cs.summary()
     p1.set_graph_capture(False)
     yh1 = torch.from_numpy(batch.y[:1].copy()).pin_memory()
     oh1 = torch.empty((1, link.T, link.F, nb), dtype=torch.float32).pin_memory()
@@ -413,6 +417,7 @@ def latency_b1(torch, P, g, prec, batch, link, local):
     p1.close()
     return {"device_ms": {"p50": float(np.percentile(dev_lat, 50)), "p99": float(np.percentile(dev_lat, 99))},
             "e2e_ms": {"p50": float(np.percentile(e2e_lat, 50)), "p99": float(np.percentile(e2e_lat, 99))},
+            "device_clocks": {k: lat_clocks.get(k) for k in ("sm_mhz", "sm_min_mhz", "sm_max_mhz", "samples")},
             "how": "B=1, 200 runs; device: CUDA-graph replay between CUDA events; e2e: cnrx_receive from pinned host"}
 
 
